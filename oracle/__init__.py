@@ -1,0 +1,203 @@
+"""ctypes wrapper over oracle/evospec_oracle.c.
+
+TEST INFRASTRUCTURE ONLY: imported by tests/, __graft_entry__.smoke() and
+bench.py's cpu_baseline / --impl reference legs, never by the product package
+(paper_2605_27390_b200/). The C source shares no code with the CUDA path.
+
+Every function here is argument marshalling; the arithmetic is in the C file,
+each function there citing the PAPER.md / SPEC.md passage it follows.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "evospec_oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+_lib = None
+
+BF16, FP32 = 0, 1
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle with g++/gcc -O2 (no -ffast-math)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", "-O2", "-std=c11", "-fPIC", "-shared",
+                               "-fno-fast-math", "-ffp-contract=off",
+                               "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+def _L():
+    global _lib
+    if _lib is None:
+        build()
+        _lib = C.CDLL(_LIB)
+    return _lib
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+def _dt(a: np.ndarray) -> int:
+    if a.dtype == np.uint16:
+        return BF16
+    if a.dtype == np.float32:
+        return FP32
+    raise TypeError(f"oracle inputs are bf16 bits (uint16) or float32, got {a.dtype}")
+
+
+def _check(rc: int, what: str):
+    if rc != 0:
+        raise ValueError(f"oracle {what}: input error (rc={rc})")
+
+
+def _i32(a):
+    return None if a is None else np.ascontiguousarray(a, dtype=np.int32)
+
+
+def sem_scores(E: np.ndarray, q: np.ndarray) -> np.ndarray:
+    E = np.ascontiguousarray(E)
+    q = np.ascontiguousarray(q).reshape(-1)
+    n, d = E.shape
+    out = np.empty(n, dtype=np.float64)
+    f = _L().eo_sem_scores
+    f.argtypes = [C.c_void_p, C.c_int, C.c_int64, C.c_int, C.c_void_p, C.c_int, C.c_void_p]
+    _check(f(_p(E), _dt(E), n, d, _p(q), _dt(q), _p(out)), "sem_scores")
+    return out
+
+
+def topn(s: np.ndarray, N: int) -> np.ndarray:
+    s = np.ascontiguousarray(s, dtype=np.float64)
+    out = np.empty(N, dtype=np.int32)
+    f = _L().eo_topn
+    f.argtypes = [C.c_void_p, C.c_int64, C.c_int, C.c_void_p]
+    _check(f(_p(s), s.size, N, _p(out)), "topn")
+    return out
+
+
+def graph_expand(G, row_ptr, col, per_seed: int) -> np.ndarray:
+    G = _i32(G)
+    row_ptr = _i32(row_ptr)
+    col = _i32(col)
+    out = np.empty(max(1, G.size * per_seed), dtype=np.int32)
+    n = C.c_int(0)
+    f = _L().eo_graph_expand
+    f.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]
+    _check(f(_p(G), G.size, _p(row_ptr), _p(col), per_seed, _p(out), C.byref(n)), "graph_expand")
+    return out[:n.value].copy()
+
+
+def ctx_tokens(ctx, V: int, min_count: int, n_max: int) -> np.ndarray:
+    ctx = _i32(ctx) if ctx is not None else np.zeros(0, np.int32)
+    out = np.empty(max(1, n_max), dtype=np.int32)
+    n = C.c_int(0)
+    f = _L().eo_ctx_tokens
+    f.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p]
+    _check(f(_p(ctx), ctx.size, V, min_count, n_max, _p(out), C.byref(n)), "ctx_tokens")
+    return out[:n.value].copy()
+
+
+def build_subset(E, q, static_ids, seed_ids, row_ptr, col, *, n_sem: int,
+                 n_graph_sem_seeds: int = 10, per_seed: int = 8, n_dyn: int,
+                 ctx_ids=None, ctx_min_count: int = 0, n_ctx_max: int = 0):
+    """Returns dict(S, sem, dyn) per SURVEY §8(c) steps 2-8."""
+    E = np.ascontiguousarray(E)
+    q = np.ascontiguousarray(q).reshape(-1)
+    V, d = E.shape
+    static_ids = _i32(static_ids)
+    seed_ids = _i32(seed_ids) if seed_ids is not None else np.zeros(0, np.int32)
+    ctx = _i32(ctx_ids) if ctx_ids is not None else np.zeros(0, np.int32)
+    row_ptr = _i32(row_ptr)
+    col = _i32(col)
+    S = np.empty(static_ids.size + n_dyn + 1, dtype=np.int32)
+    nS = C.c_int32(0)
+    sem = np.empty(max(1, n_sem), dtype=np.int32)
+    dyn = np.empty(max(1, n_dyn), dtype=np.int32)
+    nd = C.c_int32(0)
+    f = _L().eo_build_subset
+    f.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_int,
+                  C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p,
+                  C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                  C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+    rc = f(_p(E), _dt(E), V, d, _p(q), _dt(q), _p(static_ids), static_ids.size,
+           _p(seed_ids), seed_ids.size, _p(row_ptr), _p(col), _p(ctx), ctx.size,
+           n_sem, n_graph_sem_seeds, per_seed, ctx_min_count, n_ctx_max, n_dyn,
+           _p(S), C.byref(nS), _p(sem), _p(dyn), C.byref(nd))
+    _check(rc, "build_subset")
+    return dict(S=S[:nS.value].copy(), sem=sem[:n_sem].copy(), dyn=dyn[:nd.value].copy())
+
+
+def subset_logits(W, H, S, *, R: int = 1, inv_temp: float = 1.0) -> np.ndarray:
+    """z [n_h, n_S] (float64) for a shard's W_local (rows v // R)."""
+    W = np.ascontiguousarray(W)
+    H = np.ascontiguousarray(H)
+    S = _i32(S)
+    n_rows, d = W.shape
+    n_h = H.shape[0]
+    out = np.empty((n_h, S.size), dtype=np.float64)
+    f = _L().eo_subset_logits
+    f.argtypes = [C.c_void_p, C.c_int, C.c_int64, C.c_int, C.c_void_p, C.c_int, C.c_int,
+                  C.c_void_p, C.c_int, C.c_int, C.c_double, C.c_void_p]
+    _check(f(_p(W), _dt(W), n_rows, d, _p(H), _dt(H), n_h, _p(S), S.size, R,
+             float(inv_temp), _p(out)), "subset_logits")
+    return out
+
+
+def softmax_topk(z: np.ndarray, S, k: int):
+    """Returns dict(ids, vals, m, s, lse, probs) per §8(c) steps 10-11."""
+    z = np.ascontiguousarray(z, dtype=np.float64)
+    S = _i32(S)
+    n_h = z.shape[0]
+    ids = np.empty((n_h, k), np.int32)
+    vals = np.empty((n_h, k), np.float64)
+    probs = np.empty((n_h, k), np.float64)
+    m = np.empty(n_h, np.float64)
+    s = np.empty(n_h, np.float64)
+    lse = np.empty(n_h, np.float64)
+    f = _L().eo_softmax_topk
+    f.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int] + [C.c_void_p] * 6
+    _check(f(_p(z), n_h, S.size, _p(S), k, _p(ids), _p(vals), _p(m), _p(s), _p(lse),
+             _p(probs)), "softmax_topk")
+    return dict(ids=ids, vals=vals, m=m, s=s, lse=lse, probs=probs)
+
+
+def subset_logits_topk(W, H, S, k: int, *, R: int = 1, inv_temp: float = 1.0):
+    """The shard triple (ids, vals, m, s) plus lse/probs of the shard alone."""
+    z = subset_logits(W, H, S, R=R, inv_temp=inv_temp)
+    return softmax_topk(z, S, k)
+
+
+def merge(ids, vals, m, s, k: int):
+    """Stacked [R, n_h, k] / [R, n_h] shard triples -> dict(ids, vals, lse, probs)."""
+    ids = np.ascontiguousarray(ids, dtype=np.int32)
+    vals = np.ascontiguousarray(vals, dtype=np.float64)
+    m = np.ascontiguousarray(m, dtype=np.float64)
+    s = np.ascontiguousarray(s, dtype=np.float64)
+    R, n_h = m.shape
+    oi = np.empty((n_h, k), np.int32)
+    ov = np.empty((n_h, k), np.float64)
+    ol = np.empty(n_h, np.float64)
+    op = np.empty((n_h, k), np.float64)
+    f = _L().eo_merge
+    f.argtypes = [C.c_int, C.c_int, C.c_int] + [C.c_void_p] * 8
+    _check(f(R, n_h, k, _p(ids), _p(vals), _p(m), _p(s), _p(oi), _p(ov), _p(ol), _p(op)), "merge")
+    return dict(ids=oi, vals=ov, lse=ol, probs=op)
+
+
+def shard_subset(S, R: int, r: int) -> np.ndarray:
+    """S_r = [v in S : v mod R = r] (§8(c) step 12, interleaved ownership)."""
+    S = np.asarray(S)
+    return S[S % R == r].astype(np.int32)
+
+
+def shard_rows(W, R: int, r: int):
+    """W_local for shard r: global rows v = r (mod R), local row v // R."""
+    return np.ascontiguousarray(W[r::R])

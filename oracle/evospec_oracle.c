@@ -1,0 +1,351 @@
+/*
+ * evospec_oracle.c -- plain, slow, obviously-correct CPU oracle for the
+ * EvoSpec dynamic-vocabulary draft LM-head path.
+ *
+ * TEST INFRASTRUCTURE ONLY. Nothing in the product path links, loads or
+ * calls this file: only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs may use it. It shares no code, header,
+ * table or constant with paper_2605_27390_b200/ (the CUDA path).
+ *
+ * All arithmetic is IEEE double, sequential in the hidden index c, on bf16 /
+ * fp32 inputs decoded exactly (bf16 bits << 16 is an fp32 with the same
+ * value; fp32 -> double is exact). No -ffast-math. Single-threaded.
+ *
+ * Citations: P:n = /root/reference/PAPER.md line n, S:n = SPEC.md line n,
+ * "§8(c) step i" = SURVEY.md §8(c) oracle step i (the reading of the paper
+ * adopted in DESIGN.md "Readings").
+ *
+ * Return codes: 0 ok, 2 input error (mirrors SPEC exit code 2).
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define EO_OK 0
+#define EO_EINPUT 2
+
+enum { EO_BF16 = 0, EO_FP32 = 1 };
+
+/* §8(c) step 1: exact decode of one element. */
+static double eo_decode(const void *base, int dtype, int64_t idx) {
+    if (dtype == EO_BF16) {
+        uint32_t bits = ((uint32_t)((const uint16_t *)base)[idx]) << 16;
+        float f;
+        memcpy(&f, &bits, sizeof f);
+        return (double)f;
+    }
+    return (double)((const float *)base)[idx];
+}
+
+/* Ordering key "(-value, id)": larger value first, lower id on ties
+ * ("ties broken by smallest token id"). */
+typedef struct {
+    double v;
+    int32_t id;
+} eo_key;
+
+static int eo_cmp_desc(const void *a, const void *b) {
+    const eo_key *x = (const eo_key *)a, *y = (const eo_key *)b;
+    if (x->v > y->v) return -1;
+    if (x->v < y->v) return 1;
+    return (x->id < y->id) ? -1 : (x->id > y->id);
+}
+
+static int eo_cmp_i32(const void *a, const void *b) {
+    int32_t x = *(const int32_t *)a, y = *(const int32_t *)b;
+    return (x > y) - (x < y);
+}
+
+/* ------------------------------------------------------------------ */
+/* a2: semantic scores, MIPS over the index rows.     */
+/* s_v = sum_{c=0}^{d-1} q[c] * E[v][c]        (§8(c) step 2)           */
+/* ------------------------------------------------------------------ */
+int eo_sem_scores(const void *E, int e_dtype, int64_t n_rows, int d,
+                  const void *q, int q_dtype, double *out) {
+    if (!E || !q || !out || n_rows < 0 || d < 1) return EO_EINPUT;
+    for (int64_t v = 0; v < n_rows; ++v) {
+        double acc = 0.0;
+        for (int c = 0; c < d; ++c)
+            acc += eo_decode(q, q_dtype, c) * eo_decode(E, e_dtype, v * (int64_t)d + c);
+        out[v] = acc;
+    }
+    return EO_OK;
+}
+
+/* §8(c) step 3: the first N of [0,n) ordered by (-s_v, v). */
+int eo_topn(const double *s, int64_t n, int N, int32_t *out_ids) {
+    if (!s || !out_ids || N < 0 || N > n) return EO_EINPUT;
+    eo_key *keys = (eo_key *)malloc(sizeof(eo_key) * (size_t)(n > 0 ? n : 1));
+    if (!keys) return EO_EINPUT;
+    for (int64_t v = 0; v < n; ++v) { keys[v].v = s[v]; keys[v].id = (int32_t)v; }
+    qsort(keys, (size_t)n, sizeof(eo_key), eo_cmp_desc);
+    for (int i = 0; i < N; ++i) out_ids[i] = keys[i].id;
+    free(keys);
+    return EO_OK;
+}
+
+/* ------------------------------------------------------------------ */
+/* a3: statistical expansion over the co-occurrence CSR (P:98,  */
+/* P:458; per_seed = 8 "top-8 outgoing neighbors").             */
+/* S_graph = concat_{g in G} col[row_ptr[g] : row_ptr[g]+min(per_seed, */
+/* deg g)]  (§8(c) step 5; rows are pre-sorted by (p desc, id asc)).   */
+/* ------------------------------------------------------------------ */
+int eo_graph_expand(const int32_t *G, int nG, const int32_t *row_ptr,
+                    const int32_t *col, int per_seed, int32_t *out, int *out_n) {
+    if ((nG > 0 && !G) || !out_n || per_seed < 0) return EO_EINPUT;
+    int n = 0;
+    for (int i = 0; i < nG; ++i) {
+        int32_t g = G[i];
+        if (!row_ptr) continue;              /* no graph: contributes nothing */
+        int32_t deg = row_ptr[g + 1] - row_ptr[g];
+        int32_t take = deg < per_seed ? deg : per_seed;
+        for (int32_t j = 0; j < take; ++j) out[n++] = col[row_ptr[g] + j];
+    }
+    *out_n = n;
+    return EO_OK;
+}
+
+/* §8(c) step 6 (reading C5): tokens of ctx with count >= min_count,
+ * ordered by (-count, id), the first n_max. Off when min_count == 0. */
+int eo_ctx_tokens(const int32_t *ctx, int n_ctx, int V, int min_count, int n_max,
+                  int32_t *out, int *out_n) {
+    if (!out_n || (n_ctx > 0 && !ctx)) return EO_EINPUT;
+    *out_n = 0;
+    if (min_count <= 0 || n_max <= 0 || n_ctx <= 0) return EO_OK;
+    int32_t *count = (int32_t *)calloc((size_t)V, sizeof(int32_t));
+    if (!count) return EO_EINPUT;
+    for (int i = 0; i < n_ctx; ++i) {
+        if (ctx[i] < 0 || ctx[i] >= V) { free(count); return EO_EINPUT; }
+        count[ctx[i]]++;
+    }
+    eo_key *keys = (eo_key *)malloc(sizeof(eo_key) * (size_t)V);
+    int nk = 0;
+    for (int v = 0; v < V; ++v)
+        if (count[v] >= min_count) { keys[nk].v = (double)count[v]; keys[nk].id = v; nk++; }
+    qsort(keys, (size_t)nk, sizeof(eo_key), eo_cmp_desc);
+    int take = nk < n_max ? nk : n_max;
+    for (int i = 0; i < take; ++i) out[i] = keys[i].id;
+    *out_n = take;
+    free(keys);
+    free(count);
+    return EO_OK;
+}
+
+/* ------------------------------------------------------------------ */
+/* a1-a4: V_t = V_static u S_sem(h) u S_graph(.) (Eq. vocab_union,     */
+/* P:88-93), runtime formation, budget |V_t \ V_static| <=     */
+/* N_dyn (Eq. optimization), cap order.           */
+/* ------------------------------------------------------------------ */
+int eo_build_subset(const void *E, int e_dtype, int V, int d,
+                    const void *q, int q_dtype,
+                    const int32_t *static_ids, int n_static,
+                    const int32_t *seed_ids, int n_seed,
+                    const int32_t *row_ptr, const int32_t *col,
+                    const int32_t *ctx_ids, int n_ctx,
+                    int n_sem, int n_graph_sem_seeds, int per_seed,
+                    int ctx_min_count, int n_ctx_max, int n_dyn,
+                    int32_t *out_S, int32_t *out_nS,
+                    int32_t *out_sem, int32_t *out_dyn, int32_t *out_ndyn) {
+    if (!E || !q || !out_S || !out_nS || V < 1 || d < 1 || n_sem < 0 || n_sem > V ||
+        n_dyn < 0 || n_static < 0 || n_static > V || n_seed < 0 ||
+        n_graph_sem_seeds < 0 || per_seed < 0)
+        return EO_EINPUT;
+    /* inputs: static sorted strictly ascending, all ids in range */
+    for (int i = 0; i < n_static; ++i) {
+        if (static_ids[i] < 0 || static_ids[i] >= V) return EO_EINPUT;
+        if (i > 0 && static_ids[i] <= static_ids[i - 1]) return EO_EINPUT;
+    }
+    for (int i = 0; i < n_seed; ++i)
+        if (seed_ids[i] < 0 || seed_ids[i] >= V) return EO_EINPUT;
+
+    int rc = EO_OK;
+    double *s = (double *)malloc(sizeof(double) * (size_t)V);
+    int32_t *sem = (int32_t *)malloc(sizeof(int32_t) * (size_t)(n_sem > 0 ? n_sem : 1));
+    int nG_max = n_seed + n_graph_sem_seeds;
+    int32_t *G = (int32_t *)malloc(sizeof(int32_t) * (size_t)(nG_max > 0 ? nG_max : 1));
+    int32_t *graph = (int32_t *)malloc(sizeof(int32_t) * (size_t)(nG_max * per_seed + 1));
+    int32_t *ctxs = (int32_t *)malloc(sizeof(int32_t) * (size_t)(n_ctx_max > 0 ? n_ctx_max : 1));
+    uint8_t *in_static = (uint8_t *)calloc((size_t)V, 1);
+    uint8_t *in_dyn = (uint8_t *)calloc((size_t)V, 1);
+    uint8_t *in_G = (uint8_t *)calloc((size_t)V, 1);
+    int32_t *dyn = (int32_t *)malloc(sizeof(int32_t) * (size_t)(n_dyn > 0 ? n_dyn : 1));
+    if (!s || !sem || !G || !graph || !ctxs || !in_static || !in_dyn || !in_G || !dyn) {
+        rc = EO_EINPUT;
+        goto done;
+    }
+
+    /* step 2-3: S_sem */
+    eo_sem_scores(E, e_dtype, V, d, q, q_dtype, s);
+    eo_topn(s, V, n_sem, sem);
+
+    /* step 4: G = dedupe_first(seed_ids ++ S_sem[0:n_graph_sem_seeds]) (C4) */
+    int nG = 0;
+    for (int i = 0; i < n_seed; ++i)
+        if (!in_G[seed_ids[i]]) { in_G[seed_ids[i]] = 1; G[nG++] = seed_ids[i]; }
+    for (int i = 0; i < n_graph_sem_seeds && i < n_sem; ++i)
+        if (!in_G[sem[i]]) { in_G[sem[i]] = 1; G[nG++] = sem[i]; }
+
+    /* step 5: S_graph */
+    int n_graph = 0;
+    eo_graph_expand(G, nG, row_ptr, col, per_seed, graph, &n_graph);
+    for (int i = 0; i < n_graph; ++i)
+        if (graph[i] < 0 || graph[i] >= V) { rc = EO_EINPUT; goto done; }
+
+    /* step 6: S_ctx */
+    int n_ctxs = 0;
+    rc = eo_ctx_tokens(ctx_ids, n_ctx, V, ctx_min_count, n_ctx_max, ctxs, &n_ctxs);
+    if (rc) goto done;
+
+    /* step 7: C = seeds ++ S_sem ++ S_graph ++ S_ctx; first-occurrence,
+     * skip static members, stop at N_dyn (C6, C7). */
+    for (int i = 0; i < n_static; ++i) in_static[static_ids[i]] = 1;
+    int nd = 0;
+    const int32_t *parts[4] = {seed_ids, sem, graph, ctxs};
+    int lens[4] = {n_seed, n_sem, n_graph, n_ctxs};
+    for (int p = 0; p < 4 && nd < n_dyn; ++p)
+        for (int i = 0; i < lens[p] && nd < n_dyn; ++i) {
+            int32_t c = parts[p][i];
+            if (in_static[c] || in_dyn[c]) continue;
+            in_dyn[c] = 1;
+            dyn[nd++] = c;
+        }
+
+    /* step 8: S = sort_ascending(static u dyn) */
+    int nS = 0;
+    for (int i = 0; i < n_static; ++i) out_S[nS++] = static_ids[i];
+    for (int i = 0; i < nd; ++i) out_S[nS++] = dyn[i];
+    qsort(out_S, (size_t)nS, sizeof(int32_t), eo_cmp_i32);
+    *out_nS = nS;
+    if (out_sem) memcpy(out_sem, sem, sizeof(int32_t) * (size_t)n_sem);
+    if (out_dyn) memcpy(out_dyn, dyn, sizeof(int32_t) * (size_t)nd);
+    if (out_ndyn) *out_ndyn = nd;
+
+done:
+    free(s); free(sem); free(G); free(graph); free(ctxs);
+    free(in_static); free(in_dyn); free(in_G); free(dyn);
+    return rc;
+}
+
+/* ------------------------------------------------------------------ */
+/* a5: gathered LM-head contraction, Eq. projection over     */
+/* V_t (alg:evospec P:364): l[r][j] = sum_c H[r][c] * W[S_j][c];       */
+/* z = l * inv_temp (reading C11).  A shard r of R owns the ids        */
+/* v = r (mod R) and stores id v at local row v / R (§8(e)).            */
+/* ------------------------------------------------------------------ */
+int eo_subset_logits(const void *W, int w_dtype, int64_t n_rows_local, int d,
+                     const void *H, int h_dtype, int n_h,
+                     const int32_t *S, int n_S, int R, double inv_temp,
+                     double *out_z) {
+    if (!W || !H || (n_S > 0 && (!S || !out_z)) || d < 1 || n_h < 0 || R < 1 ||
+        !(inv_temp > 0.0) || !isfinite(inv_temp))
+        return EO_EINPUT;
+    for (int j = 0; j < n_S; ++j) {
+        int64_t row = S[j] / R;
+        if (S[j] < 0 || row >= n_rows_local) return EO_EINPUT;
+    }
+    for (int r = 0; r < n_h; ++r)
+        for (int j = 0; j < n_S; ++j) {
+            int64_t row = S[j] / R;
+            double acc = 0.0;
+            for (int c = 0; c < d; ++c)
+                acc += eo_decode(H, h_dtype, (int64_t)r * d + c) *
+                       eo_decode(W, w_dtype, row * (int64_t)d + c);
+            out_z[(int64_t)r * n_S + j] = acc * inv_temp;
+        }
+    return EO_OK;
+}
+
+/* ------------------------------------------------------------------ */
+/* a6-a7: softmax restricted to S (Eq. 1; zero mass off S)  */
+/* m = max z, s = sum e^{z-m}, LSE = m + ln s, p = e^{z-LSE};           */
+/* top-k = first k under (-z, S_j).                           */
+/* Empty support: m = -inf, s = 0 (reading C16); k > n_S pads id -1,   */
+/* value -inf, prob 0.                                                 */
+/* ------------------------------------------------------------------ */
+int eo_softmax_topk(const double *z, int n_h, int n_S, const int32_t *S, int k,
+                    int32_t *ids, double *vals, double *m, double *s,
+                    double *lse, double *probs) {
+    if (k < 1 || n_h < 0 || n_S < 0 || !ids || !vals || !m || !s) return EO_EINPUT;
+    eo_key *keys = (eo_key *)malloc(sizeof(eo_key) * (size_t)(n_S > 0 ? n_S : 1));
+    if (!keys) return EO_EINPUT;
+    for (int r = 0; r < n_h; ++r) {
+        const double *zr = z + (int64_t)r * n_S;
+        double mr = -INFINITY, sr = 0.0;
+        for (int j = 0; j < n_S; ++j) if (zr[j] > mr) mr = zr[j];
+        for (int j = 0; j < n_S; ++j) sr += exp(zr[j] - mr);
+        double lr = n_S > 0 ? mr + log(sr) : -INFINITY;
+        m[r] = mr;
+        s[r] = sr;
+        if (lse) lse[r] = lr;
+        for (int j = 0; j < n_S; ++j) { keys[j].v = zr[j]; keys[j].id = S[j]; }
+        qsort(keys, (size_t)n_S, sizeof(eo_key), eo_cmp_desc);
+        for (int i = 0; i < k; ++i) {
+            int64_t o = (int64_t)r * k + i;
+            if (i < n_S) {
+                ids[o] = keys[i].id;
+                vals[o] = keys[i].v;
+                if (probs) probs[o] = exp(keys[i].v - lr);
+            } else {
+                ids[o] = -1;
+                vals[o] = -INFINITY;
+                if (probs) probs[o] = 0.0;
+            }
+        }
+    }
+    free(keys);
+    return EO_OK;
+}
+
+/* ------------------------------------------------------------------ */
+/* a8: vocab-shard merge (north star; §8(c) step 12).                   */
+/* M = max_r m_r, Sigma = sum_r s_r e^{m_r - M}, LSE = M + ln Sigma,    */
+/* over shards with s_r > 0; top-k of concat(topk_r) by (-val, id);     */
+/* p = e^{val - LSE}.  Inputs are stacked [R][n_h][k] and [R][n_h].     */
+/* ------------------------------------------------------------------ */
+int eo_merge(int R, int n_h, int k, const int32_t *ids, const double *vals,
+             const double *m, const double *s, int32_t *out_ids, double *out_vals,
+             double *out_lse, double *out_probs) {
+    if (R < 1 || n_h < 0 || k < 1 || !ids || !vals || !m || !s || !out_ids || !out_vals)
+        return EO_EINPUT;
+    eo_key *keys = (eo_key *)malloc(sizeof(eo_key) * (size_t)R * (size_t)k);
+    if (!keys) return EO_EINPUT;
+    for (int r = 0; r < n_h; ++r) {
+        double M = -INFINITY;
+        for (int t = 0; t < R; ++t) {
+            int64_t o = (int64_t)t * n_h + r;
+            if (s[o] > 0.0 && m[o] > M) M = m[o];
+        }
+        double sig = 0.0;
+        for (int t = 0; t < R; ++t) {
+            int64_t o = (int64_t)t * n_h + r;
+            if (s[o] > 0.0) sig += s[o] * exp(m[o] - M);
+        }
+        double L = sig > 0.0 ? M + log(sig) : -INFINITY;
+        if (out_lse) out_lse[r] = L;
+        int nk = 0;
+        for (int t = 0; t < R; ++t)
+            for (int i = 0; i < k; ++i) {
+                int64_t o = ((int64_t)t * n_h + r) * k + i;
+                if (ids[o] < 0) continue;     /* padding */
+                keys[nk].v = vals[o];
+                keys[nk].id = ids[o];
+                nk++;
+            }
+        qsort(keys, (size_t)nk, sizeof(eo_key), eo_cmp_desc);
+        for (int i = 0; i < k; ++i) {
+            int64_t o = (int64_t)r * k + i;
+            if (i < nk) {
+                out_ids[o] = keys[i].id;
+                out_vals[o] = keys[i].v;
+                if (out_probs) out_probs[o] = exp(keys[i].v - L);
+            } else {
+                out_ids[o] = -1;
+                out_vals[o] = -INFINITY;
+                if (out_probs) out_probs[o] = 0.0;
+            }
+        }
+    }
+    free(keys);
+    return EO_OK;
+}

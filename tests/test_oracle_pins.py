@@ -1,0 +1,365 @@
+"""Pins the C oracle (oracle/) to things other than itself (CPU only).
+
+Each test names the passage or property it checks. Chosen so that a plausible
+mistake anywhere in the oracle (a dropped term, a wrong sign or index, a
+transposed operand, a wrong bf16 decode, a wrong tie rule, a wrong cap or
+formation order, a wrong LSE combine) fails at least one of them:
+  * worked examples copied into tests/golden/spec_examples.json (cited);
+  * an independent implementation of a definition (numpy/ml_dtypes matmul,
+    scipy logsumexp, np.lexsort, the pure-Python brute force in brute.py);
+  * closed forms and invariants (sum p = 1, equal logits, shift, linearity,
+    merge(split) = unsplit, shard-order invariance).
+"""
+import json
+import math
+import os
+
+import ml_dtypes
+import numpy as np
+import pytest
+from scipy.special import logsumexp
+
+import synth
+from tests import brute
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "spec_examples.json")))
+
+
+def f32(a):
+    return np.asarray(a, dtype=np.float32)
+
+
+def csr_from_rows(V, rows):
+    row_ptr = [0]
+    col = []
+    for u in range(V):
+        col.extend(rows.get(str(u), rows.get(u, [])))
+        row_ptr.append(len(col))
+    return np.array(row_ptr, np.int32), np.array(col if col else [0], np.int32)
+
+
+def bf16_decode_independent(bits):
+    # ml_dtypes' bfloat16 is an independent implementation of the format
+    return np.asarray(bits, np.uint16).view(ml_dtypes.bfloat16).astype(np.float64)
+
+
+# ---------------------------------------------------------------- a5 logits
+def test_projection_example(oracle_mod):
+    g = GOLD["projection"]
+    z = oracle_mod.subset_logits(f32(g["W"]), f32([g["h"]]), [0, 1, 2])
+    assert z.tolist() == [g["logits"]]
+
+
+def test_projection_zero(oracle_mod):
+    g = GOLD["projection_zero"]
+    z = oracle_mod.subset_logits(f32(g["W"]), f32([g["h"]]), [0, 1, 2])
+    assert z.tolist() == [g["logits"]]
+
+
+def test_projection_subset_selects_rows(oracle_mod):
+    g = GOLD["projection"]
+    z = oracle_mod.subset_logits(f32(g["W"]), f32([g["h"]]), [2, 0])
+    assert z.tolist() == [[5, 2]]
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "fp32"])
+def test_full_vocab_subset_equals_unpruned_matmul(oracle_mod, dtype):
+    """North star: the full-vocab subset reproduces the unpruned projection."""
+    V, d, n_h = 300, 96, 5
+    W = synth.matrix(1, V, d, 0.02, dtype)
+    H = synth.matrix(2, n_h, d, 1.0, dtype)
+    dec = bf16_decode_independent if dtype == "bf16" else (lambda a: np.asarray(a, np.float64))
+    ref = dec(H) @ dec(W).T
+    z = oracle_mod.subset_logits(W, H, np.arange(V))
+    np.testing.assert_allclose(z, ref, rtol=1e-12, atol=1e-12)
+    # inv_temp scales
+    z2 = oracle_mod.subset_logits(W, H, np.arange(V), inv_temp=1 / 0.7)
+    np.testing.assert_allclose(z2, ref / 0.7, rtol=1e-12, atol=1e-12)
+
+
+def test_linearity(oracle_mod):
+    """l(a h1 + b h2) = a l(h1) + b l(h2)."""
+    V, d = 50, 16
+    W = synth.matrix(3, V, d, 1.0, "fp32")
+    h1 = synth.int_matrix(4, 1, d, "fp32")     # integer h: a*h1 + b*h2 exact in fp32
+    h2 = synth.int_matrix(5, 1, d, "fp32")
+    a, b = 0.5, -2.0
+    hc = (a * h1.astype(np.float64) + b * h2.astype(np.float64)).astype(np.float32)
+    S = np.arange(V)
+    lhs = oracle_mod.subset_logits(W, hc, S)
+    rhs = a * oracle_mod.subset_logits(W, h1, S) + b * oracle_mod.subset_logits(W, h2, S)
+    np.testing.assert_allclose(lhs, rhs, rtol=1e-9, atol=1e-9)
+
+
+def test_sharded_rows_map(oracle_mod):
+    """§8(e) interleaved ownership: shard r holds id v at local row v // R."""
+    V, d, R = 97, 8, 3
+    W = synth.int_matrix(6, V, d, "fp32")
+    H = synth.int_matrix(7, 2, d, "fp32")
+    S = np.sort(np.random.default_rng(0).choice(V, 40, replace=False)).astype(np.int32)
+    full = oracle_mod.subset_logits(W, H, S)
+    for r in range(R):
+        Sr = S[S % R == r]
+        zr = oracle_mod.subset_logits(np.ascontiguousarray(W[r::R]), H, Sr, R=R)
+        np.testing.assert_array_equal(zr, full[:, S % R == r])
+
+
+# ------------------------------------------------------- a6/a7 softmax, topk
+@pytest.mark.parametrize("name", ["restricted_singleton", "restricted_equal", "restricted_2_0"])
+def test_restricted_examples(oracle_mod, name):
+    g = GOLD[name]
+    z = np.array([g["logits"]], np.float64)
+    r = oracle_mod.softmax_topk(z, g["support"], len(g["support"]))
+    got = dict(zip(r["ids"][0].tolist(), r["probs"][0].tolist()))
+    tol = g.get("tol", 1e-12)
+    for sid, p in zip(g["support"], g["probs"]):
+        assert abs(got[sid] - p) <= tol
+
+
+def test_topk_examples(oracle_mod):
+    g = GOLD["topk"]
+    r = oracle_mod.softmax_topk(np.array([g["logits"]], float), [0, 1, 2], g["k"])
+    assert r["ids"][0].tolist() == g["ids"] and r["vals"][0].tolist() == g["vals"]
+    g = GOLD["topk_tie"]
+    r = oracle_mod.softmax_topk(np.array([g["logits"]], float), [0, 1, 2], g["k"])
+    assert r["ids"][0].tolist() == g["ids"]
+
+
+def test_topk_ties_follow_subset_ids_not_positions(oracle_mod):
+    # tie between ids 9 and 4 (support order [4, 9]): lower id wins
+    r = oracle_mod.softmax_topk(np.array([[1.0, 1.0, 0.0]]), [4, 9, 11], 2)
+    assert r["ids"][0].tolist() == [4, 9]
+
+
+def test_topk_k_equals_support_is_permutation_and_lexsort(oracle_mod):
+    rng = np.random.default_rng(0)
+    S = np.sort(rng.choice(500, 64, replace=False)).astype(np.int32)
+    z = rng.integers(-3, 4, size=(3, 64)).astype(np.float64)  # many exact ties
+    r = oracle_mod.softmax_topk(z, S, 64)
+    for i in range(3):
+        assert sorted(r["ids"][i].tolist()) == S.tolist()
+        order = np.lexsort((S, -z[i]))  # independent (-z, id) sort
+        assert r["ids"][i].tolist() == S[order].tolist()
+
+
+def test_softmax_closed_forms(oracle_mod):
+    rng = np.random.default_rng(1)
+    z = rng.standard_normal((4, 200)) * 3
+    S = np.arange(200, dtype=np.int32)
+    r = oracle_mod.softmax_topk(z, S, 200)
+    for i in range(4):
+        assert abs(math.fsum(r["probs"][i]) - 1.0) < 1e-12
+        assert abs(r["lse"][i] - logsumexp(z[i])) < 1e-12
+        assert r["m"][i] == z[i].max()
+        assert abs(r["lse"][i] - (r["m"][i] + math.log(r["s"][i]))) < 1e-12
+    # equal logits c -> LSE = c + ln n
+    r = oracle_mod.softmax_topk(np.full((1, 37), 2.5), np.arange(37), 3)
+    assert abs(r["lse"][0] - (2.5 + math.log(37))) < 1e-12
+    assert r["ids"][0].tolist() == [0, 1, 2]
+
+
+def test_shift_invariance_via_augmented_column(oracle_mod):
+    """adding c to every logit (h'=[h,c], W'=[W,1]) keeps ids and p; LSE + c."""
+    V, d, c = 64, 12, 3.0
+    W = synth.matrix(8, V, d, 1.0, "fp32")
+    H = synth.matrix(9, 2, d, 1.0, "fp32")
+    W2 = np.concatenate([W, np.ones((V, 1), np.float32)], 1)
+    H2 = np.concatenate([H, np.full((2, 1), c, np.float32)], 1)
+    S = np.arange(0, V, 2, dtype=np.int32)
+    a = oracle_mod.subset_logits_topk(W, H, S, 5)
+    b = oracle_mod.subset_logits_topk(W2, H2, S, 5)
+    np.testing.assert_array_equal(a["ids"], b["ids"])
+    np.testing.assert_allclose(a["probs"], b["probs"], atol=1e-12)
+    np.testing.assert_allclose(a["lse"] + c, b["lse"], atol=1e-9)
+
+
+@pytest.mark.parametrize("inv_temp", [1.0, 1 / 0.7])
+def test_restricted_equals_conditioned_full_softmax_bruteforce(oracle_mod, inv_temp):
+    """S:97, brute force for V <= 64 (brute.py, fsum)."""
+    V, d = 64, 8
+    W = synth.int_matrix(10, V, d, "fp32")
+    H = synth.int_matrix(11, 1, d, "fp32")
+    full = [float(brute.dot(H[0], W[v])) for v in range(V)]
+    S = [1, 5, 6, 17, 30, 31, 44, 63]
+    r = oracle_mod.subset_logits_topk(W, H, np.array(S, np.int32), len(S), inv_temp=inv_temp)
+    cond = brute.full_softmax_conditioned(full, S, inv_temp)
+    got = dict(zip(r["ids"][0].tolist(), r["probs"][0].tolist()))
+    for v in S:
+        assert abs(got[v] - cond[v]) < 1e-12
+    assert r["ids"][0].tolist() == brute.order_desc([full[v] for v in S], S)
+
+
+# ----------------------------------------------------------- a2 semantic
+def test_mips_example(oracle_mod):
+    g = GOLD["mips"]
+    s = oracle_mod.sem_scores(f32(g["E"]), f32(g["q"]))
+    assert s.tolist() == g["scores"]
+    assert oracle_mod.topn(s, g["N"]).tolist() == g["ids"]
+
+
+def test_sem_scores_bf16_against_independent_decode(oracle_mod):
+    V, d = 257, 128
+    E = synth.matrix(12, V, d, 0.02, "bf16")
+    q = synth.matrix(13, 1, d, 1.0, "fp32")
+    s = oracle_mod.sem_scores(E, q)
+    ref = bf16_decode_independent(E) @ q[0].astype(np.float64)
+    np.testing.assert_allclose(s, ref, rtol=1e-12, atol=1e-13)
+
+
+def test_topn_full_permutation_and_ties(oracle_mod):
+    rng = np.random.default_rng(2)
+    s = rng.integers(-5, 6, size=300).astype(np.float64)   # heavy exact ties
+    ids = oracle_mod.topn(s, 300)
+    assert sorted(ids.tolist()) == list(range(300))
+    assert ids.tolist() == np.lexsort((np.arange(300), -s)).tolist()
+    assert oracle_mod.topn(s, 17).tolist() == ids[:17].tolist()
+
+
+# ------------------------------------------------------------ a3 graph
+def test_graph_expand_examples(oracle_mod):
+    row_ptr, col = csr_from_rows(GOLD["graph"]["V"], GOLD["graph"]["rows"])
+    for name in ["graph_expand_1", "graph_expand_2", "graph_expand_none"]:
+        g = GOLD[name]
+        assert oracle_mod.graph_expand(g["seeds"], row_ptr, col, g["per_seed"]).tolist() == g["out"]
+
+
+@pytest.mark.parametrize("name", ["ctx", "ctx_tie"])
+def test_ctx_tokens_examples(oracle_mod, name):
+    g = GOLD[name]
+    assert oracle_mod.ctx_tokens(g["ctx"], g["V"], g["min_count"], g["n_max"]).tolist() == g["out"]
+
+
+# ------------------------------------------------------------ a4 union
+def _onehot_sem(V, order):
+    """E (d=1) and q=[1] whose semantic order starts with `order`."""
+    E = np.zeros((V, 1), np.float32)
+    for rank, v in enumerate(order):
+        E[v, 0] = len(order) - rank
+    return E, f32([1.0])
+
+
+@pytest.mark.parametrize("n_dyn", [4, 6])
+def test_formation_worked_example(oracle_mod, n_dyn):
+    g = GOLD["formation"]
+    E, q = _onehot_sem(g["V"], g["sem_order"])
+    row_ptr, col = csr_from_rows(g["V"], g["rows"])
+    r = oracle_mod.build_subset(E, q, g["static"], g["seeds"], row_ptr, col,
+                                n_sem=len(g["sem_order"]), n_graph_sem_seeds=g["n_graph_sem_seeds"],
+                                per_seed=g["per_seed"], n_dyn=n_dyn)
+    assert r["sem"].tolist() == g["sem_order"]
+    assert r["S"].tolist() == g[f"S_ndyn{n_dyn}"]
+    assert r["dyn"].tolist() == g[f"dyn_ndyn{n_dyn}"]
+
+
+def test_union_examples(oracle_mod):
+    for name in ["union", "union_overlap"]:
+        g = GOLD[name]
+        V = 20
+        # dyn enters as seeds; n_sem = 0 so nothing else contributes
+        E = np.zeros((V, 1), np.float32)
+        r = oracle_mod.build_subset(E, f32([1.0]), g["static"], g["dyn"], None, None,
+                                    n_sem=0, n_graph_sem_seeds=0, per_seed=0, n_dyn=8)
+        S = set(r["S"].tolist())
+        if "contains" in g:
+            assert all(v in S for v in g["contains"]) and all(v not in S for v in g["absent"])
+        if "size" in g:
+            assert len(S) == g["size"]
+
+
+def test_cap_example(oracle_mod):
+    g = GOLD["cap"]
+    V = 100
+    seeds = list(range(20, 40))               # 20 unique seeds
+    rows = {str(20): list(range(60, 80))}      # 20 new graph ids from the first seed
+    row_ptr, col = csr_from_rows(V, rows)
+    E = np.zeros((V, 1), np.float32)
+    r = oracle_mod.build_subset(E, f32([1.0]), [0], seeds, row_ptr, col, n_sem=0,
+                                n_graph_sem_seeds=0, per_seed=20, n_dyn=g["cap"])
+    assert len(r["dyn"]) == g["n_dyn_out"]
+    assert r["dyn"].tolist() == seeds + list(range(60, 72))  # formation order, 20 + first 12
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_build_subset_bruteforce(oracle_mod, seed):
+    rng = np.random.default_rng(100 + seed)
+    V, d = 64, 6
+    E = synth.int_matrix(seed, V, d, "fp32")
+    q = synth.int_matrix(seed + 50, 1, d, "fp32")
+    static = np.sort(rng.choice(V, 12, replace=False)).astype(np.int32)
+    seeds = rng.choice(V, 4, replace=False).astype(np.int32)
+    rows = {}
+    for u in range(V):
+        k = int(rng.integers(0, 5))
+        rows[str(u)] = [int(x) for x in rng.choice(V, k, replace=False)]
+    row_ptr, col = csr_from_rows(V, rows)
+    n_sem, ngs, per, n_dyn = 10, 3, 2, int(rng.integers(3, 20))
+    r = oracle_mod.build_subset(E, q, static, seeds, row_ptr, col, n_sem=n_sem,
+                                n_graph_sem_seeds=ngs, per_seed=per, n_dyn=n_dyn)
+    bS, bsem, bdyn = brute.build_subset(E.tolist(), q[0].tolist(), static.tolist(), seeds.tolist(),
+                                        {int(k): v for k, v in rows.items()}, n_sem, ngs, per, n_dyn)
+    assert r["sem"].tolist() == bsem
+    assert r["dyn"].tolist() == bdyn
+    assert r["S"].tolist() == bS
+    # invariants: sorted unique, in range, static subset, budget
+    S = r["S"]
+    assert np.all(np.diff(S) > 0) and S.min() >= 0 and S.max() < V
+    assert set(static.tolist()) <= set(S.tolist())
+    assert len(set(S.tolist()) - set(static.tolist())) <= n_dyn
+
+
+def test_build_subset_rejects_unsorted_static(oracle_mod):
+    E = np.zeros((10, 1), np.float32)
+    with pytest.raises(ValueError):
+        oracle_mod.build_subset(E, f32([1.0]), [3, 1], [], None, None, n_sem=0,
+                                n_graph_sem_seeds=0, per_seed=0, n_dyn=2)
+
+
+# ------------------------------------------------------------ a8 merge
+def test_merge_worked_example(oracle_mod):
+    g = GOLD["merge"]
+    z = np.array([g["z"]], np.float64)
+    R, k = g["R"], g["k"]
+    trip = []
+    for r in range(R):
+        Sr = np.array([v for v in range(6) if v % R == r], np.int32)
+        trip.append(oracle_mod.softmax_topk(z[:, Sr], Sr, k))
+    for r in range(R):
+        assert abs(trip[r]["m"][0] - g["m"][r]) < g["tol"]
+        assert abs(trip[r]["s"][0] - g["s"][r]) < g["tol"]
+    out = oracle_mod.merge(np.stack([t["ids"] for t in trip]), np.stack([t["vals"] for t in trip]),
+                           np.stack([t["m"] for t in trip]), np.stack([t["s"] for t in trip]), k)
+    assert out["ids"][0].tolist() == g["ids"]
+    assert abs(out["lse"][0] - g["lse"]) < g["tol"]
+    np.testing.assert_allclose(out["probs"][0], g["probs"], atol=g["tol"])
+
+
+@pytest.mark.parametrize("R", [1, 2, 3, 4])
+def test_merge_of_split_equals_unsplit(oracle_mod, R):
+    V, d, n_h, k = 211, 16, 3, 7
+    W = synth.int_matrix(20, V, d, "fp32")       # integer data: real ties across shards
+    H = synth.int_matrix(21, n_h, d, "fp32")
+    S = np.sort(np.random.default_rng(3).choice(V, 90, replace=False)).astype(np.int32)
+    ref = oracle_mod.subset_logits_topk(W, H, S, k)
+    parts = [oracle_mod.subset_logits_topk(np.ascontiguousarray(W[r::R]), H, S[S % R == r], k, R=R)
+             for r in range(R)]
+    st = lambda key: np.stack([p[key] for p in parts])
+    out = oracle_mod.merge(st("ids"), st("vals"), st("m"), st("s"), k)
+    np.testing.assert_array_equal(out["ids"], ref["ids"])
+    np.testing.assert_allclose(out["lse"], ref["lse"], rtol=1e-12)
+    np.testing.assert_allclose(out["probs"], ref["probs"], atol=1e-12)
+    # shard order invariance
+    perm = np.random.default_rng(4).permutation(R)
+    out2 = oracle_mod.merge(st("ids")[perm], st("vals")[perm], st("m")[perm], st("s")[perm], k)
+    np.testing.assert_array_equal(out2["ids"], out["ids"])
+    np.testing.assert_allclose(out2["lse"], out["lse"], rtol=1e-12)
+
+
+def test_merge_skips_empty_shard_and_pads(oracle_mod):
+    z = np.array([[0.5, 1.5]])
+    a = oracle_mod.softmax_topk(z, [2, 4], 3)
+    empty = oracle_mod.softmax_topk(np.zeros((1, 0)), [], 3)
+    assert empty["m"][0] == -np.inf and empty["s"][0] == 0 and empty["ids"][0].tolist() == [-1, -1, -1]
+    st = lambda key: np.stack([a[key], empty[key]])
+    out = oracle_mod.merge(st("ids"), st("vals"), st("m"), st("s"), 3)
+    assert out["ids"][0].tolist() == [4, 2, -1]
+    assert abs(out["lse"][0] - logsumexp([0.5, 1.5])) < 1e-12
