@@ -1,0 +1,260 @@
+/*
+ * evospec.h -- C ABI of libevospec.so, the B200 (sm_100a) hot path of
+ * EvoSpec's dynamic-vocabulary draft LM head (arXiv 2605.27390).
+ *
+ * The path (PAPER.md = P:n, SPEC.md = S:n):
+ *   evospec_build_subset        a1-a4  V_t = V_static u S_sem(h) u S_graph(.)
+ *                                       (Eq. vocab_union; runtime
+ *                                       formation P:458; budget P:60)
+ *   evospec_subset_logits_topk  a5-a7  z = (H . W[V_t]^T) * inv_temp, fused
+ *                                       online softmax (m, s) and top-k
+ *                                       (Eq. projection; alg:evospec
+ *                                       "restricted to V_t" P:364)
+ *   evospec_merge_shards        a8     vocab-shard merge of (top-k, m, s)
+ *                                       triples (north star; NCCL all-gather
+ *                                       when the context owns a communicator)
+ *
+ * Conventions (all entry points):
+ *   - Plain pointers and sizes only. "dev" pointers are CUDA device memory
+ *     owned by the CALLER (the library never frees them); "host" pointers are
+ *     host memory. Every call is asynchronous on the given stream (a
+ *     cudaStream_t passed as void*; NULL = legacy default stream) and performs
+ *     no host synchronisation unless stated.
+ *   - Layouts are row-major, contiguous, little-endian. bf16 is stored as its
+ *     16-bit pattern. Token ids are int32 GLOBAL vocabulary ids.
+ *   - Shards: with n_shards = R, shard r owns the ids v = r (mod R); its
+ *     W_local / E_local hold id v at local row v / R.
+ *   - Ties: every ordering is (value desc, id asc).
+ *   - Errors: host-checkable problems return EVOSPEC_EINPUT before any launch
+ *     (null pointers, sizes out of the context's capacity, k < 1, inv_temp <= 0
+ *     or non-finite, d mismatch). CUDA / NCCL failures return EVOSPEC_ECUDA /
+ *     EVOSPEC_ENCCL. Device-side conditions (unsorted or out-of-range ids when
+ *     debug_checks = 1, a top-k row whose exact order could not be certified,
+ *     a selection tie band larger than the workspace) are accumulated in a
+ *     device flag word read by evospec_get_flags(). Detail for the last error
+ *     on the calling thread: evospec_last_error().
+ */
+#ifndef EVOSPEC_H
+#define EVOSPEC_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct evospec_ctx evospec_ctx;
+
+typedef int32_t evospec_status;
+#define EVOSPEC_OK          0
+#define EVOSPEC_EINPUT      2   /* mirrors SPEC's input-error exit code */
+#define EVOSPEC_EINVARIANT  3   /* mirrors SPEC's invariant exit code   */
+#define EVOSPEC_ECUDA      10
+#define EVOSPEC_ENCCL      11
+#define EVOSPEC_ENOMEM     12
+
+#define EVOSPEC_BF16 0
+#define EVOSPEC_FP32 1
+
+/* Device flag bits (evospec_get_flags). */
+#define EVOSPEC_FLAG_BAD_IDS        0x1  /* debug: unsorted / out-of-range ids   */
+#define EVOSPEC_FLAG_UNCERTIFIED    0x2  /* a top-k row whose exact order could
+                                            not be certified from the kept band  */
+#define EVOSPEC_FLAG_SELECT_OVERFLOW 0x4 /* semantic selection overflowed        */
+#define EVOSPEC_FLAG_BUDGET         0x8  /* |V_t \ V_static| > N_dyn (never)      */
+
+/* Context configuration, fixed at create time. Sizes are capacities. */
+typedef struct {
+    int32_t V;            /* global vocabulary size |V|                 */
+    int32_t d;            /* hidden size d; multiple of 8                      */
+    int32_t w_dtype;      /* EVOSPEC_BF16 / EVOSPEC_FP32: W_local and E_local  */
+    int32_t h_dtype;      /* dtype of H and q                                  */
+    int32_t n_shards;     /* R >= 1 vocabulary shards                          */
+    int32_t shard_rank;   /* r in [0, R)                                       */
+    int32_t max_subset;   /* capacity for n_S (global), >= n_static + n_dyn    */
+    int32_t max_rows;     /* max n_h per call (draft-tree nodes: 60)    */
+    int32_t max_k;        /* max k, 1..64                                      */
+    int32_t max_sem;      /* max N_sem (semantic top-N)                        */
+    int32_t max_seeds;    /* max n_seed + n_graph_sem_seeds                    */
+    int32_t max_ctx;      /* max context tokens for the count source (<= 8192) */
+    int32_t debug_checks; /* 1: validate id lists on the device                */
+} evospec_config;
+
+/* Builder parameters; paper defaults in brackets (tab:hyperparams P:417-424). */
+typedef struct {
+    int32_t n_sem;             /* N_sem, semantic top-N            [10]         */
+    int32_t n_graph_sem_seeds; /* S_sem prefix that seeds the graph [10]        */
+    int32_t per_seed;          /* graph successors per seed         [8]         */
+    int32_t ctx_min_count;     /* context-count source; 0 = off     [0]         */
+    int32_t n_ctx_max;         /* max tokens from the count source  [0]         */
+    int32_t n_dyn;             /* N_dyn dynamic budget              [256]       */
+} evospec_build_params;
+
+/* ---- lifecycle ---------------------------------------------------------- */
+
+/* Allocates the context and its device workspace on `device`. */
+evospec_status evospec_create(evospec_ctx **out, const evospec_config *cfg, int device);
+/* Frees the workspace (and the NCCL communicator, if any). NULL is a no-op. */
+evospec_status evospec_destroy(evospec_ctx *ctx);
+const char *evospec_status_string(evospec_status st);
+/* Thread-local detail of the last non-OK status returned on this thread. */
+const char *evospec_last_error(void);
+/* Library version string. */
+const char *evospec_version(void);
+
+/* Per-weight-tensor preparation (once per W, off the hot path): computes the
+ * max row 2-norm of W_local [n_rows, d] into the context; the top-k
+ * certification band uses it. Async on stream. */
+evospec_status evospec_prepare_weights(evospec_ctx *ctx, const void *W_local_dev,
+                                       int64_t n_rows, void *stream);
+
+/* Reads (and with clear=1 resets) the device flag word. Synchronises the
+ * stream. flags_out: host int32. */
+evospec_status evospec_get_flags(evospec_ctx *ctx, int32_t *flags_out, int clear, void *stream);
+
+/* ---- multi-GPU communicator (vocab sharding) ---------------- */
+
+/* Writes a 128-byte NCCL unique id into uid_out (host). Rank 0 calls it; the
+ * caller broadcasts the bytes (e.g. over a torch.distributed group). */
+evospec_status evospec_comm_unique_id(void *uid_out);
+/* Creates the context's own communicator of n_shards ranks, rank shard_rank.
+ * Blocking (collective over all ranks). */
+evospec_status evospec_comm_init(evospec_ctx *ctx, const void *uid);
+
+/* ---- a1-a4: subset builder --------------------------------------------- */
+
+/* Builds V_t = sort(V_static u dyn), dyn = the first N_dyn ids, in formation
+ * order, of  seeds ++ S_sem ++ S_graph ++ S_ctx  that are not static and not
+ * already taken (readings C1-C9 in DESIGN.md):
+ *   S_sem  = top-N_sem ids by (q . E_v desc, id asc), exact (fp64) scores;
+ *   G      = dedupe(seeds ++ S_sem[:n_graph_sem_seeds]);
+ *   S_graph= concat over g in G of the first per_seed entries of CSR row g;
+ *   S_ctx  = ids of ctx_ids with count >= ctx_min_count by (count desc, id
+ *            asc), the first n_ctx_max (off when ctx_min_count = 0).
+ * E_dev: [n_e_rows, d] w_dtype. n_e_rows == V: the full index (every rank
+ *   scans all of it). n_e_rows == rows of this shard (R > 1): each rank scans
+ *   its interleaved shard and the candidates are exchanged over the context's
+ *   communicator (requires evospec_comm_init).
+ * q_dev: [d] h_dtype (the target-side hidden state of the verify pass).
+ * static_dev: [n_static] sorted ascending unique; seed_dev: [n_seed].
+ * csr_row_ptr_dev [V+1] / csr_col_dev [nnz]: rows sorted (p desc, id asc);
+ *   both may be NULL (no graph). ctx_dev: [n_ctx] or NULL.
+ * Outputs (device, caller-owned): out_ids [n_static + n_dyn] sorted ascending,
+ *   out_n [1] = n_S; out_local_ids [capacity n_static + n_dyn] = the ids of
+ *   out_ids owned by this shard (v mod R == r), out_local_n [1]; the local
+ *   pair may be NULL when R == 1. Nothing is synchronised: n_S stays on the
+ *   device and the LM-head call reads it there. */
+evospec_status evospec_build_subset(evospec_ctx *ctx,
+    const void *E_dev, int64_t n_e_rows, const void *q_dev,
+    const int32_t *static_dev, int32_t n_static,
+    const int32_t *seed_dev, int32_t n_seed,
+    const int32_t *csr_row_ptr_dev, const int32_t *csr_col_dev,
+    const int32_t *ctx_dev, int32_t n_ctx,
+    const evospec_build_params *params,
+    int32_t *out_ids, int32_t *out_n,
+    int32_t *out_local_ids, int32_t *out_local_n,
+    void *stream);
+
+/* Debug/parity accessor: copies the ordered S_sem of the last build on this
+ * context (device ids, N_sem entries) into out_dev. Async on stream. */
+evospec_status evospec_last_semantic(evospec_ctx *ctx, int32_t *out_dev, int32_t n, void *stream);
+
+/* ---- a5-a7: gathered LM head + fused softmax / top-k --------------------- */
+
+/* For each row r < n_h of H and each position j < n_S (n_S read from
+ * n_subset_dev on the device, n_S <= n_subset_max):
+ *   z[r][j] = inv_temp * sum_c H[r][c] * W_local[subset[j] / R][c]
+ * and returns this shard's triple:
+ *   topk_ids  [n_h, k] int32  global ids of the k largest z, (z desc, id asc)
+ *   topk_vals [n_h, k] fp32   their z (ordered by the exact fp64 re-score)
+ *   row_max   [n_h]    fp32   m = max_j z[r][j]
+ *   row_sumexp[n_h]    fp32   s = sum_j exp(z[r][j] - m)
+ * Empty subset: m = -inf, s = 0; k > n_S pads id -1 / value -inf.
+ * W_local_dev: [n_w_rows, d] w_dtype; H_dev: [n_h, d] h_dtype.
+ * subset_dev: sorted ascending unique, every id owned by this shard.
+ * logits_out: optional [n_h, n_subset_max] fp32 z (debug / parity only;
+ * NULL on the hot path -- the logits are otherwise never written). */
+evospec_status evospec_subset_logits_topk(evospec_ctx *ctx,
+    const void *W_local_dev, int64_t n_w_rows,
+    const void *H_dev, int32_t n_h,
+    const int32_t *subset_dev, const int32_t *n_subset_dev, int32_t n_subset_max,
+    int32_t k, float inv_temp,
+    int32_t *topk_ids, float *topk_vals, float *row_max, float *row_sumexp,
+    float *logits_out, void *stream);
+
+/* ---- a8: vocab-shard merge ------------------------------------------------ */
+
+/* With a communicator (R > 1): all-gathers this rank's triple over NCCL into
+ * the workspace, then merges. Without one: the inputs are the R triples
+ * already stacked as [R, n_h, k] / [R, n_h] (R = n_shards; R = 1 is the
+ * single-GPU finalisation). Over the shards with s_r > 0:
+ *   M = max_r m_r, Sigma = sum_r s_r exp(m_r - M), LSE = M + ln Sigma,
+ *   out top-k of the R*k candidates by (value desc, id asc),
+ *   out_probs = exp(value - LSE).
+ * Outputs: out_ids [n_h, k] int32, out_vals [n_h, k] fp32, out_lse [n_h] fp32,
+ * out_probs [n_h, k] fp32 (may be NULL). */
+evospec_status evospec_merge_shards(evospec_ctx *ctx, int32_t n_h, int32_t k,
+    const int32_t *topk_ids, const float *topk_vals,
+    const float *row_max, const float *row_sumexp,
+    int32_t *out_ids, float *out_vals, float *out_lse, float *out_probs,
+    void *stream);
+
+/* ---- one draft step through the whole path -------------------------------- */
+
+/* Per-step I/O for evospec_draft_step. `host_io` = 1: q, H, seeds, ctx and
+ * the four outputs are HOST buffers (pinned for async copies) and the call
+ * stages them through the context's device buffers (H2D before, D2H after,
+ * on the same stream); 0: they are device buffers. Model-resident tensors
+ * (E, W_local, static set, CSR) are always device pointers. */
+typedef struct {
+    const void *E;        int64_t n_e_rows;
+    const void *W_local;  int64_t n_w_rows;
+    const int32_t *static_ids; int32_t n_static;
+    const int32_t *csr_row_ptr; const int32_t *csr_col;
+    evospec_build_params build;
+    int32_t n_h; int32_t k; float inv_temp;
+    const void *q;                 /* [d]        */
+    const void *H;                 /* [n_h, d]   */
+    const int32_t *seeds; int32_t n_seed;
+    const int32_t *ctx_ids; int32_t n_ctx;
+    int32_t *out_ids;              /* [n_h, k]   */
+    float *out_vals;               /* [n_h, k]   */
+    float *out_lse;                /* [n_h]      */
+    float *out_probs;              /* [n_h, k]   */
+    int32_t host_io;
+} evospec_step_io;
+
+/* build_subset -> subset_logits_topk -> merge_shards on one stream. With
+ * host_io = 1 the call returns after the D2H copies are enqueued; the caller
+ * synchronises the stream before reading the outputs. */
+evospec_status evospec_draft_step(evospec_ctx *ctx, const evospec_step_io *io, void *stream);
+
+/* ---- measurement hooks (bench / profiling; off by default) ---------------- */
+
+#define EVOSPEC_STAGE_SCAN      0  /* a2 semantic scan q . E^T                 */
+#define EVOSPEC_STAGE_SELECT    1  /* a2 top-N select + exact order (+ NCCL)   */
+#define EVOSPEC_STAGE_UNION     2  /* a3/a4 context counts, formation, union   */
+#define EVOSPEC_STAGE_LMH       3  /* a5-a7 gathered LM head main kernel(s)    */
+#define EVOSPEC_STAGE_FINALIZE  4  /* a6/a7 per-shard finalisation + re-score  */
+#define EVOSPEC_STAGE_MERGE     5  /* a8 all-gather + merge                    */
+#define EVOSPEC_STAGE_COPY      6  /* draft_step host<->device staging         */
+#define EVOSPEC_NUM_STAGES      7
+
+typedef struct {
+    int64_t launches;                    /* kernels this library launched     */
+    int32_t calls[EVOSPEC_NUM_STAGES];   /* timed calls per stage             */
+    float stage_ms[EVOSPEC_NUM_STAGES];  /* summed device time per stage (ms) */
+} evospec_stats;
+
+/* enable = 1: reset the counters and record CUDA events around every stage
+ * on the caller's stream (up to 4096 calls per stage); enable = 0: stop. */
+evospec_status evospec_set_timing(evospec_ctx *ctx, int enable);
+/* Synchronises the recorded events and returns the sums since the last
+ * evospec_set_timing(ctx, 1). The launch counter runs always. */
+evospec_status evospec_read_stats(evospec_ctx *ctx, evospec_stats *out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EVOSPEC_H */

@@ -1,0 +1,297 @@
+"""Thin Python binding over libevospec.so (include/evospec.h).
+
+Argument marshalling only: every step of the EvoSpec subset LM-head path runs
+in the library's CUDA kernels. torch supplies device memory, streams and
+process groups. There is no CPU fallback: importing this package without the
+built library, or calling it without a CUDA device, raises.
+
+Names follow the C ABI: build_subset, subset_logits_topk, merge_shards,
+draft_step (PAPER.md Eq. projection, Eq. vocab_union P:88-93,
+runtime formation P:458).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libevospec.so")
+
+BF16, FP32 = 0, 1
+OK, EINPUT, EINVARIANT, ECUDA, ENCCL, ENOMEM = 0, 2, 3, 10, 11, 12
+FLAG_BAD_IDS, FLAG_UNCERTIFIED, FLAG_SELECT_OVERFLOW, FLAG_BUDGET = 0x1, 0x2, 0x4, 0x8
+
+EXPORTED = [
+    "evospec_create", "evospec_destroy", "evospec_status_string", "evospec_last_error",
+    "evospec_version", "evospec_prepare_weights", "evospec_get_flags",
+    "evospec_comm_unique_id", "evospec_comm_init", "evospec_build_subset",
+    "evospec_last_semantic", "evospec_subset_logits_topk", "evospec_merge_shards",
+    "evospec_draft_step", "evospec_set_timing", "evospec_read_stats",
+]
+
+STAGES = ["scan", "select", "union", "lmh", "finalize", "merge", "copy"]
+
+
+class EvospecError(RuntimeError):
+    def __init__(self, status: int, detail: str):
+        super().__init__(f"evospec status {status}: {detail}")
+        self.status = status
+
+
+class Config(C.Structure):
+    _fields_ = [(n, C.c_int32) for n in (
+        "V", "d", "w_dtype", "h_dtype", "n_shards", "shard_rank", "max_subset", "max_rows",
+        "max_k", "max_sem", "max_seeds", "max_ctx", "debug_checks")]
+
+
+class BuildParams(C.Structure):
+    _fields_ = [(n, C.c_int32) for n in (
+        "n_sem", "n_graph_sem_seeds", "per_seed", "ctx_min_count", "n_ctx_max", "n_dyn")]
+
+
+class Stats(C.Structure):
+    _fields_ = [("launches", C.c_int64), ("calls", C.c_int32 * 7), ("stage_ms", C.c_float * 7)]
+
+
+class StepIO(C.Structure):
+    _fields_ = [
+        ("E", C.c_void_p), ("n_e_rows", C.c_int64),
+        ("W_local", C.c_void_p), ("n_w_rows", C.c_int64),
+        ("static_ids", C.c_void_p), ("n_static", C.c_int32),
+        ("csr_row_ptr", C.c_void_p), ("csr_col", C.c_void_p),
+        ("build", BuildParams),
+        ("n_h", C.c_int32), ("k", C.c_int32), ("inv_temp", C.c_float),
+        ("q", C.c_void_p), ("H", C.c_void_p),
+        ("seeds", C.c_void_p), ("n_seed", C.c_int32),
+        ("ctx_ids", C.c_void_p), ("n_ctx", C.c_int32),
+        ("out_ids", C.c_void_p), ("out_vals", C.c_void_p), ("out_lse", C.c_void_p),
+        ("out_probs", C.c_void_p), ("host_io", C.c_int32),
+    ]
+
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Loads libevospec.so; raises if it has not been built (no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} missing: run `python -m paper_2605_27390_b200._build` "
+                              "(or __graft_entry__.build()); there is no CPU fallback")
+        L = C.CDLL(LIB_PATH)
+        vp, i32, i64 = C.c_void_p, C.c_int32, C.c_int64
+        sig = {
+            "evospec_create": ([C.POINTER(vp), C.POINTER(Config), C.c_int], i32),
+            "evospec_destroy": ([vp], i32),
+            "evospec_status_string": ([i32], C.c_char_p),
+            "evospec_last_error": ([], C.c_char_p),
+            "evospec_version": ([], C.c_char_p),
+            "evospec_prepare_weights": ([vp, vp, i64, vp], i32),
+            "evospec_get_flags": ([vp, C.POINTER(i32), C.c_int, vp], i32),
+            "evospec_comm_unique_id": ([vp], i32),
+            "evospec_comm_init": ([vp, vp], i32),
+            "evospec_build_subset": ([vp, vp, i64, vp, vp, i32, vp, i32, vp, vp, vp, i32,
+                                      C.POINTER(BuildParams), vp, vp, vp, vp, vp], i32),
+            "evospec_last_semantic": ([vp, vp, i32, vp], i32),
+            "evospec_subset_logits_topk": ([vp, vp, i64, vp, i32, vp, vp, i32, i32, C.c_float,
+                                            vp, vp, vp, vp, vp, vp], i32),
+            "evospec_merge_shards": ([vp, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp], i32),
+            "evospec_draft_step": ([vp, C.POINTER(StepIO), vp], i32),
+            "evospec_set_timing": ([vp, C.c_int], i32),
+            "evospec_read_stats": ([vp, C.POINTER(Stats)], i32),
+        }
+        for name, (args, res) in sig.items():
+            f = getattr(L, name)
+            f.argtypes = args
+            f.restype = res
+        _lib = L
+    return _lib
+
+
+def _check(st: int):
+    if st != OK:
+        raise EvospecError(st, lib().evospec_last_error().decode())
+
+
+def _ptr(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _stream(stream):
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def version() -> str:
+    return lib().evospec_version().decode()
+
+
+def _dtype_code(t) -> int:
+    import torch
+    if t == torch.bfloat16:
+        return BF16
+    if t == torch.float32:
+        return FP32
+    raise TypeError(f"unsupported dtype {t} (bf16 or fp32)")
+
+
+class Context:
+    """Owns an evospec_ctx (device workspace + optional NCCL communicator)."""
+
+    def __init__(self, *, V: int, d: int, w_dtype, h_dtype, n_shards: int = 1, shard_rank: int = 0,
+                 max_subset: int, max_rows: int, max_k: int = 64, max_sem: int = 8192,
+                 max_seeds: int = 64, max_ctx: int = 0, debug_checks: bool = False, device: int = 0):
+        import torch
+        if not torch.cuda.is_available():
+            raise RuntimeError("evospec needs a CUDA device (B200, sm_100a); there is no CPU path")
+        self.cfg = Config(V, d, _dtype_code(w_dtype), _dtype_code(h_dtype), n_shards, shard_rank,
+                          max_subset, max_rows, max_k, max_sem, max_seeds, max_ctx, int(debug_checks))
+        self.device = device
+        h = C.c_void_p()
+        _check(lib().evospec_create(C.byref(h), C.byref(self.cfg), device))
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().evospec_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- setup
+    def prepare_weights(self, W, stream=None):
+        _check(lib().evospec_prepare_weights(self._h, _ptr(W), W.shape[0], _stream(stream)))
+
+    def set_timing(self, enable: bool = True):
+        _check(lib().evospec_set_timing(self._h, int(enable)))
+
+    def read_stats(self) -> dict:
+        st = Stats()
+        _check(lib().evospec_read_stats(self._h, C.byref(st)))
+        return dict(launches=st.launches,
+                    calls={n: st.calls[i] for i, n in enumerate(STAGES)},
+                    ms={n: st.stage_ms[i] for i, n in enumerate(STAGES)})
+
+    def get_flags(self, clear: bool = True, stream=None) -> int:
+        out = C.c_int32(0)
+        _check(lib().evospec_get_flags(self._h, C.byref(out), int(clear), _stream(stream)))
+        return out.value
+
+    def comm_init(self, group=None):
+        """Creates the library's NCCL communicator; the 128-byte unique id is
+        broadcast from rank 0 over the given torch.distributed group."""
+        import torch
+        import torch.distributed as dist
+        buf = (C.c_char * 128)()
+        if dist.get_rank(group) == 0:
+            _check(lib().evospec_comm_unique_id(buf))
+        t = torch.tensor(list(bytes(buf)), dtype=torch.uint8)
+        if dist.get_backend(group) == "nccl":
+            t = t.cuda(self.device)
+        dist.broadcast(t, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+        raw = bytes(t.cpu().tolist())
+        _check(lib().evospec_comm_init(self._h, C.c_char_p(raw)))
+
+    # ---- a1-a4
+    def build_subset(self, E, q, static_ids, seed_ids, csr_row_ptr, csr_col, *, n_sem: int,
+                     n_dyn: int, n_graph_sem_seeds: int = 10, per_seed: int = 8, ctx_ids=None,
+                     ctx_min_count: int = 0, n_ctx_max: int = 0, out=None, stream=None):
+        """Returns (ids, n_dev, local_ids, local_n_dev): device tensors; n stays on the device."""
+        import torch
+        dev = E.device
+        cap = static_ids.numel() + n_dyn
+        if out is None:
+            out = (torch.empty(max(cap, 1), dtype=torch.int32, device=dev),
+                   torch.empty(1, dtype=torch.int32, device=dev),
+                   torch.empty(max(cap, 1), dtype=torch.int32, device=dev),
+                   torch.empty(1, dtype=torch.int32, device=dev))
+        ids, n, lids, ln = out
+        p = BuildParams(n_sem, n_graph_sem_seeds, per_seed, ctx_min_count, n_ctx_max, n_dyn)
+        n_ctx = 0 if ctx_ids is None else ctx_ids.numel()
+        _check(lib().evospec_build_subset(
+            self._h, _ptr(E), E.shape[0], _ptr(q), _ptr(static_ids), static_ids.numel(),
+            _ptr(seed_ids) if seed_ids is not None else None,
+            0 if seed_ids is None else seed_ids.numel(),
+            _ptr(csr_row_ptr), _ptr(csr_col), _ptr(ctx_ids), n_ctx, C.byref(p),
+            _ptr(ids), _ptr(n), _ptr(lids), _ptr(ln), _stream(stream)))
+        return ids, n, lids, ln
+
+    def last_semantic(self, n: int, stream=None):
+        import torch
+        out = torch.empty(max(n, 1), dtype=torch.int32, device=f"cuda:{self.device}")
+        _check(lib().evospec_last_semantic(self._h, _ptr(out), n, _stream(stream)))
+        return out[:n]
+
+    # ---- a5-a7
+    def subset_logits_topk(self, W_local, H, subset, n_subset_dev, n_subset_max: int, k: int,
+                           inv_temp: float = 1.0, logits_out=None, out=None, stream=None):
+        """Returns this shard's triple (topk_ids, topk_vals, row_max, row_sumexp)."""
+        import torch
+        n_h = H.shape[0]
+        dev = H.device
+        if out is None:
+            out = (torch.empty((n_h, k), dtype=torch.int32, device=dev),
+                   torch.empty((n_h, k), dtype=torch.float32, device=dev),
+                   torch.empty(n_h, dtype=torch.float32, device=dev),
+                   torch.empty(n_h, dtype=torch.float32, device=dev))
+        ids, vals, m, s = out
+        _check(lib().evospec_subset_logits_topk(
+            self._h, _ptr(W_local), W_local.shape[0], _ptr(H), n_h, _ptr(subset), _ptr(n_subset_dev),
+            n_subset_max, k, float(inv_temp), _ptr(ids), _ptr(vals), _ptr(m), _ptr(s),
+            _ptr(logits_out), _stream(stream)))
+        return ids, vals, m, s
+
+    # ---- a8
+    def merge_shards(self, ids, vals, m, s, *, n_h: int, k: int, out=None, stream=None):
+        """Returns (ids, vals, lse, probs) merged over the shards."""
+        import torch
+        dev = ids.device
+        if out is None:
+            out = (torch.empty((n_h, k), dtype=torch.int32, device=dev),
+                   torch.empty((n_h, k), dtype=torch.float32, device=dev),
+                   torch.empty(n_h, dtype=torch.float32, device=dev),
+                   torch.empty((n_h, k), dtype=torch.float32, device=dev))
+        oi, ov, ol, op = out
+        _check(lib().evospec_merge_shards(self._h, n_h, k, _ptr(ids), _ptr(vals), _ptr(m), _ptr(s),
+                                          _ptr(oi), _ptr(ov), _ptr(ol), _ptr(op), _stream(stream)))
+        return oi, ov, ol, op
+
+    # ---- whole step
+    def draft_step(self, *, E, W_local, static_ids, csr_row_ptr, csr_col, q, H, seeds, k: int,
+                   n_sem: int, n_dyn: int, n_graph_sem_seeds: int = 10, per_seed: int = 8,
+                   inv_temp: float = 1.0, ctx_ids=None, ctx_min_count: int = 0, n_ctx_max: int = 0,
+                   out=None, stream=None):
+        """One draft step. q/H/seeds/ctx and `out` may be pinned HOST tensors
+        (then the call stages them through device buffers) or device tensors."""
+        import torch
+        host_io = not H.is_cuda
+        n_h = H.shape[0]
+        if out is None:
+            kw = dict(pin_memory=True) if host_io else dict(device=H.device)
+            out = (torch.empty((n_h, k), dtype=torch.int32, **kw),
+                   torch.empty((n_h, k), dtype=torch.float32, **kw),
+                   torch.empty(n_h, dtype=torch.float32, **kw),
+                   torch.empty((n_h, k), dtype=torch.float32, **kw))
+        io = StepIO()
+        io.E, io.n_e_rows = E.data_ptr(), E.shape[0]
+        io.W_local, io.n_w_rows = W_local.data_ptr(), W_local.shape[0]
+        io.static_ids, io.n_static = static_ids.data_ptr(), static_ids.numel()
+        io.csr_row_ptr = None if csr_row_ptr is None else csr_row_ptr.data_ptr()
+        io.csr_col = None if csr_col is None else csr_col.data_ptr()
+        io.build = BuildParams(n_sem, n_graph_sem_seeds, per_seed, ctx_min_count, n_ctx_max, n_dyn)
+        io.n_h, io.k, io.inv_temp = n_h, k, float(inv_temp)
+        io.q, io.H = q.data_ptr(), H.data_ptr()
+        io.seeds = None if seeds is None else seeds.data_ptr()
+        io.n_seed = 0 if seeds is None else seeds.numel()
+        io.ctx_ids = None if ctx_ids is None else ctx_ids.data_ptr()
+        io.n_ctx = 0 if ctx_ids is None else ctx_ids.numel()
+        io.out_ids, io.out_vals, io.out_lse, io.out_probs = (t.data_ptr() for t in out)
+        io.host_io = int(host_io)
+        _check(lib().evospec_draft_step(self._h, C.byref(io), _stream(stream)))
+        return out

@@ -1,0 +1,571 @@
+// api.cu -- the C ABI of libevospec.so (include/evospec.h).
+//
+// Host side only: argument validation, workspace ownership, dispatch, and the
+// library-owned NCCL communicator (loaded with dlopen so that the library
+// links no NCCL and shares the process's already-loaded libnccl.so.2 when
+// torch has one). Every step of the path runs in the kernels of this library.
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include <nccl.h>
+
+// the C ABI is the only default-visibility surface of the library
+#pragma GCC visibility push(default)
+#include "../../include/evospec.h"
+#pragma GCC visibility pop
+#include "kernels.cuh"
+
+using namespace es;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+evospec_status fail(evospec_status st, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_last_error = buf;
+    return st;
+}
+
+#define CUDA_TRY(expr)                                                                        \
+    do {                                                                                      \
+        cudaError_t e_ = (expr);                                                              \
+        if (e_ != cudaSuccess)                                                                \
+            return fail(EVOSPEC_ECUDA, "%s: %s (%s:%d)", #expr, cudaGetErrorString(e_), __FILE__, \
+                        __LINE__);                                                            \
+    } while (0)
+
+#define LAUNCH_CHECK(what)                                                                   \
+    do {                                                                                     \
+        cudaError_t e_ = cudaGetLastError();                                                 \
+        if (e_ != cudaSuccess) return fail(EVOSPEC_ECUDA, "%s: %s", what, cudaGetErrorString(e_)); \
+    } while (0)
+
+// ---- NCCL through dlopen ---------------------------------------------------
+struct NcclApi {
+    bool loaded = false;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi& nccl() {
+    static NcclApi api;
+    if (api.loaded) return api;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD | RTLD_GLOBAL);
+    const char* env = getenv("EVOSPEC_NCCL_LIB");
+    if (!h && env) h = dlopen(env, RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return api;
+    api.GetUniqueId = (decltype(api.GetUniqueId))dlsym(h, "ncclGetUniqueId");
+    api.CommInitRank = (decltype(api.CommInitRank))dlsym(h, "ncclCommInitRank");
+    api.CommDestroy = (decltype(api.CommDestroy))dlsym(h, "ncclCommDestroy");
+    api.AllGather = (decltype(api.AllGather))dlsym(h, "ncclAllGather");
+    api.GroupStart = (decltype(api.GroupStart))dlsym(h, "ncclGroupStart");
+    api.GroupEnd = (decltype(api.GroupEnd))dlsym(h, "ncclGroupEnd");
+    api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
+    api.loaded = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.AllGather && api.GroupStart &&
+                 api.GroupEnd && api.GetErrorString;
+    return api;
+}
+
+template <typename T>
+cudaError_t dalloc(T** p, size_t n) {
+    return cudaMalloc((void**)p, std::max<size_t>(n, 1) * sizeof(T));
+}
+
+inline int64_t shard_rows(int64_t V, int R, int r) { return (V - r + R - 1) / R; }
+
+}  // namespace
+
+struct evospec_ctx {
+    evospec_config cfg;
+    int device;
+    // semantic scan + selection
+    double* s64 = nullptr;
+    uint32_t* key32 = nullptr;
+    uint32_t* hist = nullptr;
+    int* sel_count = nullptr;
+    double* sel_s = nullptr;
+    int32_t* sel_id = nullptr;
+    double* gat_s = nullptr;     // [R][max_sem] gathered candidates (sharded scan)
+    int32_t* gat_id = nullptr;
+    int* gat_count = nullptr;
+    double* sel2_s = nullptr;
+    int32_t* sel2_id = nullptr;
+    int32_t* sem_sorted = nullptr;
+    int32_t* ctx_sel = nullptr;
+    int* ctx_n = nullptr;
+    // LM head partials
+    LmhPartials part{};
+    int part_cta_cap = 0;
+    int* flags = nullptr;
+    float* wmax = nullptr;
+    // merge gather
+    int32_t* g_ids = nullptr;
+    float* g_vals = nullptr;
+    float* g_m = nullptr;
+    float* g_s = nullptr;
+    // draft-step staging
+    void* st_q = nullptr;
+    void* st_H = nullptr;
+    int32_t* st_seeds = nullptr;
+    int32_t* st_ctx = nullptr;
+    int32_t* st_S = nullptr;
+    int32_t* st_nS = nullptr;
+    int32_t* st_local = nullptr;
+    int32_t* st_nlocal = nullptr;
+    int32_t* st_tids = nullptr;
+    float* st_tvals = nullptr;
+    float* st_m = nullptr;
+    float* st_s = nullptr;
+    int32_t* st_oids = nullptr;
+    float* st_ovals = nullptr;
+    float* st_lse = nullptr;
+    float* st_probs = nullptr;
+    int last_n_sem = 0;
+    ncclComm_t comm = nullptr;
+    // measurement hooks
+    int64_t launches = 0;
+    bool timing = false;
+    std::vector<cudaEvent_t> ev;   // [stage][slot][2]
+    int ev_count[EVOSPEC_NUM_STAGES] = {0};
+};
+
+namespace {
+constexpr int kTimingSlots = 4096;
+
+// Records a start/end CUDA event pair around a stage when timing is on.
+struct StageTimer {
+    evospec_ctx* ctx;
+    int stage;
+    cudaStream_t st;
+    int slot = -1;
+    StageTimer(evospec_ctx* c, int s, cudaStream_t stream) : ctx(c), stage(s), st(stream) {
+        if (!ctx->timing || ctx->ev_count[stage] >= kTimingSlots) return;
+        slot = ctx->ev_count[stage]++;
+        cudaEventRecord(ctx->ev[((size_t)stage * kTimingSlots + slot) * 2], st);
+    }
+    void stop() {
+        if (slot >= 0) cudaEventRecord(ctx->ev[((size_t)stage * kTimingSlots + slot) * 2 + 1], st);
+        slot = -1;
+    }
+    ~StageTimer() { stop(); }
+};
+}  // namespace
+
+extern "C" {
+
+const char* evospec_version(void) { return "evospec-b200 0.1.0 (sm_100a)"; }
+
+const char* evospec_last_error(void) { return g_last_error.c_str(); }
+
+const char* evospec_status_string(evospec_status st) {
+    switch (st) {
+        case EVOSPEC_OK: return "ok";
+        case EVOSPEC_EINPUT: return "input error";
+        case EVOSPEC_EINVARIANT: return "invariant violation";
+        case EVOSPEC_ECUDA: return "CUDA error";
+        case EVOSPEC_ENCCL: return "NCCL error";
+        case EVOSPEC_ENOMEM: return "out of device memory";
+        default: return "unknown status";
+    }
+}
+
+evospec_status evospec_destroy(evospec_ctx* ctx) {
+    if (!ctx) return EVOSPEC_OK;
+    cudaSetDevice(ctx->device);
+    void* ptrs[] = {ctx->s64, ctx->key32, ctx->hist, ctx->sel_count, ctx->sel_s, ctx->sel_id, ctx->gat_s,
+                    ctx->gat_id, ctx->gat_count, ctx->sel2_s, ctx->sel2_id, ctx->sem_sorted, ctx->ctx_sel,
+                    ctx->ctx_n, ctx->part.val, ctx->part.id, ctx->part.m, ctx->part.s, ctx->part.cnt,
+                    ctx->flags, ctx->wmax, ctx->g_ids, ctx->g_vals, ctx->g_m, ctx->g_s, ctx->st_q, ctx->st_H,
+                    ctx->st_seeds, ctx->st_ctx, ctx->st_S, ctx->st_nS, ctx->st_local, ctx->st_nlocal,
+                    ctx->st_tids, ctx->st_tvals, ctx->st_m, ctx->st_s, ctx->st_oids, ctx->st_ovals,
+                    ctx->st_lse, ctx->st_probs};
+    for (void* p : ptrs)
+        if (p) cudaFree(p);
+    if (ctx->comm && nccl().loaded) nccl().CommDestroy(ctx->comm);
+    for (cudaEvent_t e : ctx->ev) cudaEventDestroy(e);
+    delete ctx;
+    return EVOSPEC_OK;
+}
+
+evospec_status evospec_create(evospec_ctx** out, const evospec_config* cfg, int device) {
+    if (!out || !cfg) return fail(EVOSPEC_EINPUT, "create: null argument");
+    *out = nullptr;
+    const evospec_config& c = *cfg;
+    if (c.V < 1 || c.d < 8 || c.d % 8 != 0)
+        return fail(EVOSPEC_EINPUT, "create: need V >= 1 and d a positive multiple of 8 (V=%d d=%d)", c.V, c.d);
+    if ((c.w_dtype != EVOSPEC_BF16 && c.w_dtype != EVOSPEC_FP32) ||
+        (c.h_dtype != EVOSPEC_BF16 && c.h_dtype != EVOSPEC_FP32))
+        return fail(EVOSPEC_EINPUT, "create: dtype must be EVOSPEC_BF16 or EVOSPEC_FP32");
+    if (c.n_shards < 1 || c.shard_rank < 0 || c.shard_rank >= c.n_shards)
+        return fail(EVOSPEC_EINPUT, "create: bad shard %d of %d", c.shard_rank, c.n_shards);
+    if (c.max_subset < 0 || c.max_subset > c.V || c.max_rows < 1 || c.max_k < 1 || c.max_k > kMaxK ||
+        c.max_sem < 0 || c.max_sem > c.V || c.max_seeds < 0 || c.max_ctx < 0 || c.max_ctx > kMaxCtx)
+        return fail(EVOSPEC_EINPUT, "create: capacity out of range (max_k <= %d, max_ctx <= %d)", kMaxK, kMaxCtx);
+    if (c.V > (1 << 20)) return fail(EVOSPEC_EINPUT, "create: V > 2^20 unsupported (bitmap in smem)");
+    CUDA_TRY(cudaSetDevice(device));
+    evospec_ctx* x = new evospec_ctx();
+    x->cfg = c;
+    x->device = device;
+    const int R = c.n_shards;
+    const size_t V = (size_t)c.V, d = (size_t)c.d;
+    const size_t sem = std::max(1, c.max_sem);
+    const int cta_cap = std::max(lmh_gemv_grid(), 2 * kNumSMs);
+    x->part_cta_cap = cta_cap;
+    const size_t pr = (size_t)cta_cap * c.max_rows;
+    const size_t hb = c.h_dtype == EVOSPEC_BF16 ? 2 : 4;
+    cudaError_t e = cudaSuccess;
+    auto A = [&](cudaError_t r) { if (e == cudaSuccess) e = r; };
+    A(dalloc(&x->s64, V)); A(dalloc(&x->key32, V)); A(dalloc(&x->hist, 12 * 2048));
+    A(dalloc(&x->sel_count, 4)); A(dalloc(&x->sel_s, sem)); A(dalloc(&x->sel_id, sem));
+    A(dalloc(&x->gat_s, sem * R)); A(dalloc(&x->gat_id, sem * R)); A(dalloc(&x->gat_count, 4));
+    A(dalloc(&x->sel2_s, sem)); A(dalloc(&x->sel2_id, sem));
+    A(dalloc(&x->sem_sorted, sem)); A(dalloc(&x->ctx_sel, std::max(1, c.max_ctx))); A(dalloc(&x->ctx_n, 1));
+    A(dalloc(&x->part.val, pr * kMaxKP)); A(dalloc(&x->part.id, pr * kMaxKP));
+    A(dalloc(&x->part.m, pr)); A(dalloc(&x->part.s, pr)); A(dalloc(&x->part.cnt, pr));
+    A(dalloc(&x->flags, 1)); A(dalloc(&x->wmax, 1));
+    const size_t trip = (size_t)R * c.max_rows * c.max_k;
+    A(dalloc(&x->g_ids, trip)); A(dalloc(&x->g_vals, trip));
+    A(dalloc(&x->g_m, (size_t)R * c.max_rows)); A(dalloc(&x->g_s, (size_t)R * c.max_rows));
+    A(cudaMalloc(&x->st_q, d * hb)); A(cudaMalloc(&x->st_H, (size_t)c.max_rows * d * hb));
+    A(dalloc(&x->st_seeds, std::max(1, c.max_seeds))); A(dalloc(&x->st_ctx, std::max(1, c.max_ctx)));
+    A(dalloc(&x->st_S, std::max(1, c.max_subset))); A(dalloc(&x->st_nS, 1));
+    A(dalloc(&x->st_local, std::max(1, c.max_subset))); A(dalloc(&x->st_nlocal, 1));
+    const size_t hk = (size_t)c.max_rows * c.max_k;
+    A(dalloc(&x->st_tids, hk)); A(dalloc(&x->st_tvals, hk)); A(dalloc(&x->st_m, c.max_rows));
+    A(dalloc(&x->st_s, c.max_rows)); A(dalloc(&x->st_oids, hk)); A(dalloc(&x->st_ovals, hk));
+    A(dalloc(&x->st_lse, c.max_rows)); A(dalloc(&x->st_probs, hk));
+    if (e == cudaSuccess) e = cudaMemset(x->flags, 0, sizeof(int));
+    if (e == cudaSuccess) {
+        const float inf = INFINITY;  // until evospec_prepare_weights: certification never passes
+        e = cudaMemcpy(x->wmax, &inf, sizeof(float), cudaMemcpyHostToDevice);
+    }
+    if (e != cudaSuccess) {
+        evospec_destroy(x);
+        return fail(e == cudaErrorMemoryAllocation ? EVOSPEC_ENOMEM : EVOSPEC_ECUDA, "create: %s",
+                    cudaGetErrorString(e));
+    }
+    *out = x;
+    return EVOSPEC_OK;
+}
+
+evospec_status evospec_prepare_weights(evospec_ctx* ctx, const void* W, int64_t n_rows, void* stream) {
+    if (!ctx || !W || n_rows < 0) return fail(EVOSPEC_EINPUT, "prepare_weights: bad argument");
+    launch_rownorm_max(W, ctx->cfg.w_dtype, n_rows, ctx->cfg.d, ctx->wmax, (cudaStream_t)stream);
+    ctx->launches += 1;
+    LAUNCH_CHECK("rownorm_max");
+    return EVOSPEC_OK;
+}
+
+evospec_status evospec_get_flags(evospec_ctx* ctx, int32_t* flags_out, int clear, void* stream) {
+    if (!ctx || !flags_out) return fail(EVOSPEC_EINPUT, "get_flags: null argument");
+    cudaStream_t st = (cudaStream_t)stream;
+    CUDA_TRY(cudaMemcpyAsync(flags_out, ctx->flags, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    if (clear) CUDA_TRY(cudaMemsetAsync(ctx->flags, 0, sizeof(int), st));
+    return EVOSPEC_OK;
+}
+
+evospec_status evospec_comm_unique_id(void* uid_out) {
+    if (!uid_out) return fail(EVOSPEC_EINPUT, "comm_unique_id: null");
+    NcclApi& n = nccl();
+    if (!n.loaded) return fail(EVOSPEC_ENCCL, "comm_unique_id: libnccl.so.2 not loadable");
+    ncclUniqueId id;
+    ncclResult_t r = n.GetUniqueId(&id);
+    if (r != ncclSuccess) return fail(EVOSPEC_ENCCL, "ncclGetUniqueId: %s", n.GetErrorString(r));
+    memcpy(uid_out, &id, sizeof(id));
+    return EVOSPEC_OK;
+}
+
+evospec_status evospec_comm_init(evospec_ctx* ctx, const void* uid) {
+    if (!ctx || !uid) return fail(EVOSPEC_EINPUT, "comm_init: null");
+    NcclApi& n = nccl();
+    if (!n.loaded) return fail(EVOSPEC_ENCCL, "comm_init: libnccl.so.2 not loadable");
+    CUDA_TRY(cudaSetDevice(ctx->device));
+    ncclUniqueId id;
+    memcpy(&id, uid, sizeof(id));
+    ncclResult_t r = n.CommInitRank(&ctx->comm, ctx->cfg.n_shards, id, ctx->cfg.shard_rank);
+    if (r != ncclSuccess) return fail(EVOSPEC_ENCCL, "ncclCommInitRank: %s", n.GetErrorString(r));
+    return EVOSPEC_OK;
+}
+
+evospec_status evospec_build_subset(evospec_ctx* ctx, const void* E, int64_t n_e_rows, const void* q,
+                                    const int32_t* static_ids, int32_t n_static, const int32_t* seeds,
+                                    int32_t n_seed, const int32_t* row_ptr, const int32_t* col,
+                                    const int32_t* ctx_ids, int32_t n_ctx, const evospec_build_params* p,
+                                    int32_t* out_ids, int32_t* out_n, int32_t* out_local_ids,
+                                    int32_t* out_local_n, void* stream) {
+    if (!ctx || !E || !q || !p || !out_ids || !out_n) return fail(EVOSPEC_EINPUT, "build_subset: null argument");
+    const evospec_config& c = ctx->cfg;
+    const int R = c.n_shards, r = c.shard_rank;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (n_static < 0 || (n_static > 0 && !static_ids) || n_seed < 0 || (n_seed > 0 && !seeds))
+        return fail(EVOSPEC_EINPUT, "build_subset: bad static / seed arguments");
+    if (p->n_sem < 0 || p->n_sem > c.max_sem || p->n_dyn < 0 || p->per_seed < 0 || p->per_seed > 64 ||
+        p->n_graph_sem_seeds < 0 || n_seed + std::min(p->n_graph_sem_seeds, p->n_sem) > std::min(c.max_seeds, 128))
+        return fail(EVOSPEC_EINPUT, "build_subset: params out of capacity (n_sem <= %d, seeds <= %d, per_seed <= 64)",
+                    c.max_sem, std::min(c.max_seeds, 128));
+    if ((int64_t)n_static + p->n_dyn > c.max_subset)
+        return fail(EVOSPEC_EINPUT, "build_subset: n_static + n_dyn = %lld > max_subset %d",
+                    (long long)n_static + p->n_dyn, c.max_subset);
+    if (p->ctx_min_count > 0 && (n_ctx < 0 || n_ctx > c.max_ctx || (n_ctx > 0 && !ctx_ids)))
+        return fail(EVOSPEC_EINPUT, "build_subset: ctx tokens exceed max_ctx %d", c.max_ctx);
+    if ((row_ptr == nullptr) != (col == nullptr)) return fail(EVOSPEC_EINPUT, "build_subset: CSR half given");
+    if (R > 1 && (!out_local_ids || !out_local_n))
+        return fail(EVOSPEC_EINPUT, "build_subset: sharded context needs out_local_ids / out_local_n");
+    const bool full_scan = n_e_rows == c.V;
+    const int64_t local_rows = shard_rows(c.V, R, r);
+    if (!full_scan && !(R > 1 && n_e_rows == local_rows))
+        return fail(EVOSPEC_EINPUT, "build_subset: n_e_rows must be V=%d or this shard's %lld rows", c.V,
+                    (long long)local_rows);
+    if (!full_scan && !ctx->comm)
+        return fail(EVOSPEC_EINPUT, "build_subset: a sharded index needs evospec_comm_init");
+
+    const int N = p->n_sem;
+    // a2: exact scores + top-N selection
+    {
+        StageTimer t(ctx, EVOSPEC_STAGE_SCAN, st);
+        launch_sem_scan(E, c.w_dtype, n_e_rows, c.d, q, c.h_dtype, ctx->s64, ctx->key32, st);
+        ctx->launches += 1;
+    }
+    LAUNCH_CHECK("sem_scan");
+    StageTimer t_sel(ctx, EVOSPEC_STAGE_SELECT, st);
+    if (full_scan) {
+        ctx->launches += 2;
+        CUDA_TRY(launch_topn_select(ctx->s64, nullptr, n_e_rows, 1, 0, N, ctx->hist, ctx->sel_count, ctx->sel_s,
+                                    ctx->sel_id, st));
+        launch_rank_sort(ctx->sel_s, ctx->sel_id, ctx->sel_count, N, ctx->sem_sorted, st);
+        LAUNCH_CHECK("rank_sort");
+    } else {
+        // local top-N (ids = row*R + r), exchange N (s, id) pairs per rank, global top-N
+        ctx->launches += 3;
+        CUDA_TRY(launch_topn_select(ctx->s64, nullptr, n_e_rows, R, r, N, ctx->hist, ctx->sel_count, ctx->sel_s,
+                                    ctx->sel_id, st));
+        NcclApi& n = nccl();
+        n.GroupStart();
+        ncclResult_t r1 = n.AllGather(ctx->sel_s, ctx->gat_s, (size_t)N, ncclFloat64, ctx->comm, st);
+        ncclResult_t r2 = n.AllGather(ctx->sel_id, ctx->gat_id, (size_t)N, ncclInt32, ctx->comm, st);
+        ncclResult_t r3 = n.GroupEnd();
+        if (r1 != ncclSuccess || r2 != ncclSuccess || r3 != ncclSuccess)
+            return fail(EVOSPEC_ENCCL, "build_subset all-gather failed");
+        CUDA_TRY(launch_topn_select(ctx->gat_s, ctx->gat_id, (int64_t)N * R, 0, 0, N, ctx->hist, ctx->gat_count,
+                                    ctx->sel2_s, ctx->sel2_id, st));
+        launch_rank_sort(ctx->sel2_s, ctx->sel2_id, ctx->gat_count, N, ctx->sem_sorted, st);
+        LAUNCH_CHECK("rank_sort");
+    }
+    t_sel.stop();
+    ctx->last_n_sem = N;
+    const int* n_sem_dev = full_scan ? ctx->sel_count : ctx->gat_count;
+    // a3 context counts (optional)
+    const bool use_ctx = p->ctx_min_count > 0 && p->n_ctx_max > 0 && n_ctx > 0;
+    StageTimer t_union(ctx, EVOSPEC_STAGE_UNION, st);
+    ctx->launches += 1 + (use_ctx ? 1 : 0);
+    if (use_ctx) {
+        launch_ctx_select(ctx_ids, n_ctx, c.V, p->ctx_min_count, std::min(p->n_ctx_max, c.max_ctx), ctx->ctx_sel,
+                          ctx->ctx_n, ctx->flags, st);
+        LAUNCH_CHECK("ctx_select");
+    }
+    // a3/a4 formation, cap, union
+    launch_union(c.V, static_ids, n_static, seeds, n_seed, ctx->sem_sorted, n_sem_dev, N, row_ptr, col,
+                 use_ctx ? ctx->ctx_sel : nullptr, ctx->ctx_n, p->n_graph_sem_seeds, p->per_seed, p->n_dyn, R, r,
+                 out_ids, out_n, out_local_ids, out_local_n, c.debug_checks, ctx->flags, st);
+    LAUNCH_CHECK("union");
+    return EVOSPEC_OK;
+}
+
+evospec_status evospec_last_semantic(evospec_ctx* ctx, int32_t* out_dev, int32_t n, void* stream) {
+    if (!ctx || !out_dev || n < 0 || n > ctx->cfg.max_sem) return fail(EVOSPEC_EINPUT, "last_semantic: bad argument");
+    CUDA_TRY(cudaMemcpyAsync(out_dev, ctx->sem_sorted, (size_t)n * 4, cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+    return EVOSPEC_OK;
+}
+
+static float gemv_gamma(int d) {
+    // recursive-summation bound gamma_n = n u / (1 - n u), u = 2^-24, with the
+    // chain length n = d/32 per-lane products + 5 butterfly levels + 1 scale
+    const double u = 1.0 / 16777216.0;
+    const double n = d / 32.0 + 6.0;
+    return (float)(1.01 * n * u / (1.0 - n * u));
+}
+
+evospec_status evospec_subset_logits_topk(evospec_ctx* ctx, const void* W, int64_t n_w_rows, const void* H,
+                                          int32_t n_h, const int32_t* subset, const int32_t* n_subset_dev,
+                                          int32_t n_subset_max, int32_t k, float inv_temp, int32_t* topk_ids,
+                                          float* topk_vals, float* row_max, float* row_sumexp, float* logits_out,
+                                          void* stream) {
+    if (!ctx || !W || !H || !subset || !n_subset_dev || !topk_ids || !topk_vals || !row_max || !row_sumexp)
+        return fail(EVOSPEC_EINPUT, "subset_logits_topk: null argument");
+    const evospec_config& c = ctx->cfg;
+    if (n_h < 1 || n_h > c.max_rows) return fail(EVOSPEC_EINPUT, "subset_logits_topk: n_h=%d not in [1,%d]", n_h, c.max_rows);
+    if (k < 1 || k > c.max_k) return fail(EVOSPEC_EINPUT, "subset_logits_topk: k=%d not in [1,%d]", k, c.max_k);
+    if (!(inv_temp > 0.0f) || !std::isfinite(inv_temp))
+        return fail(EVOSPEC_EINPUT, "subset_logits_topk: inv_temp must be finite and > 0");
+    if (n_subset_max < 0 || n_subset_max > c.max_subset)
+        return fail(EVOSPEC_EINPUT, "subset_logits_topk: n_subset_max=%d > max_subset %d", n_subset_max, c.max_subset);
+    if (n_w_rows < shard_rows(c.V, c.n_shards, c.shard_rank))
+        return fail(EVOSPEC_EINPUT, "subset_logits_topk: W_local has %lld rows, shard needs %lld", (long long)n_w_rows,
+                    (long long)shard_rows(c.V, c.n_shards, c.shard_rank));
+    cudaStream_t st = (cudaStream_t)stream;
+    if (c.debug_checks) {
+        ctx->launches += 1;
+        launch_check_sorted(subset, n_subset_dev, n_subset_max, c.V, ctx->flags, st);
+        LAUNCH_CHECK("check_sorted");
+    }
+    LmhArgs a{};
+    a.W = W; a.n_w_rows = n_w_rows; a.d = c.d; a.w_dtype = c.w_dtype;
+    a.H = H; a.n_h = n_h; a.h_dtype = c.h_dtype;
+    a.subset = subset; a.n_subset_dev = n_subset_dev; a.n_subset_max = n_subset_max;
+    a.R = c.n_shards; a.KP = k + kTopkPad; a.inv_temp = inv_temp;
+    a.logits_out = logits_out;
+    a.part = ctx->part;
+    int n_cta = 0;
+    {
+        StageTimer t(ctx, EVOSPEC_STAGE_LMH, st);
+        for (int h0 = 0; h0 < n_h;) {
+            const int g = lmh_gemv_group_width(a, n_h - h0);
+            n_cta = launch_lmh_gemv(a, h0, g, st);
+            ctx->launches += 1;
+            LAUNCH_CHECK("lmh_gemv");
+            h0 += g;
+        }
+    }
+    {
+        StageTimer t(ctx, EVOSPEC_STAGE_FINALIZE, st);
+        launch_lmh_finalize(a, n_cta, k, ctx->wmax, topk_ids, topk_vals, row_max, row_sumexp, ctx->flags, st,
+                            gemv_gamma(c.d));
+        ctx->launches += 1;
+    }
+    LAUNCH_CHECK("lmh_finalize");
+    return EVOSPEC_OK;
+}
+
+evospec_status evospec_merge_shards(evospec_ctx* ctx, int32_t n_h, int32_t k, const int32_t* ids, const float* vals,
+                                    const float* m, const float* s, int32_t* out_ids, float* out_vals, float* out_lse,
+                                    float* out_probs, void* stream) {
+    if (!ctx || !ids || !vals || !m || !s || !out_ids || !out_vals || !out_lse)
+        return fail(EVOSPEC_EINPUT, "merge_shards: null argument");
+    const evospec_config& c = ctx->cfg;
+    if (n_h < 1 || n_h > c.max_rows || k < 1 || k > c.max_k)
+        return fail(EVOSPEC_EINPUT, "merge_shards: n_h=%d / k=%d out of capacity", n_h, k);
+    const int R = c.n_shards;
+    if (R * k > 64 * 32) return fail(EVOSPEC_EINPUT, "merge_shards: R*k > 2048");
+    cudaStream_t st = (cudaStream_t)stream;
+    StageTimer t_merge(ctx, EVOSPEC_STAGE_MERGE, st);
+    const int32_t* gi = ids;
+    const float *gv = vals, *gm = m, *gs = s;
+    if (ctx->comm && R > 1) {
+        NcclApi& n = nccl();
+        const size_t nk = (size_t)n_h * k;
+        n.GroupStart();
+        ncclResult_t r1 = n.AllGather(ids, ctx->g_ids, nk, ncclInt32, ctx->comm, st);
+        ncclResult_t r2 = n.AllGather(vals, ctx->g_vals, nk, ncclFloat32, ctx->comm, st);
+        ncclResult_t r3 = n.AllGather(m, ctx->g_m, (size_t)n_h, ncclFloat32, ctx->comm, st);
+        ncclResult_t r4 = n.AllGather(s, ctx->g_s, (size_t)n_h, ncclFloat32, ctx->comm, st);
+        ncclResult_t r5 = n.GroupEnd();
+        if (r1 || r2 || r3 || r4 || r5) return fail(EVOSPEC_ENCCL, "merge_shards: all-gather failed");
+        gi = ctx->g_ids; gv = ctx->g_vals; gm = ctx->g_m; gs = ctx->g_s;
+    }
+    launch_merge(R, n_h, k, gi, gv, gm, gs, out_ids, out_vals, out_lse, out_probs, st);
+    ctx->launches += 1;
+    LAUNCH_CHECK("merge");
+    return EVOSPEC_OK;
+}
+
+evospec_status evospec_draft_step(evospec_ctx* ctx, const evospec_step_io* io, void* stream) {
+    if (!ctx || !io) return fail(EVOSPEC_EINPUT, "draft_step: null argument");
+    const evospec_config& c = ctx->cfg;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (io->n_h < 1 || io->n_h > c.max_rows || io->n_seed < 0 || io->n_seed > c.max_seeds || io->n_ctx < 0 ||
+        io->n_ctx > c.max_ctx || !io->q || !io->H || !io->out_ids || !io->out_vals || !io->out_lse)
+        return fail(EVOSPEC_EINPUT, "draft_step: bad I/O arguments");
+    if (c.n_shards > 1 && !ctx->comm) return fail(EVOSPEC_EINPUT, "draft_step: sharded context needs evospec_comm_init");
+    const size_t hb = c.h_dtype == EVOSPEC_BF16 ? 2 : 4;
+    const void *q = io->q, *H = io->H;
+    const int32_t *seeds = io->seeds, *cx = io->ctx_ids;
+    if (io->host_io) {
+        StageTimer t(ctx, EVOSPEC_STAGE_COPY, st);
+        CUDA_TRY(cudaMemcpyAsync(ctx->st_q, io->q, (size_t)c.d * hb, cudaMemcpyHostToDevice, st));
+        CUDA_TRY(cudaMemcpyAsync(ctx->st_H, io->H, (size_t)io->n_h * c.d * hb, cudaMemcpyHostToDevice, st));
+        if (io->n_seed > 0)
+            CUDA_TRY(cudaMemcpyAsync(ctx->st_seeds, io->seeds, (size_t)io->n_seed * 4, cudaMemcpyHostToDevice, st));
+        if (io->n_ctx > 0 && io->ctx_ids)
+            CUDA_TRY(cudaMemcpyAsync(ctx->st_ctx, io->ctx_ids, (size_t)io->n_ctx * 4, cudaMemcpyHostToDevice, st));
+        q = ctx->st_q; H = ctx->st_H; seeds = ctx->st_seeds; cx = io->ctx_ids ? ctx->st_ctx : nullptr;
+    }
+    const int n_sub_max = io->n_static + io->build.n_dyn;
+    evospec_status s = evospec_build_subset(ctx, io->E, io->n_e_rows, q, io->static_ids, io->n_static, seeds,
+                                            io->n_seed, io->csr_row_ptr, io->csr_col, cx, io->n_ctx, &io->build,
+                                            ctx->st_S, ctx->st_nS, ctx->st_local, ctx->st_nlocal, st);
+    if (s != EVOSPEC_OK) return s;
+    const int32_t* sub = c.n_shards > 1 ? ctx->st_local : ctx->st_S;
+    const int32_t* nsub = c.n_shards > 1 ? ctx->st_nlocal : ctx->st_nS;
+    s = evospec_subset_logits_topk(ctx, io->W_local, io->n_w_rows, H, io->n_h, sub, nsub, n_sub_max, io->k,
+                                   io->inv_temp, ctx->st_tids, ctx->st_tvals, ctx->st_m, ctx->st_s, nullptr, st);
+    if (s != EVOSPEC_OK) return s;
+    int32_t* oi = io->host_io ? ctx->st_oids : io->out_ids;
+    float* ov = io->host_io ? ctx->st_ovals : io->out_vals;
+    float* ol = io->host_io ? ctx->st_lse : io->out_lse;
+    float* op = io->host_io ? (io->out_probs ? ctx->st_probs : nullptr) : io->out_probs;
+    s = evospec_merge_shards(ctx, io->n_h, io->k, ctx->st_tids, ctx->st_tvals, ctx->st_m, ctx->st_s, oi, ov, ol, op,
+                             st);
+    if (s != EVOSPEC_OK) return s;
+    if (io->host_io) {
+        StageTimer t(ctx, EVOSPEC_STAGE_COPY, st);
+        const size_t hk = (size_t)io->n_h * io->k;
+        CUDA_TRY(cudaMemcpyAsync(io->out_ids, oi, hk * 4, cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaMemcpyAsync(io->out_vals, ov, hk * 4, cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaMemcpyAsync(io->out_lse, ol, (size_t)io->n_h * 4, cudaMemcpyDeviceToHost, st));
+        if (io->out_probs) CUDA_TRY(cudaMemcpyAsync(io->out_probs, op, hk * 4, cudaMemcpyDeviceToHost, st));
+    }
+    return EVOSPEC_OK;
+}
+
+evospec_status evospec_set_timing(evospec_ctx* ctx, int enable) {
+    if (!ctx) return fail(EVOSPEC_EINPUT, "set_timing: null");
+    if (enable && ctx->ev.empty()) {
+        CUDA_TRY(cudaSetDevice(ctx->device));
+        ctx->ev.resize((size_t)EVOSPEC_NUM_STAGES * kTimingSlots * 2);
+        for (auto& e : ctx->ev) CUDA_TRY(cudaEventCreate(&e));
+    }
+    if (enable)
+        for (int i = 0; i < EVOSPEC_NUM_STAGES; ++i) ctx->ev_count[i] = 0;
+    ctx->timing = enable != 0;
+    return EVOSPEC_OK;
+}
+
+evospec_status evospec_read_stats(evospec_ctx* ctx, evospec_stats* out) {
+    if (!ctx || !out) return fail(EVOSPEC_EINPUT, "read_stats: null");
+    memset(out, 0, sizeof(*out));
+    out->launches = ctx->launches;
+    for (int s = 0; s < EVOSPEC_NUM_STAGES; ++s) {
+        out->calls[s] = ctx->ev_count[s];
+        double sum = 0.0;
+        for (int i = 0; i < ctx->ev_count[s]; ++i) {
+            cudaEvent_t a = ctx->ev[((size_t)s * kTimingSlots + i) * 2], b = ctx->ev[((size_t)s * kTimingSlots + i) * 2 + 1];
+            CUDA_TRY(cudaEventSynchronize(b));
+            float ms = 0.0f;
+            CUDA_TRY(cudaEventElapsedTime(&ms, a, b));
+            sum += ms;
+        }
+        out->stage_ms[s] = (float)sum;
+    }
+    return EVOSPEC_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,79 @@
+// kernels.cuh -- launch interface between api.cu and the kernel files.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+namespace es {
+
+constexpr int kScanWarps = 16;      // sem scan: warps per CTA (1 CTA / SM)
+constexpr int kSelThreads = 512;    // topn select (cooperative), 2048 bins = 4 / thread
+constexpr int kRankThreads = 512;
+constexpr int kRankTile = 4096;
+constexpr int kRankMaxPerWarp = 8;
+constexpr int kUnionThreads = 1024;
+constexpr int kTopkPad = 8;         // extra fp32 candidates kept per row for the exact re-score
+constexpr int kMaxK = 64;
+constexpr int kMaxKP = kMaxK + kTopkPad;
+constexpr int kMaxCtx = 8192;
+
+// device flag bits (mirror EVOSPEC_FLAG_* in include/evospec.h)
+constexpr int kFlagBadIds = 0x1;
+constexpr int kFlagUncertified = 0x2;
+constexpr int kFlagSelectOverflow = 0x4;
+constexpr int kFlagBudget = 0x8;
+
+// ---- semantic (sem.cu)
+void launch_sem_scan(const void* E, int e_dtype, int64_t n_rows, int d, const void* q, int q_dtype,
+                     double* s64, uint32_t* key32, cudaStream_t st);
+cudaError_t launch_topn_select(const double* s64, const int32_t* ids, int64_t n, int id_mul, int id_add,
+                               int N, uint32_t* hist_g, int* out_count, double* out_s, int32_t* out_id,
+                               cudaStream_t st);
+void launch_rank_sort(const double* s, const int32_t* id, const int* n_dev, int n_max, int32_t* out_ids,
+                      cudaStream_t st);
+
+// ---- union / formation (union.cu)
+void launch_ctx_select(const int32_t* ctx, int n_ctx, int V, int min_count, int n_max,
+                       int32_t* out, int* out_n, int* flags, cudaStream_t st);
+void launch_union(int V, const int32_t* static_ids, int n_static, const int32_t* seeds, int n_seed,
+                  const int32_t* sem_sorted, const int* n_sem_dev, int n_sem_max,
+                  const int32_t* row_ptr, const int32_t* col,
+                  const int32_t* ctx_sel, const int* n_ctx_sel_dev,
+                  int n_graph_sem_seeds, int per_seed, int n_dyn, int R, int r,
+                  int32_t* out_ids, int32_t* out_n, int32_t* out_local, int32_t* out_local_n,
+                  int debug, int* flags, cudaStream_t st);
+
+// ---- LM head (lmh_gemv.cu, lmh_tc.cu)
+struct LmhPartials {
+    float* val;    // [n_cta][n_h][KP]
+    int32_t* id;   // [n_cta][n_h][KP]
+    float* m;      // [n_cta][n_h]
+    float* s;      // [n_cta][n_h]
+    int* cnt;      // [n_cta][n_h] number of valid entries
+};
+struct LmhArgs {
+    const void* W; int64_t n_w_rows; int d; int w_dtype;
+    const void* H; int n_h; int h_dtype;
+    const int32_t* subset; const int* n_subset_dev; int n_subset_max;
+    int R; int KP; float inv_temp;
+    float* logits_out;  // optional [n_h][n_subset_max]
+    LmhPartials part;
+};
+// returns the number of CTAs whose partials were written
+int launch_lmh_gemv(const LmhArgs& a, int h_row0, int n_h_grp, cudaStream_t st);
+int lmh_gemv_grid();
+int lmh_gemv_group_width(const LmhArgs& a, int n_left);
+
+// ---- finalize / merge / prepare (finalize.cu)
+void launch_lmh_finalize(const LmhArgs& a, int n_cta, int k, const float* wmax_dev,
+                         int32_t* topk_ids, float* topk_vals, float* row_max, float* row_sumexp,
+                         int* flags, cudaStream_t st, float gamma);
+void launch_merge(int R, int n_h, int k, const int32_t* ids, const float* vals, const float* m,
+                  const float* s, int32_t* out_ids, float* out_vals, float* out_lse, float* out_probs,
+                  cudaStream_t st);
+void launch_rownorm_max(const void* W, int w_dtype, int64_t n_rows, int d, float* out, cudaStream_t st);
+void launch_check_sorted(const int32_t* ids, const int* n_dev, int n_host, int V, int* flags,
+                         cudaStream_t st);
+
+}  // namespace es

@@ -1,0 +1,323 @@
+// sem.cu -- a2: semantic retrieval S_sem as an EXACT GPU scan.
+//
+// The paper retrieves the top-N MIPS neighbours of the target hidden state
+// over the LM-head rows with HNSW (App. A.3). HNSW
+// approximates the exact answer; on a B200 the exact scan q . E^T over all
+// 128k rows is one HBM pass (~1 GB, ~160 us), so we compute the exact answer
+// (reading C2 in DESIGN.md) and select the top-N by (score desc, id asc).
+//
+// Kernels:
+//   sem_scan_kernel     s64[v] = sum_c q[c] E[v][c] in fp64 (bf16 x fp32 products
+//                       are exact in fp64), one warp per 16-row chunk, 16-byte
+//                       streaming loads, q held per lane from a lane-interleaved
+//                       fp64 copy in shared memory.
+//   topn_select_kernel  cooperative radix select of the N largest composite
+//                       keys (float_key(s), double_key(s), ~id): 3 passes on the
+//                       fp32 key settle almost every case; further passes run
+//                       only when the boundary holds fp32-equal scores.
+//   rank_sort_kernel    exact order (s64 desc, id asc) of the N selected by
+//                       counting, one warp per element, lanes split the scan.
+#include <cooperative_groups.h>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace es {
+
+// ---------------------------------------------------------------- scan
+// Block: kScanWarps warps; each warp owns a contiguous row range and walks it
+// in chunks of 16 rows. Per chunk and per 256-column slab (bf16; 128 for
+// fp32) each lane loads one 16-byte piece of each of the 16 rows.
+template <int DT>  // element type of E: 0 bf16, 1 fp32
+__global__ void __launch_bounds__(kScanWarps * 32, 1)
+sem_scan_kernel(const void* __restrict__ E, int64_t n_rows, int d,
+                const void* __restrict__ q, int q_dtype, int id_mul, int id_add,
+                double* __restrict__ s64, uint32_t* __restrict__ key32) {
+    constexpr int ELEMS = DT == 0 ? 8 : 4;           // elements per 16 bytes
+    constexpr int SLAB = 32 * ELEMS;                  // columns per slab
+    extern __shared__ double q_sm[];                  // [n_slabs][ELEMS][32]
+    const int n_slabs = (d + SLAB - 1) / SLAB;
+    // stage q as fp64 in the lane-interleaved layout (exact: q is bf16/fp32)
+    for (int i = threadIdx.x; i < n_slabs * SLAB; i += blockDim.x) {
+        int s = i / SLAB, within = i % SLAB, lane = within / ELEMS, j = within % ELEMS;
+        int c = s * SLAB + within;
+        double v = 0.0;
+        if (c < d) v = q_dtype == 0 ? (double)bf16_bits_to_f32(((const uint16_t*)q)[c])
+                                    : (double)((const float*)q)[c];
+        q_sm[(s * ELEMS + j) * 32 + lane] = v;
+    }
+    __syncthreads();
+
+    const int lane = lane_id();
+    const int64_t gw = (int64_t)blockIdx.x * kScanWarps + warp_id();
+    const int64_t nw = (int64_t)gridDim.x * kScanWarps;
+    const int64_t r0 = n_rows * gw / nw, r1 = n_rows * (gw + 1) / nw;
+    const size_t row_bytes = (size_t)d * (DT == 0 ? 2 : 4);
+
+    for (int64_t base = r0; base < r1; base += 16) {
+        double acc[16];
+#pragma unroll
+        for (int r = 0; r < 16; ++r) acc[r] = 0.0;
+        for (int s = 0; s < n_slabs; ++s) {
+            const int c0 = s * SLAB + lane * ELEMS;
+            const bool col_ok = c0 < d;
+            uint4 u[16];
+#pragma unroll
+            for (int r = 0; r < 16; ++r) {
+                int64_t row = base + r;
+                if (col_ok && row < r1)
+                    u[r] = ld_stream((const char*)E + row * row_bytes + (size_t)c0 * (DT == 0 ? 2 : 4));
+                else
+                    u[r] = make_uint4(0, 0, 0, 0);
+            }
+            double qv[ELEMS];
+#pragma unroll
+            for (int j = 0; j < ELEMS; ++j) qv[j] = q_sm[(s * ELEMS + j) * 32 + lane];
+#pragma unroll
+            for (int r = 0; r < 16; ++r) {
+                if constexpr (DT == 0) {
+                    float f[8];
+                    unpack_bf16x8(u[r], f);
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) acc[r] = fma((double)f[j], qv[j], acc[r]);
+                } else {
+                    float f[4] = {__uint_as_float(u[r].x), __uint_as_float(u[r].y),
+                                  __uint_as_float(u[r].z), __uint_as_float(u[r].w)};
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) acc[r] = fma((double)f[j], qv[j], acc[r]);
+                }
+            }
+        }
+        // reduce-scatter 16 rows over 32 lanes: lane l ends with row (l & 15)
+#pragma unroll
+        for (int h = 8; h >= 1; h >>= 1) {
+            const bool upper = (lane & h) != 0;
+#pragma unroll
+            for (int i = 0; i < h; ++i) {
+                double send = upper ? acc[i] : acc[i + h];
+                double keep = upper ? acc[i + h] : acc[i];
+                acc[i] = keep + __shfl_xor_sync(0xffffffffu, send, h);
+            }
+        }
+        double tot = acc[0] + __shfl_xor_sync(0xffffffffu, acc[0], 16);
+        int64_t row = base + (lane & 15);
+        if (lane < 16 && row < r1) {
+            s64[row] = tot;
+            key32[row] = float_key((float)tot);
+        }
+        (void)id_mul; (void)id_add;
+    }
+}
+
+void launch_sem_scan(const void* E, int e_dtype, int64_t n_rows, int d, const void* q, int q_dtype,
+                     double* s64, uint32_t* key32, cudaStream_t st) {
+    const int elems = e_dtype == 0 ? 8 : 4;
+    const int n_slabs = (d + 32 * elems - 1) / (32 * elems);
+    const size_t smem = (size_t)n_slabs * 32 * elems * sizeof(double);
+    if (e_dtype == 0) {
+        cudaFuncSetAttribute(sem_scan_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        sem_scan_kernel<0><<<kNumSMs, kScanWarps * 32, smem, st>>>(E, n_rows, d, q, q_dtype, 1, 0, s64, key32);
+    } else {
+        cudaFuncSetAttribute(sem_scan_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        sem_scan_kernel<1><<<kNumSMs, kScanWarps * 32, smem, st>>>(E, n_rows, d, q, q_dtype, 1, 0, s64, key32);
+    }
+}
+
+// ---------------------------------------------------------------- select
+struct SelWords { uint32_t w[4]; };
+
+ES_DEV SelWords sel_words(double s, int32_t id) {
+    SelWords k;
+    k.w[0] = float_key((float)s);
+    uint64_t dk = double_key(s);
+    k.w[1] = (uint32_t)(dk >> 32);
+    k.w[2] = (uint32_t)dk;
+    k.w[3] = 0xFFFFFFFFu - (uint32_t)id;   // lower id ranks higher
+    return k;
+}
+
+struct SelState {
+    uint32_t pmask[4], pval[4];
+    int remaining;
+    int done;
+};
+
+ES_DEV bool sel_matches(const SelWords& k, const SelState& st) {
+#pragma unroll
+    for (int w = 0; w < 4; ++w)
+        if ((k.w[w] & st.pmask[w]) != st.pval[w]) return false;
+    return true;
+}
+// composite-prefix >= selected prefix
+ES_DEV bool sel_selected(const SelWords& k, const SelState& st) {
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+        uint32_t a = k.w[w] & st.pmask[w];
+        if (a != st.pval[w]) return a > st.pval[w];
+    }
+    return true;
+}
+
+__global__ void __launch_bounds__(kSelThreads, 1)
+topn_select_kernel(const double* __restrict__ s64, const int32_t* __restrict__ ids, int64_t n,
+                   int id_mul, int id_add, int N, uint32_t* __restrict__ hist_g,
+                   int* __restrict__ out_count, double* __restrict__ out_s, int32_t* __restrict__ out_id) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ uint32_t hist[2048];
+    __shared__ uint32_t suffix_warp[kSelThreads / 32];
+    __shared__ SelState st;
+    __shared__ int found_bin, found_above;
+
+    const int64_t lo = n * blockIdx.x / gridDim.x, hi = n * (blockIdx.x + 1) / gridDim.x;
+    auto id_of = [&](int64_t i) -> int32_t { return ids ? ids[i] : (int32_t)(i * id_mul + id_add); };
+
+    if (threadIdx.x == 0) {
+        for (int w = 0; w < 4; ++w) { st.pmask[w] = 0; st.pval[w] = 0; }
+        st.remaining = N;
+        st.done = (N >= n) || (N <= 0);
+        if (N <= 0) st.remaining = 0;
+    }
+    __syncthreads();
+
+    for (int pass = 0; pass < 12 && !st.done; ++pass) {
+        const int word = pass / 3, part = pass % 3;
+        const int shift = part == 0 ? 21 : (part == 1 ? 10 : 0);
+        const int nbits = part == 2 ? 10 : 11;
+        const uint32_t dmask = (1u << nbits) - 1u;
+        for (int b = threadIdx.x; b < 2048; b += blockDim.x) hist[b] = 0;
+        __syncthreads();
+        SelState my = st;
+        for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+            SelWords k = sel_words(s64[i], id_of(i));
+            if (sel_matches(k, my)) atomicAdd(&hist[(k.w[word] >> shift) & dmask], 1u);
+        }
+        __syncthreads();
+        uint32_t* hp = hist_g + (size_t)pass * 2048;
+        for (int b = threadIdx.x; b < 2048; b += blockDim.x)
+            if (hist[b]) atomicAdd(&hp[b], hist[b]);
+        grid.sync();
+        // every CTA: find bin b* (descending) where the running count reaches `remaining`
+        // thread t owns bins [4t, 4t+4)
+        uint32_t c[4], tot = 0;
+        const int t = threadIdx.x;  // kSelThreads == 512 -> 2048 bins
+#pragma unroll
+        for (int j = 0; j < 4; ++j) { c[j] = __ldcg(&hp[4 * t + j]); tot += c[j]; }
+        // suffix sum over threads: count of bins strictly above thread t's range
+        // warp-level inclusive suffix scan
+        uint32_t inc = tot;
+        const int lane = lane_id(), wid = warp_id();
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t v = __shfl_down_sync(0xffffffffu, inc, o);
+            if (lane + o < 32) inc += v;
+        }
+        if (lane == 0) suffix_warp[wid] = inc;   // total of warp
+        __syncthreads();
+        uint32_t above_w = 0;
+        for (int w2 = wid + 1; w2 < kSelThreads / 32; ++w2) above_w += suffix_warp[w2];
+        uint32_t above = above_w + inc - tot;     // bins strictly above this thread's range
+        const uint32_t rem = (uint32_t)st.remaining;
+        uint32_t run = above;
+#pragma unroll
+        for (int j = 3; j >= 0; --j) {
+            if (run < rem && run + c[j] >= rem) { found_bin = 4 * t + j; found_above = (int)run; }
+            run += c[j];
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const int b = found_bin;
+            st.remaining -= found_above;
+            st.pmask[word] |= dmask << shift;
+            st.pval[word] |= ((uint32_t)b) << shift;
+            if ((uint32_t)st.remaining == __ldcg(&hp[b])) st.done = 1;
+        }
+        __syncthreads();
+    }
+    // compaction (order arbitrary; the rank sort fixes it)
+    SelState my = st;
+    const bool take_all = (N >= n);
+    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+        double s = s64[i];
+        int32_t id = id_of(i);
+        bool sel = take_all || (N > 0 && sel_selected(sel_words(s, id), my));
+        if (sel) {
+            int o = atomicAdd(out_count, 1);
+            if (o < N || take_all) { out_s[o] = s; out_id[o] = id; }
+        }
+    }
+}
+
+cudaError_t launch_topn_select(const double* s64, const int32_t* ids, int64_t n, int id_mul, int id_add,
+                               int N, uint32_t* hist_g, int* out_count, double* out_s, int32_t* out_id,
+                               cudaStream_t st) {
+    cudaMemsetAsync(hist_g, 0, 12 * 2048 * sizeof(uint32_t), st);
+    cudaMemsetAsync(out_count, 0, sizeof(int), st);
+    int grid = kNumSMs;
+    if (n < (int64_t)grid * 64) grid = (int)((n + 63) / 64);
+    if (grid < 1) grid = 1;
+    void* args[] = {(void*)&s64, (void*)&ids, (void*)&n, (void*)&id_mul, (void*)&id_add, (void*)&N,
+                    (void*)&hist_g, (void*)&out_count, (void*)&out_s, (void*)&out_id};
+    return cudaLaunchCooperativeKernel((void*)topn_select_kernel, grid, kSelThreads, args, 0, st);
+}
+
+// ---------------------------------------------------------------- rank sort
+// out_ids[rank(i)] = id_i with rank(i) = #{j : (s_j, id_j) before (s_i, id_i)}.
+__global__ void __launch_bounds__(kRankThreads)
+rank_sort_kernel(const double* __restrict__ s, const int32_t* __restrict__ id, const int* __restrict__ n_dev,
+                 int n_max, int32_t* __restrict__ out_ids) {
+    extern __shared__ unsigned char rs_sm[];
+    const int n = min(*n_dev, n_max);
+    constexpr int TILE = kRankTile;
+    double* ts = (double*)rs_sm;
+    int32_t* ti = (int32_t*)(ts + TILE);
+    const int lane = lane_id();
+    const int nwarps = blockDim.x / 32;
+    // each warp owns elements e = blockIdx.x*nwarps + w, stepping by grid*nwarps
+    const int first = blockIdx.x * nwarps + warp_id();
+    const int step = gridDim.x * nwarps;
+    const int per_warp = (n + step - 1) / step;  // <= 64 kept in registers below
+    int cnt[kRankMaxPerWarp];
+    double my_s[kRankMaxPerWarp];
+    int32_t my_id[kRankMaxPerWarp];
+#pragma unroll
+    for (int e = 0; e < kRankMaxPerWarp; ++e) {
+        cnt[e] = 0;
+        int idx = first + e * step;
+        if (e < per_warp && idx < n) { my_s[e] = s[idx]; my_id[e] = id[idx]; }
+        else { my_s[e] = -INFINITY; my_id[e] = 0x7fffffff; }
+    }
+    for (int t0 = 0; t0 < n; t0 += TILE) {
+        const int tn = min(TILE, n - t0);
+        __syncthreads();
+        for (int j = threadIdx.x; j < tn; j += blockDim.x) { ts[j] = s[t0 + j]; ti[j] = id[t0 + j]; }
+        __syncthreads();
+        for (int j = lane; j < tn; j += 32) {
+            const double sj = ts[j];
+            const int32_t ij = ti[j];
+#pragma unroll
+            for (int e = 0; e < kRankMaxPerWarp; ++e)
+                if (e < per_warp) cnt[e] += before(sj, ij, my_s[e], my_id[e]) ? 1 : 0;
+        }
+    }
+#pragma unroll
+    for (int e = 0; e < kRankMaxPerWarp; ++e) {
+        if (e >= per_warp) break;
+        int c = warp_sum_i(cnt[e]);
+        int idx = first + e * step;
+        if (lane == 0 && idx < n) out_ids[c] = my_id[e];
+    }
+}
+
+void launch_rank_sort(const double* s, const int32_t* id, const int* n_dev, int n_max, int32_t* out_ids,
+                      cudaStream_t st) {
+    const int nwarps = kRankThreads / 32;
+    int grid = (n_max + nwarps * kRankMaxPerWarp - 1) / (nwarps * kRankMaxPerWarp);
+    if (grid < kNumSMs) grid = std::max(1, std::min(kNumSMs, (n_max + nwarps - 1) / nwarps));
+    const size_t smem = (size_t)kRankTile * (sizeof(double) + sizeof(int32_t));
+    cudaFuncSetAttribute(rank_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    rank_sort_kernel<<<grid, kRankThreads, smem, st>>>(s, id, n_dev, n_max, out_ids);
+}
+
+}  // namespace es

@@ -32,9 +32,12 @@ __all__ = [
 def bf16_bits(x: np.ndarray) -> np.ndarray:
     """fp32 -> bf16 bit patterns (uint16), round-to-nearest-even."""
     x = np.ascontiguousarray(x, dtype=np.float32)
-    u = x.view(np.uint32).astype(np.uint64)
-    rounding = ((u >> 16) & 1) + 0x7FFF
-    return ((u + rounding) >> 16).astype(np.uint16)
+    u = x.view(np.uint32)
+    r = (u >> 16) & 1          # finite inputs: u + 0x7FFF + 1 never wraps uint32
+    r += 0x7FFF
+    r += u
+    r >>= 16
+    return r.astype(np.uint16)
 
 
 def bf16_to_f32(b: np.ndarray) -> np.ndarray:
@@ -49,15 +52,33 @@ def _normal(rng: np.random.Generator, shape, std: float) -> np.ndarray:
     return out
 
 
+_CHUNK_ROWS = 4096
+
+
 def matrix(seed: int, rows: int, cols: int, std: float, dtype: str) -> np.ndarray:
-    """Gaussian matrix; dtype 'bf16' returns uint16 bit patterns, 'fp32' float32."""
-    rng = np.random.default_rng(seed)
-    x = _normal(rng, (rows, cols), std)
-    if dtype == "bf16":
-        return bf16_bits(x)
-    if dtype == "fp32":
-        return x
-    raise ValueError(dtype)
+    """Gaussian matrix; dtype 'bf16' returns uint16 bit patterns, 'fp32' float32.
+
+    Large matrices are drawn in fixed chunks of 4096 rows, chunk i from the
+    i-th child of SeedSequence(seed) (deterministic, thread-parallel)."""
+    if dtype not in ("bf16", "fp32"):
+        raise ValueError(dtype)
+    if rows <= _CHUNK_ROWS:
+        x = _normal(np.random.default_rng(seed), (rows, cols), std)
+        return bf16_bits(x) if dtype == "bf16" else x
+    from concurrent.futures import ThreadPoolExecutor
+    n_chunks = (rows + _CHUNK_ROWS - 1) // _CHUNK_ROWS
+    kids = np.random.SeedSequence(seed).spawn(n_chunks)
+    out = np.empty((rows, cols), dtype=np.uint16 if dtype == "bf16" else np.float32)
+
+    def work(i):
+        r0, r1 = i * _CHUNK_ROWS, min(rows, (i + 1) * _CHUNK_ROWS)
+        x = _normal(np.random.default_rng(kids[i]), (r1 - r0, cols), std)
+        out[r0:r1] = bf16_bits(x) if dtype == "bf16" else x
+
+    import os
+    with ThreadPoolExecutor(max_workers=min(32, os.cpu_count() or 1)) as ex:
+        list(ex.map(work, range(n_chunks)))
+    return out
 
 
 def int_matrix(seed: int, rows: int, cols: int, dtype: str, lo: int = -3, hi: int = 3) -> np.ndarray:

@@ -1,0 +1,208 @@
+"""GPU parity: the CUDA path through the C ABI vs the oracle, element by element.
+
+Bar (BASELINE.json north_star): subset ids and top-k ids bit-exact (ties to
+the lower id); logits / LSE |d| <= 2e-3 (1 + |z|); probabilities |d| <= 1e-4.
+Sizes span several CTA tiles and ragged tails; the full Llama-3 config
+(V=128256, d=4096, n_S=36,864, n_h=60) runs in the launch configuration
+bench.py times.
+"""
+import numpy as np
+import pytest
+
+import oracle
+from tests import gpu_helpers as G
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_2605_27390_b200 as es  # noqa: E402
+
+DEV = "cuda:0"
+
+
+def ctx_for(P, **kw):
+    cfg = dict(V=P["V"], d=P["d"], w_dtype=G.torch_dtype(P["dtype"]), h_dtype=G.torch_dtype(P["dtype"]),
+               max_subset=P["static"].size + P["n_dyn"], max_rows=max(P["n_h"], 1), max_k=64,
+               max_sem=max(P["n_sem"], 1), max_seeds=64, debug_checks=True)
+    cfg.update(kw)
+    return es.Context(**cfg)
+
+
+def run_path(P, ctx=None, inv_temp=1.0, logits=False):
+    ctx = ctx or ctx_for(P)
+    W = G.to_dev(P["W"], DEV)
+    ctx.prepare_weights(W)
+    ids, n, _, _ = ctx.build_subset(W, G.to_dev(P["q"], DEV), G.to_dev(P["static"], DEV),
+                                    G.to_dev(P["seeds"], DEV), G.to_dev(P["row_ptr"], DEV),
+                                    G.to_dev(P["col"], DEV), n_sem=P["n_sem"], n_dyn=P["n_dyn"],
+                                    n_graph_sem_seeds=P["n_graph_sem_seeds"], per_seed=P["per_seed"])
+    nmax = P["static"].size + P["n_dyn"]
+    lo = torch.full((P["n_h"], max(nmax, 1)), float("nan"), device=DEV) if logits else None
+    tri = ctx.subset_logits_topk(W, G.to_dev(P["H"], DEV), ids, n, nmax, P["k"], inv_temp, logits_out=lo)
+    mrg = ctx.merge_shards(*tri, n_h=P["n_h"], k=P["k"])
+    sem = ctx.last_semantic(P["n_sem"])
+    torch.cuda.synchronize()
+    nS = int(n.item())
+    out = dict(S=ids[:nS].cpu().numpy(), sem=sem.cpu().numpy(),
+               tri=[t.cpu().numpy() for t in tri], mrg=[t.cpu().numpy() for t in mrg],
+               flags=ctx.get_flags())
+    if logits:
+        out["logits"] = lo[:, :nS].cpu().numpy()
+    return out
+
+
+def check(P, got, ref, k):
+    np.testing.assert_array_equal(got["sem"], ref["sem"])
+    np.testing.assert_array_equal(got["S"], ref["S"])
+    G.assert_triple_close(*got["tri"], ref["triple"], k)
+    oi, ov, ol, op = got["mrg"]
+    np.testing.assert_array_equal(oi, ref["triple"]["ids"])
+    fin = np.isfinite(ref["triple"]["lse"])
+    assert np.all(np.abs(ol[fin] - ref["triple"]["lse"][fin]) <= G.LOGIT_TOL * (1 + np.abs(ref["triple"]["lse"][fin])))
+    assert np.max(np.abs(op - ref["triple"]["probs"]), initial=0) <= G.PROB_TOL
+    assert got["flags"] == 0, got["flags"]
+
+
+TINY = dict(V=1024, d=64, n_static=128, n_sem=32, n_dyn=64, n_h=4, k=8, w_std=1.0, h_std=0.125)
+
+
+@pytest.mark.parametrize("seed", range(4))
+@pytest.mark.parametrize("dtype", ["fp32", "bf16"])
+def test_tiny(seed, dtype):
+    P = G.make_problem(seed, dtype=dtype, **TINY)
+    got = run_path(P, logits=True)
+    ref = G.oracle_step(oracle, P)
+    check(P, got, ref, P["k"])
+    z = oracle.subset_logits(P["W"], P["H"], ref["S"])
+    assert np.all(np.abs(got["logits"] - z) <= G.LOGIT_TOL * (1 + np.abs(z)))
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_integer_family_exact_ties(seed):
+    """Integer data: every sum exact, many exact ties in scores and logits."""
+    P = G.make_problem(seed, dtype="bf16", integer=True, V=3000, d=72 * 8, n_static=300, n_sem=200,
+                       n_dyn=150, n_h=5, k=16)
+    got = run_path(P, logits=True)
+    ref = G.oracle_step(oracle, P)
+    check(P, got, ref, P["k"])
+    z = oracle.subset_logits(P["W"], P["H"], ref["S"])
+    np.testing.assert_array_equal(got["logits"], z)   # exact
+
+
+@pytest.mark.parametrize("n_h,k,inv_temp", [(1, 1, 1.0), (3, 10, 1.0), (4, 64, 1 / 0.7), (10, 10, 1.0)])
+def test_medium_ragged(n_h, k, inv_temp):
+    P = G.make_problem(11, dtype="bf16", V=20011, d=512, n_static=2999, n_sem=700, n_dyn=517,
+                       n_h=n_h, k=k, avg_deg=16)
+    got = run_path(P, inv_temp=inv_temp)
+    ref = G.oracle_step(oracle, P, inv_temp=inv_temp)
+    check(P, got, ref, k)
+
+
+def test_duplicate_rows_tie_to_lower_id():
+    P = G.make_problem(5, dtype="bf16", V=8192, d=256, n_static=1000, n_sem=400, n_dyn=300,
+                       n_h=4, k=12, dup_rows=2000)
+    got = run_path(P)
+    ref = G.oracle_step(oracle, P)
+    check(P, got, ref, P["k"])
+
+
+def test_cap_not_reached_graph_and_seeds_fill():
+    """Paper-default formation: N_sem = 10, graph top-8 per seed, cap binds inside S_graph."""
+    P = G.make_problem(2, dtype="bf16", V=50000, d=256, n_static=5000, n_sem=10, n_dyn=100,
+                       n_seed=10, per_seed=8, n_h=2, k=10, avg_deg=32)
+    got = run_path(P)
+    ref = G.oracle_step(oracle, P)
+    check(P, got, ref, P["k"])
+
+
+def test_empty_subset_and_k_gt_nS():
+    P = G.make_problem(3, dtype="fp32", V=512, d=64, n_static=0, n_sem=3, n_dyn=3, n_seed=0,
+                       n_graph_sem_seeds=0, n_h=2, k=8, w_std=1.0)
+    got = run_path(P)
+    ref = G.oracle_step(oracle, P)
+    assert got["S"].size == 3
+    check(P, got, ref, 8)
+    assert (got["tri"][0][:, 3:] == -1).all()
+    P0 = dict(P, n_sem=0, n_dyn=0)
+    got0 = run_path(P0)
+    assert got0["S"].size == 0
+    assert np.all(got0["tri"][2] == -np.inf) and np.all(got0["tri"][3] == 0)
+    assert np.all(got0["mrg"][0] == -1)
+
+
+def test_vocab_shards_on_one_gpu():
+    """T3: R interleaved W slices, one triple per shard, stacked merge == unsplit oracle."""
+    P = G.make_problem(7, dtype="bf16", V=30000, d=256, n_static=3000, n_sem=600, n_dyn=400, n_h=6, k=10)
+    ref = G.oracle_step(oracle, P)
+    S = ref["S"]
+    for R in (2, 3, 4):
+        trips = []
+        for r in range(R):
+            Sr = S[S % R == r].astype(np.int32)
+            Wr = np.ascontiguousarray(P["W"][r::R])
+            ctx = ctx_for(P, n_shards=R, shard_rank=r)
+            Wd = G.to_dev(Wr, DEV)
+            ctx.prepare_weights(Wd)
+            Sd = G.to_dev(Sr, DEV) if Sr.size else torch.zeros(1, dtype=torch.int32, device=DEV)
+            nd = torch.tensor([Sr.size], dtype=torch.int32, device=DEV)
+            trips.append(ctx.subset_logits_topk(Wd, G.to_dev(P["H"], DEV), Sd, nd, S.size, P["k"]))
+            assert ctx.get_flags() == 0
+        mctx = ctx_for(P, n_shards=R, shard_rank=0)
+        st = [torch.stack([t[i] for t in trips]) for i in range(4)]
+        oi, ov, ol, op = mctx.merge_shards(*st, n_h=P["n_h"], k=P["k"])
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(oi.cpu().numpy(), ref["triple"]["ids"])
+        assert np.max(np.abs(op.cpu().numpy() - ref["triple"]["probs"])) <= G.PROB_TOL
+        lse = ref["triple"]["lse"]
+        assert np.all(np.abs(ol.cpu().numpy() - lse) <= G.LOGIT_TOL * (1 + np.abs(lse)))
+
+
+def test_draft_step_host_io_equals_device_path():
+    P = G.make_problem(9, dtype="bf16", V=16000, d=256, n_static=2000, n_sem=300, n_dyn=250, n_h=3, k=10)
+    ctx = ctx_for(P)
+    W = G.to_dev(P["W"], DEV)
+    ctx.prepare_weights(W)
+    kw = dict(E=W, W_local=W, static_ids=G.to_dev(P["static"], DEV), csr_row_ptr=G.to_dev(P["row_ptr"], DEV),
+              csr_col=G.to_dev(P["col"], DEV), k=P["k"], n_sem=P["n_sem"], n_dyn=P["n_dyn"])
+    H = G.to_dev(P["H"], "cpu").pin_memory()
+    q = G.to_dev(P["q"], "cpu").pin_memory()
+    seeds = torch.from_numpy(P["seeds"]).pin_memory()
+    out_h = ctx.draft_step(q=q, H=H, seeds=seeds, **kw)
+    torch.cuda.synchronize()
+    out_d = ctx.draft_step(q=q.to(DEV), H=H.to(DEV), seeds=seeds.to(DEV), **kw)
+    torch.cuda.synchronize()
+    ref = G.oracle_step(oracle, P)
+    for a, b in zip(out_h, out_d):
+        np.testing.assert_array_equal(a.numpy(), b.cpu().numpy())
+    np.testing.assert_array_equal(out_h[0].numpy(), ref["triple"]["ids"])
+    assert np.max(np.abs(out_h[3].numpy() - ref["triple"]["probs"])) <= G.PROB_TOL
+
+
+def test_input_errors():
+    P = G.make_problem(0, dtype="fp32", **TINY)
+    ctx = ctx_for(P)
+    W = G.to_dev(P["W"], DEV)
+    H = G.to_dev(P["H"], DEV)
+    S = torch.arange(10, dtype=torch.int32, device=DEV)
+    n = torch.tensor([10], dtype=torch.int32, device=DEV)
+    for kw in [dict(k=0), dict(k=65), dict(inv_temp=0.0), dict(inv_temp=float("inf"))]:
+        args = dict(k=4, inv_temp=1.0)
+        args.update(kw)
+        with pytest.raises(es.EvospecError) as ei:
+            ctx.subset_logits_topk(W, H, S, n, 10, args["k"], args["inv_temp"])
+        assert ei.value.status == es.EINPUT
+
+
+@pytest.mark.slow
+def test_llama_full_size():
+    """Config L at full size: V=128256, d=4096, static 32768 + 4096 retrieved, n_h=60, k=10."""
+    import synth
+    c = dict(synth.CONFIGS["llama"])
+    P = G.make_problem(0, **c)
+    got = run_path(P)
+    ref = G.oracle_step(oracle, P)
+    assert got["S"].size == 36864
+    check(P, got, ref, c["k"])
