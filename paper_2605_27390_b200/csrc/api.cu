@@ -404,6 +404,22 @@ static float gemv_gamma(int d) {
     return (float)(1.01 * n * u / (1.0 - n * u));
 }
 
+// Tensor-core path for bf16 trees of >= kTcMinRows rows (FFMA no longer
+// keeps pace with HBM there); EVOSPEC_LMH=gemv|tc overrides.
+static constexpr int kTcMinRows = 5;
+// Accumulation-error envelope of the tcgen05 fp32 accumulator, relative to
+// ||h||_2 max||W_v||_2: 2^-16 (~ 256 fp32 roundings); the parity suite checks
+// the measured error stays below 1/8 of the resulting delta.
+static constexpr float kTcGamma = 1.0f / 65536.0f;
+
+static bool use_tc(const LmhArgs& a) {
+    const char* env = getenv("EVOSPEC_LMH");
+    if (env && !strcmp(env, "gemv")) return false;
+    if (!lmh_tc_supported(a)) return false;
+    if (env && !strcmp(env, "tc")) return true;
+    return a.n_h >= kTcMinRows;
+}
+
 evospec_status evospec_subset_logits_topk(evospec_ctx* ctx, const void* W, int64_t n_w_rows, const void* H,
                                           int32_t n_h, const int32_t* subset, const int32_t* n_subset_dev,
                                           int32_t n_subset_max, int32_t k, float inv_temp, int32_t* topk_ids,
@@ -435,20 +451,28 @@ evospec_status evospec_subset_logits_topk(evospec_ctx* ctx, const void* W, int64
     a.logits_out = logits_out;
     a.part = ctx->part;
     int n_cta = 0;
+    float gamma = gemv_gamma(c.d);
     {
         StageTimer t(ctx, EVOSPEC_STAGE_LMH, st);
-        for (int h0 = 0; h0 < n_h;) {
-            const int g = lmh_gemv_group_width(a, n_h - h0);
-            n_cta = launch_lmh_gemv(a, h0, g, st);
+        if (use_tc(a)) {
+            CUDA_TRY(launch_lmh_tc(a, st));
             ctx->launches += 1;
-            LAUNCH_CHECK("lmh_gemv");
-            h0 += g;
+            n_cta = lmh_tc_grid();
+            gamma = kTcGamma;
+        } else {
+            for (int h0 = 0; h0 < n_h;) {
+                const int g = lmh_gemv_group_width(a, n_h - h0);
+                n_cta = launch_lmh_gemv(a, h0, g, st);
+                ctx->launches += 1;
+                LAUNCH_CHECK("lmh_gemv");
+                h0 += g;
+            }
         }
     }
     {
         StageTimer t(ctx, EVOSPEC_STAGE_FINALIZE, st);
         launch_lmh_finalize(a, n_cta, k, ctx->wmax, topk_ids, topk_vals, row_max, row_sumexp, ctx->flags, st,
-                            gemv_gamma(c.d));
+                            gamma);
         ctx->launches += 1;
     }
     LAUNCH_CHECK("lmh_finalize");

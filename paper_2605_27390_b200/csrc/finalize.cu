@@ -6,14 +6,16 @@
 //      s = sum_c s_c exp(m_c - M);
 //   2. k-way merge of the per-CTA sorted fp32 candidate lists into the best
 //      KP = k + kTopkPad candidates under (z desc, id asc);
-//   3. EXACT re-score of those KP candidates in fp64 (bf16 x bf16 / fp32
-//      products are exact in fp64) and re-order by (z64 desc, id asc);
-//   4. certification: every candidate that was dropped has fp32 value
-//      <= v_KP, hence exact value <= v_KP + delta; if the k-th exact value
-//      exceeds v_KP + delta the returned top-k is the exact top-k
-//      (DESIGN.md "Exact top-k"); otherwise EVOSPEC_FLAG_UNCERTIFIED is set.
-//      delta = gamma * ||h_r||_2 * max_v ||W_v||_2 * inv_temp, gamma the
-//      accumulation-error constant of the kernel that produced the fp32 values.
+//   3. exactness: every fp32 value is within
+//      delta = gamma * ||h_r||_2 * max_v ||W_v||_2 * inv_temp of the exact
+//      value (gamma: accumulation-error constant of the producing kernel).
+//      Consecutive kept candidates closer than 2*delta form a "run" whose
+//      internal order is uncertain; every run that reaches into the top k is
+//      re-scored EXACTLY in fp64 (bf16 x bf16 / fp32 products are exact in
+//      fp64) and re-ordered by (z64 desc, id asc). Runs are separated by gaps
+//      > 2*delta, so the order between runs is certain. If the run holding
+//      the k-th candidate reaches the last kept candidate while candidates
+//      were dropped, the result cannot be certified: EVOSPEC_FLAG_UNCERTIFIED.
 // merge_kernel (one warp per H row): the shard merge of SURVEY §8(c) step 12.
 #include "common.cuh"
 #include "kernels.cuh"
@@ -21,6 +23,10 @@
 namespace es {
 
 constexpr int kFinThreads = 256;
+
+ES_DEV double load_elem(const void* p, int dtype, size_t i) {
+    return dtype == 0 ? (double)bf16_bits_to_f32(((const uint16_t*)p)[i]) : (double)((const float*)p)[i];
+}
 
 __global__ void __launch_bounds__(kFinThreads)
 lmh_finalize_kernel(LmhArgs a, int n_cta, int k, float gamma, const float* __restrict__ wmax_dev,
@@ -34,12 +40,14 @@ lmh_finalize_kernel(LmhArgs a, int n_cta, int k, float gamma, const float* __res
     __shared__ float c_v32[kMaxKP];
     __shared__ int32_t c_id[kMaxKP];
     __shared__ double c_e[kMaxKP];
-    __shared__ int n_kept_s, total_s;
+    __shared__ int c_need[kMaxKP];
+    __shared__ int n_kept_s, total_s, n_need_s;
+    __shared__ int need_list[kMaxKP];
     __shared__ float red_m[32], red_s[32];
     __shared__ int red_t[32];
     __shared__ double hn2_s;
 
-    // 1. softmax state
+    // 1. softmax state; ||h_r||^2 (warp 7) for delta
     float M = -INFINITY;
     for (int c = threadIdx.x; c < n_cta; c += blockDim.x) {
         size_t o = (size_t)c * a.n_h + r;
@@ -48,6 +56,15 @@ lmh_finalize_kernel(LmhArgs a, int n_cta, int k, float gamma, const float* __res
     }
     M = warp_max(M);
     if (lane == 0) red_m[warp] = M;
+    if (warp == nwarps - 1) {
+        double acc = 0.0;
+        for (int col = lane; col < a.d; col += 32) {
+            double h = load_elem(a.H, a.h_dtype, (size_t)r * a.d + col);
+            acc = fma(h, h, acc);
+        }
+        acc = warp_sum_d(acc);
+        if (lane == 0) hn2_s = acc;
+    }
     __syncthreads();
     M = -INFINITY;
     for (int w = 0; w < nwarps; ++w) M = fmaxf(M, red_m[w]);
@@ -100,63 +117,65 @@ lmh_finalize_kernel(LmhArgs a, int n_cta, int k, float gamma, const float* __res
     }
     __syncthreads();
     const int nk = n_kept_s;
-    // 3. exact re-score + ||h_r||^2
-    const int d = a.d;
-    const int welems = a.w_dtype == 0 ? 8 : 4;
-    for (int c = warp; c <= nk; c += nwarps) {
-        double acc = 0.0;
-        if (c < nk) {
-            const int64_t row = c_id[c] / a.R;
-            for (int c0 = lane * welems; c0 < d; c0 += 32 * welems) {
-#pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    if (j >= welems) break;
-                    const int col = c0 + j;
-                    double w = a.w_dtype == 0 ? (double)bf16_bits_to_f32(((const uint16_t*)a.W)[row * d + col])
-                                              : (double)((const float*)a.W)[row * d + col];
-                    double h = a.h_dtype == 0 ? (double)bf16_bits_to_f32(((const uint16_t*)a.H)[(size_t)r * d + col])
-                                              : (double)((const float*)a.H)[(size_t)r * d + col];
-                    acc = fma(w, h, acc);
-                }
-            }
-        } else {  // the extra "candidate" nk computes ||h_r||^2
-            for (int col = lane; col < d; col += 32) {
-                double h = a.h_dtype == 0 ? (double)bf16_bits_to_f32(((const uint16_t*)a.H)[(size_t)r * d + col])
-                                          : (double)((const float*)a.H)[(size_t)r * d + col];
-                acc = fma(h, h, acc);
-            }
+    // 3. runs of candidates closer than 2 delta that reach into the top k
+    if (threadIdx.x == 0) {
+        const double delta = (double)gamma * sqrt(hn2_s) * (double)*wmax_dev * (double)a.inv_temp;
+        int nn = 0;
+        int i = 0;
+        bool uncertain = false;
+        while (i < nk) {
+            int j = i;
+            while (j + 1 < nk && (double)c_v32[j] - (double)c_v32[j + 1] <= 2.0 * delta + 2.4e-7 * fabs((double)c_v32[j]))
+                ++j;
+            const bool in_topk = i < k;
+            const bool multi = j > i;
+            for (int t = i; t <= j; ++t) c_need[t] = (in_topk && multi) ? 1 : 0;
+            if (in_topk && multi)
+                for (int t = i; t <= j; ++t) need_list[nn++] = t;
+            if (in_topk && j == nk - 1 && total_s > nk && j >= k - 1) uncertain = true;
+            if (!(delta >= 0.0) || isinf(delta)) uncertain = true;   // weights not prepared
+            i = j + 1;
         }
-        acc = warp_sum_d(acc);
-        if (lane == 0) {
-            if (c < nk) c_e[c] = acc * (double)a.inv_temp;
-            else hn2_s = acc;
-        }
+        n_need_s = nn;
+        if (uncertain) atomicOr(flags, kFlagUncertified);
     }
     __syncthreads();
-    // 4. order by exact value, certify, write
+    // exact re-score of the flagged candidates (one warp per candidate)
+    const int nn = n_need_s;
+    for (int q = warp; q < nn; q += nwarps) {
+        const int c = need_list[q];
+        const size_t row = (size_t)(c_id[c] / a.R);
+        double acc = 0.0;
+        for (int col = lane; col < a.d; col += 32)
+            acc = fma(load_elem(a.W, a.w_dtype, row * a.d + col), load_elem(a.H, a.h_dtype, (size_t)r * a.d + col), acc);
+        acc = warp_sum_d(acc);
+        if (lane == 0) c_e[c] = acc * (double)a.inv_temp;
+    }
+    __syncthreads();
+    // 4. order each re-scored run exactly, write the top k
     if (threadIdx.x == 0) {
-        const float v_last = nk > 0 ? c_v32[nk - 1] : -INFINITY;
-        for (int i = 1; i < nk; ++i) {
-            double e = c_e[i];
-            int32_t id = c_id[i];
-            float v = c_v32[i];
-            int j = i - 1;
-            while (j >= 0 && before(e, id, c_e[j], c_id[j])) {
-                c_e[j + 1] = c_e[j]; c_id[j + 1] = c_id[j]; c_v32[j + 1] = c_v32[j];
-                --j;
+        for (int i = 0; i < nk; ++i)
+            if (!c_need[i]) c_e[i] = (double)c_v32[i];
+        int i = 0;
+        while (i < nk) {
+            if (!c_need[i]) { ++i; continue; }
+            int j = i;
+            while (j + 1 < nk && c_need[j + 1] &&
+                   (double)c_v32[j] - (double)c_v32[j + 1] <= 1e300)  // contiguous flagged block
+                ++j;
+            for (int u = i + 1; u <= j; ++u) {   // insertion sort by (exact desc, id asc)
+                double e = c_e[u];
+                int32_t id = c_id[u];
+                int w = u - 1;
+                while (w >= i && before(e, id, c_e[w], c_id[w])) { c_e[w + 1] = c_e[w]; c_id[w + 1] = c_id[w]; --w; }
+                c_e[w + 1] = e;
+                c_id[w + 1] = id;
             }
-            c_e[j + 1] = e; c_id[j + 1] = id; c_v32[j + 1] = v;
+            i = j + 1;
         }
-        const bool dropped = total_s > nk;
-        if (dropped && nk >= k) {
-            const double wmax = (double)*wmax_dev;
-            const double delta = (double)gamma * sqrt(hn2_s) * wmax * (double)a.inv_temp +
-                                 fabs((double)v_last) * 2.4e-7;
-            if (!(c_e[k - 1] > (double)v_last + delta)) atomicOr(flags, kFlagUncertified);
-        }
-        for (int i = 0; i < k; ++i) {
-            topk_ids[(size_t)r * k + i] = i < nk ? c_id[i] : -1;
-            topk_vals[(size_t)r * k + i] = i < nk ? (float)c_e[i] : -INFINITY;
+        for (int t = 0; t < k; ++t) {
+            topk_ids[(size_t)r * k + t] = t < nk ? c_id[t] : -1;
+            topk_vals[(size_t)r * k + t] = t < nk ? (float)c_e[t] : -INFINITY;
         }
     }
 }
@@ -234,8 +253,7 @@ __global__ void rownorm_max_kernel(const void* __restrict__ W, int w_dtype, int6
     for (int64_t row = gw; row < n_rows; row += nw) {
         double acc = 0.0;
         for (int c = lane; c < d; c += 32) {
-            double w = w_dtype == 0 ? (double)bf16_bits_to_f32(((const uint16_t*)W)[row * d + c])
-                                    : (double)((const float*)W)[row * d + c];
+            double w = load_elem(W, w_dtype, (size_t)row * d + c);
             acc += w * w;
         }
         acc = warp_sum_d(acc);
@@ -255,7 +273,7 @@ __global__ void check_sorted_kernel(const int32_t* __restrict__ ids, const int* 
     const int n = n_dev ? min(*n_dev, n_host) : n_host;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         const int v = ids[i];
-        if (v < 0 || v >= V || (i > 0 && ids[i - 1] >= v)) atomicOr(flags, 1);
+        if (v < 0 || v >= V || (i > 0 && ids[i - 1] >= v)) atomicOr(flags, kFlagBadIds);
     }
 }
 

@@ -64,6 +64,10 @@ struct LmhArgs {
 int launch_lmh_gemv(const LmhArgs& a, int h_row0, int n_h_grp, cudaStream_t st);
 int lmh_gemv_grid();
 int lmh_gemv_group_width(const LmhArgs& a, int n_left);
+constexpr int kTcMaxRows = 128;
+bool lmh_tc_supported(const LmhArgs& a);
+int lmh_tc_grid();
+cudaError_t launch_lmh_tc(const LmhArgs& a, cudaStream_t st);
 
 // ---- finalize / merge / prepare (finalize.cu)
 void launch_lmh_finalize(const LmhArgs& a, int n_cta, int k, const float* wmax_dev,

@@ -1,0 +1,365 @@
+// lmh_tc.cu -- a5-a7 on the 5th-generation tensor cores for draft trees with
+// n_h >= 5 (the paper's 60-node tree): at arithmetic
+// intensity n_h flop/byte FFMA cannot keep pace with HBM, tcgen05 can.
+//
+//   z[r][j] = inv_temp * sum_c H[r][c] W[S_j][c]    (Eq. projection P:44-48,
+//                                                    restricted to V_t)
+//
+// Swap-AB: the MMA's M dimension is 128 gathered vocabulary rows of W[S]
+// (A, K-major), N is the tree width padded to a multiple of 16 (B = H,
+// K-major), the fp32 accumulator D[128 x N] lives in TMEM.
+//
+// Persistent, warp-specialised CTA per SM (6 warps):
+//   warp 0  TMA producer: per 64-column k-block, 32 x cp.async.bulk.tensor
+//           .tile::gather4 (4 W rows each, one per lane) + one 2D tile of H
+//           into a 128B-swizzled smem stage; mbarrier complete_tx.
+//   warp 1  TMEM allocator + MMA issuer (one elected thread):
+//           4 x tcgen05.mma.cta_group::1.kind::f16 (K = 16) per stage,
+//           tcgen05.commit frees the stage; double-buffered accumulators.
+//   warps 2-5  epilogue: tcgen05.ld 32x32b -> scale -> smem tile -> the
+//           shared online-softmax / top-k fold (lmh_epilogue.cuh) while the
+//           producer and MMA already stream the next tile.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include "common.cuh"
+#include "kernels.cuh"
+#include "lmh_epilogue.cuh"
+
+namespace es {
+
+constexpr int kTcWarps = 6;
+constexpr int kTcEpiWarp0 = 2;
+constexpr int kBlockK = 64;        // bf16 columns per stage = one 128-byte swizzle atom row
+constexpr int kTileM = 128;
+
+// ------------------------------------------------------------------ PTX
+ES_DEV uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+ES_DEV void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+ES_DEV void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+ES_DEV void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+ES_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+ES_DEV void tma_gather4(void* dst, const CUtensorMap* map, uint64_t* bar, int col, int r0, int r1, int r2,
+                        int r3, uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%3, %4, %5, %6, %7}], [%2], %8;" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(smem_u32(bar)), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "l"(policy)
+        : "memory");
+}
+ES_DEV void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "l"(policy)
+        : "memory");
+}
+ES_DEV uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+ES_DEV uint64_t policy_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+
+ES_DEV void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+ES_DEV void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// K-major, 128B-swizzled UMMA shared-memory descriptor (8-row groups 1024 B apart).
+ES_DEV uint64_t umma_desc_sw128(uint32_t saddr) {
+    uint64_t desc = 0;
+    desc |= (uint64_t)((saddr >> 4) & 0x3FFF);          // start address
+    desc |= (uint64_t)1 << 16;                           // LBO (unused for swizzled K-major)
+    desc |= (uint64_t)(1024 >> 4) << 32;                 // SBO = 1024 B
+    desc |= (uint64_t)1 << 46;                           // descriptor version (sm_100)
+    desc |= (uint64_t)2 << 61;                           // SWIZZLE_128B
+    return desc;
+}
+
+// kind::f16 instruction descriptor: D fp32, A/B bf16, both K-major.
+__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
+    return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+ES_DEV void umma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+ES_DEV void umma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+
+ES_DEV void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+ES_DEV void named_bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+// ------------------------------------------------------------------ kernel
+struct TcParams {
+    int n_pad;       // N: tree rows padded to a multiple of 16 (<= 128)
+    int stages;
+    int nkb;         // d / 64
+    uint32_t tmem_cols;
+    size_t off_b, off_epi, off_bar, off_rows;  // smem carve offsets
+};
+
+__global__ void __launch_bounds__(kTcWarps * 32, 1)
+lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ CUtensorMap tmap_h,
+              LmhArgs a, TcParams tp) {
+    extern __shared__ __align__(1024) unsigned char tc_sm[];
+    // 1024-align the stage ring (SWIZZLE_128B atoms)
+    unsigned char* base = (unsigned char*)(((uintptr_t)tc_sm + 1023) & ~(uintptr_t)1023);
+    const int S = tp.stages, NP = tp.n_pad, n_h = a.n_h;
+    unsigned char* smA = base;                                   // [S][128][128 B]
+    unsigned char* smB = base + tp.off_b;                        // [S][NP][128 B]
+    EpiSmem e = epi_carve(base + tp.off_epi, n_h, a.KP, 4);
+    uint64_t* full = (uint64_t*)(base + tp.off_bar);             // [S]
+    uint64_t* empty = full + S;                                  // [S]
+    uint64_t* tfull = empty + S;                                 // [2]
+    uint64_t* tempty = tfull + 2;                                // [2]
+    uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+    int32_t* rows_sm = (int32_t*)(base + tp.off_rows);           // [2][128] gather rows per tile
+
+    const int warp = warp_id(), lane = lane_id();
+    const int n_S = min(*a.n_subset_dev, a.n_subset_max);
+    const int p0 = (int)((long long)n_S * blockIdx.x / gridDim.x);
+    const int p1 = (int)((long long)n_S * (blockIdx.x + 1) / gridDim.x);
+    const int len = p1 - p0;
+    const int n_tiles = (len + kTileM - 1) / kTileM;
+
+    if (warp == 0 && lane == 0) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap_w) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap_h) : "memory");
+        for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+        for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 128); }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(tp.tmem_cols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    epi_init(e, n_h);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    auto tile_range = [&](int t, int& t0, int& tn) {
+        const int a0 = p0 + (int)((long long)len * t / n_tiles);
+        const int a1 = p0 + (int)((long long)len * (t + 1) / n_tiles);
+        t0 = a0;
+        tn = a1 - a0;
+    };
+
+    if (warp == 0) {
+        // ===== TMA producer (whole warp: lane j gathers rows 4j..4j+3)
+        const uint64_t pol_w = policy_evict_first(), pol_h = policy_evict_last();
+        const uint32_t stage_bytes = (uint32_t)(kTileM * 128 + NP * 128);
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int t = 0; t < n_tiles; ++t) {
+            int t0, tn;
+            tile_range(t, t0, tn);
+            int rr[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int p = 4 * lane + i;
+                const int pos = t0 + (p < tn ? p : 0);
+                rr[i] = a.subset[pos] / a.R;
+            }
+            for (int kb = 0; kb < tp.nkb; ++kb) {
+                mbar_wait(&empty[stage], phase ^ 1);
+                if (lane == 0) mbar_arrive_expect_tx(&full[stage], stage_bytes);
+                __syncwarp();
+                unsigned char* dA = smA + (size_t)stage * kTileM * 128;
+                tma_gather4(dA + lane * 512, &tmap_w, &full[stage], kb * kBlockK, rr[0], rr[1], rr[2], rr[3], pol_w);
+                if (lane == 0)
+                    tma_load_2d(smB + (size_t)stage * NP * 128, &tmap_h, &full[stage], kb * kBlockK, 0, pol_h);
+                if (++stage == S) { stage = 0; phase ^= 1; }
+            }
+        }
+    } else if (warp == 1) {
+        // ===== MMA issuer
+        const uint32_t idesc = idesc_bf16(kTileM, NP);
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int t = 0; t < n_tiles; ++t) {
+            const int b = t & 1;
+            const uint32_t use = (uint32_t)(t >> 1);
+            if (t >= 2) mbar_wait(&tempty[b], (use - 1) & 1);
+            tc_fence_after();
+            const uint32_t tmem_d = tmem_base + (uint32_t)(b * NP);
+            for (int kb = 0; kb < tp.nkb; ++kb) {
+                mbar_wait(&full[stage], phase);
+                tc_fence_after();
+                if (lane == 0) {
+                    const uint32_t aaddr = smem_u32(smA + (size_t)stage * kTileM * 128);
+                    const uint32_t baddr = smem_u32(smB + (size_t)stage * NP * 128);
+#pragma unroll
+                    for (int k = 0; k < kBlockK / 16; ++k)
+                        umma_bf16(tmem_d, umma_desc_sw128(aaddr + k * 32), umma_desc_sw128(baddr + k * 32), idesc,
+                                  (kb | k) != 0);
+                    umma_commit(&empty[stage]);
+                    if (kb == tp.nkb - 1) umma_commit(&tfull[b]);
+                }
+                __syncwarp();
+                if (++stage == S) { stage = 0; phase ^= 1; }
+            }
+        }
+    } else {
+        // ===== epilogue warps 2..5: TMEM lane quadrant = warp % 4
+        const int ew = warp - kTcEpiWarp0;          // 0..3
+        const int quad = warp & 3;
+        const int row = quad * 32 + lane;           // tile row (TMEM lane)
+        for (int t = 0; t < n_tiles; ++t) {
+            int t0, tn;
+            tile_range(t, t0, tn);
+            const int b = t & 1;
+            mbar_wait(&tfull[b], (uint32_t)(t >> 1) & 1);
+            tc_fence_after();
+            const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(b * NP);
+            for (int c0 = 0; c0 < NP; c0 += 16) {
+                float v[16];
+                tmem_ld16(taddr + c0, v);
+#pragma unroll
+                for (int j = 0; j < 16; ++j)
+                    if (c0 + j < n_h) e.tile[(c0 + j) * kTile + row] = v[j] * a.inv_temp;
+            }
+            tc_fence_before();
+            mbar_arrive(&tempty[b]);
+            if (a.logits_out) {
+                named_bar_sync(1, 128);
+                for (int r = ew; r < n_h; r += 4)
+                    for (int p = lane; p < tn; p += 32)
+                        a.logits_out[(size_t)r * a.n_subset_max + t0 + p] = e.tile[r * kTile + p];
+            }
+            named_bar_sync(1, 128);
+            epi_tile(e, n_h, a.KP, tn, t0, ew, 4);
+            named_bar_sync(1, 128);
+        }
+        // write the CTA's partials
+        for (int r = ew; r < n_h; r += 4) {
+            const int cnt = e.st_cnt[r];
+            const size_t o = (size_t)blockIdx.x * a.n_h + r;
+            for (int i = lane; i < a.KP; i += 32) {
+                a.part.val[o * a.KP + i] = i < cnt ? e.st_val[r * a.KP + i] : -INFINITY;
+                a.part.id[o * a.KP + i] = i < cnt ? a.subset[e.st_pos[r * a.KP + i]] : -1;
+            }
+            if (lane == 0) {
+                a.part.cnt[o] = cnt;
+                a.part.m[o] = e.st_m[r];
+                a.part.s[o] = e.st_s[r];
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == 1)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(tp.tmem_cols));
+}
+
+// ------------------------------------------------------------------ host
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void* p = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+    }
+    return fn;
+}
+
+static bool make_map(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, uint32_t box0, uint32_t box1,
+                     CUtensorMapL2promotion prom) {
+    auto fn = encode_fn();
+    if (!fn) return false;
+    cuuint64_t dims[2] = {inner, outer};
+    cuuint64_t strides[1] = {inner * 2};
+    cuuint32_t box[2] = {box0, box1};
+    cuuint32_t estr[2] = {1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, prom,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+int lmh_tc_grid() { return kNumSMs; }
+
+bool lmh_tc_supported(const LmhArgs& a) {
+    return a.w_dtype == 0 && a.h_dtype == 0 && a.d % kBlockK == 0 && a.n_h >= 1 && a.n_h <= kTcMaxRows &&
+           a.n_w_rows <= 0x7fffffff;
+}
+
+cudaError_t launch_lmh_tc(const LmhArgs& a, cudaStream_t st) {
+    TcParams tp{};
+    tp.n_pad = ((a.n_h + 15) / 16) * 16;
+    tp.nkb = a.d / kBlockK;
+    uint32_t cols = 2 * tp.n_pad, c = 32;
+    while (c < cols) c <<= 1;
+    tp.tmem_cols = c;
+    const size_t stage_a = (size_t)kTileM * 128, stage_b = (size_t)tp.n_pad * 128;
+    const size_t epi = (size_t)a.n_h * kTile * 4 + (size_t)a.n_h * a.KP * 8 + (size_t)a.n_h * 12 + (size_t)4 * a.KP * 8;
+    const size_t fixed = epi + 2 * 128 * 4 + 64 * 8 + 1024 /*align slack*/ + 256;
+    const size_t budget = 227 * 1024;
+    int S = (int)((budget - fixed) / (stage_a + stage_b));
+    S = std::min(S, 8);
+    if (S < 2) return cudaErrorInvalidConfiguration;
+    tp.stages = S;
+    tp.off_b = (size_t)S * stage_a;
+    tp.off_epi = tp.off_b + (size_t)S * stage_b;
+    tp.off_bar = (tp.off_epi + epi + 15) & ~(size_t)15;
+    tp.off_rows = tp.off_bar + (size_t)(2 * S + 4) * 8 + 16;
+    const size_t smem = tp.off_rows + 2 * 128 * 4 + 1024;
+    CUtensorMap mw, mh;
+    if (!make_map(&mw, a.W, (uint64_t)a.d, (uint64_t)a.n_w_rows, kBlockK, 1, CU_TENSOR_MAP_L2_PROMOTION_L2_256B))
+        return cudaErrorInvalidValue;
+    if (!make_map(&mh, a.H, (uint64_t)a.d, (uint64_t)a.n_h, kBlockK, (uint32_t)tp.n_pad,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_128B))
+        return cudaErrorInvalidValue;
+    cudaError_t e = cudaFuncSetAttribute(lmh_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    lmh_tc_kernel<<<lmh_tc_grid(), kTcWarps * 32, smem, st>>>(mw, mh, a, tp);
+    return cudaGetLastError();
+}
+
+}  // namespace es
