@@ -535,7 +535,8 @@ evospec_status evospec_draft_step(evospec_ctx* ctx, const evospec_step_io* io, v
     const int n_sub_max = io->n_static + io->build.n_dyn;
     evospec_status s = evospec_build_subset(ctx, io->E, io->n_e_rows, q, io->static_ids, io->n_static, seeds,
                                             io->n_seed, io->csr_row_ptr, io->csr_col, cx, io->n_ctx, &io->build,
-                                            ctx->st_S, ctx->st_nS, ctx->st_local, ctx->st_nlocal, st);
+                                            ctx->st_S, ctx->st_nS, c.n_shards > 1 ? ctx->st_local : nullptr,
+                                            c.n_shards > 1 ? ctx->st_nlocal : nullptr, st);
     if (s != EVOSPEC_OK) return s;
     const int32_t* sub = c.n_shards > 1 ? ctx->st_local : ctx->st_S;
     const int32_t* nsub = c.n_shards > 1 ? ctx->st_nlocal : ctx->st_nS;

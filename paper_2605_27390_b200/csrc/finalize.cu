@@ -37,6 +37,9 @@ lmh_finalize_kernel(LmhArgs a, int n_cta, int k, float gamma, const float* __res
     const int lane = lane_id(), warp = warp_id(), nwarps = blockDim.x / 32;
     extern __shared__ unsigned char f_sm[];
     int* head = (int*)f_sm;                         // [n_cta]
+    int* l_cnt = head + n_cta;                      // [n_cta]
+    float* l_val = (float*)(l_cnt + n_cta);         // [n_cta][KP]
+    int32_t* l_id = (int32_t*)(l_val + (size_t)n_cta * KP);  // [n_cta][KP]
     __shared__ float c_v32[kMaxKP];
     __shared__ int32_t c_id[kMaxKP];
     __shared__ double c_e[kMaxKP];
@@ -79,6 +82,16 @@ lmh_finalize_kernel(LmhArgs a, int n_cta, int k, float gamma, const float* __res
     S = warp_sum(S);
     tot = warp_sum_i(tot);
     if (lane == 0) { red_s[warp] = S; red_t[warp] = tot; }
+    // stage every CTA's sorted list in shared memory (coalesced per list)
+    for (int c = warp; c < n_cta; c += nwarps) {
+        const size_t o = (size_t)c * a.n_h + r;
+        const int cnt = a.part.cnt[o];
+        if (lane == 0) l_cnt[c] = cnt;
+        for (int i = lane; i < cnt; i += 32) {
+            l_val[(size_t)c * KP + i] = a.part.val[o * KP + i];
+            l_id[(size_t)c * KP + i] = a.part.id[o * KP + i];
+        }
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
         float s_all = 0.0f;
@@ -94,22 +107,19 @@ lmh_finalize_kernel(LmhArgs a, int n_cta, int k, float gamma, const float* __res
         for (; produced < KP; ++produced) {
             float bv = -INFINITY;
             int bid = 0x7fffffff;
+            int bc = -1;
             for (int c = lane; c < n_cta; c += 32) {
-                size_t o = (size_t)c * a.n_h + r;
-                int h = head[c];
-                if (h < a.part.cnt[o]) {
-                    float v = a.part.val[o * KP + h];
-                    int id = a.part.id[o * KP + h];
-                    if (before(v, id, bv, bid)) { bv = v; bid = id; }
+                const int h = head[c];
+                if (h < l_cnt[c]) {
+                    const float v = l_val[(size_t)c * KP + h];
+                    const int id = l_id[(size_t)c * KP + h];
+                    if (before(v, id, bv, bid)) { bv = v; bid = id; bc = c; }
                 }
             }
+            const int my_id = bid;
             warp_argbest(bv, bid);
             if (bid == 0x7fffffff) break;
-            for (int c = lane; c < n_cta; c += 32) {
-                size_t o = (size_t)c * a.n_h + r;
-                int h = head[c];
-                if (h < a.part.cnt[o] && a.part.id[o * KP + h] == bid) head[c] = h + 1;
-            }
+            if (bc >= 0 && my_id == bid) head[bc] += 1;   // ids are unique: one owner
             if (lane == 0) { c_v32[produced] = bv; c_id[produced] = bid; }
             __syncwarp();
         }
@@ -160,9 +170,8 @@ lmh_finalize_kernel(LmhArgs a, int n_cta, int k, float gamma, const float* __res
         while (i < nk) {
             if (!c_need[i]) { ++i; continue; }
             int j = i;
-            while (j + 1 < nk && c_need[j + 1] &&
-                   (double)c_v32[j] - (double)c_v32[j + 1] <= 1e300)  // contiguous flagged block
-                ++j;
+            while (j + 1 < nk && c_need[j + 1]) ++j;   // contiguous re-scored block
+
             for (int u = i + 1; u <= j; ++u) {   // insertion sort by (exact desc, id asc)
                 double e = c_e[u];
                 int32_t id = c_id[u];
@@ -183,7 +192,8 @@ lmh_finalize_kernel(LmhArgs a, int n_cta, int k, float gamma, const float* __res
 void launch_lmh_finalize(const LmhArgs& a, int n_cta, int k, const float* wmax_dev, int32_t* topk_ids,
                          float* topk_vals, float* row_max, float* row_sumexp, int* flags, cudaStream_t st,
                          float gamma) {
-    size_t smem = (size_t)n_cta * sizeof(int);
+    size_t smem = (size_t)n_cta * 2 * sizeof(int) + (size_t)n_cta * a.KP * 8;
+    cudaFuncSetAttribute(lmh_finalize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     lmh_finalize_kernel<<<a.n_h, kFinThreads, smem, st>>>(a, n_cta, k, gamma, wmax_dev, topk_ids, topk_vals,
                                                            row_max, row_sumexp, flags);
 }

@@ -189,9 +189,16 @@ topn_select_kernel(const double* __restrict__ s64, const int32_t* __restrict__ i
         for (int b = threadIdx.x; b < 2048; b += blockDim.x) hist[b] = 0;
         __syncthreads();
         SelState my = st;
-        for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-            SelWords k = sel_words(s64[i], id_of(i));
-            if (sel_matches(k, my)) atomicAdd(&hist[(k.w[word] >> shift) & dmask], 1u);
+        for (int64_t b0 = lo; b0 < hi; b0 += blockDim.x) {   // uniform trip count per warp
+            const int64_t i = b0 + threadIdx.x;
+            uint32_t digit = 0xFFFFFFFFu;
+            if (i < hi) {
+                SelWords k = sel_words(s64[i], id_of(i));
+                if (sel_matches(k, my)) digit = (k.w[word] >> shift) & dmask;
+            }
+            // warp-aggregated increments: scores cluster in few bins
+            const unsigned peers = __match_any_sync(0xffffffffu, digit);
+            if (digit != 0xFFFFFFFFu && lane_id() == __ffs(peers) - 1) atomicAdd(&hist[digit], (uint32_t)__popc(peers));
         }
         __syncthreads();
         uint32_t* hp = hist_g + (size_t)pass * 2048;

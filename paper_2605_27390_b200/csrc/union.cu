@@ -148,7 +148,7 @@ union_kernel(int V, const int32_t* __restrict__ static_ids, int n_static,
     int32_t* goff = G + kMaxG;                               // [kMaxG + 1]
     int32_t* graph = goff + kMaxG + 1;                       // [kMaxG * per_seed]
     __shared__ int warp_tot[33];
-    __shared__ int nG_s, bad_s;
+    __shared__ int nG_s, bad_s, taken_s;
 
     const int tid = threadIdx.x, lane = lane_id();
     for (int w = tid; w < nwords; w += blockDim.x) bits[w] = 0;
@@ -163,27 +163,43 @@ union_kernel(int V, const int32_t* __restrict__ static_ids, int n_static,
     }
     const int n_sem = min(*n_sem_dev, n_sem_max);
     const int n_ctx_sel = ctx_sel ? *n_ctx_sel_dev : 0;
-    // 2. graph seeds and S_graph (lane 0 of warp 0: <= kMaxG entries)
-    if (tid == 0) {
-        int nG = 0;
+    // 2. graph seeds G = dedupe(seeds ++ S_sem[:ngs]) and S_graph, warp 0 in parallel
+    if (warp_id() == 0) {
         const int ngs = min(n_graph_sem_seeds, n_sem);
-        for (int i = 0; i < n_seed + ngs; ++i) {
+        const int nc = min(n_seed + ngs, kMaxG);
+        for (int i = lane; i < nc; i += 32) {          // candidates -> graph[] as scratch
             int32_t g = i < n_seed ? seeds[i] : sem[i - n_seed];
-            if (g < 0 || g >= V) { bad_s = 1; continue; }
-            bool dup = false;
-            for (int j = 0; j < nG; ++j) dup |= (G[j] == g);
-            if (!dup && nG < kMaxG) G[nG++] = g;
+            if (g < 0 || g >= V) { bad_s = 1; g = -1; }
+            graph[i] = g;
         }
-        int off = 0;
-        for (int j = 0; j < nG; ++j) {
-            goff[j] = off;
-            if (row_ptr) {
-                int deg = row_ptr[G[j] + 1] - row_ptr[G[j]];
-                off += min(deg, per_seed);
+        __syncwarp();
+        int nG = 0;
+        for (int base = 0; base < nc; base += 32) {
+            const int i = base + lane;
+            int32_t g = i < nc ? graph[i] : -1;
+            bool keep = g >= 0;
+            for (int j = 0; j < i && keep; ++j) keep = graph[j] != g;   // first occurrence
+            const unsigned bal = __ballot_sync(0xffffffffu, keep);
+            if (keep) G[nG + __popc(bal & ((1u << lane) - 1u))] = g;
+            nG += __popc(bal);
+        }
+        __syncwarp();
+        // degrees and offsets (exclusive scan of min(deg, per_seed))
+        int carry = 0;
+        for (int base = 0; base < nG; base += 32) {
+            const int j = base + lane;
+            int c = 0;
+            if (j < nG && row_ptr) c = min(row_ptr[G[j] + 1] - row_ptr[G[j]], per_seed);
+            int inc = c;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                int t = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= o) inc += t;
             }
+            if (j < nG) goff[j] = carry + inc - c;
+            carry += __shfl_sync(0xffffffffu, inc, 31);
         }
-        goff[nG] = off;
-        nG_s = nG;
+        if (lane == 0) { goff[nG] = carry; nG_s = nG; }
     }
     __syncthreads();
     const int nG = nG_s;
@@ -196,29 +212,60 @@ union_kernel(int V, const int32_t* __restrict__ static_ids, int n_static,
         }
     __syncthreads();
 
-    // 3. formation walk (warp 0)
+    // 3. formation: seeds ++ S_sem ++ S_graph ++ S_ctx, first occurrence, skip
+    //    members, stop at N_dyn. Seeds, graph and ctx are walked by warp 0 in
+    //    32-wide windows; S_sem (distinct ids by construction) is taken in
+    //    parallel with a block-wide order-preserving scan.
+    const unsigned lt_mask = (1u << lane) - 1u;
+    auto walk = [&](const int32_t* src, int len, int taken) -> int {
+        for (int base = 0; base < len && taken < n_dyn; base += 32) {
+            const int idx = base + lane;
+            int32_t c = idx < len ? src[idx] : -1;
+            bool valid = c >= 0 && c < V;
+            if (idx < len && !valid) bad_s = 1;
+            if (!valid) c = -1 - lane;            // distinct non-matching sentinel
+            const unsigned peers = __match_any_sync(0xffffffffu, c);
+            const bool first = valid && ((__ffs(peers) - 1) == lane);
+            const bool cand = first && !((bits[c < 0 ? 0 : (c >> 5)] >> (c & 31)) & 1u);
+            const unsigned bal = __ballot_sync(0xffffffffu, cand);
+            const int before = __popc(bal & lt_mask);
+            if (cand && taken + before < n_dyn) atomicOr(&bits[c >> 5], 1u << (c & 31));
+            taken += min(__popc(bal), n_dyn - taken);
+            __syncwarp();
+        }
+        return taken;
+    };
     if (warp_id() == 0) {
-        int taken = 0;
-        const unsigned lt_mask = (1u << lane) - 1u;
-        for (int part = 0; part < 4 && taken < n_dyn; ++part) {
-            const int32_t* src = part == 0 ? seeds : part == 1 ? sem : part == 2 ? graph : ctx_sel;
-            const int len = part == 0 ? n_seed : part == 1 ? n_sem : part == 2 ? n_graph : n_ctx_sel;
-            for (int base = 0; base < len && taken < n_dyn; base += 32) {
-                const int idx = base + lane;
-                int32_t c = idx < len ? src[idx] : -1;
-                bool valid = c >= 0 && c < V;
-                if (idx < len && !valid) bad_s = 1;
-                if (!valid) c = -1 - lane;            // distinct non-matching sentinel
-                const unsigned peers = __match_any_sync(0xffffffffu, c);
-                const bool first = valid && ((__ffs(peers) - 1) == lane);
-                const bool cand = first && !((bits[c < 0 ? 0 : (c >> 5)] >> (c & 31)) & 1u);
-                const unsigned bal = __ballot_sync(0xffffffffu, cand);
-                const int before = __popc(bal & lt_mask);
-                if (cand && taken + before < n_dyn) atomicOr(&bits[c >> 5], 1u << (c & 31));
-                taken += min(__popc(bal), n_dyn - taken);
-                __syncwarp();
+        const int t = walk(seeds, n_seed, 0);
+        if (lane == 0) taken_s = t;
+    }
+    __syncthreads();
+    {
+        const int taken0 = taken_s;
+        const int T = blockDim.x;
+        const int i0 = (int)((long long)n_sem * tid / T), i1 = (int)((long long)n_sem * (tid + 1) / T);
+        int cnt = 0;
+        for (int i = i0; i < i1; ++i) {
+            const int32_t c = sem[i];
+            cnt += (c >= 0 && c < V && !((bits[c >> 5] >> (c & 31)) & 1u)) ? 1 : 0;
+        }
+        int total = 0;
+        int off = block_excl_scan(cnt, warp_tot, total);   // contains __syncthreads
+        const int budget = n_dyn - taken0;
+        for (int i = i0; i < i1 && off < budget; ++i) {
+            const int32_t c = sem[i];
+            if (c >= 0 && c < V && !((bits[c >> 5] >> (c & 31)) & 1u)) {
+                atomicOr(&bits[c >> 5], 1u << (c & 31));
+                ++off;
             }
         }
+        __syncthreads();
+        if (tid == 0) taken_s = taken0 + min(total, budget);
+    }
+    __syncthreads();
+    if (warp_id() == 0 && taken_s < n_dyn) {
+        int t = walk(graph, n_graph, taken_s);
+        t = walk(ctx_sel, n_ctx_sel, t);
     }
     __syncthreads();
 

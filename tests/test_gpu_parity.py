@@ -206,3 +206,41 @@ def test_llama_full_size():
     ref = G.oracle_step(oracle, P)
     assert got["S"].size == 36864
     check(P, got, ref, c["k"])
+
+
+@pytest.fixture
+def lmh_path(monkeypatch):
+    def set_path(p):
+        monkeypatch.setenv("EVOSPEC_LMH", p)
+    return set_path
+
+
+@pytest.mark.parametrize("path", ["tc", "gemv"])
+@pytest.mark.parametrize("n_h,k", [(5, 10), (16, 1), (60, 10), (128, 64)])
+def test_lmh_paths(lmh_path, path, n_h, k):
+    """Both LM-head kernels (tcgen05 and FFMA) against the oracle, same inputs."""
+    lmh_path(path)
+    P = G.make_problem(21, dtype="bf16", V=40000, d=1024, n_static=5000, n_sem=900, n_dyn=777,
+                       n_h=n_h, k=k, avg_deg=16)
+    got = run_path(P, logits=True)
+    ref = G.oracle_step(oracle, P)
+    check(P, got, ref, k)
+    z = oracle.subset_logits(P["W"], P["H"], ref["S"])
+    # accumulation error stays well inside the certification envelope (1/8 of delta)
+    gamma = 2.0 ** -16 if path == "tc" else 1.01 * (1024 / 32 + 6) * 2.0 ** -24
+    W64 = P["W"].astype(np.uint32) << 16
+    wmax = np.sqrt((W64.view(np.float32).astype(np.float64) ** 2).sum(1)).max()
+    hn = np.sqrt((((P["H"].astype(np.uint32) << 16).view(np.float32).astype(np.float64)) ** 2).sum(1))
+    err = np.abs(got["logits"] - z).max(1)
+    assert np.all(err <= gamma * hn * wmax / 8), (err / (hn * wmax)).max()
+
+
+def test_tc_integer_exact(lmh_path):
+    """Integer inputs: tcgen05 fp32 accumulation is exact (sums < 2^24)."""
+    lmh_path("tc")
+    P = G.make_problem(4, dtype="bf16", integer=True, V=6000, d=512, n_static=700, n_sem=300,
+                       n_dyn=260, n_h=37, k=12)
+    got = run_path(P, logits=True)
+    ref = G.oracle_step(oracle, P)
+    check(P, got, ref, P["k"])
+    np.testing.assert_array_equal(got["logits"], oracle.subset_logits(P["W"], P["H"], ref["S"]))
