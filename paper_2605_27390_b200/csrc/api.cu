@@ -318,7 +318,7 @@ evospec_status evospec_build_subset(evospec_ctx* ctx, const void* E, int64_t n_e
     cudaStream_t st = (cudaStream_t)stream;
     if (n_static < 0 || (n_static > 0 && !static_ids) || n_seed < 0 || (n_seed > 0 && !seeds))
         return fail(EVOSPEC_EINPUT, "build_subset: bad static / seed arguments");
-    if (p->n_sem < 0 || p->n_sem > c.max_sem || p->n_dyn < 0 || p->per_seed < 0 || p->per_seed > 64 ||
+    if (p->n_sem < 0 || p->n_sem > c.max_sem || p->n_sem > 16384 || p->n_dyn < 0 || p->per_seed < 0 || p->per_seed > 64 ||
         p->n_graph_sem_seeds < 0 || n_seed + std::min(p->n_graph_sem_seeds, p->n_sem) > std::min(c.max_seeds, 128))
         return fail(EVOSPEC_EINPUT, "build_subset: params out of capacity (n_sem <= %d, seeds <= %d, per_seed <= 64)",
                     c.max_sem, std::min(c.max_seeds, 128));

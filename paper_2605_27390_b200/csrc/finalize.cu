@@ -49,6 +49,7 @@ lmh_finalize_kernel(LmhArgs a, int n_cta, int k, float gamma, const float* __res
     __shared__ float red_m[32], red_s[32];
     __shared__ int red_t[32];
     __shared__ double hn2_s;
+    __shared__ double red_d[32];
 
     // 1. softmax state; ||h_r||^2 (warp 7) for delta
     float M = -INFINITY;
@@ -59,16 +60,21 @@ lmh_finalize_kernel(LmhArgs a, int n_cta, int k, float gamma, const float* __res
     }
     M = warp_max(M);
     if (lane == 0) red_m[warp] = M;
-    if (warp == nwarps - 1) {
+    {   // ||h_r||^2 by all threads (independent loads), fp64
         double acc = 0.0;
-        for (int col = lane; col < a.d; col += 32) {
-            double h = load_elem(a.H, a.h_dtype, (size_t)r * a.d + col);
+        for (int col = threadIdx.x; col < a.d; col += blockDim.x) {
+            const double h = load_elem(a.H, a.h_dtype, (size_t)r * a.d + col);
             acc = fma(h, h, acc);
         }
         acc = warp_sum_d(acc);
-        if (lane == 0) hn2_s = acc;
+        if (lane == 0) red_d[warp] = acc;
     }
     __syncthreads();
+    if (threadIdx.x == 0) {
+        double hn = 0.0;
+        for (int w = 0; w < nwarps; ++w) hn += red_d[w];
+        hn2_s = hn;
+    }
     M = -INFINITY;
     for (int w = 0; w < nwarps; ++w) M = fmaxf(M, red_m[w]);
     float S = 0.0f;
@@ -82,15 +88,14 @@ lmh_finalize_kernel(LmhArgs a, int n_cta, int k, float gamma, const float* __res
     S = warp_sum(S);
     tot = warp_sum_i(tot);
     if (lane == 0) { red_s[warp] = S; red_t[warp] = tot; }
-    // stage every CTA's sorted list in shared memory (coalesced per list)
-    for (int c = warp; c < n_cta; c += nwarps) {
-        const size_t o = (size_t)c * a.n_h + r;
-        const int cnt = a.part.cnt[o];
-        if (lane == 0) l_cnt[c] = cnt;
-        for (int i = lane; i < cnt; i += 32) {
-            l_val[(size_t)c * KP + i] = a.part.val[o * KP + i];
-            l_id[(size_t)c * KP + i] = a.part.id[o * KP + i];
-        }
+    // stage every CTA's sorted list in shared memory: flat, independent loads
+    // (entries past a list's count are -inf / -1 in the partials)
+    for (int c = threadIdx.x; c < n_cta; c += blockDim.x) l_cnt[c] = a.part.cnt[(size_t)c * a.n_h + r];
+    for (int f = threadIdx.x; f < n_cta * KP; f += blockDim.x) {
+        const int c = f / KP, i = f - c * KP;
+        const size_t o = ((size_t)c * a.n_h + r) * KP + i;
+        l_val[f] = a.part.val[o];
+        l_id[f] = a.part.id[o];
     }
     __syncthreads();
     if (threadIdx.x == 0) {

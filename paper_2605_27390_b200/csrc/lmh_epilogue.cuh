@@ -10,7 +10,15 @@
 //   the best KP = k + kTopkPad (z, position) pairs, ordered (z desc, pos asc).
 // Positions ascend with token id (the subset is sorted), so "lower id wins
 // ties" is "earlier position wins"; state from earlier tiles always wins a tie
-// against the current tile, which the strict comparison below implements.
+// against the current tile.
+//
+// Top-KP fold (one warp per H row): the sorted list lives in registers, entry
+// i on lane i % 32, slot i / 32. Tile values above the list's KP-th entry are
+// inserted one at a time (ballot -> rank, shfl_up -> shift), so the cost is
+// proportional to the number of values that actually enter. For a row whose
+// list is not yet full, a pre-threshold theta0 = the KP-th largest of the 32
+// per-lane maxima (a lower bound of the tile's KP-th value: those KP maxima
+// are KP distinct tile elements) filters the tile first.
 #pragma once
 #include "common.cuh"
 #include "kernels.cuh"
@@ -18,6 +26,7 @@
 namespace es {
 
 constexpr int kTile = 128;
+constexpr int kTileJ = kTile / 32;
 
 struct EpiSmem {
     float* tile;     // [n_h][kTile]
@@ -26,24 +35,20 @@ struct EpiSmem {
     int* st_cnt;     // [n_h]
     float* st_m;     // [n_h]
     float* st_s;     // [n_h]
-    float* scr_val;  // [n_warps][KP]
-    int* scr_pos;    // [n_warps][KP]
 };
 
-ES_DEV size_t epi_smem_bytes(int n_h, int KP, int n_warps) {
-    return (size_t)n_h * kTile * 4 + (size_t)n_h * KP * 8 + (size_t)n_h * 12 + (size_t)n_warps * KP * 8;
+__host__ __device__ inline size_t epi_smem_bytes(int n_h, int KP) {
+    return (size_t)n_h * kTile * 4 + (size_t)n_h * KP * 8 + (size_t)n_h * 12;
 }
 
-ES_DEV EpiSmem epi_carve(unsigned char* p, int n_h, int KP, int n_warps) {
+ES_DEV EpiSmem epi_carve(unsigned char* p, int n_h, int KP) {
     EpiSmem e;
     e.tile = (float*)p;        p += (size_t)n_h * kTile * 4;
     e.st_val = (float*)p;      p += (size_t)n_h * KP * 4;
     e.st_pos = (int*)p;        p += (size_t)n_h * KP * 4;
     e.st_cnt = (int*)p;        p += (size_t)n_h * 4;
     e.st_m = (float*)p;        p += (size_t)n_h * 4;
-    e.st_s = (float*)p;        p += (size_t)n_h * 4;
-    e.scr_val = (float*)p;     p += (size_t)n_warps * KP * 4;
-    e.scr_pos = (int*)p;
+    e.st_s = (float*)p;
     return e;
 }
 
@@ -55,90 +60,143 @@ ES_DEV void epi_init(const EpiSmem& e, int n_h) {
     }
 }
 
-// local best of the lane's kTile/32 values under (value desc, pos asc)
-ES_DEV void lane_best(const float (&v)[kTile / 32], int base_pos, int lane, float& bv, int& bp) {
-    bv = -INFINITY;
-    bp = 0x7fffffff;
+// KP-th largest value (1-based) of the 32 lane values, every lane gets it.
+ES_DEV float warp_kth_largest(float x, int kth) {
+    // bitonic sort descending across the warp (15 compare-exchange stages)
+    const int lane = lane_id();
 #pragma unroll
-    for (int j = 0; j < kTile / 32; ++j) {
-        int p = base_pos + lane + 32 * j;
-        if (v[j] != -INFINITY && before(v[j], p, bv, bp)) { bv = v[j]; bp = p; }
+    for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            const float y = __shfl_xor_sync(0xffffffffu, x, j);
+            const bool lower = (lane & j) == 0;
+            const bool desc = (lane & k) == 0;
+            // in a descending block the lower lane keeps the larger value
+            const bool keep_max = (lower == desc);
+            x = keep_max ? fmaxf(x, y) : fminf(x, y);
+        }
     }
+    return __shfl_sync(0xffffffffu, x, kth - 1);
+}
+
+template <int SLOTS>
+struct TopList {
+    float v[SLOTS];
+    int p[SLOTS];
+};
+
+// Fold one row's tile values into its sorted top-KP list (SLOTS*32 >= KP).
+template <int SLOTS>
+ES_DEV void fold_row(const EpiSmem& e, int r, int KP, int tn, int base_pos) {
+    const int lane = lane_id();
+    float v[kTileJ];
+    float mx = -INFINITY;
+#pragma unroll
+    for (int j = 0; j < kTileJ; ++j) {
+        const int p = lane + 32 * j;
+        v[j] = p < tn ? e.tile[r * kTile + p] : -INFINITY;
+        mx = fmaxf(mx, v[j]);
+    }
+    const float lane_max = mx;
+    mx = warp_max(mx);
+    if (tn <= 0) return;
+    // online softmax
+    const float m_old = e.st_m[r];
+    const float m_new = fmaxf(m_old, mx);
+    float acc = 0.0f;
+#pragma unroll
+    for (int j = 0; j < kTileJ; ++j)
+        if (v[j] != -INFINITY) acc += expf(v[j] - m_new);
+    acc = warp_sum(acc);
+    // load the list
+    int cnt = e.st_cnt[r];
+    TopList<SLOTS> L;
+#pragma unroll
+    for (int s = 0; s < SLOTS; ++s) {
+        const int i = lane + 32 * s;
+        L.v[s] = i < cnt ? e.st_val[r * KP + i] : -INFINITY;
+        L.p[s] = i < cnt ? e.st_pos[r * KP + i] : 0x7fffffff;
+    }
+    __syncwarp();
+    if (lane == 0) {
+        e.st_s[r] = e.st_s[r] * (m_old == -INFINITY ? 0.0f : expf(m_old - m_new)) + acc;
+        e.st_m[r] = m_new;
+    }
+    const int kl = (KP - 1) & 31, ks = (KP - 1) >> 5;   // holder of entry KP-1
+    auto kth = [&](float& tv, int& tp) {
+        float cv = L.v[0];
+        int cp = L.p[0];
+#pragma unroll
+        for (int s = 1; s < SLOTS; ++s) if (s == ks) { cv = L.v[s]; cp = L.p[s]; }
+        tv = __shfl_sync(0xffffffffu, cv, kl);
+        tp = __shfl_sync(0xffffffffu, cp, kl);
+    };
+    float tv;
+    int tp;
+    kth(tv, tp);                      // (-inf, INT_MAX) while the list is not full
+    float theta0 = -INFINITY;         // pre-threshold for a list that is not full
+    if (cnt < KP && KP <= 32) theta0 = warp_kth_largest(lane_max, KP);
+    if (cnt == KP && !(mx > tv)) {    // nothing in this tile can enter
+        if (lane == 0) e.st_cnt[r] = cnt;
+        return;
+    }
+#pragma unroll
+    for (int j = 0; j < kTileJ; ++j) {
+        const int pj = base_pos + lane + 32 * j;
+        bool cand = v[j] != -INFINITY && v[j] >= theta0 && (cnt < KP ? true : before(v[j], pj, tv, tp));
+        unsigned m = __ballot_sync(0xffffffffu, cand);
+        while (m) {
+            const int src = __ffs(m) - 1;
+            m &= m - 1;
+            const float x = __shfl_sync(0xffffffffu, v[j], src);
+            const int xp = base_pos + src + 32 * j;
+            if (cnt == KP && !before(x, xp, tv, tp)) continue;   // threshold rose meanwhile
+            // rank of x in the list
+            int at = 0;
+#pragma unroll
+            for (int s = 0; s < SLOTS; ++s)
+                at += __popc(__ballot_sync(0xffffffffu, (lane + 32 * s) < cnt && before(L.v[s], L.p[s], x, xp)));
+            // shift entries at index >= at by one, insert at `at`
+#pragma unroll
+            for (int s = SLOTS - 1; s >= 0; --s) {
+                float pv = __shfl_up_sync(0xffffffffu, L.v[s], 1);
+                int pp = __shfl_up_sync(0xffffffffu, L.p[s], 1);
+                if (s > 0) {
+                    const float cv = __shfl_sync(0xffffffffu, L.v[s > 0 ? s - 1 : 0], 31);
+                    const int cp = __shfl_sync(0xffffffffu, L.p[s > 0 ? s - 1 : 0], 31);
+                    if (lane == 0) { pv = cv; pp = cp; }
+                }
+                const int i = lane + 32 * s;
+                if (i > at) { L.v[s] = pv; L.p[s] = pp; }
+                if (i == at) { L.v[s] = x; L.p[s] = xp; }
+            }
+            cnt = min(cnt + 1, KP);
+            if (cnt == KP) kth(tv, tp);
+        }
+    }
+#pragma unroll
+    for (int s = 0; s < SLOTS; ++s) {
+        const int i = lane + 32 * s;
+        if (i < cnt) { e.st_val[r * KP + i] = L.v[s]; e.st_pos[r * KP + i] = L.p[s]; }
+    }
+    if (lane == 0) e.st_cnt[r] = cnt;
+    __syncwarp();
 }
 
 // Fold the current tile (tn valid positions starting at global position
 // base_pos) into the state of rows r = warp, warp + n_warps, ...
 ES_DEV void epi_tile(const EpiSmem& e, int n_h, int KP, int tn, int base_pos, int warp, int n_warps) {
-    const int lane = lane_id();
-    float* sv = e.scr_val + warp * KP;
-    int* sp = e.scr_pos + warp * KP;
     for (int r = warp; r < n_h; r += n_warps) {
-        float v[kTile / 32];
-        float mx = -INFINITY;
-#pragma unroll
-        for (int j = 0; j < kTile / 32; ++j) {
-            int p = lane + 32 * j;
-            v[j] = p < tn ? e.tile[r * kTile + p] : -INFINITY;
-            mx = fmaxf(mx, v[j]);
-        }
-        mx = warp_max(mx);
-        if (tn <= 0) continue;
-        // online softmax
-        const float m_old = e.st_m[r];
-        const float m_new = fmaxf(m_old, mx);
-        float acc = 0.0f;
-#pragma unroll
-        for (int j = 0; j < kTile / 32; ++j)
-            if (v[j] != -INFINITY) acc += expf(v[j] - m_new);
-        acc = warp_sum(acc);
-        // top-KP merge
-        const int cnt = e.st_cnt[r];
-        const float theta = cnt == KP ? e.st_val[r * KP + KP - 1] : -INFINITY;
-        __syncwarp();
-        if (lane == 0) {
-            e.st_s[r] = e.st_s[r] * (m_old == -INFINITY ? 0.0f : expf(m_old - m_new)) + acc;
-            e.st_m[r] = m_new;
-        }
-        if (!(mx > theta) && cnt == KP) { __syncwarp(); continue; }
-        float bv; int bp;
-        lane_best(v, base_pos, lane, bv, bp);
-        warp_argbest(bv, bp);
-        int a = 0, produced = 0;
-        while (produced < KP) {
-            const bool tile_ok = bp != 0x7fffffff;
-            const bool old_ok = a < cnt;
-            if (!tile_ok && !old_ok) break;
-            const float ov = old_ok ? e.st_val[r * KP + a] : -INFINITY;
-            const int op = old_ok ? e.st_pos[r * KP + a] : 0x7fffffff;
-            if (tile_ok && (!old_ok || before(bv, bp, ov, op))) {
-                if (lane == 0) { sv[produced] = bv; sp[produced] = bp; }
-                const int lp = bp - base_pos;        // remove it from the tile
-                if ((lp & 31) == lane) {
-#pragma unroll
-                    for (int j = 0; j < kTile / 32; ++j) if (j == (lp >> 5)) v[j] = -INFINITY;
-                }
-                lane_best(v, base_pos, lane, bv, bp);
-                warp_argbest(bv, bp);
-            } else {
-                if (lane == 0) { sv[produced] = ov; sp[produced] = op; }
-                ++a;
-            }
-            ++produced;
-        }
-        __syncwarp();
-        for (int i = lane; i < produced; i += 32) {
-            e.st_val[r * KP + i] = sv[i];
-            e.st_pos[r * KP + i] = sp[i];
-        }
-        if (lane == 0) e.st_cnt[r] = produced;
-        __syncwarp();
+        if (KP <= 32) fold_row<1>(e, r, KP, tn, base_pos);
+        else if (KP <= 64) fold_row<2>(e, r, KP, tn, base_pos);
+        else fold_row<3>(e, r, KP, tn, base_pos);
     }
 }
 
 // Write the CTA's state to the global partials (positions -> global ids).
 ES_DEV void epi_store(const EpiSmem& e, const LmhPartials& P, int cta, int n_h_total, int h_row0,
-                      int n_h, int KP, const int32_t* subset) {
-    for (int r = warp_id(); r < n_h; r += blockDim.x / 32) {
+                      int n_h, int KP, const int32_t* subset, int warp, int n_warps) {
+    for (int r = warp; r < n_h; r += n_warps) {
         const int cnt = e.st_cnt[r];
         const size_t o = ((size_t)cta * n_h_total + h_row0 + r);
         for (int i = lane_id(); i < KP; i += 32) {

@@ -65,7 +65,7 @@ lmh_gemv_kernel(LmhArgs a, int h_row0) {
     const int d = a.d;
     const int n_chunks = (d + 32 * ELEMS - 1) / (32 * ELEMS);
     float* H_sm = (float*)g_sm;                              // [NH][n_chunks][ELEMS][32]
-    EpiSmem e = epi_carve(g_sm + (size_t)NH * n_chunks * ELEMS * 32 * 4, NH, a.KP, kGemvWarps);
+    EpiSmem e = epi_carve(g_sm + (size_t)NH * n_chunks * ELEMS * 32 * 4, NH, a.KP);
     const int lane = lane_id(), warp = warp_id();
 
     for (int i = threadIdx.x; i < NH * n_chunks * ELEMS * 32; i += blockDim.x) {
@@ -155,15 +155,14 @@ lmh_gemv_kernel(LmhArgs a, int h_row0) {
         epi_tile(e, NH, a.KP, tn, tb, warp, kGemvWarps);
         __syncthreads();
     }
-    epi_store(e, a.part, blockIdx.x, a.n_h, h_row0, NH, a.KP, a.subset);
+    epi_store(e, a.part, blockIdx.x, a.n_h, h_row0, NH, a.KP, a.subset, warp, kGemvWarps);
 }
 
 template <int DT, int NH>
 static size_t smem_t(const LmhArgs& a) {
     const int elems = DT == 0 ? 8 : 4;
     const int n_chunks = (a.d + 32 * elems - 1) / (32 * elems);
-    return (size_t)NH * n_chunks * elems * 32 * 4 +
-           ((size_t)NH * kTile * 4 + (size_t)NH * a.KP * 8 + (size_t)NH * 12 + (size_t)kGemvWarps * a.KP * 8);
+    return (size_t)NH * n_chunks * elems * 32 * 4 + epi_smem_bytes(NH, a.KP);
 }
 
 template <int DT, int NH>

@@ -28,7 +28,8 @@
 
 namespace es {
 
-constexpr int kTcWarps = 6;
+constexpr int kTcWarps = 10;
+constexpr int kTcEpiWarps = 8;
 constexpr int kTcEpiWarp0 = 2;
 constexpr int kBlockK = 64;        // bf16 columns per stage = one 128-byte swizzle atom row
 constexpr int kTileM = 128;
@@ -149,7 +150,7 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
     const int S = tp.stages, NP = tp.n_pad, n_h = a.n_h;
     unsigned char* smA = base;                                   // [S][128][128 B]
     unsigned char* smB = base + tp.off_b;                        // [S][NP][128 B]
-    EpiSmem e = epi_carve(base + tp.off_epi, n_h, a.KP, 4);
+    EpiSmem e = epi_carve(base + tp.off_epi, n_h, a.KP);
     uint64_t* full = (uint64_t*)(base + tp.off_bar);             // [S]
     uint64_t* empty = full + S;                                  // [S]
     uint64_t* tfull = empty + S;                                 // [2]
@@ -168,7 +169,7 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
         asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap_w) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap_h) : "memory");
         for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-        for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 128); }
+        for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], kTcEpiWarps * 32); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) {
@@ -245,10 +246,13 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
             }
         }
     } else {
-        // ===== epilogue warps 2..5: TMEM lane quadrant = warp % 4
-        const int ew = warp - kTcEpiWarp0;          // 0..3
+        // ===== epilogue warps 2..9: TMEM lane quadrant = warp % 4; the two
+        // warps of a quadrant split the accumulator columns (16-column chunks)
+        const int ew = warp - kTcEpiWarp0;          // 0..7
         const int quad = warp & 3;
+        const int half = ew >> 2;
         const int row = quad * 32 + lane;           // tile row (TMEM lane)
+        const int nthr = kTcEpiWarps * 32;
         for (int t = 0; t < n_tiles; ++t) {
             int t0, tn;
             tile_range(t, t0, tn);
@@ -256,7 +260,7 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
             mbar_wait(&tfull[b], (uint32_t)(t >> 1) & 1);
             tc_fence_after();
             const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(b * NP);
-            for (int c0 = 0; c0 < NP; c0 += 16) {
+            for (int c0 = half * 16; c0 < NP; c0 += 32) {
                 float v[16];
                 tmem_ld16(taddr + c0, v);
 #pragma unroll
@@ -265,30 +269,16 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
             }
             tc_fence_before();
             mbar_arrive(&tempty[b]);
+            named_bar_sync(1, nthr);
             if (a.logits_out) {
-                named_bar_sync(1, 128);
-                for (int r = ew; r < n_h; r += 4)
+                for (int r = ew; r < n_h; r += kTcEpiWarps)
                     for (int p = lane; p < tn; p += 32)
                         a.logits_out[(size_t)r * a.n_subset_max + t0 + p] = e.tile[r * kTile + p];
             }
-            named_bar_sync(1, 128);
-            epi_tile(e, n_h, a.KP, tn, t0, ew, 4);
-            named_bar_sync(1, 128);
+            epi_tile(e, n_h, a.KP, tn, t0, ew, kTcEpiWarps);
+            named_bar_sync(1, nthr);
         }
-        // write the CTA's partials
-        for (int r = ew; r < n_h; r += 4) {
-            const int cnt = e.st_cnt[r];
-            const size_t o = (size_t)blockIdx.x * a.n_h + r;
-            for (int i = lane; i < a.KP; i += 32) {
-                a.part.val[o * a.KP + i] = i < cnt ? e.st_val[r * a.KP + i] : -INFINITY;
-                a.part.id[o * a.KP + i] = i < cnt ? a.subset[e.st_pos[r * a.KP + i]] : -1;
-            }
-            if (lane == 0) {
-                a.part.cnt[o] = cnt;
-                a.part.m[o] = e.st_m[r];
-                a.part.s[o] = e.st_s[r];
-            }
-        }
+        epi_store(e, a.part, blockIdx.x, a.n_h, 0, n_h, a.KP, a.subset, ew, kTcEpiWarps);
     }
     tc_fence_before();
     __syncthreads();
@@ -338,7 +328,7 @@ cudaError_t launch_lmh_tc(const LmhArgs& a, cudaStream_t st) {
     while (c < cols) c <<= 1;
     tp.tmem_cols = c;
     const size_t stage_a = (size_t)kTileM * 128, stage_b = (size_t)tp.n_pad * 128;
-    const size_t epi = (size_t)a.n_h * kTile * 4 + (size_t)a.n_h * a.KP * 8 + (size_t)a.n_h * 12 + (size_t)4 * a.KP * 8;
+    const size_t epi = epi_smem_bytes(a.n_h, a.KP);
     const size_t fixed = epi + 2 * 128 * 4 + 64 * 8 + 1024 /*align slack*/ + 256;
     const size_t budget = 227 * 1024;
     int S = (int)((budget - fixed) / (stage_a + stage_b));

@@ -155,11 +155,21 @@ union_kernel(int V, const int32_t* __restrict__ static_ids, int n_static,
     if (tid == 0) bad_s = 0;
     __syncthreads();
     // 1. static members
-    for (int i = tid; i < n_static; i += blockDim.x) {
-        int32_t v = static_ids[i];
-        if (v < 0 || v >= V) { bad_s = 1; continue; }
-        if (debug && i > 0 && static_ids[i - 1] >= v) bad_s = 1;
-        atomicOr(&bits[v >> 5], 1u << (v & 31));
+    for (int i0 = 0; i0 < n_static; i0 += 8 * blockDim.x) {   // 8 independent loads in flight
+        int32_t v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int i = i0 + u * blockDim.x + tid;
+            v[u] = i < n_static ? __ldg(&static_ids[i]) : -1;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int i = i0 + u * blockDim.x + tid;
+            if (i >= n_static) continue;
+            if (v[u] < 0 || v[u] >= V) { bad_s = 1; continue; }
+            if (debug && i > 0 && static_ids[i - 1] >= v[u]) bad_s = 1;
+            atomicOr(&bits[v[u] >> 5], 1u << (v[u] & 31));
+        }
     }
     const int n_sem = min(*n_sem_dev, n_sem_max);
     const int n_ctx_sel = ctx_sel ? *n_ctx_sel_dev : 0;
@@ -244,18 +254,27 @@ union_kernel(int V, const int32_t* __restrict__ static_ids, int n_static,
         const int taken0 = taken_s;
         const int T = blockDim.x;
         const int i0 = (int)((long long)n_sem * tid / T), i1 = (int)((long long)n_sem * (tid + 1) / T);
+        // each thread owns <= kSemPerThread consecutive S_sem entries, loaded once
+        constexpr int kSemPerThread = 16;
+        int32_t cv[kSemPerThread];
+        unsigned newm = 0;
+#pragma unroll
+        for (int u = 0; u < kSemPerThread; ++u) cv[u] = (i0 + u < i1) ? __ldg(&sem[i0 + u]) : -1;
         int cnt = 0;
-        for (int i = i0; i < i1; ++i) {
-            const int32_t c = sem[i];
-            cnt += (c >= 0 && c < V && !((bits[c >> 5] >> (c & 31)) & 1u)) ? 1 : 0;
+#pragma unroll
+        for (int u = 0; u < kSemPerThread; ++u) {
+            const int32_t c = cv[u];
+            const bool nw = c >= 0 && c < V && !((bits[c >> 5] >> (c & 31)) & 1u);
+            newm |= (unsigned)nw << u;
+            cnt += nw;
         }
         int total = 0;
         int off = block_excl_scan(cnt, warp_tot, total);   // contains __syncthreads
         const int budget = n_dyn - taken0;
-        for (int i = i0; i < i1 && off < budget; ++i) {
-            const int32_t c = sem[i];
-            if (c >= 0 && c < V && !((bits[c >> 5] >> (c & 31)) & 1u)) {
-                atomicOr(&bits[c >> 5], 1u << (c & 31));
+#pragma unroll
+        for (int u = 0; u < kSemPerThread; ++u) {
+            if (((newm >> u) & 1u) && off < budget) {
+                atomicOr(&bits[cv[u] >> 5], 1u << (cv[u] & 31));
                 ++off;
             }
         }
