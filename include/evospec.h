@@ -156,8 +156,8 @@ evospec_status evospec_build_subset(evospec_ctx *ctx,
     int32_t *out_local_ids, int32_t *out_local_n,
     void *stream);
 
-/* Debug/parity accessor: copies the ordered S_sem of the last build on this
- * context (device ids, N_sem entries) into out_dev. Async on stream. */
+/* Debug/parity accessor: copies the S_sem SET of the last build on this
+ * context (N_sem device ids, in no particular order) into out_dev. Async. */
 evospec_status evospec_last_semantic(evospec_ctx *ctx, int32_t *out_dev, int32_t n, void *stream);
 
 /* ---- a5-a7: gathered LM head + fused softmax / top-k --------------------- */

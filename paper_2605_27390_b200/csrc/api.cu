@@ -99,16 +99,19 @@ struct evospec_ctx {
     // semantic scan + selection
     double* s64 = nullptr;
     uint32_t* key32 = nullptr;
-    uint32_t* hist = nullptr;
-    int* sel_count = nullptr;
-    double* sel_s = nullptr;
-    int32_t* sel_id = nullptr;
-    double* gat_s = nullptr;     // [R][max_sem] gathered candidates (sharded scan)
+    uint32_t* hist12 = nullptr;   // scan-fused pass-0 histogram
+    uint32_t* hist = nullptr;     // [12][4096] further select passes
+    int cand_cap = 0;             // candidate superset capacity (union smem)
+    int* cand_count = nullptr;
+    double* cand_s = nullptr;     // [cand_cap]
+    int32_t* cand_id = nullptr;
+    int* loc_count = nullptr;     // sharded index: exact local top-N
+    double* loc_s = nullptr;      // [max_sem]
+    int32_t* loc_id = nullptr;
+    double* gat_s = nullptr;      // [R][max_sem] gathered local top-N
     int32_t* gat_id = nullptr;
-    int* gat_count = nullptr;
-    double* sel2_s = nullptr;
-    int32_t* sel2_id = nullptr;
-    int32_t* sem_sorted = nullptr;
+    int32_t* sem_ids = nullptr;   // S_sem of the last build (unordered)
+    int* sem_n = nullptr;
     int32_t* ctx_sel = nullptr;
     int* ctx_n = nullptr;
     // LM head partials
@@ -190,8 +193,9 @@ const char* evospec_status_string(evospec_status st) {
 evospec_status evospec_destroy(evospec_ctx* ctx) {
     if (!ctx) return EVOSPEC_OK;
     cudaSetDevice(ctx->device);
-    void* ptrs[] = {ctx->s64, ctx->key32, ctx->hist, ctx->sel_count, ctx->sel_s, ctx->sel_id, ctx->gat_s,
-                    ctx->gat_id, ctx->gat_count, ctx->sel2_s, ctx->sel2_id, ctx->sem_sorted, ctx->ctx_sel,
+    void* ptrs[] = {ctx->s64, ctx->key32, ctx->hist12, ctx->hist, ctx->cand_count, ctx->cand_s, ctx->cand_id,
+                    ctx->loc_count, ctx->loc_s, ctx->loc_id, ctx->gat_s, ctx->gat_id, ctx->sem_ids, ctx->sem_n,
+                    ctx->ctx_sel,
                     ctx->ctx_n, ctx->part.val, ctx->part.id, ctx->part.m, ctx->part.s, ctx->part.cnt,
                     ctx->flags, ctx->wmax, ctx->g_ids, ctx->g_vals, ctx->g_m, ctx->g_s, ctx->st_q, ctx->st_H,
                     ctx->st_seeds, ctx->st_ctx, ctx->st_S, ctx->st_nS, ctx->st_local, ctx->st_nlocal,
@@ -233,11 +237,21 @@ evospec_status evospec_create(evospec_ctx** out, const evospec_config* cfg, int 
     const size_t hb = c.h_dtype == EVOSPEC_BF16 ? 2 : 4;
     cudaError_t e = cudaSuccess;
     auto A = [&](cudaError_t r) { if (e == cudaSuccess) e = r; };
-    A(dalloc(&x->s64, V)); A(dalloc(&x->key32, V)); A(dalloc(&x->hist, 12 * 2048));
-    A(dalloc(&x->sel_count, 4)); A(dalloc(&x->sel_s, sem)); A(dalloc(&x->sel_id, sem));
-    A(dalloc(&x->gat_s, sem * R)); A(dalloc(&x->gat_id, sem * R)); A(dalloc(&x->gat_count, 4));
-    A(dalloc(&x->sel2_s, sem)); A(dalloc(&x->sel2_id, sem));
-    A(dalloc(&x->sem_sorted, sem)); A(dalloc(&x->ctx_sel, std::max(1, c.max_ctx))); A(dalloc(&x->ctx_n, 1));
+    x->cand_cap = union_cand_cap(c.V, 64);
+    if (c.max_sem > x->cand_cap) {
+        const int cap_v = x->cand_cap;
+        delete x;
+        return fail(EVOSPEC_EINPUT, "create: max_sem=%d exceeds the selection capacity %d at V=%d", c.max_sem,
+                    cap_v, c.V);
+    }
+    const size_t cap = (size_t)x->cand_cap;
+    A(dalloc(&x->s64, V)); A(dalloc(&x->key32, V)); A(dalloc(&x->hist12, kHistBins));
+    A(dalloc(&x->hist, 12 * kHistBins));
+    A(dalloc(&x->cand_count, 4)); A(dalloc(&x->cand_s, cap)); A(dalloc(&x->cand_id, cap));
+    A(dalloc(&x->loc_count, 4)); A(dalloc(&x->loc_s, sem)); A(dalloc(&x->loc_id, sem));
+    A(dalloc(&x->gat_s, sem * R)); A(dalloc(&x->gat_id, sem * R));
+    A(dalloc(&x->sem_ids, sem)); A(dalloc(&x->sem_n, 1));
+    A(dalloc(&x->ctx_sel, std::max(1, c.max_ctx))); A(dalloc(&x->ctx_n, 1));
     A(dalloc(&x->part.val, pr * kMaxKP)); A(dalloc(&x->part.id, pr * kMaxKP));
     A(dalloc(&x->part.m, pr)); A(dalloc(&x->part.s, pr)); A(dalloc(&x->part.cnt, pr));
     A(dalloc(&x->flags, 1)); A(dalloc(&x->wmax, 1));
@@ -318,7 +332,7 @@ evospec_status evospec_build_subset(evospec_ctx* ctx, const void* E, int64_t n_e
     cudaStream_t st = (cudaStream_t)stream;
     if (n_static < 0 || (n_static > 0 && !static_ids) || n_seed < 0 || (n_seed > 0 && !seeds))
         return fail(EVOSPEC_EINPUT, "build_subset: bad static / seed arguments");
-    if (p->n_sem < 0 || p->n_sem > c.max_sem || p->n_sem > 16384 || p->n_dyn < 0 || p->per_seed < 0 || p->per_seed > 64 ||
+    if (p->n_sem < 0 || p->n_sem > c.max_sem || p->n_dyn < 0 || p->per_seed < 0 || p->per_seed > 64 ||
         p->n_graph_sem_seeds < 0 || n_seed + std::min(p->n_graph_sem_seeds, p->n_sem) > std::min(c.max_seeds, 128))
         return fail(EVOSPEC_EINPUT, "build_subset: params out of capacity (n_sem <= %d, seeds <= %d, per_seed <= 64)",
                     c.max_sem, std::min(c.max_seeds, 128));
@@ -339,40 +353,37 @@ evospec_status evospec_build_subset(evospec_ctx* ctx, const void* E, int64_t n_e
         return fail(EVOSPEC_EINPUT, "build_subset: a sharded index needs evospec_comm_init");
 
     const int N = p->n_sem;
-    // a2: exact scores + top-N selection
+    // a2: exact fp64 scores (+ fused pass-0 histogram), candidate superset of the top-N
     {
         StageTimer t(ctx, EVOSPEC_STAGE_SCAN, st);
-        launch_sem_scan(E, c.w_dtype, n_e_rows, c.d, q, c.h_dtype, ctx->s64, ctx->key32, st);
+        launch_sem_scan(E, c.w_dtype, n_e_rows, c.d, q, c.h_dtype, ctx->s64, ctx->key32, ctx->hist12, st);
         ctx->launches += 1;
     }
     LAUNCH_CHECK("sem_scan");
     StageTimer t_sel(ctx, EVOSPEC_STAGE_SELECT, st);
     if (full_scan) {
-        ctx->launches += 2;
-        CUDA_TRY(launch_topn_select(ctx->s64, nullptr, n_e_rows, 1, 0, N, ctx->hist, ctx->sel_count, ctx->sel_s,
-                                    ctx->sel_id, st));
-        launch_rank_sort(ctx->sel_s, ctx->sel_id, ctx->sel_count, N, ctx->sem_sorted, st);
-        LAUNCH_CHECK("rank_sort");
+        ctx->launches += 1;
+        CUDA_TRY(launch_topn_cand(ctx->s64, nullptr, n_e_rows, 1, 0, N, ctx->cand_cap, ctx->hist12, ctx->hist,
+                                  ctx->cand_count, ctx->cand_s, ctx->cand_id, st));
     } else {
-        // local top-N (ids = row*R + r), exchange N (s, id) pairs per rank, global top-N
-        ctx->launches += 3;
-        CUDA_TRY(launch_topn_select(ctx->s64, nullptr, n_e_rows, R, r, N, ctx->hist, ctx->sel_count, ctx->sel_s,
-                                    ctx->sel_id, st));
+        // exact local top-N (ids = row*R + r; padded with id -1), all-gather N (s, id) pairs per rank,
+        // candidate superset of the global top-N over the R*N gathered pairs
+        ctx->launches += 2;
+        CUDA_TRY(cudaMemsetAsync(ctx->loc_id, 0xFF, (size_t)N * sizeof(int32_t), st));
+        CUDA_TRY(launch_topn_cand(ctx->s64, nullptr, n_e_rows, R, r, N, N, ctx->hist12, ctx->hist, ctx->loc_count,
+                                  ctx->loc_s, ctx->loc_id, st));
         NcclApi& n = nccl();
         n.GroupStart();
-        ncclResult_t r1 = n.AllGather(ctx->sel_s, ctx->gat_s, (size_t)N, ncclFloat64, ctx->comm, st);
-        ncclResult_t r2 = n.AllGather(ctx->sel_id, ctx->gat_id, (size_t)N, ncclInt32, ctx->comm, st);
+        ncclResult_t r1 = n.AllGather(ctx->loc_s, ctx->gat_s, (size_t)N, ncclFloat64, ctx->comm, st);
+        ncclResult_t r2 = n.AllGather(ctx->loc_id, ctx->gat_id, (size_t)N, ncclInt32, ctx->comm, st);
         ncclResult_t r3 = n.GroupEnd();
         if (r1 != ncclSuccess || r2 != ncclSuccess || r3 != ncclSuccess)
             return fail(EVOSPEC_ENCCL, "build_subset all-gather failed");
-        CUDA_TRY(launch_topn_select(ctx->gat_s, ctx->gat_id, (int64_t)N * R, 0, 0, N, ctx->hist, ctx->gat_count,
-                                    ctx->sel2_s, ctx->sel2_id, st));
-        launch_rank_sort(ctx->sel2_s, ctx->sel2_id, ctx->gat_count, N, ctx->sem_sorted, st);
-        LAUNCH_CHECK("rank_sort");
+        CUDA_TRY(launch_topn_cand(ctx->gat_s, ctx->gat_id, (int64_t)N * R, 0, 0, N, ctx->cand_cap, nullptr, ctx->hist,
+                                  ctx->cand_count, ctx->cand_s, ctx->cand_id, st));
     }
     t_sel.stop();
     ctx->last_n_sem = N;
-    const int* n_sem_dev = full_scan ? ctx->sel_count : ctx->gat_count;
     // a3 context counts (optional)
     const bool use_ctx = p->ctx_min_count > 0 && p->n_ctx_max > 0 && n_ctx > 0;
     StageTimer t_union(ctx, EVOSPEC_STAGE_UNION, st);
@@ -382,17 +393,18 @@ evospec_status evospec_build_subset(evospec_ctx* ctx, const void* E, int64_t n_e
                           ctx->ctx_n, ctx->flags, st);
         LAUNCH_CHECK("ctx_select");
     }
-    // a3/a4 formation, cap, union
-    launch_union(c.V, static_ids, n_static, seeds, n_seed, ctx->sem_sorted, n_sem_dev, N, row_ptr, col,
-                 use_ctx ? ctx->ctx_sel : nullptr, ctx->ctx_n, p->n_graph_sem_seeds, p->per_seed, p->n_dyn, R, r,
-                 out_ids, out_n, out_local_ids, out_local_n, c.debug_checks, ctx->flags, st);
+    // a2 exact S_sem + a3/a4 formation, cap, union
+    launch_union(c.V, static_ids, n_static, seeds, n_seed, ctx->cand_s, ctx->cand_id, ctx->cand_count, ctx->cand_cap,
+                 N, row_ptr, col, use_ctx ? ctx->ctx_sel : nullptr, ctx->ctx_n, p->n_graph_sem_seeds, p->per_seed,
+                 p->n_dyn, R, r, out_ids, out_n, out_local_ids, out_local_n, ctx->sem_ids, ctx->sem_n,
+                 c.debug_checks, ctx->flags, st);
     LAUNCH_CHECK("union");
     return EVOSPEC_OK;
 }
 
 evospec_status evospec_last_semantic(evospec_ctx* ctx, int32_t* out_dev, int32_t n, void* stream) {
     if (!ctx || !out_dev || n < 0 || n > ctx->cfg.max_sem) return fail(EVOSPEC_EINPUT, "last_semantic: bad argument");
-    CUDA_TRY(cudaMemcpyAsync(out_dev, ctx->sem_sorted, (size_t)n * 4, cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+    CUDA_TRY(cudaMemcpyAsync(out_dev, ctx->sem_ids, (size_t)n * 4, cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
     return EVOSPEC_OK;
 }
 

@@ -62,9 +62,19 @@ lmh_finalize_kernel(LmhArgs a, int n_cta, int k, float gamma, const float* __res
     if (lane == 0) red_m[warp] = M;
     {   // ||h_r||^2 by all threads (independent loads), fp64
         double acc = 0.0;
-        for (int col = threadIdx.x; col < a.d; col += blockDim.x) {
-            const double h = load_elem(a.H, a.h_dtype, (size_t)r * a.d + col);
-            acc = fma(h, h, acc);
+        if (a.h_dtype == 0 && a.d % 8 == 0) {
+            const uint4* hp = (const uint4*)((const uint16_t*)a.H + (size_t)r * a.d);
+            for (int c = threadIdx.x; c < a.d / 8; c += blockDim.x) {
+                float f[8];
+                unpack_bf16x8(hp[c], f);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) acc = fma((double)f[j], (double)f[j], acc);
+            }
+        } else {
+            for (int col = threadIdx.x; col < a.d; col += blockDim.x) {
+                const double h = load_elem(a.H, a.h_dtype, (size_t)r * a.d + col);
+                acc = fma(h, h, acc);
+            }
         }
         acc = warp_sum_d(acc);
         if (lane == 0) red_d[warp] = acc;
@@ -161,8 +171,31 @@ lmh_finalize_kernel(LmhArgs a, int n_cta, int k, float gamma, const float* __res
         const int c = need_list[q];
         const size_t row = (size_t)(c_id[c] / a.R);
         double acc = 0.0;
-        for (int col = lane; col < a.d; col += 32)
-            acc = fma(load_elem(a.W, a.w_dtype, row * a.d + col), load_elem(a.H, a.h_dtype, (size_t)r * a.d + col), acc);
+        if (a.w_dtype == 0 && a.h_dtype == 0 && a.d % 8 == 0) {   // 16-byte loads, 4 in flight per lane
+            const uint4* wp = (const uint4*)((const uint16_t*)a.W + row * a.d);
+            const uint4* hp = (const uint4*)((const uint16_t*)a.H + (size_t)r * a.d);
+            const int nc = a.d / 8;
+            for (int c0 = lane; c0 < nc; c0 += 32 * 4) {
+                uint4 wv[4], hv[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int cc = c0 + 32 * u;
+                    wv[u] = cc < nc ? wp[cc] : make_uint4(0, 0, 0, 0);
+                    hv[u] = cc < nc ? hp[cc] : make_uint4(0, 0, 0, 0);
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    float fw[8], fh[8];
+                    unpack_bf16x8(wv[u], fw);
+                    unpack_bf16x8(hv[u], fh);
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) acc = fma((double)fw[j], (double)fh[j], acc);
+                }
+            }
+        } else {
+            for (int col = lane; col < a.d; col += 32)
+                acc = fma(load_elem(a.W, a.w_dtype, row * a.d + col), load_elem(a.H, a.h_dtype, (size_t)r * a.d + col), acc);
+        }
         acc = warp_sum_d(acc);
         if (lane == 0) c_e[c] = acc * (double)a.inv_temp;
     }
@@ -224,23 +257,30 @@ merge_kernel(int R, int n_h, int k, const int32_t* __restrict__ ids, const float
     const float L = sig > 0.0f ? M + logf(sig) : -INFINITY;
     if (lane == 0 && out_lse) out_lse[r] = L;
     const int nc = R * k;
-    unsigned long long taken = 0;  // per-lane bitmask over its candidates (<= 64 per lane)
+    extern __shared__ unsigned char m_sm[];
+    float* sv = (float*)m_sm + (size_t)warp_id() * nc * 2;
+    int* si = (int*)(sv + nc);
+    for (int c = lane; c < nc; c += 32) {          // independent loads, then smem only
+        const int t = c / k, j = c - t * k;
+        const size_t o = ((size_t)t * n_h + r) * k + j;
+        si[c] = ids[o];
+        sv[c] = vals[o];
+    }
+    __syncwarp();
     for (int i = 0; i < k; ++i) {
         float bv = -INFINITY;
-        int bid = 0x7fffffff, bslot = -1;
-        for (int c = lane, q = 0; c < nc; c += 32, ++q) {
-            if ((taken >> q) & 1ull) continue;
-            const int t = c / k, j = c % k;
-            const size_t o = ((size_t)t * n_h + r) * k + j;
-            const int id = ids[o];
-            if (id < 0) continue;
-            const float v = vals[o];
-            if (before(v, id, bv, bid)) { bv = v; bid = id; bslot = q; }
+        int bid = 0x7fffffff, bc = -1;
+        for (int c = lane; c < nc; c += 32) {
+            const int id = si[c];
+            if (id < 0) continue;                     // padding or taken
+            if (before(sv[c], id, bv, bid)) { bv = sv[c]; bid = id; bc = c; }
         }
+        const int my = bid;
         float wv = bv;
         int wid = bid;
         warp_argbest(wv, wid);
-        if (wid != 0x7fffffff && wid == bid && bslot >= 0 && wv == bv) taken |= 1ull << bslot;
+        if (bc >= 0 && my == wid) si[bc] = -2;       // ids are unique across shards
+        __syncwarp();
         if (lane == 0) {
             const size_t o = (size_t)r * k + i;
             out_ids[o] = wid == 0x7fffffff ? -1 : wid;
@@ -254,7 +294,9 @@ void launch_merge(int R, int n_h, int k, const int32_t* ids, const float* vals, 
                   const float* s, int32_t* out_ids, float* out_vals, float* out_lse, float* out_probs,
                   cudaStream_t st) {
     const int grid = (n_h + 7) / 8;
-    merge_kernel<<<grid, 256, 0, st>>>(R, n_h, k, ids, vals, m, s, out_ids, out_vals, out_lse, out_probs);
+    const size_t smem = (size_t)8 * R * k * 8;
+    cudaFuncSetAttribute(merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    merge_kernel<<<grid, 256, smem, st>>>(R, n_h, k, ids, vals, m, s, out_ids, out_vals, out_lse, out_probs);
 }
 
 // ------------------------------------------------------------ helpers

@@ -8,10 +8,8 @@
 namespace es {
 
 constexpr int kScanWarps = 16;      // sem scan: warps per CTA (1 CTA / SM)
-constexpr int kSelThreads = 512;    // topn select (cooperative), 2048 bins = 4 / thread
-constexpr int kRankThreads = 512;
-constexpr int kRankTile = 4096;
-constexpr int kRankMaxPerWarp = 8;
+constexpr int kSelThreads = 512;    // topn candidates (cooperative), 4096 bins = 8 / thread
+constexpr int kHistBins = 4096;     // top 12 bits of the fp32 score key
 constexpr int kUnionThreads = 1024;
 constexpr int kTopkPad = 8;         // extra fp32 candidates kept per row for the exact re-score
 constexpr int kMaxK = 64;
@@ -26,23 +24,22 @@ constexpr int kFlagBudget = 0x8;
 
 // ---- semantic (sem.cu)
 void launch_sem_scan(const void* E, int e_dtype, int64_t n_rows, int d, const void* q, int q_dtype,
-                     double* s64, uint32_t* key32, cudaStream_t st);
-cudaError_t launch_topn_select(const double* s64, const int32_t* ids, int64_t n, int id_mul, int id_add,
-                               int N, uint32_t* hist_g, int* out_count, double* out_s, int32_t* out_id,
-                               cudaStream_t st);
-void launch_rank_sort(const double* s, const int32_t* id, const int* n_dev, int n_max, int32_t* out_ids,
-                      cudaStream_t st);
+                     double* s64, uint32_t* key32, uint32_t* hist12, cudaStream_t st);
+cudaError_t launch_topn_cand(const double* s64, const int32_t* ids, int64_t n, int id_mul, int id_add,
+                             int N, int cap, const uint32_t* hist_pre, uint32_t* hist_g, int* out_count,
+                             double* out_s, int32_t* out_id, cudaStream_t st);
 
 // ---- union / formation (union.cu)
 void launch_ctx_select(const int32_t* ctx, int n_ctx, int V, int min_count, int n_max,
                        int32_t* out, int* out_n, int* flags, cudaStream_t st);
+int union_cand_cap(int V, int per_seed);
 void launch_union(int V, const int32_t* static_ids, int n_static, const int32_t* seeds, int n_seed,
-                  const int32_t* sem_sorted, const int* n_sem_dev, int n_sem_max,
+                  const double* cand_s, const int32_t* cand_id, const int* n_cand_dev, int cap, int n_sem,
                   const int32_t* row_ptr, const int32_t* col,
                   const int32_t* ctx_sel, const int* n_ctx_sel_dev,
                   int n_graph_sem_seeds, int per_seed, int n_dyn, int R, int r,
                   int32_t* out_ids, int32_t* out_n, int32_t* out_local, int32_t* out_local_n,
-                  int debug, int* flags, cudaStream_t st);
+                  int32_t* sem_out, int* sem_out_n, int debug, int* flags, cudaStream_t st);
 
 // ---- LM head (lmh_gemv.cu, lmh_tc.cu)
 struct LmhPartials {

@@ -28,9 +28,16 @@
 
 namespace es {
 
-constexpr int kTcWarps = 10;
+// W-operand producer: 4 warps of 16-byte cp.async (LDGSTS) with the 128B
+// swizzle applied in the address, one mbarrier arrival per thread
+// (cp.async.mbarrier.arrive.noinc). The TMA tile::gather4 producer (one warp)
+// is kept for comparison: it is issue-bound at ~1.6 TB/s for 128-byte rows
+// (profiles/r01_*), while LDGSTS streams the same gathered rows at HBM rate.
+constexpr int kProdWarps = 4;
+constexpr int kTcMmaWarp = kProdWarps;
+constexpr int kTcEpiWarp0 = kProdWarps + 1;
 constexpr int kTcEpiWarps = 8;
-constexpr int kTcEpiWarp0 = 2;
+constexpr int kTcWarps = kProdWarps + 1 + kTcEpiWarps;
 constexpr int kBlockK = 64;        // bf16 columns per stage = one 128-byte swizzle atom row
 constexpr int kTileM = 128;
 
@@ -73,6 +80,13 @@ ES_DEV void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0
         " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
         "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "l"(policy)
         : "memory");
+}
+ES_DEV void cp_async16(uint32_t dst, const void* src, uint64_t policy) {
+    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "l"(policy)
+                 : "memory");
+}
+ES_DEV void cp_async_arrive_noinc(uint64_t* bar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 ES_DEV uint64_t policy_evict_first() {
     uint64_t p;
@@ -168,11 +182,11 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
     if (warp == 0 && lane == 0) {
         asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap_w) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap_h) : "memory");
-        for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+        for (int s = 0; s < S; ++s) { mbar_init(&full[s], kProdWarps * 32 + 1); mbar_init(&empty[s], 1); }
         for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], kTcEpiWarps * 32); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (warp == 1) {
+    if (warp == kTcMmaWarp) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                      "r"(tp.tmem_cols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -190,34 +204,42 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
         tn = a1 - a0;
     };
 
-    if (warp == 0) {
-        // ===== TMA producer (whole warp: lane j gathers rows 4j..4j+3)
+    if (warp < kProdWarps) {
+        // ===== producers: W rows by 16-byte cp.async into the swizzled stage,
+        // H by one 2D TMA tile (rows >= n_h zero-filled) per stage.
+        // Thread (w, l) copies chunk l&7 of tile rows 16 i + 4 w + (l >> 3), i < 8:
+        // one warp instruction moves 4 whole 128-byte row segments.
         const uint64_t pol_w = policy_evict_first(), pol_h = policy_evict_last();
-        const uint32_t stage_bytes = (uint32_t)(kTileM * 128 + NP * 128);
+        const int chunk = lane & 7;
         int stage = 0;
         uint32_t phase = 0;
         for (int t = 0; t < n_tiles; ++t) {
             int t0, tn;
             tile_range(t, t0, tn);
-            int rr[4];
+            const char* src[8];
+            uint32_t dsto[8];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const int p = 4 * lane + i;
-                const int pos = t0 + (p < tn ? p : 0);
-                rr[i] = a.subset[pos] / a.R;
+            for (int i = 0; i < 8; ++i) {
+                const int row = 16 * i + 4 * warp + (lane >> 3);
+                const int pos = t0 + (row < tn ? row : 0);
+                src[i] = (const char*)a.W + (size_t)(a.subset[pos] / a.R) * (size_t)a.d * 2 + chunk * 16;
+                dsto[i] = (uint32_t)(row * 128 + ((chunk ^ (row & 7)) << 4));
             }
             for (int kb = 0; kb < tp.nkb; ++kb) {
                 mbar_wait(&empty[stage], phase ^ 1);
-                if (lane == 0) mbar_arrive_expect_tx(&full[stage], stage_bytes);
-                __syncwarp();
-                unsigned char* dA = smA + (size_t)stage * kTileM * 128;
-                tma_gather4(dA + lane * 512, &tmap_w, &full[stage], kb * kBlockK, rr[0], rr[1], rr[2], rr[3], pol_w);
-                if (lane == 0)
+                if (warp == 0 && lane == 0) {
+                    mbar_arrive_expect_tx(&full[stage], (uint32_t)(NP * 128));
                     tma_load_2d(smB + (size_t)stage * NP * 128, &tmap_h, &full[stage], kb * kBlockK, 0, pol_h);
+                }
+                const uint32_t dA = smem_u32(smA + (size_t)stage * kTileM * 128);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) cp_async16(dA + dsto[i], src[i] + kb * 128, pol_w);
+                cp_async_arrive_noinc(&full[stage]);
                 if (++stage == S) { stage = 0; phase ^= 1; }
             }
         }
-    } else if (warp == 1) {
+        (void)tmap_w;
+    } else if (warp == kTcMmaWarp) {
         // ===== MMA issuer
         const uint32_t idesc = idesc_bf16(kTileM, NP);
         int stage = 0;
@@ -246,7 +268,7 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
             }
         }
     } else {
-        // ===== epilogue warps 2..9: TMEM lane quadrant = warp % 4; the two
+        // ===== epilogue warps: TMEM lane quadrant = warp % 4; the two
         // warps of a quadrant split the accumulator columns (16-column chunks)
         const int ew = warp - kTcEpiWarp0;          // 0..7
         const int quad = warp & 3;
@@ -283,7 +305,7 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    if (warp == 1)
+    if (warp == kTcMmaWarp)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(tp.tmem_cols));
 }
 

@@ -11,12 +11,18 @@
 //                       are exact in fp64), one warp per 16-row chunk, 16-byte
 //                       streaming loads, q held per lane from a lane-interleaved
 //                       fp64 copy in shared memory.
-//   topn_select_kernel  cooperative radix select of the N largest composite
-//                       keys (float_key(s), double_key(s), ~id): 3 passes on the
-//                       fp32 key settle almost every case; further passes run
-//                       only when the boundary holds fp32-equal scores.
-//   rank_sort_kernel    exact order (s64 desc, id asc) of the N selected by
-//                       counting, one warp per element, lanes split the scan.
+//                       The scan also histograms the top 12 bits of the
+//                       order-preserving fp32 key of every score.
+//   topn_cand_kernel    cooperative radix select over the composite key
+//                       (float_key(s), double_key(s), ~id). Pass 0 reuses the
+//                       scan's histogram, so in the common case no grid-wide
+//                       sync runs: every CTA finds the boundary bin b and emits
+//                       all scores in bins >= b -- a candidate SUPERSET of the
+//                       top-N of at most `cap` elements, carrying exact keys.
+//                       Further passes (grid.sync) run only if that superset
+//                       would not fit. The exact top-N, its order where the
+//                       formation needs it, and the cap are resolved in the
+//                       union kernel (union.cu) on those exact keys.
 #include <cooperative_groups.h>
 
 #include "common.cuh"
@@ -33,12 +39,14 @@ namespace es {
 template <int DT>  // element type of E: 0 bf16, 1 fp32
 __global__ void __launch_bounds__(kScanWarps * 32, 1)
 sem_scan_kernel(const void* __restrict__ E, int64_t n_rows, int d,
-                const void* __restrict__ q, int q_dtype, int id_mul, int id_add,
+                const void* __restrict__ q, int q_dtype, uint32_t* __restrict__ hist12,
                 double* __restrict__ s64, uint32_t* __restrict__ key32) {
     constexpr int ELEMS = DT == 0 ? 8 : 4;           // elements per 16 bytes
     constexpr int SLAB = 32 * ELEMS;                  // columns per slab
     extern __shared__ double q_sm[];                  // [n_slabs][ELEMS][32]
+    __shared__ uint32_t hist_sm[kHistBins];           // top-12-bit histogram of key32
     const int n_slabs = (d + SLAB - 1) / SLAB;
+    for (int i = threadIdx.x; i < kHistBins; i += blockDim.x) hist_sm[i] = 0;
     // stage q as fp64 in the lane-interleaved layout (exact: q is bf16/fp32)
     for (int i = threadIdx.x; i < n_slabs * SLAB; i += blockDim.x) {
         int s = i / SLAB, within = i % SLAB, lane = within / ELEMS, j = within % ELEMS;
@@ -103,25 +111,33 @@ sem_scan_kernel(const void* __restrict__ E, int64_t n_rows, int d,
         }
         double tot = acc[0] + __shfl_xor_sync(0xffffffffu, acc[0], 16);
         int64_t row = base + (lane & 15);
+        uint32_t digit = 0xFFFFFFFFu;
         if (lane < 16 && row < r1) {
+            const uint32_t k = float_key((float)tot);
             s64[row] = tot;
-            key32[row] = float_key((float)tot);
+            key32[row] = k;
+            digit = k >> 20;
         }
-        (void)id_mul; (void)id_add;
+        const unsigned peers = __match_any_sync(0xffffffffu, digit);
+        if (digit != 0xFFFFFFFFu && lane == __ffs(peers) - 1) atomicAdd(&hist_sm[digit], (uint32_t)__popc(peers));
     }
+    __syncthreads();
+    for (int i = threadIdx.x; i < kHistBins; i += blockDim.x)
+        if (hist_sm[i]) atomicAdd(&hist12[i], hist_sm[i]);
 }
 
 void launch_sem_scan(const void* E, int e_dtype, int64_t n_rows, int d, const void* q, int q_dtype,
-                     double* s64, uint32_t* key32, cudaStream_t st) {
+                     double* s64, uint32_t* key32, uint32_t* hist12, cudaStream_t st) {
+    cudaMemsetAsync(hist12, 0, kHistBins * sizeof(uint32_t), st);
     const int elems = e_dtype == 0 ? 8 : 4;
     const int n_slabs = (d + 32 * elems - 1) / (32 * elems);
     const size_t smem = (size_t)n_slabs * 32 * elems * sizeof(double);
     if (e_dtype == 0) {
         cudaFuncSetAttribute(sem_scan_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        sem_scan_kernel<0><<<kNumSMs, kScanWarps * 32, smem, st>>>(E, n_rows, d, q, q_dtype, 1, 0, s64, key32);
+        sem_scan_kernel<0><<<kNumSMs, kScanWarps * 32, smem, st>>>(E, n_rows, d, q, q_dtype, hist12, s64, key32);
     } else {
         cudaFuncSetAttribute(sem_scan_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        sem_scan_kernel<1><<<kNumSMs, kScanWarps * 32, smem, st>>>(E, n_rows, d, q, q_dtype, 1, 0, s64, key32);
+        sem_scan_kernel<1><<<kNumSMs, kScanWarps * 32, smem, st>>>(E, n_rows, d, q, q_dtype, hist12, s64, key32);
     }
 }
 
@@ -160,171 +176,139 @@ ES_DEV bool sel_selected(const SelWords& k, const SelState& st) {
     return true;
 }
 
+// digit schedule: word 0 (fp32 key) 12/10/10 bits -- pass 0 matches the
+// scan's 4096-bin histogram; words 1-3: 11/11/10 bits.
+ES_DEV void pass_digit(int pass, int& word, int& shift, int& nbits) {
+    word = pass / 3;
+    const int part = pass % 3;
+    if (word == 0) { shift = part == 0 ? 20 : (part == 1 ? 10 : 0); nbits = part == 0 ? 12 : 10; }
+    else { shift = part == 0 ? 21 : (part == 1 ? 10 : 0); nbits = part == 2 ? 10 : 11; }
+}
+
 __global__ void __launch_bounds__(kSelThreads, 1)
-topn_select_kernel(const double* __restrict__ s64, const int32_t* __restrict__ ids, int64_t n,
-                   int id_mul, int id_add, int N, uint32_t* __restrict__ hist_g,
-                   int* __restrict__ out_count, double* __restrict__ out_s, int32_t* __restrict__ out_id) {
+topn_cand_kernel(const double* __restrict__ s64, const int32_t* __restrict__ ids, int64_t n,
+                 int id_mul, int id_add, int N, int cap, const uint32_t* __restrict__ hist_pre,
+                 uint32_t* __restrict__ hist_g, int* __restrict__ out_count, double* __restrict__ out_s,
+                 int32_t* __restrict__ out_id) {
     cg::grid_group grid = cg::this_grid();
-    __shared__ uint32_t hist[2048];
-    __shared__ uint32_t suffix_warp[kSelThreads / 32];
+    __shared__ uint32_t hist[kHistBins];
+    __shared__ uint32_t warp_sum_s[kSelThreads / 32];
     __shared__ SelState st;
     __shared__ int found_bin, found_above;
 
     const int64_t lo = n * blockIdx.x / gridDim.x, hi = n * (blockIdx.x + 1) / gridDim.x;
     auto id_of = [&](int64_t i) -> int32_t { return ids ? ids[i] : (int32_t)(i * id_mul + id_add); };
+    const int lane = lane_id(), wid = warp_id();
 
     if (threadIdx.x == 0) {
         for (int w = 0; w < 4; ++w) { st.pmask[w] = 0; st.pval[w] = 0; }
-        st.remaining = N;
+        st.remaining = N < 0 ? 0 : N;
         st.done = (N >= n) || (N <= 0);
-        if (N <= 0) st.remaining = 0;
     }
     __syncthreads();
 
     for (int pass = 0; pass < 12 && !st.done; ++pass) {
-        const int word = pass / 3, part = pass % 3;
-        const int shift = part == 0 ? 21 : (part == 1 ? 10 : 0);
-        const int nbits = part == 2 ? 10 : 11;
+        int word, shift, nbits;
+        pass_digit(pass, word, shift, nbits);
         const uint32_t dmask = (1u << nbits) - 1u;
-        for (int b = threadIdx.x; b < 2048; b += blockDim.x) hist[b] = 0;
-        __syncthreads();
-        SelState my = st;
-        for (int64_t b0 = lo; b0 < hi; b0 += blockDim.x) {   // uniform trip count per warp
-            const int64_t i = b0 + threadIdx.x;
-            uint32_t digit = 0xFFFFFFFFu;
-            if (i < hi) {
-                SelWords k = sel_words(s64[i], id_of(i));
-                if (sel_matches(k, my)) digit = (k.w[word] >> shift) & dmask;
+        const uint32_t* hp;
+        if (pass == 0 && hist_pre) {
+            hp = hist_pre;
+        } else {
+            for (int b = threadIdx.x; b < kHistBins; b += blockDim.x) hist[b] = 0;
+            __syncthreads();
+            SelState my = st;
+            for (int64_t b0 = lo; b0 < hi; b0 += blockDim.x) {   // uniform trip count per warp
+                const int64_t i = b0 + threadIdx.x;
+                uint32_t digit = 0xFFFFFFFFu;
+                if (i < hi && id_of(i) >= 0) {
+                    SelWords k = sel_words(s64[i], id_of(i));
+                    if (sel_matches(k, my)) digit = (k.w[word] >> shift) & dmask;
+                }
+                const unsigned peers = __match_any_sync(0xffffffffu, digit);
+                if (digit != 0xFFFFFFFFu && lane == __ffs(peers) - 1) atomicAdd(&hist[digit], (uint32_t)__popc(peers));
             }
-            // warp-aggregated increments: scores cluster in few bins
-            const unsigned peers = __match_any_sync(0xffffffffu, digit);
-            if (digit != 0xFFFFFFFFu && lane_id() == __ffs(peers) - 1) atomicAdd(&hist[digit], (uint32_t)__popc(peers));
+            __syncthreads();
+            uint32_t* hw = hist_g + (size_t)pass * kHistBins;
+            for (int b = threadIdx.x; b < (1 << nbits); b += blockDim.x)
+                if (hist[b]) atomicAdd(&hw[b], hist[b]);
+            grid.sync();
+            hp = hw;
         }
-        __syncthreads();
-        uint32_t* hp = hist_g + (size_t)pass * 2048;
-        for (int b = threadIdx.x; b < 2048; b += blockDim.x)
-            if (hist[b]) atomicAdd(&hp[b], hist[b]);
-        grid.sync();
-        // every CTA: find bin b* (descending) where the running count reaches `remaining`
-        // thread t owns bins [4t, 4t+4)
-        uint32_t c[4], tot = 0;
-        const int t = threadIdx.x;  // kSelThreads == 512 -> 2048 bins
+        // every CTA: the bin (descending) where the running count reaches `remaining`;
+        // thread t owns bins [8t, 8t+8)
+        constexpr int BPT = kHistBins / kSelThreads;
+        uint32_t c[BPT], tot = 0;
+        const int t = threadIdx.x;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) { c[j] = __ldcg(&hp[4 * t + j]); tot += c[j]; }
-        // suffix sum over threads: count of bins strictly above thread t's range
-        // warp-level inclusive suffix scan
+        for (int j = 0; j < BPT; ++j) {
+            const int b = BPT * t + j;
+            c[j] = b < (1 << nbits) ? __ldcg(&hp[b]) : 0u;
+            tot += c[j];
+        }
         uint32_t inc = tot;
-        const int lane = lane_id(), wid = warp_id();
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             uint32_t v = __shfl_down_sync(0xffffffffu, inc, o);
             if (lane + o < 32) inc += v;
         }
-        if (lane == 0) suffix_warp[wid] = inc;   // total of warp
+        if (lane == 0) warp_sum_s[wid] = inc;
         __syncthreads();
         uint32_t above_w = 0;
-        for (int w2 = wid + 1; w2 < kSelThreads / 32; ++w2) above_w += suffix_warp[w2];
-        uint32_t above = above_w + inc - tot;     // bins strictly above this thread's range
+        for (int w2 = wid + 1; w2 < kSelThreads / 32; ++w2) above_w += warp_sum_s[w2];
         const uint32_t rem = (uint32_t)st.remaining;
-        uint32_t run = above;
+        uint32_t run = above_w + inc - tot;   // count in bins above this thread's range
 #pragma unroll
-        for (int j = 3; j >= 0; --j) {
-            if (run < rem && run + c[j] >= rem) { found_bin = 4 * t + j; found_above = (int)run; }
+        for (int j = BPT - 1; j >= 0; --j) {
+            if (run < rem && run + c[j] >= rem) { found_bin = BPT * t + j; found_above = (int)run; }
             run += c[j];
         }
         __syncthreads();
         if (threadIdx.x == 0) {
             const int b = found_bin;
+            const uint32_t in_bin = __ldcg(&hp[b]);
+            const long long superset = (long long)(N - st.remaining) + found_above + in_bin;
             st.remaining -= found_above;
             st.pmask[word] |= dmask << shift;
             st.pval[word] |= ((uint32_t)b) << shift;
-            if ((uint32_t)st.remaining == __ldcg(&hp[b])) st.done = 1;
+            // exact, or a candidate superset (everything in bins >= b) that fits
+            if ((uint32_t)st.remaining == in_bin || superset <= cap) st.done = 1;
         }
         __syncthreads();
     }
-    // compaction (order arbitrary; the rank sort fixes it)
+    // compaction: warp-aggregated appends of (double_key(s), id)
     SelState my = st;
     const bool take_all = (N >= n);
-    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-        double s = s64[i];
-        int32_t id = id_of(i);
-        bool sel = take_all || (N > 0 && sel_selected(sel_words(s, id), my));
-        if (sel) {
-            int o = atomicAdd(out_count, 1);
-            if (o < N || take_all) { out_s[o] = s; out_id[o] = id; }
+    for (int64_t b0 = lo; b0 < hi; b0 += blockDim.x) {
+        const int64_t i = b0 + threadIdx.x;
+        bool sel = false;
+        double s = 0.0;
+        int32_t id = 0;
+        if (i < hi) {
+            s = s64[i];
+            id = id_of(i);
+            sel = id >= 0 && (take_all || (N > 0 && sel_selected(sel_words(s, id), my)));
         }
+        const unsigned m = __ballot_sync(0xffffffffu, sel);
+        int base = 0;
+        if (lane == 0 && m) base = atomicAdd(out_count, __popc(m));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        const int o = base + __popc(m & ((1u << lane) - 1u));
+        if (sel && o < cap) { out_s[o] = s; out_id[o] = id; }
     }
 }
 
-cudaError_t launch_topn_select(const double* s64, const int32_t* ids, int64_t n, int id_mul, int id_add,
-                               int N, uint32_t* hist_g, int* out_count, double* out_s, int32_t* out_id,
-                               cudaStream_t st) {
-    cudaMemsetAsync(hist_g, 0, 12 * 2048 * sizeof(uint32_t), st);
+cudaError_t launch_topn_cand(const double* s64, const int32_t* ids, int64_t n, int id_mul, int id_add,
+                             int N, int cap, const uint32_t* hist_pre, uint32_t* hist_g, int* out_count,
+                             double* out_s, int32_t* out_id, cudaStream_t st) {
+    cudaMemsetAsync(hist_g, 0, 12 * kHistBins * sizeof(uint32_t), st);
     cudaMemsetAsync(out_count, 0, sizeof(int), st);
     int grid = kNumSMs;
     if (n < (int64_t)grid * 64) grid = (int)((n + 63) / 64);
     if (grid < 1) grid = 1;
-    void* args[] = {(void*)&s64, (void*)&ids, (void*)&n, (void*)&id_mul, (void*)&id_add, (void*)&N,
-                    (void*)&hist_g, (void*)&out_count, (void*)&out_s, (void*)&out_id};
-    return cudaLaunchCooperativeKernel((void*)topn_select_kernel, grid, kSelThreads, args, 0, st);
-}
-
-// ---------------------------------------------------------------- rank sort
-// out_ids[rank(i)] = id_i with rank(i) = #{j : (s_j, id_j) before (s_i, id_i)}.
-__global__ void __launch_bounds__(kRankThreads)
-rank_sort_kernel(const double* __restrict__ s, const int32_t* __restrict__ id, const int* __restrict__ n_dev,
-                 int n_max, int32_t* __restrict__ out_ids) {
-    extern __shared__ unsigned char rs_sm[];
-    const int n = min(*n_dev, n_max);
-    constexpr int TILE = kRankTile;
-    double* ts = (double*)rs_sm;
-    int32_t* ti = (int32_t*)(ts + TILE);
-    const int lane = lane_id();
-    const int nwarps = blockDim.x / 32;
-    // each warp owns elements e = blockIdx.x*nwarps + w, stepping by grid*nwarps
-    const int first = blockIdx.x * nwarps + warp_id();
-    const int step = gridDim.x * nwarps;
-    const int per_warp = (n + step - 1) / step;  // <= 64 kept in registers below
-    int cnt[kRankMaxPerWarp];
-    double my_s[kRankMaxPerWarp];
-    int32_t my_id[kRankMaxPerWarp];
-#pragma unroll
-    for (int e = 0; e < kRankMaxPerWarp; ++e) {
-        cnt[e] = 0;
-        int idx = first + e * step;
-        if (e < per_warp && idx < n) { my_s[e] = s[idx]; my_id[e] = id[idx]; }
-        else { my_s[e] = -INFINITY; my_id[e] = 0x7fffffff; }
-    }
-    for (int t0 = 0; t0 < n; t0 += TILE) {
-        const int tn = min(TILE, n - t0);
-        __syncthreads();
-        for (int j = threadIdx.x; j < tn; j += blockDim.x) { ts[j] = s[t0 + j]; ti[j] = id[t0 + j]; }
-        __syncthreads();
-        for (int j = lane; j < tn; j += 32) {
-            const double sj = ts[j];
-            const int32_t ij = ti[j];
-#pragma unroll
-            for (int e = 0; e < kRankMaxPerWarp; ++e)
-                if (e < per_warp) cnt[e] += before(sj, ij, my_s[e], my_id[e]) ? 1 : 0;
-        }
-    }
-#pragma unroll
-    for (int e = 0; e < kRankMaxPerWarp; ++e) {
-        if (e >= per_warp) break;
-        int c = warp_sum_i(cnt[e]);
-        int idx = first + e * step;
-        if (lane == 0 && idx < n) out_ids[c] = my_id[e];
-    }
-}
-
-void launch_rank_sort(const double* s, const int32_t* id, const int* n_dev, int n_max, int32_t* out_ids,
-                      cudaStream_t st) {
-    const int nwarps = kRankThreads / 32;
-    int grid = (n_max + nwarps * kRankMaxPerWarp - 1) / (nwarps * kRankMaxPerWarp);
-    if (grid < kNumSMs) grid = std::max(1, std::min(kNumSMs, (n_max + nwarps - 1) / nwarps));
-    const size_t smem = (size_t)kRankTile * (sizeof(double) + sizeof(int32_t));
-    cudaFuncSetAttribute(rank_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    rank_sort_kernel<<<grid, kRankThreads, smem, st>>>(s, id, n_dev, n_max, out_ids);
+    void* args[] = {(void*)&s64, (void*)&ids, (void*)&n, (void*)&id_mul, (void*)&id_add, (void*)&N, (void*)&cap,
+                    (void*)&hist_pre, (void*)&hist_g, (void*)&out_count, (void*)&out_s, (void*)&out_id};
+    return cudaLaunchCooperativeKernel((void*)topn_cand_kernel, grid, kSelThreads, args, 0, st);
 }
 
 }  // namespace es

@@ -3,18 +3,20 @@
 // P:88-93; formation App. A.3; budget |V_t \ V_static| <= N_dyn,
 // Eq. optimization; cap order S:260; readings C4-C9).
 //
-// One CTA: the candidate list is at most a few thousand ids and the answer
-// is a V-bit membership bitmap in shared memory (16 KB at V = 128k), so a
-// single SM does the whole step in a few microseconds:
+// One CTA: the semantic candidates (an exact-keyed superset of S_sem from
+// sem.cu), the answer as a V-bit membership bitmap (16 KB at V = 128k) and
+// the graph lists all live in shared memory:
 //   1. static ids -> bitmap;
-//   2. G = dedupe(seeds ++ S_sem[:n_graph_sem_seeds]); S_graph = the first
-//      per_seed CSR successors of each g in G, in G order;
-//   3. one warp walks  seeds ++ S_sem ++ S_graph ++ S_ctx  32 ids at a time:
-//      an id is taken iff it is not yet a member (static or already taken)
-//      and is the first occurrence inside its 32-wide window (match.any),
-//      until N_dyn ids are taken -- exactly the sequential first-occurrence
-//      walk of the definition;
-//   4. block-wide popcount scan of the bitmap writes the sorted ids (and this
+//   2. S_sem = exact top-N_sem of the candidates (block radix select on
+//      (double_key(s), ~id));
+//   3. the ordered prefix S_sem[:n_graph_sem_seeds] (select + rank);
+//      G = dedupe(seeds ++ that prefix); S_graph = the first per_seed CSR
+//      successors of each g in G, in G order;
+//   4. formation: seeds, then the first (budget) NEW ids of S_sem in S_sem
+//      order (= exact top-budget of the new ones), then S_graph and S_ctx
+//      walked 32 ids at a time (match.any first-occurrence) until N_dyn ids
+//      are taken -- the same set the sequential walk of the definition takes;
+//   5. block-wide popcount scan of the bitmap writes the sorted ids (and this
 //      shard's slice v mod R == r).
 #include "common.cuh"
 #include "kernels.cuh"
@@ -131,54 +133,195 @@ void launch_ctx_select(const int32_t* ctx, int n_ctx, int V, int min_count, int 
 }
 
 // ------------------------------------------------------------ union
+// Block-wide exact top-M (key desc, id asc) among the candidates whose flag
+// has any bit of A; marks them with bit S. Radix select on the 96-bit
+// composite (double_key(s), ~id), 8 bits per pass, exits as soon as the
+// boundary bin is taken whole.
+struct BSel {
+    uint32_t pmask[3], pval[3];
+    int remaining, done, found_bin, found_above;
+};
+
+ES_DEV uint32_t bword(uint64_t k, int32_t id, int w) {
+    return w == 0 ? (uint32_t)(k >> 32) : (w == 1 ? (uint32_t)k : 0xFFFFFFFFu - (uint32_t)id);
+}
+ES_DEV bool bmatch(uint64_t k, int32_t id, const BSel& st) {
+#pragma unroll
+    for (int w = 0; w < 3; ++w)
+        if ((bword(k, id, w) & st.pmask[w]) != st.pval[w]) return false;
+    return true;
+}
+ES_DEV bool bselected(uint64_t k, int32_t id, const BSel& st) {
+#pragma unroll
+    for (int w = 0; w < 3; ++w) {
+        const uint32_t a = bword(k, id, w) & st.pmask[w];
+        if (a != st.pval[w]) return a > st.pval[w];
+    }
+    return true;
+}
+
+ES_DEV int block_count(int v, int* warp_tot) {
+    int total;
+    block_excl_scan(v, warp_tot, total);
+    return total;
+}
+
+ES_DEV void block_topM(const uint64_t* ck, const int32_t* cid, uint8_t* cf, int n, uint8_t A, uint8_t S, int M,
+                       uint32_t* hist, BSel& st, int* warp_tot) {
+    const int tid = threadIdx.x, T = blockDim.x, lane = lane_id();
+    int c = 0;
+    for (int i = tid; i < n; i += T) c += (cf[i] & A) != 0;
+    const int cnt = block_count(c, warp_tot);
+    if (M >= cnt || M <= 0) {
+        if (M > 0)
+            for (int i = tid; i < n; i += T)
+                if (cf[i] & A) cf[i] |= S;
+        __syncthreads();
+        return;
+    }
+    if (tid == 0) {
+        for (int w = 0; w < 3; ++w) { st.pmask[w] = 0; st.pval[w] = 0; }
+        st.remaining = M;
+        st.done = 0;
+    }
+    __syncthreads();
+    for (int pass = 0; pass < 12; ++pass) {
+        if (st.done) break;
+        const int w = pass >> 2, shift = 24 - 8 * (pass & 3);
+        for (int b = tid; b < 256; b += T) hist[b] = 0;
+        __syncthreads();
+        const BSel my = st;
+        for (int base = 0; base < n; base += T) {            // uniform trip count: warp-aggregated adds
+            const int i = base + tid;
+            uint32_t digit = 0xFFFFFFFFu;
+            if (i < n && (cf[i] & A) && bmatch(ck[i], cid[i], my)) digit = (bword(ck[i], cid[i], w) >> shift) & 255u;
+            const unsigned peers = __match_any_sync(0xffffffffu, digit);
+            if (digit != 0xFFFFFFFFu && lane == __ffs(peers) - 1) atomicAdd(&hist[digit], (uint32_t)__popc(peers));
+        }
+        __syncthreads();
+        if (warp_id() == 0) {   // lane l owns bins [8l, 8l+8); higher bins = higher lanes
+            uint32_t hb[8], tot = 0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) { hb[j] = hist[8 * lane + j]; tot += hb[j]; }
+            uint32_t inc = tot;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t v = __shfl_down_sync(0xffffffffu, inc, o);
+                if (lane + o < 32) inc += v;
+            }
+            uint32_t run = inc - tot;
+            const uint32_t rem = (uint32_t)my.remaining;
+#pragma unroll
+            for (int j = 7; j >= 0; --j) {
+                if (run < rem && run + hb[j] >= rem) { st.found_bin = 8 * lane + j; st.found_above = (int)run; }
+                run += hb[j];
+            }
+        }
+        __syncthreads();
+        if (tid == 0) {
+            const int b = st.found_bin;
+            st.remaining -= st.found_above;
+            st.pmask[w] |= 255u << shift;
+            st.pval[w] |= (uint32_t)b << shift;
+            if ((uint32_t)st.remaining == hist[b]) st.done = 1;
+        }
+        __syncthreads();
+    }
+    const BSel my = st;
+    for (int i = tid; i < n; i += T)
+        if ((cf[i] & A) && bselected(ck[i], cid[i], my)) cf[i] |= S;
+    __syncthreads();
+}
+
+enum : uint8_t { kCand = 1, kSem = 2, kGs = 4, kNew = 8, kTake = 16 };
+
 __global__ void __launch_bounds__(kUnionThreads, 1)
 union_kernel(int V, const int32_t* __restrict__ static_ids, int n_static,
              const int32_t* __restrict__ seeds, int n_seed,
-             const int32_t* __restrict__ sem, const int* __restrict__ n_sem_dev, int n_sem_max,
+             const double* __restrict__ cand_s, const int32_t* __restrict__ cand_id,
+             const int* __restrict__ n_cand_dev, int cap, int n_sem,
              const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
              const int32_t* __restrict__ ctx_sel, const int* __restrict__ n_ctx_sel_dev,
              int n_graph_sem_seeds, int per_seed, int n_dyn, int R, int r,
              int32_t* __restrict__ out_ids, int32_t* __restrict__ out_n,
              int32_t* __restrict__ out_local, int32_t* __restrict__ out_local_n,
-             int debug, int* flags) {
-    extern __shared__ unsigned char u_sm[];
+             int32_t* __restrict__ sem_out, int* __restrict__ sem_out_n, int debug, int* flags) {
+    extern __shared__ __align__(16) unsigned char u_sm[];
     const int nwords = (V + 31) / 32;
-    uint32_t* bits = (uint32_t*)u_sm;                       // [nwords]
+    uint64_t* ck = (uint64_t*)u_sm;                          // [cap]
+    int32_t* cid = (int32_t*)(ck + cap);                     // [cap]
+    uint32_t* bits = (uint32_t*)(cid + cap);                 // [nwords]
     int32_t* G = (int32_t*)(bits + nwords);                  // [kMaxG]
     int32_t* goff = G + kMaxG;                               // [kMaxG + 1]
-    int32_t* graph = goff + kMaxG + 1;                       // [kMaxG * per_seed]
+    int32_t* gs = goff + kMaxG + 1;                          // [kMaxG] ordered S_sem prefix
+    int32_t* graph = gs + kMaxG;                             // [kMaxG * per_seed]
+    uint8_t* cf = (uint8_t*)(graph + kMaxG * per_seed);      // [cap]
     __shared__ int warp_tot[33];
-    __shared__ int nG_s, bad_s, taken_s;
+    __shared__ uint32_t hist[256];
+    __shared__ BSel bsel;
+    __shared__ int nG_s, bad_s, taken_s, ngs_s, sem_n_s;
 
-    const int tid = threadIdx.x, lane = lane_id();
-    for (int w = tid; w < nwords; w += blockDim.x) bits[w] = 0;
-    if (tid == 0) bad_s = 0;
+    const int tid = threadIdx.x, lane = lane_id(), T = blockDim.x;
+    const int n_cand = min(*n_cand_dev, cap);
+    for (int w = tid; w < nwords; w += T) bits[w] = 0;
+    for (int i = tid; i < n_cand; i += T) {
+        ck[i] = double_key(cand_s[i]);
+        const int32_t id = cand_id[i];
+        cid[i] = id;
+        cf[i] = (id >= 0 && id < V) ? kCand : 0;
+    }
+    if (tid == 0) { bad_s = 0; sem_n_s = 0; }
     __syncthreads();
-    // 1. static members
-    for (int i0 = 0; i0 < n_static; i0 += 8 * blockDim.x) {   // 8 independent loads in flight
+    // 1. static members (8 independent loads in flight per thread)
+    for (int i0 = 0; i0 < n_static; i0 += 8 * T) {
         int32_t v[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
-            const int i = i0 + u * blockDim.x + tid;
+            const int i = i0 + u * T + tid;
             v[u] = i < n_static ? __ldg(&static_ids[i]) : -1;
         }
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
-            const int i = i0 + u * blockDim.x + tid;
+            const int i = i0 + u * T + tid;
             if (i >= n_static) continue;
             if (v[u] < 0 || v[u] >= V) { bad_s = 1; continue; }
             if (debug && i > 0 && static_ids[i - 1] >= v[u]) bad_s = 1;
             atomicOr(&bits[v[u] >> 5], 1u << (v[u] & 31));
         }
     }
-    const int n_sem = min(*n_sem_dev, n_sem_max);
-    const int n_ctx_sel = ctx_sel ? *n_ctx_sel_dev : 0;
-    // 2. graph seeds G = dedupe(seeds ++ S_sem[:ngs]) and S_graph, warp 0 in parallel
+    // 2. S_sem = exact top-N of the candidate superset
+    block_topM(ck, cid, cf, n_cand, kCand, kSem, n_sem, hist, bsel, warp_tot);
+    if (sem_out) {
+        for (int i = tid; i < n_cand; i += T)
+            if (cf[i] & kSem) sem_out[atomicAdd(&sem_n_s, 1)] = cid[i];
+    }
+    // 3. ordered prefix S_sem[:n_graph_sem_seeds]: select, then rank inside
+    const int ngs = min(n_graph_sem_seeds, min(n_sem, kMaxG));
+    block_topM(ck, cid, cf, n_cand, kSem, kGs, ngs, hist, bsel, warp_tot);
+    if (tid == 0) ngs_s = 0;
+    __syncthreads();
+    for (int i = tid; i < n_cand; i += T)
+        if (cf[i] & kGs) {
+            const int slot = atomicAdd(&ngs_s, 1);
+            if (slot < kMaxG) graph[slot] = i;               // graph[] as scratch: candidate index
+        }
+    __syncthreads();
+    const int ngs_found = min(ngs_s, kMaxG);
+    for (int a = tid; a < ngs_found; a += T) {
+        const int ia = graph[a];
+        int rank = 0;
+        for (int b = 0; b < ngs_found; ++b) {
+            const int ib = graph[b];
+            rank += before(ck[ib], cid[ib], ck[ia], cid[ia]) ? 1 : 0;   // (key desc, id asc)
+        }
+        gs[rank] = cid[ia];
+    }
+    __syncthreads();
+    // 4. G = dedupe(seeds ++ S_sem[:ngs]) and S_graph (warp 0)
     if (warp_id() == 0) {
-        const int ngs = min(n_graph_sem_seeds, n_sem);
-        const int nc = min(n_seed + ngs, kMaxG);
-        for (int i = lane; i < nc; i += 32) {          // candidates -> graph[] as scratch
-            int32_t g = i < n_seed ? seeds[i] : sem[i - n_seed];
+        const int nc = min(n_seed + ngs_found, kMaxG);
+        for (int i = lane; i < nc; i += 32) {
+            int32_t g = i < n_seed ? seeds[i] : gs[i - n_seed];
             if (g < 0 || g >= V) { bad_s = 1; g = -1; }
             graph[i] = g;
         }
@@ -186,7 +329,7 @@ union_kernel(int V, const int32_t* __restrict__ static_ids, int n_static,
         int nG = 0;
         for (int base = 0; base < nc; base += 32) {
             const int i = base + lane;
-            int32_t g = i < nc ? graph[i] : -1;
+            const int32_t g = i < nc ? graph[i] : -1;
             bool keep = g >= 0;
             for (int j = 0; j < i && keep; ++j) keep = graph[j] != g;   // first occurrence
             const unsigned bal = __ballot_sync(0xffffffffu, keep);
@@ -194,7 +337,6 @@ union_kernel(int V, const int32_t* __restrict__ static_ids, int n_static,
             nG += __popc(bal);
         }
         __syncwarp();
-        // degrees and offsets (exclusive scan of min(deg, per_seed))
         int carry = 0;
         for (int base = 0; base < nG; base += 32) {
             const int j = base + lane;
@@ -203,7 +345,7 @@ union_kernel(int V, const int32_t* __restrict__ static_ids, int n_static,
             int inc = c;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
-                int t = __shfl_up_sync(0xffffffffu, inc, o);
+                const int t = __shfl_up_sync(0xffffffffu, inc, o);
                 if (lane >= o) inc += t;
             }
             if (j < nG) goff[j] = carry + inc - c;
@@ -215,31 +357,32 @@ union_kernel(int V, const int32_t* __restrict__ static_ids, int n_static,
     const int nG = nG_s;
     const int n_graph = goff[nG];
     if (row_ptr)
-        for (int j = warp_id(); j < nG; j += blockDim.x / 32) {
+        for (int j = warp_id(); j < nG; j += T / 32) {
             const int cnt = goff[j + 1] - goff[j];
             const int base = row_ptr[G[j]];
             for (int e = lane; e < cnt; e += 32) graph[goff[j] + e] = col[base + e];
         }
     __syncthreads();
 
-    // 3. formation: seeds ++ S_sem ++ S_graph ++ S_ctx, first occurrence, skip
-    //    members, stop at N_dyn. Seeds, graph and ctx are walked by warp 0 in
-    //    32-wide windows; S_sem (distinct ids by construction) is taken in
-    //    parallel with a block-wide order-preserving scan.
+    // 5. formation: seeds ++ S_sem ++ S_graph ++ S_ctx, first occurrence, skip
+    //    members (static or taken), stop at N_dyn. Seeds, graph and ctx are
+    //    walked by warp 0 in 32-wide windows; the S_sem part (distinct ids)
+    //    takes its first (budget) new ids in S_sem order by an exact block
+    //    top-M over the new ones -- the same set the sequential walk takes.
     const unsigned lt_mask = (1u << lane) - 1u;
     auto walk = [&](const int32_t* src, int len, int taken) -> int {
         for (int base = 0; base < len && taken < n_dyn; base += 32) {
             const int idx = base + lane;
             int32_t c = idx < len ? src[idx] : -1;
-            bool valid = c >= 0 && c < V;
+            const bool valid = c >= 0 && c < V;
             if (idx < len && !valid) bad_s = 1;
             if (!valid) c = -1 - lane;            // distinct non-matching sentinel
             const unsigned peers = __match_any_sync(0xffffffffu, c);
             const bool first = valid && ((__ffs(peers) - 1) == lane);
             const bool cand = first && !((bits[c < 0 ? 0 : (c >> 5)] >> (c & 31)) & 1u);
             const unsigned bal = __ballot_sync(0xffffffffu, cand);
-            const int before = __popc(bal & lt_mask);
-            if (cand && taken + before < n_dyn) atomicOr(&bits[c >> 5], 1u << (c & 31));
+            const int bf = __popc(bal & lt_mask);
+            if (cand && taken + bf < n_dyn) atomicOr(&bits[c >> 5], 1u << (c & 31));
             taken += min(__popc(bal), n_dyn - taken);
             __syncwarp();
         }
@@ -250,46 +393,25 @@ union_kernel(int V, const int32_t* __restrict__ static_ids, int n_static,
         if (lane == 0) taken_s = t;
     }
     __syncthreads();
-    {
-        const int taken0 = taken_s;
-        const int T = blockDim.x;
-        const int i0 = (int)((long long)n_sem * tid / T), i1 = (int)((long long)n_sem * (tid + 1) / T);
-        // each thread owns <= kSemPerThread consecutive S_sem entries, loaded once
-        constexpr int kSemPerThread = 16;
-        int32_t cv[kSemPerThread];
-        unsigned newm = 0;
-#pragma unroll
-        for (int u = 0; u < kSemPerThread; ++u) cv[u] = (i0 + u < i1) ? __ldg(&sem[i0 + u]) : -1;
-        int cnt = 0;
-#pragma unroll
-        for (int u = 0; u < kSemPerThread; ++u) {
-            const int32_t c = cv[u];
-            const bool nw = c >= 0 && c < V && !((bits[c >> 5] >> (c & 31)) & 1u);
-            newm |= (unsigned)nw << u;
-            cnt += nw;
-        }
-        int total = 0;
-        int off = block_excl_scan(cnt, warp_tot, total);   // contains __syncthreads
-        const int budget = n_dyn - taken0;
-#pragma unroll
-        for (int u = 0; u < kSemPerThread; ++u) {
-            if (((newm >> u) & 1u) && off < budget) {
-                atomicOr(&bits[cv[u] >> 5], 1u << (cv[u] & 31));
-                ++off;
-            }
-        }
-        __syncthreads();
-        if (tid == 0) taken_s = taken0 + min(total, budget);
-    }
+    const int taken0 = taken_s;
+    const int budget = n_dyn - taken0;
+    for (int i = tid; i < n_cand; i += T)
+        if ((cf[i] & kSem) && !((bits[cid[i] >> 5] >> (cid[i] & 31)) & 1u)) cf[i] |= kNew;
     __syncthreads();
-    if (warp_id() == 0 && taken_s < n_dyn) {
-        int t = walk(graph, n_graph, taken_s);
-        t = walk(ctx_sel, n_ctx_sel, t);
+    block_topM(ck, cid, cf, n_cand, kNew, kTake, budget, hist, bsel, warp_tot);
+    int c_take = 0;
+    for (int i = tid; i < n_cand; i += T)
+        if (cf[i] & kTake) { atomicOr(&bits[cid[i] >> 5], 1u << (cid[i] & 31)); ++c_take; }
+    const int took = block_count(c_take, warp_tot);
+    if (warp_id() == 0) {
+        const int n_ctx_sel = ctx_sel ? *n_ctx_sel_dev : 0;
+        int t = taken0 + took;
+        if (t < n_dyn) t = walk(graph, n_graph, t);
+        if (t < n_dyn) t = walk(ctx_sel, n_ctx_sel, t);
     }
     __syncthreads();
 
-    // 4. compaction: thread t owns words [t*nwords/T, (t+1)*nwords/T)
-    const int T = blockDim.x;
+    // 6. compaction: thread t owns words [t*nwords/T, (t+1)*nwords/T)
     const int w0 = (int)((long long)nwords * tid / T), w1 = (int)((long long)nwords * (tid + 1) / T);
     int cnt = 0, cnt_local = 0;
     for (int w = w0; w < w1; ++w) {
@@ -305,9 +427,9 @@ union_kernel(int V, const int32_t* __restrict__ static_ids, int n_static,
     for (int w = w0; w < w1; ++w) {
         uint32_t b = bits[w];
         while (b) {
-            int bit = __ffs(b) - 1;
+            const int bit = __ffs(b) - 1;
             b &= b - 1;
-            int v = w * 32 + bit;
+            const int v = w * 32 + bit;
             out_ids[off++] = v;
             if (out_local && (R == 1 || v % R == r)) out_local[off_local++] = v;
         }
@@ -315,25 +437,39 @@ union_kernel(int V, const int32_t* __restrict__ static_ids, int n_static,
     if (tid == 0) {
         *out_n = total;
         if (out_local_n) *out_local_n = total_local;
+        if (sem_out_n) *sem_out_n = sem_n_s;
         if (bad_s) atomicOr(flags, kFlagBadIds);
         if (total > n_static + n_dyn) atomicOr(flags, kFlagBudget);
+        if (*n_cand_dev > cap) atomicOr(flags, kFlagSelectOverflow);
     }
 }
 
+static size_t union_fixed_bytes(int V, int per_seed) {
+    const int nwords = (V + 31) / 32;
+    return (size_t)nwords * 4 + (size_t)(3 * kMaxG + 1) * 4 + (size_t)kMaxG * per_seed * 4 + 64;
+}
+
+// Largest candidate superset the union kernel can hold in shared memory.
+int union_cand_cap(int V, int per_seed) {
+    const size_t budget = 220 * 1024;
+    const size_t fixed = union_fixed_bytes(V, per_seed);
+    if (fixed >= budget) return 0;
+    return (int)((budget - fixed) / 13) & ~15;
+}
+
 void launch_union(int V, const int32_t* static_ids, int n_static, const int32_t* seeds, int n_seed,
-                  const int32_t* sem_sorted, const int* n_sem_dev, int n_sem_max,
+                  const double* cand_s, const int32_t* cand_id, const int* n_cand_dev, int cap, int n_sem,
                   const int32_t* row_ptr, const int32_t* col,
                   const int32_t* ctx_sel, const int* n_ctx_sel_dev,
                   int n_graph_sem_seeds, int per_seed, int n_dyn, int R, int r,
                   int32_t* out_ids, int32_t* out_n, int32_t* out_local, int32_t* out_local_n,
-                  int debug, int* flags, cudaStream_t st) {
-    const int nwords = (V + 31) / 32;
-    size_t smem = (size_t)nwords * 4 + (size_t)(2 * kMaxG + 1) * 4 + (size_t)kMaxG * per_seed * 4;
+                  int32_t* sem_out, int* sem_out_n, int debug, int* flags, cudaStream_t st) {
+    const size_t smem = (size_t)cap * 13 + union_fixed_bytes(V, per_seed) + 16;
     cudaFuncSetAttribute(union_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    union_kernel<<<1, kUnionThreads, smem, st>>>(V, static_ids, n_static, seeds, n_seed, sem_sorted,
-                                                  n_sem_dev, n_sem_max, row_ptr, col, ctx_sel, n_ctx_sel_dev,
-                                                  n_graph_sem_seeds, per_seed, n_dyn, R, r, out_ids, out_n,
-                                                  out_local, out_local_n, debug, flags);
+    union_kernel<<<1, kUnionThreads, smem, st>>>(V, static_ids, n_static, seeds, n_seed, cand_s, cand_id, n_cand_dev,
+                                                  cap, n_sem, row_ptr, col, ctx_sel, n_ctx_sel_dev, n_graph_sem_seeds,
+                                                  per_seed, n_dyn, R, r, out_ids, out_n, out_local, out_local_n,
+                                                  sem_out, sem_out_n, debug, flags);
 }
 
 }  // namespace es

@@ -55,7 +55,7 @@ def run_path(P, ctx=None, inv_temp=1.0, logits=False):
 
 
 def check(P, got, ref, k):
-    np.testing.assert_array_equal(got["sem"], ref["sem"])
+    np.testing.assert_array_equal(np.sort(got["sem"]), np.sort(ref["sem"]))
     np.testing.assert_array_equal(got["S"], ref["S"])
     G.assert_triple_close(*got["tri"], ref["triple"], k)
     oi, ov, ol, op = got["mrg"]
