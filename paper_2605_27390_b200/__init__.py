@@ -186,16 +186,12 @@ class Context:
     def comm_init(self, group=None):
         """Creates the library's NCCL communicator; the 128-byte unique id is
         broadcast from rank 0 over the given torch.distributed group."""
-        import torch
         import torch.distributed as dist
+        from . import dist as esd
         buf = (C.c_char * 128)()
         if dist.get_rank(group) == 0:
             _check(lib().evospec_comm_unique_id(buf))
-        t = torch.tensor(list(bytes(buf)), dtype=torch.uint8)
-        if dist.get_backend(group) == "nccl":
-            t = t.cuda(self.device)
-        dist.broadcast(t, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
-        raw = bytes(t.cpu().tolist())
+        raw = esd.broadcast_bytes(bytes(buf), group)
         _check(lib().evospec_comm_init(self._h, C.c_char_p(raw)))
 
     # ---- a1-a4
