@@ -19,6 +19,7 @@
 // merge_kernel (one warp per H row): the shard merge of SURVEY §8(c) step 12.
 #include "common.cuh"
 #include "kernels.cuh"
+#include "lmh_epilogue.cuh"   // warp_kth_largest
 
 namespace es {
 
@@ -98,14 +99,25 @@ lmh_finalize_kernel(LmhArgs a, int n_cta, int k, float gamma, const float* __res
     S = warp_sum(S);
     tot = warp_sum_i(tot);
     if (lane == 0) { red_s[warp] = S; red_t[warp] = tot; }
-    // stage every CTA's sorted list in shared memory: flat, independent loads
-    // (entries past a list's count are -inf / -1 in the partials)
+    // stage every CTA's sorted list in shared memory: flat, 4 independent loads
+    // in flight per thread (entries past a list's count are -inf / -1)
     for (int c = threadIdx.x; c < n_cta; c += blockDim.x) l_cnt[c] = a.part.cnt[(size_t)c * a.n_h + r];
-    for (int f = threadIdx.x; f < n_cta * KP; f += blockDim.x) {
-        const int c = f / KP, i = f - c * KP;
-        const size_t o = ((size_t)c * a.n_h + r) * KP + i;
-        l_val[f] = a.part.val[o];
-        l_id[f] = a.part.id[o];
+    for (int f0 = 0; f0 < n_cta * KP; f0 += 4 * blockDim.x) {
+        float vv[4];
+        int32_t ii[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int f = f0 + u * blockDim.x + threadIdx.x;
+            const int c = f / KP, i = f - c * KP;
+            const size_t o = ((size_t)c * a.n_h + r) * KP + i;
+            vv[u] = f < n_cta * KP ? __ldcg(&a.part.val[o]) : -INFINITY;
+            ii[u] = f < n_cta * KP ? __ldcg(&a.part.id[o]) : -1;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int f = f0 + u * blockDim.x + threadIdx.x;
+            if (f < n_cta * KP) { l_val[f] = vv[u]; l_id[f] = ii[u]; }
+        }
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -116,8 +128,45 @@ lmh_finalize_kernel(LmhArgs a, int n_cta, int k, float gamma, const float* __res
         row_sumexp[r] = s_all;
         total_s = t_all;
     }
-    // 2. k-way merge (warp 0)
-    if (warp == 0) {
+    // 2. the best KP of the per-CTA sorted lists (warp 0)
+    if (warp == 0 && KP <= 32) {
+        // pre-threshold: KP-th largest of the lane maxima of the list heads (a lower
+        // bound of the KP-th best entry); entries >= it are inserted into a sorted
+        // register list (lane i = entry i) by ballot rank + shfl_up shift.
+        float lm = -INFINITY;
+        for (int c = lane; c < n_cta; c += 32)
+            if (l_cnt[c] > 0) lm = fmaxf(lm, l_val[(size_t)c * KP]);
+        const float th0 = warp_kth_largest(lm, KP);
+        float Lv = -INFINITY, tv = -INFINITY;
+        int Lid = 0x7fffffff, tid_ = 0x7fffffff, cnt = 0;
+        for (int c0 = 0; c0 < n_cta; c0 += 32) {
+            const int c = c0 + lane;
+            const int len = c < n_cta ? l_cnt[c] : 0;
+            for (int i = 0;; ++i) {
+                const bool has = i < len && l_val[(size_t)c * KP + i] >= th0;
+                const float x = has ? l_val[(size_t)c * KP + i] : 0.0f;
+                const int xid = has ? l_id[(size_t)c * KP + i] : 0;
+                unsigned m = __ballot_sync(0xffffffffu, has);
+                if (!m) break;
+                while (m) {
+                    const int src = __ffs(m) - 1;
+                    m &= m - 1;
+                    const float xv = __shfl_sync(0xffffffffu, x, src);
+                    const int xi = __shfl_sync(0xffffffffu, xid, src);
+                    if (cnt == KP && !before(xv, xi, tv, tid_)) continue;
+                    const int at = __popc(__ballot_sync(0xffffffffu, lane < cnt && before(Lv, Lid, xv, xi)));
+                    const float pv = __shfl_up_sync(0xffffffffu, Lv, 1);
+                    const int pi = __shfl_up_sync(0xffffffffu, Lid, 1);
+                    if (lane > at) { Lv = pv; Lid = pi; }
+                    if (lane == at) { Lv = xv; Lid = xi; }
+                    cnt = min(cnt + 1, KP);
+                    if (cnt == KP) { tv = __shfl_sync(0xffffffffu, Lv, KP - 1); tid_ = __shfl_sync(0xffffffffu, Lid, KP - 1); }
+                }
+            }
+        }
+        if (lane < cnt) { c_v32[lane] = Lv; c_id[lane] = Lid; }
+        if (lane == 0) n_kept_s = cnt;
+    } else if (warp == 0) {   // KP > 32: k-way merge of the list heads
         int produced = 0;
         for (; produced < KP; ++produced) {
             float bv = -INFINITY;

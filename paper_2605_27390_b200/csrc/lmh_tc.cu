@@ -38,6 +38,8 @@ constexpr int kTcMmaWarp = kProdWarps;
 constexpr int kTcEpiWarp0 = kProdWarps + 1;
 constexpr int kTcEpiWarps = 8;
 constexpr int kTcWarps = kProdWarps + 1 + kTcEpiWarps;
+constexpr int kPfBytes = 1024;     // L2 prefetch window per row (8 stages of 128 B)
+constexpr int kPfDist = 2;         // windows ahead of the cp.async stream
 constexpr int kBlockK = 64;        // bf16 columns per stage = one 128-byte swizzle atom row
 constexpr int kTileM = 128;
 
@@ -87,6 +89,9 @@ ES_DEV void cp_async16(uint32_t dst, const void* src, uint64_t policy) {
 }
 ES_DEV void cp_async_arrive_noinc(uint64_t* bar) {
     asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+ES_DEV void l2_prefetch(const void* p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 ES_DEV uint64_t policy_evict_first() {
     uint64_t p;
@@ -211,6 +216,26 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
         // one warp instruction moves 4 whole 128-byte row segments.
         const uint64_t pol_w = policy_evict_first(), pol_h = policy_evict_last();
         const int chunk = lane & 7;
+        // L2 prefetch: thread p (0..127) owns tile row p and pulls its row into L2
+        // in 1 KB windows (8 stages) kPfDist windows ahead of the cp.async stream,
+        // so DRAM sees 1 KB contiguous reads per row instead of 128 B pieces.
+        const int prow = warp * 32 + lane;
+        const size_t row_bytes = (size_t)a.d * 2;
+        const int n_win = (int)((row_bytes + kPfBytes - 1) / kPfBytes);
+        auto row_ptr_of = [&](int t, int row) -> const char* {
+            int t0, tn;
+            tile_range(t, t0, tn);
+            const int pos = t0 + (row < tn ? row : 0);
+            return (const char*)a.W + (size_t)(a.subset[pos] / a.R) * row_bytes;
+        };
+        auto prefetch_win = [&](const char* rp, int w) {
+            if (w < 0 || w >= n_win) return;
+            const size_t off = (size_t)w * kPfBytes;
+            const uint32_t sz = (uint32_t)min((size_t)kPfBytes, row_bytes - off);
+            l2_prefetch(rp + off, sz);
+        };
+        const char* pf_cur = n_tiles > 0 ? row_ptr_of(0, prow) : nullptr;
+        for (int w = 0; w < kPfDist && pf_cur; ++w) prefetch_win(pf_cur, w);
         int stage = 0;
         uint32_t phase = 0;
         for (int t = 0; t < n_tiles; ++t) {
@@ -222,10 +247,18 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
             for (int i = 0; i < 8; ++i) {
                 const int row = 16 * i + 4 * warp + (lane >> 3);
                 const int pos = t0 + (row < tn ? row : 0);
-                src[i] = (const char*)a.W + (size_t)(a.subset[pos] / a.R) * (size_t)a.d * 2 + chunk * 16;
+                src[i] = (const char*)a.W + (size_t)(a.subset[pos] / a.R) * row_bytes + chunk * 16;
                 dsto[i] = (uint32_t)(row * 128 + ((chunk ^ (row & 7)) << 4));
             }
+            const char* pf_next = t + 1 < n_tiles ? row_ptr_of(t + 1, prow) : nullptr;
             for (int kb = 0; kb < tp.nkb; ++kb) {
+                // prefetch: window (kb/8 + kPfDist) of this tile; the next tile's first
+                // windows once this tile's remaining windows are all requested
+                if ((kb & 7) == 0) {
+                    const int w = (kb >> 3) + kPfDist;
+                    if (w < n_win) prefetch_win(pf_cur, w);
+                    else if (pf_next) prefetch_win(pf_next, w - n_win);
+                }
                 mbar_wait(&empty[stage], phase ^ 1);
                 if (warp == 0 && lane == 0) {
                     mbar_arrive_expect_tx(&full[stage], (uint32_t)(NP * 128));
@@ -237,6 +270,7 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
                 cp_async_arrive_noinc(&full[stage]);
                 if (++stage == S) { stage = 0; phase ^= 1; }
             }
+            pf_cur = pf_next;
         }
         (void)tmap_w;
     } else if (warp == kTcMmaWarp) {

@@ -133,31 +133,26 @@ void launch_ctx_select(const int32_t* ctx, int n_ctx, int V, int min_count, int 
 }
 
 // ------------------------------------------------------------ union
-// Block-wide exact top-M (key desc, id asc) among the candidates whose flag
-// has any bit of A; marks them with bit S. Radix select on the 96-bit
-// composite (double_key(s), ~id), 8 bits per pass, exits as soon as the
-// boundary bin is taken whole.
+// Block-wide exact top-M under (key desc, id asc) among the candidates whose
+// flag has any bit of A; marks them with bit S. Radix select on the composite
+// (64-bit order key, ~id) with 10-bit digits (one histogram bin per thread),
+// starting at the highest bit in which the active keys differ, so two or
+// three passes settle ~10k fp64 scores; the ~id digits run only when the
+// boundary holds equal keys. Exits as soon as the boundary bin is taken whole.
 struct BSel {
-    uint32_t pmask[3], pval[3];
+    uint64_t kmask, kval;
+    uint32_t imask, ival;
     int remaining, done, found_bin, found_above;
+    uint64_t kmin, kmax;
 };
 
-ES_DEV uint32_t bword(uint64_t k, int32_t id, int w) {
-    return w == 0 ? (uint32_t)(k >> 32) : (w == 1 ? (uint32_t)k : 0xFFFFFFFFu - (uint32_t)id);
-}
 ES_DEV bool bmatch(uint64_t k, int32_t id, const BSel& st) {
-#pragma unroll
-    for (int w = 0; w < 3; ++w)
-        if ((bword(k, id, w) & st.pmask[w]) != st.pval[w]) return false;
-    return true;
+    return (k & st.kmask) == st.kval && ((0xFFFFFFFFu - (uint32_t)id) & st.imask) == st.ival;
 }
 ES_DEV bool bselected(uint64_t k, int32_t id, const BSel& st) {
-#pragma unroll
-    for (int w = 0; w < 3; ++w) {
-        const uint32_t a = bword(k, id, w) & st.pmask[w];
-        if (a != st.pval[w]) return a > st.pval[w];
-    }
-    return true;
+    const uint64_t a = k & st.kmask;
+    if (a != st.kval) return a > st.kval;
+    return ((0xFFFFFFFFu - (uint32_t)id) & st.imask) >= st.ival;
 }
 
 ES_DEV int block_count(int v, int* warp_tot) {
@@ -166,12 +161,31 @@ ES_DEV int block_count(int v, int* warp_tot) {
     return total;
 }
 
+ES_DEV uint64_t warp_min_u64(uint64_t v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) { const uint64_t w = __shfl_xor_sync(0xffffffffu, v, o); v = w < v ? w : v; }
+    return v;
+}
+ES_DEV uint64_t warp_max_u64(uint64_t v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) { const uint64_t w = __shfl_xor_sync(0xffffffffu, v, o); v = w > v ? w : v; }
+    return v;
+}
+
+constexpr int kSelBins = 1024;   // == kUnionThreads: one bin per thread in the scan
+
 ES_DEV void block_topM(const uint64_t* ck, const int32_t* cid, uint8_t* cf, int n, uint8_t A, uint8_t S, int M,
                        uint32_t* hist, BSel& st, int* warp_tot) {
     const int tid = threadIdx.x, T = blockDim.x, lane = lane_id();
     int c = 0;
-    for (int i = tid; i < n; i += T) c += (cf[i] & A) != 0;
-    const int cnt = block_count(c, warp_tot);
+    uint64_t kmin = ~0ull, kmax = 0ull;
+    for (int i = tid; i < n; i += T)
+        if (cf[i] & A) { ++c; kmin = min(kmin, ck[i]); kmax = max(kmax, ck[i]); }
+    kmin = warp_min_u64(kmin);
+    kmax = warp_max_u64(kmax);
+    if (tid == 0) { st.kmin = ~0ull; st.kmax = 0ull; }
+    const int cnt = block_count(c, warp_tot);   // syncs: st initialised before the atomics below
+    if (lane == 0 && kmin <= kmax) { atomicMin((unsigned long long*)&st.kmin, kmin); atomicMax((unsigned long long*)&st.kmax, kmax); }
     if (M >= cnt || M <= 0) {
         if (M > 0)
             for (int i = tid; i < n; i += T)
@@ -179,53 +193,54 @@ ES_DEV void block_topM(const uint64_t* ck, const int32_t* cid, uint8_t* cf, int 
         __syncthreads();
         return;
     }
+    __syncthreads();
     if (tid == 0) {
-        for (int w = 0; w < 3; ++w) { st.pmask[w] = 0; st.pval[w] = 0; }
+        st.kmask = 0; st.kval = 0; st.imask = 0; st.ival = 0;
         st.remaining = M;
         st.done = 0;
     }
     __syncthreads();
-    for (int pass = 0; pass < 12; ++pass) {
-        if (st.done) break;
-        const int w = pass >> 2, shift = 24 - 8 * (pass & 3);
-        for (int b = tid; b < 256; b += T) hist[b] = 0;
+    const uint64_t diff = st.kmin ^ st.kmax;
+    int kbit = diff ? 63 - __clzll((long long)diff) : -1;   // highest differing key bit
+    int ibit = 31;
+    for (int pass = 0; pass < 16; ++pass) {
+        if (st.done || (kbit < 0 && ibit < 0)) break;
+        const bool on_key = kbit >= 0;
+        const int hi = on_key ? kbit : ibit;
+        const int width = hi + 1 < 10 ? hi + 1 : 10;
+        const int lo = hi - width + 1;
+        const uint32_t dmask = (1u << width) - 1u;
+        for (int b = tid; b < kSelBins; b += T) hist[b] = 0;
         __syncthreads();
         const BSel my = st;
         for (int base = 0; base < n; base += T) {            // uniform trip count: warp-aggregated adds
             const int i = base + tid;
             uint32_t digit = 0xFFFFFFFFu;
-            if (i < n && (cf[i] & A) && bmatch(ck[i], cid[i], my)) digit = (bword(ck[i], cid[i], w) >> shift) & 255u;
+            if (i < n && (cf[i] & A) && bmatch(ck[i], cid[i], my))
+                digit = on_key ? (uint32_t)(ck[i] >> lo) & dmask : ((0xFFFFFFFFu - (uint32_t)cid[i]) >> lo) & dmask;
             const unsigned peers = __match_any_sync(0xffffffffu, digit);
             if (digit != 0xFFFFFFFFu && lane == __ffs(peers) - 1) atomicAdd(&hist[digit], (uint32_t)__popc(peers));
         }
         __syncthreads();
-        if (warp_id() == 0) {   // lane l owns bins [8l, 8l+8); higher bins = higher lanes
-            uint32_t hb[8], tot = 0;
-#pragma unroll
-            for (int j = 0; j < 8; ++j) { hb[j] = hist[8 * lane + j]; tot += hb[j]; }
-            uint32_t inc = tot;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t v = __shfl_down_sync(0xffffffffu, inc, o);
-                if (lane + o < 32) inc += v;
-            }
-            uint32_t run = inc - tot;
-            const uint32_t rem = (uint32_t)my.remaining;
-#pragma unroll
-            for (int j = 7; j >= 0; --j) {
-                if (run < rem && run + hb[j] >= rem) { st.found_bin = 8 * lane + j; st.found_above = (int)run; }
-                run += hb[j];
-            }
+        // thread t owns bin (kSelBins-1-t): an exclusive scan over t counts the bins above it
+        const int bin = kSelBins - 1 - tid;
+        const uint32_t hb = tid < kSelBins ? hist[bin] : 0u;
+        int total;
+        const int above = block_excl_scan((int)hb, warp_tot, total);
+        if (tid < kSelBins && above < my.remaining && above + (int)hb >= my.remaining) {
+            st.found_bin = bin;
+            st.found_above = above;
         }
         __syncthreads();
         if (tid == 0) {
             const int b = st.found_bin;
             st.remaining -= st.found_above;
-            st.pmask[w] |= 255u << shift;
-            st.pval[w] |= (uint32_t)b << shift;
+            if (on_key) { st.kmask |= (uint64_t)dmask << lo; st.kval |= (uint64_t)b << lo; }
+            else { st.imask |= dmask << lo; st.ival |= (uint32_t)b << lo; }
             if ((uint32_t)st.remaining == hist[b]) st.done = 1;
         }
         __syncthreads();
+        if (on_key) kbit = lo - 1; else ibit = lo - 1;
     }
     const BSel my = st;
     for (int i = tid; i < n; i += T)
@@ -257,18 +272,30 @@ union_kernel(int V, const int32_t* __restrict__ static_ids, int n_static,
     int32_t* graph = gs + kMaxG;                             // [kMaxG * per_seed]
     uint8_t* cf = (uint8_t*)(graph + kMaxG * per_seed);      // [cap]
     __shared__ int warp_tot[33];
-    __shared__ uint32_t hist[256];
+    __shared__ uint32_t hist[kSelBins];
     __shared__ BSel bsel;
     __shared__ int nG_s, bad_s, taken_s, ngs_s, sem_n_s;
 
     const int tid = threadIdx.x, lane = lane_id(), T = blockDim.x;
     const int n_cand = min(*n_cand_dev, cap);
     for (int w = tid; w < nwords; w += T) bits[w] = 0;
-    for (int i = tid; i < n_cand; i += T) {
-        ck[i] = double_key(cand_s[i]);
-        const int32_t id = cand_id[i];
-        cid[i] = id;
-        cf[i] = (id >= 0 && id < V) ? kCand : 0;
+    for (int i0 = 0; i0 < n_cand; i0 += 4 * T) {           // 4 independent loads in flight
+        double sv[4];
+        int32_t iv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int i = i0 + u * T + tid;
+            sv[u] = i < n_cand ? __ldcg(&cand_s[i]) : 0.0;
+            iv[u] = i < n_cand ? __ldcg(&cand_id[i]) : -1;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int i = i0 + u * T + tid;
+            if (i >= n_cand) continue;
+            ck[i] = double_key(sv[u]);
+            cid[i] = iv[u];
+            cf[i] = (iv[u] >= 0 && iv[u] < V) ? kCand : 0;
+        }
     }
     if (tid == 0) { bad_s = 0; sem_n_s = 0; }
     __syncthreads();
@@ -292,8 +319,15 @@ union_kernel(int V, const int32_t* __restrict__ static_ids, int n_static,
     // 2. S_sem = exact top-N of the candidate superset
     block_topM(ck, cid, cf, n_cand, kCand, kSem, n_sem, hist, bsel, warp_tot);
     if (sem_out) {
-        for (int i = tid; i < n_cand; i += T)
-            if (cf[i] & kSem) sem_out[atomicAdd(&sem_n_s, 1)] = cid[i];
+        for (int base = 0; base < n_cand; base += T) {      // one smem atomic per warp
+            const int i = base + tid;
+            const bool in = i < n_cand && (cf[i] & kSem);
+            const unsigned m = __ballot_sync(0xffffffffu, in);
+            int o = 0;
+            if (lane == 0 && m) o = atomicAdd(&sem_n_s, __popc(m));
+            o = __shfl_sync(0xffffffffu, o, 0) + __popc(m & ((1u << lane) - 1u));
+            if (in) sem_out[o] = cid[i];
+        }
     }
     // 3. ordered prefix S_sem[:n_graph_sem_seeds]: select, then rank inside
     const int ngs = min(n_graph_sem_seeds, min(n_sem, kMaxG));
