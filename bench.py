@@ -193,7 +193,7 @@ def run_ours(args):
     staticd, rpd, cold, seedsd = tdev(static), tdev(row_ptr), tdev(col), tdev(seeds)
     nmax = c["n_static"] + c["n_dyn"]
     ctx = es.Context(V=V, d=d, w_dtype=bf, h_dtype=bf, n_shards=world, shard_rank=rank,
-                     max_subset=nmax, max_rows=n_h, max_k=k, max_sem=c["n_sem"], max_seeds=32, device=local)
+                     max_subset=V, max_rows=n_h, max_k=k, max_sem=c["n_sem"], max_seeds=32, device=local)
     if world > 1:
         ctx.comm_init()
     ctx.prepare_weights(Wd)
@@ -265,6 +265,9 @@ def run_ours(args):
     d2h = sum(t.numel() * t.element_size() for t in out_h)
 
     flags = ctx.get_flags()
+    sweep = None
+    if world == 1 and not args.no_sweep:
+        sweep = subset_sweep(ctx, Wd, Hd, n_h, k, V, d, dev, args)
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -311,11 +314,45 @@ def run_ours(args):
                 e2e=dict(value=tokens / (ms_e2e * 1e-3), unit="tokens/s", h2d_bytes_per_step=h2d,
                          d2h_bytes_per_step=d2h),
                 gpu_launches=launches, clocks=clk, breakdown=breakdown, device_flags=flags,
-                lmh_tokens_per_s=n_h / (per["lmh"] + per["finalize"] + per["merge"]) * 1e3 if per["lmh"] else None)
+                lmh_tokens_per_s=n_h / (per["lmh"] + per["finalize"] + per["merge"]) * 1e3 if per["lmh"] else None,
+                subset_sweep=sweep)
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def subset_sweep(ctx, Wd, Hd, n_h, k, V, d, dev, args):
+    """Draft LM-head tokens/s and HBM GB/s vs subset size (the metric's x-axis):
+    subset_logits_topk + merge_shards on a seeded sorted subset of n_S ids,
+    L2 flushed (256 MB write) before every timed iteration, CUDA events around
+    the LM-head calls only."""
+    import torch
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    out = []
+    rng = np.random.default_rng(11)
+    for n_S in (8192, 16384, 36864, 65536, V):
+        S = np.sort(rng.permutation(V)[:n_S]).astype(np.int32)
+        Sd = torch.from_numpy(S).to(dev)
+        nd = torch.tensor([n_S], dtype=torch.int32, device=dev)
+        trip = None
+        times = []
+        for it in range(args.warmup + args.sweep_steps):
+            flush.fill_(it & 0xFF)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            trip = ctx.subset_logits_topk(Wd, Hd, Sd, nd, n_S, k, out=trip)
+            ctx.merge_shards(*trip, n_h=n_h, k=k)
+            e1.record()
+            torch.cuda.synchronize()
+            if it >= args.warmup:
+                times.append(e0.elapsed_time(e1))
+        t = statistics.median(times) * 1e-3
+        nbytes = n_S * d * 2 + n_h * d * 2 + n_S * 4
+        out.append(dict(n_S=n_S, us=t * 1e6, tokens_per_s=n_h / t, GBps=nbytes / t / 1e9,
+                        frac_of_copy_peak=nbytes / t / 1e9 / load_peaks()["hbm_gbs"]))
+    del flush
+    return out
 
 
 def main():
@@ -325,6 +362,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--sweep-steps", type=int, default=10)
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

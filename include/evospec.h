@@ -253,6 +253,11 @@ evospec_status evospec_set_timing(evospec_ctx *ctx, int enable);
 /* Synchronises the recorded events and returns the sums since the last
  * evospec_set_timing(ctx, 1). The launch counter runs always. */
 evospec_status evospec_read_stats(evospec_ctx *ctx, evospec_stats *out);
+/* Profiling: with EVOSPEC_TRACE set in the environment, the tcgen05 LM-head
+ * kernel stamps %globaltimer (ns) per CTA into 8 slots [start, producers
+ * done, MMA done, tile-0 accumulator ready, tile-0 folded, tile-1 ready,
+ * tile-1 folded, end]; this copies the first n int64 (synchronous). */
+evospec_status evospec_read_trace(evospec_ctx *ctx, int64_t *host_out, int32_t n);
 
 #ifdef __cplusplus
 }

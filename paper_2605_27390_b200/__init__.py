@@ -26,7 +26,7 @@ EXPORTED = [
     "evospec_version", "evospec_prepare_weights", "evospec_get_flags",
     "evospec_comm_unique_id", "evospec_comm_init", "evospec_build_subset",
     "evospec_last_semantic", "evospec_subset_logits_topk", "evospec_merge_shards",
-    "evospec_draft_step", "evospec_set_timing", "evospec_read_stats",
+    "evospec_draft_step", "evospec_set_timing", "evospec_read_stats", "evospec_read_trace",
 ]
 
 STAGES = ["scan", "select", "union", "lmh", "finalize", "merge", "copy"]
@@ -100,6 +100,7 @@ def lib() -> C.CDLL:
             "evospec_draft_step": ([vp, C.POINTER(StepIO), vp], i32),
             "evospec_set_timing": ([vp, C.c_int], i32),
             "evospec_read_stats": ([vp, C.POINTER(Stats)], i32),
+            "evospec_read_trace": ([vp, vp, i32], i32),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, name)
@@ -177,6 +178,12 @@ class Context:
         return dict(launches=st.launches,
                     calls={n: st.calls[i] for i, n in enumerate(STAGES)},
                     ms={n: st.stage_ms[i] for i, n in enumerate(STAGES)})
+
+    def read_trace(self, n_cta: int = 148):
+        import numpy as np
+        out = np.zeros(n_cta * 8, dtype=np.int64)
+        _check(lib().evospec_read_trace(self._h, out.ctypes.data_as(C.c_void_p), out.size))
+        return out.reshape(n_cta, 8)
 
     def get_flags(self, clear: bool = True, stream=None) -> int:
         out = C.c_int32(0)

@@ -145,6 +145,7 @@ struct evospec_ctx {
     ncclComm_t comm = nullptr;
     // measurement hooks
     int64_t launches = 0;
+    long long* trace = nullptr;   // EVOSPEC_TRACE=1: per-CTA LM-head stamps [148][8]
     bool timing = false;
     std::vector<cudaEvent_t> ev;   // [stage][slot][2]
     int ev_count[EVOSPEC_NUM_STAGES] = {0};
@@ -205,6 +206,7 @@ evospec_status evospec_destroy(evospec_ctx* ctx) {
         if (p) cudaFree(p);
     if (ctx->comm && nccl().loaded) nccl().CommDestroy(ctx->comm);
     for (cudaEvent_t e : ctx->ev) cudaEventDestroy(e);
+    if (ctx->trace) cudaFree(ctx->trace);
     delete ctx;
     return EVOSPEC_OK;
 }
@@ -462,6 +464,11 @@ evospec_status evospec_subset_logits_topk(evospec_ctx* ctx, const void* W, int64
     a.R = c.n_shards; a.KP = k + kTopkPad; a.inv_temp = inv_temp;
     a.logits_out = logits_out;
     a.part = ctx->part;
+    if (getenv("EVOSPEC_TRACE")) {
+        if (!ctx->trace) CUDA_TRY(cudaMalloc(&ctx->trace, 2 * kNumSMs * 8 * sizeof(long long)));
+        CUDA_TRY(cudaMemsetAsync(ctx->trace, 0, 2 * kNumSMs * 8 * sizeof(long long), st));
+        a.trace = ctx->trace;
+    }
     int n_cta = 0;
     float gamma = gemv_gamma(c.d);
     {
@@ -602,6 +609,13 @@ evospec_status evospec_read_stats(evospec_ctx* ctx, evospec_stats* out) {
         }
         out->stage_ms[s] = (float)sum;
     }
+    return EVOSPEC_OK;
+}
+
+evospec_status evospec_read_trace(evospec_ctx* ctx, int64_t* host_out, int32_t n) {
+    if (!ctx || !host_out || n < 0 || n > 2 * kNumSMs * 8) return fail(EVOSPEC_EINPUT, "read_trace: bad argument");
+    if (!ctx->trace) return fail(EVOSPEC_EINPUT, "read_trace: run with EVOSPEC_TRACE=1");
+    CUDA_TRY(cudaMemcpy(host_out, ctx->trace, (size_t)n * sizeof(long long), cudaMemcpyDeviceToHost));
     return EVOSPEC_OK;
 }
 

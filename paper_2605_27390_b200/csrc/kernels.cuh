@@ -55,6 +55,7 @@ struct LmhArgs {
     const int32_t* subset; const int* n_subset_dev; int n_subset_max;
     int R; int KP; float inv_temp;
     float* logits_out;  // optional [n_h][n_subset_max]
+    long long* trace;   // optional per-CTA globaltimer stamps [n_cta][8] (profiling)
     LmhPartials part;
 };
 // returns the number of CTAs whose partials were written

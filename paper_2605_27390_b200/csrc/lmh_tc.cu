@@ -9,16 +9,19 @@
 // (A, K-major), N is the tree width padded to a multiple of 16 (B = H,
 // K-major), the fp32 accumulator D[128 x N] lives in TMEM.
 //
-// Persistent, warp-specialised CTA per SM (6 warps):
-//   warp 0  TMA producer: per 64-column k-block, 32 x cp.async.bulk.tensor
-//           .tile::gather4 (4 W rows each, one per lane) + one 2D tile of H
-//           into a 128B-swizzled smem stage; mbarrier complete_tx.
-//   warp 1  TMEM allocator + MMA issuer (one elected thread):
+// Persistent, warp-specialised CTA per SM (13 warps):
+//   warps 0-3  producers: 16-byte cp.async of the gathered W rows into a
+//           128B-swizzled smem stage (swizzle applied in the address), one
+//           cp.async.mbarrier.arrive.noinc per thread; an L2 bulk prefetch runs
+//           1 KB windows ahead per row; H by one 2D TMA tile per stage.
+//   warp 4  TMEM allocator + MMA issuer (one elected thread):
 //           4 x tcgen05.mma.cta_group::1.kind::f16 (K = 16) per stage,
 //           tcgen05.commit frees the stage; double-buffered accumulators.
-//   warps 2-5  epilogue: tcgen05.ld 32x32b -> scale -> smem tile -> the
+//   warps 5-12 epilogue: tcgen05.ld 32x32b -> scale -> smem tile -> the
 //           shared online-softmax / top-k fold (lmh_epilogue.cuh) while the
-//           producer and MMA already stream the next tile.
+//           producers and MMA already stream the next tile.
+#include <cstdlib>
+
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -149,6 +152,13 @@ ES_DEV void tmem_ld16(uint32_t taddr, float (&v)[16]) {
     for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+ES_DEV long long gtime() {
+    long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define TC_TRACE(slot) do { if (a.trace) a.trace[(size_t)blockIdx.x * 8 + (slot)] = gtime(); } while (0)
+
 ES_DEV void named_bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
 // ------------------------------------------------------------------ kernel
@@ -157,6 +167,7 @@ struct TcParams {
     int stages;
     int nkb;         // d / 64
     uint32_t tmem_cols;
+    int pf_dist;     // L2 prefetch distance in 1 KB windows (0 = off)
     size_t off_b, off_epi, off_bar, off_rows;  // smem carve offsets
 };
 
@@ -201,6 +212,7 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    if (threadIdx.x == 0) TC_TRACE(0);
 
     auto tile_range = [&](int t, int& t0, int& tn) {
         const int a0 = p0 + (int)((long long)len * t / n_tiles);
@@ -234,8 +246,9 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
             const uint32_t sz = (uint32_t)min((size_t)kPfBytes, row_bytes - off);
             l2_prefetch(rp + off, sz);
         };
-        const char* pf_cur = n_tiles > 0 ? row_ptr_of(0, prow) : nullptr;
-        for (int w = 0; w < kPfDist && pf_cur; ++w) prefetch_win(pf_cur, w);
+        const int pf_dist = tp.pf_dist;
+        const char* pf_cur = n_tiles > 0 && pf_dist > 0 ? row_ptr_of(0, prow) : nullptr;
+        for (int w = 0; w < pf_dist && pf_cur; ++w) prefetch_win(pf_cur, w);
         int stage = 0;
         uint32_t phase = 0;
         for (int t = 0; t < n_tiles; ++t) {
@@ -250,12 +263,12 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
                 src[i] = (const char*)a.W + (size_t)(a.subset[pos] / a.R) * row_bytes + chunk * 16;
                 dsto[i] = (uint32_t)(row * 128 + ((chunk ^ (row & 7)) << 4));
             }
-            const char* pf_next = t + 1 < n_tiles ? row_ptr_of(t + 1, prow) : nullptr;
+            const char* pf_next = t + 1 < n_tiles && pf_dist > 0 ? row_ptr_of(t + 1, prow) : nullptr;
             for (int kb = 0; kb < tp.nkb; ++kb) {
                 // prefetch: window (kb/8 + kPfDist) of this tile; the next tile's first
                 // windows once this tile's remaining windows are all requested
-                if ((kb & 7) == 0) {
-                    const int w = (kb >> 3) + kPfDist;
+                if (pf_dist > 0 && (kb & 7) == 0) {
+                    const int w = (kb >> 3) + pf_dist;
                     if (w < n_win) prefetch_win(pf_cur, w);
                     else if (pf_next) prefetch_win(pf_next, w - n_win);
                 }
@@ -272,6 +285,7 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
             }
             pf_cur = pf_next;
         }
+        if (warp == 0 && lane == 0) TC_TRACE(1);
         (void)tmap_w;
     } else if (warp == kTcMmaWarp) {
         // ===== MMA issuer
@@ -301,6 +315,7 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
                 if (++stage == S) { stage = 0; phase ^= 1; }
             }
         }
+        if (lane == 0) TC_TRACE(2);
     } else {
         // ===== epilogue warps: TMEM lane quadrant = warp % 4; the two
         // warps of a quadrant split the accumulator columns (16-column chunks)
@@ -314,6 +329,7 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
             tile_range(t, t0, tn);
             const int b = t & 1;
             mbar_wait(&tfull[b], (uint32_t)(t >> 1) & 1);
+            if (ew == 0 && lane == 0 && t < 2) TC_TRACE(3 + 2 * t);
             tc_fence_after();
             const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(b * NP);
             for (int c0 = half * 16; c0 < NP; c0 += 32) {
@@ -332,6 +348,7 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
                         a.logits_out[(size_t)r * a.n_subset_max + t0 + p] = e.tile[r * kTile + p];
             }
             epi_tile(e, n_h, a.KP, tn, t0, ew, kTcEpiWarps);
+            if (ew == 0 && lane == 0 && t < 2) TC_TRACE(4 + 2 * t);
             named_bar_sync(1, nthr);
         }
         epi_store(e, a.part, blockIdx.x, a.n_h, 0, n_h, a.KP, a.subset, ew, kTcEpiWarps);
@@ -339,6 +356,7 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
+    if (threadIdx.x == 0) TC_TRACE(7);
     if (warp == kTcMmaWarp)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(tp.tmem_cols));
 }
@@ -380,6 +398,8 @@ cudaError_t launch_lmh_tc(const LmhArgs& a, cudaStream_t st) {
     TcParams tp{};
     tp.n_pad = ((a.n_h + 15) / 16) * 16;
     tp.nkb = a.d / kBlockK;
+    tp.pf_dist = kPfDist;
+    if (const char* e = getenv("EVOSPEC_PF")) tp.pf_dist = atoi(e);
     uint32_t cols = 2 * tp.n_pad, c = 32;
     while (c < cols) c <<= 1;
     tp.tmem_cols = c;

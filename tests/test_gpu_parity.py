@@ -244,3 +244,40 @@ def test_tc_integer_exact(lmh_path):
     ref = G.oracle_step(oracle, P)
     check(P, got, ref, P["k"])
     np.testing.assert_array_equal(got["logits"], oracle.subset_logits(P["W"], P["H"], ref["S"]))
+
+
+def test_ctx_count_source():
+    """Reading C5: context-count source (count >= min, (count desc, id asc), first n_ctx_max)."""
+    import synth
+    P = G.make_problem(13, dtype="bf16", V=30000, d=256, n_static=3000, n_sem=40, n_dyn=120, n_h=3, k=10)
+    ctx_ids = synth.ctx_tokens(14, P["V"], 900)
+    ctx = ctx_for(P, max_ctx=1024)
+    W = G.to_dev(P["W"], DEV)
+    ctx.prepare_weights(W)
+    ids, n, _, _ = ctx.build_subset(W, G.to_dev(P["q"], DEV), G.to_dev(P["static"], DEV),
+                                    G.to_dev(P["seeds"], DEV), G.to_dev(P["row_ptr"], DEV),
+                                    G.to_dev(P["col"], DEV), n_sem=P["n_sem"], n_dyn=P["n_dyn"],
+                                    n_graph_sem_seeds=2, per_seed=1,
+                                    ctx_ids=G.to_dev(ctx_ids, DEV), ctx_min_count=2, n_ctx_max=64)
+    torch.cuda.synchronize()
+    ref = oracle.build_subset(P["W"], P["q"], P["static"], P["seeds"], P["row_ptr"], P["col"],
+                              n_sem=P["n_sem"], n_dyn=P["n_dyn"], n_graph_sem_seeds=2, per_seed=1,
+                              ctx_ids=ctx_ids, ctx_min_count=2, n_ctx_max=64)
+    np.testing.assert_array_equal(ids[:int(n.item())].cpu().numpy(), ref["S"])
+    # the ctx source contributed (cap not reached by seeds + sem + graph alone)
+    ref0 = oracle.build_subset(P["W"], P["q"], P["static"], P["seeds"], P["row_ptr"], P["col"],
+                               n_sem=P["n_sem"], n_dyn=P["n_dyn"], n_graph_sem_seeds=2, per_seed=1)
+    assert ref["S"].size > ref0["S"].size
+    assert ctx.get_flags() == 0
+
+
+@pytest.mark.slow
+def test_qwen_full_size():
+    """Config Q (Qwen2.5-7B head): V=152064, d=3584, static 32768 + 4096, n_h=60."""
+    import synth
+    c = dict(synth.CONFIGS["qwen"])
+    P = G.make_problem(1, **c)
+    got = run_path(P)
+    ref = G.oracle_step(oracle, P)
+    assert got["S"].size == 32768 + 4096
+    check(P, got, ref, c["k"])

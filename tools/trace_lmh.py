@@ -1,0 +1,51 @@
+"""Phase trace of the tcgen05 LM-head kernel on the llama config (profiling aid).
+
+Runs subset_logits_topk on n_S = 36,864 gathered rows, n_h = 60, with
+EVOSPEC_TRACE=1 and prints per-CTA globaltimer phases (us, relative to the
+earliest CTA start), for each EVOSPEC_PF prefetch distance given on argv.
+"""
+import os
+import statistics
+import sys
+
+os.environ["EVOSPEC_TRACE"] = "1"
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+
+import paper_2605_27390_b200 as es
+import synth
+
+V, d, n_h, k, n_S = 128256, 4096, 60, 10, 36864
+W = synth.matrix(0, V, d, 0.02, "bf16")
+H = synth.matrix(1, n_h, d, 1.0, "bf16")
+Wd = torch.from_numpy(W.view(np.int16)).view(torch.bfloat16).cuda()
+Hd = torch.from_numpy(H.view(np.int16)).view(torch.bfloat16).cuda()
+S = np.sort(np.random.default_rng(11).permutation(V)[:n_S]).astype(np.int32)
+Sd = torch.from_numpy(S).cuda()
+nd = torch.tensor([n_S], dtype=torch.int32, device="cuda")
+ctx = es.Context(V=V, d=d, w_dtype=torch.bfloat16, h_dtype=torch.bfloat16, max_subset=V, max_rows=n_h, max_k=k,
+                 max_sem=8192)
+ctx.prepare_weights(Wd)
+flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+names = ["start", "prod_done", "mma_done", "t0_ready", "t0_fold", "t1_ready", "t1_fold", "end"]
+for pf in (sys.argv[1:] or ["2"]):
+    os.environ["EVOSPEC_PF"] = pf
+    times = []
+    for it in range(8):
+        flush.fill_(it)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        ctx.subset_logits_topk(Wd, Hd, Sd, nd, n_S, k)
+        e1.record()
+        torch.cuda.synchronize()
+        times.append(e0.elapsed_time(e1) * 1e3)
+    tr = ctx.read_trace(148).astype(np.float64)
+    t0 = tr[:, 0].min()
+    rel = (tr - t0) / 1e3
+    print(f"PF={pf}: kernel+finalize median {statistics.median(times[2:]):.1f} us")
+    for j, n in enumerate(names):
+        col = rel[:, j]
+        col = col[tr[:, j] > 0]
+        if col.size:
+            print(f"   {n:10s} min {col.min():7.1f}  med {np.median(col):7.1f}  max {col.max():7.1f}")
