@@ -25,6 +25,14 @@ namespace es {
 
 constexpr int kFinThreads = 256;
 
+ES_DEV long long fin_gtime() {
+    long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+// profiling stamps (EVOSPEC_TRACE): slots [148*8 + row*8 + i]
+#define FIN_TRACE(slot) do { if (a.trace && blockIdx.x < 148) a.trace[148 * 8 + (size_t)blockIdx.x * 8 + (slot)] = fin_gtime(); } while (0)
+
 ES_DEV double load_elem(const void* p, int dtype, size_t i) {
     return dtype == 0 ? (double)bf16_bits_to_f32(((const uint16_t*)p)[i]) : (double)((const float*)p)[i];
 }
@@ -35,6 +43,7 @@ lmh_finalize_kernel(LmhArgs a, int n_cta, int k, float gamma, const float* __res
                     float* __restrict__ row_max, float* __restrict__ row_sumexp, int* flags) {
     const int r = blockIdx.x;
     const int KP = a.KP;
+    if (threadIdx.x == 0) FIN_TRACE(0);
     const int lane = lane_id(), warp = warp_id(), nwarps = blockDim.x / 32;
     extern __shared__ unsigned char f_sm[];
     int* head = (int*)f_sm;                         // [n_cta]
@@ -81,6 +90,7 @@ lmh_finalize_kernel(LmhArgs a, int n_cta, int k, float gamma, const float* __res
         if (lane == 0) red_d[warp] = acc;
     }
     __syncthreads();
+    if (threadIdx.x == 0) FIN_TRACE(1);
     if (threadIdx.x == 0) {
         double hn = 0.0;
         for (int w = 0; w < nwarps; ++w) hn += red_d[w];
@@ -120,6 +130,7 @@ lmh_finalize_kernel(LmhArgs a, int n_cta, int k, float gamma, const float* __res
         }
     }
     __syncthreads();
+    if (threadIdx.x == 0) FIN_TRACE(2);
     if (threadIdx.x == 0) {
         float s_all = 0.0f;
         int t_all = 0;
@@ -190,6 +201,7 @@ lmh_finalize_kernel(LmhArgs a, int n_cta, int k, float gamma, const float* __res
         if (lane == 0) n_kept_s = produced;
     }
     __syncthreads();
+    if (threadIdx.x == 0) FIN_TRACE(3);
     const int nk = n_kept_s;
     // 3. runs of candidates closer than 2 delta that reach into the top k
     if (threadIdx.x == 0) {
@@ -214,6 +226,7 @@ lmh_finalize_kernel(LmhArgs a, int n_cta, int k, float gamma, const float* __res
         if (uncertain) atomicOr(flags, kFlagUncertified);
     }
     __syncthreads();
+    if (threadIdx.x == 0) FIN_TRACE(4);
     // exact re-score of the flagged candidates (one warp per candidate)
     const int nn = n_need_s;
     for (int q = warp; q < nn; q += nwarps) {
@@ -249,6 +262,7 @@ lmh_finalize_kernel(LmhArgs a, int n_cta, int k, float gamma, const float* __res
         if (lane == 0) c_e[c] = acc * (double)a.inv_temp;
     }
     __syncthreads();
+    if (threadIdx.x == 0) FIN_TRACE(5);
     // 4. order each re-scored run exactly, write the top k
     if (threadIdx.x == 0) {
         for (int i = 0; i < nk; ++i)
@@ -273,6 +287,8 @@ lmh_finalize_kernel(LmhArgs a, int n_cta, int k, float gamma, const float* __res
             topk_ids[(size_t)r * k + t] = t < nk ? c_id[t] : -1;
             topk_vals[(size_t)r * k + t] = t < nk ? (float)c_e[t] : -INFINITY;
         }
+        FIN_TRACE(6);
+        if (a.trace && blockIdx.x < 148) a.trace[148 * 8 + (size_t)blockIdx.x * 8 + 7] = nn;   // re-scored count
     }
 }
 

@@ -33,22 +33,27 @@ struct EpiSmem {
     float* st_val;   // [n_h][KP]
     int* st_pos;     // [n_h][KP]
     int* st_cnt;     // [n_h]
-    float* st_m;     // [n_h]
-    float* st_s;     // [n_h]
+    float* st_m;     // [n_h]   running max
+    float* st_ls;    // [n_h][32] per-lane partial sum of exp(z - m)
+    float* scr_v;    // [n_warps][32] candidate batch scratch
+    int* scr_p;      // [n_warps][32]
 };
 
-__host__ __device__ inline size_t epi_smem_bytes(int n_h, int KP) {
-    return (size_t)n_h * kTile * 4 + (size_t)n_h * KP * 8 + (size_t)n_h * 12;
+__host__ __device__ inline size_t epi_smem_bytes(int n_h, int KP, int n_warps) {
+    return (size_t)n_h * kTile * 4 + (size_t)n_h * KP * 8 + (size_t)n_h * 8 + (size_t)n_h * 32 * 4 +
+           (size_t)n_warps * 32 * 8;
 }
 
-ES_DEV EpiSmem epi_carve(unsigned char* p, int n_h, int KP) {
+ES_DEV EpiSmem epi_carve(unsigned char* p, int n_h, int KP, int n_warps) {
     EpiSmem e;
     e.tile = (float*)p;        p += (size_t)n_h * kTile * 4;
     e.st_val = (float*)p;      p += (size_t)n_h * KP * 4;
     e.st_pos = (int*)p;        p += (size_t)n_h * KP * 4;
     e.st_cnt = (int*)p;        p += (size_t)n_h * 4;
     e.st_m = (float*)p;        p += (size_t)n_h * 4;
-    e.st_s = (float*)p;
+    e.st_ls = (float*)p;       p += (size_t)n_h * 32 * 4;
+    e.scr_v = (float*)p;       p += (size_t)n_warps * 32 * 4;
+    e.scr_p = (int*)p;
     return e;
 }
 
@@ -56,8 +61,8 @@ ES_DEV void epi_init(const EpiSmem& e, int n_h) {
     for (int r = threadIdx.x; r < n_h; r += blockDim.x) {
         e.st_cnt[r] = 0;
         e.st_m[r] = -INFINITY;
-        e.st_s[r] = 0.0f;
     }
+    for (int i = threadIdx.x; i < n_h * 32; i += blockDim.x) e.st_ls[i] = 0.0f;
 }
 
 // KP-th largest value (1-based) of the 32 lane values, every lane gets it.
@@ -85,6 +90,109 @@ struct TopList {
     int p[SLOTS];
 };
 
+// Online softmax for one row: lazy max (a warp reduction only when some value
+// exceeds the running max), per-lane partial sums of exp(z - m) kept in smem
+// and reduced across the warp only once, in epi_store.
+ES_DEV void fold_softmax(const EpiSmem& e, int r, const float (&v)[kTileJ], float lane_max) {
+    const int lane = lane_id();
+    const float m_old = e.st_m[r];
+    float m_new = m_old, scale = 1.0f;
+    if (__any_sync(0xffffffffu, lane_max > m_old)) {
+        m_new = fmaxf(m_old, warp_max(lane_max));
+        scale = m_old == -INFINITY ? 0.0f : expf(m_old - m_new);
+    }
+    float acc = e.st_ls[r * 32 + lane] * scale;
+#pragma unroll
+    for (int j = 0; j < kTileJ; ++j)
+        if (v[j] != -INFINITY) acc += expf(v[j] - m_new);
+    e.st_ls[r * 32 + lane] = acc;
+    __syncwarp();
+    if (lane == 0) e.st_m[r] = m_new;
+}
+
+// Descending bitonic sort of 32 (value, position) pairs, one per lane, under
+// (value desc, position asc).
+ES_DEV void warp_sort32(float& v, int& p) {
+    const int lane = lane_id();
+#pragma unroll
+    for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            const float ov = __shfl_xor_sync(0xffffffffu, v, j);
+            const int op = __shfl_xor_sync(0xffffffffu, p, j);
+            const bool keep_better = ((lane & j) == 0) == ((lane & k) == 0);
+            const bool o_better = before(ov, op, v, p);
+            if (keep_better == o_better) { v = ov; p = op; }
+        }
+    }
+}
+
+// Top-KP fold for KP <= 32: candidates above the threshold are compacted
+// into batches of 32, each batch bitonic-sorted and merged into the sorted
+// register list with one bitonic merge -- no per-candidate shuffle chains.
+ES_DEV void fold_topk32(const EpiSmem& e, int r, int KP, int tn, int base_pos, int warp,
+                        const float (&v)[kTileJ], float lane_max) {
+    const int lane = lane_id();
+    int cnt = e.st_cnt[r];
+    float Lv = lane < cnt ? e.st_val[r * KP + lane] : -INFINITY;
+    int Lp = lane < cnt ? e.st_pos[r * KP + lane] : 0x7fffffff;
+    float tv = -INFINITY;
+    int tp = 0x7fffffff;
+    float theta0 = -INFINITY;
+    if (cnt == KP) {
+        tv = __shfl_sync(0xffffffffu, Lv, KP - 1);
+        tp = __shfl_sync(0xffffffffu, Lp, KP - 1);
+        if (!__any_sync(0xffffffffu, lane_max >= tv)) return;   // nothing can enter
+    } else {
+        theta0 = warp_kth_largest(lane_max, KP);
+    }
+    bool cand[kTileJ];
+    unsigned msk[kTileJ];
+    int total = 0;
+#pragma unroll
+    for (int j = 0; j < kTileJ; ++j) {
+        const int pj = base_pos + lane + 32 * j;
+        cand[j] = v[j] != -INFINITY && v[j] >= theta0 && (cnt < KP || before(v[j], pj, tv, tp));
+        msk[j] = __ballot_sync(0xffffffffu, cand[j]);
+        total += __popc(msk[j]);
+    }
+    if (total == 0) return;
+    float* sv = e.scr_v + warp * 32;
+    int* sp = e.scr_p + warp * 32;
+    for (int done = 0; done < total; done += 32) {
+        int base = 0;
+#pragma unroll
+        for (int j = 0; j < kTileJ; ++j) {
+            const int idx = base + __popc(msk[j] & ((1u << lane) - 1u)) - done;
+            if (cand[j] && idx >= 0 && idx < 32) { sv[idx] = v[j]; sp[idx] = base_pos + lane + 32 * j; }
+            base += __popc(msk[j]);
+        }
+        __syncwarp();
+        const int nb = min(32, total - done);
+        float bv = lane < nb ? sv[lane] : -INFINITY;
+        int bp = lane < nb ? sp[lane] : 0x7fffffff;
+        __syncwarp();
+        warp_sort32(bv, bp);
+        // top 32 of (list desc) u (batch desc): elementwise best against the
+        // reversed batch gives a bitonic sequence; one bitonic merge sorts it
+        const float rv = __shfl_sync(0xffffffffu, bv, 31 - lane);
+        const int rp = __shfl_sync(0xffffffffu, bp, 31 - lane);
+        if (before(rv, rp, Lv, Lp)) { Lv = rv; Lp = rp; }
+#pragma unroll
+        for (int j = 16; j > 0; j >>= 1) {
+            const float ov = __shfl_xor_sync(0xffffffffu, Lv, j);
+            const int op = __shfl_xor_sync(0xffffffffu, Lp, j);
+            const bool keep_better = (lane & j) == 0;
+            if (keep_better == before(ov, op, Lv, Lp)) { Lv = ov; Lp = op; }
+        }
+        cnt = min(cnt + nb, KP);
+    }
+    if (lane < cnt) { e.st_val[r * KP + lane] = Lv; e.st_pos[r * KP + lane] = Lp; }
+    if (lane == 0) e.st_cnt[r] = cnt;
+    __syncwarp();
+    (void)tn;
+}
+
 // Fold one row's tile values into its sorted top-KP list (SLOTS*32 >= KP).
 template <int SLOTS>
 ES_DEV void fold_row(const EpiSmem& e, int r, int KP, int tn, int base_pos) {
@@ -100,14 +208,6 @@ ES_DEV void fold_row(const EpiSmem& e, int r, int KP, int tn, int base_pos) {
     const float lane_max = mx;
     mx = warp_max(mx);
     if (tn <= 0) return;
-    // online softmax
-    const float m_old = e.st_m[r];
-    const float m_new = fmaxf(m_old, mx);
-    float acc = 0.0f;
-#pragma unroll
-    for (int j = 0; j < kTileJ; ++j)
-        if (v[j] != -INFINITY) acc += expf(v[j] - m_new);
-    acc = warp_sum(acc);
     // load the list
     int cnt = e.st_cnt[r];
     TopList<SLOTS> L;
@@ -118,10 +218,6 @@ ES_DEV void fold_row(const EpiSmem& e, int r, int KP, int tn, int base_pos) {
         L.p[s] = i < cnt ? e.st_pos[r * KP + i] : 0x7fffffff;
     }
     __syncwarp();
-    if (lane == 0) {
-        e.st_s[r] = e.st_s[r] * (m_old == -INFINITY ? 0.0f : expf(m_old - m_new)) + acc;
-        e.st_m[r] = m_new;
-    }
     const int kl = (KP - 1) & 31, ks = (KP - 1) >> 5;   // holder of entry KP-1
     auto kth = [&](float& tv, int& tp) {
         float cv = L.v[0];
@@ -186,8 +282,19 @@ ES_DEV void fold_row(const EpiSmem& e, int r, int KP, int tn, int base_pos) {
 // Fold the current tile (tn valid positions starting at global position
 // base_pos) into the state of rows r = warp, warp + n_warps, ...
 ES_DEV void epi_tile(const EpiSmem& e, int n_h, int KP, int tn, int base_pos, int warp, int n_warps) {
+    if (tn <= 0) return;
+    const int lane = lane_id();
     for (int r = warp; r < n_h; r += n_warps) {
-        if (KP <= 32) fold_row<1>(e, r, KP, tn, base_pos);
+        float v[kTileJ];
+        float lm = -INFINITY;
+#pragma unroll
+        for (int j = 0; j < kTileJ; ++j) {
+            const int p = lane + 32 * j;
+            v[j] = p < tn ? e.tile[r * kTile + p] : -INFINITY;
+            lm = fmaxf(lm, v[j]);
+        }
+        fold_softmax(e, r, v, lm);
+        if (KP <= 32) fold_topk32(e, r, KP, tn, base_pos, warp, v, lm);
         else if (KP <= 64) fold_row<2>(e, r, KP, tn, base_pos);
         else fold_row<3>(e, r, KP, tn, base_pos);
     }
@@ -203,10 +310,11 @@ ES_DEV void epi_store(const EpiSmem& e, const LmhPartials& P, int cta, int n_h_t
             P.val[o * KP + i] = i < cnt ? e.st_val[r * KP + i] : -INFINITY;
             P.id[o * KP + i] = i < cnt ? subset[e.st_pos[r * KP + i]] : -1;
         }
+        const float ssum = warp_sum(e.st_ls[r * 32 + lane_id()]);
         if (lane_id() == 0) {
             P.cnt[o] = cnt;
             P.m[o] = e.st_m[r];
-            P.s[o] = e.st_s[r];
+            P.s[o] = ssum;
         }
     }
 }

@@ -65,7 +65,7 @@ lmh_gemv_kernel(LmhArgs a, int h_row0) {
     const int d = a.d;
     const int n_chunks = (d + 32 * ELEMS - 1) / (32 * ELEMS);
     float* H_sm = (float*)g_sm;                              // [NH][n_chunks][ELEMS][32]
-    EpiSmem e = epi_carve(g_sm + (size_t)NH * n_chunks * ELEMS * 32 * 4, NH, a.KP);
+    EpiSmem e = epi_carve(g_sm + (size_t)NH * n_chunks * ELEMS * 32 * 4, NH, a.KP, kGemvWarps);
     const int lane = lane_id(), warp = warp_id();
 
     for (int i = threadIdx.x; i < NH * n_chunks * ELEMS * 32; i += blockDim.x) {
@@ -162,7 +162,7 @@ template <int DT, int NH>
 static size_t smem_t(const LmhArgs& a) {
     const int elems = DT == 0 ? 8 : 4;
     const int n_chunks = (a.d + 32 * elems - 1) / (32 * elems);
-    return (size_t)NH * n_chunks * elems * 32 * 4 + epi_smem_bytes(NH, a.KP);
+    return (size_t)NH * n_chunks * elems * 32 * 4 + epi_smem_bytes(NH, a.KP, kGemvWarps);
 }
 
 template <int DT, int NH>

@@ -180,7 +180,7 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
     const int S = tp.stages, NP = tp.n_pad, n_h = a.n_h;
     unsigned char* smA = base;                                   // [S][128][128 B]
     unsigned char* smB = base + tp.off_b;                        // [S][NP][128 B]
-    EpiSmem e = epi_carve(base + tp.off_epi, n_h, a.KP);
+    EpiSmem e = epi_carve(base + tp.off_epi, n_h, a.KP, kTcEpiWarps);
     uint64_t* full = (uint64_t*)(base + tp.off_bar);             // [S]
     uint64_t* empty = full + S;                                  // [S]
     uint64_t* tfull = empty + S;                                 // [2]
@@ -404,7 +404,7 @@ cudaError_t launch_lmh_tc(const LmhArgs& a, cudaStream_t st) {
     while (c < cols) c <<= 1;
     tp.tmem_cols = c;
     const size_t stage_a = (size_t)kTileM * 128, stage_b = (size_t)tp.n_pad * 128;
-    const size_t epi = epi_smem_bytes(a.n_h, a.KP);
+    const size_t epi = epi_smem_bytes(a.n_h, a.KP, kTcEpiWarps);
     const size_t fixed = epi + 2 * 128 * 4 + 64 * 8 + 1024 /*align slack*/ + 256;
     const size_t budget = 227 * 1024;
     int S = (int)((budget - fixed) / (stage_a + stage_b));

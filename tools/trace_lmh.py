@@ -40,7 +40,9 @@ for pf in (sys.argv[1:] or ["2"]):
         e1.record()
         torch.cuda.synchronize()
         times.append(e0.elapsed_time(e1) * 1e3)
-    tr = ctx.read_trace(148).astype(np.float64)
+    full = ctx.read_trace(296).astype(np.float64)
+    tr = full[:148]
+    fin = full[148:148 + n_h]
     t0 = tr[:, 0].min()
     rel = (tr - t0) / 1e3
     print(f"PF={pf}: kernel+finalize median {statistics.median(times[2:]):.1f} us")
@@ -49,3 +51,8 @@ for pf in (sys.argv[1:] or ["2"]):
         col = col[tr[:, j] > 0]
         if col.size:
             print(f"   {n:10s} min {col.min():7.1f}  med {np.median(col):7.1f}  max {col.max():7.1f}")
+    frel = (fin[:, :7] - t0) / 1e3
+    for j, n in enumerate(["fin_start", "fin_hnorm", "fin_stage", "fin_merge", "fin_runs", "fin_rescore", "fin_end"]):
+        col = frel[:, j]
+        print(f"   {n:10s} min {col.min():7.1f}  med {np.median(col):7.1f}  max {col.max():7.1f}")
+    print("   rescored per row: mean", fin[:, 7].mean(), "max", fin[:, 7].max())
