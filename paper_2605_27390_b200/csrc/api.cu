@@ -153,6 +153,14 @@ struct evospec_ctx {
 
 namespace {
 constexpr int kTimingSlots = 4096;
+constexpr int kTraceLen = 2 * kNumSMs * 8 + 16;   // LM-head CTAs, finalize rows, union stamps
+
+// union stamps live after the LM-head / finalize slots
+long long* union_trace(evospec_ctx* ctx, cudaStream_t st) {
+    if (!getenv("EVOSPEC_TRACE")) return nullptr;
+    if (!ctx->trace && cudaMalloc(&ctx->trace, kTraceLen * sizeof(long long)) != cudaSuccess) return nullptr;
+    return ctx->trace + 2 * kNumSMs * 8;
+}
 
 // Records a start/end CUDA event pair around a stage when timing is on.
 struct StageTimer {
@@ -399,7 +407,7 @@ evospec_status evospec_build_subset(evospec_ctx* ctx, const void* E, int64_t n_e
     launch_union(c.V, static_ids, n_static, seeds, n_seed, ctx->cand_s, ctx->cand_id, ctx->cand_count, ctx->cand_cap,
                  N, row_ptr, col, use_ctx ? ctx->ctx_sel : nullptr, ctx->ctx_n, p->n_graph_sem_seeds, p->per_seed,
                  p->n_dyn, R, r, out_ids, out_n, out_local_ids, out_local_n, ctx->sem_ids, ctx->sem_n,
-                 c.debug_checks, ctx->flags, st);
+                 c.debug_checks, ctx->flags, st, union_trace(ctx, st));
     LAUNCH_CHECK("union");
     return EVOSPEC_OK;
 }
@@ -465,7 +473,7 @@ evospec_status evospec_subset_logits_topk(evospec_ctx* ctx, const void* W, int64
     a.logits_out = logits_out;
     a.part = ctx->part;
     if (getenv("EVOSPEC_TRACE")) {
-        if (!ctx->trace) CUDA_TRY(cudaMalloc(&ctx->trace, 2 * kNumSMs * 8 * sizeof(long long)));
+        if (!ctx->trace) CUDA_TRY(cudaMalloc(&ctx->trace, kTraceLen * sizeof(long long)));
         CUDA_TRY(cudaMemsetAsync(ctx->trace, 0, 2 * kNumSMs * 8 * sizeof(long long), st));
         a.trace = ctx->trace;
     }
@@ -613,7 +621,7 @@ evospec_status evospec_read_stats(evospec_ctx* ctx, evospec_stats* out) {
 }
 
 evospec_status evospec_read_trace(evospec_ctx* ctx, int64_t* host_out, int32_t n) {
-    if (!ctx || !host_out || n < 0 || n > 2 * kNumSMs * 8) return fail(EVOSPEC_EINPUT, "read_trace: bad argument");
+    if (!ctx || !host_out || n < 0 || n > kTraceLen) return fail(EVOSPEC_EINPUT, "read_trace: bad argument");
     if (!ctx->trace) return fail(EVOSPEC_EINPUT, "read_trace: run with EVOSPEC_TRACE=1");
     CUDA_TRY(cudaMemcpy(host_out, ctx->trace, (size_t)n * sizeof(long long), cudaMemcpyDeviceToHost));
     return EVOSPEC_OK;

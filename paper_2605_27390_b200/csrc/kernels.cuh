@@ -39,7 +39,8 @@ void launch_union(int V, const int32_t* static_ids, int n_static, const int32_t*
                   const int32_t* ctx_sel, const int* n_ctx_sel_dev,
                   int n_graph_sem_seeds, int per_seed, int n_dyn, int R, int r,
                   int32_t* out_ids, int32_t* out_n, int32_t* out_local, int32_t* out_local_n,
-                  int32_t* sem_out, int* sem_out_n, int debug, int* flags, cudaStream_t st);
+                  int32_t* sem_out, int* sem_out_n, int debug, int* flags, cudaStream_t st,
+                  long long* trace = nullptr);
 
 // ---- LM head (lmh_gemv.cu, lmh_tc.cu)
 struct LmhPartials {

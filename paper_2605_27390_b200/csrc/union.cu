@@ -260,7 +260,8 @@ union_kernel(int V, const int32_t* __restrict__ static_ids, int n_static,
              int n_graph_sem_seeds, int per_seed, int n_dyn, int R, int r,
              int32_t* __restrict__ out_ids, int32_t* __restrict__ out_n,
              int32_t* __restrict__ out_local, int32_t* __restrict__ out_local_n,
-             int32_t* __restrict__ sem_out, int* __restrict__ sem_out_n, int debug, int* flags) {
+             int32_t* __restrict__ sem_out, int* __restrict__ sem_out_n, int debug, int* flags,
+             long long* __restrict__ trace) {
     extern __shared__ __align__(16) unsigned char u_sm[];
     const int nwords = (V + 31) / 32;
     uint64_t* ck = (uint64_t*)u_sm;                          // [cap]
@@ -278,6 +279,7 @@ union_kernel(int V, const int32_t* __restrict__ static_ids, int n_static,
 
     const int tid = threadIdx.x, lane = lane_id(), T = blockDim.x;
     const int n_cand = min(*n_cand_dev, cap);
+    if (trace) { __syncthreads(); if (threadIdx.x == 0) { long long t_; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); trace[0] = t_; } }
     for (int w = tid; w < nwords; w += T) bits[w] = 0;
     for (int i0 = 0; i0 < n_cand; i0 += 4 * T) {           // 4 independent loads in flight
         double sv[4];
@@ -316,6 +318,7 @@ union_kernel(int V, const int32_t* __restrict__ static_ids, int n_static,
             atomicOr(&bits[v[u] >> 5], 1u << (v[u] & 31));
         }
     }
+    if (trace) { __syncthreads(); if (threadIdx.x == 0) { long long t_; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); trace[1] = t_; } }
     // 2. S_sem = exact top-N of the candidate superset
     block_topM(ck, cid, cf, n_cand, kCand, kSem, n_sem, hist, bsel, warp_tot);
     if (sem_out) {
@@ -329,6 +332,7 @@ union_kernel(int V, const int32_t* __restrict__ static_ids, int n_static,
             if (in) sem_out[o] = cid[i];
         }
     }
+    if (trace) { __syncthreads(); if (threadIdx.x == 0) { long long t_; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); trace[2] = t_; } }
     // 3. ordered prefix S_sem[:n_graph_sem_seeds]: select, then rank inside
     const int ngs = min(n_graph_sem_seeds, min(n_sem, kMaxG));
     block_topM(ck, cid, cf, n_cand, kSem, kGs, ngs, hist, bsel, warp_tot);
@@ -351,6 +355,7 @@ union_kernel(int V, const int32_t* __restrict__ static_ids, int n_static,
         gs[rank] = cid[ia];
     }
     __syncthreads();
+    if (trace) { __syncthreads(); if (threadIdx.x == 0) { long long t_; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); trace[3] = t_; } }
     // 4. G = dedupe(seeds ++ S_sem[:ngs]) and S_graph (warp 0)
     if (warp_id() == 0) {
         const int nc = min(n_seed + ngs_found, kMaxG);
@@ -398,6 +403,7 @@ union_kernel(int V, const int32_t* __restrict__ static_ids, int n_static,
         }
     __syncthreads();
 
+    if (trace) { __syncthreads(); if (threadIdx.x == 0) { long long t_; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); trace[4] = t_; } }
     // 5. formation: seeds ++ S_sem ++ S_graph ++ S_ctx, first occurrence, skip
     //    members (static or taken), stop at N_dyn. Seeds, graph and ctx are
     //    walked by warp 0 in 32-wide windows; the S_sem part (distinct ids)
@@ -445,6 +451,7 @@ union_kernel(int V, const int32_t* __restrict__ static_ids, int n_static,
     }
     __syncthreads();
 
+    if (trace) { __syncthreads(); if (threadIdx.x == 0) { long long t_; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); trace[5] = t_; } }
     // 6. compaction: thread t owns words [t*nwords/T, (t+1)*nwords/T)
     const int w0 = (int)((long long)nwords * tid / T), w1 = (int)((long long)nwords * (tid + 1) / T);
     int cnt = 0, cnt_local = 0;
@@ -476,6 +483,7 @@ union_kernel(int V, const int32_t* __restrict__ static_ids, int n_static,
         if (total > n_static + n_dyn) atomicOr(flags, kFlagBudget);
         if (*n_cand_dev > cap) atomicOr(flags, kFlagSelectOverflow);
     }
+    if (trace) { __syncthreads(); if (threadIdx.x == 0) { long long t_; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); trace[6] = t_; } }
 }
 
 static size_t union_fixed_bytes(int V, int per_seed) {
@@ -497,13 +505,13 @@ void launch_union(int V, const int32_t* static_ids, int n_static, const int32_t*
                   const int32_t* ctx_sel, const int* n_ctx_sel_dev,
                   int n_graph_sem_seeds, int per_seed, int n_dyn, int R, int r,
                   int32_t* out_ids, int32_t* out_n, int32_t* out_local, int32_t* out_local_n,
-                  int32_t* sem_out, int* sem_out_n, int debug, int* flags, cudaStream_t st) {
+                  int32_t* sem_out, int* sem_out_n, int debug, int* flags, cudaStream_t st, long long* trace) {
     const size_t smem = (size_t)cap * 13 + union_fixed_bytes(V, per_seed) + 16;
     cudaFuncSetAttribute(union_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     union_kernel<<<1, kUnionThreads, smem, st>>>(V, static_ids, n_static, seeds, n_seed, cand_s, cand_id, n_cand_dev,
                                                   cap, n_sem, row_ptr, col, ctx_sel, n_ctx_sel_dev, n_graph_sem_seeds,
                                                   per_seed, n_dyn, R, r, out_ids, out_n, out_local, out_local_n,
-                                                  sem_out, sem_out_n, debug, flags);
+                                                  sem_out, sem_out_n, debug, flags, trace);
 }
 
 }  // namespace es
