@@ -256,7 +256,9 @@ evospec_status evospec_read_stats(evospec_ctx *ctx, evospec_stats *out);
 /* Profiling: with EVOSPEC_TRACE set in the environment, the tcgen05 LM-head
  * kernel stamps %globaltimer (ns) per CTA into 8 slots [start, producers
  * done, MMA done, tile-0 accumulator ready, tile-0 folded, tile-1 ready,
- * tile-1 folded, end]; this copies the first n int64 (synchronous). */
+ * tile-1 folded, end] (slots [0, 148*8)), the finalize kernel per H row
+ * (slots [148*8, 2*148*8)) and the union kernel 7 phase stamps (slots
+ * [2*148*8, +7)); this copies the first n int64 (synchronous). */
 evospec_status evospec_read_trace(evospec_ctx *ctx, int64_t *host_out, int32_t n);
 
 #ifdef __cplusplus

@@ -179,11 +179,12 @@ class Context:
                     calls={n: st.calls[i] for i, n in enumerate(STAGES)},
                     ms={n: st.stage_ms[i] for i, n in enumerate(STAGES)})
 
-    def read_trace(self, n_cta: int = 148):
+    def read_trace(self, n: int = 2 * 148 * 8 + 16):
+        """Flat int64 profiling stamps (EVOSPEC_TRACE=1); see include/evospec.h."""
         import numpy as np
-        out = np.zeros(n_cta * 8, dtype=np.int64)
+        out = np.zeros(n, dtype=np.int64)
         _check(lib().evospec_read_trace(self._h, out.ctypes.data_as(C.c_void_p), out.size))
-        return out.reshape(n_cta, 8)
+        return out
 
     def get_flags(self, clear: bool = True, stream=None) -> int:
         out = C.c_int32(0)

@@ -333,27 +333,67 @@ union_kernel(int V, const int32_t* __restrict__ static_ids, int n_static,
         }
     }
     if (trace) { __syncthreads(); if (threadIdx.x == 0) { long long t_; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); trace[2] = t_; } }
-    // 3. ordered prefix S_sem[:n_graph_sem_seeds]: select, then rank inside
+    // 3. ordered prefix S_sem[:n_graph_sem_seeds]: one 1024-bin histogram pass
+    //    over the S_sem key range finds the few candidates that can be in the
+    //    prefix; they are gathered and ranked exactly (block_topM fallback).
     const int ngs = min(n_graph_sem_seeds, min(n_sem, kMaxG));
-    block_topM(ck, cid, cf, n_cand, kSem, kGs, ngs, hist, bsel, warp_tot);
-    if (tid == 0) ngs_s = 0;
+    if (tid == 0) { ngs_s = 0; bsel.kmin = ~0ull; bsel.kmax = 0ull; bsel.found_bin = 0; bsel.found_above = 0x7fffffff; }
     __syncthreads();
-    for (int i = tid; i < n_cand; i += T)
-        if (cf[i] & kGs) {
-            const int slot = atomicAdd(&ngs_s, 1);
-            if (slot < kMaxG) graph[slot] = i;               // graph[] as scratch: candidate index
+    {
+        uint64_t kmn = ~0ull, kmx = 0ull;
+        for (int i = tid; i < n_cand; i += T)
+            if (cf[i] & kSem) { kmn = min(kmn, ck[i]); kmx = max(kmx, ck[i]); }
+        kmn = warp_min_u64(kmn);
+        kmx = warp_max_u64(kmx);
+        if (lane == 0 && kmn <= kmx) { atomicMin((unsigned long long*)&bsel.kmin, kmn); atomicMax((unsigned long long*)&bsel.kmax, kmx); }
+        for (int b = tid; b < kSelBins; b += T) hist[b] = 0;
+    }
+    __syncthreads();
+    const uint64_t gkmin = bsel.kmin, grange = bsel.kmax >= bsel.kmin ? bsel.kmax - bsel.kmin : 0ull;
+    const int gshift = grange ? max(0, 64 - __clzll((long long)grange) - 10) : 0;
+    if (ngs > 0) {
+        for (int base = 0; base < n_cand; base += T) {
+            const int i = base + tid;
+            uint32_t digit = 0xFFFFFFFFu;
+            if (i < n_cand && (cf[i] & kSem)) digit = (uint32_t)((ck[i] - gkmin) >> gshift);
+            const unsigned peers = __match_any_sync(0xffffffffu, digit);
+            if (digit != 0xFFFFFFFFu && lane == __ffs(peers) - 1) atomicAdd(&hist[digit], (uint32_t)__popc(peers));
         }
+        __syncthreads();
+        const int bin = kSelBins - 1 - tid;
+        const uint32_t hb = hist[bin];
+        int tot_unused;
+        const int above = block_excl_scan((int)hb, warp_tot, tot_unused);
+        if (above < ngs && above + (int)hb >= ngs) { bsel.found_bin = bin; bsel.found_above = above + (int)hb; }
+        __syncthreads();
+        const uint32_t bmin = (uint32_t)bsel.found_bin;
+        if (bsel.found_above <= kMaxG) {
+            for (int i = tid; i < n_cand; i += T)
+                if ((cf[i] & kSem) && (uint32_t)((ck[i] - gkmin) >> gshift) >= bmin) {
+                    const int slot = atomicAdd(&ngs_s, 1);
+                    if (slot < kMaxG) graph[slot] = i;      // graph[] as scratch: candidate index
+                }
+        } else {
+            block_topM(ck, cid, cf, n_cand, kSem, kGs, ngs, hist, bsel, warp_tot);
+            for (int i = tid; i < n_cand; i += T)
+                if (cf[i] & kGs) {
+                    const int slot = atomicAdd(&ngs_s, 1);
+                    if (slot < kMaxG) graph[slot] = i;
+                }
+        }
+    }
     __syncthreads();
-    const int ngs_found = min(ngs_s, kMaxG);
-    for (int a = tid; a < ngs_found; a += T) {
+    const int ngs_pool = min(ngs_s, kMaxG);
+    for (int a = tid; a < ngs_pool; a += T) {
         const int ia = graph[a];
         int rank = 0;
-        for (int b = 0; b < ngs_found; ++b) {
+        for (int b = 0; b < ngs_pool; ++b) {
             const int ib = graph[b];
             rank += before(ck[ib], cid[ib], ck[ia], cid[ia]) ? 1 : 0;   // (key desc, id asc)
         }
-        gs[rank] = cid[ia];
+        if (rank < ngs) gs[rank] = cid[ia];
     }
+    const int ngs_found = min(ngs, ngs_pool);
     __syncthreads();
     if (trace) { __syncthreads(); if (threadIdx.x == 0) { long long t_; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); trace[3] = t_; } }
     // 4. G = dedupe(seeds ++ S_sem[:ngs]) and S_graph (warp 0)
@@ -452,27 +492,37 @@ union_kernel(int V, const int32_t* __restrict__ static_ids, int n_static,
     __syncthreads();
 
     if (trace) { __syncthreads(); if (threadIdx.x == 0) { long long t_; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); trace[5] = t_; } }
-    // 6. compaction: thread t owns words [t*nwords/T, (t+1)*nwords/T)
-    const int w0 = (int)((long long)nwords * tid / T), w1 = (int)((long long)nwords * (tid + 1) / T);
+    // 6. compaction, one warp per run of bitmap words: lane l tests bit l of
+    //    each word, ballot + popc give the slots, the warp stores coalesced.
+    const int nwarp = T / 32, wid = warp_id();
+    const int w0 = (int)((long long)nwords * wid / nwarp), w1 = (int)((long long)nwords * (wid + 1) / nwarp);
     int cnt = 0, cnt_local = 0;
-    for (int w = w0; w < w1; ++w) {
-        uint32_t b = bits[w];
+    for (int w = w0 + lane; w < w1; w += 32) {
+        const uint32_t b = bits[w];
         cnt += __popc(b);
         if (R > 1)
-            while (b) { int bit = __ffs(b) - 1; b &= b - 1; cnt_local += ((w * 32 + bit) % R) == r; }
+            for (uint32_t bb = b; bb; bb &= bb - 1) cnt_local += ((w * 32 + __ffs(bb) - 1) % R) == r;
     }
-    if (R == 1) cnt_local = cnt;
+    cnt = warp_sum_i(cnt);
+    cnt_local = R > 1 ? warp_sum_i(cnt_local) : cnt;
     int total = 0, total_local = 0;
-    int off = block_excl_scan(cnt, warp_tot, total);
-    int off_local = block_excl_scan(cnt_local, warp_tot, total_local);
+    int off = block_excl_scan(lane == 0 ? cnt : 0, warp_tot, total);
+    int off_local = block_excl_scan(lane == 0 ? cnt_local : 0, warp_tot, total_local);
+    off = __shfl_sync(0xffffffffu, off, 0);
+    off_local = __shfl_sync(0xffffffffu, off_local, 0);
+    const unsigned lt = (1u << lane) - 1u;
     for (int w = w0; w < w1; ++w) {
-        uint32_t b = bits[w];
-        while (b) {
-            const int bit = __ffs(b) - 1;
-            b &= b - 1;
-            const int v = w * 32 + bit;
-            out_ids[off++] = v;
-            if (out_local && (R == 1 || v % R == r)) out_local[off_local++] = v;
+        const uint32_t b = bits[w];
+        if (!b) continue;
+        const int v = w * 32 + lane;
+        const bool in = (b >> lane) & 1u;
+        if (in) out_ids[off + __popc(b & lt)] = v;
+        off += __popc(b);
+        if (out_local) {
+            const bool mine = in && (R == 1 || v % R == r);
+            const unsigned ml = __ballot_sync(0xffffffffu, mine);
+            if (mine) out_local[off_local + __popc(ml & lt)] = v;
+            off_local += __popc(ml);
         }
     }
     if (tid == 0) {

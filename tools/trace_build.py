@@ -28,6 +28,6 @@ for it in range(6):
 torch.cuda.synchronize()
 st = ctx.read_stats()
 print({k: round(v / max(1, st["calls"][k]) * 1e3, 1) for k, v in st["ms"].items() if st["calls"][k]})
-tr = ctx.read_trace(2 * 148 * 8 + 16)[2 * 148 * 8:2 * 148 * 8 + 7].astype(np.float64)
+tr = ctx.read_trace()[2 * 148 * 8:2 * 148 * 8 + 7].astype(np.float64)
 names = ["start", "loaded", "S_sem", "gs", "G/graph", "formation", "end"]
 print("union phases (us from start):", {n: round((t - tr[0]) / 1e3, 1) for n, t in zip(names, tr)})

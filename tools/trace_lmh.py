@@ -40,7 +40,7 @@ for pf in (sys.argv[1:] or ["2"]):
         e1.record()
         torch.cuda.synchronize()
         times.append(e0.elapsed_time(e1) * 1e3)
-    full = ctx.read_trace(296).astype(np.float64)
+    full = ctx.read_trace(296 * 8).astype(np.float64).reshape(296, 8)
     tr = full[:148]
     fin = full[148:148 + n_h]
     t0 = tr[:, 0].min()
