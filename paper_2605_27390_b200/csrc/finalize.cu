@@ -292,9 +292,244 @@ lmh_finalize_kernel(LmhArgs a, int n_cta, int k, float gamma, const float* __res
     }
 }
 
+
+// Leaner finalisation for KP <= 32 (k <= 24): all global loads are issued up
+// front, the best KP of the per-CTA lists are formed by warp 0 with batched
+// bitonic sort + merge (lmh_epilogue.cuh), runs are detected warp-parallel in
+// registers, flagged candidates are re-scored exactly by all warps, and one
+// warp sort by (exact-if-re-scored value desc, id asc) yields the order.
+__global__ void __launch_bounds__(kFinThreads)
+lmh_finalize32_kernel(LmhArgs a, int n_cta, int k, float gamma, const float* __restrict__ wmax_dev,
+                      int32_t* __restrict__ topk_ids, float* __restrict__ topk_vals,
+                      float* __restrict__ row_max, float* __restrict__ row_sumexp, int* flags) {
+    const int r = blockIdx.x;
+    const int KP = a.KP;
+    const int lane = lane_id(), warp = warp_id(), nwarps = blockDim.x / 32;
+    extern __shared__ unsigned char f_sm[];
+    int* l_cnt = (int*)f_sm;                        // [n_cta]
+    float* l_m = (float*)(l_cnt + n_cta);           // [n_cta]
+    float* l_s = l_m + n_cta;                       // [n_cta]
+    float* l_val = l_s + n_cta;                     // [n_cta][KP]
+    int32_t* l_id = (int32_t*)(l_val + (size_t)n_cta * KP);
+    __shared__ float c_v[32];
+    __shared__ int32_t c_id[32];
+    __shared__ double c_e[32];
+    __shared__ int need_list[32];
+    __shared__ int n_need_s, nk_s;
+    __shared__ double red_d[32];
+    __shared__ float bat_v[32];
+    __shared__ int bat_p[32];
+    if (threadIdx.x == 0) FIN_TRACE(0);
+    // A. every load at once: CTA states, list entries (4 in flight / thread), H row
+    for (int c = threadIdx.x; c < n_cta; c += blockDim.x) {
+        const size_t o = (size_t)c * a.n_h + r;
+        l_cnt[c] = __ldcg(&a.part.cnt[o]);
+        l_m[c] = __ldcg(&a.part.m[o]);
+        l_s[c] = __ldcg(&a.part.s[o]);
+    }
+    for (int f0 = 0; f0 < n_cta * KP; f0 += 4 * blockDim.x) {
+        float vv[4];
+        int32_t ii[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int f = f0 + u * blockDim.x + threadIdx.x;
+            const int c = f / KP, i = f - c * KP;
+            const size_t o = ((size_t)c * a.n_h + r) * KP + i;
+            vv[u] = f < n_cta * KP ? __ldcg(&a.part.val[o]) : -INFINITY;
+            ii[u] = f < n_cta * KP ? __ldcg(&a.part.id[o]) : -1;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int f = f0 + u * blockDim.x + threadIdx.x;
+            if (f < n_cta * KP) { l_val[f] = vv[u]; l_id[f] = ii[u]; }
+        }
+    }
+    {
+        double acc = 0.0;
+        if (a.h_dtype == 0 && a.d % 8 == 0) {
+            const uint4* hp = (const uint4*)((const uint16_t*)a.H + (size_t)r * a.d);
+            for (int c = threadIdx.x; c < a.d / 8; c += blockDim.x) {
+                float f[8];
+                unpack_bf16x8(hp[c], f);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) acc = fma((double)f[j], (double)f[j], acc);
+            }
+        } else {
+            for (int col = threadIdx.x; col < a.d; col += blockDim.x) {
+                const double h = load_elem(a.H, a.h_dtype, (size_t)r * a.d + col);
+                acc = fma(h, h, acc);
+            }
+        }
+        acc = warp_sum_d(acc);
+        if (lane == 0) red_d[warp] = acc;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) FIN_TRACE(1);
+    // B. warp 0: softmax combine + the best KP entries; warp 1: delta
+    if (warp == 0) {
+        float M = -INFINITY;
+        for (int c = lane; c < n_cta; c += 32) if (l_s[c] > 0.0f) M = fmaxf(M, l_m[c]);
+        M = warp_max(M);
+        float S = 0.0f;
+        int tot = 0;
+        float lm = -INFINITY;                       // lane max of its list heads
+        for (int c = lane; c < n_cta; c += 32) {
+            if (l_s[c] > 0.0f) S += l_s[c] * expf(l_m[c] - M);
+            tot += l_cnt[c];
+            if (l_cnt[c] > 0) lm = fmaxf(lm, l_val[(size_t)c * KP]);
+        }
+        S = warp_sum(S);
+        tot = warp_sum_i(tot);
+        if (lane == 0) { row_max[r] = M; row_sumexp[r] = S; }
+        // pre-threshold: KP-th largest lane max of the heads bounds the KP-th best from below
+        const float th0 = warp_kth_largest(lm, KP);
+        float Lv = -INFINITY;
+        int Lp = 0x7fffffff, cnt = 0;
+        // candidates: every list entry >= th0, gathered in batches of 32
+        int c_list = lane, c_pos = 0;               // this lane's cursor over its lists
+        float th = th0;                             // rises to the KP-th entry once the list is full
+        while (true) {
+            // each lane contributes its next candidate (if any) to the batch
+            float x = -INFINITY;
+            int xid = 0x7fffffff;
+            bool has = false;
+            while (c_list < n_cta) {
+                if (c_pos < l_cnt[c_list] && l_val[(size_t)c_list * KP + c_pos] >= th) {
+                    x = l_val[(size_t)c_list * KP + c_pos];
+                    xid = l_id[(size_t)c_list * KP + c_pos];
+                    has = true;
+                    ++c_pos;
+                    break;
+                }
+                c_list += 32;
+                c_pos = 0;
+            }
+            const unsigned m = __ballot_sync(0xffffffffu, has);
+            if (!m) break;
+            bat_v[lane] = x;                        // one batch = one candidate per lane
+            bat_p[lane] = xid;
+            __syncwarp();
+            float bv = bat_v[lane];
+            int bp = bat_p[lane];
+            __syncwarp();
+            warp_sort32(bv, bp);
+            const float rv = __shfl_sync(0xffffffffu, bv, 31 - lane);
+            const int rp = __shfl_sync(0xffffffffu, bp, 31 - lane);
+            if (before(rv, rp, Lv, Lp)) { Lv = rv; Lp = rp; }
+#pragma unroll
+            for (int j = 16; j > 0; j >>= 1) {
+                const float ov = __shfl_xor_sync(0xffffffffu, Lv, j);
+                const int op = __shfl_xor_sync(0xffffffffu, Lp, j);
+                if (((lane & j) == 0) == before(ov, op, Lv, Lp)) { Lv = ov; Lp = op; }
+            }
+            cnt = min(cnt + __popc(m), KP);
+            if (cnt == KP) th = fmaxf(th, __shfl_sync(0xffffffffu, Lv, KP - 1));
+        }
+        // C. runs: consecutive kept entries closer than 2 delta; those reaching the top k are re-scored
+        double hn = 0.0;
+        for (int w = 0; w < nwarps; ++w) hn += red_d[w];
+        const double delta = (double)gamma * sqrt(hn) * (double)*wmax_dev * (double)a.inv_temp;
+        const float nv = __shfl_down_sync(0xffffffffu, Lv, 1);
+        const bool close = lane + 1 < cnt && (double)Lv - (double)nv <= 2.0 * delta + 2.4e-7 * fabs((double)Lv);
+        const unsigned cm = __ballot_sync(0xffffffffu, close);   // bit i: entry i and i+1 in one run
+        // entry i is in a multi-entry run reaching the top k if a chain of close links connects it to an index < k
+        bool need = false;
+        {
+            // run start s(i): walk down while link (i-1) is close
+            int st_i = lane;
+            while (st_i > 0 && ((cm >> (st_i - 1)) & 1u)) --st_i;
+            const bool multi = (lane > 0 && ((cm >> (lane - 1)) & 1u)) || ((cm >> lane) & 1u);
+            need = lane < cnt && multi && st_i < k;
+        }
+        const unsigned nm = __ballot_sync(0xffffffffu, need);
+        if (need) need_list[__popc(nm & ((1u << lane) - 1u))] = lane;
+        // uncertified: the run holding index k-1 reaches the last kept entry while entries were dropped
+        {
+            int end_k = k - 1;
+            while (end_k + 1 < cnt && ((cm >> end_k) & 1u)) ++end_k;
+            const bool unc = (k - 1 < cnt && end_k == cnt - 1 && tot > cnt && cnt >= k) || !(delta >= 0.0) || isinf(delta);
+            if (lane == 0 && unc) atomicOr(flags, kFlagUncertified);
+        }
+        c_v[lane] = Lv;
+        c_id[lane] = Lp;
+        if (lane == 0) { n_need_s = __popc(nm); nk_s = cnt; }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) FIN_TRACE(4);
+    // D. exact re-score of the flagged entries (one warp each)
+    const int nn = n_need_s;
+    for (int q = warp; q < nn; q += nwarps) {
+        const int c = need_list[q];
+        const size_t row = (size_t)(c_id[c] / a.R);
+        double acc = 0.0;
+        if (a.w_dtype == 0 && a.h_dtype == 0 && a.d % 8 == 0) {
+            const uint4* wp = (const uint4*)((const uint16_t*)a.W + row * a.d);
+            const uint4* hp = (const uint4*)((const uint16_t*)a.H + (size_t)r * a.d);
+            const int nc = a.d / 8;
+            for (int c0 = lane; c0 < nc; c0 += 32 * 4) {
+                uint4 wv[4], hv[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int cc = c0 + 32 * u;
+                    wv[u] = cc < nc ? wp[cc] : make_uint4(0, 0, 0, 0);
+                    hv[u] = cc < nc ? hp[cc] : make_uint4(0, 0, 0, 0);
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    float fw[8], fh[8];
+                    unpack_bf16x8(wv[u], fw);
+                    unpack_bf16x8(hv[u], fh);
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) acc = fma((double)fw[j], (double)fh[j], acc);
+                }
+            }
+        } else {
+            for (int col = lane; col < a.d; col += 32)
+                acc = fma(load_elem(a.W, a.w_dtype, row * a.d + col), load_elem(a.H, a.h_dtype, (size_t)r * a.d + col), acc);
+        }
+        acc = warp_sum_d(acc);
+        if (lane == 0) c_e[c] = acc * (double)a.inv_temp;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) FIN_TRACE(5);
+    // E. one sort by (exact value if re-scored else fp32 value desc, id asc): runs are
+    //    more than 2 delta apart, so this is the exact order; write the top k
+    if (warp == 0) {
+        const int cnt = nk_s;
+        bool flagged = false;
+        for (int q = 0; q < nn; ++q) flagged |= need_list[q] == lane;
+        double e = lane < cnt ? (flagged ? c_e[lane] : (double)c_v[lane]) : -INFINITY;
+        int id = lane < cnt ? c_id[lane] : 0x7fffffff;
+        // bitonic sort on (double, id)
+#pragma unroll
+        for (int kk = 2; kk <= 32; kk <<= 1) {
+#pragma unroll
+            for (int j = kk >> 1; j > 0; j >>= 1) {
+                const double oe = __shfl_xor_sync(0xffffffffu, e, j);
+                const int oi = __shfl_xor_sync(0xffffffffu, id, j);
+                const bool keep_better = ((lane & j) == 0) == ((lane & kk) == 0);
+                if (keep_better == before(oe, oi, e, id)) { e = oe; id = oi; }
+            }
+        }
+        if (lane < k) {
+            topk_ids[(size_t)r * k + lane] = lane < cnt ? id : -1;
+            topk_vals[(size_t)r * k + lane] = lane < cnt ? (float)e : -INFINITY;
+        }
+        if (lane == 0) FIN_TRACE(6);
+        if (lane == 0 && a.trace && blockIdx.x < 148) a.trace[148 * 8 + (size_t)blockIdx.x * 8 + 7] = nn;
+    }
+}
+
 void launch_lmh_finalize(const LmhArgs& a, int n_cta, int k, const float* wmax_dev, int32_t* topk_ids,
                          float* topk_vals, float* row_max, float* row_sumexp, int* flags, cudaStream_t st,
                          float gamma) {
+    if (a.KP <= 32) {
+        const size_t smem32 = (size_t)n_cta * 12 + (size_t)n_cta * a.KP * 8;
+        cudaFuncSetAttribute(lmh_finalize32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem32);
+        lmh_finalize32_kernel<<<a.n_h, kFinThreads, smem32, st>>>(a, n_cta, k, gamma, wmax_dev, topk_ids, topk_vals,
+                                                                   row_max, row_sumexp, flags);
+        return;
+    }
     size_t smem = (size_t)n_cta * 2 * sizeof(int) + (size_t)n_cta * a.KP * 8;
     cudaFuncSetAttribute(lmh_finalize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     lmh_finalize_kernel<<<a.n_h, kFinThreads, smem, st>>>(a, n_cta, k, gamma, wmax_dev, topk_ids, topk_vals,

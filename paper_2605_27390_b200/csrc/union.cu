@@ -213,14 +213,11 @@ ES_DEV void block_topM(const uint64_t* ck, const int32_t* cid, uint8_t* cf, int 
         for (int b = tid; b < kSelBins; b += T) hist[b] = 0;
         __syncthreads();
         const BSel my = st;
-        for (int base = 0; base < n; base += T) {            // uniform trip count: warp-aggregated adds
-            const int i = base + tid;
-            uint32_t digit = 0xFFFFFFFFu;
-            if (i < n && (cf[i] & A) && bmatch(ck[i], cid[i], my))
-                digit = on_key ? (uint32_t)(ck[i] >> lo) & dmask : ((0xFFFFFFFFu - (uint32_t)cid[i]) >> lo) & dmask;
-            const unsigned peers = __match_any_sync(0xffffffffu, digit);
-            if (digit != 0xFFFFFFFFu && lane == __ffs(peers) - 1) atomicAdd(&hist[digit], (uint32_t)__popc(peers));
-        }
+        // digits spread over ~1k bins (range-normalised), so plain smem atomics
+        for (int i = tid; i < n; i += T)
+            if ((cf[i] & A) && bmatch(ck[i], cid[i], my))
+                atomicAdd(&hist[on_key ? (uint32_t)(ck[i] >> lo) & dmask
+                                        : ((0xFFFFFFFFu - (uint32_t)cid[i]) >> lo) & dmask], 1u);
         __syncthreads();
         // thread t owns bin (kSelBins-1-t): an exclusive scan over t counts the bins above it
         const int bin = kSelBins - 1 - tid;
@@ -352,13 +349,8 @@ union_kernel(int V, const int32_t* __restrict__ static_ids, int n_static,
     const uint64_t gkmin = bsel.kmin, grange = bsel.kmax >= bsel.kmin ? bsel.kmax - bsel.kmin : 0ull;
     const int gshift = grange ? max(0, 64 - __clzll((long long)grange) - 10) : 0;
     if (ngs > 0) {
-        for (int base = 0; base < n_cand; base += T) {
-            const int i = base + tid;
-            uint32_t digit = 0xFFFFFFFFu;
-            if (i < n_cand && (cf[i] & kSem)) digit = (uint32_t)((ck[i] - gkmin) >> gshift);
-            const unsigned peers = __match_any_sync(0xffffffffu, digit);
-            if (digit != 0xFFFFFFFFu && lane == __ffs(peers) - 1) atomicAdd(&hist[digit], (uint32_t)__popc(peers));
-        }
+        for (int i = tid; i < n_cand; i += T)
+            if (cf[i] & kSem) atomicAdd(&hist[(uint32_t)((ck[i] - gkmin) >> gshift)], 1u);
         __syncthreads();
         const int bin = kSelBins - 1 - tid;
         const uint32_t hb = hist[bin];
