@@ -3,6 +3,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include <utility>
+
 #define ES_DEV __device__ __forceinline__
 
 namespace es {
@@ -77,6 +79,28 @@ ES_DEV void warp_argbest(float& v, int& key) {
 }
 
 ES_DEV int lane_id() { return threadIdx.x & 31; }
+
+// Programmatic dependent launch: a kernel launched with launch_pdl() may start
+// while its predecessor drains; it must pdl_wait() before touching the
+// predecessor's outputs. pdl_trigger() lets the successor be scheduled early.
+ES_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+ES_DEV void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 ES_DEV int warp_id() { return threadIdx.x >> 5; }
 
 }  // namespace es

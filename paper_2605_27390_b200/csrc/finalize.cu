@@ -319,6 +319,8 @@ lmh_finalize32_kernel(LmhArgs a, int n_cta, int k, float gamma, const float* __r
     __shared__ double red_d[32];
     __shared__ float bat_v[32];
     __shared__ int bat_p[32];
+    pdl_trigger();
+    pdl_wait();
     if (threadIdx.x == 0) FIN_TRACE(0);
     // A. every load at once: CTA states, list entries (4 in flight / thread), H row
     for (int c = threadIdx.x; c < n_cta; c += blockDim.x) {
@@ -526,8 +528,8 @@ void launch_lmh_finalize(const LmhArgs& a, int n_cta, int k, const float* wmax_d
     if (a.KP <= 32) {
         const size_t smem32 = (size_t)n_cta * 12 + (size_t)n_cta * a.KP * 8;
         cudaFuncSetAttribute(lmh_finalize32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem32);
-        lmh_finalize32_kernel<<<a.n_h, kFinThreads, smem32, st>>>(a, n_cta, k, gamma, wmax_dev, topk_ids, topk_vals,
-                                                                   row_max, row_sumexp, flags);
+        launch_pdl(lmh_finalize32_kernel, dim3(a.n_h), dim3(kFinThreads), smem32, st, a, n_cta, k, gamma, wmax_dev,
+                   topk_ids, topk_vals, row_max, row_sumexp, flags);
         return;
     }
     size_t smem = (size_t)n_cta * 2 * sizeof(int) + (size_t)n_cta * a.KP * 8;
@@ -541,6 +543,8 @@ __global__ void __launch_bounds__(256)
 merge_kernel(int R, int n_h, int k, const int32_t* __restrict__ ids, const float* __restrict__ vals,
              const float* __restrict__ m, const float* __restrict__ s, int32_t* __restrict__ out_ids,
              float* __restrict__ out_vals, float* __restrict__ out_lse, float* __restrict__ out_probs) {
+    pdl_trigger();
+    pdl_wait();
     const int r = blockIdx.x * (blockDim.x / 32) + warp_id();
     if (r >= n_h) return;
     const int lane = lane_id();
@@ -596,7 +600,8 @@ void launch_merge(int R, int n_h, int k, const int32_t* ids, const float* vals, 
     const int grid = (n_h + 7) / 8;
     const size_t smem = (size_t)8 * R * k * 8;
     cudaFuncSetAttribute(merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    merge_kernel<<<grid, 256, smem, st>>>(R, n_h, k, ids, vals, m, s, out_ids, out_vals, out_lse, out_probs);
+    launch_pdl(merge_kernel, dim3(grid), dim3(256), smem, st, R, n_h, k, ids, vals, m, s, out_ids, out_vals, out_lse,
+               out_probs);
 }
 
 // ------------------------------------------------------------ helpers

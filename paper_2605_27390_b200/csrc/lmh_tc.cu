@@ -180,7 +180,7 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
     const int S = tp.stages, NP = tp.n_pad, n_h = a.n_h;
     unsigned char* smA = base;                                   // [S][128][128 B]
     unsigned char* smB = base + tp.off_b;                        // [S][NP][128 B]
-    EpiSmem e = epi_carve(base + tp.off_epi, n_h, a.KP, kTcEpiWarps);
+    EpiSmem e = epi_carve(base + tp.off_epi, n_h, a.KP, kTcWarps);
     uint64_t* full = (uint64_t*)(base + tp.off_bar);             // [S]
     uint64_t* empty = full + S;                                  // [S]
     uint64_t* tfull = empty + S;                                 // [2]
@@ -189,6 +189,8 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
     int32_t* rows_sm = (int32_t*)(base + tp.off_rows);           // [2][128] gather rows per tile
 
     const int warp = warp_id(), lane = lane_id();
+    pdl_trigger();
+    pdl_wait();   // the subset (and n_S) come from the previous kernel on the stream
     const int n_S = min(*a.n_subset_dev, a.n_subset_max);
     const int p0 = (int)((long long)n_S * blockIdx.x / gridDim.x);
     const int p1 = (int)((long long)n_S * (blockIdx.x + 1) / gridDim.x);
@@ -347,15 +349,25 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
                     for (int p = lane; p < tn; p += 32)
                         a.logits_out[(size_t)r * a.n_subset_max + t0 + p] = e.tile[r * kTile + p];
             }
+            if (t == n_tiles - 1) break;            // the last tile is folded by all warps below
             epi_tile(e, n_h, a.KP, tn, t0, ew, kTcEpiWarps);
             if (ew == 0 && lane == 0 && t < 2) TC_TRACE(4 + 2 * t);
             named_bar_sync(1, nthr);
         }
-        epi_store(e, a.part, blockIdx.x, a.n_h, 0, n_h, a.KP, a.subset, ew, kTcEpiWarps);
+    }
+    // the last tile's fold is the exposed tail: producers and the MMA warp are
+    // idle by now, so all 13 warps split its rows
+    if (n_tiles > 0) {
+        int t0, tn;
+        tile_range(n_tiles - 1, t0, tn);
+        named_bar_sync(2, kTcWarps * 32);
+        epi_tile(e, n_h, a.KP, tn, t0, warp, kTcWarps);
+        if (warp == kTcEpiWarp0 && lane == 0 && n_tiles - 1 < 2) TC_TRACE(4 + 2 * (n_tiles - 1));
     }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
+    epi_store(e, a.part, blockIdx.x, a.n_h, 0, n_h, a.KP, a.subset, warp, kTcWarps);
     if (threadIdx.x == 0) TC_TRACE(7);
     if (warp == kTcMmaWarp)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(tp.tmem_cols));
@@ -404,7 +416,7 @@ cudaError_t launch_lmh_tc(const LmhArgs& a, cudaStream_t st) {
     while (c < cols) c <<= 1;
     tp.tmem_cols = c;
     const size_t stage_a = (size_t)kTileM * 128, stage_b = (size_t)tp.n_pad * 128;
-    const size_t epi = epi_smem_bytes(a.n_h, a.KP, kTcEpiWarps);
+    const size_t epi = epi_smem_bytes(a.n_h, a.KP, kTcWarps);
     const size_t fixed = epi + 2 * 128 * 4 + 64 * 8 + 1024 /*align slack*/ + 256;
     const size_t budget = 227 * 1024;
     int S = (int)((budget - fixed) / (stage_a + stage_b));
@@ -424,8 +436,7 @@ cudaError_t launch_lmh_tc(const LmhArgs& a, cudaStream_t st) {
         return cudaErrorInvalidValue;
     cudaError_t e = cudaFuncSetAttribute(lmh_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    lmh_tc_kernel<<<lmh_tc_grid(), kTcWarps * 32, smem, st>>>(mw, mh, a, tp);
-    return cudaGetLastError();
+    return launch_pdl(lmh_tc_kernel, dim3(lmh_tc_grid()), dim3(kTcWarps * 32), smem, st, mw, mh, a, tp);
 }
 
 }  // namespace es

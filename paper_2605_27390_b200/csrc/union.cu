@@ -275,6 +275,8 @@ union_kernel(int V, const int32_t* __restrict__ static_ids, int n_static,
     __shared__ int nG_s, bad_s, taken_s, ngs_s, sem_n_s;
 
     const int tid = threadIdx.x, lane = lane_id(), T = blockDim.x;
+    pdl_trigger();
+    pdl_wait();
     const int n_cand = min(*n_cand_dev, cap);
     if (trace) { __syncthreads(); if (threadIdx.x == 0) { long long t_; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); trace[0] = t_; } }
     for (int w = tid; w < nwords; w += T) bits[w] = 0;
@@ -484,37 +486,40 @@ union_kernel(int V, const int32_t* __restrict__ static_ids, int n_static,
     __syncthreads();
 
     if (trace) { __syncthreads(); if (threadIdx.x == 0) { long long t_; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); trace[5] = t_; } }
-    // 6. compaction, one warp per run of bitmap words: lane l tests bit l of
-    //    each word, ballot + popc give the slots, the warp stores coalesced.
-    const int nwarp = T / 32, wid = warp_id();
-    const int w0 = (int)((long long)nwords * wid / nwarp), w1 = (int)((long long)nwords * (wid + 1) / nwarp);
-    int cnt = 0, cnt_local = 0;
-    for (int w = w0 + lane; w < w1; w += 32) {
-        const uint32_t b = bits[w];
-        cnt += __popc(b);
-        if (R > 1)
-            for (uint32_t bb = b; bb; bb &= bb - 1) cnt_local += ((w * 32 + __ffs(bb) - 1) % R) == r;
-    }
-    cnt = warp_sum_i(cnt);
-    cnt_local = R > 1 ? warp_sum_i(cnt_local) : cnt;
+    // 6. compaction. Thread t owns words [t*nwords/T, (t+1)*nwords/T); a block
+    //    scan of the popcounts gives each thread's output offset. The sorted
+    //    ids are staged in shared memory (the candidate arrays are dead by now)
+    //    and copied out coalesced; the shard slice (v mod R == r) is filtered
+    //    from the staged copy. Outputs larger than the staging area fall back to
+    //    direct per-thread stores.
+    const int w0 = (int)((long long)nwords * tid / T), w1 = (int)((long long)nwords * (tid + 1) / T);
+    int cnt = 0;
+    for (int w = w0; w < w1; ++w) cnt += __popc(bits[w]);
     int total = 0, total_local = 0;
-    int off = block_excl_scan(lane == 0 ? cnt : 0, warp_tot, total);
-    int off_local = block_excl_scan(lane == 0 ? cnt_local : 0, warp_tot, total_local);
-    off = __shfl_sync(0xffffffffu, off, 0);
-    off_local = __shfl_sync(0xffffffffu, off_local, 0);
-    const unsigned lt = (1u << lane) - 1u;
-    for (int w = w0; w < w1; ++w) {
-        const uint32_t b = bits[w];
-        if (!b) continue;
-        const int v = w * 32 + lane;
-        const bool in = (b >> lane) & 1u;
-        if (in) out_ids[off + __popc(b & lt)] = v;
-        off += __popc(b);
-        if (out_local) {
-            const bool mine = in && (R == 1 || v % R == r);
-            const unsigned ml = __ballot_sync(0xffffffffu, mine);
-            if (mine) out_local[off_local + __popc(ml & lt)] = v;
-            off_local += __popc(ml);
+    int off = block_excl_scan(cnt, warp_tot, total);
+    int32_t* stage = (int32_t*)u_sm;                          // aliases ck/cid: 3*cap int32
+    const bool staged = total <= 3 * cap;
+    int32_t* dst = staged ? stage : out_ids;
+    for (int w = w0; w < w1; ++w)
+        for (uint32_t bb = bits[w]; bb; bb &= bb - 1) dst[off++] = w * 32 + __ffs(bb) - 1;
+    __syncthreads();
+    if (staged)
+        for (int i = tid; i < total; i += T) out_ids[i] = stage[i];
+    if (out_local) {
+        if (R == 1) {
+            if (staged)
+                for (int i = tid; i < total; i += T) out_local[i] = stage[i];
+            else
+                for (int i = tid; i < total; i += T) out_local[i] = out_ids[i];   // own writes: visible after the sync
+            total_local = total;
+        } else {
+            const int32_t* srcv = staged ? stage : out_ids;
+            const int i0 = (int)((long long)total * tid / T), i1 = (int)((long long)total * (tid + 1) / T);
+            int cl = 0;
+            for (int i = i0; i < i1; ++i) cl += (srcv[i] % R) == r;
+            int offl = block_excl_scan(cl, warp_tot, total_local);
+            for (int i = i0; i < i1; ++i)
+                if ((srcv[i] % R) == r) out_local[offl++] = srcv[i];
         }
     }
     if (tid == 0) {
@@ -550,7 +555,7 @@ void launch_union(int V, const int32_t* static_ids, int n_static, const int32_t*
                   int32_t* sem_out, int* sem_out_n, int debug, int* flags, cudaStream_t st, long long* trace) {
     const size_t smem = (size_t)cap * 13 + union_fixed_bytes(V, per_seed) + 16;
     cudaFuncSetAttribute(union_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    union_kernel<<<1, kUnionThreads, smem, st>>>(V, static_ids, n_static, seeds, n_seed, cand_s, cand_id, n_cand_dev,
+    launch_pdl(union_kernel, dim3(1), dim3(kUnionThreads), smem, st, V, static_ids, n_static, seeds, n_seed, cand_s, cand_id, n_cand_dev,
                                                   cap, n_sem, row_ptr, col, ctx_sel, n_ctx_sel_dev, n_graph_sem_seeds,
                                                   per_seed, n_dyn, R, r, out_ids, out_n, out_local, out_local_n,
                                                   sem_out, sem_out_n, debug, flags, trace);
