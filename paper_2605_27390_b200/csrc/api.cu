@@ -442,11 +442,13 @@ static bool use_tc(const LmhArgs& a) {
     return a.n_h >= kTcMinRows;
 }
 
-evospec_status evospec_subset_logits_topk(evospec_ctx* ctx, const void* W, int64_t n_w_rows, const void* H,
-                                          int32_t n_h, const int32_t* subset, const int32_t* n_subset_dev,
-                                          int32_t n_subset_max, int32_t k, float inv_temp, int32_t* topk_ids,
-                                          float* topk_vals, float* row_max, float* row_sumexp, float* logits_out,
-                                          void* stream) {
+// merged outputs (m_*) non-null: the single-shard merge (LSE, probabilities)
+// is fused into the finalisation kernel (used by evospec_draft_step at R = 1)
+static evospec_status lmh_impl(evospec_ctx* ctx, const void* W, int64_t n_w_rows, const void* H, int32_t n_h,
+                               const int32_t* subset, const int32_t* n_subset_dev, int32_t n_subset_max, int32_t k,
+                               float inv_temp, int32_t* topk_ids, float* topk_vals, float* row_max,
+                               float* row_sumexp, float* logits_out, void* stream, int32_t* m_ids, float* m_vals,
+                               float* m_lse, float* m_probs) {
     if (!ctx || !W || !H || !subset || !n_subset_dev || !topk_ids || !topk_vals || !row_max || !row_sumexp)
         return fail(EVOSPEC_EINPUT, "subset_logits_topk: null argument");
     const evospec_config& c = ctx->cfg;
@@ -472,6 +474,7 @@ evospec_status evospec_subset_logits_topk(evospec_ctx* ctx, const void* W, int64
     a.R = c.n_shards; a.KP = k + kTopkPad; a.inv_temp = inv_temp;
     a.logits_out = logits_out;
     a.part = ctx->part;
+    a.m_ids = m_ids; a.m_vals = m_vals; a.m_lse = m_lse; a.m_probs = m_probs;
     if (getenv("EVOSPEC_TRACE")) {
         if (!ctx->trace) CUDA_TRY(cudaMalloc(&ctx->trace, kTraceLen * sizeof(long long)));
         CUDA_TRY(cudaMemsetAsync(ctx->trace, 0, 2 * kNumSMs * 8 * sizeof(long long), st));
@@ -504,6 +507,15 @@ evospec_status evospec_subset_logits_topk(evospec_ctx* ctx, const void* W, int64
     }
     LAUNCH_CHECK("lmh_finalize");
     return EVOSPEC_OK;
+}
+
+evospec_status evospec_subset_logits_topk(evospec_ctx* ctx, const void* W, int64_t n_w_rows, const void* H,
+                                          int32_t n_h, const int32_t* subset, const int32_t* n_subset_dev,
+                                          int32_t n_subset_max, int32_t k, float inv_temp, int32_t* topk_ids,
+                                          float* topk_vals, float* row_max, float* row_sumexp, float* logits_out,
+                                          void* stream) {
+    return lmh_impl(ctx, W, n_w_rows, H, n_h, subset, n_subset_dev, n_subset_max, k, inv_temp, topk_ids, topk_vals,
+                    row_max, row_sumexp, logits_out, stream, nullptr, nullptr, nullptr, nullptr);
 }
 
 evospec_status evospec_merge_shards(evospec_ctx* ctx, int32_t n_h, int32_t k, const int32_t* ids, const float* vals,
@@ -567,16 +579,20 @@ evospec_status evospec_draft_step(evospec_ctx* ctx, const evospec_step_io* io, v
     if (s != EVOSPEC_OK) return s;
     const int32_t* sub = c.n_shards > 1 ? ctx->st_local : ctx->st_S;
     const int32_t* nsub = c.n_shards > 1 ? ctx->st_nlocal : ctx->st_nS;
-    s = evospec_subset_logits_topk(ctx, io->W_local, io->n_w_rows, H, io->n_h, sub, nsub, n_sub_max, io->k,
-                                   io->inv_temp, ctx->st_tids, ctx->st_tvals, ctx->st_m, ctx->st_s, nullptr, st);
-    if (s != EVOSPEC_OK) return s;
     int32_t* oi = io->host_io ? ctx->st_oids : io->out_ids;
     float* ov = io->host_io ? ctx->st_ovals : io->out_vals;
     float* ol = io->host_io ? ctx->st_lse : io->out_lse;
     float* op = io->host_io ? (io->out_probs ? ctx->st_probs : nullptr) : io->out_probs;
-    s = evospec_merge_shards(ctx, io->n_h, io->k, ctx->st_tids, ctx->st_tvals, ctx->st_m, ctx->st_s, oi, ov, ol, op,
-                             st);
+    const bool fuse = c.n_shards == 1;    // single shard: the merge is the finalisation itself
+    s = lmh_impl(ctx, io->W_local, io->n_w_rows, H, io->n_h, sub, nsub, n_sub_max, io->k, io->inv_temp, ctx->st_tids,
+                 ctx->st_tvals, ctx->st_m, ctx->st_s, nullptr, st, fuse ? oi : nullptr, fuse ? ov : nullptr,
+                 fuse ? ol : nullptr, fuse ? op : nullptr);
     if (s != EVOSPEC_OK) return s;
+    if (!fuse) {
+        s = evospec_merge_shards(ctx, io->n_h, io->k, ctx->st_tids, ctx->st_tvals, ctx->st_m, ctx->st_s, oi, ov, ol,
+                                 op, st);
+        if (s != EVOSPEC_OK) return s;
+    }
     if (io->host_io) {
         StageTimer t(ctx, EVOSPEC_STAGE_COPY, st);
         const size_t hk = (size_t)io->n_h * io->k;

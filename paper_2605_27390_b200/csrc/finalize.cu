@@ -283,10 +283,17 @@ lmh_finalize_kernel(LmhArgs a, int n_cta, int k, float gamma, const float* __res
             }
             i = j + 1;
         }
+        const float lse = row_sumexp[r] > 0.0f ? row_max[r] + logf(row_sumexp[r]) : -INFINITY;
         for (int t = 0; t < k; ++t) {
             topk_ids[(size_t)r * k + t] = t < nk ? c_id[t] : -1;
             topk_vals[(size_t)r * k + t] = t < nk ? (float)c_e[t] : -INFINITY;
+            if (a.m_ids) {   // fused single-shard merge (R = 1)
+                a.m_ids[(size_t)r * k + t] = t < nk ? c_id[t] : -1;
+                a.m_vals[(size_t)r * k + t] = t < nk ? (float)c_e[t] : -INFINITY;
+                if (a.m_probs) a.m_probs[(size_t)r * k + t] = t < nk ? expf((float)c_e[t] - lse) : 0.0f;
+            }
         }
+        if (a.m_ids) a.m_lse[r] = lse;
         FIN_TRACE(6);
         if (a.trace && blockIdx.x < 148) a.trace[148 * 8 + (size_t)blockIdx.x * 8 + 7] = nn;   // re-scored count
     }
@@ -319,6 +326,7 @@ lmh_finalize32_kernel(LmhArgs a, int n_cta, int k, float gamma, const float* __r
     __shared__ double red_d[32];
     __shared__ float bat_v[32];
     __shared__ int bat_p[32];
+    __shared__ float lse_s;
     pdl_trigger();
     pdl_wait();
     if (threadIdx.x == 0) FIN_TRACE(0);
@@ -382,7 +390,7 @@ lmh_finalize32_kernel(LmhArgs a, int n_cta, int k, float gamma, const float* __r
         }
         S = warp_sum(S);
         tot = warp_sum_i(tot);
-        if (lane == 0) { row_max[r] = M; row_sumexp[r] = S; }
+        if (lane == 0) { row_max[r] = M; row_sumexp[r] = S; lse_s = S > 0.0f ? M + logf(S) : -INFINITY; }
         // pre-threshold: KP-th largest lane max of the heads bounds the KP-th best from below
         const float th0 = warp_kth_largest(lm, KP);
         float Lv = -INFINITY;
@@ -514,8 +522,16 @@ lmh_finalize32_kernel(LmhArgs a, int n_cta, int k, float gamma, const float* __r
             }
         }
         if (lane < k) {
-            topk_ids[(size_t)r * k + lane] = lane < cnt ? id : -1;
-            topk_vals[(size_t)r * k + lane] = lane < cnt ? (float)e : -INFINITY;
+            const int oid = lane < cnt ? id : -1;
+            const float ovl = lane < cnt ? (float)e : -INFINITY;
+            topk_ids[(size_t)r * k + lane] = oid;
+            topk_vals[(size_t)r * k + lane] = ovl;
+            if (a.m_ids) {   // fused single-shard merge (R = 1)
+                a.m_ids[(size_t)r * k + lane] = oid;
+                a.m_vals[(size_t)r * k + lane] = ovl;
+                if (a.m_probs) a.m_probs[(size_t)r * k + lane] = lane < cnt ? expf(ovl - lse_s) : 0.0f;
+                if (lane == 0) a.m_lse[r] = lse_s;
+            }
         }
         if (lane == 0) FIN_TRACE(6);
         if (lane == 0 && a.trace && blockIdx.x < 148) a.trace[148 * 8 + (size_t)blockIdx.x * 8 + 7] = nn;

@@ -57,6 +57,8 @@ struct LmhArgs {
     int R; int KP; float inv_temp;
     float* logits_out;  // optional [n_h][n_subset_max]
     long long* trace;   // optional per-CTA globaltimer stamps [n_cta][8] (profiling)
+    // optional fused single-shard merge outputs (R = 1): ids/vals [n_h][k], lse [n_h], probs [n_h][k]
+    int32_t* m_ids; float* m_vals; float* m_lse; float* m_probs;
     LmhPartials part;
 };
 // returns the number of CTAs whose partials were written

@@ -42,7 +42,7 @@ constexpr int kTcEpiWarp0 = kProdWarps + 1;
 constexpr int kTcEpiWarps = 8;
 constexpr int kTcWarps = kProdWarps + 1 + kTcEpiWarps;
 constexpr int kPfBytes = 1024;     // L2 prefetch window per row (8 stages of 128 B)
-constexpr int kPfDist = 2;         // windows ahead of the cp.async stream
+constexpr int kPfDist = 0;         // windows ahead (0 = off: measured slower on B200, profiles/r01_trace_lmh.log)
 constexpr int kBlockK = 64;        // bf16 columns per stage = one 128-byte swizzle atom row
 constexpr int kTileM = 128;
 
