@@ -205,7 +205,7 @@ evospec_status evospec_destroy(evospec_ctx* ctx) {
     void* ptrs[] = {ctx->s64, ctx->key32, ctx->hist12, ctx->hist, ctx->cand_count, ctx->cand_s, ctx->cand_id,
                     ctx->loc_count, ctx->loc_s, ctx->loc_id, ctx->gat_s, ctx->gat_id, ctx->sem_ids, ctx->sem_n,
                     ctx->ctx_sel,
-                    ctx->ctx_n, ctx->part.val, ctx->part.id, ctx->part.m, ctx->part.s, ctx->part.cnt,
+                    ctx->ctx_n, ctx->part.val, ctx->part.id, ctx->part.m, ctx->part.s, ctx->part.cnt, ctx->part.xcnt,
                     ctx->flags, ctx->wmax, ctx->g_ids, ctx->g_vals, ctx->g_m, ctx->g_s, ctx->st_q, ctx->st_H,
                     ctx->st_seeds, ctx->st_ctx, ctx->st_S, ctx->st_nS, ctx->st_local, ctx->st_nlocal,
                     ctx->st_tids, ctx->st_tvals, ctx->st_m, ctx->st_s, ctx->st_oids, ctx->st_ovals,
@@ -263,7 +263,7 @@ evospec_status evospec_create(evospec_ctx** out, const evospec_config* cfg, int 
     A(dalloc(&x->sem_ids, sem)); A(dalloc(&x->sem_n, 1));
     A(dalloc(&x->ctx_sel, std::max(1, c.max_ctx))); A(dalloc(&x->ctx_n, 1));
     A(dalloc(&x->part.val, pr * kMaxKP)); A(dalloc(&x->part.id, pr * kMaxKP));
-    A(dalloc(&x->part.m, pr)); A(dalloc(&x->part.s, pr)); A(dalloc(&x->part.cnt, pr));
+    A(dalloc(&x->part.m, pr)); A(dalloc(&x->part.s, pr)); A(dalloc(&x->part.cnt, pr)); A(dalloc(&x->part.xcnt, pr));
     A(dalloc(&x->flags, 1)); A(dalloc(&x->wmax, 1));
     const size_t trip = (size_t)R * c.max_rows * c.max_k;
     A(dalloc(&x->g_ids, trip)); A(dalloc(&x->g_vals, trip));
@@ -471,7 +471,7 @@ static evospec_status lmh_impl(evospec_ctx* ctx, const void* W, int64_t n_w_rows
     a.W = W; a.n_w_rows = n_w_rows; a.d = c.d; a.w_dtype = c.w_dtype;
     a.H = H; a.n_h = n_h; a.h_dtype = c.h_dtype;
     a.subset = subset; a.n_subset_dev = n_subset_dev; a.n_subset_max = n_subset_max;
-    a.R = c.n_shards; a.KP = k + kTopkPad; a.inv_temp = inv_temp;
+    a.R = c.n_shards; a.KP = k + kTopkPad; a.LS = a.KP <= 32 ? 32 : a.KP; a.inv_temp = inv_temp;
     a.logits_out = logits_out;
     a.part = ctx->part;
     a.m_ids = m_ids; a.m_vals = m_vals; a.m_lse = m_lse; a.m_probs = m_probs;

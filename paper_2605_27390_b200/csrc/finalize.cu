@@ -313,11 +313,13 @@ lmh_finalize32_kernel(LmhArgs a, int n_cta, int k, float gamma, const float* __r
     const int KP = a.KP;
     const int lane = lane_id(), warp = warp_id(), nwarps = blockDim.x / 32;
     extern __shared__ unsigned char f_sm[];
-    int* l_cnt = (int*)f_sm;                        // [n_cta]
-    float* l_m = (float*)(l_cnt + n_cta);           // [n_cta]
+    const int LS = a.LS;                            // list stride (32): sorted + extras
+    int* l_cnt = (int*)f_sm;                        // [n_cta] sorted entries
+    int* l_x = l_cnt + n_cta;                       // [n_cta] unsorted extras
+    float* l_m = (float*)(l_x + n_cta);             // [n_cta]
     float* l_s = l_m + n_cta;                       // [n_cta]
-    float* l_val = l_s + n_cta;                     // [n_cta][KP]
-    int32_t* l_id = (int32_t*)(l_val + (size_t)n_cta * KP);
+    float* l_val = (float*)(((uintptr_t)(l_s + n_cta) + 15) & ~(uintptr_t)15);   // [n_cta][LS]
+    int32_t* l_id = (int32_t*)(l_val + (size_t)n_cta * LS);
     __shared__ float c_v[32];
     __shared__ int32_t c_id[32];
     __shared__ double c_e[32];
@@ -330,28 +332,34 @@ lmh_finalize32_kernel(LmhArgs a, int n_cta, int k, float gamma, const float* __r
     pdl_trigger();
     pdl_wait();
     if (threadIdx.x == 0) FIN_TRACE(0);
-    // A. every load at once: CTA states, list entries (4 in flight / thread), H row
+    // A. every load at once: CTA states, list entries (16-byte loads, 4 in flight), H row
     for (int c = threadIdx.x; c < n_cta; c += blockDim.x) {
         const size_t o = (size_t)c * a.n_h + r;
         l_cnt[c] = __ldcg(&a.part.cnt[o]);
+        l_x[c] = __ldcg(&a.part.xcnt[o]);
         l_m[c] = __ldcg(&a.part.m[o]);
         l_s[c] = __ldcg(&a.part.s[o]);
     }
-    for (int f0 = 0; f0 < n_cta * KP; f0 += 4 * blockDim.x) {
-        float vv[4];
-        int32_t ii[4];
+    {
+        const int nq = n_cta * (LS / 4);            // float4 per list
+        for (int q0 = 0; q0 < nq; q0 += 4 * blockDim.x) {
+            float4 vv[4];
+            int4 ii[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const int f = f0 + u * blockDim.x + threadIdx.x;
-            const int c = f / KP, i = f - c * KP;
-            const size_t o = ((size_t)c * a.n_h + r) * KP + i;
-            vv[u] = f < n_cta * KP ? __ldcg(&a.part.val[o]) : -INFINITY;
-            ii[u] = f < n_cta * KP ? __ldcg(&a.part.id[o]) : -1;
-        }
+            for (int u = 0; u < 4; ++u) {
+                const int q = q0 + u * blockDim.x + threadIdx.x;
+                const int c = q / (LS / 4), part = q - c * (LS / 4);
+                const size_t o = ((size_t)c * a.n_h + r) * LS + part * 4;
+                if (q < nq) {
+                    vv[u] = __ldcg((const float4*)&a.part.val[o]);
+                    ii[u] = __ldcg((const int4*)&a.part.id[o]);
+                }
+            }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const int f = f0 + u * blockDim.x + threadIdx.x;
-            if (f < n_cta * KP) { l_val[f] = vv[u]; l_id[f] = ii[u]; }
+            for (int u = 0; u < 4; ++u) {
+                const int q = q0 + u * blockDim.x + threadIdx.x;
+                if (q < nq) { ((float4*)l_val)[q] = vv[u]; ((int4*)l_id)[q] = ii[u]; }
+            }
         }
     }
     {
@@ -375,38 +383,42 @@ lmh_finalize32_kernel(LmhArgs a, int n_cta, int k, float gamma, const float* __r
     }
     __syncthreads();
     if (threadIdx.x == 0) FIN_TRACE(1);
-    // B. warp 0: softmax combine + the best KP entries; warp 1: delta
+    // B. warp 0: softmax combine + the best KP entries
     if (warp == 0) {
         float M = -INFINITY;
         for (int c = lane; c < n_cta; c += 32) if (l_s[c] > 0.0f) M = fmaxf(M, l_m[c]);
         M = warp_max(M);
         float S = 0.0f;
         int tot = 0;
-        float lm = -INFINITY;                       // lane max of its list heads
+        float lm = -INFINITY;                       // lane max of its lists (head and extras)
         for (int c = lane; c < n_cta; c += 32) {
             if (l_s[c] > 0.0f) S += l_s[c] * expf(l_m[c] - M);
-            tot += l_cnt[c];
-            if (l_cnt[c] > 0) lm = fmaxf(lm, l_val[(size_t)c * KP]);
+            tot += l_cnt[c] + l_x[c];
+            if (l_cnt[c] > 0) lm = fmaxf(lm, l_val[(size_t)c * LS]);
+            for (int i = l_cnt[c]; i < l_cnt[c] + l_x[c]; ++i) lm = fmaxf(lm, l_val[(size_t)c * LS + i]);
         }
         S = warp_sum(S);
         tot = warp_sum_i(tot);
         if (lane == 0) { row_max[r] = M; row_sumexp[r] = S; lse_s = S > 0.0f ? M + logf(S) : -INFINITY; }
-        // pre-threshold: KP-th largest lane max of the heads bounds the KP-th best from below
+        // pre-threshold: KP-th largest lane max bounds the KP-th best from below
         const float th0 = warp_kth_largest(lm, KP);
         float Lv = -INFINITY;
         int Lp = 0x7fffffff, cnt = 0;
-        // candidates: every list entry >= th0, gathered in batches of 32
+        // candidates: every entry >= th, gathered in batches of 32 (one per lane):
+        // sorted part with early exit, then the unsorted extras
         int c_list = lane, c_pos = 0;               // this lane's cursor over its lists
         float th = th0;                             // rises to the KP-th entry once the list is full
         while (true) {
-            // each lane contributes its next candidate (if any) to the batch
             float x = -INFINITY;
             int xid = 0x7fffffff;
             bool has = false;
             while (c_list < n_cta) {
-                if (c_pos < l_cnt[c_list] && l_val[(size_t)c_list * KP + c_pos] >= th) {
-                    x = l_val[(size_t)c_list * KP + c_pos];
-                    xid = l_id[(size_t)c_list * KP + c_pos];
+                const int ns = l_cnt[c_list], ne = ns + l_x[c_list];
+                if (c_pos < ns && l_val[(size_t)c_list * LS + c_pos] < th) c_pos = ns;   // sorted: rest is lower
+                while (c_pos >= ns && c_pos < ne && l_val[(size_t)c_list * LS + c_pos] < th) ++c_pos;
+                if (c_pos < ne) {
+                    x = l_val[(size_t)c_list * LS + c_pos];
+                    xid = l_id[(size_t)c_list * LS + c_pos];
                     has = true;
                     ++c_pos;
                     break;
@@ -542,7 +554,7 @@ void launch_lmh_finalize(const LmhArgs& a, int n_cta, int k, const float* wmax_d
                          float* topk_vals, float* row_max, float* row_sumexp, int* flags, cudaStream_t st,
                          float gamma) {
     if (a.KP <= 32) {
-        const size_t smem32 = (size_t)n_cta * 12 + (size_t)n_cta * a.KP * 8;
+        const size_t smem32 = (size_t)n_cta * 16 + 16 + (size_t)n_cta * a.LS * 8;
         cudaFuncSetAttribute(lmh_finalize32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem32);
         launch_pdl(lmh_finalize32_kernel, dim3(a.n_h), dim3(kFinThreads), smem32, st, a, n_cta, k, gamma, wmax_dev,
                    topk_ids, topk_vals, row_max, row_sumexp, flags);

@@ -43,18 +43,23 @@ void launch_union(int V, const int32_t* static_ids, int n_static, const int32_t*
                   long long* trace = nullptr);
 
 // ---- LM head (lmh_gemv.cu, lmh_tc.cu)
+// Per-CTA partial state of the LM head, per H row: entries [0, cnt) are the
+// CTA's best candidates sorted by (z desc, id asc); entries [cnt, cnt + xcnt)
+// are unsorted extras from the CTA's last tile that beat entry KP-1 of the
+// sorted list (the last tile is not folded, its survivors are appended).
 struct LmhPartials {
-    float* val;    // [n_cta][n_h][KP]
-    int32_t* id;   // [n_cta][n_h][KP]
+    float* val;    // [n_cta][n_h][LS]
+    int32_t* id;   // [n_cta][n_h][LS]
     float* m;      // [n_cta][n_h]
     float* s;      // [n_cta][n_h]
-    int* cnt;      // [n_cta][n_h] number of valid entries
+    int* cnt;      // [n_cta][n_h] sorted entries
+    int* xcnt;     // [n_cta][n_h] unsorted extras
 };
 struct LmhArgs {
     const void* W; int64_t n_w_rows; int d; int w_dtype;
     const void* H; int n_h; int h_dtype;
     const int32_t* subset; const int* n_subset_dev; int n_subset_max;
-    int R; int KP; float inv_temp;
+    int R; int KP; int LS; float inv_temp;   // LS: list stride (KP <= 32: 32, else KP)
     float* logits_out;  // optional [n_h][n_subset_max]
     long long* trace;   // optional per-CTA globaltimer stamps [n_cta][8] (profiling)
     // optional fused single-shard merge outputs (R = 1): ids/vals [n_h][k], lse [n_h], probs [n_h][k]

@@ -35,12 +35,13 @@ struct EpiSmem {
     int* st_cnt;     // [n_h]
     float* st_m;     // [n_h]   running max
     float* st_ls;    // [n_h][32] per-lane partial sum of exp(z - m)
+    int* st_xcnt;    // [n_h] extras appended by the last tile (global partials)
     float* scr_v;    // [n_warps][32] candidate batch scratch
     int* scr_p;      // [n_warps][32]
 };
 
 __host__ __device__ inline size_t epi_smem_bytes(int n_h, int KP, int n_warps) {
-    return (size_t)n_h * kTile * 4 + (size_t)n_h * KP * 8 + (size_t)n_h * 8 + (size_t)n_h * 32 * 4 +
+    return (size_t)n_h * kTile * 4 + (size_t)n_h * KP * 8 + (size_t)n_h * 12 + (size_t)n_h * 32 * 4 +
            (size_t)n_warps * 32 * 8;
 }
 
@@ -52,6 +53,7 @@ ES_DEV EpiSmem epi_carve(unsigned char* p, int n_h, int KP, int n_warps) {
     e.st_cnt = (int*)p;        p += (size_t)n_h * 4;
     e.st_m = (float*)p;        p += (size_t)n_h * 4;
     e.st_ls = (float*)p;       p += (size_t)n_h * 32 * 4;
+    e.st_xcnt = (int*)p;       p += (size_t)n_h * 4;
     e.scr_v = (float*)p;       p += (size_t)n_warps * 32 * 4;
     e.scr_p = (int*)p;
     return e;
@@ -60,6 +62,7 @@ ES_DEV EpiSmem epi_carve(unsigned char* p, int n_h, int KP, int n_warps) {
 ES_DEV void epi_init(const EpiSmem& e, int n_h) {
     for (int r = threadIdx.x; r < n_h; r += blockDim.x) {
         e.st_cnt[r] = 0;
+        e.st_xcnt[r] = 0;
         e.st_m[r] = -INFINITY;
     }
     for (int i = threadIdx.x; i < n_h * 32; i += blockDim.x) e.st_ls[i] = 0.0f;
@@ -301,21 +304,80 @@ ES_DEV void epi_tile(const EpiSmem& e, int n_h, int KP, int tn, int base_pos, in
 }
 
 // Write the CTA's state to the global partials (positions -> global ids).
+// Only [0, cnt) is written: extras may already sit at [cnt, cnt + xcnt).
 ES_DEV void epi_store(const EpiSmem& e, const LmhPartials& P, int cta, int n_h_total, int h_row0,
-                      int n_h, int KP, const int32_t* subset, int warp, int n_warps) {
+                      int n_h, int KP, int LS, const int32_t* subset, int warp, int n_warps) {
     for (int r = warp; r < n_h; r += n_warps) {
         const int cnt = e.st_cnt[r];
         const size_t o = ((size_t)cta * n_h_total + h_row0 + r);
-        for (int i = lane_id(); i < KP; i += 32) {
-            P.val[o * KP + i] = i < cnt ? e.st_val[r * KP + i] : -INFINITY;
-            P.id[o * KP + i] = i < cnt ? subset[e.st_pos[r * KP + i]] : -1;
+        for (int i = lane_id(); i < cnt; i += 32) {
+            P.val[o * LS + i] = e.st_val[r * KP + i];
+            P.id[o * LS + i] = subset[e.st_pos[r * KP + i]];
         }
         const float ssum = warp_sum(e.st_ls[r * 32 + lane_id()]);
         if (lane_id() == 0) {
             P.cnt[o] = cnt;
+            P.xcnt[o] = e.st_xcnt[r];
             P.m[o] = e.st_m[r];
             P.s[o] = ssum;
         }
+    }
+}
+
+// The CTA's last tile: online softmax as usual, but instead of folding the
+// survivors into the sorted list they are appended to the global partials as
+// unsorted extras (the finalisation scans them). Survivors must beat the
+// list's entry KP-1 -- any element of the CTA's top-KP does. Rows whose list
+// is not full, or with more survivors than LS - KP slots, take the full fold.
+ES_DEV void epi_tile_last(const EpiSmem& e, const LmhPartials& P, int cta, int n_h_total, int n_h, int KP, int LS,
+                          int tn, int base_pos, int warp, int n_warps, const int32_t* subset) {
+    if (tn <= 0) return;
+    const int lane = lane_id();
+    for (int r = warp; r < n_h; r += n_warps) {
+        float v[kTileJ];
+        float lm = -INFINITY;
+#pragma unroll
+        for (int j = 0; j < kTileJ; ++j) {
+            const int p = lane + 32 * j;
+            v[j] = p < tn ? e.tile[r * kTile + p] : -INFINITY;
+            lm = fmaxf(lm, v[j]);
+        }
+        fold_softmax(e, r, v, lm);
+        const int cnt = e.st_cnt[r];
+        if (KP > 32 || cnt < KP) {
+            if (KP <= 32) fold_topk32(e, r, KP, tn, base_pos, warp, v, lm);
+            else if (KP <= 64) fold_row<2>(e, r, KP, tn, base_pos);
+            else fold_row<3>(e, r, KP, tn, base_pos);
+            continue;
+        }
+        const float tv = e.st_val[r * KP + KP - 1];
+        const int tp = e.st_pos[r * KP + KP - 1];
+        bool cand[kTileJ];
+        unsigned msk[kTileJ];
+        int total = 0;
+#pragma unroll
+        for (int j = 0; j < kTileJ; ++j) {
+            cand[j] = v[j] != -INFINITY && before(v[j], base_pos + lane + 32 * j, tv, tp);
+            msk[j] = __ballot_sync(0xffffffffu, cand[j]);
+            total += __popc(msk[j]);
+        }
+        if (total > LS - KP) {
+            fold_topk32(e, r, KP, tn, base_pos, warp, v, lm);
+            continue;
+        }
+        const size_t o = ((size_t)cta * n_h_total + r);
+        int base = cnt;
+#pragma unroll
+        for (int j = 0; j < kTileJ; ++j) {
+            if (cand[j]) {
+                const int idx = base + __popc(msk[j] & ((1u << lane) - 1u));
+                P.val[o * LS + idx] = v[j];
+                P.id[o * LS + idx] = subset[base_pos + lane + 32 * j];
+            }
+            base += __popc(msk[j]);
+        }
+        if (lane == 0) e.st_xcnt[r] = total;
+        __syncwarp();
     }
 }
 
