@@ -471,7 +471,7 @@ static evospec_status lmh_impl(evospec_ctx* ctx, const void* W, int64_t n_w_rows
     a.W = W; a.n_w_rows = n_w_rows; a.d = c.d; a.w_dtype = c.w_dtype;
     a.H = H; a.n_h = n_h; a.h_dtype = c.h_dtype;
     a.subset = subset; a.n_subset_dev = n_subset_dev; a.n_subset_max = n_subset_max;
-    a.R = c.n_shards; a.KP = k + kTopkPad; a.LS = a.KP <= 32 ? 32 : a.KP; a.inv_temp = inv_temp;
+    a.R = c.n_shards; a.KP = k + kTopkPad; a.LS = a.KP <= 32 ? 64 : a.KP; a.inv_temp = inv_temp;
     a.logits_out = logits_out;
     a.part = ctx->part;
     a.m_ids = m_ids; a.m_vals = m_vals; a.m_lse = m_lse; a.m_probs = m_probs;

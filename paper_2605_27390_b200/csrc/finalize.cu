@@ -24,6 +24,7 @@
 namespace es {
 
 constexpr int kFinThreads = 256;
+constexpr int kFinCand = 1024;   // candidate buffer of the flat filter (finalize32)
 
 ES_DEV long long fin_gtime() {
     long long t;
@@ -328,7 +329,10 @@ lmh_finalize32_kernel(LmhArgs a, int n_cta, int k, float gamma, const float* __r
     __shared__ double red_d[32];
     __shared__ float bat_v[32];
     __shared__ int bat_p[32];
-    __shared__ float lse_s;
+    __shared__ float lse_s, th_s;
+    __shared__ int tot_s, cand_n;
+    __shared__ float cand_v[kFinCand];
+    __shared__ int cand_p[kFinCand];
     pdl_trigger();
     pdl_wait();
     if (threadIdx.x == 0) FIN_TRACE(0);
@@ -400,14 +404,58 @@ lmh_finalize32_kernel(LmhArgs a, int n_cta, int k, float gamma, const float* __r
         S = warp_sum(S);
         tot = warp_sum_i(tot);
         if (lane == 0) { row_max[r] = M; row_sumexp[r] = S; lse_s = S > 0.0f ? M + logf(S) : -INFINITY; }
-        // pre-threshold: KP-th largest lane max bounds the KP-th best from below
-        const float th0 = warp_kth_largest(lm, KP);
+        // pre-threshold: the KP-th largest lane max, and any full list's entry KP-1,
+        // bound the KP-th best from below
+        float thl = -INFINITY;
+        for (int c = lane; c < n_cta; c += 32)
+            if (l_cnt[c] >= KP) thl = fmaxf(thl, l_val[(size_t)c * LS + KP - 1]);
+        const float th0 = fmaxf(warp_kth_largest(lm, KP), warp_max(thl));
+        if (lane == 0) { th_s = th0; tot_s = tot; cand_n = 0; }
+    }
+    __syncthreads();
+    // B2. all threads: flat filter of every entry >= th0 into a candidate buffer
+    {
+        const float th0 = th_s;
+        for (int f = threadIdx.x; f < n_cta * LS; f += blockDim.x) {
+            const int c = f / LS, i = f - c * LS;
+            if (i < l_cnt[c] + l_x[c] && l_val[f] >= th0) {
+                const int o = atomicAdd(&cand_n, 1);
+                if (o < kFinCand) { cand_v[o] = l_val[f]; cand_p[o] = l_id[f]; }
+            }
+        }
+    }
+    __syncthreads();
+    if (warp == 0) {
+        const int tot = tot_s;
         float Lv = -INFINITY;
         int Lp = 0x7fffffff, cnt = 0;
-        // candidates: every entry >= th, gathered in batches of 32 (one per lane):
-        // sorted part with early exit, then the unsorted extras
+        float th = th_s;
+        const int ncand = cand_n;
+        if (ncand <= kFinCand) {
+            // batches of 32 candidates: bitonic sort, merge into the register list
+            for (int b0 = 0; b0 < ncand; b0 += 32) {
+                const int i = b0 + lane;
+                float bv = i < ncand ? cand_v[i] : -INFINITY;
+                int bp = i < ncand ? cand_p[i] : 0x7fffffff;
+                if (!(bv >= th)) { bv = -INFINITY; bp = 0x7fffffff; }
+                const unsigned m = __ballot_sync(0xffffffffu, bv != -INFINITY);
+                if (!m) continue;
+                warp_sort32(bv, bp);
+                const float rv = __shfl_sync(0xffffffffu, bv, 31 - lane);
+                const int rp = __shfl_sync(0xffffffffu, bp, 31 - lane);
+                if (before(rv, rp, Lv, Lp)) { Lv = rv; Lp = rp; }
+#pragma unroll
+                for (int j = 16; j > 0; j >>= 1) {
+                    const float ov = __shfl_xor_sync(0xffffffffu, Lv, j);
+                    const int op = __shfl_xor_sync(0xffffffffu, Lp, j);
+                    if (((lane & j) == 0) == before(ov, op, Lv, Lp)) { Lv = ov; Lp = op; }
+                }
+                cnt = min(cnt + __popc(m), KP);
+                if (cnt == KP) th = fmaxf(th, __shfl_sync(0xffffffffu, Lv, KP - 1));
+            }
+        } else {
+        // overflow fallback: every lane streams its own lists, one candidate per round
         int c_list = lane, c_pos = 0;               // this lane's cursor over its lists
-        float th = th0;                             // rises to the KP-th entry once the list is full
         while (true) {
             float x = -INFINITY;
             int xid = 0x7fffffff;
@@ -446,6 +494,7 @@ lmh_finalize32_kernel(LmhArgs a, int n_cta, int k, float gamma, const float* __r
             }
             cnt = min(cnt + __popc(m), KP);
             if (cnt == KP) th = fmaxf(th, __shfl_sync(0xffffffffu, Lv, KP - 1));
+        }
         }
         // C. runs: consecutive kept entries closer than 2 delta; those reaching the top k are re-scored
         double hn = 0.0;

@@ -59,7 +59,7 @@ struct LmhArgs {
     const void* W; int64_t n_w_rows; int d; int w_dtype;
     const void* H; int n_h; int h_dtype;
     const int32_t* subset; const int* n_subset_dev; int n_subset_max;
-    int R; int KP; int LS; float inv_temp;   // LS: list stride (KP <= 32: 32, else KP)
+    int R; int KP; int LS; float inv_temp;   // LS: list stride (KP <= 32: 64, else KP)
     float* logits_out;  // optional [n_h][n_subset_max]
     long long* trace;   // optional per-CTA globaltimer stamps [n_cta][8] (profiling)
     // optional fused single-shard merge outputs (R = 1): ids/vals [n_h][k], lse [n_h], probs [n_h][k]
