@@ -329,8 +329,9 @@ lmh_finalize32_kernel(LmhArgs a, int n_cta, int k, float gamma, const float* __r
     __shared__ double red_d[32];
     __shared__ float bat_v[32];
     __shared__ int bat_p[32];
-    __shared__ float lse_s, th_s;
-    __shared__ int tot_s, cand_n;
+    __shared__ float lse_s, th_s, vmax_s;
+    __shared__ int tot_s, cand_n, bmin_s;
+    __shared__ int fhist[256];
     __shared__ float cand_v[kFinCand];
     __shared__ int cand_p[kFinCand];
     pdl_trigger();
@@ -410,15 +411,52 @@ lmh_finalize32_kernel(LmhArgs a, int n_cta, int k, float gamma, const float* __r
         for (int c = lane; c < n_cta; c += 32)
             if (l_cnt[c] >= KP) thl = fmaxf(thl, l_val[(size_t)c * LS + KP - 1]);
         const float th0 = fmaxf(warp_kth_largest(lm, KP), warp_max(thl));
-        if (lane == 0) { th_s = th0; tot_s = tot; cand_n = 0; }
+        const float vmax = warp_max(lm);
+        if (lane == 0) { th_s = th0; vmax_s = vmax; tot_s = tot; cand_n = 0; }
+    }
+    for (int b = threadIdx.x; b < 256; b += blockDim.x) fhist[b] = 0;
+    __syncthreads();
+    // B2. all threads: histogram the entries >= th0 over [th0, vmax] (256 bins),
+    //     then keep the bins from the top down to the one that reaches KP: bin()
+    //     is monotone in the value, so every true top-KP entry is kept
+    const float th0 = th_s, vmax = vmax_s;
+    const float bscale = vmax > th0 ? 255.99f / (vmax - th0) : 0.0f;
+    auto bin_of = [&](float v) { return min(255, (int)((v - th0) * bscale)); };
+    for (int f = threadIdx.x; f < n_cta * LS; f += blockDim.x) {
+        const int c = f / LS, i = f - c * LS;
+        if (i < l_cnt[c] + l_x[c] && l_val[f] >= th0) atomicAdd(&fhist[bin_of(l_val[f])], 1);
     }
     __syncthreads();
-    // B2. all threads: flat filter of every entry >= th0 into a candidate buffer
+    if (warp == 0) {
+        int hb[8], t8 = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) { hb[j] = fhist[8 * lane + j]; t8 += hb[j]; }
+        int inc = t8;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_down_sync(0xffffffffu, inc, o);
+            if (lane + o < 32) inc += v;
+        }
+        int run = inc - t8;                          // entries in higher lanes' bins
+        int found = 0;
+        bool hit = false;
+#pragma unroll
+        for (int j = 7; j >= 0; --j) {
+            if (!hit && run + hb[j] >= KP) { found = 8 * lane + j; hit = true; }
+            run += hb[j];
+        }
+        const unsigned hm = __ballot_sync(0xffffffffu, hit);
+        // the highest lane with a hit holds the boundary bin (bins ascend with lanes)
+        const int src = hm ? 31 - __clz(hm) : 0;
+        found = __shfl_sync(0xffffffffu, found, src);
+        if (lane == 0) bmin_s = hm ? found : 0;
+    }
+    __syncthreads();
     {
-        const float th0 = th_s;
+        const int bmin = bmin_s;
         for (int f = threadIdx.x; f < n_cta * LS; f += blockDim.x) {
             const int c = f / LS, i = f - c * LS;
-            if (i < l_cnt[c] + l_x[c] && l_val[f] >= th0) {
+            if (i < l_cnt[c] + l_x[c] && l_val[f] >= th0 && bin_of(l_val[f]) >= bmin) {
                 const int o = atomicAdd(&cand_n, 1);
                 if (o < kFinCand) { cand_v[o] = l_val[f]; cand_p[o] = l_id[f]; }
             }
