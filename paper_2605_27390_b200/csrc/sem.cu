@@ -54,6 +54,11 @@ sem_scan_kernel(const void* __restrict__ E, int64_t n_rows, int d,
         double v = 0.0;
         if (c < d) v = q_dtype == 0 ? (double)bf16_bits_to_f32(((const uint16_t*)q)[c])
                                     : (double)((const float*)q)[c];
+        // bf16 E: q is pre-scaled by 2^896 (exact; |q| < 2^128 stays finite) so
+        // that each E element can enter as the "raw" double whose fields are the
+        // bf16 fields in place (value e * 2^-896, exact, no conversion unit):
+        // the product q*e, hence every fma, is bit-identical to the unscaled one
+        if (DT == 0) v *= 0x1p896;
         q_sm[(s * ELEMS + j) * 32 + lane] = v;
     }
     __syncthreads();
@@ -86,10 +91,17 @@ sem_scan_kernel(const void* __restrict__ E, int64_t n_rows, int d,
 #pragma unroll
             for (int r = 0; r < 16; ++r) {
                 if constexpr (DT == 0) {
-                    float f[8];
-                    unpack_bf16x8(u[r], f);
+                    const uint32_t w4[4] = {u[r].x, u[r].y, u[r].z, u[r].w};
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) acc[r] = fma((double)f[j], qv[j], acc[r]);
+                    for (int j = 0; j < 4; ++j) {
+                        // sign | exp | mant of a bf16 moved to the double's field positions:
+                        // arithmetic >> 3 puts exp at [27:20], mant at [19:13]; the mask
+                        // keeps the sign at bit 31 (bf16 zero / denormal map exactly too)
+                        const uint32_t lo = (uint32_t)((int32_t)(w4[j] << 16) >> 3) & 0x8FFFE000u;
+                        const uint32_t hi = (uint32_t)((int32_t)w4[j] >> 3) & 0x8FFFE000u;
+                        acc[r] = fma(__hiloint2double((int)lo, 0), qv[2 * j], acc[r]);
+                        acc[r] = fma(__hiloint2double((int)hi, 0), qv[2 * j + 1], acc[r]);
+                    }
                 } else {
                     float f[4] = {__uint_as_float(u[r].x), __uint_as_float(u[r].y),
                                   __uint_as_float(u[r].z), __uint_as_float(u[r].w)};
