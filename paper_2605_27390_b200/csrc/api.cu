@@ -153,7 +153,7 @@ struct evospec_ctx {
 
 namespace {
 constexpr int kTimingSlots = 4096;
-constexpr int kTraceLen = 2 * kNumSMs * 8 + 16;   // LM-head CTAs, finalize rows, union stamps
+constexpr int kTraceLen = 2 * kNumSMs * 8 + 16 + 32;   // LM-head CTAs, finalize rows, union stamps
 
 // union stamps live after the LM-head / finalize slots
 long long* union_trace(evospec_ctx* ctx, cudaStream_t st) {

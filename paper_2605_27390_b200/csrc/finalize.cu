@@ -17,6 +17,9 @@
 //      the k-th candidate reaches the last kept candidate while candidates
 //      were dropped, the result cannot be certified: EVOSPEC_FLAG_UNCERTIFIED.
 // merge_kernel (one warp per H row): the shard merge of SURVEY §8(c) step 12.
+#include <algorithm>
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.cuh"
 #include "lmh_epilogue.cuh"   // warp_kth_largest
@@ -24,7 +27,8 @@
 namespace es {
 
 constexpr int kFinThreads = 256;
-constexpr int kFinCand = 1024;   // candidate buffer of the flat filter (finalize32)
+constexpr int kFinCand = 1024;   // candidate buffer of the threshold filter (finalize32)
+constexpr int kFin32MaxD = 8192; // H row staged in smem by finalize32 (d <= this for the fast re-score)
 
 ES_DEV long long fin_gtime() {
     long long t;
@@ -32,6 +36,8 @@ ES_DEV long long fin_gtime() {
     return t;
 }
 // profiling stamps (EVOSPEC_TRACE): slots [148*8 + row*8 + i]
+// fine-grained clock64 stamps of row 0 (thread 0 / warp 0 lane 0), slots [2*148*8 + 16 + i]
+#define FIN_DT(i) do { if (a.trace && blockIdx.x == 0) a.trace[2 * 148 * 8 + 16 + (i)] = clock64(); } while (0)
 #define FIN_TRACE(slot) do { if (a.trace && blockIdx.x < 148) a.trace[148 * 8 + (size_t)blockIdx.x * 8 + (slot)] = fin_gtime(); } while (0)
 
 ES_DEV double load_elem(const void* p, int dtype, size_t i) {
@@ -232,7 +238,7 @@ lmh_finalize_kernel(LmhArgs a, int n_cta, int k, float gamma, const float* __res
     const int nn = n_need_s;
     for (int q = warp; q < nn; q += nwarps) {
         const int c = need_list[q];
-        const size_t row = (size_t)(c_id[c] / a.R);
+        const size_t row = (size_t)(__ldg(&a.subset[c_id[c]]) / a.R);
         double acc = 0.0;
         if (a.w_dtype == 0 && a.h_dtype == 0 && a.d % 8 == 0) {   // 16-byte loads, 4 in flight per lane
             const uint4* wp = (const uint4*)((const uint16_t*)a.W + row * a.d);
@@ -286,10 +292,11 @@ lmh_finalize_kernel(LmhArgs a, int n_cta, int k, float gamma, const float* __res
         }
         const float lse = row_sumexp[r] > 0.0f ? row_max[r] + logf(row_sumexp[r]) : -INFINITY;
         for (int t = 0; t < k; ++t) {
-            topk_ids[(size_t)r * k + t] = t < nk ? c_id[t] : -1;
+            const int oid = t < nk ? __ldg(&a.subset[c_id[t]]) : -1;
+            topk_ids[(size_t)r * k + t] = oid;
             topk_vals[(size_t)r * k + t] = t < nk ? (float)c_e[t] : -INFINITY;
             if (a.m_ids) {   // fused single-shard merge (R = 1)
-                a.m_ids[(size_t)r * k + t] = t < nk ? c_id[t] : -1;
+                a.m_ids[(size_t)r * k + t] = oid;
                 a.m_vals[(size_t)r * k + t] = t < nk ? (float)c_e[t] : -INFINITY;
                 if (a.m_probs) a.m_probs[(size_t)r * k + t] = t < nk ? expf((float)c_e[t] - lse) : 0.0f;
             }
@@ -301,298 +308,290 @@ lmh_finalize_kernel(LmhArgs a, int n_cta, int k, float gamma, const float* __res
 }
 
 
-// Leaner finalisation for KP <= 32 (k <= 24): all global loads are issued up
-// front, the best KP of the per-CTA lists are formed by warp 0 with batched
-// bitonic sort + merge (lmh_epilogue.cuh), runs are detected warp-parallel in
-// registers, flagged candidates are re-scored exactly by all warps, and one
-// warp sort by (exact-if-re-scored value desc, id asc) yields the order.
-__global__ void __launch_bounds__(kFinThreads)
+// Finalisation for KP <= 32 (k <= 24). The partial lists have a fixed stride of
+// kFin32LS = 64 slots and unused slots hold -inf (epi_store), so a row's
+// entries form one flat array of n_cta * 64 values, loaded in one round trip
+// into registers (U float4 + int4 per thread):
+//   A. loads; per list (thread c): softmax state and th_c = its sorted entry
+//      KP-1 when the sorted part is full (th_c <= the row's KP-th best)
+//   B. th0 = max_c th_c; the entries >= th0 (every top-KP entry among them)
+//      are appended to a candidate buffer
+//   C. exact ranks: candidate i's rank is the number of candidates before it
+//      under (value desc, id asc) -- one thread per candidate, no sort network;
+//      ranks < KP give the sorted list. Warp 0 then finds the runs (consecutive
+//      entries closer than 2 delta) that reach the top k.
+//   D. exact fp64 re-score of those run members (one warp each)
+//   E. one warp sort by (exact-if-re-scored value desc, id asc); write the top k
+// Degenerate rows (more than kFin32RankMax candidates: massive ties, or no
+// full list) take a slower exact path: warp 0 merges sorted batches of 32.
+constexpr int kFin32Threads = 512;
+constexpr int kFin32LS = 64;
+constexpr int kFin32RankMax = 256;
+
+ES_DEV void sort32_rolled(float& v, int& p) {
+    const int lane = lane_id();
+#pragma unroll 1
+    for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll 1
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            const float ov = __shfl_xor_sync(0xffffffffu, v, j);
+            const int op = __shfl_xor_sync(0xffffffffu, p, j);
+            const bool keep_better = ((lane & j) == 0) == ((lane & k) == 0);
+            if (keep_better == before(ov, op, v, p)) { v = ov; p = op; }
+        }
+    }
+}
+
+template <int U>
+__global__ void __launch_bounds__(kFin32Threads)
 lmh_finalize32_kernel(LmhArgs a, int n_cta, int k, float gamma, const float* __restrict__ wmax_dev,
                       int32_t* __restrict__ topk_ids, float* __restrict__ topk_vals,
                       float* __restrict__ row_max, float* __restrict__ row_sumexp, int* flags) {
     const int r = blockIdx.x;
     const int KP = a.KP;
-    const int lane = lane_id(), warp = warp_id(), nwarps = blockDim.x / 32;
-    extern __shared__ unsigned char f_sm[];
-    const int LS = a.LS;                            // list stride (32): sorted + extras
-    int* l_cnt = (int*)f_sm;                        // [n_cta] sorted entries
-    int* l_x = l_cnt + n_cta;                       // [n_cta] unsorted extras
-    float* l_m = (float*)(l_x + n_cta);             // [n_cta]
-    float* l_s = l_m + n_cta;                       // [n_cta]
-    float* l_val = (float*)(((uintptr_t)(l_s + n_cta) + 15) & ~(uintptr_t)15);   // [n_cta][LS]
-    int32_t* l_id = (int32_t*)(l_val + (size_t)n_cta * LS);
-    __shared__ float c_v[32];
-    __shared__ int32_t c_id[32];
-    __shared__ double c_e[32];
-    __shared__ int need_list[32];
-    __shared__ int n_need_s, nk_s;
-    __shared__ double red_d[32];
-    __shared__ float bat_v[32];
-    __shared__ int bat_p[32];
-    __shared__ float lse_s, th_s, vmax_s;
-    __shared__ int tot_s, cand_n, bmin_s;
-    __shared__ int fhist[256];
+    const int lane = lane_id(), warp = warp_id();
+    constexpr int nwarps = kFin32Threads / 32;
+    __shared__ float w_M[nwarps], w_S[nwarps], w_th[nwarps];
+    __shared__ int w_tot[nwarps];
+    __shared__ double red_d[nwarps];
     __shared__ float cand_v[kFinCand];
     __shared__ int cand_p[kFinCand];
+    __shared__ float c_v[32];
+    __shared__ int32_t c_id[32], c_gid[32];
+    __shared__ double c_e[32];
+    __shared__ int need_list[32];
+    __shared__ int n_need_s, nk_s, tot_s, cand_n;
+    __shared__ float lse_s, th_s;
+    __shared__ float s_head[kFin32Threads];
+    __shared__ __align__(16) uint16_t h_row[kFin32MaxD];
     pdl_trigger();
     pdl_wait();
-    if (threadIdx.x == 0) FIN_TRACE(0);
-    // A. every load at once: CTA states, list entries (16-byte loads, 4 in flight), H row
-    for (int c = threadIdx.x; c < n_cta; c += blockDim.x) {
-        const size_t o = (size_t)c * a.n_h + r;
-        l_cnt[c] = __ldcg(&a.part.cnt[o]);
-        l_x[c] = __ldcg(&a.part.xcnt[o]);
-        l_m[c] = __ldcg(&a.part.m[o]);
-        l_s[c] = __ldcg(&a.part.s[o]);
+    if (threadIdx.x == 0) { FIN_TRACE(0); FIN_DT(0); }
+    // A. every global load at once
+    const int nq = n_cta * (kFin32LS / 4);
+    float4 vv[U];
+    int4 ii[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const int q = threadIdx.x + u * kFin32Threads;
+        vv[u] = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+        if (q < nq) {
+            const size_t o = ((size_t)(q >> 4) * a.n_h + r) * kFin32LS + (q & 15) * 4;
+            vv[u] = __ldcg((const float4*)&a.part.val[o]);
+            ii[u] = __ldcg((const int4*)&a.part.id[o]);
+        }
+    }
+    float cm_ = -INFINITY, cs_ = 0.0f, thl = -INFINITY;
+    if ((int)threadIdx.x < n_cta) {
+        const size_t o = (size_t)threadIdx.x * a.n_h + r;
+        cm_ = __ldcg(&a.part.m[o]);
+        cs_ = __ldcg(&a.part.s[o]);
+        const int cn = __ldcg(&a.part.cnt[o]);
+        const float vk = __ldcg(&a.part.val[o * kFin32LS + KP - 1]);
+        if (cn >= KP) thl = vk;
+        s_head[threadIdx.x] = __ldcg(&a.part.val[o * kFin32LS]);   // the list maximum (sorted head)
+    }
+    const float wmax = __ldg(wmax_dev);
+    double hacc = 0.0;
+    const bool h_fast = a.h_dtype == 0 && a.d % 8 == 0 && a.d <= kFin32MaxD;
+    if (h_fast) {
+        const uint4* hp = (const uint4*)((const uint16_t*)a.H + (size_t)r * a.d);
+        for (int c = threadIdx.x; c < a.d / 8; c += kFin32Threads) {
+            const uint4 hv = hp[c];
+            ((uint4*)h_row)[c] = hv;
+            float f[8];
+            unpack_bf16x8(hv, f);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) hacc = fma((double)f[j], (double)f[j], hacc);
+        }
+    } else {
+#pragma unroll 1
+        for (int col = threadIdx.x; col < a.d; col += kFin32Threads) {
+            const double h = load_elem(a.H, a.h_dtype, (size_t)r * a.d + col);
+            hacc = fma(h, h, hacc);
+        }
+    }
+    if (threadIdx.x == 0) { cand_n = 0; th_s = -INFINITY; }
+    {
+        int tcnt = 0;
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            tcnt += (vv[u].x != -INFINITY) + (vv[u].y != -INFINITY) + (vv[u].z != -INFINITY) + (vv[u].w != -INFINITY);
+        const float Mw = warp_max(cs_ > 0.0f ? cm_ : -INFINITY);
+        const float Sw = warp_sum(cs_ > 0.0f ? cs_ * expf(cm_ - Mw) : 0.0f);
+        thl = warp_max(thl);
+        tcnt = warp_sum_i(tcnt);
+        hacc = warp_sum_d(hacc);
+        if (lane == 0) { w_M[warp] = Mw; w_S[warp] = Sw; w_th[warp] = thl; w_tot[warp] = tcnt; red_d[warp] = hacc; }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) { FIN_TRACE(1); FIN_DT(1); }
+    // B. threshold: the KP-th largest list head (KP distinct entries) and any full
+    //    list's entry KP-1 both bound the row's KP-th best from below
+    if ((int)threadIdx.x < n_cta && n_cta >= KP) {
+        const float hv = s_head[threadIdx.x];
+        int gt = 0, ge = 0;
+#pragma unroll 4
+        for (int c = 0; c < n_cta; ++c) {
+            const float o = s_head[c];
+            gt += o > hv;
+            ge += o >= hv;
+        }
+        if (hv != -INFINITY && gt < KP && KP <= ge) th_s = hv;   // the KP-th largest head value
+    }
+    __syncthreads();
+    float th0 = th_s;
+#pragma unroll
+    for (int w = 0; w < nwarps; ++w) th0 = fmaxf(th0, w_th[w]);
+    if (warp == 0) {   // softmax combine and entry count (lanes = warps)
+        const bool have = lane < nwarps && w_S[lane] > 0.0f;
+        const float M = warp_max(have ? w_M[lane] : -INFINITY);
+        const float S = warp_sum(have ? w_S[lane] * expf(w_M[lane] - M) : 0.0f);
+        const int tot = warp_sum_i(lane < nwarps ? w_tot[lane] : 0);
+        if (lane == 0) {
+            row_max[r] = M;
+            row_sumexp[r] = S;
+            lse_s = S > 0.0f ? M + logf(S) : -INFINITY;
+            tot_s = tot;
+        }
     }
     {
-        const int nq = n_cta * (LS / 4);            // float4 per list
-        for (int q0 = 0; q0 < nq; q0 += 4 * blockDim.x) {
-            float4 vv[4];
-            int4 ii[4];
+        auto keep = [&](float x) { return x != -INFINITY && x >= th0; };
+        int nk = 0;
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int q = q0 + u * blockDim.x + threadIdx.x;
-                const int c = q / (LS / 4), part = q - c * (LS / 4);
-                const size_t o = ((size_t)c * a.n_h + r) * LS + part * 4;
+        for (int u = 0; u < U; ++u) nk += keep(vv[u].x) + keep(vv[u].y) + keep(vv[u].z) + keep(vv[u].w);
+        if (nk) {
+            int o = atomicAdd(&cand_n, nk);
+            auto put = [&](float x, int id) {
+                if (keep(x)) {
+                    if (o < kFinCand) { cand_v[o] = x; cand_p[o] = id; }
+                    ++o;
+                }
+            };
+#pragma unroll
+            for (int u = 0; u < U; ++u) { put(vv[u].x, ii[u].x); put(vv[u].y, ii[u].y); put(vv[u].z, ii[u].z); put(vv[u].w, ii[u].w); }
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) { FIN_TRACE(2); FIN_DT(2); }
+    const int ncand = cand_n;
+    if (ncand <= kFin32RankMax) {
+        // C1. exact ranks, one thread per candidate
+        if ((int)threadIdx.x < ncand) {
+            const float v = cand_v[threadIdx.x];
+            const int p = cand_p[threadIdx.x];
+            int rank = 0;
+#pragma unroll 4
+            for (int j = 0; j < ncand; ++j) rank += before(cand_v[j], cand_p[j], v, p);
+            if (rank < KP) { c_v[rank] = v; c_id[rank] = p; }
+        }
+        if (threadIdx.x == 0) nk_s = min(ncand, KP);
+    } else if (warp == 0) {
+        // C1'. degenerate rows: sorted batches of 32 merged into the register list,
+        //      from the candidate buffer or (overflow) the whole row in the partials
+        float Lv = -INFINITY, th = -INFINITY;
+        int Lp = 0x7fffffff, thp = 0x7fffffff, cnt = 0;
+        const bool all = ncand > kFinCand;
+        const int nb = all ? ((nq + 31) / 32) * 4 : (ncand + 31) / 32;
+#pragma unroll 1
+        for (int b = 0; b < nb; ++b) {
+            float bv = -INFINITY;
+            int bp = 0x7fffffff;
+            if (!all) {
+                const int i = b * 32 + lane;
+                if (i < ncand) { bv = cand_v[i]; bp = cand_p[i]; }
+            } else {
+                const int q = (b >> 2) * 32 + lane, comp = b & 3;
                 if (q < nq) {
-                    vv[u] = __ldcg((const float4*)&a.part.val[o]);
-                    ii[u] = __ldcg((const int4*)&a.part.id[o]);
+                    const size_t o = ((size_t)(q >> 4) * a.n_h + r) * kFin32LS + (q & 15) * 4 + comp;
+                    bv = __ldcg(&a.part.val[o]);
+                    bp = __ldcg(&a.part.id[o]);
                 }
             }
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int q = q0 + u * blockDim.x + threadIdx.x;
-                if (q < nq) { ((float4*)l_val)[q] = vv[u]; ((int4*)l_id)[q] = ii[u]; }
-            }
-        }
-    }
-    {
-        double acc = 0.0;
-        if (a.h_dtype == 0 && a.d % 8 == 0) {
-            const uint4* hp = (const uint4*)((const uint16_t*)a.H + (size_t)r * a.d);
-            for (int c = threadIdx.x; c < a.d / 8; c += blockDim.x) {
-                float f[8];
-                unpack_bf16x8(hp[c], f);
-#pragma unroll
-                for (int j = 0; j < 8; ++j) acc = fma((double)f[j], (double)f[j], acc);
-            }
-        } else {
-            for (int col = threadIdx.x; col < a.d; col += blockDim.x) {
-                const double h = load_elem(a.H, a.h_dtype, (size_t)r * a.d + col);
-                acc = fma(h, h, acc);
-            }
-        }
-        acc = warp_sum_d(acc);
-        if (lane == 0) red_d[warp] = acc;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) FIN_TRACE(1);
-    // B. warp 0: softmax combine + the best KP entries
-    if (warp == 0) {
-        float M = -INFINITY;
-        for (int c = lane; c < n_cta; c += 32) if (l_s[c] > 0.0f) M = fmaxf(M, l_m[c]);
-        M = warp_max(M);
-        float S = 0.0f;
-        int tot = 0;
-        float lm = -INFINITY;                       // lane max of its lists (head and extras)
-        for (int c = lane; c < n_cta; c += 32) {
-            if (l_s[c] > 0.0f) S += l_s[c] * expf(l_m[c] - M);
-            tot += l_cnt[c] + l_x[c];
-            if (l_cnt[c] > 0) lm = fmaxf(lm, l_val[(size_t)c * LS]);
-            for (int i = l_cnt[c]; i < l_cnt[c] + l_x[c]; ++i) lm = fmaxf(lm, l_val[(size_t)c * LS + i]);
-        }
-        S = warp_sum(S);
-        tot = warp_sum_i(tot);
-        if (lane == 0) { row_max[r] = M; row_sumexp[r] = S; lse_s = S > 0.0f ? M + logf(S) : -INFINITY; }
-        // pre-threshold: the KP-th largest lane max, and any full list's entry KP-1,
-        // bound the KP-th best from below
-        float thl = -INFINITY;
-        for (int c = lane; c < n_cta; c += 32)
-            if (l_cnt[c] >= KP) thl = fmaxf(thl, l_val[(size_t)c * LS + KP - 1]);
-        const float th0 = fmaxf(warp_kth_largest(lm, KP), warp_max(thl));
-        const float vmax = warp_max(lm);
-        if (lane == 0) { th_s = th0; vmax_s = vmax; tot_s = tot; cand_n = 0; }
-    }
-    for (int b = threadIdx.x; b < 256; b += blockDim.x) fhist[b] = 0;
-    __syncthreads();
-    // B2. all threads: histogram the entries >= th0 over [th0, vmax] (256 bins),
-    //     then keep the bins from the top down to the one that reaches KP: bin()
-    //     is monotone in the value, so every true top-KP entry is kept
-    const float th0 = th_s, vmax = vmax_s;
-    const float bscale = vmax > th0 ? 255.99f / (vmax - th0) : 0.0f;
-    auto bin_of = [&](float v) { return min(255, (int)((v - th0) * bscale)); };
-    for (int f = threadIdx.x; f < n_cta * LS; f += blockDim.x) {
-        const int c = f / LS, i = f - c * LS;
-        if (i < l_cnt[c] + l_x[c] && l_val[f] >= th0) atomicAdd(&fhist[bin_of(l_val[f])], 1);
-    }
-    __syncthreads();
-    if (warp == 0) {
-        int hb[8], t8 = 0;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) { hb[j] = fhist[8 * lane + j]; t8 += hb[j]; }
-        int inc = t8;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int v = __shfl_down_sync(0xffffffffu, inc, o);
-            if (lane + o < 32) inc += v;
-        }
-        int run = inc - t8;                          // entries in higher lanes' bins
-        int found = 0;
-        bool hit = false;
-#pragma unroll
-        for (int j = 7; j >= 0; --j) {
-            if (!hit && run + hb[j] >= KP) { found = 8 * lane + j; hit = true; }
-            run += hb[j];
-        }
-        const unsigned hm = __ballot_sync(0xffffffffu, hit);
-        // the highest lane with a hit holds the boundary bin (bins ascend with lanes)
-        const int src = hm ? 31 - __clz(hm) : 0;
-        found = __shfl_sync(0xffffffffu, found, src);
-        if (lane == 0) bmin_s = hm ? found : 0;
-    }
-    __syncthreads();
-    {
-        const int bmin = bmin_s;
-        for (int f = threadIdx.x; f < n_cta * LS; f += blockDim.x) {
-            const int c = f / LS, i = f - c * LS;
-            if (i < l_cnt[c] + l_x[c] && l_val[f] >= th0 && bin_of(l_val[f]) >= bmin) {
-                const int o = atomicAdd(&cand_n, 1);
-                if (o < kFinCand) { cand_v[o] = l_val[f]; cand_p[o] = l_id[f]; }
-            }
-        }
-    }
-    __syncthreads();
-    if (warp == 0) {
-        const int tot = tot_s;
-        float Lv = -INFINITY;
-        int Lp = 0x7fffffff, cnt = 0;
-        float th = th_s;
-        const int ncand = cand_n;
-        if (ncand <= kFinCand) {
-            // batches of 32 candidates: bitonic sort, merge into the register list
-            for (int b0 = 0; b0 < ncand; b0 += 32) {
-                const int i = b0 + lane;
-                float bv = i < ncand ? cand_v[i] : -INFINITY;
-                int bp = i < ncand ? cand_p[i] : 0x7fffffff;
-                if (!(bv >= th)) { bv = -INFINITY; bp = 0x7fffffff; }
-                const unsigned m = __ballot_sync(0xffffffffu, bv != -INFINITY);
-                if (!m) continue;
-                warp_sort32(bv, bp);
-                const float rv = __shfl_sync(0xffffffffu, bv, 31 - lane);
-                const int rp = __shfl_sync(0xffffffffu, bp, 31 - lane);
-                if (before(rv, rp, Lv, Lp)) { Lv = rv; Lp = rp; }
-#pragma unroll
-                for (int j = 16; j > 0; j >>= 1) {
-                    const float ov = __shfl_xor_sync(0xffffffffu, Lv, j);
-                    const int op = __shfl_xor_sync(0xffffffffu, Lp, j);
-                    if (((lane & j) == 0) == before(ov, op, Lv, Lp)) { Lv = ov; Lp = op; }
-                }
-                cnt = min(cnt + __popc(m), KP);
-                if (cnt == KP) th = fmaxf(th, __shfl_sync(0xffffffffu, Lv, KP - 1));
-            }
-        } else {
-        // overflow fallback: every lane streams its own lists, one candidate per round
-        int c_list = lane, c_pos = 0;               // this lane's cursor over its lists
-        while (true) {
-            float x = -INFINITY;
-            int xid = 0x7fffffff;
-            bool has = false;
-            while (c_list < n_cta) {
-                const int ns = l_cnt[c_list], ne = ns + l_x[c_list];
-                if (c_pos < ns && l_val[(size_t)c_list * LS + c_pos] < th) c_pos = ns;   // sorted: rest is lower
-                while (c_pos >= ns && c_pos < ne && l_val[(size_t)c_list * LS + c_pos] < th) ++c_pos;
-                if (c_pos < ne) {
-                    x = l_val[(size_t)c_list * LS + c_pos];
-                    xid = l_id[(size_t)c_list * LS + c_pos];
-                    has = true;
-                    ++c_pos;
-                    break;
-                }
-                c_list += 32;
-                c_pos = 0;
-            }
-            const unsigned m = __ballot_sync(0xffffffffu, has);
-            if (!m) break;
-            bat_v[lane] = x;                        // one batch = one candidate per lane
-            bat_p[lane] = xid;
-            __syncwarp();
-            float bv = bat_v[lane];
-            int bp = bat_p[lane];
-            __syncwarp();
-            warp_sort32(bv, bp);
+            if (cnt == KP && !before(bv, bp, th, thp)) { bv = -INFINITY; bp = 0x7fffffff; }
+            const unsigned m = __ballot_sync(0xffffffffu, bv != -INFINITY);
+            if (!m) continue;
+            sort32_rolled(bv, bp);
             const float rv = __shfl_sync(0xffffffffu, bv, 31 - lane);
             const int rp = __shfl_sync(0xffffffffu, bp, 31 - lane);
             if (before(rv, rp, Lv, Lp)) { Lv = rv; Lp = rp; }
-#pragma unroll
+#pragma unroll 1
             for (int j = 16; j > 0; j >>= 1) {
                 const float ov = __shfl_xor_sync(0xffffffffu, Lv, j);
                 const int op = __shfl_xor_sync(0xffffffffu, Lp, j);
                 if (((lane & j) == 0) == before(ov, op, Lv, Lp)) { Lv = ov; Lp = op; }
             }
             cnt = min(cnt + __popc(m), KP);
-            if (cnt == KP) th = fmaxf(th, __shfl_sync(0xffffffffu, Lv, KP - 1));
-        }
-        }
-        // C. runs: consecutive kept entries closer than 2 delta; those reaching the top k are re-scored
-        double hn = 0.0;
-        for (int w = 0; w < nwarps; ++w) hn += red_d[w];
-        const double delta = (double)gamma * sqrt(hn) * (double)*wmax_dev * (double)a.inv_temp;
-        const float nv = __shfl_down_sync(0xffffffffu, Lv, 1);
-        const bool close = lane + 1 < cnt && (double)Lv - (double)nv <= 2.0 * delta + 2.4e-7 * fabs((double)Lv);
-        const unsigned cm = __ballot_sync(0xffffffffu, close);   // bit i: entry i and i+1 in one run
-        // entry i is in a multi-entry run reaching the top k if a chain of close links connects it to an index < k
-        bool need = false;
-        {
-            // run start s(i): walk down while link (i-1) is close
-            int st_i = lane;
-            while (st_i > 0 && ((cm >> (st_i - 1)) & 1u)) --st_i;
-            const bool multi = (lane > 0 && ((cm >> (lane - 1)) & 1u)) || ((cm >> lane) & 1u);
-            need = lane < cnt && multi && st_i < k;
-        }
-        const unsigned nm = __ballot_sync(0xffffffffu, need);
-        if (need) need_list[__popc(nm & ((1u << lane) - 1u))] = lane;
-        // uncertified: the run holding index k-1 reaches the last kept entry while entries were dropped
-        {
-            int end_k = k - 1;
-            while (end_k + 1 < cnt && ((cm >> end_k) & 1u)) ++end_k;
-            const bool unc = (k - 1 < cnt && end_k == cnt - 1 && tot > cnt && cnt >= k) || !(delta >= 0.0) || isinf(delta);
-            if (lane == 0 && unc) atomicOr(flags, kFlagUncertified);
+            if (cnt == KP) { th = __shfl_sync(0xffffffffu, Lv, KP - 1); thp = __shfl_sync(0xffffffffu, Lp, KP - 1); }
         }
         c_v[lane] = Lv;
         c_id[lane] = Lp;
-        if (lane == 0) { n_need_s = __popc(nm); nk_s = cnt; }
+        if (lane == 0) nk_s = cnt;
     }
     __syncthreads();
-    if (threadIdx.x == 0) FIN_TRACE(4);
-    // D. exact re-score of the flagged entries (one warp each)
+    if (threadIdx.x == 0) { FIN_TRACE(3); FIN_DT(3); }
+    if (warp == 0) {
+        // C2. runs: consecutive kept entries closer than 2 delta; those reaching the top k are re-scored
+        const int cnt = nk_s, tot = tot_s;
+        const float Lv = lane < cnt ? c_v[lane] : -INFINITY;
+        c_gid[lane] = lane < cnt ? __ldg(&a.subset[c_id[lane]]) : -1;   // position -> vocabulary id
+        double hn = 0.0;
+#pragma unroll
+        for (int w = 0; w < nwarps; ++w) hn += red_d[w];
+        const double delta = (double)gamma * sqrt(hn) * (double)wmax * (double)a.inv_temp;
+        const float nv = __shfl_down_sync(0xffffffffu, Lv, 1);
+        const bool close = lane + 1 < cnt && (double)Lv - (double)nv <= 2.0 * delta + 2.4e-7 * fabs((double)Lv);
+        const unsigned cm = __ballot_sync(0xffffffffu, close);   // bit i: entry i and i+1 in one run
+        // run start: just above the highest open link below the lane
+        const unsigned below = ~cm & ((1u << lane) - 1u);
+        const int st_i = below ? 32 - __clz(below) : 0;
+        const bool multi = (lane > 0 && ((cm >> (lane - 1)) & 1u)) || ((cm >> lane) & 1u);
+        const bool need = lane < cnt && multi && st_i < k;
+        const unsigned nm = __ballot_sync(0xffffffffu, need);
+        if (need) need_list[__popc(nm & ((1u << lane) - 1u))] = lane;
+        // uncertified: the run holding index k-1 reaches the last kept entry while entries were dropped
+        const unsigned open_from_k = ~cm & ~((1u << (k - 1)) - 1u);   // open links at index >= k-1
+        const int end_k = open_from_k ? __ffs(open_from_k) - 1 : 31;
+        const bool unc = (k - 1 < cnt && min(end_k, cnt - 1) == cnt - 1 && tot > cnt && cnt >= k) ||
+                         !(delta >= 0.0) || isinf(delta);
+        if (lane == 0) {
+            if (unc) atomicOr(flags, kFlagUncertified);
+            n_need_s = __popc(nm);
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) { FIN_TRACE(4); FIN_DT(4); }
+    // D. exact re-score of the flagged entries (one warp each, W loads in flight)
     const int nn = n_need_s;
     for (int q = warp; q < nn; q += nwarps) {
         const int c = need_list[q];
-        const size_t row = (size_t)(c_id[c] / a.R);
+        const size_t row = (size_t)(c_gid[c] / a.R);
         double acc = 0.0;
-        if (a.w_dtype == 0 && a.h_dtype == 0 && a.d % 8 == 0) {
+        if (a.w_dtype == 0 && h_fast) {
             const uint4* wp = (const uint4*)((const uint16_t*)a.W + row * a.d);
-            const uint4* hp = (const uint4*)((const uint16_t*)a.H + (size_t)r * a.d);
             const int nc = a.d / 8;
-            for (int c0 = lane; c0 < nc; c0 += 32 * 4) {
-                uint4 wv[4], hv[4];
+            constexpr int kPer = 16;                 // uint4 per lane in flight (d = 4096: all)
+            for (int c0 = 0; c0 < nc; c0 += 32 * kPer) {
+                uint4 wv[kPer];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int cc = c0 + 32 * u;
-                    wv[u] = cc < nc ? wp[cc] : make_uint4(0, 0, 0, 0);
-                    hv[u] = cc < nc ? hp[cc] : make_uint4(0, 0, 0, 0);
+                for (int u = 0; u < kPer; ++u) {
+                    const int cc = c0 + lane + 32 * u;
+                    wv[u] = cc < nc ? __ldg(&wp[cc]) : make_uint4(0, 0, 0, 0);
                 }
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    float fw[8], fh[8];
-                    unpack_bf16x8(wv[u], fw);
-                    unpack_bf16x8(hv[u], fh);
+                for (int u = 0; u < kPer; ++u) {
+                    const int cc = c0 + lane + 32 * u;
+                    if (cc < nc) {
+                        float fw[8], fh[8];
+                        unpack_bf16x8(wv[u], fw);
+                        unpack_bf16x8(((const uint4*)h_row)[cc], fh);
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) acc = fma((double)fw[j], (double)fh[j], acc);
+                        for (int j = 0; j < 8; ++j) acc = fma((double)fw[j], (double)fh[j], acc);
+                    }
                 }
             }
         } else {
+#pragma unroll 1
             for (int col = lane; col < a.d; col += 32)
                 acc = fma(load_elem(a.W, a.w_dtype, row * a.d + col), load_elem(a.H, a.h_dtype, (size_t)r * a.d + col), acc);
         }
@@ -600,7 +599,7 @@ lmh_finalize32_kernel(LmhArgs a, int n_cta, int k, float gamma, const float* __r
         if (lane == 0) c_e[c] = acc * (double)a.inv_temp;
     }
     __syncthreads();
-    if (threadIdx.x == 0) FIN_TRACE(5);
+    if (threadIdx.x == 0) { FIN_TRACE(5); FIN_DT(5); }
     // E. one sort by (exact value if re-scored else fp32 value desc, id asc): runs are
     //    more than 2 delta apart, so this is the exact order; write the top k
     if (warp == 0) {
@@ -608,20 +607,23 @@ lmh_finalize32_kernel(LmhArgs a, int n_cta, int k, float gamma, const float* __r
         bool flagged = false;
         for (int q = 0; q < nn; ++q) flagged |= need_list[q] == lane;
         double e = lane < cnt ? (flagged ? c_e[lane] : (double)c_v[lane]) : -INFINITY;
-        int id = lane < cnt ? c_id[lane] : 0x7fffffff;
-        // bitonic sort on (double, id)
-#pragma unroll
-        for (int kk = 2; kk <= 32; kk <<= 1) {
-#pragma unroll
-            for (int j = kk >> 1; j > 0; j >>= 1) {
-                const double oe = __shfl_xor_sync(0xffffffffu, e, j);
-                const int oi = __shfl_xor_sync(0xffffffffu, id, j);
-                const bool keep_better = ((lane & j) == 0) == ((lane & kk) == 0);
-                if (keep_better == before(oe, oi, e, id)) { e = oe; id = oi; }
+        int id = lane < cnt ? c_id[lane] : 0x7fffffff;   // subset position (order = id order)
+        int gid = c_gid[lane];
+        if (nn > 0) {   // only re-scored runs can change the order
+#pragma unroll 1
+            for (int kk = 2; kk <= 32; kk <<= 1) {
+#pragma unroll 1
+                for (int j = kk >> 1; j > 0; j >>= 1) {
+                    const double oe = __shfl_xor_sync(0xffffffffu, e, j);
+                    const int oi = __shfl_xor_sync(0xffffffffu, id, j);
+                    const int og = __shfl_xor_sync(0xffffffffu, gid, j);
+                    const bool keep_better = ((lane & j) == 0) == ((lane & kk) == 0);
+                    if (keep_better == before(oe, oi, e, id)) { e = oe; id = oi; gid = og; }
+                }
             }
         }
         if (lane < k) {
-            const int oid = lane < cnt ? id : -1;
+            const int oid = lane < cnt ? gid : -1;
             const float ovl = lane < cnt ? (float)e : -INFINITY;
             topk_ids[(size_t)r * k + lane] = oid;
             topk_vals[(size_t)r * k + lane] = ovl;
@@ -632,19 +634,30 @@ lmh_finalize32_kernel(LmhArgs a, int n_cta, int k, float gamma, const float* __r
                 if (lane == 0) a.m_lse[r] = lse_s;
             }
         }
-        if (lane == 0) FIN_TRACE(6);
-        if (lane == 0 && a.trace && blockIdx.x < 148) a.trace[148 * 8 + (size_t)blockIdx.x * 8 + 7] = nn;
+        if (lane == 0) {
+            FIN_TRACE(6);
+            FIN_DT(6);
+            if (a.trace && blockIdx.x < 148) a.trace[148 * 8 + (size_t)blockIdx.x * 8 + 7] = ncand;
+        }
     }
 }
 
 void launch_lmh_finalize(const LmhArgs& a, int n_cta, int k, const float* wmax_dev, int32_t* topk_ids,
                          float* topk_vals, float* row_max, float* row_sumexp, int* flags, cudaStream_t st,
                          float gamma) {
-    if (a.KP <= 32) {
-        const size_t smem32 = (size_t)n_cta * 16 + 16 + (size_t)n_cta * a.LS * 8;
-        cudaFuncSetAttribute(lmh_finalize32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem32);
-        launch_pdl(lmh_finalize32_kernel, dim3(a.n_h), dim3(kFinThreads), smem32, st, a, n_cta, k, gamma, wmax_dev,
-                   topk_ids, topk_vals, row_max, row_sumexp, flags);
+    if (a.KP <= 32 && a.LS == kFin32LS && n_cta * (kFin32LS / 4) <= 10 * kFin32Threads) {
+        // one CTA per SM (the dynamic allocation is only a placement hint): two
+        // CTAs sharing an SM measured slower
+        const size_t smem = 120 * 1024;
+        if (n_cta * (kFin32LS / 4) <= 5 * kFin32Threads) {
+            cudaFuncSetAttribute(lmh_finalize32_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            launch_pdl(lmh_finalize32_kernel<5>, dim3(a.n_h), dim3(kFin32Threads), smem, st, a, n_cta, k, gamma,
+                       wmax_dev, topk_ids, topk_vals, row_max, row_sumexp, flags);
+        } else {
+            cudaFuncSetAttribute(lmh_finalize32_kernel<10>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            launch_pdl(lmh_finalize32_kernel<10>, dim3(a.n_h), dim3(kFin32Threads), smem, st, a, n_cta, k, gamma,
+                       wmax_dev, topk_ids, topk_vals, row_max, row_sumexp, flags);
+        }
         return;
     }
     size_t smem = (size_t)n_cta * 2 * sizeof(int) + (size_t)n_cta * a.KP * 8;

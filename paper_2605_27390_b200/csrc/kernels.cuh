@@ -49,7 +49,7 @@ void launch_union(int V, const int32_t* static_ids, int n_static, const int32_t*
 // sorted list (the last tile is not folded, its survivors are appended).
 struct LmhPartials {
     float* val;    // [n_cta][n_h][LS]
-    int32_t* id;   // [n_cta][n_h][LS]
+    int32_t* id;   // [n_cta][n_h][LS] subset positions (sorted subset: position order = id order)
     float* m;      // [n_cta][n_h]
     float* s;      // [n_cta][n_h]
     int* cnt;      // [n_cta][n_h] sorted entries

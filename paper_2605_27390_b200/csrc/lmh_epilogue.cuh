@@ -305,15 +305,22 @@ ES_DEV void epi_tile(const EpiSmem& e, int n_h, int KP, int tn, int base_pos, in
 
 // Write the CTA's state to the global partials (positions -> global ids).
 // Only [0, cnt) is written: extras may already sit at [cnt, cnt + xcnt).
+// Partials carry subset positions, not ids: the subset is sorted ascending, so
+// position order is id order, and only the finalisation's few winners are
+// translated (no dependent global loads in the LM-head tail).
 ES_DEV void epi_store(const EpiSmem& e, const LmhPartials& P, int cta, int n_h_total, int h_row0,
-                      int n_h, int KP, int LS, const int32_t* subset, int warp, int n_warps) {
+                      int n_h, int KP, int LS, int warp, int n_warps) {
     for (int r = warp; r < n_h; r += n_warps) {
         const int cnt = e.st_cnt[r];
         const size_t o = ((size_t)cta * n_h_total + h_row0 + r);
         for (int i = lane_id(); i < cnt; i += 32) {
             P.val[o * LS + i] = e.st_val[r * KP + i];
-            P.id[o * LS + i] = subset[e.st_pos[r * KP + i]];
+            P.id[o * LS + i] = e.st_pos[r * KP + i];
         }
+        // fixed-stride lists (LS > KP): the slots after the sorted entries and the
+        // extras hold -inf, so the finalisation reads the row as one flat array
+        if (LS > KP)
+            for (int i = cnt + e.st_xcnt[r] + lane_id(); i < LS; i += 32) P.val[o * LS + i] = -INFINITY;
         const float ssum = warp_sum(e.st_ls[r * 32 + lane_id()]);
         if (lane_id() == 0) {
             P.cnt[o] = cnt;
@@ -330,7 +337,7 @@ ES_DEV void epi_store(const EpiSmem& e, const LmhPartials& P, int cta, int n_h_t
 // list's entry KP-1 -- any element of the CTA's top-KP does. Rows whose list
 // is not full, or with more survivors than LS - KP slots, take the full fold.
 ES_DEV void epi_tile_last(const EpiSmem& e, const LmhPartials& P, int cta, int n_h_total, int n_h, int KP, int LS,
-                          int tn, int base_pos, int warp, int n_warps, const int32_t* subset) {
+                          int tn, int base_pos, int warp, int n_warps) {
     if (tn <= 0) return;
     const int lane = lane_id();
     for (int r = warp; r < n_h; r += n_warps) {
@@ -372,7 +379,7 @@ ES_DEV void epi_tile_last(const EpiSmem& e, const LmhPartials& P, int cta, int n
             if (cand[j]) {
                 const int idx = base + __popc(msk[j] & ((1u << lane) - 1u));
                 P.val[o * LS + idx] = v[j];
-                P.id[o * LS + idx] = subset[base_pos + lane + 32 * j];
+                P.id[o * LS + idx] = base_pos + lane + 32 * j;
             }
             base += __popc(msk[j]);
         }

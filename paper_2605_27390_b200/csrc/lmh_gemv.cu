@@ -155,7 +155,7 @@ lmh_gemv_kernel(LmhArgs a, int h_row0) {
         epi_tile(e, NH, a.KP, tn, tb, warp, kGemvWarps);
         __syncthreads();
     }
-    epi_store(e, a.part, blockIdx.x, a.n_h, h_row0, NH, a.KP, a.LS, a.subset, warp, kGemvWarps);
+    epi_store(e, a.part, blockIdx.x, a.n_h, h_row0, NH, a.KP, a.LS, warp, kGemvWarps);
 }
 
 template <int DT, int NH>

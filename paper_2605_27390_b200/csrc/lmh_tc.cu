@@ -362,7 +362,7 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
         tile_range(n_tiles - 1, t0, tn);
         named_bar_sync(2, kTcWarps * 32);
         if (n_tiles > 1)
-            epi_tile_last(e, a.part, blockIdx.x, a.n_h, n_h, a.KP, a.LS, tn, t0, warp, kTcWarps, a.subset);
+            epi_tile_last(e, a.part, blockIdx.x, a.n_h, n_h, a.KP, a.LS, tn, t0, warp, kTcWarps);
         else
             epi_tile(e, n_h, a.KP, tn, t0, warp, kTcWarps);
         if (warp == kTcEpiWarp0 && lane == 0 && n_tiles - 1 < 2) TC_TRACE(4 + 2 * (n_tiles - 1));
@@ -370,7 +370,7 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    epi_store(e, a.part, blockIdx.x, a.n_h, 0, n_h, a.KP, a.LS, a.subset, warp, kTcWarps);
+    epi_store(e, a.part, blockIdx.x, a.n_h, 0, n_h, a.KP, a.LS, warp, kTcWarps);
     if (threadIdx.x == 0) TC_TRACE(7);
     if (warp == kTcMmaWarp)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(tp.tmem_cols));

@@ -52,7 +52,11 @@ for pf in (sys.argv[1:] or ["2"]):
         if col.size:
             print(f"   {n:10s} min {col.min():7.1f}  med {np.median(col):7.1f}  max {col.max():7.1f}")
     frel = (fin[:, :7] - t0) / 1e3
-    for j, n in enumerate(["fin_start", "fin_hnorm", "fin_stage", "fin_merge", "fin_runs", "fin_rescore", "fin_end"]):
+    for j, n in enumerate(["fin_start", "fin_hnorm", "fin_B1", "fin_filter", "fin_runs", "fin_rescore", "fin_end"]):
         col = frel[:, j]
         print(f"   {n:10s} min {col.min():7.1f}  med {np.median(col):7.1f}  max {col.max():7.1f}")
-    print("   rescored per row: mean", fin[:, 7].mean(), "max", fin[:, 7].max())
+    print("   ncand per row: mean", fin[:, 7].mean(), "max", fin[:, 7].max())
+    det = ctx.read_trace(296 * 8 + 16 + 32)[296 * 8 + 16:].astype(np.int64)
+    if det[0] > 0:
+        print("   finalize row 0 clock64 deltas (cycles from slot 0):",
+              {i: int(det[i] - det[0]) for i in range(32) if det[i] > 0})
