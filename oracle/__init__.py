@@ -201,3 +201,43 @@ def shard_subset(S, R: int, r: int) -> np.ndarray:
 def shard_rows(W, R: int, r: int):
     """W_local for shard r: global rows v = r (mod R), local row v // R."""
     return np.ascontiguousarray(W[r::R])
+
+
+def build_subset_batched(E, Q, static_ids, seed_ids, seed_offsets, row_ptr, col, *, n_sem: int,
+                         n_dyn: int, n_graph_sem_seeds: int = 10, per_seed: int = 8, ctx_ids=None,
+                         ctx_offsets=None, ctx_min_count: int = 0, n_ctx_max: int = 0):
+    """Batched serving build (SURVEY §8(a) a4, config Bt): for each sequence b the
+    single-query build (§8(c) steps 2-8) with q = Q[b], its own seeds / context
+    tokens and the shared static set; returns (dyn_ids concatenated, offsets [B+1])
+    with dyn_b = sorted(dyn) -- the dynamic part only (static excluded)."""
+    Q = np.ascontiguousarray(Q)
+    seed_ids = np.zeros(0, np.int32) if seed_ids is None else _i32(seed_ids)
+    out, offs = [], [0]
+    for b in range(Q.shape[0]):
+        seeds_b = seed_ids[seed_offsets[b]:seed_offsets[b + 1]]
+        ctx_b = None if ctx_ids is None else _i32(ctx_ids)[ctx_offsets[b]:ctx_offsets[b + 1]]
+        r = build_subset(E, Q[b], static_ids, seeds_b, row_ptr, col, n_sem=n_sem,
+                         n_graph_sem_seeds=n_graph_sem_seeds, per_seed=per_seed, n_dyn=n_dyn,
+                         ctx_ids=ctx_b, ctx_min_count=ctx_min_count, n_ctx_max=n_ctx_max)
+        dyn_b = np.sort(r["dyn"]).astype(np.int32)
+        out.append(dyn_b)
+        offs.append(offs[-1] + dyn_b.size)
+    dyn = np.concatenate(out) if out else np.zeros(0, np.int32)
+    return dyn.astype(np.int32), np.asarray(offs, dtype=np.int64)
+
+
+def subset_logits_topk_ragged(W, H, h_offsets, static_ids, dyn_ids, dyn_offsets, k: int, *,
+                              inv_temp: float = 1.0):
+    """Ragged batched LM head (config Bt): the rows of sequence b against its own
+    V_b = sort(static u dyn_b) (Eq. 1 P:47 restricted per sequence; §8(c) steps
+    9-11 per sequence). Returns dict(ids, vals, m, s, lse, probs) over all rows."""
+    static_ids = _i32(static_ids)
+    dyn_ids = _i32(dyn_ids)
+    parts = []
+    for b in range(len(h_offsets) - 1):
+        h0, h1 = int(h_offsets[b]), int(h_offsets[b + 1])
+        if h1 == h0:
+            continue
+        S_b = np.union1d(static_ids, dyn_ids[int(dyn_offsets[b]):int(dyn_offsets[b + 1])]).astype(np.int32)
+        parts.append(subset_logits_topk(W, H[h0:h1], S_b, k, inv_temp=inv_temp))
+    return {key: np.concatenate([p[key] for p in parts]) for key in ("ids", "vals", "m", "s", "lse", "probs")}

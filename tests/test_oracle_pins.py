@@ -363,3 +363,94 @@ def test_merge_skips_empty_shard_and_pads(oracle_mod):
     out = oracle_mod.merge(st("ids"), st("vals"), st("m"), st("s"), 3)
     assert out["ids"][0].tolist() == [4, 2, -1]
     assert abs(out["lse"][0] - logsumexp([0.5, 1.5])) < 1e-12
+
+
+# ------------------------------------------------ batched serving (config Bt)
+def test_batched_build_worked_example(oracle_mod):
+    """Two sequences on the worked formation example (golden "formation"): sequence 0
+    keeps its seeds [5, 2]; sequence 1 has none, so by the same rules (C4, C6, C7)
+    G = S_sem[:2] = [7, 5], S_graph = [1, 10, 6, 7], C = [7, 5, 9, 1, 10, 6, 7] and,
+    skipping static 1, dyn = [7, 5, 9, 10] at N_dyn = 4 (derived by hand)."""
+    g = GOLD["formation"]
+    E, q = _onehot_sem(g["V"], g["sem_order"])
+    row_ptr, col = csr_from_rows(g["V"], g["rows"])
+    Q = np.stack([q, q])
+    dyn, offs = oracle_mod.build_subset_batched(
+        E, Q, g["static"], g["seeds"], [0, len(g["seeds"]), len(g["seeds"])], row_ptr, col,
+        n_sem=len(g["sem_order"]), n_graph_sem_seeds=g["n_graph_sem_seeds"], per_seed=g["per_seed"], n_dyn=4)
+    assert offs.tolist() == [0, 4, 8]
+    assert dyn[0:4].tolist() == sorted(g["dyn_ndyn4"])
+    assert dyn[4:8].tolist() == [5, 7, 9, 10]
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_batched_build_bruteforce(oracle_mod, seed):
+    """Every sequence of a batch equals the pure-Python brute force of its own build,
+    restricted to the dynamic part (static excluded, sorted)."""
+    rng = np.random.default_rng(300 + seed)
+    V, d, B = 64, 6, 4
+    E = synth.int_matrix(seed + 7, V, d, "fp32")
+    Q = synth.int_matrix(seed + 70, B, d, "fp32")
+    static = np.sort(rng.choice(V, 10, replace=False)).astype(np.int32)
+    n_seed = rng.integers(0, 5, B)
+    offs = np.concatenate([[0], np.cumsum(n_seed)]).astype(np.int64)
+    seeds = rng.choice(V, int(offs[-1]), replace=True).astype(np.int32)
+    rows = {str(u): [int(x) for x in rng.choice(V, int(rng.integers(0, 5)), replace=False)] for u in range(V)}
+    row_ptr, col = csr_from_rows(V, rows)
+    n_sem, ngs, per, n_dyn = 8, 3, 2, 9
+    dyn, doff = oracle_mod.build_subset_batched(E, Q, static, seeds, offs, row_ptr, col, n_sem=n_sem,
+                                                n_graph_sem_seeds=ngs, per_seed=per, n_dyn=n_dyn)
+    for b in range(B):
+        _, _, bdyn = brute.build_subset(E.tolist(), Q[b].tolist(), static.tolist(),
+                                        seeds[offs[b]:offs[b + 1]].tolist(),
+                                        {int(k): v for k, v in rows.items()}, n_sem, ngs, per, n_dyn)
+        assert dyn[doff[b]:doff[b + 1]].tolist() == sorted(bdyn)
+        assert not set(bdyn) & set(static.tolist())
+
+
+def test_ragged_equals_brute_force_per_sequence(oracle_mod):
+    """Each row's triple over its own V_b = static u dyn_b equals the brute-force
+    restricted softmax / ordering on that support."""
+    V, d, k = 48, 5, 4
+    W = synth.int_matrix(40, V, d, "fp32")
+    H = synth.int_matrix(41, 7, d, "fp32")
+    static = np.array([1, 4, 9, 16, 25, 36], np.int32)
+    dyn_lists = [[0, 2, 3], [], [40, 41, 47, 5]]
+    h_off = [0, 3, 4, 7]
+    dyn = np.array(sum(dyn_lists, []), np.int32)
+    doff = np.concatenate([[0], np.cumsum([len(x) for x in dyn_lists])])
+    out = oracle_mod.subset_logits_topk_ragged(W, H, h_off, static, dyn, doff, k)
+    for b, dl in enumerate(dyn_lists):
+        supp = sorted(set(static.tolist()) | set(dl))
+        for r in range(h_off[b], h_off[b + 1]):
+            logits = [float(brute.dot(H[r], W[v])) for v in supp]
+            order = brute.order_desc(logits, supp)[:k]
+            assert out["ids"][r].tolist() == order
+            p = brute.restricted_softmax(logits, supp)
+            np.testing.assert_allclose(out["probs"][r], [p[v] for v in order], rtol=1e-12)
+            assert abs(out["m"][r] - max(logits)) == 0.0
+
+
+def test_ragged_equals_merge_of_static_and_dynamic_parts(oracle_mod):
+    """static and dyn_b are disjoint, so the ragged result is the two-part merge
+    (the shard merge, pinned above) of the static triple and the dyn_b triple."""
+    V, d, k = 300, 12, 6
+    W = synth.matrix(50, V, d, 0.5, "fp32")
+    H = synth.matrix(51, 9, d, 1.0, "fp32")
+    rng = np.random.default_rng(52)
+    perm = rng.permutation(V)
+    static = np.sort(perm[:80]).astype(np.int32)
+    dyn_lists = [np.sort(perm[80:110]), np.sort(perm[110:111]), np.sort(perm[111:200])]
+    h_off = [0, 4, 5, 9]
+    dyn = np.concatenate(dyn_lists).astype(np.int32)
+    doff = np.concatenate([[0], np.cumsum([x.size for x in dyn_lists])])
+    out = oracle_mod.subset_logits_topk_ragged(W, H, h_off, static, dyn, doff, k)
+    st = oracle_mod.subset_logits_topk(W, H, static, k)
+    for b in range(3):
+        rows = slice(h_off[b], h_off[b + 1])
+        dy = oracle_mod.subset_logits_topk(W, H[rows], dyn_lists[b].astype(np.int32), k)
+        mg = oracle_mod.merge(np.stack([st["ids"][rows], dy["ids"]]), np.stack([st["vals"][rows], dy["vals"]]),
+                              np.stack([st["m"][rows], dy["m"]]), np.stack([st["s"][rows], dy["s"]]), k)
+        np.testing.assert_array_equal(out["ids"][rows], mg["ids"])
+        np.testing.assert_allclose(out["lse"][rows], mg["lse"], rtol=1e-12)
+        np.testing.assert_allclose(out["probs"][rows], mg["probs"], atol=1e-12)
