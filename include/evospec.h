@@ -156,6 +156,29 @@ evospec_status evospec_build_subset(evospec_ctx *ctx,
     int32_t *out_local_ids, int32_t *out_local_n,
     void *stream);
 
+/* Batched serving (config Bt, SURVEY §8(a) a4 "a shared static set + 64 ragged
+ * dynamic lists"): one query per sequence, the static set shared. For each
+ * sequence b < B the builder above runs with q_b = q_dev + b*d, seeds
+ * seed_dev[seed_offsets[b] : seed_offsets[b+1]] and context tokens
+ * ctx_dev[ctx_offsets[b] : ctx_offsets[b+1]] (ctx_offsets may be NULL), and
+ * only the sorted DYNAMIC list dyn_b (static excluded; same formation and cap,
+ * P:458) is output -- the direct input of the ragged LM head below.
+ * seed_offsets / ctx_offsets: HOST arrays [B+1] (the caller's batch layout).
+ * Outputs (device): out_dyn_ids [B * n_dyn] compacted, sequence b at
+ *   [out_dyn_offsets[b], out_dyn_offsets[b+1]); out_dyn_offsets [B+1] device,
+ *   out_dyn_offsets[0] = 0. Nothing is synchronised.
+ * Unsharded contexts and the full index (n_e_rows == V) only; EVOSPEC_EINPUT
+ * otherwise. Work: one E scan per sequence (B scans). */
+evospec_status evospec_build_subset_batched(evospec_ctx *ctx,
+    const void *E_dev, int64_t n_e_rows, const void *q_dev, int32_t B,
+    const int32_t *static_dev, int32_t n_static,
+    const int32_t *seed_dev, const int32_t *seed_offsets,
+    const int32_t *csr_row_ptr_dev, const int32_t *csr_col_dev,
+    const int32_t *ctx_dev, const int32_t *ctx_offsets,
+    const evospec_build_params *params,
+    int32_t *out_dyn_ids, int32_t *out_dyn_offsets,
+    void *stream);
+
 /* Debug/parity accessor: copies the S_sem SET of the last build on this
  * context (N_sem device ids, in no particular order) into out_dev. Async. */
 evospec_status evospec_last_semantic(evospec_ctx *ctx, int32_t *out_dev, int32_t n, void *stream);
@@ -182,6 +205,26 @@ evospec_status evospec_subset_logits_topk(evospec_ctx *ctx,
     int32_t k, float inv_temp,
     int32_t *topk_ids, float *topk_vals, float *row_max, float *row_sumexp,
     float *logits_out, void *stream);
+
+/* Ragged batched LM head (config Bt): sequence b owns H rows
+ * [h_offsets[b], h_offsets[b+1]) and the vocabulary V_b = static u dyn_b,
+ * dyn_b = dyn_dev[dyn_offsets[b] : dyn_offsets[b+1]] (sorted ascending,
+ * disjoint from static -- what evospec_build_subset_batched outputs). Each row
+ * gets the triple of Eq. 1 restricted to its own V_b:
+ *   topk over V_b (z desc, id asc), m = max z, s = sum exp(z - m).
+ * h_offsets: HOST [B+1], h_offsets[0] = 0, total rows <= max_rows.
+ * dyn_offsets: DEVICE [B+1]; max_dyn bounds every dyn_b length (<= max_subset).
+ * static_dev may be NULL when n_static = 0. The static block is shared by all
+ * rows (its rows are streamed once per group of 128 H rows); the two disjoint
+ * parts are merged per row like two vocabulary shards. */
+evospec_status evospec_subset_logits_topk_ragged(evospec_ctx *ctx,
+    const void *W_local_dev, int64_t n_w_rows, const void *H_dev,
+    const int32_t *h_offsets, int32_t B,
+    const int32_t *static_dev, int32_t n_static,
+    const int32_t *dyn_dev, const int32_t *dyn_offsets, int32_t max_dyn,
+    int32_t k, float inv_temp,
+    int32_t *topk_ids, float *topk_vals, float *row_max, float *row_sumexp,
+    void *stream);
 
 /* ---- a8: vocab-shard merge ------------------------------------------------ */
 

@@ -27,6 +27,7 @@ EXPORTED = [
     "evospec_comm_unique_id", "evospec_comm_init", "evospec_build_subset",
     "evospec_last_semantic", "evospec_subset_logits_topk", "evospec_merge_shards",
     "evospec_draft_step", "evospec_set_timing", "evospec_read_stats", "evospec_read_trace",
+    "evospec_build_subset_batched", "evospec_subset_logits_topk_ragged",
 ]
 
 STAGES = ["scan", "select", "union", "lmh", "finalize", "merge", "copy"]
@@ -101,6 +102,10 @@ def lib() -> C.CDLL:
             "evospec_set_timing": ([vp, C.c_int], i32),
             "evospec_read_stats": ([vp, C.POINTER(Stats)], i32),
             "evospec_read_trace": ([vp, vp, i32], i32),
+            "evospec_build_subset_batched": ([vp, vp, i64, vp, i32, vp, i32, vp, vp, vp, vp, vp, vp,
+                                              C.POINTER(BuildParams), vp, vp, vp], i32),
+            "evospec_subset_logits_topk_ragged": ([vp, vp, i64, vp, vp, i32, vp, i32, vp, vp, i32, i32,
+                                                   C.c_float, vp, vp, vp, vp, vp], i32),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, name)
@@ -226,6 +231,30 @@ class Context:
             _ptr(ids), _ptr(n), _ptr(lids), _ptr(ln), _stream(stream)))
         return ids, n, lids, ln
 
+    def build_subset_batched(self, E, Q, static_ids, seed_ids, seed_offsets, csr_row_ptr, csr_col, *,
+                             n_sem: int, n_dyn: int, n_graph_sem_seeds: int = 10, per_seed: int = 8,
+                             ctx_ids=None, ctx_offsets=None, ctx_min_count: int = 0, n_ctx_max: int = 0,
+                             out=None, stream=None):
+        """Q [B, d]; seed_offsets / ctx_offsets: host int sequences [B+1].
+        Returns (dyn_ids [B*n_dyn], dyn_offsets [B+1]) device tensors (per-sequence
+        sorted dynamic lists, compacted)."""
+        import torch
+        B = Q.shape[0]
+        dev = E.device
+        if out is None:
+            out = (torch.empty(max(B * n_dyn, 1), dtype=torch.int32, device=dev),
+                   torch.empty(B + 1, dtype=torch.int32, device=dev))
+        dyn, offs = out
+        so = (C.c_int32 * (B + 1))(*[int(x) for x in seed_offsets])
+        co = None if ctx_offsets is None else (C.c_int32 * (B + 1))(*[int(x) for x in ctx_offsets])
+        p = BuildParams(n_sem, n_graph_sem_seeds, per_seed, ctx_min_count, n_ctx_max, n_dyn)
+        _check(lib().evospec_build_subset_batched(
+            self._h, _ptr(E), E.shape[0], _ptr(Q), B, _ptr(static_ids), static_ids.numel(),
+            _ptr(seed_ids), C.cast(so, C.c_void_p), _ptr(csr_row_ptr), _ptr(csr_col), _ptr(ctx_ids),
+            None if co is None else C.cast(co, C.c_void_p), C.byref(p), _ptr(dyn), _ptr(offs),
+            _stream(stream)))
+        return dyn, offs
+
     def last_semantic(self, n: int, stream=None):
         import torch
         out = torch.empty(max(n, 1), dtype=torch.int32, device=f"cuda:{self.device}")
@@ -249,6 +278,28 @@ class Context:
             self._h, _ptr(W_local), W_local.shape[0], _ptr(H), n_h, _ptr(subset), _ptr(n_subset_dev),
             n_subset_max, k, float(inv_temp), _ptr(ids), _ptr(vals), _ptr(m), _ptr(s),
             _ptr(logits_out), _stream(stream)))
+        return ids, vals, m, s
+
+    def subset_logits_topk_ragged(self, W_local, H, h_offsets, static_ids, dyn_ids, dyn_offsets, max_dyn: int,
+                                  k: int, inv_temp: float = 1.0, out=None, stream=None):
+        """h_offsets: host ints [B+1]; dyn_offsets: device int32 [B+1]. Returns the
+        per-row triple (topk_ids, topk_vals, row_max, row_sumexp) over static u dyn_b."""
+        import torch
+        B = len(h_offsets) - 1
+        n_rows = int(h_offsets[-1])
+        dev = H.device
+        if out is None:
+            out = (torch.empty((n_rows, k), dtype=torch.int32, device=dev),
+                   torch.empty((n_rows, k), dtype=torch.float32, device=dev),
+                   torch.empty(n_rows, dtype=torch.float32, device=dev),
+                   torch.empty(n_rows, dtype=torch.float32, device=dev))
+        ids, vals, m, s = out
+        ho = (C.c_int32 * (B + 1))(*[int(x) for x in h_offsets])
+        n_static = 0 if static_ids is None else static_ids.numel()
+        _check(lib().evospec_subset_logits_topk_ragged(
+            self._h, _ptr(W_local), W_local.shape[0], _ptr(H), C.cast(ho, C.c_void_p), B, _ptr(static_ids),
+            n_static, _ptr(dyn_ids), _ptr(dyn_offsets), int(max_dyn), k, float(inv_temp), _ptr(ids), _ptr(vals),
+            _ptr(m), _ptr(s), _stream(stream)))
         return ids, vals, m, s
 
     # ---- a8

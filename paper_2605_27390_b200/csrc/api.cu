@@ -141,6 +141,12 @@ struct evospec_ctx {
     float* st_ovals = nullptr;
     float* st_lse = nullptr;
     float* st_probs = nullptr;
+    // ragged (batched serving) LM head: stacked [2][max_rows][max_k] static / dynamic triples
+    int32_t* rg_ids = nullptr;
+    float* rg_vals = nullptr;
+    float* rg_m = nullptr;
+    float* rg_s = nullptr;
+    int32_t* rg_seg = nullptr;   // device {0, n_static}
     int last_n_sem = 0;
     ncclComm_t comm = nullptr;
     // measurement hooks
@@ -209,7 +215,7 @@ evospec_status evospec_destroy(evospec_ctx* ctx) {
                     ctx->flags, ctx->wmax, ctx->g_ids, ctx->g_vals, ctx->g_m, ctx->g_s, ctx->st_q, ctx->st_H,
                     ctx->st_seeds, ctx->st_ctx, ctx->st_S, ctx->st_nS, ctx->st_local, ctx->st_nlocal,
                     ctx->st_tids, ctx->st_tvals, ctx->st_m, ctx->st_s, ctx->st_oids, ctx->st_ovals,
-                    ctx->st_lse, ctx->st_probs};
+                    ctx->st_lse, ctx->st_probs, ctx->rg_ids, ctx->rg_vals, ctx->rg_m, ctx->rg_s, ctx->rg_seg};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (ctx->comm && nccl().loaded) nccl().CommDestroy(ctx->comm);
@@ -276,6 +282,8 @@ evospec_status evospec_create(evospec_ctx** out, const evospec_config* cfg, int 
     A(dalloc(&x->st_tids, hk)); A(dalloc(&x->st_tvals, hk)); A(dalloc(&x->st_m, c.max_rows));
     A(dalloc(&x->st_s, c.max_rows)); A(dalloc(&x->st_oids, hk)); A(dalloc(&x->st_ovals, hk));
     A(dalloc(&x->st_lse, c.max_rows)); A(dalloc(&x->st_probs, hk));
+    A(dalloc(&x->rg_ids, 2 * hk)); A(dalloc(&x->rg_vals, 2 * hk));
+    A(dalloc(&x->rg_m, 2 * (size_t)c.max_rows)); A(dalloc(&x->rg_s, 2 * (size_t)c.max_rows)); A(dalloc(&x->rg_seg, 2));
     if (e == cudaSuccess) e = cudaMemset(x->flags, 0, sizeof(int));
     if (e == cudaSuccess) {
         const float inf = INFINITY;  // until evospec_prepare_weights: certification never passes
@@ -330,12 +338,14 @@ evospec_status evospec_comm_init(evospec_ctx* ctx, const void* uid) {
     return EVOSPEC_OK;
 }
 
-evospec_status evospec_build_subset(evospec_ctx* ctx, const void* E, int64_t n_e_rows, const void* q,
-                                    const int32_t* static_ids, int32_t n_static, const int32_t* seeds,
-                                    int32_t n_seed, const int32_t* row_ptr, const int32_t* col,
-                                    const int32_t* ctx_ids, int32_t n_ctx, const evospec_build_params* p,
-                                    int32_t* out_ids, int32_t* out_n, int32_t* out_local_ids,
-                                    int32_t* out_local_n, void* stream) {
+// dyn_base != null: batched mode -- the sorted dynamic list only, written at
+// out_ids + *dyn_base, with *out_n = *dyn_base + its length
+static evospec_status build_impl(evospec_ctx* ctx, const void* E, int64_t n_e_rows, const void* q,
+                                 const int32_t* static_ids, int32_t n_static, const int32_t* seeds, int32_t n_seed,
+                                 const int32_t* row_ptr, const int32_t* col, const int32_t* ctx_ids, int32_t n_ctx,
+                                 const evospec_build_params* p, int32_t* out_ids, int32_t* out_n,
+                                 int32_t* out_local_ids, int32_t* out_local_n, void* stream,
+                                 const int32_t* dyn_base) {
     if (!ctx || !E || !q || !p || !out_ids || !out_n) return fail(EVOSPEC_EINPUT, "build_subset: null argument");
     const evospec_config& c = ctx->cfg;
     const int R = c.n_shards, r = c.shard_rank;
@@ -407,8 +417,44 @@ evospec_status evospec_build_subset(evospec_ctx* ctx, const void* E, int64_t n_e
     launch_union(c.V, static_ids, n_static, seeds, n_seed, ctx->cand_s, ctx->cand_id, ctx->cand_count, ctx->cand_cap,
                  N, row_ptr, col, use_ctx ? ctx->ctx_sel : nullptr, ctx->ctx_n, p->n_graph_sem_seeds, p->per_seed,
                  p->n_dyn, R, r, out_ids, out_n, out_local_ids, out_local_n, ctx->sem_ids, ctx->sem_n,
-                 c.debug_checks, ctx->flags, st, union_trace(ctx, st));
+                 c.debug_checks, ctx->flags, st, union_trace(ctx, st), dyn_base);
     LAUNCH_CHECK("union");
+    return EVOSPEC_OK;
+}
+
+evospec_status evospec_build_subset(evospec_ctx* ctx, const void* E, int64_t n_e_rows, const void* q,
+                                    const int32_t* static_ids, int32_t n_static, const int32_t* seeds,
+                                    int32_t n_seed, const int32_t* row_ptr, const int32_t* col,
+                                    const int32_t* ctx_ids, int32_t n_ctx, const evospec_build_params* p,
+                                    int32_t* out_ids, int32_t* out_n, int32_t* out_local_ids,
+                                    int32_t* out_local_n, void* stream) {
+    return build_impl(ctx, E, n_e_rows, q, static_ids, n_static, seeds, n_seed, row_ptr, col, ctx_ids, n_ctx, p,
+                      out_ids, out_n, out_local_ids, out_local_n, stream, nullptr);
+}
+
+evospec_status evospec_build_subset_batched(evospec_ctx* ctx, const void* E, int64_t n_e_rows, const void* q,
+                                            int32_t B, const int32_t* static_ids, int32_t n_static,
+                                            const int32_t* seeds, const int32_t* seed_offsets,
+                                            const int32_t* row_ptr, const int32_t* col, const int32_t* ctx_ids,
+                                            const int32_t* ctx_offsets, const evospec_build_params* p,
+                                            int32_t* out_dyn_ids, int32_t* out_dyn_offsets, void* stream) {
+    if (!ctx || !q || !p || !out_dyn_ids || !out_dyn_offsets || B < 0 || (B > 0 && !seed_offsets))
+        return fail(EVOSPEC_EINPUT, "build_subset_batched: null argument or B < 0");
+    if (ctx->cfg.n_shards != 1 || n_e_rows != ctx->cfg.V)
+        return fail(EVOSPEC_EINPUT, "build_subset_batched: needs an unsharded context and the full index");
+    cudaStream_t st = (cudaStream_t)stream;
+    CUDA_TRY(cudaMemsetAsync(out_dyn_offsets, 0, sizeof(int32_t), st));
+    const size_t q_bytes = (size_t)ctx->cfg.d * (ctx->cfg.h_dtype == EVOSPEC_BF16 ? 2 : 4);
+    for (int b = 0; b < B; ++b) {
+        const int s0 = seed_offsets[b], s1 = seed_offsets[b + 1];
+        const int c0 = ctx_offsets ? ctx_offsets[b] : 0, c1 = ctx_offsets ? ctx_offsets[b + 1] : 0;
+        if (s1 < s0 || c1 < c0) return fail(EVOSPEC_EINPUT, "build_subset_batched: offsets not ascending at %d", b);
+        evospec_status rc = build_impl(ctx, E, n_e_rows, (const char*)q + q_bytes * b, static_ids, n_static,
+                                       seeds ? seeds + s0 : nullptr, s1 - s0, row_ptr, col,
+                                       ctx_ids ? ctx_ids + c0 : nullptr, c1 - c0, p, out_dyn_ids,
+                                       out_dyn_offsets + b + 1, nullptr, nullptr, stream, out_dyn_offsets + b);
+        if (rc != EVOSPEC_OK) return rc;
+    }
     return EVOSPEC_OK;
 }
 
@@ -448,8 +494,8 @@ static evospec_status lmh_impl(evospec_ctx* ctx, const void* W, int64_t n_w_rows
                                const int32_t* subset, const int32_t* n_subset_dev, int32_t n_subset_max, int32_t k,
                                float inv_temp, int32_t* topk_ids, float* topk_vals, float* row_max,
                                float* row_sumexp, float* logits_out, void* stream, int32_t* m_ids, float* m_vals,
-                               float* m_lse, float* m_probs) {
-    if (!ctx || !W || !H || !subset || !n_subset_dev || !topk_ids || !topk_vals || !row_max || !row_sumexp)
+                               float* m_lse, float* m_probs, const int32_t* seg = nullptr) {
+    if (!ctx || !W || !H || !subset || (!n_subset_dev && !seg) || !topk_ids || !topk_vals || !row_max || !row_sumexp)
         return fail(EVOSPEC_EINPUT, "subset_logits_topk: null argument");
     const evospec_config& c = ctx->cfg;
     if (n_h < 1 || n_h > c.max_rows) return fail(EVOSPEC_EINPUT, "subset_logits_topk: n_h=%d not in [1,%d]", n_h, c.max_rows);
@@ -464,13 +510,13 @@ static evospec_status lmh_impl(evospec_ctx* ctx, const void* W, int64_t n_w_rows
     cudaStream_t st = (cudaStream_t)stream;
     if (c.debug_checks) {
         ctx->launches += 1;
-        launch_check_sorted(subset, n_subset_dev, n_subset_max, c.V, ctx->flags, st);
+        if (!seg) launch_check_sorted(subset, n_subset_dev, n_subset_max, c.V, ctx->flags, st);
         LAUNCH_CHECK("check_sorted");
     }
     LmhArgs a{};
     a.W = W; a.n_w_rows = n_w_rows; a.d = c.d; a.w_dtype = c.w_dtype;
     a.H = H; a.n_h = n_h; a.h_dtype = c.h_dtype;
-    a.subset = subset; a.n_subset_dev = n_subset_dev; a.n_subset_max = n_subset_max;
+    a.subset = subset; a.n_subset_dev = n_subset_dev; a.n_subset_max = n_subset_max; a.seg = seg;
     a.R = c.n_shards; a.KP = k + kTopkPad; a.LS = a.KP <= 32 ? 64 : a.KP; a.inv_temp = inv_temp;
     a.logits_out = logits_out;
     a.part = ctx->part;
@@ -516,6 +562,64 @@ evospec_status evospec_subset_logits_topk(evospec_ctx* ctx, const void* W, int64
                                           void* stream) {
     return lmh_impl(ctx, W, n_w_rows, H, n_h, subset, n_subset_dev, n_subset_max, k, inv_temp, topk_ids, topk_vals,
                     row_max, row_sumexp, logits_out, stream, nullptr, nullptr, nullptr, nullptr);
+}
+
+__global__ void set2_kernel(int32_t* p, int32_t a, int32_t b) { p[0] = a; p[1] = b; }
+
+evospec_status evospec_subset_logits_topk_ragged(evospec_ctx* ctx, const void* W, int64_t n_w_rows, const void* H,
+                                                 const int32_t* h_offsets, int32_t B, const int32_t* static_ids,
+                                                 int32_t n_static, const int32_t* dyn_ids,
+                                                 const int32_t* dyn_offsets, int32_t max_dyn, int32_t k,
+                                                 float inv_temp, int32_t* topk_ids, float* topk_vals,
+                                                 float* row_max, float* row_sumexp, void* stream) {
+    if (!ctx || !W || !H || !h_offsets || B < 1 || !topk_ids || !topk_vals || !row_max || !row_sumexp ||
+        (n_static > 0 && !static_ids) || !dyn_ids || !dyn_offsets)
+        return fail(EVOSPEC_EINPUT, "subset_logits_topk_ragged: null argument or B < 1");
+    const evospec_config& c = ctx->cfg;
+    if (h_offsets[0] != 0) return fail(EVOSPEC_EINPUT, "subset_logits_topk_ragged: h_offsets[0] must be 0");
+    for (int b = 0; b < B; ++b)
+        if (h_offsets[b + 1] < h_offsets[b])
+            return fail(EVOSPEC_EINPUT, "subset_logits_topk_ragged: h_offsets not ascending at %d", b);
+    const int n_rows = h_offsets[B];
+    if (n_rows < 1 || n_rows > c.max_rows)
+        return fail(EVOSPEC_EINPUT, "subset_logits_topk_ragged: %d rows not in [1, max_rows=%d]", n_rows, c.max_rows);
+    if (n_static < 0 || n_static > c.max_subset || max_dyn < 0 || max_dyn > c.max_subset)
+        return fail(EVOSPEC_EINPUT, "subset_logits_topk_ragged: n_static / max_dyn exceed max_subset %d", c.max_subset);
+    if (k < 1 || k > c.max_k) return fail(EVOSPEC_EINPUT, "subset_logits_topk_ragged: k=%d not in [1,%d]", k, c.max_k);
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t row_bytes = (size_t)c.d * (c.h_dtype == EVOSPEC_BF16 ? 2 : 4);
+    const size_t hk = (size_t)n_rows * k;
+    int32_t* ids1 = ctx->rg_ids + hk;
+    float* vals1 = ctx->rg_vals + hk;
+    // static block: every row against the shared static set (row groups the
+    // tensor-core kernel holds in TMEM)
+    set2_kernel<<<1, 1, 0, st>>>(ctx->rg_seg, 0, n_static);
+    ctx->launches += 1;
+    LAUNCH_CHECK("set2");
+    for (int r0 = 0; r0 < n_rows; r0 += kTcMaxRows) {
+        const int g = std::min(kTcMaxRows, n_rows - r0);
+        evospec_status rc = lmh_impl(ctx, W, n_w_rows, (const char*)H + row_bytes * r0, g, static_ids ? static_ids : dyn_ids,
+                                     nullptr, n_static, k, inv_temp, ctx->rg_ids + (size_t)r0 * k,
+                                     ctx->rg_vals + (size_t)r0 * k, ctx->rg_m + r0, ctx->rg_s + r0, nullptr, stream,
+                                     nullptr, nullptr, nullptr, nullptr, ctx->rg_seg);
+        if (rc != EVOSPEC_OK) return rc;
+    }
+    // dynamic blocks: sequence b's rows against its own segment of dyn_ids
+    for (int b = 0; b < B; ++b) {
+        const int r0 = h_offsets[b], g = h_offsets[b + 1] - r0;
+        if (g == 0) continue;
+        evospec_status rc = lmh_impl(ctx, W, n_w_rows, (const char*)H + row_bytes * r0, g, dyn_ids, nullptr, max_dyn,
+                                     k, inv_temp, ids1 + (size_t)r0 * k, vals1 + (size_t)r0 * k,
+                                     ctx->rg_m + n_rows + r0, ctx->rg_s + n_rows + r0, nullptr, stream, nullptr,
+                                     nullptr, nullptr, nullptr, dyn_offsets + b);
+        if (rc != EVOSPEC_OK) return rc;
+    }
+    // static u dynamic are disjoint: the two triples merge like two vocabulary shards
+    launch_merge(2, n_rows, k, ctx->rg_ids, ctx->rg_vals, ctx->rg_m, ctx->rg_s, topk_ids, topk_vals, nullptr, nullptr,
+                 st, row_max, row_sumexp);
+    ctx->launches += 1;
+    LAUNCH_CHECK("merge");
+    return EVOSPEC_OK;
 }
 
 evospec_status evospec_merge_shards(evospec_ctx* ctx, int32_t n_h, int32_t k, const int32_t* ids, const float* vals,

@@ -670,7 +670,8 @@ void launch_lmh_finalize(const LmhArgs& a, int n_cta, int k, const float* wmax_d
 __global__ void __launch_bounds__(256)
 merge_kernel(int R, int n_h, int k, const int32_t* __restrict__ ids, const float* __restrict__ vals,
              const float* __restrict__ m, const float* __restrict__ s, int32_t* __restrict__ out_ids,
-             float* __restrict__ out_vals, float* __restrict__ out_lse, float* __restrict__ out_probs) {
+             float* __restrict__ out_vals, float* __restrict__ out_lse, float* __restrict__ out_probs,
+             float* __restrict__ out_m, float* __restrict__ out_s) {
     pdl_trigger();
     pdl_wait();
     const int r = blockIdx.x * (blockDim.x / 32) + warp_id();
@@ -688,6 +689,7 @@ merge_kernel(int R, int n_h, int k, const int32_t* __restrict__ ids, const float
     }
     const float L = sig > 0.0f ? M + logf(sig) : -INFINITY;
     if (lane == 0 && out_lse) out_lse[r] = L;
+    if (lane == 0 && out_m) { out_m[r] = sig > 0.0f ? M : -INFINITY; out_s[r] = sig; }
     const int nc = R * k;
     extern __shared__ unsigned char m_sm[];
     float* sv = (float*)m_sm + (size_t)warp_id() * nc * 2;
@@ -724,12 +726,12 @@ merge_kernel(int R, int n_h, int k, const int32_t* __restrict__ ids, const float
 
 void launch_merge(int R, int n_h, int k, const int32_t* ids, const float* vals, const float* m,
                   const float* s, int32_t* out_ids, float* out_vals, float* out_lse, float* out_probs,
-                  cudaStream_t st) {
+                  cudaStream_t st, float* out_m, float* out_s) {
     const int grid = (n_h + 7) / 8;
     const size_t smem = (size_t)8 * R * k * 8;
     cudaFuncSetAttribute(merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     launch_pdl(merge_kernel, dim3(grid), dim3(256), smem, st, R, n_h, k, ids, vals, m, s, out_ids, out_vals, out_lse,
-               out_probs);
+               out_probs, out_m, out_s);
 }
 
 // ------------------------------------------------------------ helpers

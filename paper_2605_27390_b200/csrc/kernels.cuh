@@ -40,7 +40,7 @@ void launch_union(int V, const int32_t* static_ids, int n_static, const int32_t*
                   int n_graph_sem_seeds, int per_seed, int n_dyn, int R, int r,
                   int32_t* out_ids, int32_t* out_n, int32_t* out_local, int32_t* out_local_n,
                   int32_t* sem_out, int* sem_out_n, int debug, int* flags, cudaStream_t st,
-                  long long* trace = nullptr);
+                  long long* trace = nullptr, const int32_t* dyn_base = nullptr);
 
 // ---- LM head (lmh_gemv.cu, lmh_tc.cu)
 // Per-CTA partial state of the LM head, per H row: entries [0, cnt) are the
@@ -59,6 +59,7 @@ struct LmhArgs {
     const void* W; int64_t n_w_rows; int d; int w_dtype;
     const void* H; int n_h; int h_dtype;
     const int32_t* subset; const int* n_subset_dev; int n_subset_max;
+    const int32_t* seg;   // optional device [2]: positions [seg[0], seg[1]) of subset (ragged segments)
     int R; int KP; int LS; float inv_temp;   // LS: list stride (KP <= 32: 64, else KP)
     float* logits_out;  // optional [n_h][n_subset_max]
     long long* trace;   // optional per-CTA globaltimer stamps [n_cta][8] (profiling)
@@ -66,6 +67,24 @@ struct LmhArgs {
     int32_t* m_ids; float* m_vals; float* m_lse; float* m_probs;
     LmhPartials part;
 };
+
+// This CTA's contiguous share [p0, p1) of the subset positions: all of
+// [0, min(*n_subset_dev, n_subset_max)), or the segment [seg[0], seg[1]).
+// Positions stay absolute, so partial lists and the finalisation index
+// a.subset directly.
+__device__ __forceinline__ void lmh_cta_range(const LmhArgs& a, int& p0, int& p1) {
+    int s0 = 0, s1;
+    if (a.seg) {
+        s0 = a.seg[0];
+        s1 = s0 + min(a.seg[1] - s0, a.n_subset_max);
+    } else {
+        s1 = min(*a.n_subset_dev, a.n_subset_max);
+    }
+    const int n = max(0, s1 - s0);
+    p0 = s0 + (int)((long long)n * blockIdx.x / gridDim.x);
+    p1 = s0 + (int)((long long)n * (blockIdx.x + 1) / gridDim.x);
+}
+
 // returns the number of CTAs whose partials were written
 int launch_lmh_gemv(const LmhArgs& a, int h_row0, int n_h_grp, cudaStream_t st);
 int lmh_gemv_grid();
@@ -81,7 +100,7 @@ void launch_lmh_finalize(const LmhArgs& a, int n_cta, int k, const float* wmax_d
                          int* flags, cudaStream_t st, float gamma);
 void launch_merge(int R, int n_h, int k, const int32_t* ids, const float* vals, const float* m,
                   const float* s, int32_t* out_ids, float* out_vals, float* out_lse, float* out_probs,
-                  cudaStream_t st);
+                  cudaStream_t st, float* out_m = nullptr, float* out_s = nullptr);
 void launch_rownorm_max(const void* W, int w_dtype, int64_t n_rows, int d, float* out, cudaStream_t st);
 void launch_check_sorted(const int32_t* ids, const int* n_dev, int n_host, int V, int* flags,
                          cudaStream_t st);

@@ -82,9 +82,8 @@ lmh_gemv_kernel(LmhArgs a, int h_row0) {
     epi_init(e, NH);
     __syncthreads();
 
-    const int n_S = min(*a.n_subset_dev, a.n_subset_max);
-    const int p0 = (int)((long long)n_S * blockIdx.x / gridDim.x);
-    const int p1 = (int)((long long)n_S * (blockIdx.x + 1) / gridDim.x);
+    int p0, p1;
+    lmh_cta_range(a, p0, p1);
     const size_t row_bytes = (size_t)d * (DT == 0 ? 2 : 4);
 
     for (int tb = p0; tb < p1; tb += kTile) {

@@ -191,9 +191,8 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
     const int warp = warp_id(), lane = lane_id();
     pdl_trigger();
     pdl_wait();   // the subset (and n_S) come from the previous kernel on the stream
-    const int n_S = min(*a.n_subset_dev, a.n_subset_max);
-    const int p0 = (int)((long long)n_S * blockIdx.x / gridDim.x);
-    const int p1 = (int)((long long)n_S * (blockIdx.x + 1) / gridDim.x);
+    int p0, p1;
+    lmh_cta_range(a, p0, p1);
     const int len = p1 - p0;
     const int n_tiles = (len + kTileM - 1) / kTileM;
 

@@ -258,7 +258,7 @@ union_kernel(int V, const int32_t* __restrict__ static_ids, int n_static,
              int32_t* __restrict__ out_ids, int32_t* __restrict__ out_n,
              int32_t* __restrict__ out_local, int32_t* __restrict__ out_local_n,
              int32_t* __restrict__ sem_out, int* __restrict__ sem_out_n, int debug, int* flags,
-             long long* __restrict__ trace) {
+             long long* __restrict__ trace, const int32_t* __restrict__ dyn_base) {
     extern __shared__ __align__(16) unsigned char u_sm[];
     const int nwords = (V + 31) / 32;
     uint64_t* ck = (uint64_t*)u_sm;                          // [cap]
@@ -486,6 +486,19 @@ union_kernel(int V, const int32_t* __restrict__ static_ids, int n_static,
     __syncthreads();
 
     if (trace) { __syncthreads(); if (threadIdx.x == 0) { long long t_; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); trace[5] = t_; } }
+    // batched mode (dyn_base != null): the output is the sorted DYNAMIC list only,
+    // written at out_ids + *dyn_base, and *out_n = *dyn_base + its length
+    // (out_n = offsets + b + 1 for sequence b, dyn_base = offsets + b)
+    int base_off = 0;
+    if (dyn_base) {
+        for (int i = tid; i < n_static; i += T) {
+            const int32_t v = static_ids[i];
+            if (v >= 0 && v < V) atomicAnd(&bits[v >> 5], ~(1u << (v & 31)));
+        }
+        base_off = *dyn_base;
+        out_ids += base_off;
+        __syncthreads();
+    }
     // 6. compaction. Thread t owns words [t*nwords/T, (t+1)*nwords/T); a block
     //    scan of the popcounts gives each thread's output offset. The sorted
     //    ids are staged in shared memory (the candidate arrays are dead by now)
@@ -523,11 +536,11 @@ union_kernel(int V, const int32_t* __restrict__ static_ids, int n_static,
         }
     }
     if (tid == 0) {
-        *out_n = total;
+        *out_n = base_off + total;
         if (out_local_n) *out_local_n = total_local;
         if (sem_out_n) *sem_out_n = sem_n_s;
         if (bad_s) atomicOr(flags, kFlagBadIds);
-        if (total > n_static + n_dyn) atomicOr(flags, kFlagBudget);
+        if (total > (dyn_base ? 0 : n_static) + n_dyn) atomicOr(flags, kFlagBudget);
         if (*n_cand_dev > cap) atomicOr(flags, kFlagSelectOverflow);
     }
     if (trace) { __syncthreads(); if (threadIdx.x == 0) { long long t_; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); trace[6] = t_; } }
@@ -552,13 +565,14 @@ void launch_union(int V, const int32_t* static_ids, int n_static, const int32_t*
                   const int32_t* ctx_sel, const int* n_ctx_sel_dev,
                   int n_graph_sem_seeds, int per_seed, int n_dyn, int R, int r,
                   int32_t* out_ids, int32_t* out_n, int32_t* out_local, int32_t* out_local_n,
-                  int32_t* sem_out, int* sem_out_n, int debug, int* flags, cudaStream_t st, long long* trace) {
+                  int32_t* sem_out, int* sem_out_n, int debug, int* flags, cudaStream_t st, long long* trace,
+                  const int32_t* dyn_base) {
     const size_t smem = (size_t)cap * 13 + union_fixed_bytes(V, per_seed) + 16;
     cudaFuncSetAttribute(union_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     launch_pdl(union_kernel, dim3(1), dim3(kUnionThreads), smem, st, V, static_ids, n_static, seeds, n_seed, cand_s, cand_id, n_cand_dev,
                                                   cap, n_sem, row_ptr, col, ctx_sel, n_ctx_sel_dev, n_graph_sem_seeds,
                                                   per_seed, n_dyn, R, r, out_ids, out_n, out_local, out_local_n,
-                                                  sem_out, sem_out_n, debug, flags, trace);
+                                                  sem_out, sem_out_n, debug, flags, trace, dyn_base);
 }
 
 }  // namespace es

@@ -281,3 +281,108 @@ def test_qwen_full_size():
     ref = G.oracle_step(oracle, P)
     assert got["S"].size == 32768 + 4096
     check(P, got, ref, c["k"])
+
+
+# ------------------------------------------------ batched serving (config Bt)
+def _ragged_problem(seed, *, V, d, n_static, n_rows_per_seq, dyn_sizes, k, dtype="bf16"):
+    rng = np.random.default_rng(seed)
+    W = synth_matrix(seed, V, d, 0.02, dtype)
+    h_off = np.concatenate([[0], np.cumsum(n_rows_per_seq)]).astype(np.int64)
+    H = synth_matrix(seed + 1, int(h_off[-1]), d, 1.0, dtype)
+    perm = rng.permutation(V)
+    static = np.sort(perm[:n_static]).astype(np.int32)
+    pool = perm[n_static:]
+    dyn_lists = [np.sort(rng.choice(pool, n, replace=False)).astype(np.int32) for n in dyn_sizes]
+    dyn = np.concatenate(dyn_lists).astype(np.int32) if dyn_lists else np.zeros(0, np.int32)
+    d_off = np.concatenate([[0], np.cumsum([x.size for x in dyn_lists])]).astype(np.int64)
+    return dict(W=W, H=H, h_off=h_off, static=static, dyn=dyn, d_off=d_off, k=k, V=V, d=d, dtype=dtype)
+
+
+def synth_matrix(seed, rows, d, std, dtype):
+    import synth
+    return synth.matrix(seed, rows, d, std, dtype)
+
+
+def _run_ragged(R, max_rows=None):
+    ctx = es.Context(V=R["V"], d=R["d"], w_dtype=G.torch_dtype(R["dtype"]), h_dtype=G.torch_dtype(R["dtype"]),
+                     max_subset=max(R["static"].size, int(np.diff(R["d_off"]).max(initial=0)), 1),
+                     max_rows=max_rows or int(R["h_off"][-1]), max_k=64, max_sem=1, max_seeds=16, debug_checks=True)
+    W = G.to_dev(R["W"], DEV)
+    ctx.prepare_weights(W)
+    dyn = G.to_dev(R["dyn"], DEV) if R["dyn"].size else torch.zeros(1, dtype=torch.int32, device=DEV)
+    max_dyn = int(np.diff(R["d_off"]).max(initial=0))
+    out = ctx.subset_logits_topk_ragged(W, G.to_dev(R["H"], DEV), R["h_off"].tolist(), G.to_dev(R["static"], DEV),
+                                        dyn, G.to_dev(R["d_off"].astype(np.int32), DEV), max_dyn, R["k"])
+    torch.cuda.synchronize()
+    assert ctx.get_flags() == 0
+    return [t.cpu().numpy() for t in out]
+
+
+@pytest.mark.parametrize("case", ["mixed", "many_rows"])
+def test_ragged_lmh(case):
+    """Per-sequence V_b = static u dyn_b: row groups on the tensor-core path (n_b >= 5)
+    and on the FFMA path (n_b < 5), an empty dyn_b, a sequence without rows, and
+    (many_rows) more than 128 rows so the static block runs in several row groups."""
+    if case == "mixed":
+        R = _ragged_problem(60, V=20000, d=256, n_static=2500, n_rows_per_seq=[10, 1, 0, 6, 3, 12],
+                            dyn_sizes=[300, 17, 40, 0, 900, 256], k=10)
+    else:
+        R = _ragged_problem(61, V=12000, d=128, n_static=1000, n_rows_per_seq=[40, 60, 50, 7],
+                            dyn_sizes=[100, 0, 500, 33], k=8)
+    ids, vals, m, s = _run_ragged(R)
+    ref = oracle.subset_logits_topk_ragged(R["W"], R["H"], R["h_off"], R["static"], R["dyn"], R["d_off"], R["k"])
+    G.assert_triple_close(ids, vals, m, s, ref, R["k"])
+
+
+def test_batched_build_then_ragged():
+    """Batched build (per-sequence seeds, shared static) feeds the ragged LM head
+    through device offsets; both stages equal the oracle."""
+    P = G.make_problem(62, dtype="bf16", V=9000, d=128, n_static=900, n_sem=120, n_dyn=80, n_h=1, k=8)
+    B = 5
+    Q = synth_matrix(63, B, P["d"], 1.0, "bf16")
+    rng = np.random.default_rng(64)
+    n_seed = [0, 3, 10, 1, 6]
+    s_off = np.concatenate([[0], np.cumsum(n_seed)]).astype(np.int64)
+    seeds = rng.choice(P["V"], int(s_off[-1]), replace=True).astype(np.int32)
+    ctx = es.Context(V=P["V"], d=P["d"], w_dtype=torch.bfloat16, h_dtype=torch.bfloat16,
+                     max_subset=P["static"].size + P["n_dyn"], max_rows=40, max_k=64, max_sem=P["n_sem"],
+                     max_seeds=64, debug_checks=True)
+    W = G.to_dev(P["W"], DEV)
+    ctx.prepare_weights(W)
+    dyn, d_off = ctx.build_subset_batched(W, G.to_dev(Q, DEV), G.to_dev(P["static"], DEV), G.to_dev(seeds, DEV),
+                                          s_off.tolist(), G.to_dev(P["row_ptr"], DEV), G.to_dev(P["col"], DEV),
+                                          n_sem=P["n_sem"], n_dyn=P["n_dyn"], n_graph_sem_seeds=5, per_seed=4)
+    ref_dyn, ref_off = oracle.build_subset_batched(P["W"], Q, P["static"], seeds, s_off, P["row_ptr"], P["col"],
+                                                   n_sem=P["n_sem"], n_dyn=P["n_dyn"], n_graph_sem_seeds=5,
+                                                   per_seed=4)
+    torch.cuda.synchronize()
+    got_off = d_off.cpu().numpy()
+    np.testing.assert_array_equal(got_off, ref_off)
+    np.testing.assert_array_equal(dyn[:int(got_off[-1])].cpu().numpy(), ref_dyn)
+    assert ctx.get_flags() == 0
+    rows = [8, 2, 5, 0, 9]
+    h_off = np.concatenate([[0], np.cumsum(rows)]).astype(np.int64)
+    H = synth_matrix(65, int(h_off[-1]), P["d"], 1.0, "bf16")
+    out = ctx.subset_logits_topk_ragged(W, G.to_dev(H, DEV), h_off.tolist(), G.to_dev(P["static"], DEV), dyn, d_off,
+                                        P["n_dyn"], 8)
+    torch.cuda.synchronize()
+    ref = oracle.subset_logits_topk_ragged(P["W"], H, h_off, P["static"], ref_dyn, ref_off, 8)
+    G.assert_triple_close(*[t.cpu().numpy() for t in out], ref, 8)
+    assert ctx.get_flags() == 0
+
+
+@pytest.mark.slow
+def test_batched_full_size_sampled():
+    """Config Bt at full size (V=128256, d=4096, 64 sequences x 10 rows, static 32768,
+    dyn_b ~ U[256, 4096]) in the launch configuration bench.py times; the oracle
+    checks three sampled sequences (first, middle, last) element by element."""
+    n_seq, n_b = 64, 10
+    sizes = np.random.default_rng(66).integers(256, 4097, n_seq)
+    R = _ragged_problem(66, V=128256, d=4096, n_static=32768, n_rows_per_seq=[n_b] * n_seq,
+                        dyn_sizes=sizes.tolist(), k=10)
+    ids, vals, m, s = _run_ragged(R)
+    for b in (0, 31, 63):
+        h0, h1 = int(R["h_off"][b]), int(R["h_off"][b + 1])
+        S_b = np.union1d(R["static"], R["dyn"][R["d_off"][b]:R["d_off"][b + 1]]).astype(np.int32)
+        ref = oracle.subset_logits_topk(R["W"], R["H"][h0:h1], S_b, R["k"])
+        G.assert_triple_close(ids[h0:h1], vals[h0:h1], m[h0:h1], s[h0:h1], ref, R["k"])
