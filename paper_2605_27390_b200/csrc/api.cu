@@ -147,6 +147,7 @@ struct evospec_ctx {
     float* rg_m = nullptr;
     float* rg_s = nullptr;
     int32_t* rg_seg = nullptr;   // device {0, n_static}
+    int32_t* rg_segcta = nullptr;   // device [kMaxSeg+1] CTA schedule of the dynamic blocks
     int last_n_sem = 0;
     ncclComm_t comm = nullptr;
     // measurement hooks
@@ -215,7 +216,7 @@ evospec_status evospec_destroy(evospec_ctx* ctx) {
                     ctx->flags, ctx->wmax, ctx->g_ids, ctx->g_vals, ctx->g_m, ctx->g_s, ctx->st_q, ctx->st_H,
                     ctx->st_seeds, ctx->st_ctx, ctx->st_S, ctx->st_nS, ctx->st_local, ctx->st_nlocal,
                     ctx->st_tids, ctx->st_tvals, ctx->st_m, ctx->st_s, ctx->st_oids, ctx->st_ovals,
-                    ctx->st_lse, ctx->st_probs, ctx->rg_ids, ctx->rg_vals, ctx->rg_m, ctx->rg_s, ctx->rg_seg};
+                    ctx->st_lse, ctx->st_probs, ctx->rg_ids, ctx->rg_vals, ctx->rg_m, ctx->rg_s, ctx->rg_seg, ctx->rg_segcta};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (ctx->comm && nccl().loaded) nccl().CommDestroy(ctx->comm);
@@ -283,7 +284,7 @@ evospec_status evospec_create(evospec_ctx** out, const evospec_config* cfg, int 
     A(dalloc(&x->st_s, c.max_rows)); A(dalloc(&x->st_oids, hk)); A(dalloc(&x->st_ovals, hk));
     A(dalloc(&x->st_lse, c.max_rows)); A(dalloc(&x->st_probs, hk));
     A(dalloc(&x->rg_ids, 2 * hk)); A(dalloc(&x->rg_vals, 2 * hk));
-    A(dalloc(&x->rg_m, 2 * (size_t)c.max_rows)); A(dalloc(&x->rg_s, 2 * (size_t)c.max_rows)); A(dalloc(&x->rg_seg, 2));
+    A(dalloc(&x->rg_m, 2 * (size_t)c.max_rows)); A(dalloc(&x->rg_s, 2 * (size_t)c.max_rows)); A(dalloc(&x->rg_seg, 2)); A(dalloc(&x->rg_segcta, kMaxSeg + 1));
     if (e == cudaSuccess) e = cudaMemset(x->flags, 0, sizeof(int));
     if (e == cudaSuccess) {
         const float inf = INFINITY;  // until evospec_prepare_weights: certification never passes
@@ -488,13 +489,21 @@ static bool use_tc(const LmhArgs& a) {
     return a.n_h >= kTcMinRows;
 }
 
+struct LmhSegs {
+    int nseg, seg_ctas, seg_rows;
+    const int32_t* seg_pos;   // device [nseg+1] or null (every segment: the whole subset)
+    const int32_t* seg_h;     // host [nseg+1]
+    const int32_t* seg_cta;   // device [nseg+1] schedule or null (seg_ctas CTAs each)
+};
+
 // merged outputs (m_*) non-null: the single-shard merge (LSE, probabilities)
 // is fused into the finalisation kernel (used by evospec_draft_step at R = 1)
 static evospec_status lmh_impl(evospec_ctx* ctx, const void* W, int64_t n_w_rows, const void* H, int32_t n_h,
                                const int32_t* subset, const int32_t* n_subset_dev, int32_t n_subset_max, int32_t k,
                                float inv_temp, int32_t* topk_ids, float* topk_vals, float* row_max,
                                float* row_sumexp, float* logits_out, void* stream, int32_t* m_ids, float* m_vals,
-                               float* m_lse, float* m_probs, const int32_t* seg = nullptr) {
+                               float* m_lse, float* m_probs, const int32_t* seg = nullptr,
+                               const LmhSegs* segs = nullptr) {
     if (!ctx || !W || !H || !subset || (!n_subset_dev && !seg) || !topk_ids || !topk_vals || !row_max || !row_sumexp)
         return fail(EVOSPEC_EINPUT, "subset_logits_topk: null argument");
     const evospec_config& c = ctx->cfg;
@@ -521,6 +530,12 @@ static evospec_status lmh_impl(evospec_ctx* ctx, const void* W, int64_t n_w_rows
     a.logits_out = logits_out;
     a.part = ctx->part;
     a.m_ids = m_ids; a.m_vals = m_vals; a.m_lse = m_lse; a.m_probs = m_probs;
+    if (segs) {
+        a.nseg = segs->nseg; a.seg_ctas = segs->seg_ctas; a.seg_rows = segs->seg_rows; a.seg_pos = segs->seg_pos;
+        a.seg_cta = segs->seg_cta;
+        for (int b = 0; b <= segs->nseg; ++b) a.seg_h[b] = segs->seg_h[b];
+        if (!use_tc(a)) return fail(EVOSPEC_EINPUT, "segment mode needs the tensor-core path");
+    }
     if (getenv("EVOSPEC_TRACE")) {
         if (!ctx->trace) CUDA_TRY(cudaMalloc(&ctx->trace, kTraceLen * sizeof(long long)));
         CUDA_TRY(cudaMemsetAsync(ctx->trace, 0, 2 * kNumSMs * 8 * sizeof(long long), st));
@@ -533,7 +548,7 @@ static evospec_status lmh_impl(evospec_ctx* ctx, const void* W, int64_t n_w_rows
         if (use_tc(a)) {
             CUDA_TRY(launch_lmh_tc(a, st));
             ctx->launches += 1;
-            n_cta = lmh_tc_grid();
+            n_cta = segs ? segs->seg_ctas : lmh_tc_grid();
             gamma = kTcGamma;
         } else {
             for (int h0 = 0; h0 < n_h;) {
@@ -596,23 +611,56 @@ evospec_status evospec_subset_logits_topk_ragged(evospec_ctx* ctx, const void* W
     set2_kernel<<<1, 1, 0, st>>>(ctx->rg_seg, 0, n_static);
     ctx->launches += 1;
     LAUNCH_CHECK("set2");
-    for (int r0 = 0; r0 < n_rows; r0 += kTcMaxRows) {
-        const int g = std::min(kTcMaxRows, n_rows - r0);
-        evospec_status rc = lmh_impl(ctx, W, n_w_rows, (const char*)H + row_bytes * r0, g, static_ids ? static_ids : dyn_ids,
-                                     nullptr, n_static, k, inv_temp, ctx->rg_ids + (size_t)r0 * k,
-                                     ctx->rg_vals + (size_t)r0 * k, ctx->rg_m + r0, ctx->rg_s + r0, nullptr, stream,
-                                     nullptr, nullptr, nullptr, nullptr, ctx->rg_seg);
+    LmhArgs probe{};
+    probe.w_dtype = c.w_dtype; probe.h_dtype = c.h_dtype; probe.d = c.d; probe.n_w_rows = n_w_rows;
+    probe.KP = k + kTopkPad; probe.n_h = 1;
+    const bool seg_ok = lmh_tc_supported(probe) && probe.KP <= 32 && !getenv("EVOSPEC_RAGGED_LOOP");
+    int max_rows_seq = 0;
+    for (int b = 0; b < B; ++b) max_rows_seq = std::max(max_rows_seq, h_offsets[b + 1] - h_offsets[b]);
+    if (seg_ok) {
+        // static block: one launch, row groups of <= 128 as segments over the same
+        // static range (their CTAs read the same W rows at about the same time)
+        const int ns = (n_rows + kTcMaxRows - 1) / kTcMaxRows;
+        const int per = (n_rows + ns - 1) / ns;
+        int sh[kMaxSeg + 1];
+        for (int b = 0; b <= ns; ++b) sh[b] = std::min(n_rows, b * per);
+        const LmhSegs ss{ns, lmh_tc_grid() / ns, per, nullptr, sh, nullptr};
+        evospec_status rc = lmh_impl(ctx, W, n_w_rows, H, n_rows, static_ids ? static_ids : dyn_ids, ctx->rg_seg + 1,
+                                     n_static, k, inv_temp, ctx->rg_ids, ctx->rg_vals, ctx->rg_m, ctx->rg_s, nullptr,
+                                     stream, nullptr, nullptr, nullptr, nullptr, nullptr, &ss);
         if (rc != EVOSPEC_OK) return rc;
+    } else {
+        for (int r0 = 0; r0 < n_rows; r0 += kTcMaxRows) {
+            const int g = std::min(kTcMaxRows, n_rows - r0);
+            evospec_status rc = lmh_impl(ctx, W, n_w_rows, (const char*)H + row_bytes * r0, g,
+                                         static_ids ? static_ids : dyn_ids, nullptr, n_static, k, inv_temp,
+                                         ctx->rg_ids + (size_t)r0 * k, ctx->rg_vals + (size_t)r0 * k, ctx->rg_m + r0,
+                                         ctx->rg_s + r0, nullptr, stream, nullptr, nullptr, nullptr, nullptr,
+                                         ctx->rg_seg);
+            if (rc != EVOSPEC_OK) return rc;
+        }
     }
-    // dynamic blocks: sequence b's rows against its own segment of dyn_ids
-    for (int b = 0; b < B; ++b) {
-        const int r0 = h_offsets[b], g = h_offsets[b + 1] - r0;
-        if (g == 0) continue;
-        evospec_status rc = lmh_impl(ctx, W, n_w_rows, (const char*)H + row_bytes * r0, g, dyn_ids, nullptr, max_dyn,
-                                     k, inv_temp, ids1 + (size_t)r0 * k, vals1 + (size_t)r0 * k,
-                                     ctx->rg_m + n_rows + r0, ctx->rg_s + n_rows + r0, nullptr, stream, nullptr,
-                                     nullptr, nullptr, nullptr, dyn_offsets + b);
+    if (seg_ok && B <= std::min(kMaxSeg, lmh_tc_grid()) && max_rows_seq <= kTcMaxRows) {
+        // dynamic blocks: one launch, sequence b = segment b (its rows, its dyn_b)
+        // CTAs in proportion to each sequence's dyn_b length (device sizes -> device schedule)
+        launch_seg_schedule(dyn_offsets, h_offsets, B, lmh_tc_grid(), ctx->rg_segcta, st);
+        ctx->launches += 1;
+        LAUNCH_CHECK("seg_schedule");
+        const LmhSegs ds{B, lmh_tc_grid() / B, std::max(1, max_rows_seq), dyn_offsets, h_offsets, ctx->rg_segcta};
+        evospec_status rc = lmh_impl(ctx, W, n_w_rows, H, n_rows, dyn_ids, nullptr, max_dyn, k, inv_temp, ids1, vals1,
+                                     ctx->rg_m + n_rows, ctx->rg_s + n_rows, nullptr, stream, nullptr, nullptr,
+                                     nullptr, nullptr, ctx->rg_seg, &ds);
         if (rc != EVOSPEC_OK) return rc;
+    } else {
+        for (int b = 0; b < B; ++b) {
+            const int r0 = h_offsets[b], g = h_offsets[b + 1] - r0;
+            if (g == 0) continue;
+            evospec_status rc = lmh_impl(ctx, W, n_w_rows, (const char*)H + row_bytes * r0, g, dyn_ids, nullptr,
+                                         max_dyn, k, inv_temp, ids1 + (size_t)r0 * k, vals1 + (size_t)r0 * k,
+                                         ctx->rg_m + n_rows + r0, ctx->rg_s + n_rows + r0, nullptr, stream, nullptr,
+                                         nullptr, nullptr, nullptr, dyn_offsets + b);
+            if (rc != EVOSPEC_OK) return rc;
+        }
     }
     // static u dynamic are disjoint: the two triples merge like two vocabulary shards
     launch_merge(2, n_rows, k, ctx->rg_ids, ctx->rg_vals, ctx->rg_m, ctx->rg_s, topk_ids, topk_vals, nullptr, nullptr,

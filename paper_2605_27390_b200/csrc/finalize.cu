@@ -344,7 +344,7 @@ ES_DEV void sort32_rolled(float& v, int& p) {
 
 template <int U>
 __global__ void __launch_bounds__(kFin32Threads)
-lmh_finalize32_kernel(LmhArgs a, int n_cta, int k, float gamma, const float* __restrict__ wmax_dev,
+lmh_finalize32_kernel(LmhArgs a, int n_cta_arg, int k, float gamma, const float* __restrict__ wmax_dev,
                       int32_t* __restrict__ topk_ids, float* __restrict__ topk_vals,
                       float* __restrict__ row_max, float* __restrict__ row_sumexp, int* flags) {
     const int r = blockIdx.x;
@@ -367,6 +367,19 @@ lmh_finalize32_kernel(LmhArgs a, int n_cta, int k, float gamma, const float* __r
     pdl_trigger();
     pdl_wait();
     if (threadIdx.x == 0) { FIN_TRACE(0); FIN_DT(0); }
+    // the row's lists: CTAs [c_base, c_base + n_cta) (segment mode: its segment's CTAs)
+    int n_cta = n_cta_arg, c_base = 0;
+    if (a.nseg > 0) {
+        int b = 0;
+        while (b + 1 < a.nseg && a.seg_h[b + 1] <= r) ++b;
+        if (a.seg_cta) {
+            c_base = a.seg_cta[b];
+            n_cta = a.seg_cta[b + 1] - c_base;
+        } else {
+            c_base = b * a.seg_ctas;
+            n_cta = a.seg_ctas;
+        }
+    }
     // A. every global load at once
     const int nq = n_cta * (kFin32LS / 4);
     float4 vv[U];
@@ -376,14 +389,14 @@ lmh_finalize32_kernel(LmhArgs a, int n_cta, int k, float gamma, const float* __r
         const int q = threadIdx.x + u * kFin32Threads;
         vv[u] = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
         if (q < nq) {
-            const size_t o = ((size_t)(q >> 4) * a.n_h + r) * kFin32LS + (q & 15) * 4;
+            const size_t o = ((size_t)(c_base + (q >> 4)) * a.n_h + r) * kFin32LS + (q & 15) * 4;
             vv[u] = __ldcg((const float4*)&a.part.val[o]);
             ii[u] = __ldcg((const int4*)&a.part.id[o]);
         }
     }
     float cm_ = -INFINITY, cs_ = 0.0f, thl = -INFINITY;
     if ((int)threadIdx.x < n_cta) {
-        const size_t o = (size_t)threadIdx.x * a.n_h + r;
+        const size_t o = (size_t)(c_base + threadIdx.x) * a.n_h + r;
         cm_ = __ldcg(&a.part.m[o]);
         cs_ = __ldcg(&a.part.s[o]);
         const int cn = __ldcg(&a.part.cnt[o]);
@@ -503,7 +516,7 @@ lmh_finalize32_kernel(LmhArgs a, int n_cta, int k, float gamma, const float* __r
             } else {
                 const int q = (b >> 2) * 32 + lane, comp = b & 3;
                 if (q < nq) {
-                    const size_t o = ((size_t)(q >> 4) * a.n_h + r) * kFin32LS + (q & 15) * 4 + comp;
+                    const size_t o = ((size_t)(c_base + (q >> 4)) * a.n_h + r) * kFin32LS + (q & 15) * 4 + comp;
                     bv = __ldcg(&a.part.val[o]);
                     bp = __ldcg(&a.part.id[o]);
                 }
@@ -646,9 +659,9 @@ void launch_lmh_finalize(const LmhArgs& a, int n_cta, int k, const float* wmax_d
                          float* topk_vals, float* row_max, float* row_sumexp, int* flags, cudaStream_t st,
                          float gamma) {
     if (a.KP <= 32 && a.LS == kFin32LS && n_cta * (kFin32LS / 4) <= 10 * kFin32Threads) {
-        // one CTA per SM (the dynamic allocation is only a placement hint): two
-        // CTAs sharing an SM measured slower
-        const size_t smem = 120 * 1024;
+        // one CTA per SM while the rows fit one wave (the dynamic allocation is only
+        // a placement hint: two CTAs sharing an SM measured slower); more rows pack
+        const size_t smem = a.n_h <= kNumSMs ? 120 * 1024 : 0;
         if (n_cta * (kFin32LS / 4) <= 5 * kFin32Threads) {
             cudaFuncSetAttribute(lmh_finalize32_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             launch_pdl(lmh_finalize32_kernel<5>, dim3(a.n_h), dim3(kFin32Threads), smem, st, a, n_cta, k, gamma,
@@ -664,6 +677,42 @@ void launch_lmh_finalize(const LmhArgs& a, int n_cta, int k, const float* wmax_d
     cudaFuncSetAttribute(lmh_finalize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     lmh_finalize_kernel<<<a.n_h, kFinThreads, smem, st>>>(a, n_cta, k, gamma, wmax_dev, topk_ids, topk_vals,
                                                            row_max, row_sumexp, flags);
+}
+
+// ------------------------------------------------------------ segment schedule
+// CTAs per segment for a segment-mode LM-head launch: one for every segment with
+// rows and positions, the rest in proportion to the segment's positions (the
+// work is rows of W streamed). Measured on config Bt (tools/bench_bt.py) faster
+// than the min-max share (sum_b ceil(size_b / T) <= grid) by ~10%.
+//   seg_cta[b] = active(<b) + floor((grid - n_active) * cum_size(<b) / total)
+__global__ void seg_schedule_kernel(const int32_t* __restrict__ seg_pos, const SegRows seg_h_p, int nseg, int grid,
+                                    int32_t* __restrict__ seg_cta) {
+    const int* seg_h = seg_h_p.h;
+    pdl_trigger();
+    pdl_wait();
+    if (threadIdx.x != 0) return;
+    long long total = 0;
+    int n_active = 0;
+    for (int b = 0; b < nseg; ++b) {
+        const int sz = seg_pos[b + 1] - seg_pos[b];
+        if (sz > 0 && seg_h[b + 1] > seg_h[b]) { total += sz; ++n_active; }
+    }
+    const int spare = max(0, grid - n_active);
+    long long cum = 0;
+    int act = 0;
+    for (int b = 0; b < nseg; ++b) {
+        seg_cta[b] = act + (total > 0 ? (int)((long long)spare * cum / total) : 0);
+        const int sz = seg_pos[b + 1] - seg_pos[b];
+        if (sz > 0 && seg_h[b + 1] > seg_h[b]) { cum += sz; ++act; }
+    }
+    seg_cta[nseg] = act + (total > 0 ? (int)((long long)spare * cum / total) : 0);
+}
+
+void launch_seg_schedule(const int32_t* seg_pos, const int32_t* seg_h_host, int nseg, int grid, int32_t* seg_cta,
+                         cudaStream_t st) {
+    SegRows sr{};
+    for (int b = 0; b <= nseg && b <= kMaxSeg; ++b) sr.h[b] = seg_h_host[b];
+    launch_pdl(seg_schedule_kernel, dim3(1), dim3(32), 0, st, seg_pos, sr, nseg, grid, seg_cta);
 }
 
 // ------------------------------------------------------------ shard merge

@@ -47,6 +47,8 @@ void launch_union(int V, const int32_t* static_ids, int n_static, const int32_t*
 // CTA's best candidates sorted by (z desc, id asc); entries [cnt, cnt + xcnt)
 // are unsorted extras from the CTA's last tile that beat entry KP-1 of the
 // sorted list (the last tile is not folded, its survivors are appended).
+constexpr int kMaxSeg = 128;     // segments of one segment-mode LM-head launch
+
 struct LmhPartials {
     float* val;    // [n_cta][n_h][LS]
     int32_t* id;   // [n_cta][n_h][LS] subset positions (sorted subset: position order = id order)
@@ -60,6 +62,14 @@ struct LmhArgs {
     const void* H; int n_h; int h_dtype;
     const int32_t* subset; const int* n_subset_dev; int n_subset_max;
     const int32_t* seg;   // optional device [2]: positions [seg[0], seg[1]) of subset (ragged segments)
+    // segment mode (tensor-core path, nseg > 0): segment b = H rows [seg_h[b], seg_h[b+1])
+    // against subset positions [seg_pos[b], seg_pos[b+1]) (seg_pos == null: every
+    // segment takes the whole subset); seg_ctas CTAs per segment, CTA c serves
+    // segment c / seg_ctas (the rest idle); n_h = total rows, seg_rows = max rows
+    int nseg, seg_ctas, seg_rows;
+    const int32_t* seg_pos;
+    const int32_t* seg_cta;   // optional device [nseg+1]: CTAs [seg_cta[b], seg_cta[b+1]) serve segment b
+    int seg_h[kMaxSeg + 1];
     int R; int KP; int LS; float inv_temp;   // LS: list stride (KP <= 32: 64, else KP)
     float* logits_out;  // optional [n_h][n_subset_max]
     long long* trace;   // optional per-CTA globaltimer stamps [n_cta][8] (profiling)
@@ -98,6 +108,9 @@ cudaError_t launch_lmh_tc(const LmhArgs& a, cudaStream_t st);
 void launch_lmh_finalize(const LmhArgs& a, int n_cta, int k, const float* wmax_dev,
                          int32_t* topk_ids, float* topk_vals, float* row_max, float* row_sumexp,
                          int* flags, cudaStream_t st, float gamma);
+struct SegRows { int h[kMaxSeg + 1]; };
+void launch_seg_schedule(const int32_t* seg_pos, const int32_t* seg_h_host, int nseg, int grid, int32_t* seg_cta,
+                         cudaStream_t st);
 void launch_merge(int R, int n_h, int k, const int32_t* ids, const float* vals, const float* m,
                   const float* s, int32_t* out_ids, float* out_vals, float* out_lse, float* out_probs,
                   cudaStream_t st, float* out_m = nullptr, float* out_s = nullptr);

@@ -336,8 +336,8 @@ ES_DEV void epi_store(const EpiSmem& e, const LmhPartials& P, int cta, int n_h_t
 // unsorted extras (the finalisation scans them). Survivors must beat the
 // list's entry KP-1 -- any element of the CTA's top-KP does. Rows whose list
 // is not full, or with more survivors than LS - KP slots, take the full fold.
-ES_DEV void epi_tile_last(const EpiSmem& e, const LmhPartials& P, int cta, int n_h_total, int n_h, int KP, int LS,
-                          int tn, int base_pos, int warp, int n_warps) {
+ES_DEV void epi_tile_last(const EpiSmem& e, const LmhPartials& P, int cta, int n_h_total, int h_row0, int n_h,
+                          int KP, int LS, int tn, int base_pos, int warp, int n_warps) {
     if (tn <= 0) return;
     const int lane = lane_id();
     for (int r = warp; r < n_h; r += n_warps) {
@@ -372,7 +372,7 @@ ES_DEV void epi_tile_last(const EpiSmem& e, const LmhPartials& P, int cta, int n
             fold_topk32(e, r, KP, tn, base_pos, warp, v, lm);
             continue;
         }
-        const size_t o = ((size_t)cta * n_h_total + r);
+        const size_t o = ((size_t)cta * n_h_total + h_row0 + r);
         int base = cnt;
 #pragma unroll
         for (int j = 0; j < kTileJ; ++j) {

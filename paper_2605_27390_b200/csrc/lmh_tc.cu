@@ -177,10 +177,27 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
     extern __shared__ __align__(1024) unsigned char tc_sm[];
     // 1024-align the stage ring (SWIZZLE_128B atoms)
     unsigned char* base = (unsigned char*)(((uintptr_t)tc_sm + 1023) & ~(uintptr_t)1023);
-    const int S = tp.stages, NP = tp.n_pad, n_h = a.n_h;
+    const int S = tp.stages, NP = tp.n_pad;
+    // rows of this CTA: all n_h, or (segment mode) its segment's rows [h_row0, h_row0 + n_h)
+    int n_h = a.n_h, h_row0 = 0, seg_b = -1, seg_c0 = 0, seg_m = 1;
+    if (a.nseg > 0) {
+        if (a.seg_cta) {
+            pdl_wait();                              // the schedule comes from the previous kernel
+            seg_b = 0;
+            while (seg_b < a.nseg && a.seg_cta[seg_b + 1] <= (int)blockIdx.x) ++seg_b;
+            if (seg_b < a.nseg) { seg_c0 = a.seg_cta[seg_b]; seg_m = a.seg_cta[seg_b + 1] - seg_c0; }
+        } else {
+            seg_b = blockIdx.x / a.seg_ctas;
+            seg_c0 = seg_b * a.seg_ctas;
+            seg_m = a.seg_ctas;
+        }
+        if (seg_b >= a.nseg || a.seg_h[seg_b + 1] == a.seg_h[seg_b]) return;   // idle: no segment, or no rows
+        h_row0 = a.seg_h[seg_b];
+        n_h = a.seg_h[seg_b + 1] - h_row0;
+    }
     unsigned char* smA = base;                                   // [S][128][128 B]
     unsigned char* smB = base + tp.off_b;                        // [S][NP][128 B]
-    EpiSmem e = epi_carve(base + tp.off_epi, n_h, a.KP, kTcWarps);
+    EpiSmem e = epi_carve(base + tp.off_epi, a.nseg > 0 ? a.seg_rows : n_h, a.KP, kTcWarps);
     uint64_t* full = (uint64_t*)(base + tp.off_bar);             // [S]
     uint64_t* empty = full + S;                                  // [S]
     uint64_t* tfull = empty + S;                                 // [2]
@@ -192,7 +209,22 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
     pdl_trigger();
     pdl_wait();   // the subset (and n_S) come from the previous kernel on the stream
     int p0, p1;
-    lmh_cta_range(a, p0, p1);
+    if (seg_b >= 0) {
+        // the CTAs of a segment split its positions identically for every segment
+        // with the same range, so concurrent row groups share W rows through L2
+        int s0 = 0, s1;
+        if (a.seg_pos) {
+            s0 = a.seg_pos[seg_b];
+            s1 = s0 + min(a.seg_pos[seg_b + 1] - s0, a.n_subset_max);
+        } else {
+            s1 = min(*a.n_subset_dev, a.n_subset_max);
+        }
+        const int n = max(0, s1 - s0), j = blockIdx.x - seg_c0;
+        p0 = s0 + (int)((long long)n * j / seg_m);
+        p1 = s0 + (int)((long long)n * (j + 1) / seg_m);
+    } else {
+        lmh_cta_range(a, p0, p1);
+    }
     const int len = p1 - p0;
     const int n_tiles = (len + kTileM - 1) / kTileM;
 
@@ -276,7 +308,7 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
                 mbar_wait(&empty[stage], phase ^ 1);
                 if (warp == 0 && lane == 0) {
                     mbar_arrive_expect_tx(&full[stage], (uint32_t)(NP * 128));
-                    tma_load_2d(smB + (size_t)stage * NP * 128, &tmap_h, &full[stage], kb * kBlockK, 0, pol_h);
+                    tma_load_2d(smB + (size_t)stage * NP * 128, &tmap_h, &full[stage], kb * kBlockK, h_row0, pol_h);
                 }
                 const uint32_t dA = smem_u32(smA + (size_t)stage * kTileM * 128);
 #pragma unroll
@@ -361,7 +393,7 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
         tile_range(n_tiles - 1, t0, tn);
         named_bar_sync(2, kTcWarps * 32);
         if (n_tiles > 1)
-            epi_tile_last(e, a.part, blockIdx.x, a.n_h, n_h, a.KP, a.LS, tn, t0, warp, kTcWarps);
+            epi_tile_last(e, a.part, blockIdx.x, a.n_h, h_row0, n_h, a.KP, a.LS, tn, t0, warp, kTcWarps);
         else
             epi_tile(e, n_h, a.KP, tn, t0, warp, kTcWarps);
         if (warp == kTcEpiWarp0 && lane == 0 && n_tiles - 1 < 2) TC_TRACE(4 + 2 * (n_tiles - 1));
@@ -369,7 +401,7 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    epi_store(e, a.part, blockIdx.x, a.n_h, 0, n_h, a.KP, a.LS, warp, kTcWarps);
+    epi_store(e, a.part, blockIdx.x, a.n_h, h_row0, n_h, a.KP, a.LS, warp, kTcWarps);
     if (threadIdx.x == 0) TC_TRACE(7);
     if (warp == kTcMmaWarp)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(tp.tmem_cols));
@@ -404,13 +436,15 @@ static bool make_map(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t o
 int lmh_tc_grid() { return kNumSMs; }
 
 bool lmh_tc_supported(const LmhArgs& a) {
-    return a.w_dtype == 0 && a.h_dtype == 0 && a.d % kBlockK == 0 && a.n_h >= 1 && a.n_h <= kTcMaxRows &&
-           a.n_w_rows <= 0x7fffffff;
+    const int rows = a.nseg > 0 ? a.seg_rows : a.n_h;
+    return a.w_dtype == 0 && a.h_dtype == 0 && a.d % kBlockK == 0 && rows >= 1 && rows <= kTcMaxRows &&
+           a.n_w_rows <= 0x7fffffff && (a.nseg == 0 || (a.nseg <= lmh_tc_grid() && a.KP <= 32));
 }
 
 cudaError_t launch_lmh_tc(const LmhArgs& a, cudaStream_t st) {
     TcParams tp{};
-    tp.n_pad = ((a.n_h + 15) / 16) * 16;
+    const int rows = a.nseg > 0 ? a.seg_rows : a.n_h;
+    tp.n_pad = ((rows + 15) / 16) * 16;
     tp.nkb = a.d / kBlockK;
     tp.pf_dist = kPfDist;
     if (const char* e = getenv("EVOSPEC_PF")) tp.pf_dist = atoi(e);
@@ -418,7 +452,7 @@ cudaError_t launch_lmh_tc(const LmhArgs& a, cudaStream_t st) {
     while (c < cols) c <<= 1;
     tp.tmem_cols = c;
     const size_t stage_a = (size_t)kTileM * 128, stage_b = (size_t)tp.n_pad * 128;
-    const size_t epi = epi_smem_bytes(a.n_h, a.KP, kTcWarps);
+    const size_t epi = epi_smem_bytes(rows, a.KP, kTcWarps);
     const size_t fixed = epi + 2 * 128 * 4 + 64 * 8 + 1024 /*align slack*/ + 256;
     const size_t budget = 227 * 1024;
     int S = (int)((budget - fixed) / (stage_a + stage_b));
