@@ -24,6 +24,8 @@
 //                       formation needs it, and the cap are resolved in the
 //                       union kernel (union.cu) on those exact keys.
 #include <cooperative_groups.h>
+#include <cstdlib>
+#include <cstring>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -138,13 +140,226 @@ sem_scan_kernel(const void* __restrict__ E, int64_t n_rows, int d,
         if (hist_sm[i]) atomicAdd(&hist12[i], hist_sm[i]);
 }
 
+// ---------------------------------------------------------------- scan (TMA ring)
+// bf16 E, d % 256 == 0, d <= 4096: the same exact fp64 scores as above, with E
+// streamed through shared memory by the bulk-copy engine instead of per-lane
+// loads, so that the bytes in flight per SM stay at the ring size (no drain
+// between column slabs).
+//   CTA: rows [r0, r1) (contiguous, 1/grid of E); stage = 8 consecutive rows
+//   (8 * d * 2 bytes, one contiguous cp.async.bulk); a ring of kScanStages.
+//   warp 16: producer (one elected thread). Warps 0 .. d/256-1: consumers; warp
+//   w owns the 256-column slab [256 w, 256 w + 256) of every row, q for it lives
+//   in registers (8 fp64 per lane, pre-scaled by 2^896), and each stage costs
+//   it 8 LDS.128 + 64 fp64 FMAs per lane. A reduce-scatter over the lanes
+//   leaves one partial per (row, slab); the stage's owner warp (stage % slabs)
+//   adds the partials of each row in slab order and writes s64 / key32 / the
+//   histogram, then frees the stage (the others free it right after their
+//   partials are written).
+constexpr int kScanStages = 3;
+constexpr int kScanConsumers = 16;
+constexpr int kScanRS = 8;          // rows per ring stage (8: one CTA per SM; 4 + two CTAs measured slower)
+constexpr int kScanPf = 0;          // stages of L2 prefetch ahead of the ring (measured slower: off)
+
+ES_DEV uint32_t s_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+ES_DEV void s_mbar_init(uint64_t* b, uint32_t n) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(s_u32(b)), "r"(n));
+}
+ES_DEV void s_mbar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(s_u32(b)) : "memory");
+}
+ES_DEV void s_mbar_expect(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(s_u32(b)), "r"(bytes) : "memory");
+}
+ES_DEV void s_mbar_wait(uint64_t* b, uint32_t parity) {
+    asm volatile(
+        "{\n.reg .pred p;\nW_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra W_%=;\n}\n" ::"r"(s_u32(b)), "r"(parity) : "memory");
+}
+ES_DEV void s_bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+        ::"r"(s_u32(dst)), "l"(src), "r"(bytes), "r"(s_u32(bar)), "l"(policy) : "memory");
+}
+
+template <int kScanRowsPerStage>
+__global__ void __launch_bounds__((kScanConsumers + 1) * 32, kScanRowsPerStage == 4 ? 2 : 1)
+sem_scan_tma_kernel(const uint16_t* __restrict__ E, int64_t n_rows, int d, const void* __restrict__ q, int q_dtype,
+                    uint32_t* __restrict__ hist12, double* __restrict__ s64, uint32_t* __restrict__ key32, int pf,
+                    int il) {
+    extern __shared__ __align__(128) unsigned char sc_sm[];
+    const size_t row_bytes = (size_t)d * 2;
+    const size_t stage_bytes = kScanRowsPerStage * row_bytes;
+    unsigned char* ring = sc_sm;                                              // [S][8][d] bf16
+    uint32_t* hist_sm = (uint32_t*)(ring + kScanStages * stage_bytes);       // [4096]
+    double* red = (double*)(hist_sm + kHistBins);                            // [S][16][8]
+    uint64_t* full = (uint64_t*)(red + kScanStages * kScanConsumers * kScanRowsPerStage);
+    uint64_t* empty = full + kScanStages;
+    uint64_t* part_bar = empty + kScanStages;
+    const int warp = warp_id(), lane = lane_id();
+    const int n_slab = d / 256;                                              // <= 16
+    // stage i of this CTA: rows [8 g, 8 g + 8) of E with g = i * grid + cta (il = 1:
+    // all SMs sweep adjacent rows together), or a contiguous 1/grid block (il = 0)
+    const int64_t n_groups = (n_rows + kScanRowsPerStage - 1) / kScanRowsPerStage;
+    const int64_t r0 = n_rows * blockIdx.x / gridDim.x, r1 = n_rows * (blockIdx.x + 1) / gridDim.x;
+    const int n_stage = il ? (int)((n_groups - blockIdx.x + gridDim.x - 1) / gridDim.x)
+                           : (int)((r1 - r0 + kScanRowsPerStage - 1) / kScanRowsPerStage);
+    auto stage_row = [&](int i) -> int64_t {
+        return il ? ((int64_t)i * gridDim.x + blockIdx.x) * kScanRowsPerStage : r0 + (int64_t)i * kScanRowsPerStage;
+    };
+    const int64_t r_end = il ? n_rows : r1;
+    for (int i = threadIdx.x; i < kHistBins; i += blockDim.x) hist_sm[i] = 0;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kScanStages; ++s) {
+            s_mbar_init(&full[s], 1);
+            s_mbar_init(&empty[s], n_slab);
+            s_mbar_init(&part_bar[s], n_slab);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (warp == kScanConsumers) {
+        if (lane == 0) {
+            uint64_t pol;
+            asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+            // L2 prefetch pf stages ahead of the ring: HBM sees (ring + pf) stages of
+            // requests per SM, more than shared memory can hold
+            for (int i = 0; i < min(pf, n_stage); ++i) {
+                const int64_t row = stage_row(i);
+                const int nr = (int)min((int64_t)kScanRowsPerStage, r_end - row);
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"((const unsigned char*)E + row * row_bytes),
+                             "r"((uint32_t)(nr * row_bytes)) : "memory");
+            }
+            for (int i = 0; i < n_stage; ++i) {
+                const int slot = i % kScanStages;
+                if (pf > 0 && i + pf < n_stage) {
+                    const int64_t prow = stage_row(i + pf);
+                    const int pnr = (int)min((int64_t)kScanRowsPerStage, r_end - prow);
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;"
+                                 ::"l"((const unsigned char*)E + prow * row_bytes), "r"((uint32_t)(pnr * row_bytes)) : "memory");
+                }
+                if (i >= kScanStages) s_mbar_wait(&empty[slot], (uint32_t)((i / kScanStages) - 1) & 1);
+                const int64_t row = stage_row(i);
+                const int nr = (int)min((int64_t)kScanRowsPerStage, r_end - row);
+                const uint32_t bytes = (uint32_t)(nr * row_bytes);
+                s_mbar_expect(&full[slot], bytes);
+                s_bulk_g2s(ring + slot * stage_bytes, (const unsigned char*)E + row * row_bytes, bytes, &full[slot], pol);
+            }
+        }
+        return;
+    }
+    if (warp >= n_slab) return;                  // d < 4096: fewer slab warps
+    // q for this warp's slab, lane's 8 columns, fp64 pre-scaled by 2^896 (see sem_scan_kernel)
+    double qv[8];
+    {
+        const int c0 = warp * 256 + lane * 8;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const double v = q_dtype == 0 ? (double)bf16_bits_to_f32(((const uint16_t*)q)[c0 + j])
+                                          : (double)((const float*)q)[c0 + j];
+            qv[j] = v * 0x1p896;
+        }
+    }
+    for (int i = 0; i < n_stage; ++i) {
+        const int slot = i % kScanStages;
+        s_mbar_wait(&full[slot], (uint32_t)(i / kScanStages) & 1);
+        const int64_t row0 = stage_row(i);
+        const int nr = (int)min((int64_t)kScanRowsPerStage, r_end - row0);
+        const unsigned char* st = ring + slot * stage_bytes + (size_t)warp * 512 + (size_t)lane * 16;
+        double acc[kScanRowsPerStage];
+#pragma unroll
+        for (int r = 0; r < kScanRowsPerStage; ++r) {
+            acc[r] = 0.0;
+            if (r < nr) {
+                const uint4 u = *(const uint4*)(st + (size_t)r * row_bytes);
+                const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    // bf16 fields in place in the double's high word (see sem_scan_kernel)
+                    const uint32_t lo = (uint32_t)((int32_t)(w4[j] << 16) >> 3) & 0x8FFFE000u;
+                    const uint32_t hi = (uint32_t)((int32_t)w4[j] >> 3) & 0x8FFFE000u;
+                    acc[r] = fma(__hiloint2double((int)lo, 0), qv[2 * j], acc[r]);
+                    acc[r] = fma(__hiloint2double((int)hi, 0), qv[2 * j + 1], acc[r]);
+                }
+            }
+        }
+        // reduce-scatter 8 rows over 32 lanes: lanes (l & 7) == r end with row r's
+        // sum over 4 lanes, then two butterflies finish it
+#pragma unroll
+        for (int h = kScanRowsPerStage / 2; h >= 1; h >>= 1) {
+            const bool upper = (lane & h) != 0;
+#pragma unroll
+            for (int k = 0; k < h; ++k) {
+                const double send = upper ? acc[k] : acc[k + h];
+                const double keep = upper ? acc[k + h] : acc[k];
+                acc[k] = keep + __shfl_xor_sync(0xffffffffu, send, h);
+            }
+        }
+        double part = acc[0];
+#pragma unroll
+        for (int o = kScanRowsPerStage; o < 32; o <<= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+        double* rd = red + (size_t)slot * kScanConsumers * kScanRowsPerStage;
+        if (lane < kScanRowsPerStage) rd[warp * kScanRowsPerStage + lane] = part;   // lane r holds row r
+        __syncwarp();
+        if (lane == 0) s_mbar_arrive(&part_bar[slot]);
+        const int owner = i % n_slab;
+        if (warp != owner) {
+            if (lane == 0) s_mbar_arrive(&empty[slot]);   // the stage's data is no longer needed
+            continue;
+        }
+        // owner: the 16 partials of each row, added in slab order
+        s_mbar_wait(&part_bar[slot], (uint32_t)(i / kScanStages) & 1);
+        uint32_t digit = 0xFFFFFFFFu;
+        if (lane < nr) {
+            double tot = 0.0;
+            for (int w = 0; w < n_slab; ++w) tot += rd[w * kScanRowsPerStage + lane];
+            const int64_t row = row0 + lane;
+            const uint32_t kk = float_key((float)tot);
+            s64[row] = tot;
+            key32[row] = kk;
+            digit = kk >> 20;
+        }
+        const unsigned peers = __match_any_sync(0xffffffffu, digit);
+        if (digit != 0xFFFFFFFFu && lane == __ffs(peers) - 1) atomicAdd(&hist_sm[digit], (uint32_t)__popc(peers));
+        __syncwarp();
+        if (lane == 0) s_mbar_arrive(&empty[slot]);
+    }
+    // every slab warp has retired its stages; merge the histogram
+    asm volatile("bar.sync 1, %0;" ::"r"(n_slab * 32) : "memory");
+    for (int i = threadIdx.x; i < kHistBins; i += n_slab * 32)
+        if (hist_sm[i]) atomicAdd(&hist12[i], hist_sm[i]);
+}
+
 void launch_sem_scan(const void* E, int e_dtype, int64_t n_rows, int d, const void* q, int q_dtype,
                      double* s64, uint32_t* key32, uint32_t* hist12, cudaStream_t st) {
     cudaMemsetAsync(hist12, 0, kHistBins * sizeof(uint32_t), st);
     const int elems = e_dtype == 0 ? 8 : 4;
     const int n_slabs = (d + 32 * elems - 1) / (32 * elems);
     const size_t smem = (size_t)n_slabs * 32 * elems * sizeof(double);
-    if (e_dtype == 0) {
+    // rows per stage RS and CTAs per SM: RS = 8, one CTA (216 KB) or RS = 4, two CTAs
+    const char* rse = getenv("EVOSPEC_SCAN_RS");
+    const int RS = rse ? atoi(rse) : kScanRS;
+    auto smem_for = [&](int rs) {
+        return (size_t)kScanStages * rs * d * 2 + kHistBins * 4 + (size_t)kScanStages * kScanConsumers * rs * 8 +
+               3 * kScanStages * 8;
+    };
+    const char* env = getenv("EVOSPEC_SCAN");
+    if (e_dtype == 0 && d % 256 == 0 && d <= 256 * kScanConsumers && smem_for(RS) <= 227 * 1024 &&
+        !(env && !strcmp(env, "v1"))) {
+        const char* pfe = getenv("EVOSPEC_SCAN_PF");
+        const int pf = pfe ? atoi(pfe) : kScanPf;
+        const int il = getenv("EVOSPEC_SCAN_IL") ? atoi(getenv("EVOSPEC_SCAN_IL")) : 1;
+        const size_t sm = smem_for(RS);
+        if (RS == 4) {
+            cudaFuncSetAttribute(sem_scan_tma_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            sem_scan_tma_kernel<4><<<2 * kNumSMs, (kScanConsumers + 1) * 32, sm, st>>>(
+                (const uint16_t*)E, n_rows, d, q, q_dtype, hist12, s64, key32, pf, il);
+        } else {
+            cudaFuncSetAttribute(sem_scan_tma_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            sem_scan_tma_kernel<8><<<kNumSMs, (kScanConsumers + 1) * 32, sm, st>>>(
+                (const uint16_t*)E, n_rows, d, q, q_dtype, hist12, s64, key32, pf, il);
+        }
+    } else if (e_dtype == 0) {
         cudaFuncSetAttribute(sem_scan_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         sem_scan_kernel<0><<<kNumSMs, kScanWarps * 32, smem, st>>>(E, n_rows, d, q, q_dtype, hist12, s64, key32);
     } else {
