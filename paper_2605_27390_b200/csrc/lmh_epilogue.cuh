@@ -28,10 +28,14 @@ namespace es {
 constexpr int kTile = 128;
 constexpr int kTileJ = kTile / 32;
 
+constexpr int kBuf = 64;   // unsorted candidate buffer per row (buffered path, KP <= 32)
+
 struct EpiSmem {
     float* tile;     // [n_h][kTile]
-    float* st_val;   // [n_h][KP]
-    int* st_pos;     // [n_h][KP]
+    float* st_val;   // [n_h][cap]  cap = KP (sorted list) or kBuf (buffered path)
+    int* st_pos;     // [n_h][cap]
+    float* st_thv;   // [n_h] buffered path: admission bound (value, position)
+    int* st_thp;     // [n_h]
     int* st_cnt;     // [n_h]
     float* st_m;     // [n_h]   running max
     float* st_ls;    // [n_h][32] per-lane partial sum of exp(z - m)
@@ -40,16 +44,18 @@ struct EpiSmem {
     int* scr_p;      // [n_warps][32]
 };
 
-__host__ __device__ inline size_t epi_smem_bytes(int n_h, int KP, int n_warps) {
-    return (size_t)n_h * kTile * 4 + (size_t)n_h * KP * 8 + (size_t)n_h * 12 + (size_t)n_h * 32 * 4 +
+__host__ __device__ inline size_t epi_smem_bytes(int n_h, int cap, int n_warps) {
+    return (size_t)n_h * kTile * 4 + (size_t)n_h * cap * 8 + (size_t)n_h * 20 + (size_t)n_h * 32 * 4 +
            (size_t)n_warps * 32 * 8;
 }
 
-ES_DEV EpiSmem epi_carve(unsigned char* p, int n_h, int KP, int n_warps) {
+ES_DEV EpiSmem epi_carve(unsigned char* p, int n_h, int cap, int n_warps) {
     EpiSmem e;
     e.tile = (float*)p;        p += (size_t)n_h * kTile * 4;
-    e.st_val = (float*)p;      p += (size_t)n_h * KP * 4;
-    e.st_pos = (int*)p;        p += (size_t)n_h * KP * 4;
+    e.st_val = (float*)p;      p += (size_t)n_h * cap * 4;
+    e.st_pos = (int*)p;        p += (size_t)n_h * cap * 4;
+    e.st_thv = (float*)p;      p += (size_t)n_h * 4;
+    e.st_thp = (int*)p;        p += (size_t)n_h * 4;
     e.st_cnt = (int*)p;        p += (size_t)n_h * 4;
     e.st_m = (float*)p;        p += (size_t)n_h * 4;
     e.st_ls = (float*)p;       p += (size_t)n_h * 32 * 4;
@@ -64,6 +70,8 @@ ES_DEV void epi_init(const EpiSmem& e, int n_h) {
         e.st_cnt[r] = 0;
         e.st_xcnt[r] = 0;
         e.st_m[r] = -INFINITY;
+        e.st_thv[r] = -INFINITY;
+        e.st_thp[r] = 0x7fffffff;
     }
     for (int i = threadIdx.x; i < n_h * 32; i += blockDim.x) e.st_ls[i] = 0.0f;
 }
@@ -351,6 +359,55 @@ ES_DEV void epi_tile_last(const EpiSmem& e, const LmhPartials& P, int cta, int n
         }
         fold_softmax(e, r, v, lm);
         const int cnt = e.st_cnt[r];
+        if (KP <= 32 && cnt == 0 && LS > KP) {
+            // the CTA's only tile: no sorted list to extend, so the values at or
+            // above theta0 = the KP-th largest lane maximum (a superset of the
+            // tile's top KP) go out unsorted when they fit the list
+            // (a tile of at most LS positions goes out whole)
+            const float th0 = tn <= LS ? -INFINITY : warp_kth_largest(lm, KP);
+            bool cand[kTileJ];
+            unsigned msk[kTileJ];
+            int total = 0;
+#pragma unroll
+            for (int j = 0; j < kTileJ; ++j) {
+                cand[j] = v[j] != -INFINITY && v[j] >= th0;
+                msk[j] = __ballot_sync(0xffffffffu, cand[j]);
+                total += __popc(msk[j]);
+            }
+            if (total <= LS) {
+                // the list maximum goes to slot 0 (the finalisation ranks list heads)
+                const float mv = warp_max(lm);
+                int i_max = 0, base = 0;
+                {
+                    int b2 = 0;
+                    bool found = false;
+#pragma unroll
+                    for (int j = 0; j < kTileJ; ++j) {
+                        const unsigned hm = __ballot_sync(0xffffffffu, cand[j] && v[j] == mv);
+                        if (!found && hm) {
+                            const int ln = __ffs(hm) - 1;
+                            i_max = b2 + __popc(msk[j] & ((1u << ln) - 1u));
+                            found = true;
+                        }
+                        b2 += __popc(msk[j]);
+                    }
+                }
+                const size_t o = ((size_t)cta * n_h_total + h_row0 + r);
+#pragma unroll
+                for (int j = 0; j < kTileJ; ++j) {
+                    if (cand[j]) {
+                        int idx = base + __popc(msk[j] & ((1u << lane) - 1u));
+                        idx = idx == i_max ? 0 : (idx == 0 ? i_max : idx);
+                        P.val[o * LS + idx] = v[j];
+                        P.id[o * LS + idx] = base_pos + lane + 32 * j;
+                    }
+                    base += __popc(msk[j]);
+                }
+                if (lane == 0) e.st_xcnt[r] = total;
+                __syncwarp();
+                continue;
+            }
+        }
         if (KP > 32 || cnt < KP) {
             if (KP <= 32) fold_topk32(e, r, KP, tn, base_pos, warp, v, lm);
             else if (KP <= 64) fold_row<2>(e, r, KP, tn, base_pos);
@@ -385,6 +442,199 @@ ES_DEV void epi_tile_last(const EpiSmem& e, const LmhPartials& P, int cta, int n
         }
         if (lane == 0) e.st_xcnt[r] = total;
         __syncwarp();
+    }
+}
+
+
+// ---------------------------------------------------------------- buffered path
+// KP <= 32 on the tensor-core kernel: no sorted list per row, but an unsorted
+// buffer of at most kBuf (position, value) candidates and an admission bound
+// (thv, thp): an element that is not before(thv, thp) under (value desc,
+// position asc) cannot be among the CTA's best KP. The buffer always holds a
+// superset of the CTA's best KP seen so far, and the finalisation selects from
+// the flat lists exactly. Per tile and row the work is a ballot and an append;
+// only the first tile pays a bound (the KP-th largest of the 32 lane maxima:
+// KP distinct values at or above it), and only an overflowing buffer pays an
+// exact rank-by-count compaction to its best KP (sorted; the bound becomes the
+// KP-th entry).
+// The buffer's best KP, sorted, into slots [0, KP) (cnt <= kBuf = 64): bitonic
+// sort of each 32-slot half, one bitonic merge; returns the new bound.
+ES_DEV void buf_compact_sorted(float* bv, int* bp, int cnt, int KP, float& thv, int& thp) {
+    const int lane = lane_id();
+    float x0 = lane < cnt ? bv[lane] : -INFINITY;
+    int q0 = lane < cnt ? bp[lane] : 0x7fffffff;
+    warp_sort32(x0, q0);
+    if (cnt > 32) {
+        float x1 = lane + 32 < cnt ? bv[lane + 32] : -INFINITY;
+        int q1 = lane + 32 < cnt ? bp[lane + 32] : 0x7fffffff;
+        warp_sort32(x1, q1);
+        const float rv = __shfl_sync(0xffffffffu, x1, 31 - lane);
+        const int rp = __shfl_sync(0xffffffffu, q1, 31 - lane);
+        if (before(rv, rp, x0, q0)) { x0 = rv; q0 = rp; }
+#pragma unroll
+        for (int j = 16; j > 0; j >>= 1) {
+            const float ov = __shfl_xor_sync(0xffffffffu, x0, j);
+            const int op = __shfl_xor_sync(0xffffffffu, q0, j);
+            if (((lane & j) == 0) == before(ov, op, x0, q0)) { x0 = ov; q0 = op; }
+        }
+    }
+    __syncwarp();
+    if (lane < KP) { bv[lane] = x0; bp[lane] = q0; }
+    thv = __shfl_sync(0xffffffffu, x0, KP - 1);
+    thp = __shfl_sync(0xffffffffu, q0, KP - 1);
+    __syncwarp();
+}
+
+ES_DEV void fold_buf(const EpiSmem& e, int r, int KP, int tn, int base_pos, const float (&v)[kTileJ], float lm,
+                     bool tighten, float* scr_v, int* scr_p) {
+    const int lane = lane_id();
+    int cnt = e.st_cnt[r];
+    float thv = e.st_thv[r];
+    int thp = e.st_thp[r];
+    if (cnt == 0 && thv == -INFINITY) {
+        const float t0 = warp_kth_largest(lm, KP);
+        if (t0 > -INFINITY) { thv = t0; thp = 0x7fffffff; }
+    }
+    if (__any_sync(0xffffffffu, lm >= thv)) {
+        bool cand[kTileJ];
+        unsigned msk[kTileJ];
+        int c = 0;
+#pragma unroll
+        for (int j = 0; j < kTileJ; ++j) {
+            const int pj = base_pos + lane + 32 * j;
+            cand[j] = v[j] != -INFINITY && before(v[j], pj, thv, thp);
+            msk[j] = __ballot_sync(0xffffffffu, cand[j]);
+            c += __popc(msk[j]);
+        }
+        float* bv = e.st_val + (size_t)r * kBuf;
+        int* bp = e.st_pos + (size_t)r * kBuf;
+        if (cnt + c > kBuf && cnt > KP) {
+            // make room: the buffer's best KP, then re-admit against the tighter bound
+            buf_compact_sorted(bv, bp, cnt, KP, thv, thp);
+            cnt = KP;
+            c = 0;
+#pragma unroll
+            for (int j = 0; j < kTileJ; ++j) {
+                cand[j] = cand[j] && before(v[j], base_pos + lane + 32 * j, thv, thp);
+                msk[j] = __ballot_sync(0xffffffffu, cand[j]);
+                c += __popc(msk[j]);
+            }
+        }
+        if (cnt + c <= kBuf) {
+            int base = cnt;
+#pragma unroll
+            for (int j = 0; j < kTileJ; ++j) {
+                if (cand[j]) {
+                    const int idx = base + __popc(msk[j] & ((1u << lane) - 1u));
+                    bv[idx] = v[j];
+                    bp[idx] = base_pos + lane + 32 * j;
+                }
+                base += __popc(msk[j]);
+            }
+            cnt += c;
+        } else if (c > 0) {
+            // more than kBuf - KP candidates against a buffer of at most KP: the sorted
+            // buffer becomes a register list and the candidates are merged into it in
+            // sorted batches of 32 (warp scratch), keeping the best 32
+            float Lv = lane < cnt ? bv[lane] : -INFINITY;
+            int Lp = lane < cnt ? bp[lane] : 0x7fffffff;
+            warp_sort32(Lv, Lp);
+            for (int done = 0; done < c; done += 32) {
+                int base = 0;
+#pragma unroll
+                for (int j = 0; j < kTileJ; ++j) {
+                    const int idx = base + __popc(msk[j] & ((1u << lane) - 1u)) - done;
+                    if (cand[j] && idx >= 0 && idx < 32) { scr_v[idx] = v[j]; scr_p[idx] = base_pos + lane + 32 * j; }
+                    base += __popc(msk[j]);
+                }
+                __syncwarp();
+                const int nb = min(32, c - done);
+                float xv = lane < nb ? scr_v[lane] : -INFINITY;
+                int xp = lane < nb ? scr_p[lane] : 0x7fffffff;
+                __syncwarp();
+                warp_sort32(xv, xp);
+                const float rv = __shfl_sync(0xffffffffu, xv, 31 - lane);
+                const int rp = __shfl_sync(0xffffffffu, xp, 31 - lane);
+                if (before(rv, rp, Lv, Lp)) { Lv = rv; Lp = rp; }
+#pragma unroll
+                for (int j = 16; j > 0; j >>= 1) {
+                    const float ov = __shfl_xor_sync(0xffffffffu, Lv, j);
+                    const int op = __shfl_xor_sync(0xffffffffu, Lp, j);
+                    if (((lane & j) == 0) == before(ov, op, Lv, Lp)) { Lv = ov; Lp = op; }
+                }
+            }
+            if (lane < KP) { bv[lane] = Lv; bp[lane] = Lp; }
+            thv = __shfl_sync(0xffffffffu, Lv, KP - 1);
+            thp = __shfl_sync(0xffffffffu, Lp, KP - 1);
+            cnt = KP;
+            __syncwarp();
+        }
+        // between tiles (the next tile still streams): tighten the bound to the
+        // CTA's current KP-th best so that later tiles admit few candidates
+        if (tighten && cnt > KP) {
+            buf_compact_sorted(bv, bp, cnt, KP, thv, thp);
+            cnt = KP;
+        }
+    }
+    __syncwarp();
+    if (lane == 0) { e.st_cnt[r] = cnt; e.st_thv[r] = thv; e.st_thp[r] = thp; }
+    __syncwarp();
+}
+
+ES_DEV void epi_tile_buf(const EpiSmem& e, int n_h, int KP, int tn, int base_pos, int warp, int n_warps,
+                         bool tighten) {
+    if (tn <= 0) return;
+    const int lane = lane_id();
+    for (int r = warp; r < n_h; r += n_warps) {
+        float v[kTileJ];
+        float lm = -INFINITY;
+#pragma unroll
+        for (int j = 0; j < kTileJ; ++j) {
+            const int p = lane + 32 * j;
+            v[j] = p < tn ? e.tile[r * kTile + p] : -INFINITY;
+            lm = fmaxf(lm, v[j]);
+        }
+        fold_softmax(e, r, v, lm);
+        fold_buf(e, r, KP, tn, base_pos, v, lm, tighten, e.scr_v + warp * 32, e.scr_p + warp * 32);
+    }
+}
+
+// Buffered path store: the row's list is kBuf slots, all "extras" (cnt = 0),
+// the buffer maximum in slot 0 (the finalisation ranks list heads), -inf pads.
+ES_DEV void epi_store_buf(const EpiSmem& e, const LmhPartials& P, int cta, int n_h_total, int h_row0, int n_h,
+                          int warp, int n_warps) {
+    const int lane = lane_id();
+    for (int r = warp; r < n_h; r += n_warps) {
+        const int cnt = e.st_cnt[r];
+        const size_t o = ((size_t)cta * n_h_total + h_row0 + r);
+        float x0 = lane < cnt ? e.st_val[(size_t)r * kBuf + lane] : -INFINITY;
+        float x1 = lane + 32 < cnt ? e.st_val[(size_t)r * kBuf + lane + 32] : -INFINITY;
+        int p0 = lane < cnt ? e.st_pos[(size_t)r * kBuf + lane] : 0;
+        int p1 = lane + 32 < cnt ? e.st_pos[(size_t)r * kBuf + lane + 32] : 0;
+        // slot of the maximum -> 0
+        float mv = fmaxf(x0, x1);
+        int ms = x0 >= x1 ? lane : lane + 32;
+        warp_argbest(mv, ms);   // (value desc, slot asc)
+        if (cnt > 0 && ms != 0) {
+            const float sv = __shfl_sync(0xffffffffu, x0, 0);
+            const int sp = __shfl_sync(0xffffffffu, p0, 0);
+            const float mxv = __shfl_sync(0xffffffffu, ms < 32 ? x0 : x1, ms & 31);
+            const int mxp = __shfl_sync(0xffffffffu, ms < 32 ? p0 : p1, ms & 31);
+            if (lane == 0) { x0 = mxv; p0 = mxp; }
+            if (ms < 32 && lane == ms) { x0 = sv; p0 = sp; }
+            if (ms >= 32 && lane == ms - 32) { x1 = sv; p1 = sp; }
+        }
+        P.val[o * kBuf + lane] = x0;
+        P.val[o * kBuf + lane + 32] = x1;
+        if (lane < cnt) P.id[o * kBuf + lane] = p0;
+        if (lane + 32 < cnt) P.id[o * kBuf + lane + 32] = p1;
+        const float ssum = warp_sum(e.st_ls[r * 32 + lane]);
+        if (lane == 0) {
+            P.cnt[o] = 0;
+            P.xcnt[o] = cnt;
+            P.m[o] = e.st_m[r];
+            P.s[o] = ssum;
+        }
     }
 }
 

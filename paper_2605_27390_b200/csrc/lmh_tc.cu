@@ -20,6 +20,7 @@
 //   warps 5-12 epilogue: tcgen05.ld 32x32b -> scale -> smem tile -> the
 //           shared online-softmax / top-k fold (lmh_epilogue.cuh) while the
 //           producers and MMA already stream the next tile.
+#include <algorithm>
 #include <cstdlib>
 
 #include <cuda.h>
@@ -45,6 +46,7 @@ constexpr int kPfBytes = 1024;     // L2 prefetch window per row (8 stages of 12
 constexpr int kPfDist = 0;         // windows ahead (0 = off: measured slower on B200, profiles/r01_trace_lmh.log)
 constexpr int kBlockK = 64;        // bf16 columns per stage = one 128-byte swizzle atom row
 constexpr int kTileM = 128;
+constexpr int kLastTile = 128;    // rows of a short last tile (128 = no split; see the launch)
 
 // ------------------------------------------------------------------ PTX
 ES_DEV uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -168,6 +170,7 @@ struct TcParams {
     int nkb;         // d / 64
     uint32_t tmem_cols;
     int pf_dist;     // L2 prefetch distance in 1 KB windows (0 = off)
+    int last_tile;   // rows of a CTA's short last tile (ranges longer than one tile)
     size_t off_b, off_epi, off_bar, off_rows;  // smem carve offsets
 };
 
@@ -197,7 +200,8 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
     }
     unsigned char* smA = base;                                   // [S][128][128 B]
     unsigned char* smB = base + tp.off_b;                        // [S][NP][128 B]
-    EpiSmem e = epi_carve(base + tp.off_epi, a.nseg > 0 ? a.seg_rows : n_h, a.KP, kTcWarps);
+    const bool buffered = a.KP <= 32 && a.LS == kBuf;   // unsorted candidate buffers (lmh_epilogue.cuh)
+    EpiSmem e = epi_carve(base + tp.off_epi, a.nseg > 0 ? a.seg_rows : n_h, buffered ? kBuf : a.KP, kTcWarps);
     uint64_t* full = (uint64_t*)(base + tp.off_bar);             // [S]
     uint64_t* empty = full + S;                                  // [S]
     uint64_t* tfull = empty + S;                                 // [2]
@@ -226,7 +230,13 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
         lmh_cta_range(a, p0, p1);
     }
     const int len = p1 - p0;
-    const int n_tiles = (len + kTileM - 1) / kTileM;
+    // tiles: the CTA's range split evenly into <= 128-row tiles, except that a
+    // range longer than one tile ends in a short tile of kLastTile rows -- only the
+    // last tile's fold is exposed (the others overlap the next tile's streaming)
+    const int last_len = len > kTileM ? min(tp.last_tile, len) : len;
+    const int body = len - last_len;
+    const int n_body = (body + kTileM - 1) / kTileM;
+    const int n_tiles = n_body + (last_len > 0 ? 1 : 0);
 
     if (warp == 0 && lane == 0) {
         asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap_w) : "memory");
@@ -248,10 +258,13 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
     if (threadIdx.x == 0) TC_TRACE(0);
 
     auto tile_range = [&](int t, int& t0, int& tn) {
-        const int a0 = p0 + (int)((long long)len * t / n_tiles);
-        const int a1 = p0 + (int)((long long)len * (t + 1) / n_tiles);
-        t0 = a0;
-        tn = a1 - a0;
+        if (t < n_body) {
+            t0 = p0 + (int)((long long)body * t / n_body);
+            tn = p0 + (int)((long long)body * (t + 1) / n_body) - t0;
+        } else {
+            t0 = p0 + body;
+            tn = last_len;
+        }
     };
 
     if (warp < kProdWarps) {
@@ -312,7 +325,8 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
                 }
                 const uint32_t dA = smem_u32(smA + (size_t)stage * kTileM * 128);
 #pragma unroll
-                for (int i = 0; i < 8; ++i) cp_async16(dA + dsto[i], src[i] + kb * 128, pol_w);
+                for (int i = 0; i < 8; ++i)   // rows past the tile's end are never read back
+                    if (16 * i + 4 * warp + (lane >> 3) < tn) cp_async16(dA + dsto[i], src[i] + kb * 128, pol_w);
                 cp_async_arrive_noinc(&full[stage]);
                 if (++stage == S) { stage = 0; phase ^= 1; }
             }
@@ -381,7 +395,8 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
                         a.logits_out[(size_t)r * a.n_subset_max + t0 + p] = e.tile[r * kTile + p];
             }
             if (t == n_tiles - 1) break;            // the last tile is folded by all warps below
-            epi_tile(e, n_h, a.KP, tn, t0, ew, kTcEpiWarps);
+            if (buffered) epi_tile_buf(e, n_h, a.KP, tn, t0, ew, kTcEpiWarps, true);
+            else epi_tile(e, n_h, a.KP, tn, t0, ew, kTcEpiWarps);
             if (ew == 0 && lane == 0 && t < 2) TC_TRACE(4 + 2 * t);
             named_bar_sync(1, nthr);
         }
@@ -392,16 +407,15 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
         int t0, tn;
         tile_range(n_tiles - 1, t0, tn);
         named_bar_sync(2, kTcWarps * 32);
-        if (n_tiles > 1)
-            epi_tile_last(e, a.part, blockIdx.x, a.n_h, h_row0, n_h, a.KP, a.LS, tn, t0, warp, kTcWarps);
-        else
-            epi_tile(e, n_h, a.KP, tn, t0, warp, kTcWarps);
+        if (buffered) epi_tile_buf(e, n_h, a.KP, tn, t0, warp, kTcWarps, false);
+        else epi_tile_last(e, a.part, blockIdx.x, a.n_h, h_row0, n_h, a.KP, a.LS, tn, t0, warp, kTcWarps);
         if (warp == kTcEpiWarp0 && lane == 0 && n_tiles - 1 < 2) TC_TRACE(4 + 2 * (n_tiles - 1));
     }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    epi_store(e, a.part, blockIdx.x, a.n_h, h_row0, n_h, a.KP, a.LS, warp, kTcWarps);
+    if (buffered) epi_store_buf(e, a.part, blockIdx.x, a.n_h, h_row0, n_h, warp, kTcWarps);
+    else epi_store(e, a.part, blockIdx.x, a.n_h, h_row0, n_h, a.KP, a.LS, warp, kTcWarps);
     if (threadIdx.x == 0) TC_TRACE(7);
     if (warp == kTcMmaWarp)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(tp.tmem_cols));
@@ -448,11 +462,13 @@ cudaError_t launch_lmh_tc(const LmhArgs& a, cudaStream_t st) {
     tp.nkb = a.d / kBlockK;
     tp.pf_dist = kPfDist;
     if (const char* e = getenv("EVOSPEC_PF")) tp.pf_dist = atoi(e);
+    tp.last_tile = kLastTile;
+    if (const char* e = getenv("EVOSPEC_LAST_TILE")) tp.last_tile = std::max(1, std::min(kTileM, atoi(e)));
     uint32_t cols = 2 * tp.n_pad, c = 32;
     while (c < cols) c <<= 1;
     tp.tmem_cols = c;
     const size_t stage_a = (size_t)kTileM * 128, stage_b = (size_t)tp.n_pad * 128;
-    const size_t epi = epi_smem_bytes(rows, a.KP, kTcWarps);
+    const size_t epi = epi_smem_bytes(rows, (a.KP <= 32 && a.LS == kBuf) ? kBuf : a.KP, kTcWarps);
     const size_t fixed = epi + 2 * 128 * 4 + 64 * 8 + 1024 /*align slack*/ + 256;
     const size_t budget = 227 * 1024;
     int S = (int)((budget - fixed) / (stage_a + stage_b));

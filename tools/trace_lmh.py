@@ -16,7 +16,8 @@ import torch
 import paper_2605_27390_b200 as es
 import synth
 
-V, d, n_h, k, n_S = 128256, 4096, 60, 10, 36864
+V, d, n_h, k = 128256, 4096, 60, 10
+n_S = int(os.environ.get("TRACE_NS", "36864"))
 W = synth.matrix(0, V, d, 0.02, "bf16")
 H = synth.matrix(1, n_h, d, 1.0, "bf16")
 Wd = torch.from_numpy(W.view(np.int16)).view(torch.bfloat16).cuda()
