@@ -45,13 +45,12 @@ def report(rep, out, rx=None):
         st = sorted([(a, float(b)) for a, b in st if b and float(b) > 0], key=lambda x: -x[1])[:8]
         lines.append("   top stall samples: " + ", ".join(f"{a}={int(b)}" for a, b in st))
         try:
-            rd = float(row[hdr.index("dram__bytes_read.sum")])
-            wr = float(row[hdr.index("dram__bytes_write.sum")])
-            u = units[hdr.index("dram__bytes_read.sum")]
-            scale = {"Mbyte": 1e6, "Gbyte": 1e9, "Kbyte": 1e3, "byte": 1.0}.get(u, 1e6)
+            sc = {"Mbyte": 1e6, "Gbyte": 1e9, "Kbyte": 1e3, "byte": 1.0}
+            rd = float(row[hdr.index("dram__bytes_read.sum")]) * sc.get(units[hdr.index("dram__bytes_read.sum")], 1e6)
+            wr = float(row[hdr.index("dram__bytes_write.sum")]) * sc.get(units[hdr.index("dram__bytes_write.sum")], 1e6)
             key = "lmh" if "lmh_tc" in name else ("scan" if "sem_scan" in name else None)
             if key:
-                traffic[key] = (rd + wr) * scale
+                traffic[key] = rd + wr   # bytes per launch (read + write)
         except (ValueError, IndexError):
             pass
     open(out, "w").write("\n".join(lines) + "\n")
@@ -72,12 +71,16 @@ def launches(csv_path, out):
         if len(r) < len(hdr):
             continue
         agg[r[idx["Kernel Name"]][:70]].append(float(r[idx["Metric Value"]]) / 1e3)
-    tot = sum(sum(v) / len(v) for v in agg.values())
-    lines = ["kernel launches (ncu gpu__time_duration.sum, cold-cache, serialised): mean us per launch, share of one step",
+    setup = [k for k in agg if "rownorm_max" in k]       # once per weight tensor, not per step
+    steps = max(len(v) for k, v in agg.items() if k not in setup)
+    tot = sum(sum(v) for k, v in agg.items() if k not in setup) / steps
+    lines = ["kernel launches (ncu gpu__time_duration.sum, cold-cache, serialised): launches captured, mean us per",
+             "launch, share of one step (setup kernels listed, excluded from the shares)",
              f"{'n':>4s} {'mean_us':>9s} {'share':>6s}  kernel"]
-    for k, v in sorted(agg.items(), key=lambda kv: -sum(kv[1]) / len(kv[1])):
+    for k, v in sorted(agg.items(), key=lambda kv: -sum(kv[1])):
         m = sum(v) / len(v)
-        lines.append(f"{len(v):4d} {m:9.1f} {m / tot:6.1%}  {k}")
+        share = "setup" if k in setup else f"{sum(v) / steps / tot:6.1%}"
+        lines.append(f"{len(v):4d} {m:9.1f} {share:>6s}  {k}")
     open(out, "w").write("\n".join(lines) + "\n")
 
 
