@@ -276,6 +276,11 @@ def run_ours(args):
     bt = None
     if world == 1 and not args.no_bt:
         bt = batched_bt(Wd, V, d, k, dev, args)
+    extra = None
+    if world == 1 and not args.no_extra:
+        del Wd
+        torch.cuda.empty_cache()
+        extra = dict(qwen_topic_segment=qwen_segment(dev, args), sharded_d8192_r1=sharded_sweep(dev, args))
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -323,7 +328,7 @@ def run_ours(args):
                          d2h_bytes_per_step=d2h),
                 gpu_launches=launches, clocks=clk, breakdown=breakdown, device_flags=flags,
                 lmh_tokens_per_s=n_h / (per["lmh"] + per["finalize"] + per["merge"]) * 1e3 if per["lmh"] else None,
-                subset_sweep=sweep, batched=bt)
+                subset_sweep=sweep, batched=bt, extra_configs=extra)
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -353,16 +358,16 @@ def batched_bt(Wd, V, d, k, dev, args):
     ctx.prepare_weights(Wd)
     sd, dd, od = (torch.from_numpy(x).to(dev) for x in (static, dyn, d_off))
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
-    times, out = [], None
+    evs, out = [], None
     for it in range(args.warmup + args.sweep_steps):
         flush.fill_(it & 0xFF)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         out = ctx.subset_logits_topk_ragged(Wd, Hd, h_off, sd, dd, od, int(sizes.max()), k, out=out)
         e1.record()
-        torch.cuda.synchronize()
-        if it >= args.warmup:
-            times.append(e0.elapsed_time(e1))
+        evs.append((e0, e1))
+    torch.cuda.synchronize()
+    times = [a.elapsed_time(b) for a, b in evs[args.warmup:]]
     t = statistics.median(times) * 1e-3
     distinct = 32768 + np.unique(dyn).size
     nbytes = distinct * d * 2 + H.nbytes
@@ -372,6 +377,88 @@ def batched_bt(Wd, V, d, k, dev, args):
                 us=t * 1e6, tokens_per_s=B * n_b / t, alg_bytes_distinct=int(nbytes),
                 GBps_distinct=nbytes / t / 1e9, bytes_streamed_min=int(streamed),
                 frac_of_copy_peak_distinct=nbytes / t / 1e9 / load_peaks()["hbm_gbs"], flags=ctx.get_flags())
+
+
+def qwen_segment(dev, args):
+    """Config Q: Qwen2.5-7B head shapes (V=152064, d=3584), 3 domain
+    hot blocks of 4096 ids shifted along a domain mean; the query of a
+    segment is mu_dom + 0.5 xi, the domain switches every segment. One segment =
+    1 subset rebuild (build_subset) + 64 LM-head calls (n_H = 60, k = 10) on the
+    rebuilt subset, the rebuild cost included. Device-timed per segment."""
+    import torch
+    import paper_2605_27390_b200 as es
+    c = synth.CONFIGS["qwen"]
+    V, d, n_h, k = c["V"], c["d"], c["n_h"], c["k"]
+    W, mus, _ = synth.domain_matrix(30, V, d, 0.02, 3, 4096, 0.5, "bf16")
+    Wd = torch.from_numpy(W.view(np.int16)).view(torch.bfloat16).to(dev)
+    del W
+    H = synth.matrix(31, n_h, d, 1.0, "bf16")
+    Hd = torch.from_numpy(H.view(np.int16)).view(torch.bfloat16).to(dev)
+    rng = np.random.default_rng(32)
+    qs = [synth.bf16_bits((mus[j % 3] + 0.5 * rng.standard_normal(d)).astype(np.float32)) for j in range(6)]
+    static = synth.static_ids(33, V, c["n_static"])
+    rp, col, _ = synth.csr_graph(34, V, c["avg_deg"])
+    seeds = synth.seed_ids(35, V, c["n_seed"])
+    ctx = es.Context(V=V, d=d, w_dtype=torch.bfloat16, h_dtype=torch.bfloat16, max_subset=V, max_rows=n_h,
+                     max_k=k, max_sem=c["n_sem"], max_seeds=32)
+    ctx.prepare_weights(Wd)
+    t = lambda a: torch.from_numpy(a.view(np.int16) if a.dtype == np.uint16 else a).to(dev)
+    sd, rpd, cold, seedd = t(static), t(rp), t(col), t(seeds)
+    qd = [torch.from_numpy(q.view(np.int16)).view(torch.bfloat16).to(dev) for q in qs]
+    nmax = c["n_static"] + c["n_dyn"]
+    evs, trip = [], None
+    for seg in range(6):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        ids, n, _, _ = ctx.build_subset(Wd, qd[seg], sd, seedd, rpd, cold, n_sem=c["n_sem"], n_dyn=c["n_dyn"])
+        for _ in range(64):
+            trip = ctx.subset_logits_topk(Wd, Hd, ids, n, nmax, k, out=trip)
+        e1.record()
+        evs.append((e0, e1))
+    torch.cuda.synchronize()
+    ms = statistics.median([a.elapsed_time(b) for a, b in evs[2:]])
+    return dict(workload="Q: V=152064 d=3584, 3 domains, segment = 1 rebuild + 64 LM-head calls (n_H=60, k=10)",
+                ms_per_segment=ms, tokens_per_s=64 * n_h / (ms * 1e-3), flags=ctx.get_flags())
+
+
+def sharded_sweep(dev, args):
+    """Config Sh at R = 1 (one GPU here): d = 8192, V = 128256, LM head + top-k
+    (subset_logits_topk; at R = 1 the shard merge is the identity) vs subset size,
+    L2 flushed, iterations enqueued back to back."""
+    import torch
+    import paper_2605_27390_b200 as es
+    V, d, n_h, k = 128256, 8192, 60, 10
+    W = synth.matrix(40, V, d, 0.02, "bf16")
+    Wd = torch.from_numpy(W.view(np.int16)).view(torch.bfloat16).to(dev)
+    del W
+    H = synth.matrix(41, n_h, d, 1.0, "bf16")
+    Hd = torch.from_numpy(H.view(np.int16)).view(torch.bfloat16).to(dev)
+    ctx = es.Context(V=V, d=d, w_dtype=torch.bfloat16, h_dtype=torch.bfloat16, max_subset=V, max_rows=n_h,
+                     max_k=k, max_sem=1, max_seeds=1)
+    ctx.prepare_weights(Wd)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    rng = np.random.default_rng(42)
+    out = []
+    for n_S in (8192, 16384, 32768, 65536, V):
+        S = np.sort(rng.permutation(V)[:n_S]).astype(np.int32)
+        Sd = torch.from_numpy(S).to(dev)
+        nd = torch.tensor([n_S], dtype=torch.int32, device=dev)
+        evs, trip = [], None
+        for it in range(args.warmup + args.sweep_steps):
+            flush.fill_(it & 0xFF)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            trip = ctx.subset_logits_topk(Wd, Hd, Sd, nd, n_S, k, out=trip)
+            e1.record()
+            evs.append((e0, e1))
+        torch.cuda.synchronize()
+        t = statistics.median([a.elapsed_time(b) for a, b in evs[args.warmup:]]) * 1e-3
+        nbytes = n_S * d * 2 + n_h * d * 2 + n_S * 4
+        out.append(dict(n_S=n_S, us=t * 1e6, tokens_per_s=n_h / t, GBps=nbytes / t / 1e9,
+                        frac_of_copy_peak=nbytes / t / 1e9 / load_peaks()["hbm_gbs"]))
+    del flush
+    return dict(workload="Sh at R=1: V=128256 d=8192 n_H=60 k=10 (R>1 needs more GPUs than this run has)",
+                sweep=out, flags=ctx.get_flags())
 
 
 def subset_sweep(ctx, Wd, Hd, n_h, k, V, d, dev, args):
@@ -388,7 +475,9 @@ def subset_sweep(ctx, Wd, Hd, n_h, k, V, d, dev, args):
         Sd = torch.from_numpy(S).to(dev)
         nd = torch.tensor([n_S], dtype=torch.int32, device=dev)
         trip = None
-        times = []
+        evs = []
+        # iterations are enqueued back to back (the 256 MB flush between them keeps
+        # the host ahead of the GPU), so the events time the device, not the launch
         for it in range(args.warmup + args.sweep_steps):
             flush.fill_(it & 0xFF)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -396,9 +485,9 @@ def subset_sweep(ctx, Wd, Hd, n_h, k, V, d, dev, args):
             trip = ctx.subset_logits_topk(Wd, Hd, Sd, nd, n_S, k, out=trip)
             ctx.merge_shards(*trip, n_h=n_h, k=k)
             e1.record()
-            torch.cuda.synchronize()
-            if it >= args.warmup:
-                times.append(e0.elapsed_time(e1))
+            evs.append((e0, e1))
+        torch.cuda.synchronize()
+        times = [a.elapsed_time(b) for a, b in evs[args.warmup:]]
         t = statistics.median(times) * 1e-3
         nbytes = n_S * d * 2 + n_h * d * 2 + n_S * 4
         out.append(dict(n_S=n_S, us=t * 1e6, tokens_per_s=n_h / t, GBps=nbytes / t / 1e9,
@@ -416,6 +505,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-bt", action="store_true", help="skip the batched (config Bt) ragged LM-head line")
+    ap.add_argument("--no-extra", action="store_true", help="skip the Q topic-segment and Sh d=8192 lines")
     ap.add_argument("--sweep-steps", type=int, default=10)
     args = ap.parse_args()
     if args.warmup < 3:
