@@ -663,11 +663,15 @@ void launch_lmh_finalize(const LmhArgs& a, int n_cta, int k, const float* wmax_d
         // a placement hint: two CTAs sharing an SM measured slower); more rows pack
         const size_t smem = a.n_h <= kNumSMs ? 120 * 1024 : 0;
         if (n_cta * (kFin32LS / 4) <= 5 * kFin32Threads) {
-            cudaFuncSetAttribute(lmh_finalize32_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            static thread_local bool set5 = false;   // (placement hint size is fixed)
+            if (!set5) set5 = cudaFuncSetAttribute(lmh_finalize32_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   120 * 1024) == cudaSuccess;
             launch_pdl(lmh_finalize32_kernel<5>, dim3(a.n_h), dim3(kFin32Threads), smem, st, a, n_cta, k, gamma,
                        wmax_dev, topk_ids, topk_vals, row_max, row_sumexp, flags);
         } else {
-            cudaFuncSetAttribute(lmh_finalize32_kernel<10>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            static thread_local bool set10 = false;
+            if (!set10) set10 = cudaFuncSetAttribute(lmh_finalize32_kernel<10>,
+                                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 120 * 1024) == cudaSuccess;
             launch_pdl(lmh_finalize32_kernel<10>, dim3(a.n_h), dim3(kFin32Threads), smem, st, a, n_cta, k, gamma,
                        wmax_dev, topk_ids, topk_vals, row_max, row_sumexp, flags);
         }

@@ -239,7 +239,6 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
     const int n_tiles = n_body + (last_len > 0 ? 1 : 0);
 
     if (warp == 0 && lane == 0) {
-        asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap_w) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap_h) : "memory");
         for (int s = 0; s < S; ++s) { mbar_init(&full[s], kProdWarps * 32 + 1); mbar_init(&empty[s], 1); }
         for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], kTcEpiWarps * 32); }
@@ -447,6 +446,41 @@ static bool make_map(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t o
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// Encoded tensor maps, cached per thread by (pointer, shape, box): encoding costs
+// host time on every call otherwise (the LM head is a per-draft-step launch).
+static bool cached_map(CUtensorMap* out, const void* ptr, uint64_t inner, uint64_t outer, uint32_t box0,
+                       uint32_t box1, CUtensorMapL2promotion prom) {
+    struct Entry { const void* ptr; uint64_t inner, outer; uint32_t b0, b1; int prom; CUtensorMap m; };
+    thread_local Entry cache[8];
+    thread_local int n = 0, next = 0;
+    for (int i = 0; i < n; ++i) {
+        const Entry& c = cache[i];
+        if (c.ptr == ptr && c.inner == inner && c.outer == outer && c.b0 == box0 && c.b1 == box1 && c.prom == (int)prom) {
+            *out = c.m;
+            return true;
+        }
+    }
+    Entry e{ptr, inner, outer, box0, box1, (int)prom, {}};
+    if (!make_map(&e.m, ptr, inner, outer, box0, box1, prom)) return false;
+    cache[next] = e;
+    next = (next + 1) % 8;
+    n = n < 8 ? n + 1 : 8;
+    *out = e.m;
+    return true;
+}
+
+// cudaFuncSetAttribute once per device and size (not on every launch)
+template <typename K>
+static cudaError_t ensure_smem(K kern, size_t smem) {
+    thread_local int done[16] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 16 && done[dev] >= (int)smem) return cudaSuccess;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess && dev < 16) done[dev] = (int)smem;
+    return e;
+}
+
 int lmh_tc_grid() { return kNumSMs; }
 
 bool lmh_tc_supported(const LmhArgs& a) {
@@ -473,6 +507,7 @@ cudaError_t launch_lmh_tc(const LmhArgs& a, cudaStream_t st) {
     const size_t budget = 227 * 1024;
     int S = (int)((budget - fixed) / (stage_a + stage_b));
     S = std::min(S, 8);
+    if (const char* e = getenv("EVOSPEC_STAGES")) S = std::max(2, std::min(S, atoi(e)));
     if (S < 2) return cudaErrorInvalidConfiguration;
     tp.stages = S;
     tp.off_b = (size_t)S * stage_a;
@@ -480,13 +515,11 @@ cudaError_t launch_lmh_tc(const LmhArgs& a, cudaStream_t st) {
     tp.off_bar = (tp.off_epi + epi + 15) & ~(size_t)15;
     tp.off_rows = tp.off_bar + (size_t)(2 * S + 4) * 8 + 16;
     const size_t smem = tp.off_rows + 2 * 128 * 4 + 1024;
-    CUtensorMap mw, mh;
-    if (!make_map(&mw, a.W, (uint64_t)a.d, (uint64_t)a.n_w_rows, kBlockK, 1, CU_TENSOR_MAP_L2_PROMOTION_L2_256B))
+    CUtensorMap mw{}, mh;   // W rows are gathered by cp.async: no W map is needed
+    if (!cached_map(&mh, a.H, (uint64_t)a.d, (uint64_t)a.n_h, kBlockK, (uint32_t)tp.n_pad,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_128B))
         return cudaErrorInvalidValue;
-    if (!make_map(&mh, a.H, (uint64_t)a.d, (uint64_t)a.n_h, kBlockK, (uint32_t)tp.n_pad,
-                  CU_TENSOR_MAP_L2_PROMOTION_L2_128B))
-        return cudaErrorInvalidValue;
-    cudaError_t e = cudaFuncSetAttribute(lmh_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = ensure_smem(lmh_tc_kernel, smem);
     if (e != cudaSuccess) return e;
     return launch_pdl(lmh_tc_kernel, dim3(lmh_tc_grid()), dim3(kTcWarps * 32), smem, st, mw, mh, a, tp);
 }

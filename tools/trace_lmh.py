@@ -32,15 +32,16 @@ flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 names = ["start", "prod_done", "mma_done", "t0_ready", "t0_fold", "t1_ready", "t1_fold", "end"]
 for pf in (sys.argv[1:] or ["2"]):
     os.environ["EVOSPEC_PF"] = pf
-    times = []
+    evs = []
     for it in range(8):
         flush.fill_(it)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         ctx.subset_logits_topk(Wd, Hd, Sd, nd, n_S, k)
         e1.record()
-        torch.cuda.synchronize()
-        times.append(e0.elapsed_time(e1) * 1e3)
+        evs.append((e0, e1))
+    torch.cuda.synchronize()
+    times = [a.elapsed_time(b) * 1e3 for a, b in evs]
     full = ctx.read_trace(296 * 8).astype(np.float64).reshape(296, 8)
     tr = full[:148]
     fin = full[148:148 + n_h]
