@@ -448,7 +448,7 @@ def sharded_sweep(dev, args):
             flush.fill_(it & 0xFF)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-            trip = ctx.subset_logits_topk(Wd, Hd, Sd, nd, n_S, k, out=trip)
+            trip = ctx.subset_logits_topk_merged(Wd, Hd, Sd, nd, n_S, k, out=trip)
             e1.record()
             evs.append((e0, e1))
         torch.cuda.synchronize()
@@ -463,7 +463,8 @@ def sharded_sweep(dev, args):
 
 def subset_sweep(ctx, Wd, Hd, n_h, k, V, d, dev, args):
     """Draft LM-head tokens/s and HBM GB/s vs subset size (the metric's x-axis):
-    subset_logits_topk + merge_shards on a seeded sorted subset of n_S ids,
+    LM head + softmax + top-k + merge (R = 1: subset_logits_topk_merged, the merge
+    fused into the finalisation) on a seeded sorted subset of n_S ids,
     L2 flushed (256 MB write) before every timed iteration, CUDA events around
     the LM-head calls only."""
     import torch
@@ -482,8 +483,8 @@ def subset_sweep(ctx, Wd, Hd, n_h, k, V, d, dev, args):
             flush.fill_(it & 0xFF)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-            trip = ctx.subset_logits_topk(Wd, Hd, Sd, nd, n_S, k, out=trip)
-            ctx.merge_shards(*trip, n_h=n_h, k=k)
+            # R = 1: the shard merge (LSE, probabilities) is fused into the finalisation
+            trip = ctx.subset_logits_topk_merged(Wd, Hd, Sd, nd, n_S, k, out=trip)
             e1.record()
             evs.append((e0, e1))
         torch.cuda.synchronize()

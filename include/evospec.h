@@ -206,6 +206,21 @@ evospec_status evospec_subset_logits_topk(evospec_ctx *ctx,
     int32_t *topk_ids, float *topk_vals, float *row_max, float *row_sumexp,
     float *logits_out, void *stream);
 
+/* Single-shard LM head with the merge fused (R = 1): the same projection,
+ * softmax and exact top-k as evospec_subset_logits_topk, and the outputs of
+ * evospec_merge_shards at R = 1 written by the finalisation kernel itself:
+ *   out_ids [n_h, k] int32 global ids, out_vals [n_h, k] fp32 z,
+ *   out_lse [n_h] fp32 = m + ln s, out_probs [n_h, k] fp32 (may be NULL),
+ *   row_max / row_sumexp [n_h] (may be NULL) the m, s of Eq. 1.
+ * EVOSPEC_EINPUT for contexts with n_shards > 1 (use the triple + merge). */
+evospec_status evospec_subset_logits_topk_merged(evospec_ctx *ctx,
+    const void *W_local_dev, int64_t n_w_rows,
+    const void *H_dev, int32_t n_h,
+    const int32_t *subset_dev, const int32_t *n_subset_dev, int32_t n_subset_max,
+    int32_t k, float inv_temp,
+    int32_t *out_ids, float *out_vals, float *out_lse, float *out_probs,
+    float *row_max, float *row_sumexp, void *stream);
+
 /* Ragged batched LM head (config Bt): sequence b owns H rows
  * [h_offsets[b], h_offsets[b+1]) and the vocabulary V_b = static u dyn_b,
  * dyn_b = dyn_dev[dyn_offsets[b] : dyn_offsets[b+1]] (sorted ascending,

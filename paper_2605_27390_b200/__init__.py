@@ -27,7 +27,7 @@ EXPORTED = [
     "evospec_comm_unique_id", "evospec_comm_init", "evospec_build_subset",
     "evospec_last_semantic", "evospec_subset_logits_topk", "evospec_merge_shards",
     "evospec_draft_step", "evospec_set_timing", "evospec_read_stats", "evospec_read_trace",
-    "evospec_build_subset_batched", "evospec_subset_logits_topk_ragged",
+    "evospec_build_subset_batched", "evospec_subset_logits_topk_ragged", "evospec_subset_logits_topk_merged",
 ]
 
 STAGES = ["scan", "select", "union", "lmh", "finalize", "merge", "copy"]
@@ -106,6 +106,8 @@ def lib() -> C.CDLL:
                                               C.POINTER(BuildParams), vp, vp, vp], i32),
             "evospec_subset_logits_topk_ragged": ([vp, vp, i64, vp, vp, i32, vp, i32, vp, vp, i32, i32,
                                                    C.c_float, vp, vp, vp, vp, vp], i32),
+            "evospec_subset_logits_topk_merged": ([vp, vp, i64, vp, i32, vp, vp, i32, i32, C.c_float,
+                                                   vp, vp, vp, vp, vp, vp, vp], i32),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, name)
@@ -279,6 +281,25 @@ class Context:
             n_subset_max, k, float(inv_temp), _ptr(ids), _ptr(vals), _ptr(m), _ptr(s),
             _ptr(logits_out), _stream(stream)))
         return ids, vals, m, s
+
+    def subset_logits_topk_merged(self, W_local, H, subset, n_subset_dev, n_subset_max: int, k: int,
+                                  inv_temp: float = 1.0, out=None, stream=None):
+        """Single shard (R = 1): returns (ids, vals, lse, probs) -- merge_shards' outputs,
+        written by the LM head's finalisation."""
+        import torch
+        n_h = H.shape[0]
+        dev = H.device
+        if out is None:
+            out = (torch.empty((n_h, k), dtype=torch.int32, device=dev),
+                   torch.empty((n_h, k), dtype=torch.float32, device=dev),
+                   torch.empty(n_h, dtype=torch.float32, device=dev),
+                   torch.empty((n_h, k), dtype=torch.float32, device=dev))
+        ids, vals, lse, probs = out
+        _check(lib().evospec_subset_logits_topk_merged(
+            self._h, _ptr(W_local), W_local.shape[0], _ptr(H), n_h, _ptr(subset), _ptr(n_subset_dev),
+            n_subset_max, k, float(inv_temp), _ptr(ids), _ptr(vals), _ptr(lse), _ptr(probs), None, None,
+            _stream(stream)))
+        return ids, vals, lse, probs
 
     def subset_logits_topk_ragged(self, W_local, H, h_offsets, static_ids, dyn_ids, dyn_offsets, max_dyn: int,
                                   k: int, inv_temp: float = 1.0, out=None, stream=None):

@@ -579,6 +579,22 @@ evospec_status evospec_subset_logits_topk(evospec_ctx* ctx, const void* W, int64
                     row_max, row_sumexp, logits_out, stream, nullptr, nullptr, nullptr, nullptr);
 }
 
+evospec_status evospec_subset_logits_topk_merged(evospec_ctx* ctx, const void* W, int64_t n_w_rows, const void* H,
+                                                 int32_t n_h, const int32_t* subset, const int32_t* n_subset_dev,
+                                                 int32_t n_subset_max, int32_t k, float inv_temp, int32_t* out_ids,
+                                                 float* out_vals, float* out_lse, float* out_probs, float* row_max,
+                                                 float* row_sumexp, void* stream) {
+    if (!ctx) return fail(EVOSPEC_EINPUT, "subset_logits_topk_merged: null context");
+    if (ctx->cfg.n_shards != 1)
+        return fail(EVOSPEC_EINPUT, "subset_logits_topk_merged: single-shard contexts only (R = %d)", ctx->cfg.n_shards);
+    if (!out_ids || !out_vals || !out_lse) return fail(EVOSPEC_EINPUT, "subset_logits_topk_merged: null output");
+    int32_t* tids = ctx->g_ids;   // the shard triple lands in the workspace; the outputs are the merged ones
+    float* tvals = ctx->g_vals;
+    return lmh_impl(ctx, W, n_w_rows, H, n_h, subset, n_subset_dev, n_subset_max, k, inv_temp, tids, tvals,
+                    row_max ? row_max : ctx->g_m, row_sumexp ? row_sumexp : ctx->g_s, nullptr, stream, out_ids,
+                    out_vals, out_lse, out_probs);
+}
+
 __global__ void set2_kernel(int32_t* p, int32_t a, int32_t b) { p[0] = a; p[1] = b; }
 
 evospec_status evospec_subset_logits_topk_ragged(evospec_ctx* ctx, const void* W, int64_t n_w_rows, const void* H,

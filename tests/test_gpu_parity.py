@@ -386,3 +386,24 @@ def test_batched_full_size_sampled():
         S_b = np.union1d(R["static"], R["dyn"][R["d_off"][b]:R["d_off"][b + 1]]).astype(np.int32)
         ref = oracle.subset_logits_topk(R["W"], R["H"][h0:h1], S_b, R["k"])
         G.assert_triple_close(ids[h0:h1], vals[h0:h1], m[h0:h1], s[h0:h1], ref, R["k"])
+
+
+def test_merged_single_shard_equals_oracle():
+    """evospec_subset_logits_topk_merged (R = 1: merge fused into the finalisation)
+    returns merge_shards' outputs: ids exact, LSE and probabilities within tolerance."""
+    P = G.make_problem(70, dtype="bf16", V=30000, d=256, n_static=3000, n_sem=500, n_dyn=700, n_h=12, k=10)
+    ref = G.oracle_step(oracle, P)
+    S = ref["S"]
+    ctx = ctx_for(P)
+    W = G.to_dev(P["W"], DEV)
+    ctx.prepare_weights(W)
+    Sd = G.to_dev(S, DEV)
+    nd = torch.tensor([S.size], dtype=torch.int32, device=DEV)
+    ids, vals, lse, probs = ctx.subset_logits_topk_merged(W, G.to_dev(P["H"], DEV), Sd, nd, S.size, P["k"])
+    torch.cuda.synchronize()
+    t = ref["triple"]
+    np.testing.assert_array_equal(ids.cpu().numpy(), t["ids"])
+    assert np.all(np.abs(lse.cpu().numpy() - t["lse"]) <= G.LOGIT_TOL * (1 + np.abs(t["lse"])))
+    assert np.max(np.abs(probs.cpu().numpy() - t["probs"])) <= G.PROB_TOL
+    assert np.all(np.abs(vals.cpu().numpy() - t["vals"]) <= G.LOGIT_TOL * (1 + np.abs(t["vals"])))
+    assert ctx.get_flags() == 0
