@@ -155,7 +155,6 @@ sem_scan_kernel(const void* __restrict__ E, int64_t n_rows, int d,
 //   adds the partials of each row in slab order and writes s64 / key32 / the
 //   histogram, then frees the stage (the others free it right after their
 //   partials are written).
-constexpr int kScanStages = 3;
 constexpr int kScanConsumers = 16;
 constexpr int kScanRS = 8;          // rows per ring stage (8: one CTA per SM; 4 + two CTAs measured slower)
 constexpr int kScanPf = 0;          // stages of L2 prefetch ahead of the ring (measured slower: off)
@@ -182,8 +181,8 @@ ES_DEV void s_bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar
         ::"r"(s_u32(dst)), "l"(src), "r"(bytes), "r"(s_u32(bar)), "l"(policy) : "memory");
 }
 
-template <int kScanRowsPerStage>
-__global__ void __launch_bounds__((kScanConsumers + 1) * 32, kScanRowsPerStage == 4 ? 2 : 1)
+template <int kScanRowsPerStage, int kScanStages>
+__global__ void __launch_bounds__((kScanConsumers + 1) * 32, 1)
 sem_scan_tma_kernel(const uint16_t* __restrict__ E, int64_t n_rows, int d, const void* __restrict__ q, int q_dtype,
                     uint32_t* __restrict__ hist12, double* __restrict__ s64, uint32_t* __restrict__ key32, int pf,
                     int il) {
@@ -339,24 +338,28 @@ void launch_sem_scan(const void* E, int e_dtype, int64_t n_rows, int d, const vo
     // rows per stage RS and CTAs per SM: RS = 8, one CTA (216 KB) or RS = 4, two CTAs
     const char* rse = getenv("EVOSPEC_SCAN_RS");
     const int RS = rse ? atoi(rse) : kScanRS;
-    auto smem_for = [&](int rs) {
-        return (size_t)kScanStages * rs * d * 2 + kHistBins * 4 + (size_t)kScanStages * kScanConsumers * rs * 8 +
-               3 * kScanStages * 8;
+    auto smem_for = [&](int rs, int ns) {
+        return (size_t)ns * rs * d * 2 + kHistBins * 4 + (size_t)ns * kScanConsumers * rs * 8 + 3 * ns * 8;
     };
+    const int NS = RS == 4 ? 6 : (RS == 2 ? 12 : 3);   // ~192 KB of ring at d = 4096
     const char* env = getenv("EVOSPEC_SCAN");
-    if (e_dtype == 0 && d % 256 == 0 && d <= 256 * kScanConsumers && smem_for(RS) <= 227 * 1024 &&
+    if (e_dtype == 0 && d % 256 == 0 && d <= 256 * kScanConsumers && smem_for(RS, NS) <= 227 * 1024 &&
         !(env && !strcmp(env, "v1"))) {
         const char* pfe = getenv("EVOSPEC_SCAN_PF");
         const int pf = pfe ? atoi(pfe) : kScanPf;
         const int il = getenv("EVOSPEC_SCAN_IL") ? atoi(getenv("EVOSPEC_SCAN_IL")) : 1;
-        const size_t sm = smem_for(RS);
+        const size_t sm = smem_for(RS, NS);
         if (RS == 4) {
-            cudaFuncSetAttribute(sem_scan_tma_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            sem_scan_tma_kernel<4><<<2 * kNumSMs, (kScanConsumers + 1) * 32, sm, st>>>(
+            cudaFuncSetAttribute(sem_scan_tma_kernel<4, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            sem_scan_tma_kernel<4, 6><<<kNumSMs, (kScanConsumers + 1) * 32, sm, st>>>(
+                (const uint16_t*)E, n_rows, d, q, q_dtype, hist12, s64, key32, pf, il);
+        } else if (RS == 2) {
+            cudaFuncSetAttribute(sem_scan_tma_kernel<2, 12>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            sem_scan_tma_kernel<2, 12><<<kNumSMs, (kScanConsumers + 1) * 32, sm, st>>>(
                 (const uint16_t*)E, n_rows, d, q, q_dtype, hist12, s64, key32, pf, il);
         } else {
-            cudaFuncSetAttribute(sem_scan_tma_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            sem_scan_tma_kernel<8><<<kNumSMs, (kScanConsumers + 1) * 32, sm, st>>>(
+            cudaFuncSetAttribute(sem_scan_tma_kernel<8, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            sem_scan_tma_kernel<8, 3><<<kNumSMs, (kScanConsumers + 1) * 32, sm, st>>>(
                 (const uint16_t*)E, n_rows, d, q, q_dtype, hist12, s64, key32, pf, il);
         }
     } else if (e_dtype == 0) {
