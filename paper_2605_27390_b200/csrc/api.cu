@@ -527,6 +527,9 @@ static evospec_status lmh_impl(evospec_ctx* ctx, const void* W, int64_t n_w_rows
     a.H = H; a.n_h = n_h; a.h_dtype = c.h_dtype;
     a.subset = subset; a.n_subset_dev = n_subset_dev; a.n_subset_max = n_subset_max; a.seg = seg;
     a.R = c.n_shards; a.KP = k + kTopkPad; a.LS = a.KP <= 32 ? 64 : a.KP; a.inv_temp = inv_temp;
+    // a triple that is merged with other parts (vocabulary shards, or the static /
+    // dynamic parts of the ragged head) carries exact top-k values
+    a.exact_vals = (c.n_shards > 1 || segs || seg) ? 1 : 0;
     a.logits_out = logits_out;
     a.part = ctx->part;
     a.m_ids = m_ids; a.m_vals = m_vals; a.m_lse = m_lse; a.m_probs = m_probs;

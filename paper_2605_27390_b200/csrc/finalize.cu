@@ -222,9 +222,13 @@ lmh_finalize_kernel(LmhArgs a, int n_cta, int k, float gamma, const float* __res
                 ++j;
             const bool in_topk = i < k;
             const bool multi = j > i;
-            for (int t = i; t <= j; ++t) c_need[t] = (in_topk && multi) ? 1 : 0;
-            if (in_topk && multi)
-                for (int t = i; t <= j; ++t) need_list[nn++] = t;
+            // exact_vals (the triple feeds a merge across shards / parts): every top-k entry
+            // is re-scored, so the merge compares the exact logits (rounded to fp32)
+            for (int t = i; t <= j; ++t) {
+                const bool nd = (in_topk && multi) || (a.exact_vals && t < k);
+                c_need[t] = nd ? 1 : 0;
+                if (nd) need_list[nn++] = t;
+            }
             if (in_topk && j == nk - 1 && total_s > nk && j >= k - 1) uncertain = true;
             if (!(delta >= 0.0) || isinf(delta)) uncertain = true;   // weights not prepared
             i = j + 1;
@@ -559,7 +563,10 @@ lmh_finalize32_kernel(LmhArgs a, int n_cta_arg, int k, float gamma, const float*
         const unsigned below = ~cm & ((1u << lane) - 1u);
         const int st_i = below ? 32 - __clz(below) : 0;
         const bool multi = (lane > 0 && ((cm >> (lane - 1)) & 1u)) || ((cm >> lane) & 1u);
-        const bool need = lane < cnt && multi && st_i < k;
+        // members of runs reaching the top k; with exact_vals (the triple feeds a merge
+        // across shards or across the static / dynamic parts of the ragged head) every
+        // top-k entry, so that the merge compares the exact logits (rounded to fp32)
+        const bool need = lane < cnt && ((multi && st_i < k) || (a.exact_vals && lane < k));
         const unsigned nm = __ballot_sync(0xffffffffu, need);
         if (need) need_list[__popc(nm & ((1u << lane) - 1u))] = lane;
         // uncertified: the run holding index k-1 reaches the last kept entry while entries were dropped

@@ -66,6 +66,7 @@ struct LmhArgs {
     // against subset positions [seg_pos[b], seg_pos[b+1]) (seg_pos == null: every
     // segment takes the whole subset); seg_ctas CTAs per segment, CTA c serves
     // segment c / seg_ctas (the rest idle); n_h = total rows, seg_rows = max rows
+    int exact_vals;   // re-score every top-k entry (the triple feeds a cross-part merge)
     int nseg, seg_ctas, seg_rows;
     const int32_t* seg_pos;
     const int32_t* seg_cta;   // optional device [nseg+1]: CTAs [seg_cta[b], seg_cta[b+1]) serve segment b

@@ -216,7 +216,7 @@ def lmh_path(monkeypatch):
 
 
 @pytest.mark.parametrize("path", ["tc", "gemv"])
-@pytest.mark.parametrize("n_h,k", [(5, 10), (16, 1), (60, 10), (128, 64)])
+@pytest.mark.parametrize("n_h,k", [(5, 10), (16, 1), (60, 10), (60, 24), (60, 25), (128, 64)])
 def test_lmh_paths(lmh_path, path, n_h, k):
     """Both LM-head kernels (tcgen05 and FFMA) against the oracle, same inputs."""
     lmh_path(path)
