@@ -421,6 +421,7 @@ topn_cand_kernel(const double* __restrict__ s64, const int32_t* __restrict__ ids
                  uint32_t* __restrict__ hist_g, int* __restrict__ out_count, double* __restrict__ out_s,
                  int32_t* __restrict__ out_id) {
     cg::grid_group grid = cg::this_grid();
+    pdl_trigger();   // the union kernel may start its input-only prologue (static bitmap) now
     __shared__ uint32_t hist[kHistBins];
     __shared__ uint32_t warp_sum_s[kSelThreads / 32];
     __shared__ SelState st;

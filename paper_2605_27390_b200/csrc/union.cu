@@ -276,10 +276,30 @@ union_kernel(int V, const int32_t* __restrict__ static_ids, int n_static,
 
     const int tid = threadIdx.x, lane = lane_id(), T = blockDim.x;
     pdl_trigger();
+    // 1. static members -- an input, not the predecessor's output: built before
+    //    griddepcontrol.wait, overlapping the candidate selection (8 loads in flight)
+    if (trace) { if (threadIdx.x == 0) { long long t_; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); trace[0] = t_; } }
+    for (int w = tid; w < nwords; w += T) bits[w] = 0;
+    if (tid == 0) { bad_s = 0; sem_n_s = 0; }
+    __syncthreads();
+    for (int i0 = 0; i0 < n_static; i0 += 8 * T) {
+        int32_t v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int i = i0 + u * T + tid;
+            v[u] = i < n_static ? __ldg(&static_ids[i]) : -1;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int i = i0 + u * T + tid;
+            if (i >= n_static) continue;
+            if (v[u] < 0 || v[u] >= V) { bad_s = 1; continue; }
+            if (debug && i > 0 && static_ids[i - 1] >= v[u]) bad_s = 1;
+            atomicOr(&bits[v[u] >> 5], 1u << (v[u] & 31));
+        }
+    }
     pdl_wait();
     const int n_cand = min(*n_cand_dev, cap);
-    if (trace) { __syncthreads(); if (threadIdx.x == 0) { long long t_; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); trace[0] = t_; } }
-    for (int w = tid; w < nwords; w += T) bits[w] = 0;
     for (int i0 = 0; i0 < n_cand; i0 += 4 * T) {           // 4 independent loads in flight
         double sv[4];
         int32_t iv[4];
@@ -298,25 +318,7 @@ union_kernel(int V, const int32_t* __restrict__ static_ids, int n_static,
             cf[i] = (iv[u] >= 0 && iv[u] < V) ? kCand : 0;
         }
     }
-    if (tid == 0) { bad_s = 0; sem_n_s = 0; }
     __syncthreads();
-    // 1. static members (8 independent loads in flight per thread)
-    for (int i0 = 0; i0 < n_static; i0 += 8 * T) {
-        int32_t v[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            const int i = i0 + u * T + tid;
-            v[u] = i < n_static ? __ldg(&static_ids[i]) : -1;
-        }
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            const int i = i0 + u * T + tid;
-            if (i >= n_static) continue;
-            if (v[u] < 0 || v[u] >= V) { bad_s = 1; continue; }
-            if (debug && i > 0 && static_ids[i - 1] >= v[u]) bad_s = 1;
-            atomicOr(&bits[v[u] >> 5], 1u << (v[u] & 31));
-        }
-    }
     if (trace) { __syncthreads(); if (threadIdx.x == 0) { long long t_; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); trace[1] = t_; } }
     // 2. S_sem = exact top-N of the candidate superset
     block_topM(ck, cid, cf, n_cand, kCand, kSem, n_sem, hist, bsel, warp_tot);
