@@ -148,6 +148,13 @@ struct evospec_ctx {
     float* rg_s = nullptr;
     int32_t* rg_seg = nullptr;   // device {0, n_static}
     int32_t* rg_segcta = nullptr;   // device [kMaxSeg+1] CTA schedule of the dynamic blocks
+    // draft_step as a CUDA graph (see evospec_draft_step)
+    cudaGraphExec_t g_exec = nullptr;
+    evospec_step_io g_key{};
+    long long g_launches = 0;
+    cudaStream_t cap_stream = nullptr;
+    cudaStream_t s_h = nullptr;         // host-staged H copy, overlapping the build
+    cudaEvent_t ev_in = nullptr, ev_h = nullptr;
     int last_n_sem = 0;
     ncclComm_t comm = nullptr;
     // measurement hooks
@@ -222,6 +229,11 @@ evospec_status evospec_destroy(evospec_ctx* ctx) {
     if (ctx->comm && nccl().loaded) nccl().CommDestroy(ctx->comm);
     for (cudaEvent_t e : ctx->ev) cudaEventDestroy(e);
     if (ctx->trace) cudaFree(ctx->trace);
+    if (ctx->g_exec) cudaGraphExecDestroy(ctx->g_exec);
+    if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
+    if (ctx->s_h) cudaStreamDestroy(ctx->s_h);
+    if (ctx->ev_in) cudaEventDestroy(ctx->ev_in);
+    if (ctx->ev_h) cudaEventDestroy(ctx->ev_h);
     delete ctx;
     return EVOSPEC_OK;
 }
@@ -721,10 +733,10 @@ evospec_status evospec_merge_shards(evospec_ctx* ctx, int32_t n_h, int32_t k, co
     return EVOSPEC_OK;
 }
 
-evospec_status evospec_draft_step(evospec_ctx* ctx, const evospec_step_io* io, void* stream) {
-    if (!ctx || !io) return fail(EVOSPEC_EINPUT, "draft_step: null argument");
+// phases: 1 host->device staging, 2 the compute (build + LM head + merge), 4 device->host
+static evospec_status draft_step_impl(evospec_ctx* ctx, const evospec_step_io* io, cudaStream_t st,
+                                      int phases = 7) {
     const evospec_config& c = ctx->cfg;
-    cudaStream_t st = (cudaStream_t)stream;
     if (io->n_h < 1 || io->n_h > c.max_rows || io->n_seed < 0 || io->n_seed > c.max_seeds || io->n_ctx < 0 ||
         io->n_ctx > c.max_ctx || !io->q || !io->H || !io->out_ids || !io->out_vals || !io->out_lse)
         return fail(EVOSPEC_EINPUT, "draft_step: bad I/O arguments");
@@ -732,16 +744,30 @@ evospec_status evospec_draft_step(evospec_ctx* ctx, const evospec_step_io* io, v
     const size_t hb = c.h_dtype == EVOSPEC_BF16 ? 2 : 4;
     const void *q = io->q, *H = io->H;
     const int32_t *seeds = io->seeds, *cx = io->ctx_ids;
-    if (io->host_io) {
+    if (io->host_io && !ctx->s_h) {
+        CUDA_TRY(cudaStreamCreateWithFlags(&ctx->s_h, cudaStreamNonBlocking));
+        CUDA_TRY(cudaEventCreateWithFlags(&ctx->ev_in, cudaEventDisableTiming));
+        CUDA_TRY(cudaEventCreateWithFlags(&ctx->ev_h, cudaEventDisableTiming));
+    }
+    if (io->host_io && (phases & 1)) {
         StageTimer t(ctx, EVOSPEC_STAGE_COPY, st);
         CUDA_TRY(cudaMemcpyAsync(ctx->st_q, io->q, (size_t)c.d * hb, cudaMemcpyHostToDevice, st));
-        CUDA_TRY(cudaMemcpyAsync(ctx->st_H, io->H, (size_t)io->n_h * c.d * hb, cudaMemcpyHostToDevice, st));
+        // H is needed only by the LM head: its copy runs on a side stream under the build
+        CUDA_TRY(cudaEventRecord(ctx->ev_in, st));
+        CUDA_TRY(cudaStreamWaitEvent(ctx->s_h, ctx->ev_in, 0));
+        CUDA_TRY(cudaMemcpyAsync(ctx->st_H, io->H, (size_t)io->n_h * c.d * hb, cudaMemcpyHostToDevice, ctx->s_h));
+        CUDA_TRY(cudaEventRecord(ctx->ev_h, ctx->s_h));
         if (io->n_seed > 0)
             CUDA_TRY(cudaMemcpyAsync(ctx->st_seeds, io->seeds, (size_t)io->n_seed * 4, cudaMemcpyHostToDevice, st));
         if (io->n_ctx > 0 && io->ctx_ids)
             CUDA_TRY(cudaMemcpyAsync(ctx->st_ctx, io->ctx_ids, (size_t)io->n_ctx * 4, cudaMemcpyHostToDevice, st));
-        q = ctx->st_q; H = ctx->st_H; seeds = ctx->st_seeds; cx = io->ctx_ids ? ctx->st_ctx : nullptr;
     }
+    if (io->host_io) { q = ctx->st_q; H = ctx->st_H; seeds = ctx->st_seeds; cx = io->ctx_ids ? ctx->st_ctx : nullptr; }
+    int32_t* oi = io->host_io ? ctx->st_oids : io->out_ids;
+    float* ov = io->host_io ? ctx->st_ovals : io->out_vals;
+    float* ol = io->host_io ? ctx->st_lse : io->out_lse;
+    float* op = io->host_io ? (io->out_probs ? ctx->st_probs : nullptr) : io->out_probs;
+    if (phases & 2) {
     const int n_sub_max = io->n_static + io->build.n_dyn;
     evospec_status s = evospec_build_subset(ctx, io->E, io->n_e_rows, q, io->static_ids, io->n_static, seeds,
                                             io->n_seed, io->csr_row_ptr, io->csr_col, cx, io->n_ctx, &io->build,
@@ -750,10 +776,11 @@ evospec_status evospec_draft_step(evospec_ctx* ctx, const evospec_step_io* io, v
     if (s != EVOSPEC_OK) return s;
     const int32_t* sub = c.n_shards > 1 ? ctx->st_local : ctx->st_S;
     const int32_t* nsub = c.n_shards > 1 ? ctx->st_nlocal : ctx->st_nS;
-    int32_t* oi = io->host_io ? ctx->st_oids : io->out_ids;
-    float* ov = io->host_io ? ctx->st_ovals : io->out_vals;
-    float* ol = io->host_io ? ctx->st_lse : io->out_lse;
-    float* op = io->host_io ? (io->out_probs ? ctx->st_probs : nullptr) : io->out_probs;
+    if (io->host_io) {   // the staged H (side stream) before the LM head
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        cudaStreamIsCapturing(st, &cs);
+        CUDA_TRY(cudaStreamWaitEvent(st, ctx->ev_h, cs == cudaStreamCaptureStatusActive ? cudaEventWaitExternal : 0));
+    }
     const bool fuse = c.n_shards == 1;    // single shard: the merge is the finalisation itself
     s = lmh_impl(ctx, io->W_local, io->n_w_rows, H, io->n_h, sub, nsub, n_sub_max, io->k, io->inv_temp, ctx->st_tids,
                  ctx->st_tvals, ctx->st_m, ctx->st_s, nullptr, st, fuse ? oi : nullptr, fuse ? ov : nullptr,
@@ -764,7 +791,8 @@ evospec_status evospec_draft_step(evospec_ctx* ctx, const evospec_step_io* io, v
                                  op, st);
         if (s != EVOSPEC_OK) return s;
     }
-    if (io->host_io) {
+    }   // phases & 2
+    if (io->host_io && (phases & 4)) {
         StageTimer t(ctx, EVOSPEC_STAGE_COPY, st);
         const size_t hk = (size_t)io->n_h * io->k;
         CUDA_TRY(cudaMemcpyAsync(io->out_ids, oi, hk * 4, cudaMemcpyDeviceToHost, st));
@@ -773,6 +801,49 @@ evospec_status evospec_draft_step(evospec_ctx* ctx, const evospec_step_io* io, v
         if (io->out_probs) CUDA_TRY(cudaMemcpyAsync(io->out_probs, op, hk * 4, cudaMemcpyDeviceToHost, st));
     }
     return EVOSPEC_OK;
+}
+
+// The whole step as one CUDA graph (single shard): captured on the context's
+// own stream the first time an I/O descriptor is seen, replayed while the
+// descriptor (pointers, sizes, parameters) stays the same -- one launch instead
+// of ~10 kernel launches, copies and memsets per step. Timing / tracing /
+// debug checks and sharded contexts take the direct path.
+evospec_status evospec_draft_step(evospec_ctx* ctx, const evospec_step_io* io, void* stream) {
+    if (!ctx || !io) return fail(EVOSPEC_EINPUT, "draft_step: null argument");
+    cudaStream_t st = (cudaStream_t)stream;
+    const bool use_graph = ctx->cfg.n_shards == 1 && !ctx->timing && !ctx->cfg.debug_checks &&
+                           !getenv("EVOSPEC_NO_GRAPH") && !getenv("EVOSPEC_TRACE");
+    if (!use_graph) return draft_step_impl(ctx, io, st);
+    // host staging copies stay ordinary stream copies (measured faster than graph
+    // memcpy nodes from pinned memory); the graph holds the compute
+    if (ctx->g_exec && memcmp(&ctx->g_key, io, sizeof(*io)) == 0) {
+        evospec_status s0 = draft_step_impl(ctx, io, st, 1);
+        if (s0 != EVOSPEC_OK) return s0;
+        CUDA_TRY(cudaGraphLaunch(ctx->g_exec, st));
+        ctx->launches += ctx->g_launches;
+        return draft_step_impl(ctx, io, st, 4);
+    }
+    if (!ctx->cap_stream) CUDA_TRY(cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking));
+    const long long l0 = ctx->launches;
+    CUDA_TRY(cudaStreamBeginCapture(ctx->cap_stream, cudaStreamCaptureModeThreadLocal));
+    evospec_status s = draft_step_impl(ctx, io, ctx->cap_stream, 2);
+    cudaGraph_t g = nullptr;
+    const cudaError_t e = cudaStreamEndCapture(ctx->cap_stream, &g);
+    if (s != EVOSPEC_OK || e != cudaSuccess) {
+        if (g) cudaGraphDestroy(g);
+        if (s != EVOSPEC_OK) return s;
+        return fail(EVOSPEC_ECUDA, "draft_step: graph capture failed: %s", cudaGetErrorString(e));
+    }
+    if (ctx->g_exec) { cudaGraphExecDestroy(ctx->g_exec); ctx->g_exec = nullptr; }
+    const cudaError_t ei = cudaGraphInstantiate(&ctx->g_exec, g, 0);
+    cudaGraphDestroy(g);
+    if (ei != cudaSuccess) { ctx->g_exec = nullptr; return fail(EVOSPEC_ECUDA, "draft_step: %s", cudaGetErrorString(ei)); }
+    memcpy(&ctx->g_key, io, sizeof(*io));
+    ctx->g_launches = ctx->launches - l0;
+    s = draft_step_impl(ctx, io, st, 1);
+    if (s != EVOSPEC_OK) return s;
+    CUDA_TRY(cudaGraphLaunch(ctx->g_exec, st));
+    return draft_step_impl(ctx, io, st, 4);
 }
 
 evospec_status evospec_set_timing(evospec_ctx* ctx, int enable) {

@@ -407,3 +407,43 @@ def test_merged_single_shard_equals_oracle():
     assert np.max(np.abs(probs.cpu().numpy() - t["probs"])) <= G.PROB_TOL
     assert np.all(np.abs(vals.cpu().numpy() - t["vals"]) <= G.LOGIT_TOL * (1 + np.abs(t["vals"])))
     assert ctx.get_flags() == 0
+
+
+def test_draft_step_graph_replay_matches_direct():
+    """evospec_draft_step replays a captured CUDA graph while the I/O descriptor is
+    unchanged; its results equal the direct path's and the oracle's, also after the
+    inputs behind the same pointers change."""
+    import os
+    P = G.make_problem(71, dtype="bf16", V=16000, d=256, n_static=2000, n_sem=300, n_dyn=250, n_h=8, k=10)
+    ctx = ctx_for(P, debug_checks=False)
+    W = G.to_dev(P["W"], DEV)
+    ctx.prepare_weights(W)
+    kw = dict(E=W, W_local=W, static_ids=G.to_dev(P["static"], DEV), csr_row_ptr=G.to_dev(P["row_ptr"], DEV),
+              csr_col=G.to_dev(P["col"], DEV), k=P["k"], n_sem=P["n_sem"], n_dyn=P["n_dyn"])
+    H = G.to_dev(P["H"], DEV)
+    q = G.to_dev(P["q"], DEV)
+    seeds = G.to_dev(P["seeds"], DEV)
+    n_h, k = P["n_h"], P["k"]
+    out = (torch.empty((n_h, k), dtype=torch.int32, device=DEV), torch.empty((n_h, k), device=DEV),
+           torch.empty(n_h, device=DEV), torch.empty((n_h, k), device=DEV))
+    l0 = ctx.read_stats()["launches"]
+    outs = []
+    for _ in range(3):                                   # capture, replay, replay
+        o = ctx.draft_step(q=q, H=H, seeds=seeds, out=out, **kw)
+        torch.cuda.synchronize()
+        outs.append([t.cpu().numpy().copy() for t in o])
+    per_step = (ctx.read_stats()["launches"] - l0) / 3
+    assert per_step >= 4                                 # replays still count the graph's kernels
+    ref = G.oracle_step(oracle, P)
+    for o in outs:
+        np.testing.assert_array_equal(o[0], ref["triple"]["ids"])
+        assert np.max(np.abs(o[3] - ref["triple"]["probs"])) <= G.PROB_TOL
+    # new data behind the same pointers: the replay must see it
+    P2 = dict(P)
+    P2["H"] = synth_matrix(72, P["n_h"], P["d"], 1.0, "bf16")
+    H.copy_(G.to_dev(P2["H"], DEV))
+    o = ctx.draft_step(q=q, H=H, seeds=seeds, out=out, **kw)
+    torch.cuda.synchronize()
+    ref2 = G.oracle_step(oracle, P2)
+    np.testing.assert_array_equal(o[0].cpu().numpy(), ref2["triple"]["ids"])
+    assert ctx.get_flags() == 0
