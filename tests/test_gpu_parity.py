@@ -447,3 +447,14 @@ def test_draft_step_graph_replay_matches_direct():
     ref2 = G.oracle_step(oracle, P2)
     np.testing.assert_array_equal(o[0].cpu().numpy(), ref2["triple"]["ids"])
     assert ctx.get_flags() == 0
+
+
+@pytest.mark.parametrize("V,d,n_dyn", [(12345, 192, 0), (12345, 192, 77), (4099, 320, 500)])
+def test_odd_shapes_static_only_and_ragged_vocab(V, d, n_dyn):
+    """V not a multiple of 32, d not a multiple of 256 (the LDG scan variant; d = 192 / 320
+    still on the tensor-core head), a static-only subset (N_dyn = 0), and a dynamic budget
+    larger than the non-static pool can fill."""
+    P = G.make_problem(80 + n_dyn, dtype="bf16", V=V, d=d, n_static=1500, n_sem=200, n_dyn=n_dyn, n_h=7, k=10)
+    got = run_path(P)
+    ref = G.oracle_step(oracle, P)
+    check(P, got, ref, P["k"])
