@@ -389,7 +389,9 @@ static evospec_status build_impl(evospec_ctx* ctx, const void* E, int64_t n_e_ro
     // a2: exact fp64 scores (+ fused pass-0 histogram), candidate superset of the top-N
     {
         StageTimer t(ctx, EVOSPEC_STAGE_SCAN, st);
-        launch_sem_scan(E, c.w_dtype, n_e_rows, c.d, q, c.h_dtype, ctx->s64, ctx->key32, ctx->hist12, st);
+        // the scan zeroes the next selection's histogram scratch and count
+        launch_sem_scan(E, c.w_dtype, n_e_rows, c.d, q, c.h_dtype, ctx->s64, ctx->key32, ctx->hist12, st, ctx->hist,
+                        12 * kHistBins, full_scan ? ctx->cand_count : ctx->loc_count);
         ctx->launches += 1;
     }
     LAUNCH_CHECK("sem_scan");
@@ -397,14 +399,14 @@ static evospec_status build_impl(evospec_ctx* ctx, const void* E, int64_t n_e_ro
     if (full_scan) {
         ctx->launches += 1;
         CUDA_TRY(launch_topn_cand(ctx->s64, nullptr, n_e_rows, 1, 0, N, ctx->cand_cap, ctx->hist12, ctx->hist,
-                                  ctx->cand_count, ctx->cand_s, ctx->cand_id, st));
+                                  ctx->cand_count, ctx->cand_s, ctx->cand_id, st, true));
     } else {
         // exact local top-N (ids = row*R + r; padded with id -1), all-gather N (s, id) pairs per rank,
         // candidate superset of the global top-N over the R*N gathered pairs
         ctx->launches += 2;
         CUDA_TRY(cudaMemsetAsync(ctx->loc_id, 0xFF, (size_t)N * sizeof(int32_t), st));
         CUDA_TRY(launch_topn_cand(ctx->s64, nullptr, n_e_rows, R, r, N, N, ctx->hist12, ctx->hist, ctx->loc_count,
-                                  ctx->loc_s, ctx->loc_id, st));
+                                  ctx->loc_s, ctx->loc_id, st, true));
         NcclApi& n = nccl();
         n.GroupStart();
         ncclResult_t r1 = n.AllGather(ctx->loc_s, ctx->gat_s, (size_t)N, ncclFloat64, ctx->comm, st);

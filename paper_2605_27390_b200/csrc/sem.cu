@@ -42,7 +42,11 @@ template <int DT>  // element type of E: 0 bf16, 1 fp32
 __global__ void __launch_bounds__(kScanWarps * 32, 1)
 sem_scan_kernel(const void* __restrict__ E, int64_t n_rows, int d,
                 const void* __restrict__ q, int q_dtype, uint32_t* __restrict__ hist12,
-                double* __restrict__ s64, uint32_t* __restrict__ key32) {
+                double* __restrict__ s64, uint32_t* __restrict__ key32, uint32_t* __restrict__ zero_w, int n_zero_w,
+                int* __restrict__ zero_c) {
+    // zero the candidate selection's scratch for the next kernel (saves two memsets)
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_zero_w; i += gridDim.x * blockDim.x) zero_w[i] = 0;
+    if (zero_c && blockIdx.x == 0 && threadIdx.x == 0) *zero_c = 0;
     constexpr int ELEMS = DT == 0 ? 8 : 4;           // elements per 16 bytes
     constexpr int SLAB = 32 * ELEMS;                  // columns per slab
     extern __shared__ double q_sm[];                  // [n_slabs][ELEMS][32]
@@ -185,7 +189,10 @@ template <int kScanRowsPerStage, int kScanStages>
 __global__ void __launch_bounds__((kScanConsumers + 1) * 32, 1)
 sem_scan_tma_kernel(const uint16_t* __restrict__ E, int64_t n_rows, int d, const void* __restrict__ q, int q_dtype,
                     uint32_t* __restrict__ hist12, double* __restrict__ s64, uint32_t* __restrict__ key32, int pf,
-                    int il) {
+                    int il, uint32_t* __restrict__ zero_w, int n_zero_w, int* __restrict__ zero_c) {
+    // zero the candidate selection's scratch for the next kernel (saves two memsets)
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_zero_w; i += gridDim.x * blockDim.x) zero_w[i] = 0;
+    if (zero_c && blockIdx.x == 0 && threadIdx.x == 0) *zero_c = 0;
     extern __shared__ __align__(128) unsigned char sc_sm[];
     const size_t row_bytes = (size_t)d * 2;
     const size_t stage_bytes = kScanRowsPerStage * row_bytes;
@@ -330,7 +337,8 @@ sem_scan_tma_kernel(const uint16_t* __restrict__ E, int64_t n_rows, int d, const
 }
 
 void launch_sem_scan(const void* E, int e_dtype, int64_t n_rows, int d, const void* q, int q_dtype,
-                     double* s64, uint32_t* key32, uint32_t* hist12, cudaStream_t st) {
+                     double* s64, uint32_t* key32, uint32_t* hist12, cudaStream_t st, uint32_t* zero_w,
+                     int n_zero_w, int* zero_c) {
     cudaMemsetAsync(hist12, 0, kHistBins * sizeof(uint32_t), st);
     const int elems = e_dtype == 0 ? 8 : 4;
     const int n_slabs = (d + 32 * elems - 1) / (32 * elems);
@@ -352,22 +360,24 @@ void launch_sem_scan(const void* E, int e_dtype, int64_t n_rows, int d, const vo
         if (RS == 4) {
             cudaFuncSetAttribute(sem_scan_tma_kernel<4, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
             sem_scan_tma_kernel<4, 6><<<kNumSMs, (kScanConsumers + 1) * 32, sm, st>>>(
-                (const uint16_t*)E, n_rows, d, q, q_dtype, hist12, s64, key32, pf, il);
+                (const uint16_t*)E, n_rows, d, q, q_dtype, hist12, s64, key32, pf, il, zero_w, n_zero_w, zero_c);
         } else if (RS == 2) {
             cudaFuncSetAttribute(sem_scan_tma_kernel<2, 12>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
             sem_scan_tma_kernel<2, 12><<<kNumSMs, (kScanConsumers + 1) * 32, sm, st>>>(
-                (const uint16_t*)E, n_rows, d, q, q_dtype, hist12, s64, key32, pf, il);
+                (const uint16_t*)E, n_rows, d, q, q_dtype, hist12, s64, key32, pf, il, zero_w, n_zero_w, zero_c);
         } else {
             cudaFuncSetAttribute(sem_scan_tma_kernel<8, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
             sem_scan_tma_kernel<8, 3><<<kNumSMs, (kScanConsumers + 1) * 32, sm, st>>>(
-                (const uint16_t*)E, n_rows, d, q, q_dtype, hist12, s64, key32, pf, il);
+                (const uint16_t*)E, n_rows, d, q, q_dtype, hist12, s64, key32, pf, il, zero_w, n_zero_w, zero_c);
         }
     } else if (e_dtype == 0) {
         cudaFuncSetAttribute(sem_scan_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        sem_scan_kernel<0><<<kNumSMs, kScanWarps * 32, smem, st>>>(E, n_rows, d, q, q_dtype, hist12, s64, key32);
+        sem_scan_kernel<0><<<kNumSMs, kScanWarps * 32, smem, st>>>(E, n_rows, d, q, q_dtype, hist12, s64, key32,
+                                                                    zero_w, n_zero_w, zero_c);
     } else {
         cudaFuncSetAttribute(sem_scan_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        sem_scan_kernel<1><<<kNumSMs, kScanWarps * 32, smem, st>>>(E, n_rows, d, q, q_dtype, hist12, s64, key32);
+        sem_scan_kernel<1><<<kNumSMs, kScanWarps * 32, smem, st>>>(E, n_rows, d, q, q_dtype, hist12, s64, key32,
+                                                                    zero_w, n_zero_w, zero_c);
     }
 }
 
@@ -531,9 +541,11 @@ topn_cand_kernel(const double* __restrict__ s64, const int32_t* __restrict__ ids
 
 cudaError_t launch_topn_cand(const double* s64, const int32_t* ids, int64_t n, int id_mul, int id_add,
                              int N, int cap, const uint32_t* hist_pre, uint32_t* hist_g, int* out_count,
-                             double* out_s, int32_t* out_id, cudaStream_t st) {
-    cudaMemsetAsync(hist_g, 0, 12 * kHistBins * sizeof(uint32_t), st);
-    cudaMemsetAsync(out_count, 0, sizeof(int), st);
+                             double* out_s, int32_t* out_id, cudaStream_t st, bool prezeroed) {
+    if (!prezeroed) {   // (the scan zeroes them when it directly precedes this selection)
+        cudaMemsetAsync(hist_g, 0, 12 * kHistBins * sizeof(uint32_t), st);
+        cudaMemsetAsync(out_count, 0, sizeof(int), st);
+    }
     int grid = kNumSMs;
     if (n < (int64_t)grid * 64) grid = (int)((n + 63) / 64);
     if (grid < 1) grid = 1;
