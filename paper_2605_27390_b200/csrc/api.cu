@@ -99,7 +99,9 @@ struct evospec_ctx {
     // semantic scan + selection
     double* s64 = nullptr;
     uint32_t* key32 = nullptr;
-    uint32_t* hist12 = nullptr;   // scan-fused pass-0 histogram
+    uint32_t* hist12 = nullptr;   // scan-fused pass-0 histogram; zero between builds (the union kernel
+                                  // clears it after the selection has read it)
+    bool hist_dirty = false;      // a build stopped between its scan and its union: clear first
     uint32_t* hist = nullptr;     // [12][4096] further select passes
     int cand_cap = 0;             // candidate superset capacity (union smem)
     int* cand_count = nullptr;
@@ -274,7 +276,7 @@ evospec_status evospec_create(evospec_ctx** out, const evospec_config* cfg, int 
                     cap_v, c.V);
     }
     const size_t cap = (size_t)x->cand_cap;
-    A(dalloc(&x->s64, V)); A(dalloc(&x->key32, V)); A(dalloc(&x->hist12, kHistBins));
+    A(dalloc(&x->s64, V)); A(dalloc(&x->key32, V)); A(dalloc(&x->hist12, kHistBins)); A(cudaMemset(x->hist12, 0, kHistBins * sizeof(uint32_t)));
     A(dalloc(&x->hist, 12 * kHistBins));
     A(dalloc(&x->cand_count, 4)); A(dalloc(&x->cand_s, cap)); A(dalloc(&x->cand_id, cap));
     A(dalloc(&x->loc_count, 4)); A(dalloc(&x->loc_s, sem)); A(dalloc(&x->loc_id, sem));
@@ -386,26 +388,30 @@ static evospec_status build_impl(evospec_ctx* ctx, const void* E, int64_t n_e_ro
         return fail(EVOSPEC_EINPUT, "build_subset: a sharded index needs evospec_comm_init");
 
     const int N = p->n_sem;
+    const uint32_t* hist_pre = nullptr;
     // a2: exact fp64 scores (+ fused pass-0 histogram), candidate superset of the top-N
     {
         StageTimer t(ctx, EVOSPEC_STAGE_SCAN, st);
         // the scan zeroes the next selection's histogram scratch and count
+        if (ctx->hist_dirty) CUDA_TRY(cudaMemsetAsync(ctx->hist12, 0, kHistBins * sizeof(uint32_t), st));
         launch_sem_scan(E, c.w_dtype, n_e_rows, c.d, q, c.h_dtype, ctx->s64, ctx->key32, ctx->hist12, st, ctx->hist,
-                        12 * kHistBins, full_scan ? ctx->cand_count : ctx->loc_count);
+                        12 * kHistBins, full_scan ? ctx->cand_count : ctx->loc_count, true);
+        hist_pre = ctx->hist12;
+        ctx->hist_dirty = true;
         ctx->launches += 1;
     }
     LAUNCH_CHECK("sem_scan");
     StageTimer t_sel(ctx, EVOSPEC_STAGE_SELECT, st);
     if (full_scan) {
         ctx->launches += 1;
-        CUDA_TRY(launch_topn_cand(ctx->s64, nullptr, n_e_rows, 1, 0, N, ctx->cand_cap, ctx->hist12, ctx->hist,
+        CUDA_TRY(launch_topn_cand(ctx->s64, nullptr, n_e_rows, 1, 0, N, ctx->cand_cap, hist_pre, ctx->hist,
                                   ctx->cand_count, ctx->cand_s, ctx->cand_id, st, true));
     } else {
         // exact local top-N (ids = row*R + r; padded with id -1), all-gather N (s, id) pairs per rank,
         // candidate superset of the global top-N over the R*N gathered pairs
         ctx->launches += 2;
         CUDA_TRY(cudaMemsetAsync(ctx->loc_id, 0xFF, (size_t)N * sizeof(int32_t), st));
-        CUDA_TRY(launch_topn_cand(ctx->s64, nullptr, n_e_rows, R, r, N, N, ctx->hist12, ctx->hist, ctx->loc_count,
+        CUDA_TRY(launch_topn_cand(ctx->s64, nullptr, n_e_rows, R, r, N, N, hist_pre, ctx->hist, ctx->loc_count,
                                   ctx->loc_s, ctx->loc_id, st, true));
         NcclApi& n = nccl();
         n.GroupStart();
@@ -432,8 +438,9 @@ static evospec_status build_impl(evospec_ctx* ctx, const void* E, int64_t n_e_ro
     launch_union(c.V, static_ids, n_static, seeds, n_seed, ctx->cand_s, ctx->cand_id, ctx->cand_count, ctx->cand_cap,
                  N, row_ptr, col, use_ctx ? ctx->ctx_sel : nullptr, ctx->ctx_n, p->n_graph_sem_seeds, p->per_seed,
                  p->n_dyn, R, r, out_ids, out_n, out_local_ids, out_local_n, ctx->sem_ids, ctx->sem_n,
-                 c.debug_checks, ctx->flags, st, union_trace(ctx, st), dyn_base);
+                 c.debug_checks, ctx->flags, st, union_trace(ctx, st), dyn_base, ctx->hist12);
     LAUNCH_CHECK("union");
+    ctx->hist_dirty = false;
     return EVOSPEC_OK;
 }
 

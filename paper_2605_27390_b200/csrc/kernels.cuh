@@ -25,7 +25,7 @@ constexpr int kFlagBudget = 0x8;
 // ---- semantic (sem.cu)
 void launch_sem_scan(const void* E, int e_dtype, int64_t n_rows, int d, const void* q, int q_dtype,
                      double* s64, uint32_t* key32, uint32_t* hist12, cudaStream_t st, uint32_t* zero_w = nullptr,
-                     int n_zero_w = 0, int* zero_c = nullptr);
+                     int n_zero_w = 0, int* zero_c = nullptr, bool hist_zero = false);
 cudaError_t launch_topn_cand(const double* s64, const int32_t* ids, int64_t n, int id_mul, int id_add,
                              int N, int cap, const uint32_t* hist_pre, uint32_t* hist_g, int* out_count,
                              double* out_s, int32_t* out_id, cudaStream_t st, bool prezeroed = false);
@@ -41,7 +41,8 @@ void launch_union(int V, const int32_t* static_ids, int n_static, const int32_t*
                   int n_graph_sem_seeds, int per_seed, int n_dyn, int R, int r,
                   int32_t* out_ids, int32_t* out_n, int32_t* out_local, int32_t* out_local_n,
                   int32_t* sem_out, int* sem_out_n, int debug, int* flags, cudaStream_t st,
-                  long long* trace = nullptr, const int32_t* dyn_base = nullptr);
+                  long long* trace = nullptr, const int32_t* dyn_base = nullptr,
+                  uint32_t* clear_hist = nullptr);
 
 // ---- LM head (lmh_gemv.cu, lmh_tc.cu)
 // Per-CTA partial state of the LM head, per H row: entries [0, cnt) are the

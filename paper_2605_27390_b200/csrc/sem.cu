@@ -338,8 +338,9 @@ sem_scan_tma_kernel(const uint16_t* __restrict__ E, int64_t n_rows, int d, const
 
 void launch_sem_scan(const void* E, int e_dtype, int64_t n_rows, int d, const void* q, int q_dtype,
                      double* s64, uint32_t* key32, uint32_t* hist12, cudaStream_t st, uint32_t* zero_w,
-                     int n_zero_w, int* zero_c) {
-    cudaMemsetAsync(hist12, 0, kHistBins * sizeof(uint32_t), st);
+                     int n_zero_w, int* zero_c, bool hist_zero) {
+    // hist_zero: hist12 is already zero (the previous build's union kernel cleared it)
+    if (!hist_zero) cudaMemsetAsync(hist12, 0, kHistBins * sizeof(uint32_t), st);
     const int elems = e_dtype == 0 ? 8 : 4;
     const int n_slabs = (d + 32 * elems - 1) / (32 * elems);
     const size_t smem = (size_t)n_slabs * 32 * elems * sizeof(double);

@@ -258,7 +258,7 @@ union_kernel(int V, const int32_t* __restrict__ static_ids, int n_static,
              int32_t* __restrict__ out_ids, int32_t* __restrict__ out_n,
              int32_t* __restrict__ out_local, int32_t* __restrict__ out_local_n,
              int32_t* __restrict__ sem_out, int* __restrict__ sem_out_n, int debug, int* flags,
-             long long* __restrict__ trace, const int32_t* __restrict__ dyn_base) {
+             long long* __restrict__ trace, const int32_t* __restrict__ dyn_base, uint32_t* __restrict__ clear_hist) {
     extern __shared__ __align__(16) unsigned char u_sm[];
     const int nwords = (V + 31) / 32;
     uint64_t* ck = (uint64_t*)u_sm;                          // [cap]
@@ -299,6 +299,9 @@ union_kernel(int V, const int32_t* __restrict__ static_ids, int n_static,
         }
     }
     pdl_wait();
+    // the selection has consumed the scan's histogram: leave it zero for the next build
+    if (clear_hist)
+        for (int i = tid; i < kHistBins; i += T) clear_hist[i] = 0;
     const int n_cand = min(*n_cand_dev, cap);
     for (int i0 = 0; i0 < n_cand; i0 += 4 * T) {           // 4 independent loads in flight
         double sv[4];
@@ -568,13 +571,13 @@ void launch_union(int V, const int32_t* static_ids, int n_static, const int32_t*
                   int n_graph_sem_seeds, int per_seed, int n_dyn, int R, int r,
                   int32_t* out_ids, int32_t* out_n, int32_t* out_local, int32_t* out_local_n,
                   int32_t* sem_out, int* sem_out_n, int debug, int* flags, cudaStream_t st, long long* trace,
-                  const int32_t* dyn_base) {
+                  const int32_t* dyn_base, uint32_t* clear_hist) {
     const size_t smem = (size_t)cap * 13 + union_fixed_bytes(V, per_seed) + 16;
     cudaFuncSetAttribute(union_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     launch_pdl(union_kernel, dim3(1), dim3(kUnionThreads), smem, st, V, static_ids, n_static, seeds, n_seed, cand_s, cand_id, n_cand_dev,
                                                   cap, n_sem, row_ptr, col, ctx_sel, n_ctx_sel_dev, n_graph_sem_seeds,
                                                   per_seed, n_dyn, R, r, out_ids, out_n, out_local, out_local_n,
-                                                  sem_out, sem_out_n, debug, flags, trace, dyn_base);
+                                                  sem_out, sem_out_n, debug, flags, trace, dyn_base, clear_hist);
 }
 
 }  // namespace es
