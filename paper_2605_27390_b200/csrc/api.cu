@@ -102,6 +102,7 @@ struct evospec_ctx {
     uint32_t* hist12 = nullptr;   // scan-fused pass-0 histogram; zero between builds (the union kernel
                                   // clears it after the selection has read it)
     bool hist_dirty = false;      // a build stopped between its scan and its union: clear first
+    uint32_t* ubits = nullptr;    // [V/32] union bitmap handed to the emit kernel
     uint32_t* hist = nullptr;     // [12][4096] further select passes
     int cand_cap = 0;             // candidate superset capacity (union smem)
     int* cand_count = nullptr;
@@ -225,7 +226,7 @@ evospec_status evospec_destroy(evospec_ctx* ctx) {
                     ctx->flags, ctx->wmax, ctx->g_ids, ctx->g_vals, ctx->g_m, ctx->g_s, ctx->st_q, ctx->st_H,
                     ctx->st_seeds, ctx->st_ctx, ctx->st_S, ctx->st_nS, ctx->st_local, ctx->st_nlocal,
                     ctx->st_tids, ctx->st_tvals, ctx->st_m, ctx->st_s, ctx->st_oids, ctx->st_ovals,
-                    ctx->st_lse, ctx->st_probs, ctx->rg_ids, ctx->rg_vals, ctx->rg_m, ctx->rg_s, ctx->rg_seg, ctx->rg_segcta};
+                    ctx->st_lse, ctx->st_probs, ctx->ubits, ctx->rg_ids, ctx->rg_vals, ctx->rg_m, ctx->rg_s, ctx->rg_seg, ctx->rg_segcta};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (ctx->comm && nccl().loaded) nccl().CommDestroy(ctx->comm);
@@ -276,7 +277,7 @@ evospec_status evospec_create(evospec_ctx** out, const evospec_config* cfg, int 
                     cap_v, c.V);
     }
     const size_t cap = (size_t)x->cand_cap;
-    A(dalloc(&x->s64, V)); A(dalloc(&x->key32, V)); A(dalloc(&x->hist12, kHistBins)); A(cudaMemset(x->hist12, 0, kHistBins * sizeof(uint32_t)));
+    A(dalloc(&x->s64, V)); A(dalloc(&x->key32, V)); A(dalloc(&x->hist12, kHistBins)); A(dalloc(&x->ubits, (V + 31) / 32)); A(cudaMemset(x->hist12, 0, kHistBins * sizeof(uint32_t)));
     A(dalloc(&x->hist, 12 * kHistBins));
     A(dalloc(&x->cand_count, 4)); A(dalloc(&x->cand_s, cap)); A(dalloc(&x->cand_id, cap));
     A(dalloc(&x->loc_count, 4)); A(dalloc(&x->loc_s, sem)); A(dalloc(&x->loc_id, sem));
@@ -435,12 +436,20 @@ static evospec_status build_impl(evospec_ctx* ctx, const void* E, int64_t n_e_ro
         LAUNCH_CHECK("ctx_select");
     }
     // a2 exact S_sem + a3/a4 formation, cap, union
+    const bool emit = R == 1 && !dyn_base;
     launch_union(c.V, static_ids, n_static, seeds, n_seed, ctx->cand_s, ctx->cand_id, ctx->cand_count, ctx->cand_cap,
                  N, row_ptr, col, use_ctx ? ctx->ctx_sel : nullptr, ctx->ctx_n, p->n_graph_sem_seeds, p->per_seed,
                  p->n_dyn, R, r, out_ids, out_n, out_local_ids, out_local_n, ctx->sem_ids, ctx->sem_n,
-                 c.debug_checks, ctx->flags, st, union_trace(ctx, st), dyn_base, ctx->hist12);
+                 c.debug_checks, ctx->flags, st, union_trace(ctx, st), dyn_base, ctx->hist12,
+                 emit ? ctx->ubits : nullptr);
     LAUNCH_CHECK("union");
     ctx->hist_dirty = false;
+    if (emit) {   // single shard: the sorted ids from the bitmap by a multi-CTA kernel
+        launch_union_emit(ctx->ubits, c.V, out_ids, out_n, out_local_ids, out_local_n, n_static + p->n_dyn,
+                          ctx->flags, st);
+        ctx->launches += 1;
+        LAUNCH_CHECK("union_emit");
+    }
     return EVOSPEC_OK;
 }
 

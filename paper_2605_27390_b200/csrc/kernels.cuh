@@ -42,7 +42,9 @@ void launch_union(int V, const int32_t* static_ids, int n_static, const int32_t*
                   int32_t* out_ids, int32_t* out_n, int32_t* out_local, int32_t* out_local_n,
                   int32_t* sem_out, int* sem_out_n, int debug, int* flags, cudaStream_t st,
                   long long* trace = nullptr, const int32_t* dyn_base = nullptr,
-                  uint32_t* clear_hist = nullptr);
+                  uint32_t* clear_hist = nullptr, uint32_t* emit_bits = nullptr);
+void launch_union_emit(const uint32_t* bits, int V, int32_t* out_ids, int32_t* out_n, int32_t* out_local,
+                       int32_t* out_local_n, int budget_max, int* flags, cudaStream_t st);
 
 // ---- LM head (lmh_gemv.cu, lmh_tc.cu)
 // Per-CTA partial state of the LM head, per H row: entries [0, cnt) are the

@@ -258,7 +258,8 @@ union_kernel(int V, const int32_t* __restrict__ static_ids, int n_static,
              int32_t* __restrict__ out_ids, int32_t* __restrict__ out_n,
              int32_t* __restrict__ out_local, int32_t* __restrict__ out_local_n,
              int32_t* __restrict__ sem_out, int* __restrict__ sem_out_n, int debug, int* flags,
-             long long* __restrict__ trace, const int32_t* __restrict__ dyn_base, uint32_t* __restrict__ clear_hist) {
+             long long* __restrict__ trace, const int32_t* __restrict__ dyn_base, uint32_t* __restrict__ clear_hist,
+             uint32_t* __restrict__ emit_bits) {
     extern __shared__ __align__(16) unsigned char u_sm[];
     const int nwords = (V + 31) / 32;
     uint64_t* ck = (uint64_t*)u_sm;                          // [cap]
@@ -504,6 +505,18 @@ union_kernel(int V, const int32_t* __restrict__ static_ids, int n_static,
         out_ids += base_off;
         __syncthreads();
     }
+    if (emit_bits) {
+        // single shard, full output: the sorted ids are written by the multi-CTA
+        // emit kernel from the bitmap (union_emit_kernel)
+        for (int w = tid; w < nwords; w += T) emit_bits[w] = bits[w];
+        if (tid == 0) {
+            if (sem_out_n) *sem_out_n = sem_n_s;
+            if (bad_s) atomicOr(flags, kFlagBadIds);
+            if (*n_cand_dev > cap) atomicOr(flags, kFlagSelectOverflow);
+        }
+        if (trace) { __syncthreads(); if (threadIdx.x == 0) { long long t_; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); trace[6] = t_; } }
+        return;
+    }
     // 6. compaction. Thread t owns words [t*nwords/T, (t+1)*nwords/T); a block
     //    scan of the popcounts gives each thread's output offset. The sorted
     //    ids are staged in shared memory (the candidate arrays are dead by now)
@@ -551,6 +564,62 @@ union_kernel(int V, const int32_t* __restrict__ static_ids, int n_static,
     if (trace) { __syncthreads(); if (threadIdx.x == 0) { long long t_; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); trace[6] = t_; } }
 }
 
+// Sorted ids from the union bitmap, 32 words (1024 ids) per CTA: a CTA's
+// output offset is the popcount of all words before its chunk (each CTA sums
+// them from L2 itself: no inter-CTA chain), warp 0 scans its 32 words and
+// writes the ids. The last CTA writes n_S and the budget check.
+constexpr int kEmitThreads = 128;
+
+__global__ void __launch_bounds__(kEmitThreads)
+union_emit_kernel(const uint32_t* __restrict__ bits, int nwords, int32_t* __restrict__ out_ids,
+                  int32_t* __restrict__ out_n, int32_t* __restrict__ out_local, int32_t* __restrict__ out_local_n,
+                  int budget_max, int* flags) {
+    pdl_trigger();
+    pdl_wait();
+    __shared__ int wsum[kEmitThreads / 32];
+    const int tid = threadIdx.x, lane = lane_id(), warp = warp_id();
+    const int w0 = blockIdx.x * 32, w1 = min(nwords, w0 + 32);
+    int c = 0;
+#pragma unroll 4
+    for (int w = tid; w < w0; w += kEmitThreads) c += __popc(__ldcg(&bits[w]));
+    c = warp_sum_i(c);
+    if (lane == 0) wsum[warp] = c;
+    __syncthreads();
+    if (warp != 0) return;
+    int prefix = 0;
+#pragma unroll
+    for (int i = 0; i < kEmitThreads / 32; ++i) prefix += wsum[i];
+    const int w = w0 + lane;
+    const uint32_t x = w < w1 ? __ldcg(&bits[w]) : 0u;
+    const int pc = __popc(x);
+    int inc = pc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += t;
+    }
+    int off = prefix + inc - pc;
+    for (uint32_t bb = x; bb; bb &= bb - 1) {
+        const int32_t id = w * 32 + __ffs(bb) - 1;
+        out_ids[off] = id;
+        if (out_local) out_local[off] = id;
+        ++off;
+    }
+    if (blockIdx.x == gridDim.x - 1 && lane == 31) {
+        const int total = prefix + inc;
+        *out_n = total;
+        if (out_local_n) *out_local_n = total;
+        if (total > budget_max) atomicOr(flags, kFlagBudget);
+    }
+}
+
+void launch_union_emit(const uint32_t* bits, int V, int32_t* out_ids, int32_t* out_n, int32_t* out_local,
+                       int32_t* out_local_n, int budget_max, int* flags, cudaStream_t st) {
+    const int nwords = (V + 31) / 32;
+    launch_pdl(union_emit_kernel, dim3((nwords + 31) / 32), dim3(kEmitThreads), 0, st, bits, nwords, out_ids, out_n,
+               out_local, out_local_n, budget_max, flags);
+}
+
 static size_t union_fixed_bytes(int V, int per_seed) {
     const int nwords = (V + 31) / 32;
     return (size_t)nwords * 4 + (size_t)(3 * kMaxG + 1) * 4 + (size_t)kMaxG * per_seed * 4 + 64;
@@ -571,13 +640,13 @@ void launch_union(int V, const int32_t* static_ids, int n_static, const int32_t*
                   int n_graph_sem_seeds, int per_seed, int n_dyn, int R, int r,
                   int32_t* out_ids, int32_t* out_n, int32_t* out_local, int32_t* out_local_n,
                   int32_t* sem_out, int* sem_out_n, int debug, int* flags, cudaStream_t st, long long* trace,
-                  const int32_t* dyn_base, uint32_t* clear_hist) {
+                  const int32_t* dyn_base, uint32_t* clear_hist, uint32_t* emit_bits) {
     const size_t smem = (size_t)cap * 13 + union_fixed_bytes(V, per_seed) + 16;
     cudaFuncSetAttribute(union_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     launch_pdl(union_kernel, dim3(1), dim3(kUnionThreads), smem, st, V, static_ids, n_static, seeds, n_seed, cand_s, cand_id, n_cand_dev,
                                                   cap, n_sem, row_ptr, col, ctx_sel, n_ctx_sel_dev, n_graph_sem_seeds,
                                                   per_seed, n_dyn, R, r, out_ids, out_n, out_local, out_local_n,
-                                                  sem_out, sem_out_n, debug, flags, trace, dyn_base, clear_hist);
+                                                  sem_out, sem_out_n, debug, flags, trace, dyn_base, clear_hist, emit_bits);
 }
 
 }  // namespace es
