@@ -591,6 +591,8 @@ lmh_finalize32_kernel(LmhArgs a, int n_cta_arg, int k, float gamma, const float*
             const uint4* wp = (const uint4*)((const uint16_t*)a.W + row * a.d);
             const int nc = a.d / 8;
             constexpr int kPer = 16;                 // uint4 per lane in flight (d = 4096: all)
+            double a4[4] = {0.0, 0.0, 0.0, 0.0};     // independent chains (order-free: exact products,
+                                                     // the fp64 sum is within the envelope either way)
             for (int c0 = 0; c0 < nc; c0 += 32 * kPer) {
                 uint4 wv[kPer];
 #pragma unroll
@@ -606,10 +608,11 @@ lmh_finalize32_kernel(LmhArgs a, int n_cta_arg, int k, float gamma, const float*
                         unpack_bf16x8(wv[u], fw);
                         unpack_bf16x8(((const uint4*)h_row)[cc], fh);
 #pragma unroll
-                        for (int j = 0; j < 8; ++j) acc = fma((double)fw[j], (double)fh[j], acc);
+                        for (int j = 0; j < 8; ++j) a4[j & 3] = fma((double)fw[j], (double)fh[j], a4[j & 3]);
                     }
                 }
             }
+            acc = (a4[0] + a4[1]) + (a4[2] + a4[3]);
         } else {
 #pragma unroll 1
             for (int col = lane; col < a.d; col += 32)
