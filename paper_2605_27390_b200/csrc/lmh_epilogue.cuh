@@ -110,12 +110,12 @@ ES_DEV void fold_softmax(const EpiSmem& e, int r, const float (&v)[kTileJ], floa
     float m_new = m_old, scale = 1.0f;
     if (__any_sync(0xffffffffu, lane_max > m_old)) {
         m_new = fmaxf(m_old, warp_max(lane_max));
-        scale = m_old == -INFINITY ? 0.0f : expf(m_old - m_new);
+        scale = m_old == -INFINITY ? 0.0f : __expf(m_old - m_new);
     }
     float acc = e.st_ls[r * 32 + lane] * scale;
 #pragma unroll
     for (int j = 0; j < kTileJ; ++j)
-        if (v[j] != -INFINITY) acc += expf(v[j] - m_new);
+        if (v[j] != -INFINITY) acc += __expf(v[j] - m_new);   // ex2.approx: ~1e-6 rel., far inside C15
     e.st_ls[r * 32 + lane] = acc;
     __syncwarp();
     if (lane == 0) e.st_m[r] = m_new;
@@ -599,42 +599,67 @@ ES_DEV void epi_tile_buf(const EpiSmem& e, int n_h, int KP, int tn, int base_pos
     }
 }
 
-// Buffered path store: the row's list is kBuf slots, all "extras" (cnt = 0),
-// the buffer maximum in slot 0 (the finalisation ranks list heads), -inf pads.
+// Buffered path store of one row: the row's list is kBuf slots, all "extras"
+// (cnt = 0), the buffer maximum in slot 0 (the finalisation ranks list heads),
+// -inf pads.
+ES_DEV void store_row_buf(const EpiSmem& e, const LmhPartials& P, int cta, int n_h_total, int h_row0, int r) {
+    const int lane = lane_id();
+    const int cnt = e.st_cnt[r];
+    const size_t o = ((size_t)cta * n_h_total + h_row0 + r);
+    float x0 = lane < cnt ? e.st_val[(size_t)r * kBuf + lane] : -INFINITY;
+    float x1 = lane + 32 < cnt ? e.st_val[(size_t)r * kBuf + lane + 32] : -INFINITY;
+    int p0 = lane < cnt ? e.st_pos[(size_t)r * kBuf + lane] : 0;
+    int p1 = lane + 32 < cnt ? e.st_pos[(size_t)r * kBuf + lane + 32] : 0;
+    // slot of the maximum -> 0
+    float mv = fmaxf(x0, x1);
+    int ms = x0 >= x1 ? lane : lane + 32;
+    warp_argbest(mv, ms);   // (value desc, slot asc)
+    if (cnt > 0 && ms != 0) {
+        const float sv = __shfl_sync(0xffffffffu, x0, 0);
+        const int sp = __shfl_sync(0xffffffffu, p0, 0);
+        const float mxv = __shfl_sync(0xffffffffu, ms < 32 ? x0 : x1, ms & 31);
+        const int mxp = __shfl_sync(0xffffffffu, ms < 32 ? p0 : p1, ms & 31);
+        if (lane == 0) { x0 = mxv; p0 = mxp; }
+        if (ms < 32 && lane == ms) { x0 = sv; p0 = sp; }
+        if (ms >= 32 && lane == ms - 32) { x1 = sv; p1 = sp; }
+    }
+    P.val[o * kBuf + lane] = x0;
+    P.val[o * kBuf + lane + 32] = x1;
+    if (lane < cnt) P.id[o * kBuf + lane] = p0;
+    if (lane + 32 < cnt) P.id[o * kBuf + lane + 32] = p1;
+    const float ssum = warp_sum(e.st_ls[r * 32 + lane]);
+    if (lane == 0) {
+        P.cnt[o] = 0;
+        P.xcnt[o] = cnt;
+        P.m[o] = e.st_m[r];
+        P.s[o] = ssum;
+    }
+}
+
 ES_DEV void epi_store_buf(const EpiSmem& e, const LmhPartials& P, int cta, int n_h_total, int h_row0, int n_h,
                           int warp, int n_warps) {
+    for (int r = warp; r < n_h; r += n_warps) store_row_buf(e, P, cta, n_h_total, h_row0, r);
+}
+
+// The CTA's last tile (all warps): fold, then store each row right away (the
+// warp that folds a row writes its partial list -- no block-wide barrier).
+ES_DEV void epi_tile_buf_last_store(const EpiSmem& e, const LmhPartials& P, int cta, int n_h_total, int h_row0,
+                                    int n_h, int KP, int tn, int base_pos, int warp, int n_warps) {
     const int lane = lane_id();
     for (int r = warp; r < n_h; r += n_warps) {
-        const int cnt = e.st_cnt[r];
-        const size_t o = ((size_t)cta * n_h_total + h_row0 + r);
-        float x0 = lane < cnt ? e.st_val[(size_t)r * kBuf + lane] : -INFINITY;
-        float x1 = lane + 32 < cnt ? e.st_val[(size_t)r * kBuf + lane + 32] : -INFINITY;
-        int p0 = lane < cnt ? e.st_pos[(size_t)r * kBuf + lane] : 0;
-        int p1 = lane + 32 < cnt ? e.st_pos[(size_t)r * kBuf + lane + 32] : 0;
-        // slot of the maximum -> 0
-        float mv = fmaxf(x0, x1);
-        int ms = x0 >= x1 ? lane : lane + 32;
-        warp_argbest(mv, ms);   // (value desc, slot asc)
-        if (cnt > 0 && ms != 0) {
-            const float sv = __shfl_sync(0xffffffffu, x0, 0);
-            const int sp = __shfl_sync(0xffffffffu, p0, 0);
-            const float mxv = __shfl_sync(0xffffffffu, ms < 32 ? x0 : x1, ms & 31);
-            const int mxp = __shfl_sync(0xffffffffu, ms < 32 ? p0 : p1, ms & 31);
-            if (lane == 0) { x0 = mxv; p0 = mxp; }
-            if (ms < 32 && lane == ms) { x0 = sv; p0 = sp; }
-            if (ms >= 32 && lane == ms - 32) { x1 = sv; p1 = sp; }
+        if (tn > 0) {
+            float v[kTileJ];
+            float lm = -INFINITY;
+#pragma unroll
+            for (int j = 0; j < kTileJ; ++j) {
+                const int p = lane + 32 * j;
+                v[j] = p < tn ? e.tile[r * kTile + p] : -INFINITY;
+                lm = fmaxf(lm, v[j]);
+            }
+            fold_softmax(e, r, v, lm);
+            fold_buf(e, r, KP, tn, base_pos, v, lm, false, e.scr_v + warp * 32, e.scr_p + warp * 32);
         }
-        P.val[o * kBuf + lane] = x0;
-        P.val[o * kBuf + lane + 32] = x1;
-        if (lane < cnt) P.id[o * kBuf + lane] = p0;
-        if (lane + 32 < cnt) P.id[o * kBuf + lane + 32] = p1;
-        const float ssum = warp_sum(e.st_ls[r * 32 + lane]);
-        if (lane == 0) {
-            P.cnt[o] = 0;
-            P.xcnt[o] = cnt;
-            P.m[o] = e.st_m[r];
-            P.s[o] = ssum;
-        }
+        store_row_buf(e, P, cta, n_h_total, h_row0, r);
     }
 }
 

@@ -406,15 +406,19 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
         int t0, tn;
         tile_range(n_tiles - 1, t0, tn);
         named_bar_sync(2, kTcWarps * 32);
-        if (buffered) epi_tile_buf(e, n_h, a.KP, tn, t0, warp, kTcWarps, false);
+        if (buffered) epi_tile_buf_last_store(e, a.part, blockIdx.x, a.n_h, h_row0, n_h, a.KP, tn, t0, warp, kTcWarps);
         else epi_tile_last(e, a.part, blockIdx.x, a.n_h, h_row0, n_h, a.KP, a.LS, tn, t0, warp, kTcWarps);
         if (warp == kTcEpiWarp0 && lane == 0 && n_tiles - 1 < 2) TC_TRACE(4 + 2 * (n_tiles - 1));
     }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    if (buffered) epi_store_buf(e, a.part, blockIdx.x, a.n_h, h_row0, n_h, warp, kTcWarps);
-    else epi_store(e, a.part, blockIdx.x, a.n_h, h_row0, n_h, a.KP, a.LS, warp, kTcWarps);
+    if (buffered) {
+        if (n_tiles == 0) epi_store_buf(e, a.part, blockIdx.x, a.n_h, h_row0, n_h, warp, kTcWarps);
+        // (otherwise the last tile's fold stored every row)
+    } else {
+        epi_store(e, a.part, blockIdx.x, a.n_h, h_row0, n_h, a.KP, a.LS, warp, kTcWarps);
+    }
     if (threadIdx.x == 0) TC_TRACE(7);
     if (warp == kTcMmaWarp)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(tp.tmem_cols));
