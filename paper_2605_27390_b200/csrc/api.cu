@@ -519,6 +519,8 @@ static bool use_tc(const LmhArgs& a) {
     return a.n_h >= kTcMinRows;
 }
 
+constexpr int kRaggedSegRows = 128;   // rows per static segment of the ragged head
+
 struct LmhSegs {
     int nseg, seg_ctas, seg_rows;
     const int32_t* seg_pos;   // device [nseg+1] or null (every segment: the whole subset)
@@ -669,7 +671,11 @@ evospec_status evospec_subset_logits_topk_ragged(evospec_ctx* ctx, const void* W
     if (seg_ok) {
         // static block: one launch, row groups of <= 128 as segments over the same
         // static range (their CTAs read the same W rows at about the same time)
-        const int ns = (n_rows + kTcMaxRows - 1) / kTcMaxRows;
+        // rows per static segment: smaller segments leave shared memory for more
+        // pipeline stages but stream the static rows more often (EVOSPEC_SEG_ROWS)
+        const int seg_cap = getenv("EVOSPEC_SEG_ROWS") ? std::max(16, std::min(kTcMaxRows, atoi(getenv("EVOSPEC_SEG_ROWS"))))
+                                                       : kRaggedSegRows;
+        const int ns = (n_rows + seg_cap - 1) / seg_cap;
         const int per = (n_rows + ns - 1) / ns;
         int sh[kMaxSeg + 1];
         for (int b = 0; b <= ns; ++b) sh[b] = std::min(n_rows, b * per);
