@@ -23,12 +23,12 @@
 #include "common.cuh"
 #include "kernels.cuh"
 #include "lmh_epilogue.cuh"   // warp_kth_largest
+#include "finalize32.cuh"   // fin32_row (also fused into the LM-head kernel)
 
 namespace es {
 
 constexpr int kFinThreads = 256;
 constexpr int kFinCand = 1024;   // candidate buffer of the threshold filter (finalize32)
-constexpr int kFin32MaxD = 8192; // H row staged in smem by finalize32 (d <= this for the fast re-score)
 
 ES_DEV long long fin_gtime() {
     long long t;
@@ -312,357 +312,18 @@ lmh_finalize_kernel(LmhArgs a, int n_cta, int k, float gamma, const float* __res
 }
 
 
-// Finalisation for KP <= 32 (k <= 24). The partial lists have a fixed stride of
-// kFin32LS = 64 slots and unused slots hold -inf (epi_store), so a row's
-// entries form one flat array of n_cta * 64 values, loaded in one round trip
-// into registers (U float4 + int4 per thread):
-//   A. loads; per list (thread c): softmax state and th_c = its sorted entry
-//      KP-1 when the sorted part is full (th_c <= the row's KP-th best)
-//   B. th0 = max_c th_c; the entries >= th0 (every top-KP entry among them)
-//      are appended to a candidate buffer
-//   C. exact ranks: candidate i's rank is the number of candidates before it
-//      under (value desc, id asc) -- one thread per candidate, no sort network;
-//      ranks < KP give the sorted list. Warp 0 then finds the runs (consecutive
-//      entries closer than 2 delta) that reach the top k.
-//   D. exact fp64 re-score of those run members (one warp each)
-//   E. one warp sort by (exact-if-re-scored value desc, id asc); write the top k
-// Degenerate rows (more than kFin32RankMax candidates: massive ties, or no
-// full list) take a slower exact path: warp 0 merges sorted batches of 32.
-constexpr int kFin32Threads = 512;
-constexpr int kFin32LS = 64;
-constexpr int kFin32RankMax = 256;
-
-ES_DEV void sort32_rolled(float& v, int& p) {
-    const int lane = lane_id();
-#pragma unroll 1
-    for (int k = 2; k <= 32; k <<= 1) {
-#pragma unroll 1
-        for (int j = k >> 1; j > 0; j >>= 1) {
-            const float ov = __shfl_xor_sync(0xffffffffu, v, j);
-            const int op = __shfl_xor_sync(0xffffffffu, p, j);
-            const bool keep_better = ((lane & j) == 0) == ((lane & k) == 0);
-            if (keep_better == before(ov, op, v, p)) { v = ov; p = op; }
-        }
-    }
-}
 
 template <int U>
 __global__ void __launch_bounds__(kFin32Threads)
 lmh_finalize32_kernel(LmhArgs a, int n_cta_arg, int k, float gamma, const float* __restrict__ wmax_dev,
                       int32_t* __restrict__ topk_ids, float* __restrict__ topk_vals,
                       float* __restrict__ row_max, float* __restrict__ row_sumexp, int* flags) {
-    const int r = blockIdx.x;
-    const int KP = a.KP;
-    const int lane = lane_id(), warp = warp_id();
-    constexpr int nwarps = kFin32Threads / 32;
-    __shared__ float w_M[nwarps], w_S[nwarps], w_th[nwarps];
-    __shared__ int w_tot[nwarps];
-    __shared__ double red_d[nwarps];
-    __shared__ float cand_v[kFinCand];
-    __shared__ int cand_p[kFinCand];
-    __shared__ float c_v[32];
-    __shared__ int32_t c_id[32], c_gid[32];
-    __shared__ double c_e[32];
-    __shared__ int need_list[32];
-    __shared__ int n_need_s, nk_s, tot_s, cand_n;
-    __shared__ float lse_s, th_s;
-    __shared__ float s_head[kFin32Threads];
-    __shared__ __align__(16) uint16_t h_row[kFin32MaxD];
+    extern __shared__ __align__(16) unsigned char f32_sm[];
     pdl_trigger();
     pdl_wait();
-    if (threadIdx.x == 0) { FIN_TRACE(0); FIN_DT(0); }
-    // the row's lists: CTAs [c_base, c_base + n_cta) (segment mode: its segment's CTAs)
-    int n_cta = n_cta_arg, c_base = 0;
-    if (a.nseg > 0) {
-        int b = 0;
-        while (b + 1 < a.nseg && a.seg_h[b + 1] <= r) ++b;
-        if (a.seg_cta) {
-            c_base = a.seg_cta[b];
-            n_cta = a.seg_cta[b + 1] - c_base;
-        } else {
-            c_base = b * a.seg_ctas;
-            n_cta = a.seg_ctas;
-        }
-    }
-    // A. every global load at once
-    const int nq = n_cta * (kFin32LS / 4);
-    float4 vv[U];
-    int4 ii[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-        const int q = threadIdx.x + u * kFin32Threads;
-        vv[u] = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
-        if (q < nq) {
-            const size_t o = ((size_t)(c_base + (q >> 4)) * a.n_h + r) * kFin32LS + (q & 15) * 4;
-            vv[u] = __ldcg((const float4*)&a.part.val[o]);
-            ii[u] = __ldcg((const int4*)&a.part.id[o]);
-        }
-    }
-    float cm_ = -INFINITY, cs_ = 0.0f, thl = -INFINITY;
-    if ((int)threadIdx.x < n_cta) {
-        const size_t o = (size_t)(c_base + threadIdx.x) * a.n_h + r;
-        cm_ = __ldcg(&a.part.m[o]);
-        cs_ = __ldcg(&a.part.s[o]);
-        const int cn = __ldcg(&a.part.cnt[o]);
-        const float vk = __ldcg(&a.part.val[o * kFin32LS + KP - 1]);
-        if (cn >= KP) thl = vk;
-        s_head[threadIdx.x] = __ldcg(&a.part.val[o * kFin32LS]);   // the list maximum (sorted head)
-    }
-    const float wmax = __ldg(wmax_dev);
-    double hacc = 0.0;
-    const bool h_fast = a.h_dtype == 0 && a.d % 8 == 0 && a.d <= kFin32MaxD;
-    if (h_fast) {
-        const uint4* hp = (const uint4*)((const uint16_t*)a.H + (size_t)r * a.d);
-        for (int c = threadIdx.x; c < a.d / 8; c += kFin32Threads) {
-            const uint4 hv = hp[c];
-            ((uint4*)h_row)[c] = hv;
-            float f[8];
-            unpack_bf16x8(hv, f);
-#pragma unroll
-            for (int j = 0; j < 8; ++j) hacc = fma((double)f[j], (double)f[j], hacc);
-        }
-    } else {
-#pragma unroll 1
-        for (int col = threadIdx.x; col < a.d; col += kFin32Threads) {
-            const double h = load_elem(a.H, a.h_dtype, (size_t)r * a.d + col);
-            hacc = fma(h, h, hacc);
-        }
-    }
-    if (threadIdx.x == 0) { cand_n = 0; th_s = -INFINITY; }
-    {
-        int tcnt = 0;
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-            tcnt += (vv[u].x != -INFINITY) + (vv[u].y != -INFINITY) + (vv[u].z != -INFINITY) + (vv[u].w != -INFINITY);
-        const float Mw = warp_max(cs_ > 0.0f ? cm_ : -INFINITY);
-        const float Sw = warp_sum(cs_ > 0.0f ? cs_ * expf(cm_ - Mw) : 0.0f);
-        thl = warp_max(thl);
-        tcnt = warp_sum_i(tcnt);
-        hacc = warp_sum_d(hacc);
-        if (lane == 0) { w_M[warp] = Mw; w_S[warp] = Sw; w_th[warp] = thl; w_tot[warp] = tcnt; red_d[warp] = hacc; }
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) { FIN_TRACE(1); FIN_DT(1); }
-    // B. threshold: the KP-th largest list head (KP distinct entries) and any full
-    //    list's entry KP-1 both bound the row's KP-th best from below
-    if ((int)threadIdx.x < n_cta && n_cta >= KP) {
-        const float hv = s_head[threadIdx.x];
-        int gt = 0, ge = 0;
-#pragma unroll 4
-        for (int c = 0; c < n_cta; ++c) {
-            const float o = s_head[c];
-            gt += o > hv;
-            ge += o >= hv;
-        }
-        if (hv != -INFINITY && gt < KP && KP <= ge) th_s = hv;   // the KP-th largest head value
-    }
-    __syncthreads();
-    float th0 = th_s;
-#pragma unroll
-    for (int w = 0; w < nwarps; ++w) th0 = fmaxf(th0, w_th[w]);
-    if (warp == 0) {   // softmax combine and entry count (lanes = warps)
-        const bool have = lane < nwarps && w_S[lane] > 0.0f;
-        const float M = warp_max(have ? w_M[lane] : -INFINITY);
-        const float S = warp_sum(have ? w_S[lane] * expf(w_M[lane] - M) : 0.0f);
-        const int tot = warp_sum_i(lane < nwarps ? w_tot[lane] : 0);
-        if (lane == 0) {
-            row_max[r] = M;
-            row_sumexp[r] = S;
-            lse_s = S > 0.0f ? M + logf(S) : -INFINITY;
-            tot_s = tot;
-        }
-    }
-    {
-        auto keep = [&](float x) { return x != -INFINITY && x >= th0; };
-        int nk = 0;
-#pragma unroll
-        for (int u = 0; u < U; ++u) nk += keep(vv[u].x) + keep(vv[u].y) + keep(vv[u].z) + keep(vv[u].w);
-        if (nk) {
-            int o = atomicAdd(&cand_n, nk);
-            auto put = [&](float x, int id) {
-                if (keep(x)) {
-                    if (o < kFinCand) { cand_v[o] = x; cand_p[o] = id; }
-                    ++o;
-                }
-            };
-#pragma unroll
-            for (int u = 0; u < U; ++u) { put(vv[u].x, ii[u].x); put(vv[u].y, ii[u].y); put(vv[u].z, ii[u].z); put(vv[u].w, ii[u].w); }
-        }
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) { FIN_TRACE(2); FIN_DT(2); }
-    const int ncand = cand_n;
-    if (ncand <= kFin32RankMax) {
-        // C1. exact ranks, one thread per candidate
-        if ((int)threadIdx.x < ncand) {
-            const float v = cand_v[threadIdx.x];
-            const int p = cand_p[threadIdx.x];
-            int rank = 0;
-#pragma unroll 4
-            for (int j = 0; j < ncand; ++j) rank += before(cand_v[j], cand_p[j], v, p);
-            if (rank < KP) { c_v[rank] = v; c_id[rank] = p; }
-        }
-        if (threadIdx.x == 0) nk_s = min(ncand, KP);
-    } else if (warp == 0) {
-        // C1'. degenerate rows: sorted batches of 32 merged into the register list,
-        //      from the candidate buffer or (overflow) the whole row in the partials
-        float Lv = -INFINITY, th = -INFINITY;
-        int Lp = 0x7fffffff, thp = 0x7fffffff, cnt = 0;
-        const bool all = ncand > kFinCand;
-        const int nb = all ? ((nq + 31) / 32) * 4 : (ncand + 31) / 32;
-#pragma unroll 1
-        for (int b = 0; b < nb; ++b) {
-            float bv = -INFINITY;
-            int bp = 0x7fffffff;
-            if (!all) {
-                const int i = b * 32 + lane;
-                if (i < ncand) { bv = cand_v[i]; bp = cand_p[i]; }
-            } else {
-                const int q = (b >> 2) * 32 + lane, comp = b & 3;
-                if (q < nq) {
-                    const size_t o = ((size_t)(c_base + (q >> 4)) * a.n_h + r) * kFin32LS + (q & 15) * 4 + comp;
-                    bv = __ldcg(&a.part.val[o]);
-                    bp = __ldcg(&a.part.id[o]);
-                }
-            }
-            if (cnt == KP && !before(bv, bp, th, thp)) { bv = -INFINITY; bp = 0x7fffffff; }
-            const unsigned m = __ballot_sync(0xffffffffu, bv != -INFINITY);
-            if (!m) continue;
-            sort32_rolled(bv, bp);
-            const float rv = __shfl_sync(0xffffffffu, bv, 31 - lane);
-            const int rp = __shfl_sync(0xffffffffu, bp, 31 - lane);
-            if (before(rv, rp, Lv, Lp)) { Lv = rv; Lp = rp; }
-#pragma unroll 1
-            for (int j = 16; j > 0; j >>= 1) {
-                const float ov = __shfl_xor_sync(0xffffffffu, Lv, j);
-                const int op = __shfl_xor_sync(0xffffffffu, Lp, j);
-                if (((lane & j) == 0) == before(ov, op, Lv, Lp)) { Lv = ov; Lp = op; }
-            }
-            cnt = min(cnt + __popc(m), KP);
-            if (cnt == KP) { th = __shfl_sync(0xffffffffu, Lv, KP - 1); thp = __shfl_sync(0xffffffffu, Lp, KP - 1); }
-        }
-        c_v[lane] = Lv;
-        c_id[lane] = Lp;
-        if (lane == 0) nk_s = cnt;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) { FIN_TRACE(3); FIN_DT(3); }
-    if (warp == 0) {
-        // C2. runs: consecutive kept entries closer than 2 delta; those reaching the top k are re-scored
-        const int cnt = nk_s, tot = tot_s;
-        const float Lv = lane < cnt ? c_v[lane] : -INFINITY;
-        c_gid[lane] = lane < cnt ? __ldg(&a.subset[c_id[lane]]) : -1;   // position -> vocabulary id
-        double hn = 0.0;
-#pragma unroll
-        for (int w = 0; w < nwarps; ++w) hn += red_d[w];
-        const double delta = (double)gamma * sqrt(hn) * (double)wmax * (double)a.inv_temp;
-        const float nv = __shfl_down_sync(0xffffffffu, Lv, 1);
-        const bool close = lane + 1 < cnt && (double)Lv - (double)nv <= 2.0 * delta + 2.4e-7 * fabs((double)Lv);
-        const unsigned cm = __ballot_sync(0xffffffffu, close);   // bit i: entry i and i+1 in one run
-        // run start: just above the highest open link below the lane
-        const unsigned below = ~cm & ((1u << lane) - 1u);
-        const int st_i = below ? 32 - __clz(below) : 0;
-        const bool multi = (lane > 0 && ((cm >> (lane - 1)) & 1u)) || ((cm >> lane) & 1u);
-        // members of runs reaching the top k; with exact_vals (the triple feeds a merge
-        // across shards or across the static / dynamic parts of the ragged head) every
-        // top-k entry, so that the merge compares the exact logits (rounded to fp32)
-        const bool need = lane < cnt && ((multi && st_i < k) || (a.exact_vals && lane < k));
-        const unsigned nm = __ballot_sync(0xffffffffu, need);
-        if (need) need_list[__popc(nm & ((1u << lane) - 1u))] = lane;
-        // uncertified: the run holding index k-1 reaches the last kept entry while entries were dropped
-        const unsigned open_from_k = ~cm & ~((1u << (k - 1)) - 1u);   // open links at index >= k-1
-        const int end_k = open_from_k ? __ffs(open_from_k) - 1 : 31;
-        const bool unc = (k - 1 < cnt && min(end_k, cnt - 1) == cnt - 1 && tot > cnt && cnt >= k) ||
-                         !(delta >= 0.0) || isinf(delta);
-        if (lane == 0) {
-            if (unc) atomicOr(flags, kFlagUncertified);
-            n_need_s = __popc(nm);
-        }
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) { FIN_TRACE(4); FIN_DT(4); }
-    // D. exact re-score of the flagged entries (one warp each, W loads in flight)
-    const int nn = n_need_s;
-    for (int q = warp; q < nn; q += nwarps) {
-        const int c = need_list[q];
-        const size_t row = (size_t)(c_gid[c] / a.R);
-        double acc = 0.0;
-        if (a.w_dtype == 0 && h_fast) {
-            const uint4* wp = (const uint4*)((const uint16_t*)a.W + row * a.d);
-            const int nc = a.d / 8;
-            constexpr int kPer = 16;                 // uint4 per lane in flight (d = 4096: all)
-            double a4[4] = {0.0, 0.0, 0.0, 0.0};     // independent chains (order-free: exact products,
-                                                     // the fp64 sum is within the envelope either way)
-            for (int c0 = 0; c0 < nc; c0 += 32 * kPer) {
-                uint4 wv[kPer];
-#pragma unroll
-                for (int u = 0; u < kPer; ++u) {
-                    const int cc = c0 + lane + 32 * u;
-                    wv[u] = cc < nc ? __ldg(&wp[cc]) : make_uint4(0, 0, 0, 0);
-                }
-#pragma unroll
-                for (int u = 0; u < kPer; ++u) {
-                    const int cc = c0 + lane + 32 * u;
-                    if (cc < nc) {
-                        float fw[8], fh[8];
-                        unpack_bf16x8(wv[u], fw);
-                        unpack_bf16x8(((const uint4*)h_row)[cc], fh);
-#pragma unroll
-                        for (int j = 0; j < 8; ++j) a4[j & 3] = fma((double)fw[j], (double)fh[j], a4[j & 3]);
-                    }
-                }
-            }
-            acc = (a4[0] + a4[1]) + (a4[2] + a4[3]);
-        } else {
-#pragma unroll 1
-            for (int col = lane; col < a.d; col += 32)
-                acc = fma(load_elem(a.W, a.w_dtype, row * a.d + col), load_elem(a.H, a.h_dtype, (size_t)r * a.d + col), acc);
-        }
-        acc = warp_sum_d(acc);
-        if (lane == 0) c_e[c] = acc * (double)a.inv_temp;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) { FIN_TRACE(5); FIN_DT(5); }
-    // E. one sort by (exact value if re-scored else fp32 value desc, id asc): runs are
-    //    more than 2 delta apart, so this is the exact order; write the top k
-    if (warp == 0) {
-        const int cnt = nk_s;
-        bool flagged = false;
-        for (int q = 0; q < nn; ++q) flagged |= need_list[q] == lane;
-        double e = lane < cnt ? (flagged ? c_e[lane] : (double)c_v[lane]) : -INFINITY;
-        int id = lane < cnt ? c_id[lane] : 0x7fffffff;   // subset position (order = id order)
-        int gid = c_gid[lane];
-        if (nn > 0) {   // only re-scored runs can change the order
-#pragma unroll 1
-            for (int kk = 2; kk <= 32; kk <<= 1) {
-#pragma unroll 1
-                for (int j = kk >> 1; j > 0; j >>= 1) {
-                    const double oe = __shfl_xor_sync(0xffffffffu, e, j);
-                    const int oi = __shfl_xor_sync(0xffffffffu, id, j);
-                    const int og = __shfl_xor_sync(0xffffffffu, gid, j);
-                    const bool keep_better = ((lane & j) == 0) == ((lane & kk) == 0);
-                    if (keep_better == before(oe, oi, e, id)) { e = oe; id = oi; gid = og; }
-                }
-            }
-        }
-        if (lane < k) {
-            const int oid = lane < cnt ? gid : -1;
-            const float ovl = lane < cnt ? (float)e : -INFINITY;
-            topk_ids[(size_t)r * k + lane] = oid;
-            topk_vals[(size_t)r * k + lane] = ovl;
-            if (a.m_ids) {   // fused single-shard merge (R = 1)
-                a.m_ids[(size_t)r * k + lane] = oid;
-                a.m_vals[(size_t)r * k + lane] = ovl;
-                if (a.m_probs) a.m_probs[(size_t)r * k + lane] = lane < cnt ? expf(ovl - lse_s) : 0.0f;
-                if (lane == 0) a.m_lse[r] = lse_s;
-            }
-        }
-        if (lane == 0) {
-            FIN_TRACE(6);
-            FIN_DT(6);
-            if (a.trace && blockIdx.x < 148) a.trace[148 * 8 + (size_t)blockIdx.x * 8 + 7] = ncand;
-        }
-    }
+    const Fin32Smem sm = fin32_carve(f32_sm, kFin32Threads);
+    fin32_row<U, kFin32Threads>(a, blockIdx.x, n_cta_arg, k, gamma, wmax_dev, topk_ids, topk_vals, row_max,
+                                row_sumexp, flags, sm);
 }
 
 void launch_lmh_finalize(const LmhArgs& a, int n_cta, int k, const float* wmax_dev, int32_t* topk_ids,
@@ -671,7 +332,7 @@ void launch_lmh_finalize(const LmhArgs& a, int n_cta, int k, const float* wmax_d
     if (a.KP <= 32 && a.LS == kFin32LS && n_cta * (kFin32LS / 4) <= 10 * kFin32Threads) {
         // one CTA per SM while the rows fit one wave (the dynamic allocation is only
         // a placement hint: two CTAs sharing an SM measured slower); more rows pack
-        const size_t smem = a.n_h <= kNumSMs ? 120 * 1024 : 0;
+        const size_t smem = std::max(fin32_smem_bytes(kFin32Threads), (size_t)(a.n_h <= kNumSMs ? 120 * 1024 : 0));
         if (n_cta * (kFin32LS / 4) <= 5 * kFin32Threads) {
             static thread_local bool set5 = false;   // (placement hint size is fixed)
             if (!set5) set5 = cudaFuncSetAttribute(lmh_finalize32_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize,
