@@ -103,6 +103,7 @@ struct evospec_ctx {
                                   // clears it after the selection has read it)
     bool hist_dirty = false;      // a build stopped between its scan and its union: clear first
     uint32_t* ubits = nullptr;    // [V/32] union bitmap handed to the emit kernel
+    unsigned long long* fin_ctr = nullptr;   // LM-head fused finalisation arrival counter
     uint32_t* hist = nullptr;     // [12][4096] further select passes
     int cand_cap = 0;             // candidate superset capacity (union smem)
     int* cand_count = nullptr;
@@ -226,7 +227,7 @@ evospec_status evospec_destroy(evospec_ctx* ctx) {
                     ctx->flags, ctx->wmax, ctx->g_ids, ctx->g_vals, ctx->g_m, ctx->g_s, ctx->st_q, ctx->st_H,
                     ctx->st_seeds, ctx->st_ctx, ctx->st_S, ctx->st_nS, ctx->st_local, ctx->st_nlocal,
                     ctx->st_tids, ctx->st_tvals, ctx->st_m, ctx->st_s, ctx->st_oids, ctx->st_ovals,
-                    ctx->st_lse, ctx->st_probs, ctx->ubits, ctx->rg_ids, ctx->rg_vals, ctx->rg_m, ctx->rg_s, ctx->rg_seg, ctx->rg_segcta};
+                    ctx->st_lse, ctx->st_probs, ctx->ubits, ctx->fin_ctr, ctx->rg_ids, ctx->rg_vals, ctx->rg_m, ctx->rg_s, ctx->rg_seg, ctx->rg_segcta};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (ctx->comm && nccl().loaded) nccl().CommDestroy(ctx->comm);
@@ -277,7 +278,7 @@ evospec_status evospec_create(evospec_ctx** out, const evospec_config* cfg, int 
                     cap_v, c.V);
     }
     const size_t cap = (size_t)x->cand_cap;
-    A(dalloc(&x->s64, V)); A(dalloc(&x->key32, V)); A(dalloc(&x->hist12, kHistBins)); A(dalloc(&x->ubits, (V + 31) / 32)); A(cudaMemset(x->hist12, 0, kHistBins * sizeof(uint32_t)));
+    A(dalloc(&x->s64, V)); A(dalloc(&x->key32, V)); A(dalloc(&x->hist12, kHistBins)); A(dalloc(&x->ubits, (V + 31) / 32)); A(dalloc(&x->fin_ctr, 1)); A(cudaMemset(x->fin_ctr, 0, 8)); A(cudaMemset(x->hist12, 0, kHistBins * sizeof(uint32_t)));
     A(dalloc(&x->hist, 12 * kHistBins));
     A(dalloc(&x->cand_count, 4)); A(dalloc(&x->cand_s, cap)); A(dalloc(&x->cand_id, cap));
     A(dalloc(&x->loc_count, 4)); A(dalloc(&x->loc_s, sem)); A(dalloc(&x->loc_id, sem));
@@ -581,6 +582,20 @@ static evospec_status lmh_impl(evospec_ctx* ctx, const void* W, int64_t n_w_rows
     {
         StageTimer t(ctx, EVOSPEC_STAGE_LMH, st);
         if (use_tc(a)) {
+            // finalisation fused into the tensor-core kernel's last CTAs (k + 8 <= 32, no
+            // segments, rows <= CTAs): opt-in (EVOSPEC_FUSED_FIN=1) -- measured slower than
+            // the separate PDL-chained kernel (416 threads per row instead of 512, and no
+            // earlier start: the arrival wait costs what the launch gap did)
+            static const bool fused_fin = getenv("EVOSPEC_FUSED_FIN") != nullptr;
+            if (fused_fin && a.KP <= 32 && a.LS == 64 && !segs && n_h <= lmh_tc_grid()) {
+                a.fuse_fin = 1;
+                a.fin_k = k;
+                a.fin_gamma = kTcGamma;
+                a.fin_wmax = ctx->wmax;
+                a.fin_ctr = ctx->fin_ctr;
+                a.fin_ids = topk_ids; a.fin_vals = topk_vals; a.fin_m = row_max; a.fin_s = row_sumexp;
+                a.fin_flags = ctx->flags;
+            }
             CUDA_TRY(launch_lmh_tc(a, st));
             ctx->launches += 1;
             n_cta = segs ? segs->seg_ctas : lmh_tc_grid();
@@ -595,7 +610,7 @@ static evospec_status lmh_impl(evospec_ctx* ctx, const void* W, int64_t n_w_rows
             }
         }
     }
-    {
+    if (!a.fuse_fin) {
         StageTimer t(ctx, EVOSPEC_STAGE_FINALIZE, st);
         launch_lmh_finalize(a, n_cta, k, ctx->wmax, topk_ids, topk_vals, row_max, row_sumexp, ctx->flags, st,
                             gamma);

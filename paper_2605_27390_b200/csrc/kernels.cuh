@@ -81,6 +81,13 @@ struct LmhArgs {
     // optional fused single-shard merge outputs (R = 1): ids/vals [n_h][k], lse [n_h], probs [n_h][k]
     int32_t* m_ids; float* m_vals; float* m_lse; float* m_probs;
     LmhPartials part;
+    // fused finalisation (tensor-core path, k + 8 <= 32, no segments): the last n_h
+    // CTAs to finish each finalise one row once every CTA has stored its lists
+    int fuse_fin, fin_k;
+    float fin_gamma;
+    const float* fin_wmax;
+    unsigned long long* fin_ctr;   // monotone arrival counter (G arrivals per launch)
+    int32_t* fin_ids; float* fin_vals; float* fin_m; float* fin_s; int* fin_flags;
 };
 
 // This CTA's contiguous share [p0, p1) of the subset positions: all of

@@ -29,6 +29,7 @@
 #include "common.cuh"
 #include "kernels.cuh"
 #include "lmh_epilogue.cuh"
+#include "finalize32.cuh"
 
 namespace es {
 
@@ -210,7 +211,9 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
     int32_t* rows_sm = (int32_t*)(base + tp.off_rows);           // [2][128] gather rows per tile
 
     const int warp = warp_id(), lane = lane_id();
-    pdl_trigger();
+    // with the fused finalisation some CTAs wait for all others: dependents are
+    // triggered only at the end, so they cannot take an SM one of ours still needs
+    if (!a.fuse_fin) pdl_trigger();
     pdl_wait();   // the subset (and n_S) come from the previous kernel on the stream
     int p0, p1;
     if (seg_b >= 0) {
@@ -422,6 +425,39 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
     if (threadIdx.x == 0) TC_TRACE(7);
     if (warp == kTcMmaWarp)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(tp.tmem_cols));
+    if (a.fuse_fin) {
+        // fused finalisation: arrival order over a monotone counter (G per launch);
+        // the last n_h arrivals each finalise one row after all G have stored
+        __threadfence();
+        __syncthreads();
+        int* tick = (int*)base;   // the ring is free now
+        if (threadIdx.x == 0) {
+            const unsigned long long t = atomicAdd(a.fin_ctr, 1ull);
+            const unsigned long long G = gridDim.x;
+            const int arrival = (int)(t % G);
+            tick[0] = arrival;
+            if (arrival >= (int)G - n_h) {
+                const unsigned long long target = t - (unsigned long long)arrival + G;
+                unsigned long long cur;
+                for (;;) {
+                    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(cur) : "l"(a.fin_ctr) : "memory");
+                    if (cur >= target) break;
+                    __nanosleep(32);
+                }
+            }
+        }
+        __syncthreads();
+        const int arrival = tick[0];
+        if (arrival >= (int)gridDim.x - n_h) {
+            __threadfence();
+            __syncthreads();
+            const int row = arrival - ((int)gridDim.x - n_h);
+            const Fin32Smem sm = fin32_carve(base + 1024, kTcWarps * 32);
+            fin32_row<6, kTcWarps * 32>(a, row, gridDim.x, a.fin_k, a.fin_gamma, a.fin_wmax, a.fin_ids, a.fin_vals,
+                                        a.fin_m, a.fin_s, a.fin_flags, sm);
+        }
+        pdl_trigger();
+    }
 }
 
 // ------------------------------------------------------------------ host

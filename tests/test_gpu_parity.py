@@ -458,3 +458,32 @@ def test_odd_shapes_static_only_and_ragged_vocab(V, d, n_dyn):
     got = run_path(P)
     ref = G.oracle_step(oracle, P)
     check(P, got, ref, P["k"])
+
+
+def test_fused_finalisation_opt_in(monkeypatch):
+    """EVOSPEC_FUSED_FIN=1: the finalisation runs in the LM-head kernel's last-arriving
+    CTAs; the results equal the oracle (the env is read once per process, so this runs
+    in a subprocess)."""
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np, torch, oracle, paper_2605_27390_b200 as es\n"
+        "from tests import gpu_helpers as G\n"
+        "P = G.make_problem(90, dtype='bf16', V=20000, d=256, n_static=2000, n_sem=300, n_dyn=500, n_h=20, k=10)\n"
+        "ref = G.oracle_step(oracle, P)\n"
+        "S = ref['S']\n"
+        "ctx = es.Context(V=P['V'], d=P['d'], w_dtype=torch.bfloat16, h_dtype=torch.bfloat16, max_subset=S.size,\n"
+        "                 max_rows=20, max_k=16, max_sem=300)\n"
+        "W = G.to_dev(P['W']); ctx.prepare_weights(W)\n"
+        "nd = torch.tensor([S.size], dtype=torch.int32, device='cuda')\n"
+        "for _ in range(3):\n"
+        "    ids, vals, m, s = ctx.subset_logits_topk(W, G.to_dev(P['H']), G.to_dev(S), nd, S.size, 10)\n"
+        "    torch.cuda.synchronize()\n"
+        "    G.assert_triple_close(ids.cpu().numpy(), vals.cpu().numpy(), m.cpu().numpy(), s.cpu().numpy(),\n"
+        "                          ref['triple'], 10)\n"
+        "assert ctx.get_flags() == 0\n"
+        "print('fused ok')\n")
+    env = dict(__import__("os").environ, EVOSPEC_FUSED_FIN="1")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300,
+                       cwd=__import__("os").path.dirname(__import__("os").path.dirname(__file__)))
+    assert r.returncode == 0 and "fused ok" in r.stdout, r.stdout + r.stderr
