@@ -487,3 +487,46 @@ def test_fused_finalisation_opt_in(monkeypatch):
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300,
                        cwd=__import__("os").path.dirname(__import__("os").path.dirname(__file__)))
     assert r.returncode == 0 and "fused ok" in r.stdout, r.stdout + r.stderr
+
+
+@pytest.mark.slow
+def test_sharded_d8192_full_vocab_sampled():
+    """Config Sh (d = 8192, V = 128256) at the full vocabulary in the launch configuration
+    the bench times: R = 1 (merged call) and R = 2 interleaved shards on one GPU merged
+    with merge_shards. The oracle checks 3 sampled rows of the 60 (63 G MAC for all)."""
+    V, d, n_h, k = 128256, 8192, 60, 10
+    W = synth_matrix(40, V, d, 0.02, "bf16")
+    H = synth_matrix(41, n_h, d, 1.0, "bf16")
+    S = np.arange(V, dtype=np.int32)
+    rows = [0, 29, 59]
+    ref = oracle.subset_logits_topk(W, H[rows], S, k)
+    Wd, Hd = G.to_dev(W, DEV), G.to_dev(H, DEV)
+    ctx = es.Context(V=V, d=d, w_dtype=torch.bfloat16, h_dtype=torch.bfloat16, max_subset=V, max_rows=n_h,
+                     max_k=k, max_sem=1, max_seeds=1)
+    ctx.prepare_weights(Wd)
+    nd = torch.tensor([V], dtype=torch.int32, device=DEV)
+    ids, vals, lse, probs = ctx.subset_logits_topk_merged(Wd, Hd, G.to_dev(S, DEV), nd, V, k)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(ids.cpu().numpy()[rows], ref["ids"])
+    assert np.all(np.abs(lse.cpu().numpy()[rows] - ref["lse"]) <= G.LOGIT_TOL * (1 + np.abs(ref["lse"])))
+    assert np.max(np.abs(probs.cpu().numpy()[rows] - ref["probs"])) <= G.PROB_TOL
+    del Wd
+    trips = []
+    for r in range(2):
+        Wr = G.to_dev(np.ascontiguousarray(W[r::2]), DEV)
+        cr = es.Context(V=V, d=d, w_dtype=torch.bfloat16, h_dtype=torch.bfloat16, n_shards=2, shard_rank=r,
+                        max_subset=V, max_rows=n_h, max_k=k, max_sem=1, max_seeds=1)
+        cr.prepare_weights(Wr)
+        Sr = S[S % 2 == r]
+        ndr = torch.tensor([Sr.size], dtype=torch.int32, device=DEV)
+        trips.append(cr.subset_logits_topk(Wr, Hd, G.to_dev(Sr, DEV), ndr, Sr.size, k))
+        torch.cuda.synchronize()
+        assert cr.get_flags() == 0
+        del Wr
+    mctx = es.Context(V=V, d=d, w_dtype=torch.bfloat16, h_dtype=torch.bfloat16, n_shards=2, shard_rank=0,
+                      max_subset=V, max_rows=n_h, max_k=k, max_sem=1, max_seeds=1)
+    st = [torch.stack([t[i] for t in trips]) for i in range(4)]
+    oi, ov, ol, op = mctx.merge_shards(*st, n_h=n_h, k=k)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(oi.cpu().numpy()[rows], ref["ids"])
+    assert np.max(np.abs(op.cpu().numpy()[rows] - ref["probs"])) <= G.PROB_TOL
