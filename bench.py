@@ -118,17 +118,26 @@ def oracle_sample(c, W, H, q, static, row_ptr, col, seeds, rows):
                             n_graph_sem_seeds=c["n_graph_sem_seeds"], per_seed=c["per_seed"], n_dyn=c["n_dyn"])
     t1 = time.perf_counter()
     tri = oracle.subset_logits_topk(W, H[:rows], b["S"], c["k"])
-    oracle.merge(tri["ids"][None], tri["vals"][None], tri["m"][None], tri["s"][None], c["k"])
+    mrg = oracle.merge(tri["ids"][None], tri["vals"][None], tri["m"][None], tri["s"][None], c["k"])
     t2 = time.perf_counter()
-    return t1 - t0, (t2 - t1) / rows
+    return t1 - t0, (t2 - t1) / rows, mrg
 
 
-def cpu_baseline_line(c, W, H, q, static, row_ptr, col, seeds, rows=24):
-    tb, tr = oracle_sample(c, W, H, q, static, row_ptr, col, seeds, rows)
+def cpu_baseline_line(c, W, H, q, static, row_ptr, col, seeds, rows=24, gpu_out=None):
+    """The oracle timed on the host; with the GPU step's outputs, also the parity of
+    the timed workload on the sampled rows (ids exact, LSE / probability errors)."""
+    tb, tr, mrg = oracle_sample(c, W, H, q, static, row_ptr, col, seeds, rows)
     step = tb + c["n_h"] * tr
-    return dict(value=c["n_h"] / step, unit="tokens/s", cores=1, kind="oracle",
+    line = dict(value=c["n_h"] / step, unit="tokens/s", cores=1, kind="oracle",
                 sample=f"1 subset build ({tb:.2f} s) + {rows} of the 60 tree rows ({tr:.3f} s/row) of one "
                        f"llama step, single-threaded plain C fp64; value = 60 / (t_build + 60 t_row)")
+    parity = None
+    if gpu_out is not None:
+        ids, vals, lse, probs = (np.asarray(t)[:rows] for t in gpu_out)
+        parity = dict(rows_checked=rows, ids_exact=bool(np.array_equal(ids, mrg["ids"])),
+                      max_abs_lse_err_rel=float(np.max(np.abs(lse - mrg["lse"]) / (1 + np.abs(mrg["lse"])))),
+                      max_abs_prob_err=float(np.max(np.abs(probs - mrg["probs"]))))
+    return line, parity
 
 
 def run_reference(args):
@@ -142,7 +151,7 @@ def run_reference(args):
     tbs, trs = [], []
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        tb, tr = oracle_sample(c, W, H, q, static, row_ptr, col, seeds, rows)
+        tb, tr, _ = oracle_sample(c, W, H, q, static, row_ptr, col, seeds, rows)
         tbs.append(tb)
         trs.append(tr)
     wall = time.perf_counter() - t0
@@ -311,10 +320,11 @@ def run_ours(args):
 
     tokens = n_h * args.steps
     value = tokens / (ms * 1e-3)
-    cpu = None
+    cpu = parity = None
     if world == 1 and not args.no_cpu_baseline:
         c2, W2, H2, q2, st2, rp2, col2, s2 = make_workload()
-        cpu = cpu_baseline_line(c2, W2, H2, q2, st2, rp2, col2, s2)
+        gpu_out = [t.cpu().numpy() for t in out_d]   # the device-timed loop's last step
+        cpu, parity = cpu_baseline_line(c2, W2, H2, q2, st2, rp2, col2, s2, gpu_out=gpu_out)
         cpu["cores"] = 1
     line = dict(metric=METRIC, value=value, unit="tokens/s", n_gpus=world, steps=args.steps, warmup=args.warmup,
                 ms_per_step=ms / args.steps, higher_is_better=True, scaling="strong", vs_baseline=None,
@@ -328,7 +338,7 @@ def run_ours(args):
                          d2h_bytes_per_step=d2h),
                 gpu_launches=launches, clocks=clk, breakdown=breakdown, device_flags=flags,
                 lmh_tokens_per_s=n_h / (per["lmh"] + per["finalize"] + per["merge"]) * 1e3 if per["lmh"] else None,
-                subset_sweep=sweep, batched=bt, extra_configs=extra)
+                subset_sweep=sweep, batched=bt, extra_configs=extra, parity_vs_oracle=parity)
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -490,9 +500,10 @@ def subset_sweep(ctx, Wd, Hd, n_h, k, V, d, dev, args):
         torch.cuda.synchronize()
         times = [a.elapsed_time(b) for a, b in evs[args.warmup:]]
         t = statistics.median(times) * 1e-3
+        qs = np.percentile(np.asarray(times) * 1e3, [10, 90])
         nbytes = n_S * d * 2 + n_h * d * 2 + n_S * 4
-        out.append(dict(n_S=n_S, us=t * 1e6, tokens_per_s=n_h / t, GBps=nbytes / t / 1e9,
-                        frac_of_copy_peak=nbytes / t / 1e9 / load_peaks()["hbm_gbs"]))
+        out.append(dict(n_S=n_S, us=t * 1e6, us_p10=float(qs[0]), us_p90=float(qs[1]), tokens_per_s=n_h / t,
+                        GBps=nbytes / t / 1e9, frac_of_copy_peak=nbytes / t / 1e9 / load_peaks()["hbm_gbs"]))
     del flush
     return out
 
