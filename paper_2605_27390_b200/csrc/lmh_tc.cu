@@ -214,6 +214,23 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
     // with the fused finalisation some CTAs wait for all others: dependents are
     // triggered only at the end, so they cannot take an SM one of ours still needs
     if (!a.fuse_fin) pdl_trigger();
+    // setup that needs nothing from the previous kernel overlaps its tail (PDL)
+    if (warp == 0 && lane == 0) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap_h) : "memory");
+        for (int s = 0; s < S; ++s) { mbar_init(&full[s], kProdWarps * 32 + 1); mbar_init(&empty[s], 1); }
+        for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], kTcEpiWarps * 32); }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == kTcMmaWarp) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(tp.tmem_cols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    epi_init(e, n_h);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
     pdl_wait();   // the subset (and n_S) come from the previous kernel on the stream
     int p0, p1;
     if (seg_b >= 0) {
@@ -241,22 +258,6 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
     const int n_body = (body + kTileM - 1) / kTileM;
     const int n_tiles = n_body + (last_len > 0 ? 1 : 0);
 
-    if (warp == 0 && lane == 0) {
-        asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap_h) : "memory");
-        for (int s = 0; s < S; ++s) { mbar_init(&full[s], kProdWarps * 32 + 1); mbar_init(&empty[s], 1); }
-        for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], kTcEpiWarps * 32); }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    if (warp == kTcMmaWarp) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                     "r"(tp.tmem_cols));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-    }
-    epi_init(e, n_h);
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    const uint32_t tmem_base = *tmem_slot;
     if (threadIdx.x == 0) TC_TRACE(0);
 
     auto tile_range = [&](int t, int& t0, int& tn) {
