@@ -12,14 +12,18 @@
 // Persistent, warp-specialised CTA per SM (13 warps):
 //   warps 0-3  producers: 16-byte cp.async of the gathered W rows into a
 //           128B-swizzled smem stage (swizzle applied in the address), one
-//           cp.async.mbarrier.arrive.noinc per thread; an L2 bulk prefetch runs
-//           1 KB windows ahead per row; H by one 2D TMA tile per stage.
+//           cp.async.mbarrier.arrive.noinc per thread (rows past a tile's end
+//           skipped); H by one 2D TMA tile per stage (an optional L2 bulk
+//           prefetch run-ahead, EVOSPEC_PF, measured slower: off).
 //   warp 4  TMEM allocator + MMA issuer (one elected thread):
 //           4 x tcgen05.mma.cta_group::1.kind::f16 (K = 16) per stage,
 //           tcgen05.commit frees the stage; double-buffered accumulators.
 //   warps 5-12 epilogue: tcgen05.ld 32x32b -> scale -> smem tile -> the
-//           shared online-softmax / top-k fold (lmh_epilogue.cuh) while the
-//           producers and MMA already stream the next tile.
+//           shared online-softmax + candidate-buffer fold (lmh_epilogue.cuh)
+//           while the producers and MMA already stream the next tile; the
+//           CTA's last tile is folded (and its rows stored) by all 13 warps.
+// Segment mode (ragged head): CTAs serve (row group, position range) segments.
+// Optional: the finalisation fused into the last-arriving CTAs (EVOSPEC_FUSED_FIN).
 #include <algorithm>
 #include <cstdlib>
 
@@ -35,9 +39,9 @@ namespace es {
 
 // W-operand producer: 4 warps of 16-byte cp.async (LDGSTS) with the 128B
 // swizzle applied in the address, one mbarrier arrival per thread
-// (cp.async.mbarrier.arrive.noinc). The TMA tile::gather4 producer (one warp)
-// is kept for comparison: it is issue-bound at ~1.6 TB/s for 128-byte rows
-// (profiles/r01_*), while LDGSTS streams the same gathered rows at HBM rate.
+// (cp.async.mbarrier.arrive.noinc). A TMA tile::gather4 producer (one warp,
+// round-1 history) measured issue-bound at ~1.6 TB/s for 128-byte row pieces;
+// LDGSTS streams the same gathered rows at HBM rate.
 constexpr int kProdWarps = 4;
 constexpr int kTcMmaWarp = kProdWarps;
 constexpr int kTcEpiWarp0 = kProdWarps + 1;
@@ -74,14 +78,6 @@ ES_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
 }
 
-ES_DEV void tma_gather4(void* dst, const CUtensorMap* map, uint64_t* bar, int col, int r0, int r1, int r2,
-                        int r3, uint64_t policy) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes.L2::cache_hint"
-        " [%0], [%1, {%3, %4, %5, %6, %7}], [%2], %8;" ::"r"(smem_u32(dst)),
-        "l"(map), "r"(smem_u32(bar)), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "l"(policy)
-        : "memory");
-}
 ES_DEV void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, uint64_t policy) {
     asm volatile(
         "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
@@ -208,7 +204,6 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
     uint64_t* tfull = empty + S;                                 // [2]
     uint64_t* tempty = tfull + 2;                                // [2]
     uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
-    int32_t* rows_sm = (int32_t*)(base + tp.off_rows);           // [2][128] gather rows per tile
 
     const int warp = warp_id(), lane = lane_id();
     // with the fused finalisation some CTAs wait for all others: dependents are
