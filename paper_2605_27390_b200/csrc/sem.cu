@@ -275,7 +275,7 @@ sem_scan_tma_kernel(const uint16_t* __restrict__ E, int64_t n_rows, int d, const
         double acc[kScanRowsPerStage];
 #pragma unroll
         for (int r = 0; r < kScanRowsPerStage; ++r) {
-            acc[r] = 0.0;
+            double a_lo = 0.0, a_hi = 0.0;   // two chains of 4 (latency), summed at the end
             if (r < nr) {
                 const uint4 u = *(const uint4*)(st + (size_t)r * row_bytes);
                 const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
@@ -284,10 +284,11 @@ sem_scan_tma_kernel(const uint16_t* __restrict__ E, int64_t n_rows, int d, const
                     // bf16 fields in place in the double's high word (see sem_scan_kernel)
                     const uint32_t lo = (uint32_t)((int32_t)(w4[j] << 16) >> 3) & 0x8FFFE000u;
                     const uint32_t hi = (uint32_t)((int32_t)w4[j] >> 3) & 0x8FFFE000u;
-                    acc[r] = fma(__hiloint2double((int)lo, 0), qv[2 * j], acc[r]);
-                    acc[r] = fma(__hiloint2double((int)hi, 0), qv[2 * j + 1], acc[r]);
+                    a_lo = fma(__hiloint2double((int)lo, 0), qv[2 * j], a_lo);
+                    a_hi = fma(__hiloint2double((int)hi, 0), qv[2 * j + 1], a_hi);
                 }
             }
+            acc[r] = a_lo + a_hi;
         }
         // reduce-scatter 8 rows over 32 lanes: lanes (l & 7) == r end with row r's
         // sum over 4 lanes, then two butterflies finish it
