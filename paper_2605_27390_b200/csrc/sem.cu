@@ -198,10 +198,10 @@ sem_scan_tma_kernel(const uint16_t* __restrict__ E, int64_t n_rows, int d, const
     const size_t stage_bytes = kScanRowsPerStage * row_bytes;
     unsigned char* ring = sc_sm;                                              // [S][8][d] bf16
     uint32_t* hist_sm = (uint32_t*)(ring + kScanStages * stage_bytes);       // [4096]
-    double* red = (double*)(hist_sm + kHistBins);                            // [S][16][8]
-    uint64_t* full = (uint64_t*)(red + kScanStages * kScanConsumers * kScanRowsPerStage);
+    double* red = (double*)(hist_sm + kHistBins);                            // [2S][16][8]
+    uint64_t* full = (uint64_t*)(red + 2 * kScanStages * kScanConsumers * kScanRowsPerStage);
     uint64_t* empty = full + kScanStages;
-    uint64_t* part_bar = empty + kScanStages;
+    uint64_t* part_bar = empty + kScanStages;                                // [2S]
     const int warp = warp_id(), lane = lane_id();
     const int n_slab = d / 256;                                              // <= 16
     // stage i of this CTA: rows [8 g, 8 g + 8) of E with g = i * grid + cta (il = 1:
@@ -220,6 +220,7 @@ sem_scan_tma_kernel(const uint16_t* __restrict__ E, int64_t n_rows, int d, const
             s_mbar_init(&full[s], 1);
             s_mbar_init(&empty[s], n_slab);
             s_mbar_init(&part_bar[s], n_slab);
+            s_mbar_init(&part_bar[s + kScanStages], n_slab);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -272,21 +273,26 @@ sem_scan_tma_kernel(const uint16_t* __restrict__ E, int64_t n_rows, int d, const
         const int64_t row0 = stage_row(i);
         const int nr = (int)min((int64_t)kScanRowsPerStage, r_end - row0);
         const unsigned char* st = ring + slot * stage_bytes + (size_t)warp * 512 + (size_t)lane * 16;
+        // this warp's slab of the stage into registers, then the slot goes back to
+        // the producer at once: the ring refills while the warp computes
+        uint4 u[kScanRowsPerStage];
+#pragma unroll
+        for (int r = 0; r < kScanRowsPerStage; ++r)
+            u[r] = r < nr ? *(const uint4*)(st + (size_t)r * row_bytes) : make_uint4(0, 0, 0, 0);
+        __syncwarp();
+        if (lane == 0) s_mbar_arrive(&empty[slot]);
         double acc[kScanRowsPerStage];
 #pragma unroll
         for (int r = 0; r < kScanRowsPerStage; ++r) {
             double a_lo = 0.0, a_hi = 0.0;   // two chains of 4 (latency), summed at the end
-            if (r < nr) {
-                const uint4 u = *(const uint4*)(st + (size_t)r * row_bytes);
-                const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+            const uint32_t w4[4] = {u[r].x, u[r].y, u[r].z, u[r].w};
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    // bf16 fields in place in the double's high word (see sem_scan_kernel)
-                    const uint32_t lo = (uint32_t)((int32_t)(w4[j] << 16) >> 3) & 0x8FFFE000u;
-                    const uint32_t hi = (uint32_t)((int32_t)w4[j] >> 3) & 0x8FFFE000u;
-                    a_lo = fma(__hiloint2double((int)lo, 0), qv[2 * j], a_lo);
-                    a_hi = fma(__hiloint2double((int)hi, 0), qv[2 * j + 1], a_hi);
-                }
+            for (int j = 0; j < 4; ++j) {
+                // bf16 fields in place in the double's high word (see sem_scan_kernel)
+                const uint32_t lo = (uint32_t)((int32_t)(w4[j] << 16) >> 3) & 0x8FFFE000u;
+                const uint32_t hi = (uint32_t)((int32_t)w4[j] >> 3) & 0x8FFFE000u;
+                a_lo = fma(__hiloint2double((int)lo, 0), qv[2 * j], a_lo);
+                a_hi = fma(__hiloint2double((int)hi, 0), qv[2 * j + 1], a_hi);
             }
             acc[r] = a_lo + a_hi;
         }
@@ -305,17 +311,17 @@ sem_scan_tma_kernel(const uint16_t* __restrict__ E, int64_t n_rows, int d, const
         double part = acc[0];
 #pragma unroll
         for (int o = kScanRowsPerStage; o < 32; o <<= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-        double* rd = red + (size_t)slot * kScanConsumers * kScanRowsPerStage;
+        // partials double-buffered over 2S stages: a warp is at most S stages ahead of
+        // the owner of stage i (the owner must load stage i + S before the slot of
+        // stage i + 2S can refill), so stage i + 2S never overwrites unread partials
+        const int pslot = i % (2 * kScanStages);
+        double* rd = red + (size_t)pslot * kScanConsumers * kScanRowsPerStage;
         if (lane < kScanRowsPerStage) rd[warp * kScanRowsPerStage + lane] = part;   // lane r holds row r
         __syncwarp();
-        if (lane == 0) s_mbar_arrive(&part_bar[slot]);
-        const int owner = i % n_slab;
-        if (warp != owner) {
-            if (lane == 0) s_mbar_arrive(&empty[slot]);   // the stage's data is no longer needed
-            continue;
-        }
+        if (lane == 0) s_mbar_arrive(&part_bar[pslot]);
+        if (warp != i % n_slab) continue;
         // owner: the 16 partials of each row, added in slab order
-        s_mbar_wait(&part_bar[slot], (uint32_t)(i / kScanStages) & 1);
+        s_mbar_wait(&part_bar[pslot], (uint32_t)(i / (2 * kScanStages)) & 1);
         uint32_t digit = 0xFFFFFFFFu;
         if (lane < nr) {
             double tot = 0.0;
@@ -329,7 +335,6 @@ sem_scan_tma_kernel(const uint16_t* __restrict__ E, int64_t n_rows, int d, const
         const unsigned peers = __match_any_sync(0xffffffffu, digit);
         if (digit != 0xFFFFFFFFu && lane == __ffs(peers) - 1) atomicAdd(&hist_sm[digit], (uint32_t)__popc(peers));
         __syncwarp();
-        if (lane == 0) s_mbar_arrive(&empty[slot]);
     }
     // every slab warp has retired its stages; merge the histogram
     asm volatile("bar.sync 1, %0;" ::"r"(n_slab * 32) : "memory");
@@ -349,7 +354,7 @@ void launch_sem_scan(const void* E, int e_dtype, int64_t n_rows, int d, const vo
     const char* rse = getenv("EVOSPEC_SCAN_RS");
     const int RS = rse ? atoi(rse) : kScanRS;
     auto smem_for = [&](int rs, int ns) {
-        return (size_t)ns * rs * d * 2 + kHistBins * 4 + (size_t)ns * kScanConsumers * rs * 8 + 3 * ns * 8;
+        return (size_t)ns * rs * d * 2 + kHistBins * 4 + (size_t)2 * ns * kScanConsumers * rs * 8 + 4 * ns * 8;
     };
     const int NS = RS == 4 ? 6 : (RS == 2 ? 12 : 3);   // ~192 KB of ring at d = 4096
     const char* env = getenv("EVOSPEC_SCAN");
