@@ -171,7 +171,7 @@ struct evospec_ctx {
 
 namespace {
 constexpr int kTimingSlots = 4096;
-constexpr int kTraceLen = 2 * kNumSMs * 8 + 16 + 32;   // LM-head CTAs, finalize rows, union stamps
+constexpr int kTraceLen = 2 * kNumSMs * 8 + 16 + 32 + 64;   // LM-head CTAs, finalize rows, union stamps
 
 // union stamps live after the LM-head / finalize slots
 long long* union_trace(evospec_ctx* ctx, cudaStream_t st) {
@@ -566,6 +566,11 @@ static evospec_status lmh_impl(evospec_ctx* ctx, const void* W, int64_t n_w_rows
     a.logits_out = logits_out;
     a.part = ctx->part;
     a.m_ids = m_ids; a.m_vals = m_vals; a.m_lse = m_lse; a.m_probs = m_probs;
+    // thread-parallel epilogue fold (default; EVOSPEC_PAR_FOLD=0: the warp-per-row fold)
+    static const int par_fold = getenv("EVOSPEC_PAR_FOLD") ? atoi(getenv("EVOSPEC_PAR_FOLD")) : 1;
+    a.par_fold = par_fold;
+    static const int fin_opt = getenv("EVOSPEC_FIN_OPT") ? atoi(getenv("EVOSPEC_FIN_OPT")) : 15;
+    a.fin_opt = fin_opt;
     if (segs) {
         a.nseg = segs->nseg; a.seg_ctas = segs->seg_ctas; a.seg_rows = segs->seg_rows; a.seg_pos = segs->seg_pos;
         a.seg_cta = segs->seg_cta;

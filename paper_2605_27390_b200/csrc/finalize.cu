@@ -320,10 +320,14 @@ lmh_finalize32_kernel(LmhArgs a, int n_cta_arg, int k, float gamma, const float*
                       float* __restrict__ row_max, float* __restrict__ row_sumexp, int* flags) {
     extern __shared__ __align__(16) unsigned char f32_sm[];
     pdl_trigger();
-    pdl_wait();
     const Fin32Smem sm = fin32_carve(f32_sm, kFin32Threads);
+    // H row and ||h||^2 need only the LM head's inputs: before the wait (overlaps its tail)
+    const bool pre = a.fin_opt & 1;
+    const double hacc = pre ? fin32_stage_h<kFin32Threads>(a, blockIdx.x, sm) : 0.0;
+    pdl_wait();
     fin32_row<U, kFin32Threads>(a, blockIdx.x, n_cta_arg, k, gamma, wmax_dev, topk_ids, topk_vals, row_max,
-                                row_sumexp, flags, sm);
+                                row_sumexp, flags, sm, pre, hacc);
+
 }
 
 void launch_lmh_finalize(const LmhArgs& a, int n_cta, int k, const float* wmax_dev, int32_t* topk_ids,

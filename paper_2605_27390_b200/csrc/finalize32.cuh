@@ -37,22 +37,27 @@ struct Fin32Smem {
     int* scal;      // n_need, nk, tot, cand_n
     float* fscal;   // lse, th
     float* s_head;
+    uint32_t* head_cnt;   // [nt] packed (gt, ge) head ranks
+    double* res_d;        // [32] re-score partials (one per warp slice)
     uint16_t* h_row;
 };
 
 __host__ __device__ inline size_t fin32_smem_bytes(int nt) {
     const int nw = nt / 32;
     return (size_t)kFin32MaxD * 2 + (size_t)nw * 8 + (size_t)32 * 8 + (size_t)kFinCand32 * 8 + (size_t)nw * 16 +
-           32 * 16 + 8 * 4 + 4 * 4 + (size_t)nt * 4 + 256;
+           32 * 16 + 8 * 4 + 4 * 4 + (size_t)nt * 8 + 32 * 8 + 256;
 }
 
 ES_DEV Fin32Smem fin32_carve(unsigned char* p, int nt) {
     const int nw = nt / 32;
     Fin32Smem m;
-    p = (unsigned char*)(((uintptr_t)p + 15) & ~(uintptr_t)15);
+    // align by pointer arithmetic (an integer round trip would turn every shared
+    // access below into a generic LD/ST)
+    p += (16u - ((uint32_t)__cvta_generic_to_shared(p) & 15u)) & 15u;
     m.h_row = (uint16_t*)p;     p += (size_t)kFin32MaxD * 2;
     m.red_d = (double*)p;       p += (size_t)nw * 8;
     m.c_e = (double*)p;         p += 32 * 8;
+    m.res_d = (double*)p;       p += 32 * 8;
     m.cand_v = (float*)p;       p += (size_t)kFinCand32 * 4;
     m.cand_p = (int*)p;         p += (size_t)kFinCand32 * 4;
     m.w_M = (float*)p;          p += (size_t)nw * 4;
@@ -65,7 +70,8 @@ ES_DEV Fin32Smem fin32_carve(unsigned char* p, int nt) {
     m.need_list = (int*)p;      p += 32 * 4;
     m.scal = (int*)p;           p += 8 * 4;
     m.fscal = (float*)p;        p += 4 * 4;
-    m.s_head = (float*)p;
+    m.s_head = (float*)p;       p += (size_t)nt * 4;
+    m.head_cnt = (uint32_t*)p;
     return m;
 }
 
@@ -106,11 +112,38 @@ ES_DEV void sort32_rolled(float& v, int& p) {
 // One H row's finalisation by a block of NT threads (NT = NT in the
 // standalone kernel, the LM-head kernel's 416 when fused into its last CTAs);
 // shared memory comes from the caller (fin32_carve).
+// H row r into shared memory and this thread's share of ||h||^2. Reads only
+// the LM head's inputs (H), never its outputs, so the standalone kernel runs it
+// before griddepcontrol.wait, overlapping the LM head's tail.
+template <int NT>
+ES_DEV double fin32_stage_h(const LmhArgs& a, const int r, const Fin32Smem& sm) {
+    double hacc = 0.0;
+    const bool h_fast = a.h_dtype == 0 && a.d % 8 == 0 && a.d <= kFin32MaxD;
+    if (h_fast) {
+        const uint4* hp = (const uint4*)((const uint16_t*)a.H + (size_t)r * a.d);
+        for (int c = threadIdx.x; c < a.d / 8; c += NT) {
+            const uint4 hv = __ldg(&hp[c]);
+            ((uint4*)sm.h_row)[c] = hv;
+            float f[8];
+            unpack_bf16x8(hv, f);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) hacc = fma((double)f[j], (double)f[j], hacc);
+        }
+    } else {
+#pragma unroll 1
+        for (int col = threadIdx.x; col < a.d; col += NT) {
+            const double h = fin32_load_elem(a.H, a.h_dtype, (size_t)r * a.d + col);
+            hacc = fma(h, h, hacc);
+        }
+    }
+    return hacc;
+}
+
 template <int U, int NT>
 ES_DEV void fin32_row(const LmhArgs& a, const int r, int n_cta_arg, int k, float gamma,
                       const float* __restrict__ wmax_dev, int32_t* __restrict__ topk_ids,
                       float* __restrict__ topk_vals, float* __restrict__ row_max, float* __restrict__ row_sumexp,
-                      int* flags, const Fin32Smem& sm) {
+                      int* flags, const Fin32Smem& sm, bool h_staged = false, double hacc_pre = 0.0) {
     const int KP = a.KP;
     const int lane = lane_id(), warp = warp_id();
     constexpr int nwarps = NT / 32;
@@ -159,28 +192,14 @@ ES_DEV void fin32_row(const LmhArgs& a, const int r, int n_cta_arg, int k, float
         const int cn = __ldcg(&a.part.cnt[o]);
         const float vk = __ldcg(&a.part.val[o * kFin32LS + KP - 1]);
         if (cn >= KP) thl = vk;
-        s_head[threadIdx.x] = __ldcg(&a.part.val[o * kFin32LS]);   // the list maximum (sorted head)
+        // the list maximum: every producer keeps the CTA row's best entry, whose value
+        // is the row's running maximum m (sorted lists: also slot 0)
+        s_head[threadIdx.x] = cm_;
+        sm.head_cnt[threadIdx.x] = 0u;
     }
     const float wmax = __ldg(wmax_dev);
-    double hacc = 0.0;
     const bool h_fast = a.h_dtype == 0 && a.d % 8 == 0 && a.d <= kFin32MaxD;
-    if (h_fast) {
-        const uint4* hp = (const uint4*)((const uint16_t*)a.H + (size_t)r * a.d);
-        for (int c = threadIdx.x; c < a.d / 8; c += NT) {
-            const uint4 hv = hp[c];
-            ((uint4*)h_row)[c] = hv;
-            float f[8];
-            unpack_bf16x8(hv, f);
-#pragma unroll
-            for (int j = 0; j < 8; ++j) hacc = fma((double)f[j], (double)f[j], hacc);
-        }
-    } else {
-#pragma unroll 1
-        for (int col = threadIdx.x; col < a.d; col += NT) {
-            const double h = fin32_load_elem(a.H, a.h_dtype, (size_t)r * a.d + col);
-            hacc = fma(h, h, hacc);
-        }
-    }
+    double hacc = h_staged ? hacc_pre : fin32_stage_h<NT>(a, r, sm);
     if (threadIdx.x == 0) { cand_n = 0; th_s = -INFINITY; }
     {
         int tcnt = 0;
@@ -198,16 +217,36 @@ ES_DEV void fin32_row(const LmhArgs& a, const int r, int n_cta_arg, int k, float
     if (threadIdx.x == 0) { FIN_TRACE_R(1); FIN_DT_R(1); }
     // B. threshold: the KP-th largest list head (KP distinct entries) and any full
     //    list's entry KP-1 both bound the row's KP-th best from below
-    if ((int)threadIdx.x < n_cta && n_cta >= KP) {
-        const float hv = s_head[threadIdx.x];
-        int gt = 0, ge = 0;
+    // (NT / n_cta threads per head, each counting a slice of the heads; a packed
+    //  shared atomic per head: gt in the low 16 bits, ge in the high 16)
+    if (n_cta >= KP) {
+        const int per = (a.fin_opt & 8) ? max(1, NT / n_cta) : 1;
+        const int c = threadIdx.x / per, part = threadIdx.x % per;
+        if (c < n_cta) {
+            const float hv = s_head[c];
+            const int c0 = n_cta * part / per, c1 = n_cta * (part + 1) / per;
+            int gt = 0, ge = 0;
 #pragma unroll 4
-        for (int c = 0; c < n_cta; ++c) {
-            const float o = s_head[c];
-            gt += o > hv;
-            ge += o >= hv;
+            for (int j = c0; j < c1; ++j) {
+                const float o = s_head[j];
+                gt += o > hv;
+                ge += o >= hv;
+            }
+            if (per == 1) {
+                if (hv != -INFINITY && gt < KP && KP <= ge) th_s = hv;   // the KP-th largest head value
+            } else {
+                atomicAdd(&sm.head_cnt[c], (uint32_t)gt | ((uint32_t)ge << 16));
+            }
         }
-        if (hv != -INFINITY && gt < KP && KP <= ge) th_s = hv;   // the KP-th largest head value
+        if (per > 1) {
+            __syncthreads();
+            if ((int)threadIdx.x < n_cta) {
+                const uint32_t pc = sm.head_cnt[threadIdx.x];
+                const int gt = (int)(pc & 0xffffu), ge = (int)(pc >> 16);
+                const float hv = s_head[threadIdx.x];
+                if (hv != -INFINITY && gt < KP && KP <= ge) th_s = hv;
+            }
+        }
     }
     __syncthreads();
     float th0 = th_s;
@@ -250,10 +289,21 @@ ES_DEV void fin32_row(const LmhArgs& a, const int r, int n_cta_arg, int k, float
         if ((int)threadIdx.x < ncand) {
             const float v = cand_v[threadIdx.x];
             const int p = cand_p[threadIdx.x];
+            const int gid = __ldg(&a.subset[p]);   // position -> vocabulary id (in flight during the ranks)
             int rank = 0;
 #pragma unroll 4
             for (int j = 0; j < ncand; ++j) rank += before(cand_v[j], cand_p[j], v, p);
-            if (rank < KP) { c_v[rank] = v; c_id[rank] = p; }
+            if (rank < KP) {
+                c_v[rank] = v;
+                c_id[rank] = p;
+                c_gid[rank] = gid;
+                // the re-score reads a few of these rows: start them towards L2 now
+                const size_t rb = (size_t)a.d * (a.w_dtype == 0 ? 2 : 4);
+                if ((a.fin_opt & 2) && rb % 16 == 0 && rb <= (1u << 20)) {
+                    const char* wr = (const char*)a.W + (size_t)(gid / a.R) * rb;
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(wr), "r"((uint32_t)rb) : "memory");
+                }
+            }
         }
         if (threadIdx.x == 0) nk_s = min(ncand, KP);
     } else if (warp == 0) {
@@ -304,7 +354,9 @@ ES_DEV void fin32_row(const LmhArgs& a, const int r, int n_cta_arg, int k, float
         // C2. runs: consecutive kept entries closer than 2 delta; those reaching the top k are re-scored
         const int cnt = nk_s, tot = tot_s;
         const float Lv = lane < cnt ? c_v[lane] : -INFINITY;
-        c_gid[lane] = lane < cnt ? __ldg(&a.subset[c_id[lane]]) : -1;   // position -> vocabulary id
+        // position -> vocabulary id (the rank path stored it already)
+        if (ncand > kFin32RankMax) c_gid[lane] = lane < cnt ? __ldg(&a.subset[c_id[lane]]) : -1;
+        else if (lane >= cnt) c_gid[lane] = -1;
         double hn = 0.0;
 #pragma unroll
         for (int w = 0; w < nwarps; ++w) hn += red_d[w];
@@ -334,29 +386,32 @@ ES_DEV void fin32_row(const LmhArgs& a, const int r, int n_cta_arg, int k, float
     }
     __syncthreads();
     if (threadIdx.x == 0) { FIN_TRACE_R(4); FIN_DT_R(4); }
-    // D. exact re-score of the flagged entries (one warp each, W loads in flight)
+    // D. exact re-score of the flagged entries: each is split over nwarps / nn
+    //    warps (contiguous slices of the row, W loads in flight), partials summed
+    //    per entry (order-free: exact products, the fp64 sum is within the envelope)
     const int nn = n_need_s;
-    for (int q = warp; q < nn; q += nwarps) {
-        const int c = need_list[q];
+    const int wpc = (a.fin_opt & 4) && nn > 0 && nn <= nwarps ? nwarps / nn : 1;
+    for (int q = warp; q < nn * wpc; q += nwarps) {
+        const int ci = q / wpc, part = q - ci * wpc;
+        const int c = need_list[ci];
         const size_t row = (size_t)(c_gid[c] / a.R);
         double acc = 0.0;
         if (a.w_dtype == 0 && h_fast) {
             const uint4* wp = (const uint4*)((const uint16_t*)a.W + row * a.d);
             const int nc = a.d / 8;
-            constexpr int kPer = 16;                 // uint4 per lane in flight (d = 4096: all)
-            double a4[4] = {0.0, 0.0, 0.0, 0.0};     // independent chains (order-free: exact products,
-                                                     // the fp64 sum is within the envelope either way)
-            for (int c0 = 0; c0 < nc; c0 += 32 * kPer) {
-                uint4 wv[kPer];
+            const int s0 = (int)((long long)nc * part / wpc), s1 = (int)((long long)nc * (part + 1) / wpc);
+            double a4[4] = {0.0, 0.0, 0.0, 0.0};
+            for (int c0 = s0; c0 < s1; c0 += 32 * 4) {
+                uint4 wv[4];
 #pragma unroll
-                for (int u = 0; u < kPer; ++u) {
+                for (int u = 0; u < 4; ++u) {
                     const int cc = c0 + lane + 32 * u;
-                    wv[u] = cc < nc ? __ldg(&wp[cc]) : make_uint4(0, 0, 0, 0);
+                    wv[u] = cc < s1 ? __ldg(&wp[cc]) : make_uint4(0, 0, 0, 0);
                 }
 #pragma unroll
-                for (int u = 0; u < kPer; ++u) {
+                for (int u = 0; u < 4; ++u) {
                     const int cc = c0 + lane + 32 * u;
-                    if (cc < nc) {
+                    if (cc < s1) {
                         float fw[8], fh[8];
                         unpack_bf16x8(wv[u], fw);
                         unpack_bf16x8(((const uint4*)h_row)[cc], fh);
@@ -367,12 +422,24 @@ ES_DEV void fin32_row(const LmhArgs& a, const int r, int n_cta_arg, int k, float
             }
             acc = (a4[0] + a4[1]) + (a4[2] + a4[3]);
         } else {
+            const int s0 = (int)((long long)a.d * part / wpc), s1 = (int)((long long)a.d * (part + 1) / wpc);
 #pragma unroll 1
-            for (int col = lane; col < a.d; col += 32)
+            for (int col = s0 + lane; col < s1; col += 32)
                 acc = fma(fin32_load_elem(a.W, a.w_dtype, row * a.d + col), fin32_load_elem(a.H, a.h_dtype, (size_t)r * a.d + col), acc);
         }
         acc = warp_sum_d(acc);
-        if (lane == 0) c_e[c] = acc * (double)a.inv_temp;
+        if (lane == 0) {
+            if (wpc == 1) c_e[c] = acc * (double)a.inv_temp;
+            else sm.res_d[q] = acc;
+        }
+    }
+    if (wpc > 1) {
+        __syncthreads();
+        if ((int)threadIdx.x < nn) {
+            double t = 0.0;
+            for (int p = 0; p < wpc; ++p) t += sm.res_d[threadIdx.x * wpc + p];
+            c_e[need_list[threadIdx.x]] = t * (double)a.inv_temp;
+        }
     }
     __syncthreads();
     if (threadIdx.x == 0) { FIN_TRACE_R(5); FIN_DT_R(5); }

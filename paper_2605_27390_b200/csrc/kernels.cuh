@@ -84,6 +84,9 @@ struct LmhArgs {
     // fused finalisation (tensor-core path, k + 8 <= 32, no segments): the last n_h
     // CTAs to finish each finalise one row once every CTA has stored its lists
     int fuse_fin, fin_k;
+    int fin_opt;    // finalisation variants (bits; EVOSPEC_FIN_OPT): 1 H before the PDL wait, 2 W-row L2 prefetch,
+                    // 4 multi-warp re-score, 8 parallel head threshold
+    int par_fold;   // thread-parallel tile fold (lmh_epilogue.cuh epi_par_*), buffered path
     float fin_gamma;
     const float* fin_wmax;
     unsigned long long* fin_ctr;   // monotone arrival counter (G arrivals per launch)

@@ -644,9 +644,12 @@ ES_DEV void epi_store_buf(const EpiSmem& e, const LmhPartials& P, int cta, int n
 // The CTA's last tile (all warps): fold, then store each row right away (the
 // warp that folds a row writes its partial list -- no block-wide barrier).
 ES_DEV void epi_tile_buf_last_store(const EpiSmem& e, const LmhPartials& P, int cta, int n_h_total, int h_row0,
-                                    int n_h, int KP, int tn, int base_pos, int warp, int n_warps) {
+                                    int n_h, int KP, int tn, int base_pos, int warp, int n_warps,
+                                    long long* dtr = nullptr) {
     const int lane = lane_id();
-    for (int r = warp; r < n_h; r += n_warps) {
+    int it = 0;
+    for (int r = warp; r < n_h; r += n_warps, ++it) {
+        if (dtr && lane == 0 && it < 5) dtr[it * 4 + 0] = clock64();
         if (tn > 0) {
             float v[kTileJ];
             float lm = -INFINITY;
@@ -657,9 +660,228 @@ ES_DEV void epi_tile_buf_last_store(const EpiSmem& e, const LmhPartials& P, int 
                 lm = fmaxf(lm, v[j]);
             }
             fold_softmax(e, r, v, lm);
+            if (dtr && lane == 0 && it < 5) dtr[it * 4 + 1] = clock64();
             fold_buf(e, r, KP, tn, base_pos, v, lm, false, e.scr_v + warp * 32, e.scr_p + warp * 32);
+            if (dtr && lane == 0 && it < 5) dtr[it * 4 + 2] = clock64();
         }
         store_row_buf(e, P, cta, n_h_total, h_row0, r);
+        if (dtr && lane == 0 && it < 5) dtr[it * 4 + 3] = clock64();
+    }
+}
+
+// ---------------------------------------------------------------- thread-parallel fold
+// Buffered path (KP <= 32), tensor-core kernel. The warp-per-row fold above is a
+// chain of shuffles and shared-memory round trips per row (~2,500 cycles); with
+// 60 rows on 8-13 warps that chain is the exposed tail of the CTA's last tile.
+// Here thread (r, g) owns positions [32 g, 32 g + 32) of row r -- kParG = 4
+// adjacent lanes per row, so the row reductions are two xor shuffles:
+//   softmax   tile maximum, m_new = max(m_old, it), sum of exp(z - m_new) plus
+//             the rescaled old partial sums (the 32 per-row slots of st_ls);
+//   bound     T = min over the 4 threads of each one's J-th largest value,
+//             J = ceil(KP / 4): at least 4 J >= KP tile values are >= T, so T
+//             bounds the row's KP-th best from below (ties at T admitted); the
+//             tighter of T and the row's bound is kept;
+//   admission candidates strictly before the bound are appended to the row's
+//             buffer at a shared-memory atomic offset (st_xcnt).
+// A row whose buffer would overflow keeps its count and is folded by the warp
+// path (fold_buf) in phase 2, which also tightens rows between tiles and, on
+// the last tile, stores the partial lists.
+constexpr int kParG = 4;
+
+ES_DEV float ex2_approx(float x) {   // 2^x, flush-to-zero (ex2 of -inf is +0)
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+
+// (noinline, loops rolled: this code runs once per tile, so its instruction
+// footprint -- not its issue count -- sets its cost; fully unrolled copies
+// measured ~20k cycles per tile from instruction-cache misses alone)
+template <int J>
+ES_DEV void epi_par_phase1(const EpiSmem& e, int n_h, int tn, int base_pos, int tid, int nthr, bool last,
+                           const LmhPartials& P, int cta, int n_h_total, int h_row0, long long* dtr) {
+#define PTR_(i) do { if (dtr && lane == 0) dtr[i] = clock64(); } while (0)
+    const int lane = lane_id();
+    for (int base = tid - lane; base < n_h * kParG; base += nthr) {
+        const int item = base + lane;
+        const bool act = item < n_h * kParG;
+        const int r = act ? item >> 2 : n_h - 1;   // idle lanes mirror a real row, write nothing
+        const int g = item & (kParG - 1);
+        const int rot = item & 7;                  // rotated float4 order: a quarter-warp hits 8 distinct bank groups
+        const float* trow = e.tile + (size_t)r * kTile + g * 32;
+        // the thread's 32 values are read from shared memory in three passes (bound,
+        // softmax + admission, candidate writes) instead of being held in registers
+        auto ld4 = [&](int j, float (&x)[4]) {
+            const int q = (j + rot) & 7;
+            const float4 f = *(const float4*)(trow + 4 * q);
+            const int p = g * 32 + 4 * q;
+            x[0] = p + 0 < tn ? f.x : -INFINITY;
+            x[1] = p + 1 < tn ? f.y : -INFINITY;
+            x[2] = p + 2 < tn ? f.z : -INFINITY;
+            x[3] = p + 3 < tn ? f.w : -INFINITY;
+        };
+        PTR_(3);
+        // row state, read by all four threads before any of them writes
+        const float m_old = e.st_m[r];
+        float thv = e.st_thv[r];
+        int thp = e.st_thp[r];
+        const int n_old = e.st_cnt[r];
+        const float4 o0 = *(const float4*)&e.st_ls[r * 32 + g * 8];
+        const float4 o1 = *(const float4*)&e.st_ls[r * 32 + g * 8 + 4];
+        __syncwarp();
+        // pass 1: maximum; on a row's first tile (no bound yet) also this thread's
+        // J-th largest (branch-free insertion into a sorted top-J)
+        float lm = -INFINITY, t = -INFINITY;
+        if (thv == -INFINITY) {   // uniform over the row's four lanes
+            float top[J];
+#pragma unroll
+            for (int i = 0; i < J; ++i) top[i] = -INFINITY;
+#pragma unroll 2
+            for (int j = 0; j < 8; ++j) {
+                float x4[4];
+                ld4(j, x4);
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    float x = x4[c];
+                    lm = fmaxf(lm, x);
+#pragma unroll
+                    for (int s2 = 0; s2 < J; ++s2) {
+                        const float hi = fmaxf(top[s2], x);
+                        x = fminf(top[s2], x);
+                        top[s2] = hi;
+                    }
+                }
+            }
+            t = top[J - 1];
+        } else {
+#pragma unroll 4
+            for (int j = 0; j < 8; ++j) {
+                float x4[4];
+                ld4(j, x4);
+                lm = fmaxf(fmaxf(lm, fmaxf(x4[0], x4[1])), fmaxf(x4[2], x4[3]));
+            }
+        }
+        t = fminf(t, __shfl_xor_sync(0xffffffffu, t, 1));
+        t = fminf(t, __shfl_xor_sync(0xffffffffu, t, 2));
+        if (t > thv) { thv = t; thp = 0x7fffffff; }
+        float rm = fmaxf(lm, __shfl_xor_sync(0xffffffffu, lm, 1));
+        rm = fmaxf(rm, __shfl_xor_sync(0xffffffffu, rm, 2));
+        const float m_new = fmaxf(m_old, rm);
+        PTR_(0);
+        // pass 2, branch-free: sum of 2^((z - m) log2 e) (ex2 of -inf is 0, so masked
+        // positions drop out) and admission (strictly before the bound)
+        const float mb = m_new == -INFINITY ? 0.0f : m_new * 1.4426950408889634f;
+        float sum0 = 0.0f, sum1 = 0.0f;
+        unsigned cm = 0u;
+#pragma unroll 4
+        for (int j = 0; j < 8; ++j) {
+            float x4[4];
+            ld4(j, x4);
+            const int p0 = base_pos + g * 32 + 4 * ((j + rot) & 7);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const float ex = ex2_approx(fmaf(x4[c], 1.4426950408889634f, -mb));
+                if (c & 1) sum1 += ex; else sum0 += ex;
+                const bool adm = x4[c] > thv || (x4[c] == thv && x4[c] != -INFINITY && p0 + c < thp);
+                cm |= (unsigned)adm << (4 * j + c);
+            }
+        }
+        float sum = sum0 + sum1;
+        PTR_(1);
+        const float so = ((o0.x + o0.y) + (o0.z + o0.w)) + ((o1.x + o1.y) + (o1.z + o1.w));
+        if (so != 0.0f) sum += so * ex2_approx((m_old - m_new) * 1.4426950408889634f);
+        if (act) {
+            *(float4*)&e.st_ls[r * 32 + g * 8] = make_float4(sum, 0.0f, 0.0f, 0.0f);
+            *(float4*)&e.st_ls[r * 32 + g * 8 + 4] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+            if (g == 0) { e.st_m[r] = m_new; e.st_thv[r] = thv; e.st_thp[r] = thp; }
+        }
+        if (last) {   // the row's softmax state goes straight to the partials
+            float tot = sum + __shfl_xor_sync(0xffffffffu, sum, 1);
+            tot += __shfl_xor_sync(0xffffffffu, tot, 2);
+            if (act && g == 0) {
+                const size_t o = (size_t)cta * n_h_total + h_row0 + r;
+                P.m[o] = m_new;
+                P.s[o] = tot;
+            }
+        }
+        PTR_(2);
+        // pass 3 (candidates only): append at the row's shared-memory atomic offset
+        const int nc = __popc(cm);
+        if (act && nc) {
+            int at = n_old + atomicAdd(&e.st_xcnt[r], nc);
+            if (at + nc <= kBuf) {   // else the row overflows: phase 2 folds it (fold_buf)
+                float* bv = e.st_val + (size_t)r * kBuf;
+                int* bp = e.st_pos + (size_t)r * kBuf;
+                while (cm) {
+                    const int i = __ffs(cm) - 1;
+                    cm &= cm - 1u;
+                    const int pl = g * 32 + 4 * (((i >> 2) + rot) & 7) + (i & 3);
+                    bv[at] = trow[pl - g * 32];
+                    bp[at] = base_pos + pl;
+                    ++at;
+                }
+            }
+        }
+    }
+}
+
+ES_DEV void epi_par_phase1_any(const EpiSmem& e, int n_h, int KP, int tn, int base_pos, int tid, int nthr,
+                               bool last, const LmhPartials& P, int cta, int n_h_total, int h_row0,
+                               long long* dtr = nullptr) {
+    // J = ceil(KP / 4) would be exact; three instantiations keep the code small
+    // (a larger J is still a valid bound, only a looser one)
+    if (KP <= 12) epi_par_phase1<3>(e, n_h, tn, base_pos, tid, nthr, last, P, cta, n_h_total, h_row0, dtr);
+    else if (KP <= 20) epi_par_phase1<5>(e, n_h, tn, base_pos, tid, nthr, last, P, cta, n_h_total, h_row0, dtr);
+    else epi_par_phase1<8>(e, n_h, tn, base_pos, tid, nthr, last, P, cta, n_h_total, h_row0, dtr);
+}
+
+// Phase 2 (after a barrier over the group), one warp per row: overflowed rows
+// take the warp fold; between tiles a buffer above KP entries is compacted to its
+// best KP (the bound becomes its KP-th entry); on the last tile the warp stores
+// the row's list (kBuf slots, -inf pads; the list maximum is the row's m, which
+// phase 1 stored) and its count.
+ES_DEV void epi_par_phase2(const EpiSmem& e, int n_h, int KP, int tn, int base_pos, int warp, int n_warps, bool last,
+                           const LmhPartials& P, int cta, int n_h_total, int h_row0, long long* dtr = nullptr) {
+    const int lane = lane_id();
+    for (int r = warp; r < n_h; r += n_warps) {
+        const int add = e.st_xcnt[r];
+        int cnt = e.st_cnt[r];
+        if (dtr && lane == 0) atomicAdd((unsigned long long*)&dtr[cnt + add > kBuf ? 8 : 9], (unsigned long long)add);
+        if (cnt + add > kBuf) {
+            float v[kTileJ];
+            float lm = -INFINITY;
+#pragma unroll
+            for (int j = 0; j < kTileJ; ++j) {
+                const int p = lane + 32 * j;
+                v[j] = p < tn ? e.tile[r * kTile + p] : -INFINITY;
+                lm = fmaxf(lm, v[j]);
+            }
+            fold_buf(e, r, KP, tn, base_pos, v, lm, !last, e.scr_v + warp * 32, e.scr_p + warp * 32);
+            cnt = e.st_cnt[r];
+        } else {
+            cnt += add;
+            if (!last && cnt > KP) {   // between tiles (hidden behind streaming): bound = the KP-th best
+                float thv;
+                int thp;
+                buf_compact_sorted(e.st_val + (size_t)r * kBuf, e.st_pos + (size_t)r * kBuf, cnt, KP, thv, thp);
+                cnt = KP;
+                if (lane == 0) { e.st_thv[r] = thv; e.st_thp[r] = thp; }
+            }
+            if (lane == 0) e.st_cnt[r] = cnt;
+        }
+        __syncwarp();
+        if (lane == 0) e.st_xcnt[r] = 0;
+        if (last) {
+            const size_t o = (size_t)cta * n_h_total + h_row0 + r;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int sl = lane + 32 * h;
+                P.val[o * kBuf + sl] = sl < cnt ? e.st_val[(size_t)r * kBuf + sl] : -INFINITY;
+                if (sl < cnt) P.id[o * kBuf + sl] = e.st_pos[(size_t)r * kBuf + sl];
+            }
+            if (lane == 0) { P.cnt[o] = 0; P.xcnt[o] = cnt; }
+        }
     }
 }
 

@@ -176,7 +176,7 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
               LmhArgs a, TcParams tp) {
     extern __shared__ __align__(1024) unsigned char tc_sm[];
     // 1024-align the stage ring (SWIZZLE_128B atoms)
-    unsigned char* base = (unsigned char*)(((uintptr_t)tc_sm + 1023) & ~(uintptr_t)1023);
+    unsigned char* base = tc_sm + ((1024u - (smem_u32(tc_sm) & 1023u)) & 1023u);   // stays a shared-window pointer (LDS/STS, not generic LD/ST)
     const int S = tp.stages, NP = tp.n_pad;
     // rows of this CTA: all n_h, or (segment mode) its segment's rows [h_row0, h_row0 + n_h)
     int n_h = a.n_h, h_row0 = 0, seg_b = -1, seg_c0 = 0, seg_m = 1;
@@ -206,6 +206,9 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
     uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
 
     const int warp = warp_id(), lane = lane_id();
+    // clock64 details of CTA 0's last tile (EVOSPEC_TRACE; profiling aid)
+    long long* const DTR = a.trace && blockIdx.x == 0 ? a.trace + 2 * kNumSMs * 8 + 48 : nullptr;
+    if (DTR && threadIdx.x == 0) { DTR[48] = 0; DTR[49] = 0; }
     // with the fused finalisation some CTAs wait for all others: dependents are
     // triggered only at the end, so they cannot take an SM one of ours still needs
     if (!a.fuse_fin) pdl_trigger();
@@ -254,6 +257,9 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
     const int n_tiles = n_body + (last_len > 0 ? 1 : 0);
 
     if (threadIdx.x == 0) TC_TRACE(0);
+    // thread-parallel fold for CTAs with two or more tiles; a single tile (small
+    // subsets) keeps the warp fold, whose first-tile bound is tighter on short tiles
+    const bool par = buffered && a.par_fold && n_tiles >= 2;
 
     auto tile_range = [&](int t, int& t0, int& tn) {
         if (t < n_body) {
@@ -375,6 +381,7 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
             const int b = t & 1;
             mbar_wait(&tfull[b], (uint32_t)(t >> 1) & 1);
             if (ew == 0 && lane == 0 && t < 2) TC_TRACE(3 + 2 * t);
+            if (DTR && ew == 0 && lane == 0 && t == n_tiles - 1) DTR[40] = clock64();
             tc_fence_after();
             const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(b * NP);
             for (int c0 = half * 16; c0 < NP; c0 += 32) {
@@ -386,15 +393,24 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
             }
             tc_fence_before();
             mbar_arrive(&tempty[b]);
+            if (DTR && ew == 0 && lane == 0 && t == n_tiles - 1) DTR[41] = clock64();
             named_bar_sync(1, nthr);
+            if (DTR && ew == 0 && lane == 0 && t == n_tiles - 1) DTR[42] = clock64();
             if (a.logits_out) {
                 for (int r = ew; r < n_h; r += kTcEpiWarps)
                     for (int p = lane; p < tn; p += 32)
                         a.logits_out[(size_t)r * a.n_subset_max + t0 + p] = e.tile[r * kTile + p];
             }
             if (t == n_tiles - 1) break;            // the last tile is folded by all warps below
-            if (buffered) epi_tile_buf(e, n_h, a.KP, tn, t0, ew, kTcEpiWarps, true);
-            else epi_tile(e, n_h, a.KP, tn, t0, ew, kTcEpiWarps);
+            if (par) {
+                epi_par_phase1_any(e, n_h, a.KP, tn, t0, ew * 32 + lane, nthr, false, a.part, blockIdx.x, a.n_h, h_row0);
+                named_bar_sync(1, nthr);
+                epi_par_phase2(e, n_h, a.KP, tn, t0, ew, kTcEpiWarps, false, a.part, blockIdx.x, a.n_h, h_row0);
+            } else if (buffered) {
+                epi_tile_buf(e, n_h, a.KP, tn, t0, ew, kTcEpiWarps, true);
+            } else {
+                epi_tile(e, n_h, a.KP, tn, t0, ew, kTcEpiWarps);
+            }
             if (ew == 0 && lane == 0 && t < 2) TC_TRACE(4 + 2 * t);
             named_bar_sync(1, nthr);
         }
@@ -405,8 +421,22 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
         int t0, tn;
         tile_range(n_tiles - 1, t0, tn);
         named_bar_sync(2, kTcWarps * 32);
-        if (buffered) epi_tile_buf_last_store(e, a.part, blockIdx.x, a.n_h, h_row0, n_h, a.KP, tn, t0, warp, kTcWarps);
-        else epi_tile_last(e, a.part, blockIdx.x, a.n_h, h_row0, n_h, a.KP, a.LS, tn, t0, warp, kTcWarps);
+        if (DTR && warp == kTcEpiWarp0 && lane == 0) DTR[43] = clock64();
+        if (par) {
+            epi_par_phase1_any(e, n_h, a.KP, tn, t0, threadIdx.x, kTcWarps * 32, true, a.part, blockIdx.x, a.n_h, h_row0,
+                               DTR && warp == kTcEpiWarp0 ? DTR + 50 : nullptr);
+            if (DTR && warp == kTcEpiWarp0 && lane == 0) DTR[44] = clock64();
+            named_bar_sync(2, kTcWarps * 32);
+            if (DTR && warp == kTcEpiWarp0 && lane == 0) DTR[45] = clock64();
+            epi_par_phase2(e, n_h, a.KP, tn, t0, warp, kTcWarps, true, a.part, blockIdx.x, a.n_h, h_row0,
+                           DTR ? DTR + 40 : nullptr);
+            if (DTR && warp == kTcEpiWarp0 && lane == 0) DTR[46] = clock64();
+        } else if (buffered) {
+            epi_tile_buf_last_store(e, a.part, blockIdx.x, a.n_h, h_row0, n_h, a.KP, tn, t0, warp, kTcWarps,
+                                    warp == kTcEpiWarp0 ? DTR : nullptr);
+        } else {
+            epi_tile_last(e, a.part, blockIdx.x, a.n_h, h_row0, n_h, a.KP, a.LS, tn, t0, warp, kTcWarps);
+        }
         if (warp == kTcEpiWarp0 && lane == 0 && n_tiles - 1 < 2) TC_TRACE(4 + 2 * (n_tiles - 1));
     }
     tc_fence_before();

@@ -62,3 +62,23 @@ for pf in (sys.argv[1:] or ["2"]):
     if det[0] > 0:
         print("   finalize row 0 clock64 deltas (cycles from slot 0):",
               {i: int(det[i] - det[0]) for i in range(32) if det[i] > 0})
+    dd = ctx.read_trace(296 * 8 + 48 + 64)[296 * 8 + 48:].astype(np.int64)
+    b = dd[40]
+    if b > 0:
+        print("   CTA0 last tile clock64 (cycles from tfull): tmem->smem", dd[41] - b, "bar1", dd[42] - b, "bar2", dd[43] - b,
+              "par1", dd[44] - b, "bar", dd[45] - b, "par2", dd[46] - b, "cands overflow/ok", dd[48], dd[49])
+        print("   phase1 detail (rowstate, pass1 done, pass2 done, stores done):", [int(dd[50 + i] - b) for i in (3, 0, 1, 2)])
+        for it in range(5):
+            if dd[it * 4] > 0:
+                print("     row", it, [int(dd[it * 4 + j] - b) for j in range(4)])
+    evs = []
+    for it in range(8):
+        flush.fill_(it)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        ctx.subset_logits_topk_merged(Wd, Hd, Sd, nd, n_S, k)
+        e1.record()
+        evs.append((e0, e1))
+    torch.cuda.synchronize()
+    times = [a.elapsed_time(b) * 1e3 for a, b in evs]
+    print(f"   merged path: median {statistics.median(times[2:]):.1f} us")
