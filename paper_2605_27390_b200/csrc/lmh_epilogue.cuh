@@ -42,11 +42,12 @@ struct EpiSmem {
     int* st_xcnt;    // [n_h] extras appended by the last tile (global partials)
     float* scr_v;    // [n_warps][32] candidate batch scratch
     int* scr_p;      // [n_warps][32]
+    int* st_flag;    // [4] block flags (thread-parallel fold: a row overflowed)
 };
 
 __host__ __device__ inline size_t epi_smem_bytes(int n_h, int cap, int n_warps) {
     return (size_t)n_h * kTile * 4 + (size_t)n_h * cap * 8 + (size_t)n_h * 20 + (size_t)n_h * 32 * 4 +
-           (size_t)n_warps * 32 * 8;
+           (size_t)n_warps * 32 * 8 + 16;
 }
 
 ES_DEV EpiSmem epi_carve(unsigned char* p, int n_h, int cap, int n_warps) {
@@ -61,7 +62,8 @@ ES_DEV EpiSmem epi_carve(unsigned char* p, int n_h, int cap, int n_warps) {
     e.st_ls = (float*)p;       p += (size_t)n_h * 32 * 4;
     e.st_xcnt = (int*)p;       p += (size_t)n_h * 4;
     e.scr_v = (float*)p;       p += (size_t)n_warps * 32 * 4;
-    e.scr_p = (int*)p;
+    e.scr_p = (int*)p;         p += (size_t)n_warps * 32 * 4;
+    e.st_flag = (int*)p;
     return e;
 }
 
@@ -69,6 +71,7 @@ ES_DEV void epi_init(const EpiSmem& e, int n_h) {
     for (int r = threadIdx.x; r < n_h; r += blockDim.x) {
         e.st_cnt[r] = 0;
         e.st_xcnt[r] = 0;
+        if (r == 0) e.st_flag[0] = 0;
         e.st_m[r] = -INFINITY;
         e.st_thv[r] = -INFINITY;
         e.st_thp[r] = 0x7fffffff;
@@ -783,8 +786,10 @@ ES_DEV void epi_par_phase1(const EpiSmem& e, int n_h, int tn, int base_pos, int 
             for (int c = 0; c < 4; ++c) {
                 const float ex = ex2_approx(fmaf(x4[c], 1.4426950408889634f, -mb));
                 if (c & 1) sum1 += ex; else sum0 += ex;
-                const bool adm = x4[c] > thv || (x4[c] == thv && x4[c] != -INFINITY && p0 + c < thp);
-                cm |= (unsigned)adm << (4 * j + c);
+                // (bitwise, not short-circuit: no branch per value)
+                const unsigned adm = (unsigned)(x4[c] > thv) |
+                                     ((unsigned)(x4[c] == thv) & (unsigned)(x4[c] != -INFINITY) & (unsigned)(p0 + c < thp));
+                cm |= adm << (4 * j + c);
             }
         }
         float sum = sum0 + sum1;
@@ -836,19 +841,35 @@ ES_DEV void epi_par_phase1_any(const EpiSmem& e, int n_h, int KP, int tn, int ba
     else epi_par_phase1<8>(e, n_h, tn, base_pos, tid, nthr, last, P, cta, n_h_total, h_row0, dtr);
 }
 
-// Phase 2 (after a barrier over the group), one warp per row: overflowed rows
-// take the warp fold; between tiles a buffer above KP entries is compacted to its
-// best KP (the bound becomes its KP-th entry); on the last tile the warp stores
-// the row's list (kBuf slots, -inf pads; the list maximum is the row's m, which
-// phase 1 stored) and its count.
-ES_DEV void epi_par_phase2(const EpiSmem& e, int n_h, int KP, int tn, int base_pos, int warp, int n_warps, bool last,
-                           const LmhPartials& P, int cta, int n_h_total, int h_row0, long long* dtr = nullptr) {
-    const int lane = lane_id();
-    for (int r = warp; r < n_h; r += n_warps) {
-        const int add = e.st_xcnt[r];
-        int cnt = e.st_cnt[r];
-        if (dtr && lane == 0) atomicAdd((unsigned long long*)&dtr[cnt + add > kBuf ? 8 : 9], (unsigned long long)add);
+// Phase 2 (after a barrier over the group of nthr threads, named barrier bar):
+//   2a one thread per row commits the appended count (a row that would overflow
+//      keeps its count and raises a block flag);
+//   2b only if flagged: overflowed rows take the warp fold (fold_buf);
+//   2c between tiles, one warp per row compacts a buffer above KP entries to its
+//      best KP (the bound becomes its KP-th entry) -- hidden behind streaming;
+//      on the last tile every thread stores list slots instead (kBuf slots per
+//      row, -inf pads; the list maximum is the row's m, stored in phase 1).
+ES_DEV void epi_par_phase2(const EpiSmem& e, int n_h, int KP, int tn, int base_pos, int tid, int nthr, int bar,
+                           bool last, const LmhPartials& P, int cta, int n_h_total, int h_row0) {
+    const int lane = lane_id(), warp = tid >> 5, n_warps = nthr >> 5;
+    for (int r = tid; r < n_h; r += nthr) {
+        const int add = e.st_xcnt[r], cnt = e.st_cnt[r];
         if (cnt + add > kBuf) {
+            e.st_flag[0] = 1;
+        } else {
+            e.st_cnt[r] = cnt + add;
+            e.st_xcnt[r] = 0;
+            if (last) {
+                const size_t o = (size_t)cta * n_h_total + h_row0 + r;
+                P.cnt[o] = 0;
+                P.xcnt[o] = cnt + add;
+            }
+        }
+    }
+    named_bar_sync(bar, nthr);
+    if (e.st_flag[0]) {   // uniform: read by every thread after the barrier
+        for (int r = warp; r < n_h; r += n_warps) {
+            if (e.st_xcnt[r] == 0) continue;
             float v[kTileJ];
             float lm = -INFINITY;
 #pragma unroll
@@ -858,29 +879,37 @@ ES_DEV void epi_par_phase2(const EpiSmem& e, int n_h, int KP, int tn, int base_p
                 lm = fmaxf(lm, v[j]);
             }
             fold_buf(e, r, KP, tn, base_pos, v, lm, !last, e.scr_v + warp * 32, e.scr_p + warp * 32);
-            cnt = e.st_cnt[r];
-        } else {
-            cnt += add;
-            if (!last && cnt > KP) {   // between tiles (hidden behind streaming): bound = the KP-th best
+            if (lane == 0) {
+                e.st_xcnt[r] = 0;
+                if (last) {
+                    const size_t o = (size_t)cta * n_h_total + h_row0 + r;
+                    P.cnt[o] = 0;
+                    P.xcnt[o] = e.st_cnt[r];
+                }
+            }
+            __syncwarp();
+        }
+        named_bar_sync(bar, nthr);
+        if (tid == 0) e.st_flag[0] = 0;
+    }
+    if (!last) {
+        for (int r = warp; r < n_h; r += n_warps) {
+            const int cnt = e.st_cnt[r];
+            if (cnt > KP) {
                 float thv;
                 int thp;
                 buf_compact_sorted(e.st_val + (size_t)r * kBuf, e.st_pos + (size_t)r * kBuf, cnt, KP, thv, thp);
-                cnt = KP;
-                if (lane == 0) { e.st_thv[r] = thv; e.st_thp[r] = thp; }
+                if (lane == 0) { e.st_cnt[r] = KP; e.st_thv[r] = thv; e.st_thp[r] = thp; }
+                __syncwarp();
             }
-            if (lane == 0) e.st_cnt[r] = cnt;
         }
-        __syncwarp();
-        if (lane == 0) e.st_xcnt[r] = 0;
-        if (last) {
+    } else {
+        for (int i = tid; i < n_h * kBuf; i += nthr) {
+            const int r = i / kBuf, sl = i - r * kBuf;
             const size_t o = (size_t)cta * n_h_total + h_row0 + r;
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int sl = lane + 32 * h;
-                P.val[o * kBuf + sl] = sl < cnt ? e.st_val[(size_t)r * kBuf + sl] : -INFINITY;
-                if (sl < cnt) P.id[o * kBuf + sl] = e.st_pos[(size_t)r * kBuf + sl];
-            }
-            if (lane == 0) { P.cnt[o] = 0; P.xcnt[o] = cnt; }
+            const int cnt = e.st_cnt[r];
+            P.val[o * kBuf + sl] = sl < cnt ? e.st_val[i] : -INFINITY;
+            if (sl < cnt) P.id[o * kBuf + sl] = e.st_pos[i];
         }
     }
 }

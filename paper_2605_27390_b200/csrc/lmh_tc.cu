@@ -158,7 +158,6 @@ ES_DEV long long gtime() {
 }
 #define TC_TRACE(slot) do { if (a.trace) a.trace[(size_t)blockIdx.x * 8 + (slot)] = gtime(); } while (0)
 
-ES_DEV void named_bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
 // ------------------------------------------------------------------ kernel
 struct TcParams {
@@ -405,7 +404,7 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
             if (par) {
                 epi_par_phase1_any(e, n_h, a.KP, tn, t0, ew * 32 + lane, nthr, false, a.part, blockIdx.x, a.n_h, h_row0);
                 named_bar_sync(1, nthr);
-                epi_par_phase2(e, n_h, a.KP, tn, t0, ew, kTcEpiWarps, false, a.part, blockIdx.x, a.n_h, h_row0);
+                epi_par_phase2(e, n_h, a.KP, tn, t0, ew * 32 + lane, nthr, 1, false, a.part, blockIdx.x, a.n_h, h_row0);
             } else if (buffered) {
                 epi_tile_buf(e, n_h, a.KP, tn, t0, ew, kTcEpiWarps, true);
             } else {
@@ -428,8 +427,7 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
             if (DTR && warp == kTcEpiWarp0 && lane == 0) DTR[44] = clock64();
             named_bar_sync(2, kTcWarps * 32);
             if (DTR && warp == kTcEpiWarp0 && lane == 0) DTR[45] = clock64();
-            epi_par_phase2(e, n_h, a.KP, tn, t0, warp, kTcWarps, true, a.part, blockIdx.x, a.n_h, h_row0,
-                           DTR ? DTR + 40 : nullptr);
+            epi_par_phase2(e, n_h, a.KP, tn, t0, threadIdx.x, kTcWarps * 32, 2, true, a.part, blockIdx.x, a.n_h, h_row0);
             if (DTR && warp == kTcEpiWarp0 && lane == 0) DTR[46] = clock64();
         } else if (buffered) {
             epi_tile_buf_last_store(e, a.part, blockIdx.x, a.n_h, h_row0, n_h, a.KP, tn, t0, warp, kTcWarps,
