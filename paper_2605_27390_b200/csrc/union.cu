@@ -245,6 +245,175 @@ ES_DEV void block_topM(const uint64_t* ck, const int32_t* cid, uint8_t* cf, int 
     __syncthreads();
 }
 
+// K exact top-M selections at once (K <= 3): selection j takes the M[j] best
+// (key desc, id asc) of the candidates whose flag has a bit of A[j] and marks
+// them with S[j]. The radix passes of block_topM run in lockstep: one read of
+// the candidates per pass feeds K histograms, one K-wide block scan finds the K
+// boundary bins -- the passes' barriers are paid once instead of K times.
+template <int K>
+ES_DEV void block_scan_multi(const int (&v)[K], int* warp_tot /*[K][33]*/, int (&excl)[K]) {
+    const int lane = lane_id(), wid = warp_id(), nw = blockDim.x / 32;
+    int inc[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+        inc[j] = v[j];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, inc[j], o);
+            if (lane >= o) inc[j] += t;
+        }
+        if (lane == 31) warp_tot[j * 33 + wid] = inc[j];
+    }
+    __syncthreads();
+    if (wid < K) {
+        const int w = lane < nw ? warp_tot[wid * 33 + lane] : 0;
+        int wi = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, wi, o);
+            if (lane >= o) wi += t;
+        }
+        if (lane < nw) warp_tot[wid * 33 + lane] = wi - w;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < K; ++j) excl[j] = warp_tot[j * 33 + wid] + inc[j] - v[j];
+    __syncthreads();
+}
+
+template <int K>
+ES_DEV void block_topM_multi(const uint64_t* ck, const int32_t* cid, uint8_t* cf, int n, const uint8_t (&A)[K],
+                             const uint8_t (&S)[K], const int (&M)[K], uint32_t* hist /*[K][kSelBins]*/,
+                             BSel* st /*[K]*/, int* warp_tot /*[K][33]*/) {
+    const int tid = threadIdx.x, T = blockDim.x, lane = lane_id();
+    int c[K];
+    uint64_t kmin[K], kmax[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) { c[j] = 0; kmin[j] = ~0ull; kmax[j] = 0ull; }
+    for (int i = tid; i < n; i += T) {
+        const uint8_t f = cf[i];
+        const uint64_t k = ck[i];
+#pragma unroll
+        for (int j = 0; j < K; ++j)
+            if (f & A[j]) { ++c[j]; kmin[j] = min(kmin[j], k); kmax[j] = max(kmax[j], k); }
+    }
+    if (tid < K) { st[tid].kmin = ~0ull; st[tid].kmax = 0ull; }
+    int cnt[K];
+    {
+        int ex[K];
+        block_scan_multi<K>(c, warp_tot, ex);   // (syncs: st initialised before the atomics)
+#pragma unroll
+        for (int j = 0; j < K; ++j) cnt[j] = 0;
+        // totals: the last thread's exclusive prefix plus its own count
+        if (tid == T - 1)
+#pragma unroll
+            for (int j = 0; j < K; ++j) warp_tot[j * 33 + 32] = ex[j] + c[j];
+    }
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+        kmin[j] = warp_min_u64(kmin[j]);
+        kmax[j] = warp_max_u64(kmax[j]);
+        if (lane == 0 && kmin[j] <= kmax[j]) {
+            atomicMin((unsigned long long*)&st[j].kmin, kmin[j]);
+            atomicMax((unsigned long long*)&st[j].kmax, kmax[j]);
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < K; ++j) cnt[j] = warp_tot[j * 33 + 32];
+    bool all[K];   // select every active candidate (M >= count); M <= 0 selects none
+#pragma unroll
+    for (int j = 0; j < K; ++j) all[j] = M[j] >= cnt[j];
+    if (tid < K) {
+        st[tid].kmask = 0; st[tid].kval = 0; st[tid].imask = 0; st[tid].ival = 0;
+        st[tid].remaining = M[tid];
+        st[tid].done = (M[tid] <= 0 || M[tid] >= cnt[tid]) ? 1 : 0;
+    }
+    __syncthreads();
+    int kbit[K], ibit[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+        const uint64_t diff = st[j].kmin ^ st[j].kmax;
+        kbit[j] = diff ? 63 - __clzll((long long)diff) : -1;
+        ibit[j] = 31;
+    }
+    for (int pass = 0; pass < 16; ++pass) {
+        bool live[K];
+        bool any = false;
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+            live[j] = !st[j].done && (kbit[j] >= 0 || ibit[j] >= 0);
+            any |= live[j];
+        }
+        if (!any) break;
+        int lo[K], hi_[K];
+        uint32_t dmask[K];
+        bool on_key[K];
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+            on_key[j] = kbit[j] >= 0;
+            hi_[j] = on_key[j] ? kbit[j] : ibit[j];
+            const int width = hi_[j] + 1 < 10 ? hi_[j] + 1 : 10;
+            lo[j] = hi_[j] - width + 1;
+            dmask[j] = (1u << width) - 1u;
+        }
+#pragma unroll
+        for (int j = 0; j < K; ++j)
+            if (live[j]) for (int b = tid; b < kSelBins; b += T) hist[j * kSelBins + b] = 0;
+        __syncthreads();
+        BSel my[K];
+#pragma unroll
+        for (int j = 0; j < K; ++j) my[j] = st[j];
+        for (int i = tid; i < n; i += T) {
+            const uint8_t f = cf[i];
+            const uint64_t k = ck[i];
+            const int32_t id = cid[i];
+#pragma unroll
+            for (int j = 0; j < K; ++j)
+                if (live[j] && (f & A[j]) && bmatch(k, id, my[j]))
+                    atomicAdd(&hist[j * kSelBins + (on_key[j] ? (uint32_t)(k >> lo[j]) & dmask[j]
+                                                              : ((0xFFFFFFFFu - (uint32_t)id) >> lo[j]) & dmask[j])],
+                              1u);
+        }
+        __syncthreads();
+        const int bin = kSelBins - 1 - tid;
+        int hb[K], above[K];
+#pragma unroll
+        for (int j = 0; j < K; ++j) hb[j] = (live[j] && tid < kSelBins) ? (int)hist[j * kSelBins + bin] : 0;
+        block_scan_multi<K>(hb, warp_tot, above);
+#pragma unroll
+        for (int j = 0; j < K; ++j)
+            if (live[j] && tid < kSelBins && above[j] < my[j].remaining && above[j] + hb[j] >= my[j].remaining) {
+                st[j].found_bin = bin;
+                st[j].found_above = above[j];
+            }
+        __syncthreads();
+        if (tid < K && live[tid]) {
+            BSel& s2 = st[tid];
+            const int b = s2.found_bin;
+            s2.remaining -= s2.found_above;
+            if (on_key[tid]) { s2.kmask |= (uint64_t)dmask[tid] << lo[tid]; s2.kval |= (uint64_t)b << lo[tid]; }
+            else { s2.imask |= dmask[tid] << lo[tid]; s2.ival |= (uint32_t)b << lo[tid]; }
+            if ((uint32_t)s2.remaining == hist[tid * kSelBins + b]) s2.done = 1;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < K; ++j)
+            if (live[j]) { if (on_key[j]) kbit[j] = lo[j] - 1; else ibit[j] = lo[j] - 1; }
+    }
+    BSel my[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) my[j] = st[j];
+    for (int i = tid; i < n; i += T) {
+        const uint8_t f = cf[i];
+        uint8_t add = 0;
+#pragma unroll
+        for (int j = 0; j < K; ++j)
+            if ((f & A[j]) && M[j] > 0 && (all[j] || bselected(ck[i], cid[i], my[j]))) add |= S[j];
+        if (add) cf[i] = f | add;
+    }
+    __syncthreads();
+}
 enum : uint8_t { kCand = 1, kSem = 2, kGs = 4, kNew = 8, kTake = 16 };
 
 __global__ void __launch_bounds__(kUnionThreads, 1)
@@ -270,9 +439,9 @@ union_kernel(int V, const int32_t* __restrict__ static_ids, int n_static,
     int32_t* gs = goff + kMaxG + 1;                          // [kMaxG] ordered S_sem prefix
     int32_t* graph = gs + kMaxG;                             // [kMaxG * per_seed]
     uint8_t* cf = (uint8_t*)(graph + kMaxG * per_seed);      // [cap]
-    __shared__ int warp_tot[33];
-    __shared__ uint32_t hist[kSelBins];
-    __shared__ BSel bsel;
+    __shared__ int warp_tot[3 * 33];
+    __shared__ uint32_t hist[3 * kSelBins];
+    __shared__ BSel bsel[3];
     __shared__ int nG_s, bad_s, taken_s, ngs_s, sem_n_s;
 
     const int tid = threadIdx.x, lane = lane_id(), T = blockDim.x;
@@ -299,6 +468,32 @@ union_kernel(int V, const int32_t* __restrict__ static_ids, int n_static,
             atomicOr(&bits[v[u] >> 5], 1u << (v[u] & 31));
         }
     }
+    // formation starts with the seeds (C6): they and the static set are
+    // inputs, so warp 0 walks them before the wait too
+    const unsigned lt_mask = (1u << lane) - 1u;
+    auto walk = [&](const int32_t* src, int len, int taken) -> int {
+        for (int base = 0; base < len && taken < n_dyn; base += 32) {
+            const int idx = base + lane;
+            int32_t c = idx < len ? src[idx] : -1;
+            const bool valid = c >= 0 && c < V;
+            if (idx < len && !valid) bad_s = 1;
+            if (!valid) c = -1 - lane;            // distinct non-matching sentinel
+            const unsigned peers = __match_any_sync(0xffffffffu, c);
+            const bool first = valid && ((__ffs(peers) - 1) == lane);
+            const bool cand = first && !((bits[c < 0 ? 0 : (c >> 5)] >> (c & 31)) & 1u);
+            const unsigned bal = __ballot_sync(0xffffffffu, cand);
+            const int bf = __popc(bal & lt_mask);
+            if (cand && taken + bf < n_dyn) atomicOr(&bits[c >> 5], 1u << (c & 31));
+            taken += min(__popc(bal), n_dyn - taken);
+            __syncwarp();
+        }
+        return taken;
+    };
+    __syncthreads();
+    if (warp_id() == 0) {
+        const int t = walk(seeds, n_seed, 0);
+        if (lane == 0) taken_s = t;
+    }
     pdl_wait();
     // the selection has consumed the scan's histogram: leave it zero for the next build
     if (clear_hist)
@@ -324,8 +519,26 @@ union_kernel(int V, const int32_t* __restrict__ static_ids, int n_static,
     }
     __syncthreads();
     if (trace) { __syncthreads(); if (threadIdx.x == 0) { long long t_; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); trace[1] = t_; } }
-    // 2. S_sem = exact top-N of the candidate superset
-    block_topM(ck, cid, cf, n_cand, kCand, kSem, n_sem, hist, bsel, warp_tot);
+    // 2.-3. three exact selections in one set of radix passes (block_topM_multi):
+    //   S_sem      = the n_sem best candidates                          (kSem)
+    //   T_b        = the `budget` best NEW candidates (not static, not a seed) (kTake)
+    //   S_sem[:ngs] = the ngs best candidates (graph seeds, ordered below) (kGs)
+    // The new members of S_sem are a prefix of the new candidates in (key desc,
+    // id asc) order, so "the first `budget` new ids of S_sem in S_sem order"
+    // (the formation's semantic part) is T_b intersected with S_sem.
+    const int taken0 = taken_s;
+    const int budget = n_dyn - taken0;
+    for (int i = tid; i < n_cand; i += T)
+        if ((cf[i] & kCand) && !((bits[cid[i] >> 5] >> (cid[i] & 31)) & 1u)) cf[i] |= kNew;
+    const int ngs = min(n_graph_sem_seeds, min(n_sem, kMaxG));
+    if (tid == 0) ngs_s = 0;
+    __syncthreads();
+    {
+        const uint8_t A[3] = {kCand, kNew, kCand};
+        const uint8_t S[3] = {kSem, kTake, kGs};
+        const int M[3] = {n_sem, budget, ngs};
+        block_topM_multi<3>(ck, cid, cf, n_cand, A, S, M, hist, bsel, warp_tot);
+    }
     if (sem_out) {
         for (int base = 0; base < n_cand; base += T) {      // one smem atomic per warp
             const int i = base + tid;
@@ -338,57 +551,19 @@ union_kernel(int V, const int32_t* __restrict__ static_ids, int n_static,
         }
     }
     if (trace) { __syncthreads(); if (threadIdx.x == 0) { long long t_; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); trace[2] = t_; } }
-    // 3. ordered prefix S_sem[:n_graph_sem_seeds]: one 1024-bin histogram pass
-    //    over the S_sem key range finds the few candidates that can be in the
-    //    prefix; they are gathered and ranked exactly (block_topM fallback).
-    const int ngs = min(n_graph_sem_seeds, min(n_sem, kMaxG));
-    if (tid == 0) { ngs_s = 0; bsel.kmin = ~0ull; bsel.kmax = 0ull; bsel.found_bin = 0; bsel.found_above = 0x7fffffff; }
-    __syncthreads();
-    {
-        uint64_t kmn = ~0ull, kmx = 0ull;
-        for (int i = tid; i < n_cand; i += T)
-            if (cf[i] & kSem) { kmn = min(kmn, ck[i]); kmx = max(kmx, ck[i]); }
-        kmn = warp_min_u64(kmn);
-        kmx = warp_max_u64(kmx);
-        if (lane == 0 && kmn <= kmx) { atomicMin((unsigned long long*)&bsel.kmin, kmn); atomicMax((unsigned long long*)&bsel.kmax, kmx); }
-        for (int b = tid; b < kSelBins; b += T) hist[b] = 0;
-    }
-    __syncthreads();
-    const uint64_t gkmin = bsel.kmin, grange = bsel.kmax >= bsel.kmin ? bsel.kmax - bsel.kmin : 0ull;
-    const int gshift = grange ? max(0, 64 - __clzll((long long)grange) - 10) : 0;
-    if (ngs > 0) {
-        for (int i = tid; i < n_cand; i += T)
-            if (cf[i] & kSem) atomicAdd(&hist[(uint32_t)((ck[i] - gkmin) >> gshift)], 1u);
-        __syncthreads();
-        const int bin = kSelBins - 1 - tid;
-        const uint32_t hb = hist[bin];
-        int tot_unused;
-        const int above = block_excl_scan((int)hb, warp_tot, tot_unused);
-        if (above < ngs && above + (int)hb >= ngs) { bsel.found_bin = bin; bsel.found_above = above + (int)hb; }
-        __syncthreads();
-        const uint32_t bmin = (uint32_t)bsel.found_bin;
-        if (bsel.found_above <= kMaxG) {
-            for (int i = tid; i < n_cand; i += T)
-                if ((cf[i] & kSem) && (uint32_t)((ck[i] - gkmin) >> gshift) >= bmin) {
-                    const int slot = atomicAdd(&ngs_s, 1);
-                    if (slot < kMaxG) graph[slot] = i;      // graph[] as scratch: candidate index
-                }
-        } else {
-            block_topM(ck, cid, cf, n_cand, kSem, kGs, ngs, hist, bsel, warp_tot);
-            for (int i = tid; i < n_cand; i += T)
-                if (cf[i] & kGs) {
-                    const int slot = atomicAdd(&ngs_s, 1);
-                    if (slot < kMaxG) graph[slot] = i;
-                }
+    // the ngs graph seeds in S_sem order: gathered, ranked exactly by counting
+    for (int i = tid; i < n_cand; i += T)
+        if (cf[i] & kGs) {
+            const int slot = atomicAdd(&ngs_s, 1);
+            if (slot < kMaxG) graph[slot] = i;      // graph[] as scratch: candidate index
         }
-    }
     __syncthreads();
     const int ngs_pool = min(ngs_s, kMaxG);
-    for (int a = tid; a < ngs_pool; a += T) {
-        const int ia = graph[a];
+    for (int a2 = tid; a2 < ngs_pool; a2 += T) {
+        const int ia = graph[a2];
         int rank = 0;
-        for (int b = 0; b < ngs_pool; ++b) {
-            const int ib = graph[b];
+        for (int b2 = 0; b2 < ngs_pool; ++b2) {
+            const int ib = graph[b2];
             rank += before(ck[ib], cid[ib], ck[ia], cid[ia]) ? 1 : 0;   // (key desc, id asc)
         }
         if (rank < ngs) gs[rank] = cid[ia];
@@ -445,43 +620,12 @@ union_kernel(int V, const int32_t* __restrict__ static_ids, int n_static,
 
     if (trace) { __syncthreads(); if (threadIdx.x == 0) { long long t_; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); trace[4] = t_; } }
     // 5. formation: seeds ++ S_sem ++ S_graph ++ S_ctx, first occurrence, skip
-    //    members (static or taken), stop at N_dyn. Seeds, graph and ctx are
-    //    walked by warp 0 in 32-wide windows; the S_sem part (distinct ids)
-    //    takes its first (budget) new ids in S_sem order by an exact block
-    //    top-M over the new ones -- the same set the sequential walk takes.
-    const unsigned lt_mask = (1u << lane) - 1u;
-    auto walk = [&](const int32_t* src, int len, int taken) -> int {
-        for (int base = 0; base < len && taken < n_dyn; base += 32) {
-            const int idx = base + lane;
-            int32_t c = idx < len ? src[idx] : -1;
-            const bool valid = c >= 0 && c < V;
-            if (idx < len && !valid) bad_s = 1;
-            if (!valid) c = -1 - lane;            // distinct non-matching sentinel
-            const unsigned peers = __match_any_sync(0xffffffffu, c);
-            const bool first = valid && ((__ffs(peers) - 1) == lane);
-            const bool cand = first && !((bits[c < 0 ? 0 : (c >> 5)] >> (c & 31)) & 1u);
-            const unsigned bal = __ballot_sync(0xffffffffu, cand);
-            const int bf = __popc(bal & lt_mask);
-            if (cand && taken + bf < n_dyn) atomicOr(&bits[c >> 5], 1u << (c & 31));
-            taken += min(__popc(bal), n_dyn - taken);
-            __syncwarp();
-        }
-        return taken;
-    };
-    if (warp_id() == 0) {
-        const int t = walk(seeds, n_seed, 0);
-        if (lane == 0) taken_s = t;
-    }
-    __syncthreads();
-    const int taken0 = taken_s;
-    const int budget = n_dyn - taken0;
-    for (int i = tid; i < n_cand; i += T)
-        if ((cf[i] & kSem) && !((bits[cid[i] >> 5] >> (cid[i] & 31)) & 1u)) cf[i] |= kNew;
-    __syncthreads();
-    block_topM(ck, cid, cf, n_cand, kNew, kTake, budget, hist, bsel, warp_tot);
+    //    members (static or taken), stop at N_dyn. The seeds were walked before
+    //    the wait; the S_sem part is T_b and S_sem (selected above); graph and
+    //    ctx are walked by warp 0 in 32-wide windows.
     int c_take = 0;
     for (int i = tid; i < n_cand; i += T)
-        if (cf[i] & kTake) { atomicOr(&bits[cid[i] >> 5], 1u << (cid[i] & 31)); ++c_take; }
+        if ((cf[i] & kTake) && (cf[i] & kSem)) { atomicOr(&bits[cid[i] >> 5], 1u << (cid[i] & 31)); ++c_take; }
     const int took = block_count(c_take, warp_tot);
     if (warp_id() == 0) {
         const int n_ctx_sel = ctx_sel ? *n_ctx_sel_dev : 0;
@@ -627,7 +771,7 @@ static size_t union_fixed_bytes(int V, int per_seed) {
 
 // Largest candidate superset the union kernel can hold in shared memory.
 int union_cand_cap(int V, int per_seed) {
-    const size_t budget = 220 * 1024;
+    const size_t budget = 212 * 1024;   // + ~12.6 KB static (three selection histograms)
     const size_t fixed = union_fixed_bytes(V, per_seed);
     if (fixed >= budget) return 0;
     return (int)((budget - fixed) / 13) & ~15;

@@ -235,6 +235,20 @@ def test_lmh_paths(lmh_path, path, n_h, k):
     assert np.all(err <= gamma * hn * wmax / 8), (err / (hn * wmax)).max()
 
 
+@pytest.mark.parametrize("k,integer", [(1, False), (10, False), (24, False), (10, True)])
+def test_tc_multitile_thread_parallel_fold(lmh_path, k, integer):
+    """Subsets longer than two 128-row tiles per CTA (n_S > 2 * 128 * 148): the tensor-core
+    kernel's thread-parallel fold for every bound width (J = 3 / 5 / 8 for k + 8 <= 12 / 20 /
+    32), and with integer inputs (massive exact ties) its overflow fallback to the warp fold."""
+    lmh_path("tc")
+    P = G.make_problem(31, dtype="bf16", integer=integer, V=60000, d=256, n_static=40000, n_sem=6000,
+                       n_dyn=5000, n_h=8, k=k)
+    got = run_path(P)
+    ref = G.oracle_step(oracle, P)
+    assert got["S"].size > 2 * 128 * 148
+    check(P, got, ref, k)
+
+
 def test_tc_integer_exact(lmh_path):
     """Integer inputs: tcgen05 fp32 accumulation is exact (sums < 2^24)."""
     lmh_path("tc")
