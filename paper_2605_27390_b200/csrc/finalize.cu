@@ -313,20 +313,20 @@ lmh_finalize_kernel(LmhArgs a, int n_cta, int k, float gamma, const float* __res
 
 
 
-template <int U>
-__global__ void __launch_bounds__(kFin32Threads)
+template <int U, int NT>
+__global__ void __launch_bounds__(NT)
 lmh_finalize32_kernel(LmhArgs a, int n_cta_arg, int k, float gamma, const float* __restrict__ wmax_dev,
                       int32_t* __restrict__ topk_ids, float* __restrict__ topk_vals,
                       float* __restrict__ row_max, float* __restrict__ row_sumexp, int* flags) {
     extern __shared__ __align__(16) unsigned char f32_sm[];
     pdl_trigger();
-    const Fin32Smem sm = fin32_carve(f32_sm, kFin32Threads);
+    const Fin32Smem sm = fin32_carve(f32_sm, NT);
     // H row and ||h||^2 need only the LM head's inputs: before the wait (overlaps its tail)
     const bool pre = a.fin_opt & 1;
-    const double hacc = pre ? fin32_stage_h<kFin32Threads>(a, blockIdx.x, sm) : 0.0;
+    const double hacc = pre ? fin32_stage_h<NT>(a, blockIdx.x, sm) : 0.0;
     pdl_wait();
-    fin32_row<U, kFin32Threads>(a, blockIdx.x, n_cta_arg, k, gamma, wmax_dev, topk_ids, topk_vals, row_max,
-                                row_sumexp, flags, sm, pre, hacc);
+    fin32_row<U, NT>(a, blockIdx.x, n_cta_arg, k, gamma, wmax_dev, topk_ids, topk_vals, row_max,
+                     row_sumexp, flags, sm, pre, hacc);
 
 }
 
@@ -335,21 +335,23 @@ void launch_lmh_finalize(const LmhArgs& a, int n_cta, int k, const float* wmax_d
                          float gamma) {
     if (a.KP <= 32 && a.LS == kFin32LS && n_cta * (kFin32LS / 4) <= 10 * kFin32Threads) {
         // one CTA per SM while the rows fit one wave (the dynamic allocation is only
-        // a placement hint: two CTAs sharing an SM measured slower); more rows pack
-        const size_t smem = std::max(fin32_smem_bytes(kFin32Threads), (size_t)(a.n_h <= kNumSMs ? 120 * 1024 : 0));
-        if (n_cta * (kFin32LS / 4) <= 5 * kFin32Threads) {
-            static thread_local bool set5 = false;   // (placement hint size is fixed)
-            if (!set5) set5 = cudaFuncSetAttribute(lmh_finalize32_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                   120 * 1024) == cudaSuccess;
-            launch_pdl(lmh_finalize32_kernel<5>, dim3(a.n_h), dim3(kFin32Threads), smem, st, a, n_cta, k, gamma,
-                       wmax_dev, topk_ids, topk_vals, row_max, row_sumexp, flags);
-        } else {
-            static thread_local bool set10 = false;
-            if (!set10) set10 = cudaFuncSetAttribute(lmh_finalize32_kernel<10>,
-                                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 120 * 1024) == cudaSuccess;
-            launch_pdl(lmh_finalize32_kernel<10>, dim3(a.n_h), dim3(kFin32Threads), smem, st, a, n_cta, k, gamma,
-                       wmax_dev, topk_ids, topk_vals, row_max, row_sumexp, flags);
-        }
+        // a placement hint: two CTAs sharing an SM measured slower); more rows pack.
+        // 512 threads with 5 or 10 list loads each; EVOSPEC_FIN_NT=1024 takes 1024
+        // threads with 3 while the lists fit (measured equal in the sweep, slower alone)
+        static const int fin_nt = getenv("EVOSPEC_FIN_NT") ? atoi(getenv("EVOSPEC_FIN_NT")) : 512;
+        const int nq = n_cta * (kFin32LS / 4);
+        auto go = [&](auto kern, int nt, bool& attr_set) {
+            const size_t smem = std::max(fin32_smem_bytes(nt), (size_t)(a.n_h <= kNumSMs ? 120 * 1024 : 0));
+            if (!attr_set)   // once per thread (the placement-hint size is fixed)
+                attr_set = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                (int)std::max(smem, (size_t)120 * 1024)) == cudaSuccess;
+            launch_pdl(kern, dim3(a.n_h), dim3(nt), smem, st, a, n_cta, k, gamma, wmax_dev, topk_ids, topk_vals,
+                       row_max, row_sumexp, flags);
+        };
+        static thread_local bool set3 = false, set5 = false, set10 = false;
+        if (fin_nt >= 1024 && nq <= 3 * 1024) go(lmh_finalize32_kernel<3, 1024>, 1024, set3);
+        else if (nq <= 5 * kFin32Threads) go(lmh_finalize32_kernel<5, kFin32Threads>, kFin32Threads, set5);
+        else go(lmh_finalize32_kernel<10, kFin32Threads>, kFin32Threads, set10);
         return;
     }
     size_t smem = (size_t)n_cta * 2 * sizeof(int) + (size_t)n_cta * a.KP * 8;

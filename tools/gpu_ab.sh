@@ -11,5 +11,6 @@ for v in ${AB_VARIANTS:-new head par0}; do
     headB) (cd _headB && run headB) ;;
     headC) (cd _headC && run headC) ;;
     fin*) EVOSPEC_FIN_OPT=${v#fin} run $v ;;
+    nt512) EVOSPEC_FIN_NT=512 run nt512 ;;
   esac
 done
