@@ -53,6 +53,8 @@ for pf in (sys.argv[1:] or ["2"]):
         col = col[tr[:, j] > 0]
         if col.size:
             print(f"   {n:10s} min {col.min():7.1f}  med {np.median(col):7.1f}  max {col.max():7.1f}")
+    late = np.argsort(-rel[:, 7])[:8]
+    print("   latest CTAs (block: end / prod_done us):", [(int(b), round(rel[b, 7], 1), round(rel[b, 1], 1)) for b in late])
     frel = (fin[:, :7] - t0) / 1e3
     for j, n in enumerate(["fin_start", "fin_hnorm", "fin_B1", "fin_filter", "fin_runs", "fin_rescore", "fin_end"]):
         col = frel[:, j]
