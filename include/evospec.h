@@ -258,6 +258,37 @@ evospec_status evospec_merge_shards(evospec_ctx *ctx, int32_t n_h, int32_t k,
     int32_t *out_ids, float *out_vals, float *out_lse, float *out_probs,
     void *stream);
 
+/* ---- N2: lossless verification of a draft chain ----------- */
+
+/* Verifies g draft proposals against the target, the rejection criterion
+ * alpha of P:42 (Leviathan et al.) in the chain form of SPEC S:380-385 (verify
+ * phase of alg. P:366-367; greedy T = 0 is the paper's setting).
+ * Position j (0 <= j <= g): p_j(v) = exp(z_j[v] inv_temp - m_j) / s_j over the
+ * FULL vocabulary [0, V), fp64; q_j = draft_probs[j][i] at subset_ids[i] and
+ * exactly 0 outside the subset.
+ *   greedy != 0: accept x_j while x_j == argmax p_j (ties: lower id); on a
+ *     mismatch emit argmax p_j and stop; all accepted: the bonus argmax p_g.
+ *     subset_ids, draft_probs, u, w may be NULL.
+ *   greedy == 0: accept x_j iff u[j] < min(1, p_j(x_j) / q_j(x_j)); on the
+ *     first rejection emit the draw from normalize(max(0, p_j - q_j)) with w[j]
+ *     and stop; all accepted: the bonus drawn from p_g with w[g]. A draw with
+ *     w in [0, 1) is the smallest v (id order) whose running sum of the
+ *     weights exceeds w * (their total); if the residual mass is 0 (rounding
+ *     only) the draw is from p_j.
+ * Arguments (device memory, caller-owned): target_logits [g+1, V] fp32 row-
+ * major; proposals [g] int32 (each must have q_j > 0: otherwise the position
+ * is rejected with token -1 and EVOSPEC_FLAG_BAD_IDS is raised); subset_ids
+ * [n_subset] sorted ascending unique; draft_probs [g, n_subset] fp32; u [g]
+ * and w [g+1] fp64 uniforms in [0, 1) drawn by the caller (g = 0: only w).
+ * Outputs: tokens [g+1] int32 = the accepted proposals, then the corrected or
+ * bonus token, then -1 pads; n_accepted [1] int32 (the round emits
+ * n_accepted + 1 tokens). 0 <= g <= 63. Async on `stream`; two
+ * kernel launches. EVOSPEC_EINPUT on null / out-of-range host arguments. */
+evospec_status evospec_verify_chain(evospec_ctx *ctx, const float *target_logits, int32_t V, int32_t g,
+    const int32_t *proposals, const int32_t *subset_ids, int32_t n_subset, const float *draft_probs,
+    float inv_temp, int32_t greedy, const double *u, const double *w,
+    int32_t *tokens, int32_t *n_accepted, void *stream);
+
 /* ---- one draft step through the whole path -------------------------------- */
 
 /* Per-step I/O for evospec_draft_step. `host_io` = 1: q, H, seeds, ctx and

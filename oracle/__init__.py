@@ -241,3 +241,31 @@ def subset_logits_topk_ragged(W, H, h_offsets, static_ids, dyn_ids, dyn_offsets,
         S_b = np.union1d(static_ids, dyn_ids[int(dyn_offsets[b]):int(dyn_offsets[b + 1])]).astype(np.int32)
         parts.append(subset_logits_topk(W, H[h0:h1], S_b, k, inv_temp=inv_temp))
     return {key: np.concatenate([p[key] for p in parts]) for key in ("ids", "vals", "m", "s", "lse", "probs")}
+
+
+def verify_chain(z, x, S, qS, *, inv_temp: float = 1.0, greedy: bool, u=None, w=None):
+    """N2: lossless verification of a draft chain (eo_verify_chain). z float32 [g+1, V] target
+    logits, x int32 [g] proposals, S sorted int32 subset, qS float32 [g, n_S] draft
+    probabilities on S (None in greedy mode), u [g] / w [g+1] uniforms (float64).
+    Returns (tokens int32[n_acc + 1], n_acc)."""
+    z = np.ascontiguousarray(z, dtype=np.float32)
+    g1, V = z.shape
+    g = g1 - 1
+    x = _i32(np.asarray(x if x is not None else [], dtype=np.int32).reshape(-1))
+    S = _i32(np.asarray(S if S is not None else [], dtype=np.int32).reshape(-1))
+    qS = None if qS is None else np.ascontiguousarray(qS, dtype=np.float32)
+    u = None if u is None else np.ascontiguousarray(u, dtype=np.float64)
+    w = None if w is None else np.ascontiguousarray(w, dtype=np.float64)
+    tokens = np.full(g + 1, -1, np.int32)
+    n_acc = np.zeros(1, np.int32)
+    f = _L().eo_verify_chain
+    f.restype = C.c_int
+    f.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_double,
+                  C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+    rc = f(_p(z), V, g, _p(x), _p(S), int(S.size), _p(qS), float(inv_temp), int(bool(greedy)), _p(u), _p(w),
+           _p(tokens), _p(n_acc))
+    if rc == 3:
+        raise ValueError("oracle verify_chain: a proposal has draft probability 0 (S:383)")
+    _check(rc, "verify_chain")
+    n = int(n_acc[0])
+    return tokens[:n + 1].copy(), n

@@ -349,3 +349,117 @@ int eo_merge(int R, int n_h, int k, const int32_t *ids, const double *vals,
     free(keys);
     return EO_OK;
 }
+
+/* ------------------------------------------------------------------ */
+/* N2: lossless verification of a draft chain against  */
+/* the target, the rejection criterion alpha of P:42 (Leviathan et    */
+/* al.), verify phase of alg. P:366-367, chain form and rule of SPEC  */
+/* S:380-385; greedy decoding (T = 0) is the paper's setting.   */
+/*                                                                    */
+/* Position j (0 <= j <= g): p_j(v) = exp(z_j[v] it - m_j) / s_j over  */
+/* the FULL vocabulary [0, V) (it = inv_temp, m_j = max, s_j = sum),   */
+/* fp64. The draft's restricted distribution q_j is qS[j][i] at S[i]   */
+/* (S sorted, unique) and exactly 0 outside S.                 */
+/* Greedy: accept x_j while x_j == argmax p_j (ties: lower id); on a   */
+/*   mismatch emit argmax p_j and stop; all g accepted: emit argmax   */
+/*   p_g (the bonus token).                                            */
+/* Sampling: accept x_j iff u_j < min(1, p_j(x_j) / q_j(x_j)); on the  */
+/*   first rejection emit the token drawn from normalize(max(0, p_j -  */
+/*   q_j)) with w_j, stop; all accepted: the bonus drawn from p_g with */
+/*   w_g. Draw from weights r with w in [0, 1): the smallest v (id     */
+/*   order) whose running sum r(0) + ... + r(v) exceeds w * sum_v r(v). */
+/*   (Reading V1: if the residual mass is 0 -- possible only through   */
+/*   rounding, since p_j(x) < q_j(x) forces mass elsewhere -- the draw */
+/*   is from p_j instead.)                                             */
+/* The uniforms u, w are inputs (drawn by the caller).                 */
+/* Out: tokens[0 .. n_acc] = the accepted proposals then the emitted   */
+/* token; *n_acc_out = n_acc. Returns 3 if a proposal has q = 0        */
+/* (proposals must come from q's support), 2 on bad input.      */
+/* ------------------------------------------------------------------ */
+static int eo_find_sorted(const int32_t *S, int n, int32_t v) {
+    int lo = 0, hi = n - 1;
+    while (lo <= hi) {
+        int mid = lo + (hi - lo) / 2;
+        if (S[mid] == v) return mid;
+        if (S[mid] < v) lo = mid + 1; else hi = mid - 1;
+    }
+    return -1;
+}
+
+/* the target distribution of row zj: m, s in fp64 (sequential over v) */
+static void eo_target_stats(const float *zj, int V, double it, double *m, double *s, int32_t *amax) {
+    double M = -INFINITY;
+    int32_t a = -1;
+    for (int v = 0; v < V; ++v) {
+        double x = (double)zj[v] * it;
+        if (x > M) { M = x; a = v; }          /* strict: ties keep the lower id */
+    }
+    double sum = 0.0;
+    for (int v = 0; v < V; ++v) sum += exp((double)zj[v] * it - M);
+    *m = M; *s = sum; *amax = a;
+}
+
+/* draw from r(v) = max(0, p(v) - q(v)) (q from qj on S, 0 elsewhere; qj == NULL: q = 0) */
+static int32_t eo_draw(const float *zj, int V, double it, double m, double s, const int32_t *S, int n_S,
+                       const float *qj, double w) {
+    double tot = 0.0;
+    int i = 0;
+    for (int v = 0; v < V; ++v) {
+        double q = 0.0;
+        while (qj && i < n_S && S[i] < v) ++i;
+        if (qj && i < n_S && S[i] == v) q = (double)qj[i];
+        double r = exp((double)zj[v] * it - m) / s - q;
+        if (r > 0.0) tot += r;
+    }
+    if (!(tot > 0.0)) return eo_draw(zj, V, it, m, s, S, n_S, NULL, w);   /* reading V1 */
+    double target = w * tot, run = 0.0;
+    int32_t last = -1;
+    i = 0;
+    for (int v = 0; v < V; ++v) {
+        double q = 0.0;
+        while (qj && i < n_S && S[i] < v) ++i;
+        if (qj && i < n_S && S[i] == v) q = (double)qj[i];
+        double r = exp((double)zj[v] * it - m) / s - q;
+        if (r > 0.0) {
+            run += r;
+            last = v;
+            if (run > target) return v;
+        }
+    }
+    return last;   /* w * tot at the very top of the rounding band */
+}
+
+int eo_verify_chain(const float *z, int V, int g, const int32_t *x, const int32_t *S, int n_S,
+                    const float *qS, double inv_temp, int greedy, const double *u, const double *w,
+                    int32_t *tokens, int32_t *n_acc_out) {
+    if (!z || V < 1 || g < 0 || (g > 0 && !x) || !tokens || !n_acc_out || !(inv_temp > 0.0)) return EO_EINPUT;
+    if (!greedy && (!u || !w || (g > 0 && (!S || !qS || n_S < 1)))) return EO_EINPUT;
+    int n_acc = 0;
+    for (int j = 0; j <= g; ++j) {
+        const float *zj = z + (int64_t)j * V;
+        double m, s;
+        int32_t amax;
+        eo_target_stats(zj, V, inv_temp, &m, &s, &amax);
+        if (j == g) {   /* every proposal accepted: the bonus token */
+            tokens[j] = greedy ? amax : eo_draw(zj, V, inv_temp, m, s, S, n_S, NULL, w[j]);
+            break;
+        }
+        if (x[j] < 0 || x[j] >= V) return EO_EINPUT;
+        if (greedy) {
+            if (x[j] == amax) { tokens[j] = x[j]; ++n_acc; continue; }
+            tokens[j] = amax;
+            break;
+        }
+        int i = eo_find_sorted(S, n_S, x[j]);
+        const float *qj = qS + (int64_t)j * n_S;
+        if (i < 0 || !(qj[i] > 0.0f)) return 3;
+        double p = exp((double)zj[x[j]] * inv_temp - m) / s;
+        double a = p / (double)qj[i];
+        if (a > 1.0) a = 1.0;
+        if (u[j] < a) { tokens[j] = x[j]; ++n_acc; continue; }
+        tokens[j] = eo_draw(zj, V, inv_temp, m, s, S, n_S, qj, w[j]);
+        break;
+    }
+    *n_acc_out = n_acc;
+    return EO_OK;
+}

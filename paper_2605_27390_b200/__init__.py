@@ -28,6 +28,7 @@ EXPORTED = [
     "evospec_last_semantic", "evospec_subset_logits_topk", "evospec_merge_shards",
     "evospec_draft_step", "evospec_set_timing", "evospec_read_stats", "evospec_read_trace",
     "evospec_build_subset_batched", "evospec_subset_logits_topk_ragged", "evospec_subset_logits_topk_merged",
+    "evospec_verify_chain",
 ]
 
 STAGES = ["scan", "select", "union", "lmh", "finalize", "merge", "copy"]
@@ -98,6 +99,7 @@ def lib() -> C.CDLL:
             "evospec_subset_logits_topk": ([vp, vp, i64, vp, i32, vp, vp, i32, i32, C.c_float,
                                             vp, vp, vp, vp, vp, vp], i32),
             "evospec_merge_shards": ([vp, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp], i32),
+            "evospec_verify_chain": ([vp, vp, i32, i32, vp, vp, i32, vp, C.c_float, i32, vp, vp, vp, vp, vp], i32),
             "evospec_draft_step": ([vp, C.POINTER(StepIO), vp], i32),
             "evospec_set_timing": ([vp, C.c_int], i32),
             "evospec_read_stats": ([vp, C.POINTER(Stats)], i32),
@@ -337,6 +339,24 @@ class Context:
         _check(lib().evospec_merge_shards(self._h, n_h, k, _ptr(ids), _ptr(vals), _ptr(m), _ptr(s),
                                           _ptr(oi), _ptr(ov), _ptr(ol), _ptr(op), _stream(stream)))
         return oi, ov, ol, op
+
+    # ---- N2: verification of a draft chain
+    def verify_chain(self, z, proposals, *, subset=None, draft_probs=None, inv_temp: float = 1.0,
+                     greedy: bool, u=None, w=None, out=None, stream=None):
+        """Lossless verification (evospec_verify_chain). z: fp32 [g+1, V] target logits,
+        proposals int32 [g], subset int32 sorted [n_S], draft_probs fp32 [g, n_S], u / w fp64
+        [g] / [g+1] uniforms (device tensors). Returns (tokens int32 [g+1], n_accepted int32 [1])."""
+        import torch
+        g = z.shape[0] - 1
+        if out is None:
+            out = (torch.empty(g + 1, dtype=torch.int32, device=z.device),
+                   torch.empty(1, dtype=torch.int32, device=z.device))
+        tok, nacc = out
+        n_S = 0 if subset is None else int(subset.numel())
+        _check(lib().evospec_verify_chain(self._h, _ptr(z), int(z.shape[1]), g, _ptr(proposals), _ptr(subset), n_S,
+                                          _ptr(draft_probs), float(inv_temp), int(bool(greedy)), _ptr(u), _ptr(w),
+                                          _ptr(tok), _ptr(nacc), _stream(stream)))
+        return tok, nacc
 
     # ---- whole step
     def draft_step(self, *, E, W_local, static_ids, csr_row_ptr, csr_col, q, H, seeds, k: int,

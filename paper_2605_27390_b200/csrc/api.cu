@@ -104,6 +104,8 @@ struct evospec_ctx {
     bool hist_dirty = false;      // a build stopped between its scan and its union: clear first
     uint32_t* ubits = nullptr;    // [V/32] union bitmap handed to the emit kernel
     unsigned long long* fin_ctr = nullptr;   // LM-head fused finalisation arrival counter
+    int32_t* ver_acc = nullptr;   // [kMaxChain + 1] verification: per-position accept flags
+    int32_t* ver_tok = nullptr;   // [kMaxChain + 1] verification: per-position emitted token
     uint32_t* hist = nullptr;     // [12][4096] further select passes
     int cand_cap = 0;             // candidate superset capacity (union smem)
     int* cand_count = nullptr;
@@ -227,7 +229,7 @@ evospec_status evospec_destroy(evospec_ctx* ctx) {
                     ctx->flags, ctx->wmax, ctx->g_ids, ctx->g_vals, ctx->g_m, ctx->g_s, ctx->st_q, ctx->st_H,
                     ctx->st_seeds, ctx->st_ctx, ctx->st_S, ctx->st_nS, ctx->st_local, ctx->st_nlocal,
                     ctx->st_tids, ctx->st_tvals, ctx->st_m, ctx->st_s, ctx->st_oids, ctx->st_ovals,
-                    ctx->st_lse, ctx->st_probs, ctx->ubits, ctx->fin_ctr, ctx->rg_ids, ctx->rg_vals, ctx->rg_m, ctx->rg_s, ctx->rg_seg, ctx->rg_segcta};
+                    ctx->st_lse, ctx->st_probs, ctx->ubits, ctx->fin_ctr, ctx->rg_ids, ctx->rg_vals, ctx->rg_m, ctx->rg_s, ctx->rg_seg, ctx->rg_segcta, ctx->ver_acc, ctx->ver_tok};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (ctx->comm && nccl().loaded) nccl().CommDestroy(ctx->comm);
@@ -280,6 +282,7 @@ evospec_status evospec_create(evospec_ctx** out, const evospec_config* cfg, int 
     const size_t cap = (size_t)x->cand_cap;
     A(dalloc(&x->s64, V)); A(dalloc(&x->key32, V)); A(dalloc(&x->hist12, kHistBins)); A(dalloc(&x->ubits, (V + 31) / 32)); A(dalloc(&x->fin_ctr, 1)); A(cudaMemset(x->fin_ctr, 0, 8)); A(cudaMemset(x->hist12, 0, kHistBins * sizeof(uint32_t)));
     A(dalloc(&x->hist, 12 * kHistBins));
+    A(dalloc(&x->ver_acc, kMaxChain + 1)); A(dalloc(&x->ver_tok, kMaxChain + 1));
     A(dalloc(&x->cand_count, 4)); A(dalloc(&x->cand_s, cap)); A(dalloc(&x->cand_id, cap));
     A(dalloc(&x->loc_count, 4)); A(dalloc(&x->loc_s, sem)); A(dalloc(&x->loc_id, sem));
     A(dalloc(&x->gat_s, sem * R)); A(dalloc(&x->gat_id, sem * R));
@@ -774,6 +777,24 @@ evospec_status evospec_merge_shards(evospec_ctx* ctx, int32_t n_h, int32_t k, co
     launch_merge(R, n_h, k, gi, gv, gm, gs, out_ids, out_vals, out_lse, out_probs, st);
     ctx->launches += 1;
     LAUNCH_CHECK("merge");
+    return EVOSPEC_OK;
+}
+
+evospec_status evospec_verify_chain(evospec_ctx* ctx, const float* target_logits, int32_t V, int32_t g,
+                                    const int32_t* proposals, const int32_t* subset_ids, int32_t n_subset,
+                                    const float* draft_probs, float inv_temp, int32_t greedy, const double* u,
+                                    const double* w, int32_t* tokens, int32_t* n_accepted, void* stream) {
+    if (!ctx || !target_logits || !tokens || !n_accepted || (g > 0 && !proposals))
+        return fail(EVOSPEC_EINPUT, "verify_chain: null argument");
+    if (V < 1 || g < 0 || g > kMaxChain) return fail(EVOSPEC_EINPUT, "verify_chain: V=%d / g=%d out of range", V, g);
+    if (!(inv_temp > 0.0f) || !std::isfinite(inv_temp)) return fail(EVOSPEC_EINPUT, "verify_chain: inv_temp must be > 0");
+    if (!greedy && (!w || (g > 0 && (!u || !subset_ids || !draft_probs || n_subset < 1))))
+        return fail(EVOSPEC_EINPUT, "verify_chain: sampling mode needs the subset, draft_probs, u and w");
+    cudaStream_t st = (cudaStream_t)stream;
+    launch_verify(target_logits, V, g, proposals, subset_ids, n_subset, draft_probs, (double)inv_temp, greedy ? 1 : 0,
+                  u, w, ctx->ver_acc, ctx->ver_tok, tokens, n_accepted, ctx->flags, st);
+    ctx->launches += 2;
+    LAUNCH_CHECK("verify_chain");
     return EVOSPEC_OK;
 }
 

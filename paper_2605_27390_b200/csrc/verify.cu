@@ -1,0 +1,266 @@
+// verify.cu -- N2: lossless verification of a draft chain
+// against the target, the rejection criterion alpha of P:42 (Leviathan et
+// al.), the verify phase of alg. P:366-367, in the chain form and with the
+// rule of SPEC S:380-385; greedy decoding (T = 0) is the paper's setting.
+//
+// Position j (0 <= j <= g) has the target distribution over the FULL
+// vocabulary p_j(v) = exp(z_j[v] it - m_j) / s_j; the draft's restricted
+// distribution q_j is draft_probs[j][i] at subset[i] and exactly 0 outside the
+// subset (S:407 -- the residual max(0, p - q) re-covers the excluded tokens,
+// which is what makes the restricted draft lossless).
+//   greedy:   accept x_j while x_j == argmax p_j (ties: lower id); on a
+//             mismatch emit argmax p_j; all accepted: the bonus argmax p_g;
+//   sampling: accept x_j iff u_j < min(1, p_j(x_j) / q_j(x_j)); on the first
+//             rejection emit the draw from normalize(max(0, p_j - q_j)) with
+//             w_j; all accepted: the bonus drawn from p_g with w_g. A draw is
+//             the smallest v (id order) whose running sum of the weights
+//             exceeds w * (their total).
+//
+// Kernel 1 (verify_pos_kernel): one CTA per position, every position at once
+// (the first rejection is not known up front): max / argmax and the fp64 sum
+// over V; the acceptance test; for a rejected position (sampling) or the bonus
+// position the draw -- per-thread residual mass over a contiguous id range
+// (the q lookup walks the sorted subset from a binary-searched start), a block
+// scan of the masses, and the thread whose range holds w * total re-walks it.
+// The fp64 sums run in a different order than the oracle's sequential ones; a
+// different token needs w * total within ~1e-15 relative of a CDF step.
+// Kernel 2 (verify_decide_kernel, one warp): the accepted prefix and the
+// emitted token. HBM-bound: (g + 1) rows of V fp32 logits, read from HBM once
+// (the further passes hit L2).
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace es {
+
+constexpr int kVerThreads = 1024;
+constexpr int kVerWarps = kVerThreads / 32;
+
+struct VerSmem {
+    double red_d[kVerWarps];
+    double scan_d[kVerWarps + 1];
+    float red_v[kVerWarps];
+    int red_i[kVerWarps];
+    double s_M, s_sum, s_tot;
+    int s_arg, s_pick;
+};
+
+ES_DEV double warp_sum_dd(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// block sum of a double (all threads get it)
+ES_DEV double block_sum_d(double v, VerSmem& sm) {
+    const int lane = lane_id(), wid = warp_id();
+    v = warp_sum_dd(v);
+    if (lane == 0) sm.red_d[wid] = v;
+    __syncthreads();
+    if (wid == 0) {
+        double t = lane < kVerWarps ? sm.red_d[lane] : 0.0;
+        t = warp_sum_dd(t);
+        if (lane == 0) sm.s_tot = t;
+    }
+    __syncthreads();
+    const double r = sm.s_tot;
+    __syncthreads();
+    return r;
+}
+
+// exclusive block scan of a double (thread order)
+ES_DEV double block_excl_scan_d(double v, VerSmem& sm) {
+    const int lane = lane_id(), wid = warp_id();
+    double inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const double t = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += t;
+    }
+    if (lane == 31) sm.scan_d[wid] = inc;
+    __syncthreads();
+    if (wid == 0) {
+        const double w = lane < kVerWarps ? sm.scan_d[lane] : 0.0;
+        double wi = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const double t = __shfl_up_sync(0xffffffffu, wi, o);
+            if (lane >= o) wi += t;
+        }
+        if (lane < kVerWarps) sm.scan_d[lane] = wi - w;
+    }
+    __syncthreads();
+    const double r = sm.scan_d[wid] + inc - v;
+    __syncthreads();
+    return r;
+}
+
+// first index i of the sorted S with S[i] >= v
+ES_DEV int lower_bound_i32(const int32_t* S, int n, int v) {
+    int lo = 0, hi = n;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (__ldg(&S[mid]) < v) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
+// r(v) = max(0, p(v) - q(v)) over [v0, v1), q from qj on S (qj == nullptr: q = 0)
+struct Resid {
+    const float* zj; double it, M, s;
+    const int32_t* S; int n_S; const float* qj;
+    ES_DEV double q_at(int v, int& i) const {
+        if (!qj) return 0.0;
+        while (i < n_S && __ldg(&S[i]) < v) ++i;
+        return (i < n_S && __ldg(&S[i]) == v) ? (double)__ldg(&qj[i]) : 0.0;
+    }
+    ES_DEV double r_at(int v, int& i) const {
+        const double p = exp((double)__ldg(&zj[v]) * it - M) / s;
+        const double r = p - q_at(v, i);
+        return r > 0.0 ? r : 0.0;
+    }
+};
+
+// the draw from weights r over [0, V) with w in [0, 1); every thread of the block calls it
+ES_DEV int block_draw(const Resid& R, int V, double w, VerSmem& sm) {
+    const int tid = threadIdx.x;
+    const int v0 = (int)((long long)V * tid / kVerThreads), v1 = (int)((long long)V * (tid + 1) / kVerThreads);
+    const int i0 = R.qj ? lower_bound_i32(R.S, R.n_S, v0) : 0;
+    double loc = 0.0;
+    int last = -1;
+    {
+        int i = i0;
+        for (int v = v0; v < v1; ++v) {
+            const double r = R.r_at(v, i);
+            if (r > 0.0) { loc += r; last = v; }
+        }
+    }
+    const double tot = block_sum_d(loc, sm);
+    if (!(tot > 0.0)) return -2;   // no residual mass (rounding only): the caller draws from p
+    const double target = w * tot;
+    const double pre = block_excl_scan_d(loc, sm);
+    if (tid == 0) sm.s_pick = 0x7fffffff;
+    __syncthreads();
+    if (loc > 0.0 && pre <= target && target < pre + loc) atomicMin(&sm.s_pick, tid);
+    // the last id with mass, for a target in the rounding band above the total
+    __syncthreads();
+    const bool none = sm.s_pick == 0x7fffffff;
+    __syncthreads();
+    if (none) {
+        if (tid == 0) sm.s_arg = -1;
+        __syncthreads();
+        if (last >= 0) atomicMax(&sm.s_arg, last);
+        __syncthreads();
+        return sm.s_arg;
+    }
+    if (tid == sm.s_pick) {
+        double run = pre;
+        int i = i0, pick = last;
+        for (int v = v0; v < v1; ++v) {
+            const double r = R.r_at(v, i);
+            if (r > 0.0) {
+                run += r;
+                if (run > target) { pick = v; break; }
+            }
+        }
+        sm.s_arg = pick;
+    }
+    __syncthreads();
+    const int res = sm.s_arg;
+    __syncthreads();
+    return res;
+}
+
+__global__ void __launch_bounds__(kVerThreads)
+verify_pos_kernel(const float* __restrict__ z, int V, int g, const int32_t* __restrict__ x,
+                  const int32_t* __restrict__ S, int n_S, const float* __restrict__ qS, double it, int greedy,
+                  const double* __restrict__ u, const double* __restrict__ w, int32_t* __restrict__ pos_acc,
+                  int32_t* __restrict__ pos_tok, int* flags) {
+    __shared__ VerSmem sm;
+    pdl_trigger();
+    pdl_wait();
+    const int j = blockIdx.x, tid = threadIdx.x, lane = lane_id(), wid = warp_id();
+    const float* zj = z + (size_t)j * V;
+    const int v0 = (int)((long long)V * tid / kVerThreads), v1 = (int)((long long)V * (tid + 1) / kVerThreads);
+    // 1. maximum and argmax (value desc, id asc), in fp32 -- the fp64 product of an
+    //    fp32 logit and it orders exactly as the logit itself (it > 0)
+    float bv = -INFINITY;
+    int bi = 0x7fffffff;
+    for (int v = v0; v < v1; ++v) {
+        const float zz = __ldg(&zj[v]);
+        if (zz > bv) { bv = zz; bi = v; }
+    }
+    warp_argbest(bv, bi);
+    if (lane == 0) { sm.red_v[wid] = bv; sm.red_i[wid] = bi; }
+    __syncthreads();
+    if (wid == 0) {
+        float v = lane < kVerWarps ? sm.red_v[lane] : -INFINITY;
+        int i = lane < kVerWarps ? sm.red_i[lane] : 0x7fffffff;
+        warp_argbest(v, i);
+        if (lane == 0) { sm.s_M = (double)v * it; sm.s_arg = i; }
+    }
+    __syncthreads();
+    const double M = sm.s_M;
+    const int amax = sm.s_arg;
+    __syncthreads();
+    if (greedy) {
+        if (tid == 0) {
+            pos_tok[j] = amax;
+            pos_acc[j] = j < g ? (int)(__ldg(&x[j]) == amax) : 0;
+        }
+        return;
+    }
+    // 2. s = sum_v exp(z it - M), fp64
+    double loc = 0.0;
+    for (int v = v0; v < v1; ++v) loc += exp((double)__ldg(&zj[v]) * it - M);
+    const double s = block_sum_d(loc, sm);
+    // 3. acceptance (j < g) or the bonus draw (j == g)
+    bool acc = false;
+    const float* qj = nullptr;
+    if (j < g) {
+        const int xj = __ldg(&x[j]);
+        qj = qS + (size_t)j * n_S;
+        const int i = (xj >= 0 && xj < V) ? lower_bound_i32(S, n_S, xj) : n_S;
+        const bool in = i < n_S && __ldg(&S[i]) == xj && __ldg(&qj[i]) > 0.0f;
+        if (!in) {
+            if (tid == 0) { atomicOr(flags, kFlagBadIds); pos_acc[j] = 0; pos_tok[j] = -1; }
+            return;
+        }
+        double a = exp((double)__ldg(&zj[xj]) * it - M) / s / (double)__ldg(&qj[i]);
+        if (a > 1.0) a = 1.0;
+        acc = __ldg(&u[j]) < a;
+        if (acc) {
+            if (tid == 0) { pos_acc[j] = 1; pos_tok[j] = xj; }
+            return;
+        }
+    }
+    const Resid R{zj, it, M, s, S, n_S, j < g ? qj : nullptr};
+    int tok = block_draw(R, V, __ldg(&w[j]), sm);
+    if (tok == -2) {   // no residual mass: draw from p_j
+        const Resid P{zj, it, M, s, S, n_S, nullptr};
+        tok = block_draw(P, V, __ldg(&w[j]), sm);
+    }
+    if (tid == 0) { pos_acc[j] = 0; pos_tok[j] = tok; }
+}
+
+__global__ void verify_decide_kernel(int g, const int32_t* __restrict__ x, const int32_t* __restrict__ pos_acc,
+                                     const int32_t* __restrict__ pos_tok, int32_t* __restrict__ tokens,
+                                     int32_t* __restrict__ n_acc_out) {
+    pdl_wait();
+    if (threadIdx.x != 0) return;
+    int n = 0;
+    while (n < g && pos_acc[n]) { tokens[n] = x[n]; ++n; }
+    tokens[n] = pos_tok[n];
+    for (int j = n + 1; j <= g; ++j) tokens[j] = -1;
+    *n_acc_out = n;
+}
+
+void launch_verify(const float* z, int V, int g, const int32_t* x, const int32_t* S, int n_S, const float* qS,
+                   double it, int greedy, const double* u, const double* w, int32_t* pos_acc, int32_t* pos_tok,
+                   int32_t* tokens, int32_t* n_acc_out, int* flags, cudaStream_t st) {
+    launch_pdl(verify_pos_kernel, dim3(g + 1), dim3(kVerThreads), 0, st, z, V, g, x, S, n_S, qS, it, greedy, u, w,
+               pos_acc, pos_tok, flags);
+    launch_pdl(verify_decide_kernel, dim3(1), dim3(32), 0, st, g, x, (const int32_t*)pos_acc,
+               (const int32_t*)pos_tok, tokens, n_acc_out);
+}
+
+}  // namespace es

@@ -176,3 +176,25 @@ CONFIGS = {
                     n_sem=8192, n_dyn=4096, n_seed=10, n_graph_sem_seeds=10,
                     per_seed=8, n_h=60, k=10, avg_deg=32.0, w_std=0.02, h_std=1.0),
 }
+
+
+def verify_problem(seed: int, *, V: int, g: int, n_S: int, inv_temp: float = 1.0) -> dict:
+    """Inputs of the N2 verification step, seeded: target logits z
+    [g+1, V] fp32 (N(0, 1.28^2): the llama head's logit scale, §8(d)), a sorted
+    random subset S of n_S ids, the draft's restricted distribution q on S
+    ([g, n_S] fp32; a draft whose logits are the target's on S plus N(0, 0.5^2)
+    noise, normalised on S -- an input, not the method's arithmetic), proposals
+    x_j drawn from q_j, uniforms u [g] and w [g+1] (fp64, [0, 1))."""
+    rng = np.random.default_rng(seed)
+    z = (rng.normal(size=(g + 1, V)) * 1.28).astype(np.float32)
+    n_S = min(n_S, V)
+    S = np.sort(rng.choice(V, n_S, replace=False)).astype(np.int32)
+    dl = z[:g, S].astype(np.float64) * inv_temp + rng.normal(size=(g, n_S)) * 0.5
+    q = np.exp(dl - dl.max(axis=1, keepdims=True))
+    q /= q.sum(axis=1, keepdims=True)
+    q = q.astype(np.float32)
+    x = np.array([S[rng.choice(n_S, p=q[j].astype(np.float64) / q[j].astype(np.float64).sum())]
+                  for j in range(g)], np.int32)
+    u = rng.random(g)
+    w = rng.random(g + 1)
+    return dict(z=z, S=S, q=q, x=x, u=u, w=w, V=V, g=g, inv_temp=inv_temp)

@@ -454,3 +454,131 @@ def test_ragged_equals_merge_of_static_and_dynamic_parts(oracle_mod):
         np.testing.assert_array_equal(out["ids"][rows], mg["ids"])
         np.testing.assert_allclose(out["lse"][rows], mg["lse"], rtol=1e-12)
         np.testing.assert_allclose(out["probs"][rows], mg["probs"], atol=1e-12)
+
+
+# ---------------------------------------------------------------- N2 verification
+# Pins for oracle.verify_chain (eo_verify_chain): the SPEC worked example
+# (S:385), the losslessness theorem (the first emitted token is
+# distributed exactly as the target, for any draft q supported on V_t) and
+# greedy equivalence. The acceptance probability and the draw's CDF are
+# recovered from the oracle as a black box by bisection on the uniforms (its
+# decisions are monotone in u and w), never from its formulas.
+
+def _bisect(pred, lo=0.0, hi=1.0, it=60):
+    """largest x in [lo, hi) with pred(x) true, pred monotone (true then false)"""
+    for _ in range(it):
+        mid = 0.5 * (lo + hi)
+        if pred(mid):
+            lo = mid
+        else:
+            hi = mid
+    return lo
+
+
+def _draw_intervals(fn, V):
+    """{token: length of the set of w in [0, 1) that emits it}, fn(w) monotone in w"""
+    out = {}
+    w0 = 0.0
+    while w0 < 1.0:
+        t = fn(w0)
+        w1 = _bisect(lambda w: fn(w) == t, w0, 1.0)
+        if fn(w1) != t:       # numeric guard
+            w1 = w0
+        nxt = w1 + 1e-15
+        out[t] = out.get(t, 0.0) + (min(1.0, nxt) - w0)
+        w0 = nxt
+    return out
+
+
+def test_verify_spec_worked_example():
+    """p = (0.6, 0.4), q = (0.5, 0.5), proposal 1 -> accept prob 0.8; on a
+    rejection the residual is the point mass on token 0."""
+    import oracle
+    z = np.log(np.array([[0.6, 0.4], [0.5, 0.5]], np.float32))
+    q = np.array([[0.5, 0.5]], np.float32)
+    acc = lambda u: oracle.verify_chain(z, [1], [0, 1], q, greedy=False, u=[u], w=[0.5, 0.5])[1] == 1
+    assert abs(_bisect(acc) - 0.8) < 1e-6
+    for w in (0.0, 0.3, 0.999):
+        tok, n = oracle.verify_chain(z, [1], [0, 1], q, greedy=False, u=[0.95], w=[w, 0.5])
+        assert n == 0 and tok.tolist() == [0]
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_verify_lossless_first_token(seed):
+    """Losslessness: with x ~ q_0 (q supported on a subset S of V),
+    u, w uniform, the first emitted token has the target law p_0 exactly:
+    sum_x q(x) [a(x) 1{v = x} + (1 - a(x)) P(draw = v | x)] = p(v), within 1e-9.
+    a(x) and the draw's law come from the oracle by bisection on u and w."""
+    import oracle
+    rng = np.random.default_rng(100 + seed)
+    V = 7
+    S = np.sort(rng.choice(V, 4, replace=False)).astype(np.int32)
+    q = rng.dirichlet(np.ones(S.size)).astype(np.float32)
+    q = (q / q.astype(np.float64).sum()).astype(np.float32)
+    z = rng.normal(size=(2, V)).astype(np.float32)
+    p = np.exp(z[0].astype(np.float64) - z[0].max())
+    p /= p.sum()
+    law = np.zeros(V)
+    qd = q.astype(np.float64)
+    qd /= qd.sum()
+    for i, x in enumerate(S):
+        run = lambda u, w: oracle.verify_chain(z, [x], S, q[None, :], greedy=False, u=[u], w=[w, 0.5])
+        a = _bisect(lambda u: run(u, 0.5)[1] == 1)
+        law[x] += qd[i] * a
+        for t, length in _draw_intervals(lambda w: int(run(0.999999999, w)[0][0]) if a < 0.999999999 else x, V).items():
+            law[t] += qd[i] * (1.0 - a) * length
+    # q sums to 1 only up to fp32 rounding: compare against p with that slack
+    assert np.abs(law - p).max() < 1e-6, (law, p)
+    # where q(x) > p(x) the proposal is accepted with probability exactly p/q
+    i = int(np.argmax(qd / p[S]))
+    x = S[i]
+    a = _bisect(lambda u: oracle.verify_chain(z, [x], S, q[None, :], greedy=False, u=[u], w=[0.5, 0.5])[1] == 1)
+    assert abs(a - min(1.0, p[x] / float(q[i]))) < 1e-9
+
+
+def test_verify_bonus_draw_is_target_law():
+    """All proposals accepted (u = 0): the bonus token is drawn from p_g -- the
+    w-intervals of the draw have the lengths p_g(v) (inverse CDF in id order)."""
+    import oracle
+    rng = np.random.default_rng(7)
+    V = 9
+    z = rng.normal(size=(2, V)).astype(np.float32)
+    S = np.arange(V, dtype=np.int32)
+    q = np.full((1, V), 1.0 / V, np.float32)
+    x = 3
+    fn = lambda w: int(oracle.verify_chain(z, [x], S, q, greedy=False, u=[0.0], w=[0.5, w])[0][1])
+    law = _draw_intervals(fn, V)
+    p = np.exp(z[1].astype(np.float64) - z[1].max())
+    p /= p.sum()
+    got = np.array([law.get(v, 0.0) for v in range(V)])
+    assert np.abs(got - p).max() < 1e-9
+    # id order: the emitted token is non-decreasing in w
+    toks = [fn(w) for w in np.linspace(0, 0.999, 50)]
+    assert toks == sorted(toks)
+
+
+def test_verify_greedy_equivalence_and_ties():
+    """T = 0 reproduces target greedy decoding token for token; ties of the
+    target maximum go to the lower id; a mismatch at j stops with argmax p_j."""
+    import oracle
+    rng = np.random.default_rng(3)
+    g, V = 5, 50
+    z = rng.normal(size=(g + 1, V)).astype(np.float32)
+    z[2, 11] = z[2, 40] = z[2].max() + 1.0          # a tie: 11 wins
+    am = np.argmax(z, axis=1)                        # numpy argmax: first (lower) index
+    assert am[2] == 11
+    tok, n = oracle.verify_chain(z, am[:g].astype(np.int32), None, None, greedy=True)
+    assert n == g and tok.tolist() == am.tolist()
+    x = am[:g].copy()
+    x[3] = (x[3] + 1) % V
+    tok, n = oracle.verify_chain(z, x.astype(np.int32), None, None, greedy=True)
+    assert n == 3 and tok.tolist() == am[:4].tolist()
+
+
+def test_verify_rejects_proposal_outside_support():
+    """a proposal with q = 0 is an invariant violation."""
+    import oracle
+    z = np.zeros((2, 4), np.float32)
+    with pytest.raises(ValueError):
+        oracle.verify_chain(z, [2], np.array([0, 1], np.int32), np.array([[0.5, 0.5]], np.float32),
+                            greedy=False, u=[0.1], w=[0.1, 0.1])
