@@ -289,7 +289,8 @@ def run_ours(args):
     if world == 1 and not args.no_extra:
         del Wd
         torch.cuda.empty_cache()
-        extra = dict(qwen_topic_segment=qwen_segment(dev, args), sharded_d8192_r1=sharded_sweep(dev, args))
+        extra = dict(qwen_topic_segment=qwen_segment(dev, args), sharded_d8192_r1=sharded_sweep(dev, args),
+                     verify_chain=verify_line(dev, args))
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -326,6 +327,8 @@ def run_ours(args):
         gpu_out = [t.cpu().numpy() for t in out_d]   # the device-timed loop's last step
         cpu, parity = cpu_baseline_line(c2, W2, H2, q2, st2, rp2, col2, s2, gpu_out=gpu_out)
         cpu["cores"] = 1
+        if extra and extra.get("verify_chain"):
+            verify_parity_cpu_leg(extra["verify_chain"])
     line = dict(metric=METRIC, value=value, unit="tokens/s", n_gpus=world, steps=args.steps, warmup=args.warmup,
                 ms_per_step=ms / args.steps, higher_is_better=True, scaling="strong", vs_baseline=None,
                 dtype="bf16", data="synthetic (seeded; random-init bf16 W ~ N(0,0.02^2), H ~ N(0,1))",
@@ -445,6 +448,53 @@ def qwen_segment(dev, args):
     ms = statistics.median([a.elapsed_time(b) for a, b in evs[2:]])
     return dict(workload="Q: V=152064 d=3584, 3 domains, segment = 1 rebuild + 64 LM-head calls (n_H=60, k=10)",
                 ms_per_segment=ms, tokens_per_s=64 * n_h / (ms * 1e-3), flags=ctx.get_flags())
+
+
+def verify_line(dev, args):
+    """N2: evospec_verify_chain on the llama vocabulary, the paper's horizon
+    g = 6, a 36,864-id restricted draft distribution; greedy (T = 0) and
+    sampling modes, L2 flushed before each call; accepted count / tokens checked against
+    the oracle in the cpu_baseline leg (verify_parity_cpu_leg)."""
+    import torch
+    import paper_2605_27390_b200 as es
+    V, g, n_S = 128256, 6, 36864
+    P = synth.verify_problem(0, V=V, g=g, n_S=n_S)
+    ctx = es.Context(V=V, d=64, w_dtype=torch.bfloat16, h_dtype=torch.bfloat16, max_subset=1, max_rows=1,
+                     max_k=1, max_sem=1)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+    z, x, S, q, u, w = t(P["z"]), t(P["x"]), t(P["S"]), t(P["q"]), t(P["u"]), t(P["w"])
+    flush = L2Flush(dev)
+    nbytes = (g + 1) * V * 4 + g * n_S * 4 + n_S * 4
+    out = {}
+    for mode, greedy in (("greedy", True), ("sampling", False)):
+        evs, res = [], None
+        for it in range(args.warmup + args.sweep_steps):
+            flush(it)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            res = ctx.verify_chain(z, x, subset=S, draft_probs=q, greedy=greedy, u=u, w=w, out=res)
+            e1.record()
+            evs.append((e0, e1))
+        torch.cuda.synchronize()
+        us = statistics.median([a.elapsed_time(b) for a, b in evs[args.warmup:]]) * 1e3
+        n = int(res[1].item())
+        out[mode] = dict(us=us, GBps=nbytes / (us * 1e-6) / 1e9, n_accepted=n,
+                         tokens=res[0].cpu().numpy()[:n + 1].tolist())
+    out["workload"] = f"V={V}, g={g}, n_S={n_S}, fp32 target logits, fp64 decisions, L2 flushed"
+    out["flags"] = ctx.get_flags()
+    ctx.close()
+    del flush
+    return out
+
+
+def verify_parity_cpu_leg(vl):
+    """cpu_baseline leg: the verification line's tokens against the oracle (same seeded inputs)."""
+    import oracle
+    P = synth.verify_problem(0, V=128256, g=6, n_S=36864)
+    for mode, greedy in (("greedy", True), ("sampling", False)):
+        ref_tok, ref_n = oracle.verify_chain(P["z"], P["x"], P["S"], P["q"], greedy=greedy, u=P["u"], w=P["w"])
+        r = vl[mode]
+        r["parity_exact"] = r["n_accepted"] == ref_n and r["tokens"] == ref_tok.tolist()
 
 
 def sharded_sweep(dev, args):

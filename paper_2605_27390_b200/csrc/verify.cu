@@ -16,24 +16,32 @@
 //             the smallest v (id order) whose running sum of the weights
 //             exceeds w * (their total).
 //
-// Kernel 1 (verify_pos_kernel): one CTA per position, every position at once
-// (the first rejection is not known up front): max / argmax and the fp64 sum
-// over V; the acceptance test; for a rejected position (sampling) or the bonus
-// position the draw -- per-thread residual mass over a contiguous id range
-// (the q lookup walks the sorted subset from a binary-searched start), a block
-// scan of the masses, and the thread whose range holds w * total re-walks it.
+// Kernel 1 (verify_pos_kernel): a cluster of 8 CTAs per position (each a
+// contiguous slice of V), every position at once (the first rejection is not
+// known up front): max / argmax and the fp64 sum over V, combined over the
+// cluster through distributed shared memory in rank order (every CTA holds the
+// same values, so all take the same decisions); the acceptance test; for a
+// rejected position (sampling) or the bonus position the draw -- per-thread
+// residual mass over a contiguous id range (the q lookup walks the sorted
+// subset from a binary-searched start), the CTA whose mass interval holds
+// w * total, a block scan there, and the thread whose range holds it re-walks.
 // The fp64 sums run in a different order than the oracle's sequential ones; a
 // different token needs w * total within ~1e-15 relative of a CDF step.
 // Kernel 2 (verify_decide_kernel, one warp): the accepted prefix and the
 // emitted token. HBM-bound: (g + 1) rows of V fp32 logits, read from HBM once
 // (the further passes hit L2).
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "kernels.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace es {
 
 constexpr int kVerThreads = 1024;
 constexpr int kVerWarps = kVerThreads / 32;
+constexpr int kVerCluster = 8;   // CTAs per position (a portable cluster; DSMEM reductions)
 
 struct VerSmem {
     double red_d[kVerWarps];
@@ -42,6 +50,9 @@ struct VerSmem {
     int red_i[kVerWarps];
     double s_M, s_sum, s_tot;
     int s_arg, s_pick;
+    double c_part;   // this CTA's partial, read by the cluster (DSMEM)
+    float c_v;
+    int c_i;
 };
 
 ES_DEV double warp_sum_dd(double v) {
@@ -120,10 +131,29 @@ struct Resid {
     }
 };
 
-// the draw from weights r over [0, V) with w in [0, 1); every thread of the block calls it
-ES_DEV int block_draw(const Resid& R, int V, double w, VerSmem& sm) {
+// Cluster-wide reductions (kVerCluster CTAs per position, DSMEM): every CTA
+// combines the CTA partials in rank order, so all of them hold identical
+// values and take identical decisions.
+ES_DEV double cluster_sum_d(double v, VerSmem& sm, cg::cluster_group& cl) {
+    const double b = block_sum_d(v, sm);
+    if (threadIdx.x == 0) sm.c_part = b;
+    cl.sync();
+    double t = 0.0;
+#pragma unroll
+    for (int r = 0; r < kVerCluster; ++r) t += *cl.map_shared_rank(&sm.c_part, r);
+    cl.sync();
+    return t;
+}
+
+// the draw from weights r over [0, V) with w in [0, 1), cluster-wide: each CTA
+// holds a contiguous slice [c0, c1); the CTA whose mass interval (prefix in rank
+// order) holds w * total finds the id by a block scan and one thread's re-walk.
+// Returns -2 on every CTA if the total mass is 0, else the id on the picking
+// CTA's thread 0 (-1 elsewhere).
+ES_DEV int cluster_draw(const Resid& R, int c0, int c1, double w, VerSmem& sm, cg::cluster_group& cl) {
     const int tid = threadIdx.x;
-    const int v0 = (int)((long long)V * tid / kVerThreads), v1 = (int)((long long)V * (tid + 1) / kVerThreads);
+    const int n = c1 - c0;
+    const int v0 = c0 + (int)((long long)n * tid / kVerThreads), v1 = c0 + (int)((long long)n * (tid + 1) / kVerThreads);
     const int i0 = R.qj ? lower_bound_i32(R.S, R.n_S, v0) : 0;
     double loc = 0.0;
     int last = -1;
@@ -134,53 +164,68 @@ ES_DEV int block_draw(const Resid& R, int V, double w, VerSmem& sm) {
             if (r > 0.0) { loc += r; last = v; }
         }
     }
-    const double tot = block_sum_d(loc, sm);
-    if (!(tot > 0.0)) return -2;   // no residual mass (rounding only): the caller draws from p
+    const double mine = block_sum_d(loc, sm);
+    if (tid == 0) sm.c_part = mine;
+    cl.sync();
+    double masses[kVerCluster];
+#pragma unroll
+    for (int r = 0; r < kVerCluster; ++r) masses[r] = *cl.map_shared_rank(&sm.c_part, r);
+    cl.sync();
+    const int me = (int)cl.block_rank();
+    double tot = 0.0, pre = 0.0;
+    int last_rank = -1;
+#pragma unroll
+    for (int r = 0; r < kVerCluster; ++r) {
+        if (r == me) pre = tot;
+        tot += masses[r];
+        if (masses[r] > 0.0) last_rank = r;
+    }
+    if (!(tot > 0.0)) return -2;
     const double target = w * tot;
-    const double pre = block_excl_scan_d(loc, sm);
+    const bool pick = (mine > 0.0 && pre <= target && target < pre + mine) || (me == last_rank && target >= pre + mine);
+    if (!pick) return -1;
+    // this CTA: the thread whose mass interval holds the target re-walks its range
+    const double tpre = pre + block_excl_scan_d(loc, sm);
     if (tid == 0) sm.s_pick = 0x7fffffff;
     __syncthreads();
-    if (loc > 0.0 && pre <= target && target < pre + loc) atomicMin(&sm.s_pick, tid);
-    // the last id with mass, for a target in the rounding band above the total
+    if (loc > 0.0 && tpre <= target && target < tpre + loc) atomicMin(&sm.s_pick, tid);
     __syncthreads();
     const bool none = sm.s_pick == 0x7fffffff;
+    if (tid == 0) sm.s_arg = -1;
     __syncthreads();
     if (none) {
-        if (tid == 0) sm.s_arg = -1;
-        __syncthreads();
-        if (last >= 0) atomicMax(&sm.s_arg, last);
-        __syncthreads();
-        return sm.s_arg;
-    }
-    if (tid == sm.s_pick) {
-        double run = pre;
-        int i = i0, pick = last;
+        if (last >= 0) atomicMax(&sm.s_arg, last);   // the rounding band above the CTA's mass
+    } else if (tid == sm.s_pick) {
+        double run = tpre;
+        int i = i0, got = last;
         for (int v = v0; v < v1; ++v) {
             const double r = R.r_at(v, i);
             if (r > 0.0) {
                 run += r;
-                if (run > target) { pick = v; break; }
+                if (run > target) { got = v; break; }
             }
         }
-        sm.s_arg = pick;
+        sm.s_arg = got;
     }
     __syncthreads();
-    const int res = sm.s_arg;
-    __syncthreads();
-    return res;
+    return sm.s_arg;
 }
 
-__global__ void __launch_bounds__(kVerThreads)
+__global__ void __cluster_dims__(kVerCluster, 1, 1) __launch_bounds__(kVerThreads)
 verify_pos_kernel(const float* __restrict__ z, int V, int g, const int32_t* __restrict__ x,
                   const int32_t* __restrict__ S, int n_S, const float* __restrict__ qS, double it, int greedy,
                   const double* __restrict__ u, const double* __restrict__ w, int32_t* __restrict__ pos_acc,
                   int32_t* __restrict__ pos_tok, int* flags) {
     __shared__ VerSmem sm;
+    cg::cluster_group cl = cg::this_cluster();
     pdl_trigger();
     pdl_wait();
-    const int j = blockIdx.x, tid = threadIdx.x, lane = lane_id(), wid = warp_id();
+    const int j = blockIdx.x / kVerCluster, me = (int)cl.block_rank();
+    const int tid = threadIdx.x, lane = lane_id(), wid = warp_id();
     const float* zj = z + (size_t)j * V;
-    const int v0 = (int)((long long)V * tid / kVerThreads), v1 = (int)((long long)V * (tid + 1) / kVerThreads);
+    const int c0 = (int)((long long)V * me / kVerCluster), c1 = (int)((long long)V * (me + 1) / kVerCluster);
+    const int n = c1 - c0;
+    const int v0 = c0 + (int)((long long)n * tid / kVerThreads), v1 = c0 + (int)((long long)n * (tid + 1) / kVerThreads);
     // 1. maximum and argmax (value desc, id asc), in fp32 -- the fp64 product of an
     //    fp32 logit and it orders exactly as the logit itself (it > 0)
     float bv = -INFINITY;
@@ -196,25 +241,31 @@ verify_pos_kernel(const float* __restrict__ z, int V, int g, const int32_t* __re
         float v = lane < kVerWarps ? sm.red_v[lane] : -INFINITY;
         int i = lane < kVerWarps ? sm.red_i[lane] : 0x7fffffff;
         warp_argbest(v, i);
-        if (lane == 0) { sm.s_M = (double)v * it; sm.s_arg = i; }
+        if (lane == 0) { sm.c_v = v; sm.c_i = i; }
     }
-    __syncthreads();
-    const double M = sm.s_M;
-    const int amax = sm.s_arg;
-    __syncthreads();
+    cl.sync();
+    float Mv = -INFINITY;
+    int amax = 0x7fffffff;
+#pragma unroll
+    for (int r = 0; r < kVerCluster; ++r) {
+        const float v = *cl.map_shared_rank(&sm.c_v, r);
+        const int i = *cl.map_shared_rank(&sm.c_i, r);
+        if (before(v, i, Mv, amax)) { Mv = v; amax = i; }
+    }
+    cl.sync();
+    const double M = (double)Mv * it;
     if (greedy) {
-        if (tid == 0) {
+        if (me == 0 && tid == 0) {
             pos_tok[j] = amax;
             pos_acc[j] = j < g ? (int)(__ldg(&x[j]) == amax) : 0;
         }
         return;
     }
-    // 2. s = sum_v exp(z it - M), fp64
+    // 2. s = sum_v exp(z it - M), fp64, cluster-wide
     double loc = 0.0;
     for (int v = v0; v < v1; ++v) loc += exp((double)__ldg(&zj[v]) * it - M);
-    const double s = block_sum_d(loc, sm);
-    // 3. acceptance (j < g) or the bonus draw (j == g)
-    bool acc = false;
+    const double s = cluster_sum_d(loc, sm, cl);
+    // 3. acceptance (j < g) or the bonus draw (j == g) -- identical on every CTA
     const float* qj = nullptr;
     if (j < g) {
         const int xj = __ldg(&x[j]);
@@ -222,24 +273,23 @@ verify_pos_kernel(const float* __restrict__ z, int V, int g, const int32_t* __re
         const int i = (xj >= 0 && xj < V) ? lower_bound_i32(S, n_S, xj) : n_S;
         const bool in = i < n_S && __ldg(&S[i]) == xj && __ldg(&qj[i]) > 0.0f;
         if (!in) {
-            if (tid == 0) { atomicOr(flags, kFlagBadIds); pos_acc[j] = 0; pos_tok[j] = -1; }
+            if (me == 0 && tid == 0) { atomicOr(flags, kFlagBadIds); pos_acc[j] = 0; pos_tok[j] = -1; }
             return;
         }
         double a = exp((double)__ldg(&zj[xj]) * it - M) / s / (double)__ldg(&qj[i]);
         if (a > 1.0) a = 1.0;
-        acc = __ldg(&u[j]) < a;
-        if (acc) {
-            if (tid == 0) { pos_acc[j] = 1; pos_tok[j] = xj; }
+        if (__ldg(&u[j]) < a) {
+            if (me == 0 && tid == 0) { pos_acc[j] = 1; pos_tok[j] = xj; }
             return;
         }
     }
     const Resid R{zj, it, M, s, S, n_S, j < g ? qj : nullptr};
-    int tok = block_draw(R, V, __ldg(&w[j]), sm);
-    if (tok == -2) {   // no residual mass: draw from p_j
+    int tok = cluster_draw(R, c0, c1, __ldg(&w[j]), sm, cl);
+    if (tok == -2) {   // no residual mass (rounding only): draw from p_j
         const Resid P{zj, it, M, s, S, n_S, nullptr};
-        tok = block_draw(P, V, __ldg(&w[j]), sm);
+        tok = cluster_draw(P, c0, c1, __ldg(&w[j]), sm, cl);
     }
-    if (tid == 0) { pos_acc[j] = 0; pos_tok[j] = tok; }
+    if (tok >= 0 && tid == 0) { pos_acc[j] = 0; pos_tok[j] = tok; }
 }
 
 __global__ void verify_decide_kernel(int g, const int32_t* __restrict__ x, const int32_t* __restrict__ pos_acc,
@@ -257,7 +307,7 @@ __global__ void verify_decide_kernel(int g, const int32_t* __restrict__ x, const
 void launch_verify(const float* z, int V, int g, const int32_t* x, const int32_t* S, int n_S, const float* qS,
                    double it, int greedy, const double* u, const double* w, int32_t* pos_acc, int32_t* pos_tok,
                    int32_t* tokens, int32_t* n_acc_out, int* flags, cudaStream_t st) {
-    launch_pdl(verify_pos_kernel, dim3(g + 1), dim3(kVerThreads), 0, st, z, V, g, x, S, n_S, qS, it, greedy, u, w,
+    launch_pdl(verify_pos_kernel, dim3((g + 1) * kVerCluster), dim3(kVerThreads), 0, st, z, V, g, x, S, n_S, qS, it, greedy, u, w,
                pos_acc, pos_tok, flags);
     launch_pdl(verify_decide_kernel, dim3(1), dim3(32), 0, st, g, x, (const int32_t*)pos_acc,
                (const int32_t*)pos_tok, tokens, n_acc_out);
