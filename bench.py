@@ -290,7 +290,7 @@ def run_ours(args):
         del Wd
         torch.cuda.empty_cache()
         extra = dict(qwen_topic_segment=qwen_segment(dev, args), sharded_d8192_r1=sharded_sweep(dev, args),
-                     verify_chain=verify_line(dev, args))
+                     verify_chain=verify_line(dev, args), coverage=coverage_line(dev, args))
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -482,6 +482,39 @@ def verify_line(dev, args):
                          tokens=res[0].cpu().numpy()[:n + 1].tolist())
     out["workload"] = f"V={V}, g={g}, n_S={n_S}, fp32 target logits, fp64 decisions, L2 flushed"
     out["flags"] = ctx.get_flags()
+    ctx.close()
+    del flush
+    return out
+
+
+def coverage_line(dev, args):
+    """N4: covered mass and Recall@{10, 50, 100} (App. E) of a
+    36,864-id subset against 60 target rows over the llama vocabulary (synthetic logits;
+    the values only exercise the kernel), L2 flushed before each call."""
+    import torch
+    import paper_2605_27390_b200 as es
+    V, n, n_S = 128256, 60, 36864
+    rng = np.random.default_rng(17)
+    z = torch.from_numpy((rng.normal(size=(n, V)) * 1.28).astype(np.float32)).to(dev)
+    S = torch.from_numpy(np.sort(rng.choice(V, n_S, replace=False)).astype(np.int32)).to(dev)
+    ks = torch.tensor([10, 50, 100], dtype=torch.int32, device=dev)
+    ctx = es.Context(V=V, d=64, w_dtype=torch.bfloat16, h_dtype=torch.bfloat16, max_subset=1, max_rows=1,
+                     max_k=1, max_sem=1)
+    flush = L2Flush(dev)
+    evs, res = [], None
+    for it in range(args.warmup + args.sweep_steps):
+        flush(it)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        res = ctx.coverage(z, S, ks, out=res)
+        e1.record()
+        evs.append((e0, e1))
+    torch.cuda.synchronize()
+    us = statistics.median([a.elapsed_time(b) for a, b in evs[args.warmup:]]) * 1e3
+    nbytes = n * V * 4 + n_S * 4 + n * n_S * 4
+    out = dict(workload=f"{n} target rows x V={V}, |V_t|={n_S}, Recall@10/50/100, L2 flushed", us=us,
+               GBps=nbytes / (us * 1e-6) / 1e9, mean_mass=float(res[0].mean().item()),
+               mean_recall=[float(x) for x in res[1].mean(0).tolist()])
     ctx.close()
     del flush
     return out

@@ -289,6 +289,22 @@ evospec_status evospec_verify_chain(evospec_ctx *ctx, const float *target_logits
     float inv_temp, int32_t greedy, const double *u, const double *w,
     int32_t *tokens, int32_t *n_accepted, void *stream);
 
+/* ---- N4: coverage of the active vocabulary ---------------- */
+
+/* For each target row r < n_rows: p_r(v) = exp(z_r[v] inv_temp - m_r) / s_r
+ * over [0, V) (fp64) and
+ *   covered_mass[r]   = sum_{v in V_t} p_r(v)     (Eq. 2's constraint P:58-62,
+ *                                                  App. E)
+ *   recall[r][t]      = |V_t n top-ks[t](p_r)| / ks[t], the target top-k
+ *                       ordered (p desc, id asc)
+ * target_logits [n_rows, V] fp32; subset_ids [n_subset] sorted ascending
+ * unique (V_t); ks [n_ks] int32 in [1, V], n_ks <= 64; outputs covered_mass
+ * [n_rows] and recall [n_rows, n_ks] fp64 (device). Async, one launch.
+ * EVOSPEC_EINPUT on null / out-of-range host arguments. */
+evospec_status evospec_coverage(evospec_ctx *ctx, const float *target_logits, int32_t n_rows, int32_t V,
+    const int32_t *subset_ids, int32_t n_subset, float inv_temp, const int32_t *ks, int32_t n_ks,
+    double *covered_mass, double *recall, void *stream);
+
 /* ---- one draft step through the whole path -------------------------------- */
 
 /* Per-step I/O for evospec_draft_step. `host_io` = 1: q, H, seeds, ctx and

@@ -269,3 +269,22 @@ def verify_chain(z, x, S, qS, *, inv_temp: float = 1.0, greedy: bool, u=None, w=
     _check(rc, "verify_chain")
     n = int(n_acc[0])
     return tokens[:n + 1].copy(), n
+
+
+def coverage(z, S, ks, *, inv_temp: float = 1.0):
+    """N4: covered mass and Recall@k of the subset S against the target rows z (eo_coverage).
+    z float32 [n_rows, V] logits; S sorted int32; ks list of k. Returns (mass [n_rows],
+    recall [n_rows, len(ks)]) as float64."""
+    z = np.ascontiguousarray(np.atleast_2d(z), dtype=np.float32)
+    n_rows, V = z.shape
+    S = _i32(np.asarray(S, dtype=np.int32).reshape(-1))
+    ks = _i32(np.asarray(ks, dtype=np.int32).reshape(-1))
+    mass = np.zeros(n_rows, np.float64)
+    rec = np.zeros((n_rows, max(1, ks.size)), np.float64)
+    f = _L().eo_coverage
+    f.restype = C.c_int
+    f.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_double, C.c_void_p, C.c_int,
+                  C.c_void_p, C.c_void_p]
+    _check(f(_p(z), n_rows, V, _p(S), int(S.size), float(inv_temp), _p(ks), int(ks.size), _p(mass), _p(rec)),
+           "coverage")
+    return mass, rec[:, :ks.size]

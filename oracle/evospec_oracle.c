@@ -463,3 +463,55 @@ int eo_verify_chain(const float *z, int V, int g, const int32_t *x, const int32_
     *n_acc_out = n_acc;
     return EO_OK;
 }
+
+/* ------------------------------------------------------------------ */
+/* N4: coverage of the active vocabulary against a     */
+/* target distribution -- the covered mass of Eq. 2's constraint      */
+/* "sum_{x in V_t} p >= 1 - eps_cov" and App. E's "covered  */
+/* probability mass" and Recall@k.         */
+/* Row r: p_r(v) = exp(z_r[v] it - m_r) / s_r over [0, V), fp64;       */
+/*   mass_r = sum_{v in S} p_r(v);                                     */
+/*   recall_r[k] = |S n top-k(p_r)| / k, top-k by (p desc, id asc).   */
+/* Out: mass [n_rows], recall [n_rows][n_ks] (fp64).                  */
+/* ------------------------------------------------------------------ */
+typedef struct { float z; int32_t id; } eo_zid;
+static int eo_cmp_zid_desc(const void *a, const void *b) {
+    const eo_zid *x = (const eo_zid *)a, *y = (const eo_zid *)b;
+    if (x->z > y->z) return -1;
+    if (x->z < y->z) return 1;
+    return (x->id > y->id) - (x->id < y->id);
+}
+
+int eo_coverage(const float *z, int n_rows, int V, const int32_t *S, int n_S, double inv_temp,
+                const int32_t *ks, int n_ks, double *mass, double *recall) {
+    if (!z || n_rows < 0 || V < 1 || n_S < 0 || (n_S > 0 && !S) || !(inv_temp > 0.0) || n_ks < 0 ||
+        (n_ks > 0 && (!ks || !recall)) || !mass)
+        return EO_EINPUT;
+    for (int i = 0; i < n_S; ++i)
+        if (S[i] < 0 || S[i] >= V || (i > 0 && S[i - 1] >= S[i])) return EO_EINPUT;
+    for (int t = 0; t < n_ks; ++t)
+        if (ks[t] < 1 || ks[t] > V) return EO_EINPUT;
+    eo_zid *order = (eo_zid *)malloc(sizeof(eo_zid) * (size_t)V);
+    if (!order) return EO_EINPUT;
+    for (int r = 0; r < n_rows; ++r) {
+        const float *zr = z + (int64_t)r * V;
+        double M = -INFINITY;
+        for (int v = 0; v < V; ++v) if ((double)zr[v] * inv_temp > M) M = (double)zr[v] * inv_temp;
+        double s = 0.0;
+        for (int v = 0; v < V; ++v) s += exp((double)zr[v] * inv_temp - M);
+        double cm = 0.0;
+        for (int i = 0; i < n_S; ++i) cm += exp((double)zr[S[i]] * inv_temp - M) / s;
+        mass[r] = cm;
+        if (n_ks == 0) continue;
+        /* p order = logit order (inv_temp > 0); ties by the smaller id */
+        for (int v = 0; v < V; ++v) { order[v].z = zr[v]; order[v].id = v; }
+        qsort(order, (size_t)V, sizeof(eo_zid), eo_cmp_zid_desc);
+        for (int t = 0; t < n_ks; ++t) {
+            int hit = 0;
+            for (int i = 0; i < ks[t]; ++i) hit += eo_find_sorted(S, n_S, order[i].id) >= 0;
+            recall[(int64_t)r * n_ks + t] = (double)hit / (double)ks[t];
+        }
+    }
+    free(order);
+    return EO_OK;
+}

@@ -28,7 +28,7 @@ EXPORTED = [
     "evospec_last_semantic", "evospec_subset_logits_topk", "evospec_merge_shards",
     "evospec_draft_step", "evospec_set_timing", "evospec_read_stats", "evospec_read_trace",
     "evospec_build_subset_batched", "evospec_subset_logits_topk_ragged", "evospec_subset_logits_topk_merged",
-    "evospec_verify_chain",
+    "evospec_verify_chain", "evospec_coverage",
 ]
 
 STAGES = ["scan", "select", "union", "lmh", "finalize", "merge", "copy"]
@@ -100,6 +100,7 @@ def lib() -> C.CDLL:
                                             vp, vp, vp, vp, vp, vp], i32),
             "evospec_merge_shards": ([vp, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp], i32),
             "evospec_verify_chain": ([vp, vp, i32, i32, vp, vp, i32, vp, C.c_float, i32, vp, vp, vp, vp, vp], i32),
+            "evospec_coverage": ([vp, vp, i32, i32, vp, i32, C.c_float, vp, i32, vp, vp, vp], i32),
             "evospec_draft_step": ([vp, C.POINTER(StepIO), vp], i32),
             "evospec_set_timing": ([vp, C.c_int], i32),
             "evospec_read_stats": ([vp, C.POINTER(Stats)], i32),
@@ -357,6 +358,22 @@ class Context:
                                           _ptr(draft_probs), float(inv_temp), int(bool(greedy)), _ptr(u), _ptr(w),
                                           _ptr(tok), _ptr(nacc), _stream(stream)))
         return tok, nacc
+
+    # ---- N4: coverage of the active vocabulary
+    def coverage(self, z, subset, ks, *, inv_temp: float = 1.0, out=None, stream=None):
+        """Covered mass and Recall@k of `subset` (sorted int32, device) against the target rows
+        z (fp32 [n_rows, V], device); ks int32 device tensor. Returns (mass fp64 [n_rows],
+        recall fp64 [n_rows, len(ks)])."""
+        import torch
+        n_rows, V = z.shape
+        if out is None:
+            out = (torch.empty(n_rows, dtype=torch.float64, device=z.device),
+                   torch.empty((n_rows, max(1, ks.numel())), dtype=torch.float64, device=z.device))
+        mass, rec = out
+        _check(lib().evospec_coverage(self._h, _ptr(z), n_rows, V, _ptr(subset), int(subset.numel()),
+                                      float(inv_temp), _ptr(ks), int(ks.numel()), _ptr(mass), _ptr(rec),
+                                      _stream(stream)))
+        return mass, rec[:, :ks.numel()]
 
     # ---- whole step
     def draft_step(self, *, E, W_local, static_ids, csr_row_ptr, csr_col, q, H, seeds, k: int,

@@ -798,6 +798,23 @@ evospec_status evospec_verify_chain(evospec_ctx* ctx, const float* target_logits
     return EVOSPEC_OK;
 }
 
+evospec_status evospec_coverage(evospec_ctx* ctx, const float* target_logits, int32_t n_rows, int32_t V,
+                                const int32_t* subset_ids, int32_t n_subset, float inv_temp, const int32_t* ks,
+                                int32_t n_ks, double* covered_mass, double* recall, void* stream) {
+    if (!ctx || !target_logits || !covered_mass || (n_subset > 0 && !subset_ids) || (n_ks > 0 && (!ks || !recall)))
+        return fail(EVOSPEC_EINPUT, "coverage: null argument");
+    if (n_rows < 0 || V < 1 || n_subset < 0 || n_subset > V || n_ks < 0 || n_ks > 64)
+        return fail(EVOSPEC_EINPUT, "coverage: n_rows=%d / V=%d / n_subset=%d / n_ks=%d out of range", n_rows, V,
+                    n_subset, n_ks);
+    if (!(inv_temp > 0.0f) || !std::isfinite(inv_temp)) return fail(EVOSPEC_EINPUT, "coverage: inv_temp must be > 0");
+    if (n_rows == 0) return EVOSPEC_OK;
+    launch_coverage(target_logits, n_rows, V, subset_ids, n_subset, (double)inv_temp, ks, n_ks, covered_mass, recall,
+                    (cudaStream_t)stream);
+    ctx->launches += 1;
+    LAUNCH_CHECK("coverage");
+    return EVOSPEC_OK;
+}
+
 // phases: 1 host->device staging, 2 the compute (build + LM head + merge), 4 device->host
 static evospec_status draft_step_impl(evospec_ctx* ctx, const evospec_step_io* io, cudaStream_t st,
                                       int phases = 7) {

@@ -27,7 +27,8 @@ DEV = "cuda:0"
 def problem(seed, V=128256, g=6, n_S=36864, inv_temp=1.0):
     """Seeded verification inputs (synth.verify_problem: target logits, subset, draft
     distribution on it, proposals drawn from the draft, uniforms)."""
-    return synth.verify_problem(seed, V=V, g=g, n_S=n_S, inv_temp=inv_temp)
+    # the ABI's inv_temp is fp32: both sides take that value
+    return synth.verify_problem(seed, V=V, g=g, n_S=n_S, inv_temp=float(np.float32(inv_temp)))
 
 
 def run_gpu(P, greedy, ctx=None):

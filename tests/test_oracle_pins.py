@@ -582,3 +582,52 @@ def test_verify_rejects_proposal_outside_support():
     with pytest.raises(ValueError):
         oracle.verify_chain(z, [2], np.array([0, 1], np.int32), np.array([[0.5, 0.5]], np.float32),
                             greedy=False, u=[0.1], w=[0.1, 0.1])
+
+
+# ---------------------------------------------------------------- N4 coverage
+# Pins for oracle.coverage (eo_coverage): SPEC S:173-175 worked examples, an
+# independent numpy implementation (scipy softmax in fp64, np.lexsort top-k with
+# the smallest-id tie rule of S:171), and the insertion monotonicity of S:178.
+
+def test_coverage_spec_examples():
+    import oracle
+    z = np.log(np.array([[0.5, 0.3, 0.2]], np.float32))
+    m, r = oracle.coverage(z, [0, 2], [2])
+    assert abs(m[0] - 0.7) < 1e-7 and r[0, 0] == 0.5
+    m, r = oracle.coverage(z, [0, 1, 2], [1, 2, 3])
+    assert abs(m[0] - 1.0) < 1e-12 and np.all(r == 1.0)
+    z2 = np.array([[0.0, 0.0, -np.inf, -np.inf]], np.float32)   # support {0, 1}
+    m, _ = oracle.coverage(z2, [2, 3], [1])
+    assert m[0] == 0.0
+
+
+@pytest.mark.parametrize("integer", [False, True])
+def test_coverage_matches_numpy(integer):
+    import oracle
+    from scipy.special import softmax
+    rng = np.random.default_rng(5)
+    n, V = 4, 3000
+    z = (rng.integers(-3, 4, size=(n, V)) if integer else rng.normal(size=(n, V)) * 1.3).astype(np.float32)
+    S = np.sort(rng.choice(V, 700, replace=False)).astype(np.int32)
+    ks = [1, 10, 50, 100, 2999]
+    m, r = oracle.coverage(z, S, ks, inv_temp=1 / 0.7)
+    inS = np.zeros(V, bool)
+    inS[S] = True
+    for i in range(n):
+        p = softmax(z[i].astype(np.float64) / 0.7)
+        assert abs(m[i] - p[S].sum()) < 1e-12
+        order = np.lexsort((np.arange(V), -z[i]))      # (z desc, id asc)
+        for t, k in enumerate(ks):
+            assert r[i, t] == inS[order[:k]].sum() / k
+
+
+def test_coverage_monotone_under_insertion():
+    import oracle
+    rng = np.random.default_rng(9)
+    V = 500
+    z = rng.normal(size=(3, V)).astype(np.float32)
+    S = np.sort(rng.choice(V, 50, replace=False)).astype(np.int32)
+    m0, r0 = oracle.coverage(z, S, [5, 20])
+    S2 = np.union1d(S, rng.choice(V, 40, replace=False)).astype(np.int32)
+    m1, r1 = oracle.coverage(z, S2, [5, 20])
+    assert np.all(m1 >= m0) and np.all(r1 >= r0)
