@@ -290,7 +290,8 @@ def run_ours(args):
         del Wd
         torch.cuda.empty_cache()
         extra = dict(qwen_topic_segment=qwen_segment(dev, args), sharded_d8192_r1=sharded_sweep(dev, args),
-                     verify_chain=verify_line(dev, args), coverage=coverage_line(dev, args))
+                     verify_chain=verify_line(dev, args), coverage=coverage_line(dev, args),
+                     kd_loss=kd_line(dev, args))
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -517,6 +518,35 @@ def coverage_line(dev, args):
                mean_recall=[float(x) for x in res[1].mean(0).tolist()])
     ctx.close()
     del flush
+    return out
+
+
+def kd_line(dev, args):
+    """N3: the curriculum-weighted KD objective's forward + gradient for the
+    paper's buffer (B = 32 trajectories) x horizon 6 on a 64-logit support
+    (K_logit not given: reading K2), T_kd = 1, beta = 0.3; calls back to back."""
+    import torch
+    import paper_2605_27390_b200 as es
+    B, g, K = 32, 6, 64
+    rng = np.random.default_rng(31)
+    zp = torch.from_numpy((rng.normal(size=(B, g, K)) * 2).astype(np.float32)).to(dev)
+    zq = torch.from_numpy((rng.normal(size=(B, g, K)) * 2).astype(np.float32)).to(dev)
+    v = torch.from_numpy(rng.integers(0, K, size=B).astype(np.int32)).to(dev)
+    ctx = es.Context(V=1024, d=64, w_dtype=torch.bfloat16, h_dtype=torch.bfloat16, max_subset=1, max_rows=1,
+                     max_k=1, max_sem=1)
+    res = None
+    for _ in range(args.warmup):
+        res = ctx.kd_loss(zp, zq, v, out=res)
+    reps = 50
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        res = ctx.kd_loss(zp, zq, v, out=res)
+    e1.record()
+    torch.cuda.synchronize()
+    out = dict(workload=f"B={B} x g={g} x K={K}, T_kd=1, beta=0.3, forward + gradient", us=e0.elapsed_time(e1) * 1e3 / reps,
+               mean_loss=float(res[0].mean().item()))
+    ctx.close()
     return out
 
 

@@ -305,6 +305,27 @@ evospec_status evospec_coverage(evospec_ctx *ctx, const float *target_logits, in
     const int32_t *subset_ids, int32_t n_subset, float inv_temp, const int32_t *ks, int32_t n_ks,
     double *covered_mass, double *recall, void *stream);
 
+/* ---- N3: curriculum-weighted distillation objective -------- */
+
+/* Forward and gradient (w.r.t. the draft logits) of Eq. lora_objective
+ * with the horizon weights of Eq. curriculum_weight,
+ * per trajectory b < B and step j < g on the retained support of K target
+ * logits (the LoRA update itself is out of scope):
+ *   p_hat = softmax(target / T_kd), p_til = softmax(draft / T_kd),
+ *   L_base[b] = logsumexp(draft[b][0]) - draft[b][0][verified[b]]  (the
+ *     first-step cross entropy against the verified token, temperature 1),
+ *   weights[b][j] = exp(-beta L_base[b] j),
+ *   loss[b] = sum_j weights[b][j] T_kd^2 KL(p_hat || p_til),
+ *   grad[b][j][i] = weights[b][j] T_kd (p_til[i] - p_hat[i])  (weights held
+ *     fixed: a confidence proxy).
+ * target_logits / draft_logits [B, g, K] fp32, verified [B] int32 (support
+ * index in [0, K)); outputs loss [B], grad [B, g, K] (may be NULL), weights
+ * [B, g] (may be NULL), fp32, device. g <= 32, K <= 1024 (the paper: gamma =
+ * 6, T_kd = 1, beta = 0.3). fp32 arithmetic. Async. */
+evospec_status evospec_kd_loss(evospec_ctx *ctx, int32_t B, int32_t g, int32_t K, const float *target_logits,
+    const float *draft_logits, const int32_t *verified, float T_kd, float beta,
+    float *loss, float *grad, float *weights, void *stream);
+
 /* ---- one draft step through the whole path -------------------------------- */
 
 /* Per-step I/O for evospec_draft_step. `host_io` = 1: q, H, seeds, ctx and

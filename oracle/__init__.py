@@ -288,3 +288,22 @@ def coverage(z, S, ks, *, inv_temp: float = 1.0):
     _check(f(_p(z), n_rows, V, _p(S), int(S.size), float(inv_temp), _p(ks), int(ks.size), _p(mass), _p(rec)),
            "coverage")
     return mass, rec[:, :ks.size]
+
+
+def kd_loss(zp, zq, verified, *, T: float = 1.0, beta: float = 0.3):
+    """N3: curriculum-weighted KD objective (eo_kd_loss). zp, zq float32 [B, g, K] target /
+    draft logits on the retained support, verified int32 [B] (support index of the verified
+    first token). Returns (J [B], grad [B, g, K], w [B, g]) as float64."""
+    zp = np.ascontiguousarray(zp, dtype=np.float32)
+    zq = np.ascontiguousarray(zq, dtype=np.float32)
+    B, g, K = zp.shape
+    v = _i32(np.asarray(verified, dtype=np.int32).reshape(-1))
+    J = np.zeros(B, np.float64)
+    grad = np.zeros((B, g, K), np.float64)
+    w = np.zeros((B, g), np.float64)
+    f = _L().eo_kd_loss
+    f.restype = C.c_int
+    f.argtypes = [C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_double,
+                  C.c_void_p, C.c_void_p, C.c_void_p]
+    _check(f(B, g, K, _p(zp), _p(zq), _p(v), float(T), float(beta), _p(J), _p(grad), _p(w)), "kd_loss")
+    return J, grad, w

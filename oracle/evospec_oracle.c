@@ -515,3 +515,61 @@ int eo_coverage(const float *z, int n_rows, int V, const int32_t *S, int n_S, do
     free(order);
     return EO_OK;
 }
+
+/* ------------------------------------------------------------------ */
+/* N3: the curriculum-weighted distillation objective  */
+/* of Eq. lora_objective with the adaptive horizon weights */
+/* of Eq. curriculum_weight, forward and gradient with    */
+/* respect to the draft logits only (the LoRA loop is out of scope).   */
+/* Trajectory b, step j (0-based; the paper's j-1): on the retained   */
+/* support of K target logits,                                         */
+/*   p_hat = softmax(zp[b][j] / T),  p_til = softmax(zq[b][j] / T),    */
+/*   L_base[b] = logsumexp(zq[b][0]) - zq[b][0][v_b]  (the first-step */
+/*     cross entropy against the verified token at support index v_b, */
+/*     temperature 1 -- reading K1),                                   */
+/*   w[b][j] = exp(-beta * L_base[b] * j),                             */
+/*   J[b] = sum_j w[b][j] T^2 KL(p_hat || p_til),                      */
+/*   dJ/dzq[b][j][i] = w[b][j] T (p_til[i] - p_hat[i])  (w held fixed: */
+/*     the weight is a confidence proxy, reading K1).                  */
+/* fp64 throughout. Out: J [B], grad [B][g][K], w [B][g].             */
+/* ------------------------------------------------------------------ */
+static void eo_softmax_row(const float *z, int K, double scale, double *p, double *lse) {
+    double M = -INFINITY;
+    for (int i = 0; i < K; ++i) if ((double)z[i] * scale > M) M = (double)z[i] * scale;
+    double s = 0.0;
+    for (int i = 0; i < K; ++i) s += exp((double)z[i] * scale - M);
+    for (int i = 0; i < K; ++i) p[i] = exp((double)z[i] * scale - M) / s;
+    if (lse) *lse = M + log(s);
+}
+
+int eo_kd_loss(int B, int g, int K, const float *zp, const float *zq, const int32_t *verified, double T,
+               double beta, double *J, double *grad, double *w_out) {
+    if (B < 0 || g < 1 || K < 1 || !zp || !zq || !verified || !J || !(T > 0.0) || !(beta >= 0.0)) return EO_EINPUT;
+    double *ph = (double *)malloc(sizeof(double) * (size_t)K * 2);
+    if (!ph) return EO_EINPUT;
+    double *pt = ph + K;
+    for (int b = 0; b < B; ++b) {
+        if (verified[b] < 0 || verified[b] >= K) { free(ph); return EO_EINPUT; }
+        const float *q0 = zq + (int64_t)b * g * K;
+        double lse0;
+        eo_softmax_row(q0, K, 1.0, pt, &lse0);
+        const double Lb = lse0 - (double)q0[verified[b]];
+        double tot = 0.0;
+        for (int j = 0; j < g; ++j) {
+            const float *zpj = zp + ((int64_t)b * g + j) * K, *zqj = zq + ((int64_t)b * g + j) * K;
+            const double w = exp(-beta * Lb * (double)j);
+            eo_softmax_row(zpj, K, 1.0 / T, ph, NULL);
+            eo_softmax_row(zqj, K, 1.0 / T, pt, NULL);
+            double kl = 0.0;
+            for (int i = 0; i < K; ++i)
+                if (ph[i] > 0.0) kl += ph[i] * (log(ph[i]) - log(pt[i]));
+            tot += w * T * T * kl;
+            if (grad)
+                for (int i = 0; i < K; ++i) grad[((int64_t)b * g + j) * K + i] = w * T * (pt[i] - ph[i]);
+            if (w_out) w_out[(int64_t)b * g + j] = w;
+        }
+        J[b] = tot;
+    }
+    free(ph);
+    return EO_OK;
+}

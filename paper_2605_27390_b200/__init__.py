@@ -28,7 +28,7 @@ EXPORTED = [
     "evospec_last_semantic", "evospec_subset_logits_topk", "evospec_merge_shards",
     "evospec_draft_step", "evospec_set_timing", "evospec_read_stats", "evospec_read_trace",
     "evospec_build_subset_batched", "evospec_subset_logits_topk_ragged", "evospec_subset_logits_topk_merged",
-    "evospec_verify_chain", "evospec_coverage",
+    "evospec_verify_chain", "evospec_coverage", "evospec_kd_loss",
 ]
 
 STAGES = ["scan", "select", "union", "lmh", "finalize", "merge", "copy"]
@@ -101,6 +101,7 @@ def lib() -> C.CDLL:
             "evospec_merge_shards": ([vp, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp], i32),
             "evospec_verify_chain": ([vp, vp, i32, i32, vp, vp, i32, vp, C.c_float, i32, vp, vp, vp, vp, vp], i32),
             "evospec_coverage": ([vp, vp, i32, i32, vp, i32, C.c_float, vp, i32, vp, vp, vp], i32),
+            "evospec_kd_loss": ([vp, i32, i32, i32, vp, vp, vp, C.c_float, C.c_float, vp, vp, vp, vp], i32),
             "evospec_draft_step": ([vp, C.POINTER(StepIO), vp], i32),
             "evospec_set_timing": ([vp, C.c_int], i32),
             "evospec_read_stats": ([vp, C.POINTER(Stats)], i32),
@@ -374,6 +375,24 @@ class Context:
                                       float(inv_temp), _ptr(ks), int(ks.numel()), _ptr(mass), _ptr(rec),
                                       _stream(stream)))
         return mass, rec[:, :ks.numel()]
+
+    # ---- N3: curriculum-weighted distillation objective
+    def kd_loss(self, target_logits, draft_logits, verified, *, T_kd: float = 1.0, beta: float = 0.3,
+                out=None, stream=None):
+        """Eq. lora_objective with the curriculum weights (evospec_kd_loss). target_logits /
+        draft_logits fp32 [B, g, K], verified int32 [B] (device). Returns (loss [B],
+        grad [B, g, K], weights [B, g]), fp32."""
+        import torch
+        B, g, K = target_logits.shape
+        if out is None:
+            dev = target_logits.device
+            out = (torch.empty(B, dtype=torch.float32, device=dev),
+                   torch.empty((B, g, K), dtype=torch.float32, device=dev),
+                   torch.empty((B, g), dtype=torch.float32, device=dev))
+        loss, grad, w = out
+        _check(lib().evospec_kd_loss(self._h, B, g, K, _ptr(target_logits), _ptr(draft_logits), _ptr(verified),
+                                     float(T_kd), float(beta), _ptr(loss), _ptr(grad), _ptr(w), _stream(stream)))
+        return loss, grad, w
 
     # ---- whole step
     def draft_step(self, *, E, W_local, static_ids, csr_row_ptr, csr_col, q, H, seeds, k: int,

@@ -815,6 +815,21 @@ evospec_status evospec_coverage(evospec_ctx* ctx, const float* target_logits, in
     return EVOSPEC_OK;
 }
 
+evospec_status evospec_kd_loss(evospec_ctx* ctx, int32_t B, int32_t g, int32_t K, const float* target_logits,
+                               const float* draft_logits, const int32_t* verified, float T_kd, float beta,
+                               float* loss, float* grad, float* weights, void* stream) {
+    if (!ctx || !target_logits || !draft_logits || !verified || !loss) return fail(EVOSPEC_EINPUT, "kd_loss: null argument");
+    if (B < 0 || g < 1 || g > 32 || K < 1 || K > 1024)
+        return fail(EVOSPEC_EINPUT, "kd_loss: B=%d / g=%d / K=%d out of range (g <= 32, K <= 1024)", B, g, K);
+    if (!(T_kd > 0.0f) || !std::isfinite(T_kd) || !(beta >= 0.0f) || !std::isfinite(beta))
+        return fail(EVOSPEC_EINPUT, "kd_loss: T_kd must be > 0 and beta >= 0");
+    if (B == 0) return EVOSPEC_OK;
+    launch_kd_loss(B, g, K, target_logits, draft_logits, verified, T_kd, beta, loss, grad, weights, (cudaStream_t)stream);
+    ctx->launches += 1;
+    LAUNCH_CHECK("kd_loss");
+    return EVOSPEC_OK;
+}
+
 // phases: 1 host->device staging, 2 the compute (build + LM head + merge), 4 device->host
 static evospec_status draft_step_impl(evospec_ctx* ctx, const evospec_step_io* io, cudaStream_t st,
                                       int phases = 7) {

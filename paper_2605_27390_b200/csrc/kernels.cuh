@@ -116,6 +116,8 @@ int lmh_gemv_grid();
 int lmh_gemv_group_width(const LmhArgs& a, int n_left);
 constexpr int kTcMaxRows = 128;
 constexpr int kMaxChain = 63;   // verification: longest draft chain (the paper's horizon is 6)
+void launch_kd_loss(int B, int g, int K, const float* zp, const float* zq, const int32_t* verified, float T,
+                    float beta, float* J, float* grad, float* w_out, cudaStream_t st);
 void launch_coverage(const float* z, int n_rows, int V, const int32_t* S, int n_S, double it, const int32_t* ks,
                      int n_ks, double* mass, double* recall, cudaStream_t st);
 void launch_verify(const float* z, int V, int g, const int32_t* x, const int32_t* S, int n_S, const float* qS,

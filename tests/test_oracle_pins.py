@@ -631,3 +631,69 @@ def test_coverage_monotone_under_insertion():
     S2 = np.union1d(S, rng.choice(V, 40, replace=False)).astype(np.int32)
     m1, r1 = oracle.coverage(z, S2, [5, 20])
     assert np.all(m1 >= m0) and np.all(r1 >= r0)
+
+
+# ---------------------------------------------------------------- N3 KD objective
+# Pins for oracle.kd_loss (eo_kd_loss): Eq. curriculum_weight and
+# Eq. lora_objective against an independent scipy implementation
+# (softmax, rel_entr), the KL's zero / positivity, the gradient by central
+# finite differences of J (weights held fixed, reading K1), and the limits the
+# paper names: beta = 0 (no curriculum, equal weights) and a confident first
+# step (L_base -> 0: the horizon flattens).
+
+def test_kd_matches_scipy():
+    import oracle
+    from scipy.special import log_softmax, rel_entr, softmax
+    rng = np.random.default_rng(21)
+    B, g, K, T, beta = 3, 6, 64, 1.7, 0.3
+    zp = (rng.normal(size=(B, g, K)) * 2).astype(np.float32)
+    zq = (rng.normal(size=(B, g, K)) * 2).astype(np.float32)
+    v = rng.integers(0, K, size=B).astype(np.int32)
+    J, _, w = oracle.kd_loss(zp, zq, v, T=T, beta=beta)
+    for b in range(B):
+        Lb = -log_softmax(zq[b, 0].astype(np.float64))[v[b]]
+        wj = np.exp(-beta * Lb * np.arange(g))
+        kl = [rel_entr(softmax(zp[b, j].astype(np.float64) / T), softmax(zq[b, j].astype(np.float64) / T)).sum()
+              for j in range(g)]
+        assert abs(J[b] - (wj * T * T * np.array(kl)).sum()) < 1e-12 * max(1.0, J[b])
+        np.testing.assert_allclose(w[b], wj, rtol=1e-13)
+
+
+def test_kd_zero_positive_and_gradient_fd():
+    import oracle
+    rng = np.random.default_rng(22)
+    B, g, K, T = 2, 4, 16, 1.3
+    zp = rng.normal(size=(B, g, K)).astype(np.float32)
+    zq = rng.normal(size=(B, g, K)).astype(np.float32)
+    v = np.array([2, 5], np.int32)
+    J0, g0, w0 = oracle.kd_loss(zp, zp, v, T=T)
+    assert np.all(J0 == 0.0) and np.all(g0 == 0.0)
+    J, grad, w = oracle.kd_loss(zp, zq, v, T=T)
+    assert np.all(J > 0.0)
+    # central differences of J_b with the weights held at w (beta = 0 keeps them fixed)
+    J, grad, _ = oracle.kd_loss(zp, zq, v, T=T, beta=0.0)
+    h = 1e-2
+    for (b, j, i) in [(0, 0, 3), (1, 2, 7), (1, 3, 15)]:
+        zqp, zqm = zq.copy(), zq.copy()
+        zqp[b, j, i] += h
+        zqm[b, j, i] -= h
+        fd = (oracle.kd_loss(zp, zqp, v, T=T, beta=0.0)[0][b] - oracle.kd_loss(zp, zqm, v, T=T, beta=0.0)[0][b]) / (2 * h)
+        assert abs(fd - grad[b, j, i]) < 1e-4 * max(1.0, abs(fd))
+    # the gradient of each step sums to zero (softmax shift invariance)
+    assert np.abs(grad.sum(-1)).max() < 1e-12
+
+
+def test_kd_curriculum_limits():
+    import oracle
+    rng = np.random.default_rng(23)
+    B, g, K = 1, 6, 32
+    zp = rng.normal(size=(B, g, K)).astype(np.float32)
+    zq = rng.normal(size=(B, g, K)).astype(np.float32)
+    _, _, w = oracle.kd_loss(zp, zq, [0], beta=0.0)
+    assert np.all(w == 1.0)                         # beta = 0: no curriculum
+    zq[0, 0, 0] = 60.0                              # the verified token dominates: L_base ~ 0
+    _, _, w = oracle.kd_loss(zp, zq, [0], beta=0.3)
+    assert np.all(w > 0.999999)                     # the horizon flattens
+    zq[0, 0, 0] = -60.0                             # very unconfident: weights decay fast
+    _, _, w = oracle.kd_loss(zp, zq, [0], beta=0.3)
+    assert w[0, 0] == 1.0 and w[0, 1] < 1e-7
