@@ -291,7 +291,7 @@ def run_ours(args):
         torch.cuda.empty_cache()
         extra = dict(qwen_topic_segment=qwen_segment(dev, args), sharded_d8192_r1=sharded_sweep(dev, args),
                      verify_chain=verify_line(dev, args), coverage=coverage_line(dev, args),
-                     kd_loss=kd_line(dev, args))
+                     kd_loss=kd_line(dev, args), arc_update=arc_line(dev, args))
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -548,6 +548,52 @@ def kd_line(dev, args):
                mean_loss=float(res[0].mean().item()))
     ctx.close()
     return out
+
+
+def arc_line(dev, args):
+    """N1: one OOV event through the ARC dynamic buffer (capacity 256, paper
+    defaults; host) and the incremental device update of the llama subset
+    (static 32,768 + the buffer's 256, <= 32 insertions per event) -- against the full
+    rebuild it replaces."""
+    import torch
+    import paper_2605_27390_b200 as es
+    rng = np.random.default_rng(41)
+    V = 128256
+    static = np.sort(rng.choice(V, 32768, replace=False)).astype(np.int32)
+    pool = np.setdiff1d(np.arange(V), static)
+    arc = es.Arc(256)
+    t_host, n_ev = 0.0, 0
+    events = []
+    for step in range(400):
+        toks = rng.choice(pool[:4000], 32, replace=False).astype(np.int32)
+        before = set(arc.members())
+        t0 = time.perf_counter()
+        arc.admit(toks, step)
+        t_host += time.perf_counter() - t0
+        n_ev += 1
+        after = set(arc.members())
+        events.append((np.array(sorted(after - before), np.int32), np.array(sorted(before - after), np.int32)))
+    S = torch.from_numpy(np.union1d(static, np.array(arc.members(), np.int32)).astype(np.int32)).to(dev)
+    add, rem = events[-1]
+    # a full-sized delta: 32 in, 32 out of a 36,864-id subset
+    rem = S[torch.randperm(S.numel(), device=dev)[:32]].sort().values
+    cand = torch.from_numpy(np.setdiff1d(np.arange(V), S.cpu().numpy())[:32].astype(np.int32)).to(dev)
+    res = None
+    for _ in range(args.warmup):
+        res = es.subset_update(S, rem, cand)
+    reps = 50
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        res = es.subset_update(S, rem, cand, out=None)
+    e1.record()
+    torch.cuda.synchronize()
+    arc.close()
+    return dict(workload="ARC capacity 256 (p0 128, ghosts 256/256, residency 8, warm-up 50), 32-token OOV events; "
+                         "device update of the static 32,768 + ARC 256 subset with 32 in / 32 out (vs a full rebuild: "
+                         "scan + select + union + emit, breakdown above)",
+                arc_host_us_per_event=t_host / n_ev * 1e6, update_us=e0.elapsed_time(e1) * 1e3 / reps,
+                n_S=int(S.numel()))
 
 
 def verify_parity_cpu_leg(vl):

@@ -326,6 +326,43 @@ evospec_status evospec_kd_loss(evospec_ctx *ctx, int32_t B, int32_t g, int32_t K
     const float *draft_logits, const int32_t *verified, float T_kd, float beta,
     float *loss, float *grad, float *weights, void *stream);
 
+/* ---- N1: ARC dynamic buffer + incremental subset update ---- */
+
+/* The dynamic buffer's Adaptive Replacement Cache (App. A.3;
+ * SPEC S:288-348): resident lists T1 / T2 (|T1| + |T2| <= capacity = N_dyn),
+ * ghost lists B1 / B2, adaptive target p. Host-side, single writer;
+ * no GPU needed. Paper defaults: capacity 256, p0 128, ghost caps
+ * 256 / 256, min residency 8 decoding steps, warm-up 50 events.
+ *   touch:  a T1 / T2 member moves to the MRU end of T2; returns 1 on a hit.
+ *   admit:  one OOV event (the warm-up counts events): each token (a
+ *           deduplicated list) is touched if resident; a B1 ghost raises p by
+ *           max(1, |B2| / |B1|), a B2 ghost lowers it by max(1, |B1| / |B2|)
+ *           (after warm-up; integer division) and lands in T2; otherwise it
+ *           lands in T1. An insertion into a full cache first evicts one
+ *           member: from T1 if |T1| > p (or T2 empty), else T2; the LRU-most
+ *           member resident >= min_residency steps since its admission, else
+ *           the other list's, else plain LRU of the chosen list. Evicted ids
+ *           (in order) go to evicted[] (capacity n) and to B1 / B2.
+ *   state:  [|T1|, |T2|, |B1|, |B2|, p, T1..., T2..., B1..., B2...], each list
+ *           LRU -> MRU (trace-equivalence testing).
+ * EVOSPEC_EINPUT on null / out-of-range arguments. */
+typedef struct evospec_arc evospec_arc;
+evospec_status evospec_arc_create(evospec_arc **out, int32_t capacity, int32_t p0, int32_t b1_cap, int32_t b2_cap,
+    int32_t min_residency, int32_t warmup_events);
+evospec_status evospec_arc_destroy(evospec_arc *arc);
+int32_t        evospec_arc_touch(evospec_arc *arc, int32_t token, int64_t step);
+evospec_status evospec_arc_admit(evospec_arc *arc, const int32_t *tokens, int32_t n, int64_t step,
+    int32_t *evicted, int32_t *n_evicted);
+evospec_status evospec_arc_state(const evospec_arc *arc, int32_t *out, int32_t cap, int32_t *n_out);
+
+/* Incremental update of the sorted active vocabulary on the device (no full
+ * rebuild): out = sort((subset \ removed) u added). subset [n] sorted unique;
+ * removed [n_removed] sorted, a subset of `subset`; added [n_added] sorted,
+ * disjoint from subset \ removed; out [n - n_removed + n_added] and n_out [1]
+ * device. One kernel (per-element binary searches). Async on `stream`. */
+evospec_status evospec_subset_update(const int32_t *subset, int32_t n, const int32_t *removed, int32_t n_removed,
+    const int32_t *added, int32_t n_added, int32_t *out, int32_t *n_out, void *stream);
+
 /* ---- one draft step through the whole path -------------------------------- */
 
 /* Per-step I/O for evospec_draft_step. `host_io` = 1: q, H, seeds, ctx and

@@ -307,3 +307,58 @@ def kd_loss(zp, zq, verified, *, T: float = 1.0, beta: float = 0.3):
                   C.c_void_p, C.c_void_p, C.c_void_p]
     _check(f(B, g, K, _p(zp), _p(zq), _p(v), float(T), float(beta), _p(J), _p(grad), _p(w)), "kd_loss")
     return J, grad, w
+
+
+class Arc:
+    """N1: the oracle ARC dynamic buffer (eo_arc_*), one instance = one cache state."""
+
+    def __init__(self, c: int, *, p0: int = 128, b1cap: int = 256, b2cap: int = 256, min_res: int = 8,
+                 warmup: int = 50):
+        L = _L()
+        L.eo_arc_size.restype = C.c_size_t
+        self._buf = C.create_string_buffer(int(L.eo_arc_size()))
+        L.eo_arc_init.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int]
+        _check(L.eo_arc_init(self._buf, c, p0, b1cap, b2cap, min_res, warmup), "arc_init")
+        self.c = c
+
+    def touch(self, token: int, step: int) -> bool:
+        f = _L().eo_arc_touch
+        f.argtypes = [C.c_void_p, C.c_int32, C.c_int64]
+        return bool(f(self._buf, int(token), int(step)))
+
+    def admit(self, tokens, step: int) -> list:
+        t = _i32(np.asarray(tokens, dtype=np.int32).reshape(-1))
+        ev = np.zeros(max(1, t.size), np.int32)
+        ne = C.c_int(0)
+        f = _L().eo_arc_admit
+        f.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int64, C.c_void_p, C.c_void_p]
+        _check(f(self._buf, _p(t), int(t.size), int(step), _p(ev), C.byref(ne)), "arc_admit")
+        return ev[:ne.value].tolist()
+
+    def state(self) -> dict:
+        out = np.zeros(5 + 4 * 4096, np.int32)
+        f = _L().eo_arc_state
+        f.argtypes = [C.c_void_p, C.c_void_p, C.c_int]
+        _check(f(self._buf, _p(out), int(out.size)), "arc_state")
+        n1, n2, nb1, nb2, p = (int(x) for x in out[:5])
+        o = 5
+        lists = []
+        for n in (n1, n2, nb1, nb2):
+            lists.append(out[o:o + n].tolist())
+            o += n
+        return dict(T1=lists[0], T2=lists[1], B1=lists[2], B2=lists[3], p=p)
+
+    def members(self) -> list:
+        s = self.state()
+        return sorted(s["T1"] + s["T2"])
+
+
+def subset_update(S, remove, add):
+    """N1: S' = sort((S minus remove) union add) (eo_subset_update)."""
+    S, r, a = (_i32(np.asarray(x, dtype=np.int32).reshape(-1)) for x in (S, remove, add))
+    out = np.zeros(S.size + a.size, np.int32)
+    n = C.c_int(0)
+    f = _L().eo_subset_update
+    f.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]
+    _check(f(_p(S), int(S.size), _p(r), int(r.size), _p(a), int(a.size), _p(out), C.byref(n)), "subset_update")
+    return out[:n.value].copy()

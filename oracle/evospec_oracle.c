@@ -573,3 +573,177 @@ int eo_kd_loss(int B, int g, int K, const float *zp, const float *zq, const int3
     free(ph);
     return EO_OK;
 }
+
+/* ------------------------------------------------------------------ */
+/* N1: the dynamic buffer's Adaptive Replacement Cache */
+/* (App. A.3) and the incremental   */
+/* subset update it drives.                                           */
+/* Lists are arrays in LRU -> MRU order. Residents carry the step of  */
+/* their admission (reading A1: residency counts from admission;      */
+/* promotions keep it).                                                */
+/*   touch(t): t in T1 -> T2 MRU; t in T2 -> T2 MRU; else miss.        */
+/*   admit(tokens, step) = one OOV event (warm-up counts events):      */
+/*     resident -> touch; in B1 -> (after warm-up) p = min(c, p +      */
+/*     max(1, |B2| / |B1|)), to T2; in B2 -> (after warm-up) p = max(0, */
+/*     p - max(1, |B1| / |B2|)), to T2; else to T1 (MRU). Before an    */
+/*     insertion into a full cache one eviction: from T1 if |T1| > p   */
+/*     (or T2 is empty), else from T2; within the list the LRU-most    */
+/*     member resident >= min_res steps; if that list has none, the    */
+/*     other list's (reading A2); if nobody has, plain LRU of the      */
+/*     chosen list. Evicted tokens go to B1 / B2 (MRU), ghost  */
+/*     lists trimmed at their LRU end to their caps. Integer division  */
+/*     in the adaptation deltas (p is an integer).              */
+/* ------------------------------------------------------------------ */
+#define EO_ARC_MAX 4096
+typedef struct {
+    int c, p, b1cap, b2cap, min_res, warmup, events;
+    int n1, n2, nb1, nb2;
+    int32_t t1[EO_ARC_MAX], t2[EO_ARC_MAX], b1[EO_ARC_MAX], b2[EO_ARC_MAX];
+    int64_t s1[EO_ARC_MAX], s2[EO_ARC_MAX];   /* admission steps of T1 / T2 members */
+} eo_arc;
+
+static int eo_arc_find(const int32_t *a, int n, int32_t t) {
+    for (int i = 0; i < n; ++i) if (a[i] == t) return i;
+    return -1;
+}
+static void eo_arc_del(int32_t *a, int64_t *s, int *n, int i) {
+    for (int k = i; k + 1 < *n; ++k) { a[k] = a[k + 1]; if (s) s[k] = s[k + 1]; }
+    (*n)--;
+}
+static void eo_arc_push(int32_t *a, int64_t *s, int *n, int32_t t, int64_t st) {
+    a[*n] = t;
+    if (s) s[*n] = st;
+    (*n)++;
+}
+static void eo_arc_ghost(int32_t *g, int *n, int cap, int32_t t) {
+    eo_arc_push(g, NULL, n, t, 0);
+    while (*n > cap) eo_arc_del(g, NULL, n, 0);
+}
+
+size_t eo_arc_size(void) { return sizeof(eo_arc); }
+
+int eo_arc_init(eo_arc *a, int c, int p0, int b1cap, int b2cap, int min_res, int warmup) {
+    if (!a || c < 1 || c > EO_ARC_MAX || b1cap < 0 || b1cap > EO_ARC_MAX || b2cap < 0 || b2cap > EO_ARC_MAX ||
+        min_res < 0 || warmup < 0)
+        return EO_EINPUT;
+    memset(a, 0, sizeof(*a));
+    a->c = c; a->p = p0 < 0 ? 0 : (p0 > c ? c : p0);
+    a->b1cap = b1cap; a->b2cap = b2cap; a->min_res = min_res; a->warmup = warmup;
+    return EO_OK;
+}
+
+int eo_arc_touch(eo_arc *a, int32_t t, int64_t step) {
+    (void)step;
+    int i = eo_arc_find(a->t1, a->n1, t);
+    if (i >= 0) {
+        int64_t s = a->s1[i];
+        eo_arc_del(a->t1, a->s1, &a->n1, i);
+        eo_arc_push(a->t2, a->s2, &a->n2, t, s);
+        return 1;
+    }
+    i = eo_arc_find(a->t2, a->n2, t);
+    if (i >= 0) {
+        int64_t s = a->s2[i];
+        eo_arc_del(a->t2, a->s2, &a->n2, i);
+        eo_arc_push(a->t2, a->s2, &a->n2, t, s);
+        return 1;
+    }
+    return 0;
+}
+
+/* the LRU-most member of list (a, s, n) resident >= min_res at step; -1 if none */
+static int eo_arc_eligible(const eo_arc *A, const int64_t *s, int n, int64_t step) {
+    for (int i = 0; i < n; ++i) if (step - s[i] >= A->min_res) return i;
+    return -1;
+}
+
+static int32_t eo_arc_evict(eo_arc *A, int64_t step) {
+    int from1 = (A->n1 > 0 && (A->n1 > A->p || A->n2 == 0));
+    int i = from1 ? eo_arc_eligible(A, A->s1, A->n1, step) : eo_arc_eligible(A, A->s2, A->n2, step);
+    if (i < 0) {   /* reading A2: the other list's eligible member, else plain LRU of the chosen list */
+        int j = from1 ? eo_arc_eligible(A, A->s2, A->n2, step) : eo_arc_eligible(A, A->s1, A->n1, step);
+        if (j >= 0) { from1 = !from1; i = j; } else i = 0;
+    }
+    int32_t t;
+    if (from1) {
+        t = A->t1[i];
+        eo_arc_del(A->t1, A->s1, &A->n1, i);
+        eo_arc_ghost(A->b1, &A->nb1, A->b1cap, t);
+    } else {
+        t = A->t2[i];
+        eo_arc_del(A->t2, A->s2, &A->n2, i);
+        eo_arc_ghost(A->b2, &A->nb2, A->b2cap, t);
+    }
+    return t;
+}
+
+int eo_arc_admit(eo_arc *A, const int32_t *tokens, int n, int64_t step, int32_t *evicted, int *n_evicted) {
+    if (!A || n < 0 || (n > 0 && !tokens) || !n_evicted) return EO_EINPUT;
+    A->events++;
+    const int adapt = A->events > A->warmup;
+    int ne = 0;
+    for (int k = 0; k < n; ++k) {
+        int32_t t = tokens[k];
+        if (eo_arc_touch(A, t, step)) continue;
+        int to2 = 0, i;
+        if ((i = eo_arc_find(A->b1, A->nb1, t)) >= 0) {
+            if (adapt) {
+                int d = A->nb2 / A->nb1; if (d < 1) d = 1;
+                A->p = A->p + d > A->c ? A->c : A->p + d;
+            }
+            eo_arc_del(A->b1, NULL, &A->nb1, i);
+            to2 = 1;
+        } else if ((i = eo_arc_find(A->b2, A->nb2, t)) >= 0) {
+            if (adapt) {
+                int d = A->nb1 / A->nb2; if (d < 1) d = 1;
+                A->p = A->p - d < 0 ? 0 : A->p - d;
+            }
+            eo_arc_del(A->b2, NULL, &A->nb2, i);
+            to2 = 1;
+        }
+        if (A->n1 + A->n2 >= A->c) {
+            int32_t e = eo_arc_evict(A, step);
+            if (evicted) evicted[ne] = e;
+            ne++;
+        }
+        if (to2) eo_arc_push(A->t2, A->s2, &A->n2, t, step);
+        else eo_arc_push(A->t1, A->s1, &A->n1, t, step);
+    }
+    *n_evicted = ne;
+    return EO_OK;
+}
+
+/* state dump: n1, n2, nb1, nb2, p followed by the four lists (LRU -> MRU) */
+int eo_arc_state(const eo_arc *A, int32_t *out, int cap) {
+    int need = 5 + A->n1 + A->n2 + A->nb1 + A->nb2;
+    if (!out || cap < need) return EO_EINPUT;
+    int o = 0;
+    out[o++] = A->n1; out[o++] = A->n2; out[o++] = A->nb1; out[o++] = A->nb2; out[o++] = A->p;
+    for (int i = 0; i < A->n1; ++i) out[o++] = A->t1[i];
+    for (int i = 0; i < A->n2; ++i) out[o++] = A->t2[i];
+    for (int i = 0; i < A->nb1; ++i) out[o++] = A->b1[i];
+    for (int i = 0; i < A->nb2; ++i) out[o++] = A->b2[i];
+    return EO_OK;
+}
+
+/* incremental subset update: S' = sort((S \ remove) u add), S sorted unique,
+ * remove a subset of S, add disjoint from S \ remove (the definition, sorted). */
+static int eo_cmp_i32b(const void *a, const void *b) {
+    int32_t x = *(const int32_t *)a, y = *(const int32_t *)b;
+    return (x > y) - (x < y);
+}
+int eo_subset_update(const int32_t *S, int n, const int32_t *rem, int nr, const int32_t *add, int na,
+                     int32_t *out, int *n_out) {
+    if ((n > 0 && !S) || (nr > 0 && !rem) || (na > 0 && !add) || !out || !n_out) return EO_EINPUT;
+    int o = 0;
+    for (int i = 0; i < n; ++i) {
+        int gone = 0;
+        for (int j = 0; j < nr; ++j) if (rem[j] == S[i]) { gone = 1; break; }
+        if (!gone) out[o++] = S[i];
+    }
+    for (int j = 0; j < na; ++j) out[o++] = add[j];
+    qsort(out, (size_t)o, sizeof(int32_t), eo_cmp_i32b);
+    for (int i = 1; i < o; ++i) if (out[i - 1] == out[i]) return EO_EINPUT;   /* add not disjoint */
+    *n_out = o;
+    return EO_OK;
+}

@@ -29,6 +29,8 @@ EXPORTED = [
     "evospec_draft_step", "evospec_set_timing", "evospec_read_stats", "evospec_read_trace",
     "evospec_build_subset_batched", "evospec_subset_logits_topk_ragged", "evospec_subset_logits_topk_merged",
     "evospec_verify_chain", "evospec_coverage", "evospec_kd_loss",
+    "evospec_arc_create", "evospec_arc_destroy", "evospec_arc_touch", "evospec_arc_admit", "evospec_arc_state",
+    "evospec_subset_update",
 ]
 
 STAGES = ["scan", "select", "union", "lmh", "finalize", "merge", "copy"]
@@ -102,6 +104,12 @@ def lib() -> C.CDLL:
             "evospec_verify_chain": ([vp, vp, i32, i32, vp, vp, i32, vp, C.c_float, i32, vp, vp, vp, vp, vp], i32),
             "evospec_coverage": ([vp, vp, i32, i32, vp, i32, C.c_float, vp, i32, vp, vp, vp], i32),
             "evospec_kd_loss": ([vp, i32, i32, i32, vp, vp, vp, C.c_float, C.c_float, vp, vp, vp, vp], i32),
+            "evospec_arc_create": ([vp, i32, i32, i32, i32, i32, i32], i32),
+            "evospec_arc_destroy": ([vp], i32),
+            "evospec_arc_touch": ([vp, i32, i64], i32),
+            "evospec_arc_admit": ([vp, vp, i32, i64, vp, vp], i32),
+            "evospec_arc_state": ([vp, vp, i32, vp], i32),
+            "evospec_subset_update": ([vp, i32, vp, i32, vp, i32, vp, vp, vp], i32),
             "evospec_draft_step": ([vp, C.POINTER(StepIO), vp], i32),
             "evospec_set_timing": ([vp, C.c_int], i32),
             "evospec_read_stats": ([vp, C.POINTER(Stats)], i32),
@@ -147,6 +155,69 @@ def _dtype_code(t) -> int:
     if t == torch.float32:
         return FP32
     raise TypeError(f"unsupported dtype {t} (bf16 or fp32)")
+
+
+class Arc:
+    """N1: the dynamic buffer's ARC (evospec_arc_*; host-side, no GPU needed). Paper defaults:
+    capacity 256, p0 128, ghost caps 256 / 256, min residency 8 steps, warm-up 50 events."""
+
+    def __init__(self, capacity: int = 256, *, p0: int = 128, b1_cap: int = 256, b2_cap: int = 256,
+                 min_residency: int = 8, warmup_events: int = 50):
+        h = C.c_void_p()
+        _check(lib().evospec_arc_create(C.byref(h), capacity, p0, b1_cap, b2_cap, min_residency, warmup_events))
+        self._h = h
+        self.capacity = capacity
+
+    _h = None   # (set only once creation succeeded)
+
+    def close(self):
+        if self._h:
+            lib().evospec_arc_destroy(self._h)
+            self._h = None
+
+    __del__ = close
+
+    def touch(self, token: int, step: int) -> bool:
+        return bool(lib().evospec_arc_touch(self._h, int(token), int(step)))
+
+    def admit(self, tokens, step: int) -> list:
+        import numpy as np
+        t = np.ascontiguousarray(np.asarray(tokens, dtype=np.int32).reshape(-1))
+        ev = np.zeros(max(1, t.size), np.int32)
+        ne = C.c_int32(0)
+        _check(lib().evospec_arc_admit(self._h, t.ctypes.data_as(C.c_void_p), int(t.size), int(step),
+                                       ev.ctypes.data_as(C.c_void_p), C.byref(ne)))
+        return ev[:ne.value].tolist()
+
+    def state(self) -> dict:
+        import numpy as np
+        out = np.zeros(5 + 4 * max(self.capacity, 1) + 2 * 65536, np.int32)
+        n = C.c_int32(0)
+        _check(lib().evospec_arc_state(self._h, out.ctypes.data_as(C.c_void_p), int(out.size), C.byref(n)))
+        n1, n2, nb1, nb2, p = (int(x) for x in out[:5])
+        o, lists = 5, []
+        for k in (n1, n2, nb1, nb2):
+            lists.append(out[o:o + k].tolist())
+            o += k
+        return dict(T1=lists[0], T2=lists[1], B1=lists[2], B2=lists[3], p=p)
+
+    def members(self) -> list:
+        s = self.state()
+        return sorted(s["T1"] + s["T2"])
+
+
+def subset_update(subset, removed, added, *, out=None, stream=None):
+    """N1: out = sort((subset minus removed) union added) on the device (evospec_subset_update).
+    All int32 device tensors, removed / added sorted. Returns (out, n_out)."""
+    import torch
+    n_new = subset.numel() - removed.numel() + added.numel()
+    if out is None:
+        out = (torch.empty(max(1, n_new), dtype=torch.int32, device=subset.device),
+               torch.empty(1, dtype=torch.int32, device=subset.device))
+    o, n = out
+    _check(lib().evospec_subset_update(_ptr(subset), int(subset.numel()), _ptr(removed), int(removed.numel()),
+                                       _ptr(added), int(added.numel()), _ptr(o), _ptr(n), _stream(stream)))
+    return o[:n_new], n
 
 
 class Context:

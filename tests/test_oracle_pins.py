@@ -697,3 +697,86 @@ def test_kd_curriculum_limits():
     zq[0, 0, 0] = -60.0                             # very unconfident: weights decay fast
     _, _, w = oracle.kd_loss(zp, zq, [0], beta=0.3)
     assert w[0, 0] == 1.0 and w[0, 1] < 1e-7
+
+
+# ---------------------------------------------------------------- N1 ARC + update
+# Pins for oracle.Arc (eo_arc_*): the SPEC worked examples, the
+# invariants of S:295-299 / S:332-337 on random traces, and operation-for-
+# operation equality with an independently written simulator (tests/brute.py
+# ArcSim); oracle.subset_update against numpy set operations.
+
+def test_arc_spec_examples():
+    import oracle
+    a = oracle.Arc(4, p0=0, min_res=0, warmup=0)
+    assert a.admit([7], 0) == [] and a.state()["T1"] == [7]
+    a = oracle.Arc(2, p0=0, min_res=0, warmup=0)                                  # S:319 (canonical p0 = 0)
+    x, y, z = 10, 20, 30
+    assert a.admit([x], 0) == [] and a.admit([y], 1) == []
+    assert a.touch(x, 2)
+    assert a.admit([z], 3) == [y]
+    st = a.state()
+    assert st["T1"] == [z] and st["T2"] == [x] and st["B1"] == [y]
+    p_before = st["p"]                                                            # ghost re-admit
+    assert a.admit([y], 4) != []
+    st = a.state()
+    assert y in st["T2"] and st["p"] > p_before
+    b = oracle.Arc(8, min_res=0, warmup=0)
+    b.admit([3, 9], 0)
+    assert b.members() == [3, 9]
+    assert not oracle.Arc(2).touch(5, 0)
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_arc_invariants_and_independent_simulator(seed):
+    import oracle
+    rng = np.random.default_rng(40 + seed)
+    c, V = 16, 60
+    kw = dict(p0=8, b1cap=10, b2cap=7, min_res=3 if seed % 2 else 0, warmup=5 if seed >= 2 else 0)
+    a = oracle.Arc(c, **kw)
+    sim = brute.ArcSim(c, kw["p0"], kw["b1cap"], kw["b2cap"], kw["min_res"], kw["warmup"])
+    admitted_at = {}
+    for step in range(300):
+        if rng.random() < 0.5:
+            t = int(rng.integers(V))
+            assert a.touch(t, step) == sim.touch(t)
+        else:
+            toks = [int(t) for t in rng.choice(V, int(rng.integers(1, 6)), replace=False)]
+            ev = a.admit(toks, step)
+            assert ev == sim.admit(toks, step)
+            for t in toks:
+                admitted_at.setdefault(t, step)
+            for t in ev:
+                # min residency unless every resident was under-resident
+                if step - admitted_at[t] < kw["min_res"]:
+                    st = a.state()
+                    assert all(step - admitted_at.get(u, step) < kw["min_res"] for u in st["T1"] + st["T2"])
+                admitted_at.pop(t, None)
+            for t in toks:
+                admitted_at.setdefault(t, step)
+        st = a.state()
+        assert st == sim.state()
+        res = st["T1"] + st["T2"]
+        assert len(res) <= c and len(set(res)) == len(res)
+        assert not (set(res) & set(st["B1"] + st["B2"]))
+        assert len(st["B1"]) <= kw["b1cap"] and len(st["B2"]) <= kw["b2cap"]
+        assert 0 <= st["p"] <= c
+
+
+def test_arc_warmup_freezes_p():
+    import oracle
+    a = oracle.Arc(2, p0=1, min_res=0, warmup=100)
+    for s, t in enumerate([1, 2, 3, 4, 1, 2, 3, 4, 1, 2]):
+        a.admit([t], s)
+    assert a.state()["p"] == 1
+
+
+def test_subset_update_matches_set_ops():
+    import oracle
+    rng = np.random.default_rng(8)
+    S = np.sort(rng.choice(10000, 3000, replace=False)).astype(np.int32)
+    rem = np.sort(rng.choice(S, 40, replace=False)).astype(np.int32)
+    add = np.sort(rng.choice(np.setdiff1d(np.arange(10000), S), 25, replace=False)).astype(np.int32)
+    out = oracle.subset_update(S, rem, add)
+    np.testing.assert_array_equal(out, np.union1d(np.setdiff1d(S, rem), add))
+    with pytest.raises(ValueError):
+        oracle.subset_update(S, [], S[:1])                                        # not disjoint
