@@ -152,7 +152,7 @@ ES_DEV void fin32_row(const LmhArgs& a, const int r, int n_cta_arg, int k, float
     float* cand_v = sm.cand_v; int* cand_p = sm.cand_p;
     float* c_v = sm.c_v; int32_t* c_id = sm.c_id; int32_t* c_gid = sm.c_gid; double* c_e = sm.c_e;
     int* need_list = sm.need_list;
-    int& n_need_s = sm.scal[0]; int& nk_s = sm.scal[1]; int& tot_s = sm.scal[2]; int& cand_n = sm.scal[3];
+    int& n_need_s = sm.scal[0]; int& nk_s = sm.scal[1]; int& cand_n = sm.scal[3];
     float& lse_s = sm.fscal[0]; float& th_s = sm.fscal[1];
     float* s_head = sm.s_head;
     uint16_t* h_row = sm.h_row;
@@ -201,17 +201,13 @@ ES_DEV void fin32_row(const LmhArgs& a, const int r, int n_cta_arg, int k, float
     const bool h_fast = a.h_dtype == 0 && a.d % 8 == 0 && a.d <= kFin32MaxD;
     double hacc = h_staged ? hacc_pre : fin32_stage_h<NT>(a, r, sm);
     if (threadIdx.x == 0) { cand_n = 0; th_s = -INFINITY; }
-    {
-        int tcnt = 0;
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-            tcnt += (vv[u].x != -INFINITY) + (vv[u].y != -INFINITY) + (vv[u].z != -INFINITY) + (vv[u].w != -INFINITY);
+    {   // (the list entries vv / ii are still in flight: first consumed by the filter,
+        //  so their latency overlaps this and the head threshold below)
         const float Mw = warp_max(cs_ > 0.0f ? cm_ : -INFINITY);
         const float Sw = warp_sum(cs_ > 0.0f ? cs_ * expf(cm_ - Mw) : 0.0f);
         thl = warp_max(thl);
-        tcnt = warp_sum_i(tcnt);
         hacc = warp_sum_d(hacc);
-        if (lane == 0) { w_M[warp] = Mw; w_S[warp] = Sw; w_th[warp] = thl; w_tot[warp] = tcnt; red_d[warp] = hacc; }
+        if (lane == 0) { w_M[warp] = Mw; w_S[warp] = Sw; w_th[warp] = thl; red_d[warp] = hacc; }
     }
     __syncthreads();
     if (threadIdx.x == 0) { FIN_TRACE_R(1); FIN_DT_R(1); }
@@ -256,19 +252,22 @@ ES_DEV void fin32_row(const LmhArgs& a, const int r, int n_cta_arg, int k, float
         const bool have = lane < nwarps && w_S[lane] > 0.0f;
         const float M = warp_max(have ? w_M[lane] : -INFINITY);
         const float S = warp_sum(have ? w_S[lane] * expf(w_M[lane] - M) : 0.0f);
-        const int tot = warp_sum_i(lane < nwarps ? w_tot[lane] : 0);
         if (lane == 0) {
             row_max[r] = M;
             row_sumexp[r] = S;
             lse_s = S > 0.0f ? M + logf(S) : -INFINITY;
-            tot_s = tot;
         }
     }
     {
         auto keep = [&](float x) { return x != -INFINITY && x >= th0; };
-        int nk = 0;
+        int nk = 0, tcnt = 0;
 #pragma unroll
-        for (int u = 0; u < U; ++u) nk += keep(vv[u].x) + keep(vv[u].y) + keep(vv[u].z) + keep(vv[u].w);
+        for (int u = 0; u < U; ++u) {
+            nk += keep(vv[u].x) + keep(vv[u].y) + keep(vv[u].z) + keep(vv[u].w);
+            tcnt += (vv[u].x != -INFINITY) + (vv[u].y != -INFINITY) + (vv[u].z != -INFINITY) + (vv[u].w != -INFINITY);
+        }
+        tcnt = warp_sum_i(tcnt);
+        if (lane == 0) w_tot[warp] = tcnt;
         if (nk) {
             int o = atomicAdd(&cand_n, nk);
             auto put = [&](float x, int id) {
@@ -352,7 +351,7 @@ ES_DEV void fin32_row(const LmhArgs& a, const int r, int n_cta_arg, int k, float
     if (threadIdx.x == 0) { FIN_TRACE_R(3); FIN_DT_R(3); }
     if (warp == 0) {
         // C2. runs: consecutive kept entries closer than 2 delta; those reaching the top k are re-scored
-        const int cnt = nk_s, tot = tot_s;
+        const int cnt = nk_s, tot = warp_sum_i(lane < nwarps ? w_tot[lane] : 0);
         const float Lv = lane < cnt ? c_v[lane] : -INFINITY;
         // position -> vocabulary id (the rank path stored it already)
         if (ncand > kFin32RankMax) c_gid[lane] = lane < cnt ? __ldg(&a.subset[c_id[lane]]) : -1;
