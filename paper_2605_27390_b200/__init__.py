@@ -220,6 +220,41 @@ def subset_update(subset, removed, added, *, out=None, stream=None):
     return o[:n_new], n
 
 
+class DraftStep:
+    """A prepared evospec_draft_step (Context.prepare_draft_step): one ctypes call per run()."""
+
+    def __init__(self, ctx, kw, out, stream):
+        self.ctx, self.out, self._keep = ctx, out, (kw, out)
+        io = StepIO()
+        E, W, st = kw["E"], kw["W_local"], kw["static_ids"]
+        io.E, io.n_e_rows = E.data_ptr(), E.shape[0]
+        io.W_local, io.n_w_rows = W.data_ptr(), W.shape[0]
+        io.static_ids, io.n_static = st.data_ptr(), st.numel()
+        rp, col = kw.get("csr_row_ptr"), kw.get("csr_col")
+        io.csr_row_ptr = None if rp is None else rp.data_ptr()
+        io.csr_col = None if col is None else col.data_ptr()
+        io.build = BuildParams(kw["n_sem"], kw.get("n_graph_sem_seeds", 10), kw.get("per_seed", 8),
+                               kw.get("ctx_min_count", 0), kw.get("n_ctx_max", 0), kw["n_dyn"])
+        H, q, seeds, cx = kw["H"], kw["q"], kw.get("seeds"), kw.get("ctx_ids")
+        io.n_h, io.k, io.inv_temp = H.shape[0], kw["k"], float(kw.get("inv_temp", 1.0))
+        io.q, io.H = q.data_ptr(), H.data_ptr()
+        io.seeds = None if seeds is None else seeds.data_ptr()
+        io.n_seed = 0 if seeds is None else seeds.numel()
+        io.ctx_ids = None if cx is None else cx.data_ptr()
+        io.n_ctx = 0 if cx is None else cx.numel()
+        io.out_ids, io.out_vals, io.out_lse, io.out_probs = (t.data_ptr() for t in out)
+        io.host_io = int(not H.is_cuda)
+        self._io, self._ref = io, C.byref(io)
+        self._st = _stream(stream)
+        self._fn = lib().evospec_draft_step
+
+    def run(self):
+        st = self._fn(self.ctx._h, self._ref, self._st)
+        if st != OK:
+            _check(st)
+        return self.out
+
+
 class Context:
     """Owns an evospec_ctx (device workspace + optional NCCL communicator)."""
 
@@ -498,3 +533,13 @@ class Context:
         io.host_io = int(host_io)
         _check(lib().evospec_draft_step(self._h, C.byref(io), _stream(stream)))
         return out
+
+    def prepare_draft_step(self, *, out=None, stream=None, **kw):
+        """A reusable draft step for a serving loop: the I/O descriptor is marshalled
+        once; each `run()` is one evospec_draft_step call on the same buffers (the
+        caller refills q / H / seeds in place, e.g. pinned host tensors, between
+        steps). Returns a DraftStep whose `.out` holds the outputs."""
+        out = self.draft_step(out=out, stream=stream, **kw)   # one step: also builds / validates the I/O
+        return DraftStep(self, kw, out, stream)
+
+

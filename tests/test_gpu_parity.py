@@ -181,6 +181,33 @@ def test_draft_step_host_io_equals_device_path():
     assert np.max(np.abs(out_h[3].numpy() - ref["triple"]["probs"])) <= G.PROB_TOL
 
 
+def test_prepared_draft_step_refilled_host_buffers():
+    """Context.prepare_draft_step (the serving-loop call bench.py's e2e times): the
+    caller refills the pinned host H / q in place between runs; every run equals the
+    oracle for the current contents."""
+    Ps = [G.make_problem(s, dtype="bf16", V=16000, d=256, n_static=2000, n_sem=300, n_dyn=250, n_h=3, k=10)
+          for s in (9, 10)]
+    P0 = Ps[0]
+    ctx = ctx_for(P0)
+    W = G.to_dev(P0["W"], DEV)
+    ctx.prepare_weights(W)
+    kw = dict(E=W, W_local=W, static_ids=G.to_dev(P0["static"], DEV), csr_row_ptr=G.to_dev(P0["row_ptr"], DEV),
+              csr_col=G.to_dev(P0["col"], DEV), k=P0["k"], n_sem=P0["n_sem"], n_dyn=P0["n_dyn"])
+    H = G.to_dev(P0["H"], "cpu").pin_memory()
+    q = G.to_dev(P0["q"], "cpu").pin_memory()
+    seeds = torch.from_numpy(P0["seeds"]).pin_memory()
+    step = ctx.prepare_draft_step(q=q, H=H, seeds=seeds, **kw)
+    for P in Ps + Ps[:1]:
+        Q = dict(P0, H=P["H"], q=P["q"])       # same weights / graph / static set, new H and q
+        H.copy_(G.to_dev(Q["H"], "cpu"))
+        q.copy_(G.to_dev(Q["q"], "cpu"))
+        out = step.run()
+        torch.cuda.synchronize()
+        ref = G.oracle_step(oracle, Q)
+        np.testing.assert_array_equal(out[0].numpy(), ref["triple"]["ids"])
+        assert np.max(np.abs(out[3].numpy() - ref["triple"]["probs"])) <= G.PROB_TOL
+
+
 def test_input_errors():
     P = G.make_problem(0, dtype="fp32", **TINY)
     ctx = ctx_for(P)
