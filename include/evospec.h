@@ -298,7 +298,8 @@ evospec_status evospec_verify_chain(evospec_ctx *ctx, const float *target_logits
  *   recall[r][t]      = |V_t n top-ks[t](p_r)| / ks[t], the target top-k
  *                       ordered (p desc, id asc)
  * target_logits [n_rows, V] fp32; subset_ids [n_subset] sorted ascending
- * unique (V_t); ks [n_ks] int32 in [1, V], n_ks <= 64; outputs covered_mass
+ * unique (V_t); ks [n_ks] int32 in [1, min(V, 1024)] (device; a larger k
+ * yields NaN), n_ks <= 64; outputs covered_mass
  * [n_rows] and recall [n_rows, n_ks] fp64 (device). Async, one launch.
  * EVOSPEC_EINPUT on null / out-of-range host arguments. */
 evospec_status evospec_coverage(evospec_ctx *ctx, const float *target_logits, int32_t n_rows, int32_t V,

@@ -6,12 +6,14 @@
 // Row r (one CTA per row): p_r(v) = exp(z_r[v] it - m_r) / s_r over [0, V),
 // fp64; mass_r = sum_{v in S} p_r(v); recall_r[k] = |S n top-k(p_r)| / k with
 // top-k by (p desc, id asc) -- p orders as the fp32 logit (it > 0), so the
-// top-k boundary is found exactly on the logits: a block radix select (8-bit
-// digits of the monotone float key, 4 passes) gives the k-th largest key tau;
-// among the elements equal to tau the smaller ids win, found by a second radix
-// select on ~id over the tied elements only when the boundary is tied. Then one
-// pass over S counts its members above the boundary. HBM: V fp32 per row once
-// (the further passes hit L2) plus the n_S gathered logits.
+// top-k boundary is found exactly on the logits: one block radix select (8-bit
+// digits of the monotone float key, 4 passes) gives the K-th largest key tau for
+// K = max(ks); among the elements equal to tau the smaller ids win (a second
+// radix select on ~id over the tied elements, only when the boundary is tied).
+// The K elements above the boundary are ranked exactly by counting and tested
+// for membership in S by binary search; Recall@k is a prefix count over ranks.
+// HBM: V fp32 per row once (the further passes hit L2) plus the n_S gathered
+// logits.
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -20,8 +22,13 @@ namespace es {
 constexpr int kCovThreads = 1024;
 constexpr int kCovWarps = kCovThreads / 32;
 
+constexpr int kCovMaxK = 1024;   // largest k of Recall@k (the header's bound)
+
 struct CovSmem {
     uint32_t hist[256];
+    uint32_t top_key[kCovMaxK];
+    int top_id[kCovMaxK];
+    int hit_at[kCovMaxK];
     double red_d[kCovWarps];
     float red_f[kCovWarps];
     int red_i[kCovWarps];
@@ -96,6 +103,7 @@ ES_DEV uint32_t cov_select(int V, int K, KeyFn KEY, CovSmem& sm) {
             }
             uint32_t run = incl - tot;   // count in the bins above this lane's
             const int need = sm.s_need;
+            __syncwarp();                // every lane has read s_need before one lane updates it
             for (int i = 0; i < 8; ++i) {
                 if ((int)run < need && (int)(run + c[i]) >= need) {
                     const uint32_t bin = 255u - (uint32_t)(lane * 8 + i);
@@ -142,35 +150,70 @@ coverage_kernel(const float* __restrict__ z, int V, const int32_t* __restrict__ 
     for (int i = tid; i < n_S; i += kCovThreads) lm += exp((double)__ldg(&zr[__ldg(&S[i])]) * it - M);
     const double cm = cov_block_sum(lm, sm) / s;
     if (tid == 0) mass[r] = cm;
-    // 3. Recall@k: the top-k boundary (tau, iota) and the members of S above it
-    for (int t = 0; t < n_ks; ++t) {
-        const int K = __ldg(&ks[t]);
-        const uint32_t tau = cov_select(V, K, [&](int v, uint32_t& key) { key = float_key(__ldg(&zr[v])); return true; }, sm);
-        int gt = 0, eq = 0;
-        for (int v = tid; v < V; v += kCovThreads) {
-            const uint32_t key = float_key(__ldg(&zr[v]));
-            gt += key > tau;
-            eq += key == tau;
+    // 3. Recall@k: ONE selection of the K = max(ks) boundary (tau, iota); the (at
+    //    most kCovMaxK) elements above it are gathered, ranked exactly by counting
+    //    under (key desc, id asc), tested for membership in S by binary search, and
+    //    Recall@k for every k is the member count among ranks < k.
+    if (n_ks == 0) return;
+    int K = 0;
+    for (int t = 0; t < n_ks; ++t) K = max(K, __ldg(&ks[t]));
+    if (K < 1 || K > kCovMaxK || K > V) {   // outside the header's range: NaN
+        if (tid < n_ks) recall[(size_t)r * n_ks + tid] = __longlong_as_double(0x7ff8000000000000ll);
+        return;
+    }
+    const uint32_t tau = cov_select(V, K, [&](int v, uint32_t& key) { key = float_key(__ldg(&zr[v])); return true; }, sm);
+    int gt = 0, eq = 0;
+    for (int v = tid; v < V; v += kCovThreads) {
+        const uint32_t key = float_key(__ldg(&zr[v]));
+        gt += key > tau;
+        eq += key == tau;
+    }
+    gt = cov_block_count(gt, sm);
+    eq = cov_block_count(eq, sm);
+    uint32_t iota = 0xFFFFFFFFu;   // tied at tau: the (K - gt) smallest ids win
+    if (eq > K - gt) {
+        const uint32_t t2 = cov_select(V, K - gt, [&](int v, uint32_t& key) {
+            key = 0xFFFFFFFFu - (uint32_t)v;
+            return float_key(__ldg(&zr[v])) == tau;
+        }, sm);
+        iota = 0xFFFFFFFFu - t2;
+    }
+    if (tid == 0) sm.s_cnt = 0;
+    __syncthreads();
+    for (int v = tid; v < V; v += kCovThreads) {
+        const uint32_t key = float_key(__ldg(&zr[v]));
+        if (key > tau || (key == tau && (uint32_t)v <= iota)) {
+            const int slot = atomicAdd(&sm.s_cnt, 1);
+            if (slot < kCovMaxK) { sm.top_key[slot] = key; sm.top_id[slot] = v; }
         }
-        gt = cov_block_count(gt, sm);
-        eq = cov_block_count(eq, sm);
-        // tied at tau: the (K - gt) smallest ids win -- iota = the largest winning id
-        uint32_t iota = 0xFFFFFFFFu;
-        if (eq > K - gt) {
-            const uint32_t t2 = cov_select(V, K - gt, [&](int v, uint32_t& key) {
-                key = 0xFFFFFFFFu - (uint32_t)v;
-                return float_key(__ldg(&zr[v])) == tau;
-            }, sm);
-            iota = 0xFFFFFFFFu - t2;
+    }
+    __syncthreads();
+    const int nt = min(sm.s_cnt, kCovMaxK);   // == K
+    for (int i = tid; i < kCovMaxK; i += kCovThreads) sm.hit_at[i] = 0;
+    __syncthreads();
+    for (int i = tid; i < nt; i += kCovThreads) {
+        const uint32_t ki = sm.top_key[i];
+        const int vi = sm.top_id[i];
+        int rank = 0;
+        for (int j = 0; j < nt; ++j) {
+            const uint32_t kj = sm.top_key[j];
+            rank += kj > ki || (kj == ki && sm.top_id[j] < vi);
         }
-        int hit = 0;
-        for (int i = tid; i < n_S; i += kCovThreads) {
-            const int v = __ldg(&S[i]);
-            const uint32_t key = float_key(__ldg(&zr[v]));
-            hit += key > tau || (key == tau && (uint32_t)v <= iota);
+        int lo = 0, hi = n_S;   // membership of vi in the sorted S
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (__ldg(&S[mid]) < vi) lo = mid + 1; else hi = mid;
         }
-        hit = cov_block_count(hit, sm);
-        if (tid == 0) recall[(size_t)r * n_ks + t] = (double)hit / (double)K;
+        sm.hit_at[rank] = (lo < n_S && __ldg(&S[lo]) == vi) ? 1 : 0;
+    }
+    __syncthreads();
+    if (wid == 0) {   // prefix counts over ranks, one lane per k
+        for (int t = lane; t < n_ks; t += 32) {
+            const int k = __ldg(&ks[t]);
+            int hit = 0;
+            for (int i = 0; i < k; ++i) hit += sm.hit_at[i];
+            recall[(size_t)r * n_ks + t] = (double)hit / (double)k;
+        }
     }
 }
 

@@ -280,7 +280,12 @@ sem_scan_tma_kernel(const uint16_t* __restrict__ E, int64_t n_rows, int d, const
         for (int r = 0; r < kScanRowsPerStage; ++r)
             u[r] = r < nr ? *(const uint4*)(st + (size_t)r * row_bytes) : make_uint4(0, 0, 0, 0);
         __syncwarp();
-        if (lane == 0) s_mbar_arrive(&empty[slot]);
+        // the generic-proxy reads of the slot are ordered before the async-proxy
+        // (bulk copy) refill that the release lets the producer issue
+        if (lane == 0) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            s_mbar_arrive(&empty[slot]);
+        }
         double acc[kScanRowsPerStage];
 #pragma unroll
         for (int r = 0; r < kScanRowsPerStage; ++r) {
