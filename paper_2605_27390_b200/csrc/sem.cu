@@ -279,13 +279,11 @@ sem_scan_tma_kernel(const uint16_t* __restrict__ E, int64_t n_rows, int d, const
 #pragma unroll
         for (int r = 0; r < kScanRowsPerStage; ++r)
             u[r] = r < nr ? *(const uint4*)(st + (size_t)r * row_bytes) : make_uint4(0, 0, 0, 0);
-        __syncwarp();
-        // the generic-proxy reads of the slot are ordered before the async-proxy
+        // every lane orders its generic-proxy reads of the slot before the async-proxy
         // (bulk copy) refill that the release lets the producer issue
-        if (lane == 0) {
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            s_mbar_arrive(&empty[slot]);
-        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) s_mbar_arrive(&empty[slot]);
         double acc[kScanRowsPerStage];
 #pragma unroll
         for (int r = 0; r < kScanRowsPerStage; ++r) {
