@@ -284,8 +284,12 @@ ES_DEV void block_scan_multi(const int (&v)[K], int* warp_tot /*[K][33]*/, int (
 template <int K>
 ES_DEV void block_topM_multi(const uint64_t* ck, const int32_t* cid, uint8_t* cf, int n, const uint8_t (&A)[K],
                              const uint8_t (&S)[K], const int (&M)[K], uint32_t* hist /*[K][kSelBins]*/,
-                             BSel* st /*[K]*/, int* warp_tot /*[K][33]*/) {
+                             BSel* st /*[K]*/, int* warp_tot /*[K][33]*/, long long* tr = nullptr) {
     const int tid = threadIdx.x, T = blockDim.x, lane = lane_id();
+    auto stamp = [&](int i) {
+        if (tr && tid == 0 && i < 9) { long long t_; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); tr[i] = t_; }
+    };
+    stamp(0);
     int c[K];
     uint64_t kmin[K], kmax[K];
 #pragma unroll
@@ -400,6 +404,7 @@ ES_DEV void block_topM_multi(const uint64_t* ck, const int32_t* cid, uint8_t* cf
 #pragma unroll
         for (int j = 0; j < K; ++j)
             if (live[j]) { if (on_key[j]) kbit[j] = lo[j] - 1; else ibit[j] = lo[j] - 1; }
+        stamp(1 + pass);
     }
     BSel my[K];
 #pragma unroll
@@ -537,7 +542,8 @@ union_kernel(int V, const int32_t* __restrict__ static_ids, int n_static,
         const uint8_t A[3] = {kCand, kNew, kCand};
         const uint8_t S[3] = {kSem, kTake, kGs};
         const int M[3] = {n_sem, budget, ngs};
-        block_topM_multi<3>(ck, cid, cf, n_cand, A, S, M, hist, bsel, warp_tot);
+        block_topM_multi<3>(ck, cid, cf, n_cand, A, S, M, hist, bsel, warp_tot, trace ? trace + 7 : nullptr);
+        if (trace && tid == 0) trace[16] = n_cand;
     }
     if (sem_out) {
         for (int base = 0; base < n_cand; base += T) {      // one smem atomic per warp
