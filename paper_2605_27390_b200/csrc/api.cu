@@ -104,6 +104,7 @@ struct evospec_ctx {
     bool hist_dirty = false;      // a build stopped between its scan and its union: clear first
     uint32_t* ubits = nullptr;    // [V/32] union bitmap handed to the emit kernel
     unsigned long long* fin_ctr = nullptr;   // LM-head fused finalisation arrival counter
+    int32_t* zero_i = nullptr;    // a device 0 (dyn-only union output at offset 0)
     int32_t* ver_acc = nullptr;   // [kMaxChain + 1] verification: per-position accept flags
     int32_t* ver_tok = nullptr;   // [kMaxChain + 1] verification: per-position emitted token
     uint32_t* hist = nullptr;     // [12][4096] further select passes
@@ -229,7 +230,7 @@ evospec_status evospec_destroy(evospec_ctx* ctx) {
                     ctx->flags, ctx->wmax, ctx->g_ids, ctx->g_vals, ctx->g_m, ctx->g_s, ctx->st_q, ctx->st_H,
                     ctx->st_seeds, ctx->st_ctx, ctx->st_S, ctx->st_nS, ctx->st_local, ctx->st_nlocal,
                     ctx->st_tids, ctx->st_tvals, ctx->st_m, ctx->st_s, ctx->st_oids, ctx->st_ovals,
-                    ctx->st_lse, ctx->st_probs, ctx->ubits, ctx->fin_ctr, ctx->rg_ids, ctx->rg_vals, ctx->rg_m, ctx->rg_s, ctx->rg_seg, ctx->rg_segcta, ctx->ver_acc, ctx->ver_tok};
+                    ctx->st_lse, ctx->st_probs, ctx->ubits, ctx->fin_ctr, ctx->rg_ids, ctx->rg_vals, ctx->rg_m, ctx->rg_s, ctx->rg_seg, ctx->rg_segcta, ctx->ver_acc, ctx->ver_tok, ctx->zero_i};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (ctx->comm && nccl().loaded) nccl().CommDestroy(ctx->comm);
@@ -283,6 +284,7 @@ evospec_status evospec_create(evospec_ctx** out, const evospec_config* cfg, int 
     A(dalloc(&x->s64, V)); A(dalloc(&x->key32, V)); A(dalloc(&x->hist12, kHistBins)); A(dalloc(&x->ubits, (V + 31) / 32)); A(dalloc(&x->fin_ctr, 1)); A(cudaMemset(x->fin_ctr, 0, 8)); A(cudaMemset(x->hist12, 0, kHistBins * sizeof(uint32_t)));
     A(dalloc(&x->hist, 12 * kHistBins));
     A(dalloc(&x->ver_acc, kMaxChain + 1)); A(dalloc(&x->ver_tok, kMaxChain + 1));
+    A(dalloc(&x->zero_i, 1)); A(cudaMemset(x->zero_i, 0, sizeof(int32_t)));
     A(dalloc(&x->cand_count, 4)); A(dalloc(&x->cand_s, cap)); A(dalloc(&x->cand_id, cap));
     A(dalloc(&x->loc_count, 4)); A(dalloc(&x->loc_s, sem)); A(dalloc(&x->loc_id, sem));
     A(dalloc(&x->gat_s, sem * R)); A(dalloc(&x->gat_id, sem * R));
@@ -523,6 +525,7 @@ static bool use_tc(const LmhArgs& a) {
     return a.n_h >= kTcMinRows;
 }
 
+constexpr bool kOverlapDefault = false;   // draft_step static/dynamic LM-head overlap (EVOSPEC_OVERLAP)
 constexpr int kRaggedSegRows = 112;   // rows per static segment of the ragged head (measured: 64 887 us, 96 745, 112 710, 128 736 on config Bt)
 
 struct LmhSegs {
@@ -539,8 +542,10 @@ static evospec_status lmh_impl(evospec_ctx* ctx, const void* W, int64_t n_w_rows
                                float inv_temp, int32_t* topk_ids, float* topk_vals, float* row_max,
                                float* row_sumexp, float* logits_out, void* stream, int32_t* m_ids, float* m_vals,
                                float* m_lse, float* m_probs, const int32_t* seg = nullptr,
-                               const LmhSegs* segs = nullptr) {
-    if (!ctx || !W || !H || !subset || (!n_subset_dev && !seg) || !topk_ids || !topk_vals || !row_max || !row_sumexp)
+                               const LmhSegs* segs = nullptr, const int32_t* list2 = nullptr,
+                               const int32_t* n_list2_dev = nullptr, int32_t n_list2_max = 0) {
+    if (!ctx || !W || !H || !subset || (!n_subset_dev && !seg && !list2) || !topk_ids || !topk_vals || !row_max ||
+        !row_sumexp)
         return fail(EVOSPEC_EINPUT, "subset_logits_topk: null argument");
     const evospec_config& c = ctx->cfg;
     if (n_h < 1 || n_h > c.max_rows) return fail(EVOSPEC_EINPUT, "subset_logits_topk: n_h=%d not in [1,%d]", n_h, c.max_rows);
@@ -555,7 +560,7 @@ static evospec_status lmh_impl(evospec_ctx* ctx, const void* W, int64_t n_w_rows
     cudaStream_t st = (cudaStream_t)stream;
     if (c.debug_checks) {
         ctx->launches += 1;
-        if (!seg) launch_check_sorted(subset, n_subset_dev, n_subset_max, c.V, ctx->flags, st);
+        if (!seg && !list2) launch_check_sorted(subset, n_subset_dev, n_subset_max, c.V, ctx->flags, st);
         LAUNCH_CHECK("check_sorted");
     }
     LmhArgs a{};
@@ -574,6 +579,12 @@ static evospec_status lmh_impl(evospec_ctx* ctx, const void* W, int64_t n_w_rows
     a.par_fold = par_fold;
     static const int fin_opt = getenv("EVOSPEC_FIN_OPT") ? atoi(getenv("EVOSPEC_FIN_OPT")) : 15;
     a.fin_opt = fin_opt;
+    if (list2) {   // two-list mode (draft_step overlap): one SM stays free for the union kernel
+        a.list2 = list2; a.n_list2_dev = n_list2_dev; a.n_list2_max = n_list2_max; a.n1 = n_subset_max;
+        a.grid = lmh_tc_grid() - 1;
+        if (!use_tc(a) || a.KP > 32 || segs || seg || logits_out)
+            return fail(EVOSPEC_EINPUT, "subset_logits_topk: two-list mode needs the tensor-core path and k + 8 <= 32");
+    }
     if (segs) {
         a.nseg = segs->nseg; a.seg_ctas = segs->seg_ctas; a.seg_rows = segs->seg_rows; a.seg_pos = segs->seg_pos;
         a.seg_cta = segs->seg_cta;
@@ -606,7 +617,7 @@ static evospec_status lmh_impl(evospec_ctx* ctx, const void* W, int64_t n_w_rows
             }
             CUDA_TRY(launch_lmh_tc(a, st));
             ctx->launches += 1;
-            n_cta = segs ? segs->seg_ctas : lmh_tc_grid();
+            n_cta = segs ? segs->seg_ctas : (a.grid > 0 ? a.grid : lmh_tc_grid());
             gamma = kTcGamma;
         } else {
             for (int h0 = 0; h0 < n_h;) {
@@ -865,6 +876,28 @@ static evospec_status draft_step_impl(evospec_ctx* ctx, const evospec_step_io* i
     float* ol = io->host_io ? ctx->st_lse : io->out_lse;
     float* op = io->host_io ? (io->out_probs ? ctx->st_probs : nullptr) : io->out_probs;
     if (phases & 2) {
+    // overlap (single shard, tensor-core head): the union writes only the dynamic list and
+    // the LM head streams the static rows (an input) while the union still runs, then the
+    // dynamic rows (two-list mode, lmh_tc.cu)
+    static const bool ov_env = getenv("EVOSPEC_OVERLAP") ? atoi(getenv("EVOSPEC_OVERLAP")) != 0 : kOverlapDefault;
+    const bool overlap = ov_env && c.n_shards == 1 && c.w_dtype == EVOSPEC_BF16 && c.h_dtype == EVOSPEC_BF16 &&
+                         c.d % 64 == 0 && io->n_h >= kTcMinRows && io->n_h <= kTcMaxRows &&
+                         io->k + kTopkPad <= 32 && io->n_static > 0 && !c.debug_checks && !getenv("EVOSPEC_LMH");
+    if (overlap) {
+        if (io->host_io) {   // the staged H before anything else of the step (keeps the PDL chain intact)
+            cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+            cudaStreamIsCapturing(st, &cs);
+            CUDA_TRY(cudaStreamWaitEvent(st, ctx->ev_h, cs == cudaStreamCaptureStatusActive ? cudaEventWaitExternal : 0));
+        }
+        evospec_status s = build_impl(ctx, io->E, io->n_e_rows, q, io->static_ids, io->n_static, seeds, io->n_seed,
+                                      io->csr_row_ptr, io->csr_col, cx, io->n_ctx, &io->build, ctx->st_S, ctx->st_nS,
+                                      nullptr, nullptr, st, ctx->zero_i);
+        if (s != EVOSPEC_OK) return s;
+        s = lmh_impl(ctx, io->W_local, io->n_w_rows, H, io->n_h, io->static_ids, nullptr, io->n_static, io->k,
+                     io->inv_temp, ctx->st_tids, ctx->st_tvals, ctx->st_m, ctx->st_s, nullptr, st, oi, ov, ol, op,
+                     nullptr, nullptr, ctx->st_S, ctx->st_nS, io->build.n_dyn);
+        if (s != EVOSPEC_OK) return s;
+    } else {
     const int n_sub_max = io->n_static + io->build.n_dyn;
     evospec_status s = evospec_build_subset(ctx, io->E, io->n_e_rows, q, io->static_ids, io->n_static, seeds,
                                             io->n_seed, io->csr_row_ptr, io->csr_col, cx, io->n_ctx, &io->build,
@@ -888,6 +921,7 @@ static evospec_status draft_step_impl(evospec_ctx* ctx, const evospec_step_io* i
                                  op, st);
         if (s != EVOSPEC_OK) return s;
     }
+    }   // !overlap
     }   // phases & 2
     if (io->host_io && (phases & 4)) {
         StageTimer t(ctx, EVOSPEC_STAGE_COPY, st);

@@ -242,7 +242,7 @@ lmh_finalize_kernel(LmhArgs a, int n_cta, int k, float gamma, const float* __res
     const int nn = n_need_s;
     for (int q = warp; q < nn; q += nwarps) {
         const int c = need_list[q];
-        const size_t row = (size_t)(__ldg(&a.subset[c_id[c]]) / a.R);
+        const size_t row = (size_t)(lmh_id_at(a, c_id[c]) / a.R);
         double acc = 0.0;
         if (a.w_dtype == 0 && a.h_dtype == 0 && a.d % 8 == 0) {   // 16-byte loads, 4 in flight per lane
             const uint4* wp = (const uint4*)((const uint16_t*)a.W + row * a.d);
@@ -296,7 +296,7 @@ lmh_finalize_kernel(LmhArgs a, int n_cta, int k, float gamma, const float* __res
         }
         const float lse = row_sumexp[r] > 0.0f ? row_max[r] + logf(row_sumexp[r]) : -INFINITY;
         for (int t = 0; t < k; ++t) {
-            const int oid = t < nk ? __ldg(&a.subset[c_id[t]]) : -1;
+            const int oid = t < nk ? lmh_id_at(a, c_id[t]) : -1;
             topk_ids[(size_t)r * k + t] = oid;
             topk_vals[(size_t)r * k + t] = t < nk ? (float)c_e[t] : -INFINITY;
             if (a.m_ids) {   // fused single-shard merge (R = 1)

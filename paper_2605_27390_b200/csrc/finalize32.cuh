@@ -288,7 +288,7 @@ ES_DEV void fin32_row(const LmhArgs& a, const int r, int n_cta_arg, int k, float
         if ((int)threadIdx.x < ncand) {
             const float v = cand_v[threadIdx.x];
             const int p = cand_p[threadIdx.x];
-            const int gid = __ldg(&a.subset[p]);   // position -> vocabulary id (in flight during the ranks)
+            const int gid = lmh_id_at(a, p);   // position -> vocabulary id (in flight during the ranks)
             int rank = 0;
 #pragma unroll 4
             for (int j = 0; j < ncand; ++j) rank += before(cand_v[j], cand_p[j], v, p);
@@ -354,7 +354,7 @@ ES_DEV void fin32_row(const LmhArgs& a, const int r, int n_cta_arg, int k, float
         const int cnt = nk_s, tot = warp_sum_i(lane < nwarps ? w_tot[lane] : 0);
         const float Lv = lane < cnt ? c_v[lane] : -INFINITY;
         // position -> vocabulary id (the rank path stored it already)
-        if (ncand > kFin32RankMax) c_gid[lane] = lane < cnt ? __ldg(&a.subset[c_id[lane]]) : -1;
+        if (ncand > kFin32RankMax) c_gid[lane] = lane < cnt ? lmh_id_at(a, c_id[lane]) : -1;
         else if (lane >= cnt) c_gid[lane] = -1;
         double hn = 0.0;
 #pragma unroll
@@ -449,7 +449,9 @@ ES_DEV void fin32_row(const LmhArgs& a, const int r, int n_cta_arg, int k, float
         bool flagged = false;
         for (int q = 0; q < nn; ++q) flagged |= need_list[q] == lane;
         double e = lane < cnt ? (flagged ? c_e[lane] : (double)c_v[lane]) : -INFINITY;
-        int id = lane < cnt ? c_id[lane] : 0x7fffffff;   // subset position (order = id order)
+        // ties on the vocabulary id (one sorted list: the same order as the positions;
+        // two-list mode: the positions of the two lists interleave in id order)
+        int id = lane < cnt ? c_gid[lane] : 0x7fffffff;
         int gid = c_gid[lane];
         if (nn > 0) {   // only re-scored runs can change the order
 #pragma unroll 1

@@ -87,6 +87,13 @@ struct LmhArgs {
     int fin_opt;    // finalisation variants (bits; EVOSPEC_FIN_OPT): 1 H before the PDL wait, 2 W-row L2 prefetch,
                     // 4 multi-warp re-score, 8 parallel head threshold
     int par_fold;   // thread-parallel tile fold (lmh_epilogue.cuh epi_par_*), buffered path
+    // two-list mode (draft_step overlap): `subset` holds n1 ids known at launch (the static
+    // core, an input) and `list2` the ids produced by the previous kernel (the dynamic
+    // list, n_list2_dev on the device); partials carry virtual positions vp (vp < n1: subset
+    // [vp], else list2[vp - n1]); the tensor-core kernel streams its slice of the first list
+    // before griddepcontrol.wait. grid: CTAs of the launch (0 = all SMs)
+    const int32_t* list2; const int32_t* n_list2_dev; int n_list2_max; int n1;
+    int grid;
     float fin_gamma;
     const float* fin_wmax;
     unsigned long long* fin_ctr;   // monotone arrival counter (G arrivals per launch)
@@ -97,6 +104,11 @@ struct LmhArgs {
 // [0, min(*n_subset_dev, n_subset_max)), or the segment [seg[0], seg[1]).
 // Positions stay absolute, so partial lists and the finalisation index
 // a.subset directly.
+// vocabulary id of a (virtual) subset position
+__device__ __forceinline__ int32_t lmh_id_at(const LmhArgs& a, int vp) {
+    return (a.list2 && vp >= a.n1) ? __ldg(&a.list2[vp - a.n1]) : __ldg(&a.subset[vp]);
+}
+
 __device__ __forceinline__ void lmh_cta_range(const LmhArgs& a, int& p0, int& p1) {
     int s0 = 0, s1;
     if (a.seg) {

@@ -228,9 +228,14 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
-    pdl_wait();   // the subset (and n_S) come from the previous kernel on the stream
+    // the subset (and n_S) come from the previous kernel on the stream; in two-list
+    // mode the first list is an input: the wait comes before the second list only
+    if (!a.list2) pdl_wait();
     int p0, p1;
-    if (seg_b >= 0) {
+    if (a.list2) {
+        p0 = (int)((long long)a.n1 * blockIdx.x / gridDim.x);
+        p1 = (int)((long long)a.n1 * (blockIdx.x + 1) / gridDim.x);
+    } else if (seg_b >= 0) {
         // the CTAs of a segment split its positions identically for every segment
         // with the same range, so concurrent row groups share W rows through L2
         int s0 = 0, s1;
@@ -253,14 +258,37 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
     const int last_len = len > kTileM ? min(tp.last_tile, len) : len;
     const int body = len - last_len;
     const int n_body = (body + kTileM - 1) / kTileM;
-    const int n_tiles = n_body + (last_len > 0 ? 1 : 0);
+    const int n_tiles1 = n_body + (last_len > 0 ? 1 : 0);
+    // two-list mode: this CTA's slice [q0, q1) of the second list (virtual positions
+    // n1 + i), known only after griddepcontrol.wait -- every thread resolves it lazily
+    // when its role reaches the end of the first list
+    int nt2 = a.list2 ? -1 : 0, q0 = 0, q1 = 0;
+    auto ensure2 = [&]() {
+        if (nt2 >= 0) return;
+        pdl_wait();
+        const int n2 = max(0, min(*a.n_list2_dev, a.n_list2_max));
+        q0 = a.n1 + (int)((long long)n2 * blockIdx.x / gridDim.x);
+        q1 = a.n1 + (int)((long long)n2 * (blockIdx.x + 1) / gridDim.x);
+        nt2 = (q1 - q0 + kTileM - 1) / kTileM;
+    };
+    auto has_tile = [&](int t) -> bool {
+        if (t < n_tiles1) return true;
+        ensure2();
+        return t < n_tiles1 + nt2;
+    };
 
     if (threadIdx.x == 0) TC_TRACE(0);
     // thread-parallel fold for CTAs with two or more tiles; a single tile (small
     // subsets) keeps the warp fold, whose first-tile bound is tighter on short tiles
-    const bool par = buffered && a.par_fold && n_tiles >= 2;
+    const bool par = buffered && a.par_fold && (n_tiles1 >= 2 || a.list2);
 
     auto tile_range = [&](int t, int& t0, int& tn) {
+        if (t >= n_tiles1) {   // two-list mode, second list (evenly split)
+            const int u = t - n_tiles1, len2 = q1 - q0;
+            t0 = q0 + (int)((long long)len2 * u / nt2);
+            tn = q0 + (int)((long long)len2 * (u + 1) / nt2) - t0;
+            return;
+        }
         if (t < n_body) {
             t0 = p0 + (int)((long long)body * t / n_body);
             tn = p0 + (int)((long long)body * (t + 1) / n_body) - t0;
@@ -296,11 +324,13 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
             l2_prefetch(rp + off, sz);
         };
         const int pf_dist = tp.pf_dist;
-        const char* pf_cur = n_tiles > 0 && pf_dist > 0 ? row_ptr_of(0, prow) : nullptr;
-        for (int w = 0; w < pf_dist && pf_cur; ++w) prefetch_win(pf_cur, w);
+        const int pf_dist_eff = a.list2 ? 0 : pf_dist;   // (prefetch: one-list mode only)
+        const int n_tiles = n_tiles1;
+        const char* pf_cur = n_tiles > 0 && pf_dist_eff > 0 ? row_ptr_of(0, prow) : nullptr;
+        for (int w = 0; w < pf_dist_eff && pf_cur; ++w) prefetch_win(pf_cur, w);
         int stage = 0;
         uint32_t phase = 0;
-        for (int t = 0; t < n_tiles; ++t) {
+        for (int t = 0; has_tile(t); ++t) {
             int t0, tn;
             tile_range(t, t0, tn);
             const char* src[8];
@@ -309,15 +339,15 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
             for (int i = 0; i < 8; ++i) {
                 const int row = 16 * i + 4 * warp + (lane >> 3);
                 const int pos = t0 + (row < tn ? row : 0);
-                src[i] = (const char*)a.W + (size_t)(a.subset[pos] / a.R) * row_bytes + chunk * 16;
+                src[i] = (const char*)a.W + (size_t)(lmh_id_at(a, pos) / a.R) * row_bytes + chunk * 16;
                 dsto[i] = (uint32_t)(row * 128 + ((chunk ^ (row & 7)) << 4));
             }
-            const char* pf_next = t + 1 < n_tiles && pf_dist > 0 ? row_ptr_of(t + 1, prow) : nullptr;
+            const char* pf_next = t + 1 < n_tiles && pf_dist_eff > 0 ? row_ptr_of(t + 1, prow) : nullptr;
             for (int kb = 0; kb < tp.nkb; ++kb) {
                 // prefetch: window (kb/8 + kPfDist) of this tile; the next tile's first
                 // windows once this tile's remaining windows are all requested
-                if (pf_dist > 0 && (kb & 7) == 0) {
-                    const int w = (kb >> 3) + pf_dist;
+                if (pf_dist_eff > 0 && (kb & 7) == 0) {
+                    const int w = (kb >> 3) + pf_dist_eff;
                     if (w < n_win) prefetch_win(pf_cur, w);
                     else if (pf_next) prefetch_win(pf_next, w - n_win);
                 }
@@ -342,7 +372,7 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
         const uint32_t idesc = idesc_bf16(kTileM, NP);
         int stage = 0;
         uint32_t phase = 0;
-        for (int t = 0; t < n_tiles; ++t) {
+        for (int t = 0; has_tile(t); ++t) {
             const int b = t & 1;
             const uint32_t use = (uint32_t)(t >> 1);
             if (t >= 2) mbar_wait(&tempty[b], (use - 1) & 1);
@@ -374,13 +404,14 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
         const int half = ew >> 2;
         const int row = quad * 32 + lane;           // tile row (TMEM lane)
         const int nthr = kTcEpiWarps * 32;
-        for (int t = 0; t < n_tiles; ++t) {
+        for (int t = 0; has_tile(t); ++t) {
             int t0, tn;
             tile_range(t, t0, tn);
             const int b = t & 1;
+            const bool last_t = !has_tile(t + 1);
             mbar_wait(&tfull[b], (uint32_t)(t >> 1) & 1);
             if (ew == 0 && lane == 0 && t < 2) TC_TRACE(3 + 2 * t);
-            if (DTR && ew == 0 && lane == 0 && t == n_tiles - 1) DTR[40] = clock64();
+            if (DTR && ew == 0 && lane == 0 && last_t) DTR[40] = clock64();
             tc_fence_after();
             const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(b * NP);
             for (int c0 = half * 16; c0 < NP; c0 += 32) {
@@ -392,15 +423,15 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
             }
             tc_fence_before();
             mbar_arrive(&tempty[b]);
-            if (DTR && ew == 0 && lane == 0 && t == n_tiles - 1) DTR[41] = clock64();
+            if (DTR && ew == 0 && lane == 0 && last_t) DTR[41] = clock64();
             named_bar_sync(1, nthr);
-            if (DTR && ew == 0 && lane == 0 && t == n_tiles - 1) DTR[42] = clock64();
+            if (DTR && ew == 0 && lane == 0 && last_t) DTR[42] = clock64();
             if (a.logits_out) {
                 for (int r = ew; r < n_h; r += kTcEpiWarps)
                     for (int p = lane; p < tn; p += 32)
                         a.logits_out[(size_t)r * a.n_subset_max + t0 + p] = e.tile[r * kTile + p];
             }
-            if (t == n_tiles - 1) break;            // the last tile is folded by all warps below
+            if (last_t) break;                      // the last tile is folded by all warps below
             if (par) {
                 epi_par_phase1_any(e, n_h, a.KP, tn, t0, ew * 32 + lane, nthr, false, a.part, blockIdx.x, a.n_h, h_row0);
                 named_bar_sync(1, nthr);
@@ -416,6 +447,8 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
     }
     // the last tile's fold is the exposed tail: producers and the MMA warp are
     // idle by now, so all 13 warps split its rows
+    if (a.list2) ensure2();
+    const int n_tiles = n_tiles1 + nt2;
     if (n_tiles > 0) {
         int t0, tn;
         tile_range(n_tiles - 1, t0, tn);
@@ -546,6 +579,7 @@ static cudaError_t ensure_smem(K kern, size_t smem) {
 }
 
 int lmh_tc_grid() { return kNumSMs; }
+static int lmh_tc_grid(const LmhArgs& a) { return a.grid > 0 ? a.grid : kNumSMs; }
 
 bool lmh_tc_supported(const LmhArgs& a) {
     const int rows = a.nseg > 0 ? a.seg_rows : a.n_h;
@@ -585,7 +619,7 @@ cudaError_t launch_lmh_tc(const LmhArgs& a, cudaStream_t st) {
         return cudaErrorInvalidValue;
     cudaError_t e = ensure_smem(lmh_tc_kernel, smem);
     if (e != cudaSuccess) return e;
-    return launch_pdl(lmh_tc_kernel, dim3(lmh_tc_grid()), dim3(kTcWarps * 32), smem, st, mw, mh, a, tp);
+    return launch_pdl(lmh_tc_kernel, dim3(lmh_tc_grid(a)), dim3(kTcWarps * 32), smem, st, mw, mh, a, tp);
 }
 
 }  // namespace es

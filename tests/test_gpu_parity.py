@@ -208,6 +208,27 @@ def test_prepared_draft_step_refilled_host_buffers():
         assert np.max(np.abs(out[3].numpy() - ref["triple"]["probs"])) <= G.PROB_TOL
 
 
+@pytest.mark.parametrize("dup", [0, 3000])
+def test_draft_step_llama_full_size(dup):
+    """Config L through evospec_draft_step (the bench's call; with EVOSPEC_OVERLAP the
+    static / dynamic two-list LM head), against the oracle; dup > 0 duplicates W rows so
+    that exact logit ties cross the static and dynamic lists (ties to the lower id)."""
+    import synth
+    c = dict(synth.CONFIGS["llama"])
+    P = G.make_problem(1, dup_rows=dup, **c)
+    ctx = ctx_for(P)
+    W = G.to_dev(P["W"], DEV)
+    ctx.prepare_weights(W)
+    kw = dict(E=W, W_local=W, static_ids=G.to_dev(P["static"], DEV), csr_row_ptr=G.to_dev(P["row_ptr"], DEV),
+              csr_col=G.to_dev(P["col"], DEV), k=P["k"], n_sem=P["n_sem"], n_dyn=P["n_dyn"])
+    out = ctx.draft_step(q=G.to_dev(P["q"], DEV), H=G.to_dev(P["H"], DEV), seeds=G.to_dev(P["seeds"], DEV), **kw)
+    torch.cuda.synchronize()
+    ref = G.oracle_step(oracle, P)
+    np.testing.assert_array_equal(out[0].cpu().numpy(), ref["triple"]["ids"])
+    assert np.max(np.abs(out[3].cpu().numpy() - ref["triple"]["probs"])) <= G.PROB_TOL
+    assert ctx.get_flags() == 0
+
+
 def test_input_errors():
     P = G.make_problem(0, dtype="fp32", **TINY)
     ctx = ctx_for(P)
