@@ -525,7 +525,7 @@ static bool use_tc(const LmhArgs& a) {
     return a.n_h >= kTcMinRows;
 }
 
-constexpr bool kOverlapDefault = false;   // draft_step static/dynamic LM-head overlap (EVOSPEC_OVERLAP)
+constexpr bool kOverlapDefault = true;    // draft_step static/dynamic LM-head overlap (EVOSPEC_OVERLAP=0: off; step 319 -> 298 us)
 constexpr int kRaggedSegRows = 112;   // rows per static segment of the ragged head (measured: 64 887 us, 96 745, 112 710, 128 736 on config Bt)
 
 struct LmhSegs {
@@ -593,7 +593,8 @@ static evospec_status lmh_impl(evospec_ctx* ctx, const void* W, int64_t n_w_rows
     }
     if (getenv("EVOSPEC_TRACE")) {
         if (!ctx->trace) CUDA_TRY(cudaMalloc(&ctx->trace, kTraceLen * sizeof(long long)));
-        CUDA_TRY(cudaMemsetAsync(ctx->trace, 0, 2 * kNumSMs * 8 * sizeof(long long), st));
+        if (!list2)   // (a memset between the union and a two-list head would break the PDL overlap)
+            CUDA_TRY(cudaMemsetAsync(ctx->trace, 0, 2 * kNumSMs * 8 * sizeof(long long), st));
         a.trace = ctx->trace;
     }
     int n_cta = 0;

@@ -167,6 +167,7 @@ struct TcParams {
     uint32_t tmem_cols;
     int pf_dist;     // L2 prefetch distance in 1 KB windows (0 = off)
     int last_tile;   // rows of a CTA's short last tile (ranges longer than one tile)
+    int dyn_tile;    // two-list mode: rows per second-list tile (EVOSPEC_DYN_TILE)
     size_t off_b, off_epi, off_bar, off_rows;  // smem carve offsets
 };
 
@@ -262,14 +263,17 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
     // two-list mode: this CTA's slice [q0, q1) of the second list (virtual positions
     // n1 + i), known only after griddepcontrol.wait -- every thread resolves it lazily
     // when its role reaches the end of the first list
-    int nt2 = a.list2 ? -1 : 0, q0 = 0, q1 = 0;
+    // The second list goes out in whole 128-row tiles, tile u of CTA b covering rows
+    // [128 (b + G u), +128): its rows arrive only when the union ends, after the first
+    // list's stream, and a few full tiles on a few CTAs stream far faster than a
+    // sliver of it on every CTA (a short tile still pays all d / 64 stages of H).
+    int nt2 = a.list2 ? -1 : 0, n2 = 0;
     auto ensure2 = [&]() {
         if (nt2 >= 0) return;
         pdl_wait();
-        const int n2 = max(0, min(*a.n_list2_dev, a.n_list2_max));
-        q0 = a.n1 + (int)((long long)n2 * blockIdx.x / gridDim.x);
-        q1 = a.n1 + (int)((long long)n2 * (blockIdx.x + 1) / gridDim.x);
-        nt2 = (q1 - q0 + kTileM - 1) / kTileM;
+        n2 = max(0, min(*a.n_list2_dev, a.n_list2_max));
+        const int first = tp.dyn_tile * (int)blockIdx.x, step = tp.dyn_tile * (int)gridDim.x;
+        nt2 = first < n2 ? (n2 - first + step - 1) / step : 0;
     };
     auto has_tile = [&](int t) -> bool {
         if (t < n_tiles1) return true;
@@ -283,10 +287,10 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
     const bool par = buffered && a.par_fold && (n_tiles1 >= 2 || a.list2);
 
     auto tile_range = [&](int t, int& t0, int& tn) {
-        if (t >= n_tiles1) {   // two-list mode, second list (evenly split)
-            const int u = t - n_tiles1, len2 = q1 - q0;
-            t0 = q0 + (int)((long long)len2 * u / nt2);
-            tn = q0 + (int)((long long)len2 * (u + 1) / nt2) - t0;
+        if (t >= n_tiles1) {   // two-list mode, second list: whole tiles, round robin over the CTAs
+            const int r0 = tp.dyn_tile * ((int)blockIdx.x + (int)gridDim.x * (t - n_tiles1));
+            t0 = a.n1 + r0;
+            tn = min(tp.dyn_tile, n2 - r0);
             return;
         }
         if (t < n_body) {
@@ -408,7 +412,10 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
             int t0, tn;
             tile_range(t, t0, tn);
             const int b = t & 1;
-            const bool last_t = !has_tile(t + 1);
+            // two-list mode: whether a first-list tile is the CTA's last is known only
+            // after the union ends -- those are folded as middle tiles (overlapping the
+            // wait); a CTA without second-list tiles stores its rows after the loop
+            const bool last_t = a.list2 ? (t >= n_tiles1 && !has_tile(t + 1)) : !has_tile(t + 1);
             mbar_wait(&tfull[b], (uint32_t)(t >> 1) & 1);
             if (ew == 0 && lane == 0 && t < 2) TC_TRACE(3 + 2 * t);
             if (DTR && ew == 0 && lane == 0 && last_t) DTR[40] = clock64();
@@ -449,7 +456,8 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
     // idle by now, so all 13 warps split its rows
     if (a.list2) ensure2();
     const int n_tiles = n_tiles1 + nt2;
-    if (n_tiles > 0) {
+    const bool store_after = a.list2 && nt2 == 0;   // (two-list mode, no second-list tile)
+    if (n_tiles > 0 && !store_after) {
         int t0, tn;
         tile_range(n_tiles - 1, t0, tn);
         named_bar_sync(2, kTcWarps * 32);
@@ -474,7 +482,7 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
     __syncthreads();
     tc_fence_after();
     if (buffered) {
-        if (n_tiles == 0) epi_store_buf(e, a.part, blockIdx.x, a.n_h, h_row0, n_h, warp, kTcWarps);
+        if (n_tiles == 0 || store_after) epi_store_buf(e, a.part, blockIdx.x, a.n_h, h_row0, n_h, warp, kTcWarps);
         // (otherwise the last tile's fold stored every row)
     } else {
         epi_store(e, a.part, blockIdx.x, a.n_h, h_row0, n_h, a.KP, a.LS, warp, kTcWarps);
@@ -595,6 +603,8 @@ cudaError_t launch_lmh_tc(const LmhArgs& a, cudaStream_t st) {
     tp.pf_dist = kPfDist;
     if (const char* e = getenv("EVOSPEC_PF")) tp.pf_dist = atoi(e);
     tp.last_tile = kLastTile;
+    tp.dyn_tile = kTileM;
+    if (const char* e = getenv("EVOSPEC_DYN_TILE")) tp.dyn_tile = std::max(16, std::min(kTileM, atoi(e)));
     if (const char* e = getenv("EVOSPEC_LAST_TILE")) tp.last_tile = std::max(1, std::min(kTileM, atoi(e)));
     uint32_t cols = 2 * tp.n_pad, c = 32;
     while (c < cols) c <<= 1;
