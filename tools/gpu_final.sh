@@ -4,5 +4,5 @@ timeout 1200 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1; 
 timeout 900 python bench.py > gpurun_out/bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench.log
 timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref.log 2>&1; echo "ref rc=$?" >> gpurun_out/bench_ref.log
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-sweep --no-bt > gpurun_out/ncu_launch.log 2>&1
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"sem_scan|topn_cand|union_kernel|lmh_tc|lmh_finalize32" -s 7 -c 5 -o gpurun_out/prof_r01_final4 python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-sweep --no-bt > gpurun_out/ncu_full_final.log 2>&1
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"sem_scan|topn_cand|union_kernel|lmh_tc|lmh_finalize32" -s 7 -c 5 -o gpurun_out/prof_r01_final5 python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-sweep --no-bt > gpurun_out/ncu_full_final.log 2>&1
 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/smoke.log 2>&1
