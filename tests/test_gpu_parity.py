@@ -229,6 +229,28 @@ def test_draft_step_llama_full_size(dup):
     assert ctx.get_flags() == 0
 
 
+@pytest.mark.parametrize("n_h,k,n_dyn,dup", [(5, 1, 3000, 0), (17, 10, 3000, 400), (60, 24, 5000, 0),
+                                               (60, 10, 100, 0)])
+def test_draft_step_two_list_shapes(n_h, k, n_dyn, dup):
+    """draft_step's two-list LM head (static rows before the wait, dynamic rows after;
+    DESIGN §5.0) across tree widths, k and dynamic-list sizes (whole and partial
+    second-list tiles), with cross-list exact ties (dup), against the oracle."""
+    P = G.make_problem(40 + n_h, dtype="bf16", V=60000, d=256, n_static=40000, n_sem=6000, n_dyn=n_dyn,
+                       n_h=n_h, k=k, dup_rows=dup)
+    ctx = ctx_for(P)
+    W = G.to_dev(P["W"], DEV)
+    ctx.prepare_weights(W)
+    kw = dict(E=W, W_local=W, static_ids=G.to_dev(P["static"], DEV), csr_row_ptr=G.to_dev(P["row_ptr"], DEV),
+              csr_col=G.to_dev(P["col"], DEV), k=P["k"], n_sem=P["n_sem"], n_dyn=P["n_dyn"])
+    out = ctx.draft_step(q=G.to_dev(P["q"], DEV), H=G.to_dev(P["H"], DEV), seeds=G.to_dev(P["seeds"], DEV), **kw)
+    torch.cuda.synchronize()
+    ref = G.oracle_step(oracle, P)
+    np.testing.assert_array_equal(out[0].cpu().numpy(), ref["triple"]["ids"])
+    np.testing.assert_allclose(out[2].cpu().numpy(), ref["triple"]["lse"], rtol=2e-3, atol=2e-3)
+    assert np.max(np.abs(out[3].cpu().numpy() - ref["triple"]["probs"])) <= G.PROB_TOL
+    assert ctx.get_flags() == 0
+
+
 def test_input_errors():
     P = G.make_problem(0, dtype="fp32", **TINY)
     ctx = ctx_for(P)
