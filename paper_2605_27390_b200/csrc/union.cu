@@ -287,7 +287,7 @@ ES_DEV void block_topM_multi(const uint64_t* ck, const int32_t* cid, uint8_t* cf
                              BSel* st /*[K]*/, int* warp_tot /*[K][33]*/, long long* tr = nullptr) {
     const int tid = threadIdx.x, T = blockDim.x, lane = lane_id();
     auto stamp = [&](int i) {
-        if (tr && tid == 0 && i < 9) { long long t_; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); tr[i] = t_; }
+        if (tr && tid == 0 && i < 16) { long long t_; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); tr[i] = t_; }
     };
     stamp(0);
     int c[K];
@@ -301,6 +301,7 @@ ES_DEV void block_topM_multi(const uint64_t* ck, const int32_t* cid, uint8_t* cf
         for (int j = 0; j < K; ++j)
             if (f & A[j]) { ++c[j]; kmin[j] = min(kmin[j], k); kmax[j] = max(kmax[j], k); }
     }
+    stamp(10);
     if (tid < K) { st[tid].kmin = ~0ull; st[tid].kmax = 0ull; }
     int cnt[K];
     {
@@ -341,6 +342,7 @@ ES_DEV void block_topM_multi(const uint64_t* ck, const int32_t* cid, uint8_t* cf
         kbit[j] = diff ? 63 - __clzll((long long)diff) : -1;
         ibit[j] = 31;
     }
+    stamp(11);
     for (int pass = 0; pass < 16; ++pass) {
         bool live[K];
         bool any = false;
@@ -380,6 +382,7 @@ ES_DEV void block_topM_multi(const uint64_t* ck, const int32_t* cid, uint8_t* cf
                               1u);
         }
         __syncthreads();
+        if (pass == 0) stamp(12);
         const int bin = kSelBins - 1 - tid;
         int hb[K], above[K];
 #pragma unroll
