@@ -272,6 +272,12 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
         if (nt2 >= 0) return;
         pdl_wait();
         n2 = max(0, min(*a.n_list2_dev, a.n_list2_max));
+        if (tp.dyn_tile == 0) {   // even split: this CTA's slice, one tile
+            const int s0 = (int)((long long)n2 * blockIdx.x / gridDim.x);
+            const int s1 = (int)((long long)n2 * (blockIdx.x + 1) / gridDim.x);
+            nt2 = (s1 - s0 + kTileM - 1) / kTileM;
+            return;
+        }
         const int first = tp.dyn_tile * (int)blockIdx.x, step = tp.dyn_tile * (int)gridDim.x;
         nt2 = first < n2 ? (n2 - first + step - 1) / step : 0;
     };
@@ -287,8 +293,16 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
     const bool par = buffered && a.par_fold && (n_tiles1 >= 2 || a.list2);
 
     auto tile_range = [&](int t, int& t0, int& tn) {
-        if (t >= n_tiles1) {   // two-list mode, second list: whole tiles, round robin over the CTAs
-            const int r0 = tp.dyn_tile * ((int)blockIdx.x + (int)gridDim.x * (t - n_tiles1));
+        if (t >= n_tiles1) {   // two-list mode, second list
+            if (tp.dyn_tile == 0) {   // even split of the CTA's slice into nt2 tiles
+                const int s0 = (int)((long long)n2 * blockIdx.x / gridDim.x);
+                const int s1 = (int)((long long)n2 * (blockIdx.x + 1) / gridDim.x);
+                const int u = t - n_tiles1, len2 = s1 - s0;
+                t0 = a.n1 + s0 + (int)((long long)len2 * u / nt2);
+                tn = a.n1 + s0 + (int)((long long)len2 * (u + 1) / nt2) - t0;
+                return;
+            }
+            const int r0 = tp.dyn_tile * ((int)blockIdx.x + (int)gridDim.x * (t - n_tiles1));   // whole tiles, round robin
             t0 = a.n1 + r0;
             tn = min(tp.dyn_tile, n2 - r0);
             return;
@@ -604,7 +618,7 @@ cudaError_t launch_lmh_tc(const LmhArgs& a, cudaStream_t st) {
     if (const char* e = getenv("EVOSPEC_PF")) tp.pf_dist = atoi(e);
     tp.last_tile = kLastTile;
     tp.dyn_tile = kTileM;
-    if (const char* e = getenv("EVOSPEC_DYN_TILE")) tp.dyn_tile = std::max(16, std::min(kTileM, atoi(e)));
+    if (const char* e = getenv("EVOSPEC_DYN_TILE")) tp.dyn_tile = atoi(e) <= 0 ? 0 : std::max(16, std::min(kTileM, atoi(e)));
     if (const char* e = getenv("EVOSPEC_LAST_TILE")) tp.last_tile = std::max(1, std::min(kTileM, atoi(e)));
     uint32_t cols = 2 * tp.n_pad, c = 32;
     while (c < cols) c <<= 1;

@@ -1,6 +1,6 @@
 python -c "import __graft_entry__ as g; g.build()" || exit 1
 EVOSPEC_OVERLAP=1 timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -q -x -k "draft_step" 2>&1 | tail -2
-for dt in 128 64 32; do EVOSPEC_DYN_TILE=$dt EVOSPEC_OVERLAP=1 timeout 600 python bench.py --steps 30 --no-sweep --no-bt --no-extra --no-cpu-baseline 2>/dev/null | tail -1 | python -c "
+for dt in 0 128 0 128; do EVOSPEC_DYN_TILE=$dt EVOSPEC_OVERLAP=1 timeout 600 python bench.py --steps 30 --no-sweep --no-bt --no-extra --no-cpu-baseline 2>/dev/null | tail -1 | python -c "
 import json,sys; l=json.loads(sys.stdin.read()); print('dyn_tile=$dt', round(l['value']), round(l['ms_per_step']*1e3,1), 'e2e', round(l['e2e']['value']))"; done
 EVOSPEC_OVERLAP=0 timeout 600 python bench.py --steps 30 --no-sweep --no-bt --no-extra --no-cpu-baseline 2>/dev/null | tail -1 | python -c "
 import json,sys; l=json.loads(sys.stdin.read()); print('no overlap', round(l['value']), round(l['ms_per_step']*1e3,1), 'e2e', round(l['e2e']['value']))"
