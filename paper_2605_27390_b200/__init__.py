@@ -511,11 +511,14 @@ class Context:
         host_io = not H.is_cuda
         n_h = H.shape[0]
         if out is None:
+            # one contiguous block [ids | vals | lse | probs]: with host I/O the library
+            # then reads the step's outputs back with a single copy
             kw = dict(pin_memory=True) if host_io else dict(device=H.device)
-            out = (torch.empty((n_h, k), dtype=torch.int32, **kw),
-                   torch.empty((n_h, k), dtype=torch.float32, **kw),
-                   torch.empty(n_h, dtype=torch.float32, **kw),
-                   torch.empty((n_h, k), dtype=torch.float32, **kw))
+            hk = n_h * k
+            blk = torch.empty(3 * hk + n_h, dtype=torch.int32, **kw)
+            out = (blk[:hk].view(n_h, k), blk[hk:2 * hk].view(torch.float32).view(n_h, k),
+                   blk[2 * hk:2 * hk + n_h].view(torch.float32),
+                   blk[2 * hk + n_h:].view(torch.float32).view(n_h, k))
         io = StepIO()
         io.E, io.n_e_rows = E.data_ptr(), E.shape[0]
         io.W_local, io.n_w_rows = W_local.data_ptr(), W_local.shape[0]

@@ -302,8 +302,12 @@ evospec_status evospec_create(evospec_ctx** out, const evospec_config* cfg, int 
     A(dalloc(&x->st_local, std::max(1, c.max_subset))); A(dalloc(&x->st_nlocal, 1));
     const size_t hk = (size_t)c.max_rows * c.max_k;
     A(dalloc(&x->st_tids, hk)); A(dalloc(&x->st_tvals, hk)); A(dalloc(&x->st_m, c.max_rows));
-    A(dalloc(&x->st_s, c.max_rows)); A(dalloc(&x->st_oids, hk)); A(dalloc(&x->st_ovals, hk));
-    A(dalloc(&x->st_lse, c.max_rows)); A(dalloc(&x->st_probs, hk));
+    A(dalloc(&x->st_s, c.max_rows));
+    // host-I/O output staging as ONE block [ids | vals | lse | probs] (laid out per call
+    // for its n_h, k): a caller whose host outputs are one contiguous block in the same
+    // order gets one device-to-host copy per step instead of four
+    A(dalloc(&x->st_oids, 3 * hk + c.max_rows));
+    x->st_ovals = nullptr; x->st_lse = nullptr; x->st_probs = nullptr;
     A(dalloc(&x->rg_ids, 2 * hk)); A(dalloc(&x->rg_vals, 2 * hk));
     A(dalloc(&x->rg_m, 2 * (size_t)c.max_rows)); A(dalloc(&x->rg_s, 2 * (size_t)c.max_rows)); A(dalloc(&x->rg_seg, 2)); A(dalloc(&x->rg_segcta, kMaxSeg + 1));
     if (e == cudaSuccess) e = cudaMemset(x->flags, 0, sizeof(int));
@@ -872,10 +876,14 @@ static evospec_status draft_step_impl(evospec_ctx* ctx, const evospec_step_io* i
             CUDA_TRY(cudaMemcpyAsync(ctx->st_ctx, io->ctx_ids, (size_t)io->n_ctx * 4, cudaMemcpyHostToDevice, st));
     }
     if (io->host_io) { q = ctx->st_q; H = ctx->st_H; seeds = ctx->st_seeds; cx = io->ctx_ids ? ctx->st_ctx : nullptr; }
+    const size_t hk_io = (size_t)io->n_h * io->k;
+    float* const st_v = (float*)(ctx->st_oids + hk_io);   // the staging block's layout for this call
+    float* const st_l = st_v + hk_io;
+    float* const st_p = st_l + io->n_h;
     int32_t* oi = io->host_io ? ctx->st_oids : io->out_ids;
-    float* ov = io->host_io ? ctx->st_ovals : io->out_vals;
-    float* ol = io->host_io ? ctx->st_lse : io->out_lse;
-    float* op = io->host_io ? (io->out_probs ? ctx->st_probs : nullptr) : io->out_probs;
+    float* ov = io->host_io ? st_v : io->out_vals;
+    float* ol = io->host_io ? st_l : io->out_lse;
+    float* op = io->host_io ? (io->out_probs ? st_p : nullptr) : io->out_probs;
     if (phases & 2) {
     // overlap (single shard, tensor-core head): the union writes only the dynamic list and
     // the LM head streams the static rows (an input) while the union still runs, then the
@@ -927,10 +935,19 @@ static evospec_status draft_step_impl(evospec_ctx* ctx, const evospec_step_io* i
     if (io->host_io && (phases & 4)) {
         StageTimer t(ctx, EVOSPEC_STAGE_COPY, st);
         const size_t hk = (size_t)io->n_h * io->k;
-        CUDA_TRY(cudaMemcpyAsync(io->out_ids, oi, hk * 4, cudaMemcpyDeviceToHost, st));
-        CUDA_TRY(cudaMemcpyAsync(io->out_vals, ov, hk * 4, cudaMemcpyDeviceToHost, st));
-        CUDA_TRY(cudaMemcpyAsync(io->out_lse, ol, (size_t)io->n_h * 4, cudaMemcpyDeviceToHost, st));
-        if (io->out_probs) CUDA_TRY(cudaMemcpyAsync(io->out_probs, op, hk * 4, cudaMemcpyDeviceToHost, st));
+        const char* hb0 = (const char*)io->out_ids;
+        const bool one_block = (const char*)io->out_vals == hb0 + hk * 4 &&
+                               (const char*)io->out_lse == hb0 + hk * 8 &&
+                               (!io->out_probs || (const char*)io->out_probs == hb0 + hk * 8 + (size_t)io->n_h * 4);
+        if (one_block) {
+            CUDA_TRY(cudaMemcpyAsync(io->out_ids, oi, hk * 8 + (size_t)io->n_h * 4 + (io->out_probs ? hk * 4 : 0),
+                                     cudaMemcpyDeviceToHost, st));
+        } else {
+            CUDA_TRY(cudaMemcpyAsync(io->out_ids, oi, hk * 4, cudaMemcpyDeviceToHost, st));
+            CUDA_TRY(cudaMemcpyAsync(io->out_vals, ov, hk * 4, cudaMemcpyDeviceToHost, st));
+            CUDA_TRY(cudaMemcpyAsync(io->out_lse, ol, (size_t)io->n_h * 4, cudaMemcpyDeviceToHost, st));
+            if (io->out_probs) CUDA_TRY(cudaMemcpyAsync(io->out_probs, op, hk * 4, cudaMemcpyDeviceToHost, st));
+        }
     }
     return EVOSPEC_OK;
 }
