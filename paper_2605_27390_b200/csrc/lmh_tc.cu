@@ -348,7 +348,21 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
         for (int w = 0; w < pf_dist_eff && pf_cur; ++w) prefetch_win(pf_cur, w);
         int stage = 0;
         uint32_t phase = 0;
-        for (int t = 0; has_tile(t); ++t) {
+        for (int t = 0;; ++t) {
+            if (t == n_tiles1 && a.pf_ids) {
+                // first list issued: pull this CTA's slice of the candidate rows into L2
+                // (HBM is otherwise idle until the union ends; the second list then streams
+                // from L2). Read without the wait: stale ids only cost wasted prefetches.
+                const int n = min(*(volatile const int*)a.pf_n, a.pf_cap);
+                const int c0 = (int)((long long)n * blockIdx.x / gridDim.x);
+                const int c1 = (int)((long long)n * (blockIdx.x + 1) / gridDim.x);
+                for (int i = c0 + warp * 32 + lane; i < c1; i += kProdWarps * 32) {
+                    const int id = __ldcg(&a.pf_ids[i]);
+                    if (id >= 0 && (int64_t)(id / a.R) < a.n_w_rows)
+                        l2_prefetch((const char*)a.W + (size_t)(id / a.R) * row_bytes, (uint32_t)row_bytes);
+                }
+            }
+            if (!has_tile(t)) break;
             int t0, tn;
             tile_range(t, t0, tn);
             const char* src[8];
