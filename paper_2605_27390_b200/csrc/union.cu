@@ -284,7 +284,9 @@ ES_DEV void block_scan_multi(const int (&v)[K], int* warp_tot /*[K][33]*/, int (
 template <int K>
 ES_DEV void block_topM_multi(const uint64_t* ck, const int32_t* cid, uint8_t* cf, int n, const uint8_t (&A)[K],
                              const uint8_t (&S)[K], const int (&M)[K], uint32_t* hist /*[K][kSelBins]*/,
-                             BSel* st /*[K]*/, int* warp_tot /*[K][33]*/, long long* tr = nullptr) {
+                             BSel* st /*[K]*/, int* warp_tot /*[K][33]*/, long long* tr = nullptr,
+                             const int* pre_c = nullptr, const uint64_t* pre_lo = nullptr,
+                             const uint64_t* pre_hi = nullptr) {
     const int tid = threadIdx.x, T = blockDim.x, lane = lane_id();
     auto stamp = [&](int i) {
         if (tr && tid == 0 && i < 16) { long long t_; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); tr[i] = t_; }
@@ -294,12 +296,17 @@ ES_DEV void block_topM_multi(const uint64_t* ck, const int32_t* cid, uint8_t* cf
     uint64_t kmin[K], kmax[K];
 #pragma unroll
     for (int j = 0; j < K; ++j) { c[j] = 0; kmin[j] = ~0ull; kmax[j] = 0ull; }
-    for (int i = tid; i < n; i += T) {
-        const uint8_t f = cf[i];
-        const uint64_t k = ck[i];
+    if (pre_c) {   // this thread's statistics, gathered by the caller while loading
 #pragma unroll
-        for (int j = 0; j < K; ++j)
-            if (f & A[j]) { ++c[j]; kmin[j] = min(kmin[j], k); kmax[j] = max(kmax[j], k); }
+        for (int j = 0; j < K; ++j) { c[j] = pre_c[j]; kmin[j] = pre_lo[j]; kmax[j] = pre_hi[j]; }
+    } else {
+        for (int i = tid; i < n; i += T) {
+            const uint8_t f = cf[i];
+            const uint64_t k = ck[i];
+#pragma unroll
+            for (int j = 0; j < K; ++j)
+                if (f & A[j]) { ++c[j]; kmin[j] = min(kmin[j], k); kmax[j] = max(kmax[j], k); }
+        }
     }
     stamp(10);
     if (tid < K) { st[tid].kmin = ~0ull; st[tid].kmax = 0ull; }
@@ -507,6 +514,11 @@ union_kernel(int V, const int32_t* __restrict__ static_ids, int n_static,
     if (clear_hist)
         for (int i = tid; i < kHistBins; i += T) clear_hist[i] = 0;
     const int n_cand = min(*n_cand_dev, cap);
+    __syncthreads();   // the seeds walk (warp 0) has set its bits: kNew is decided while loading
+    // per-thread statistics of the three selections below (count, key range), gathered
+    // while loading: kCand (selections 0 and 2) and kNew (selection 1)
+    int st_c[2] = {0, 0};
+    uint64_t st_lo[2] = {~0ull, ~0ull}, st_hi[2] = {0ull, 0ull};
     for (int i0 = 0; i0 < n_cand; i0 += 4 * T) {           // 4 independent loads in flight
         double sv[4];
         int32_t iv[4];
@@ -520,9 +532,19 @@ union_kernel(int V, const int32_t* __restrict__ static_ids, int n_static,
         for (int u = 0; u < 4; ++u) {
             const int i = i0 + u * T + tid;
             if (i >= n_cand) continue;
-            ck[i] = double_key(sv[u]);
+            const uint64_t key = double_key(sv[u]);
+            ck[i] = key;
             cid[i] = iv[u];
-            cf[i] = (iv[u] >= 0 && iv[u] < V) ? kCand : 0;
+            uint8_t f = 0;
+            if (iv[u] >= 0 && iv[u] < V) {
+                f = kCand;
+                ++st_c[0]; st_lo[0] = min(st_lo[0], key); st_hi[0] = max(st_hi[0], key);
+                if (!((bits[iv[u] >> 5] >> (iv[u] & 31)) & 1u)) {   // not static, not a seed
+                    f |= kNew;
+                    ++st_c[1]; st_lo[1] = min(st_lo[1], key); st_hi[1] = max(st_hi[1], key);
+                }
+            }
+            cf[i] = f;
         }
     }
     __syncthreads();
@@ -536,8 +558,6 @@ union_kernel(int V, const int32_t* __restrict__ static_ids, int n_static,
     // (the formation's semantic part) is T_b intersected with S_sem.
     const int taken0 = taken_s;
     const int budget = n_dyn - taken0;
-    for (int i = tid; i < n_cand; i += T)
-        if ((cf[i] & kCand) && !((bits[cid[i] >> 5] >> (cid[i] & 31)) & 1u)) cf[i] |= kNew;
     const int ngs = min(n_graph_sem_seeds, min(n_sem, kMaxG));
     if (tid == 0) ngs_s = 0;
     __syncthreads();
@@ -545,7 +565,10 @@ union_kernel(int V, const int32_t* __restrict__ static_ids, int n_static,
         const uint8_t A[3] = {kCand, kNew, kCand};
         const uint8_t S[3] = {kSem, kTake, kGs};
         const int M[3] = {n_sem, budget, ngs};
-        block_topM_multi<3>(ck, cid, cf, n_cand, A, S, M, hist, bsel, warp_tot, trace ? trace + 7 : nullptr);
+        const int pc[3] = {st_c[0], st_c[1], st_c[0]};
+        const uint64_t plo[3] = {st_lo[0], st_lo[1], st_lo[0]}, phi[3] = {st_hi[0], st_hi[1], st_hi[0]};
+        block_topM_multi<3>(ck, cid, cf, n_cand, A, S, M, hist, bsel, warp_tot, trace ? trace + 7 : nullptr, pc, plo,
+                            phi);
         if (trace && tid == 0) trace[16] = n_cand;
     }
     if (sem_out) {
