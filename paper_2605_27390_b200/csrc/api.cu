@@ -371,7 +371,7 @@ static evospec_status build_impl(evospec_ctx* ctx, const void* E, int64_t n_e_ro
                                  const int32_t* row_ptr, const int32_t* col, const int32_t* ctx_ids, int32_t n_ctx,
                                  const evospec_build_params* p, int32_t* out_ids, int32_t* out_n,
                                  int32_t* out_local_ids, int32_t* out_local_n, void* stream,
-                                 const int32_t* dyn_base) {
+                                 const int32_t* dyn_base, cudaEvent_t wait_before_union = nullptr) {
     if (!ctx || !E || !q || !p || !out_ids || !out_n) return fail(EVOSPEC_EINPUT, "build_subset: null argument");
     const evospec_config& c = ctx->cfg;
     const int R = c.n_shards, r = c.shard_rank;
@@ -446,6 +446,11 @@ static evospec_status build_impl(evospec_ctx* ctx, const void* E, int64_t n_e_ro
         LAUNCH_CHECK("ctx_select");
     }
     // a2 exact S_sem + a3/a4 formation, cap, union
+    if (wait_before_union) {   // (draft_step overlap: the host-staged H, copied under the scan)
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        cudaStreamIsCapturing(st, &cs);
+        CUDA_TRY(cudaStreamWaitEvent(st, wait_before_union, cs == cudaStreamCaptureStatusActive ? cudaEventWaitExternal : 0));
+    }
     const bool emit = R == 1 && !dyn_base;
     launch_union(c.V, static_ids, n_static, seeds, n_seed, ctx->cand_s, ctx->cand_id, ctx->cand_count, ctx->cand_cap,
                  N, row_ptr, col, use_ctx ? ctx->ctx_sel : nullptr, ctx->ctx_n, p->n_graph_sem_seeds, p->per_seed,
@@ -896,14 +901,11 @@ static evospec_status draft_step_impl(evospec_ctx* ctx, const evospec_step_io* i
                          c.d % 64 == 0 && io->n_h >= kTcMinRows && io->n_h <= kTcMaxRows &&
                          io->k + kTopkPad <= 32 && io->n_static > 0 && !c.debug_checks && !getenv("EVOSPEC_LMH");
     if (overlap) {
-        if (io->host_io) {   // the staged H before anything else of the step (keeps the PDL chain intact)
-            cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-            cudaStreamIsCapturing(st, &cs);
-            CUDA_TRY(cudaStreamWaitEvent(st, ctx->ev_h, cs == cudaStreamCaptureStatusActive ? cudaEventWaitExternal : 0));
-        }
+        // the host-staged H (side stream, under the scan) is waited for before the union,
+        // so the union -> LM head PDL edge stays intact
         evospec_status s = build_impl(ctx, io->E, io->n_e_rows, q, io->static_ids, io->n_static, seeds, io->n_seed,
                                       io->csr_row_ptr, io->csr_col, cx, io->n_ctx, &io->build, ctx->st_S, ctx->st_nS,
-                                      nullptr, nullptr, st, ctx->zero_i);
+                                      nullptr, nullptr, st, ctx->zero_i, io->host_io ? ctx->ev_h : nullptr);
         if (s != EVOSPEC_OK) return s;
         s = lmh_impl(ctx, io->W_local, io->n_w_rows, H, io->n_h, io->static_ids, nullptr, io->n_static, io->k,
                      io->inv_temp, ctx->st_tids, ctx->st_tvals, ctx->st_m, ctx->st_s, nullptr, st, oi, ov, ol, op,
