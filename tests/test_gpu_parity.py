@@ -229,14 +229,15 @@ def test_draft_step_llama_full_size(dup):
     assert ctx.get_flags() == 0
 
 
-@pytest.mark.parametrize("n_h,k,n_dyn,dup", [(5, 1, 3000, 0), (17, 10, 3000, 400), (60, 24, 5000, 0),
-                                               (60, 10, 100, 0)])
-def test_draft_step_two_list_shapes(n_h, k, n_dyn, dup):
+@pytest.mark.parametrize("n_h,k,n_dyn,dup,n_static", [(5, 1, 3000, 0, 40000), (17, 10, 3000, 400, 40000),
+                                                        (60, 24, 5000, 0, 40000), (60, 10, 100, 0, 40000),
+                                                        (60, 10, 12000, 0, 10000)])
+def test_draft_step_two_list_shapes(n_h, k, n_dyn, dup, n_static):
     """draft_step's two-list LM head (static rows before the wait, dynamic rows after;
     DESIGN §5.0) across tree widths, k and dynamic-list sizes (whole and partial
     second-list tiles), with cross-list exact ties (dup), against the oracle."""
-    P = G.make_problem(40 + n_h, dtype="bf16", V=60000, d=256, n_static=40000, n_sem=6000, n_dyn=n_dyn,
-                       n_h=n_h, k=k, dup_rows=dup)
+    P = G.make_problem(40 + n_h, dtype="bf16", V=60000, d=256, n_static=n_static, n_sem=max(6000, n_dyn),
+                       n_dyn=n_dyn, n_h=n_h, k=k, dup_rows=dup)   # (~12k dynamic rows: most CTAs hold one)
     ctx = ctx_for(P)
     W = G.to_dev(P["W"], DEV)
     ctx.prepare_weights(W)
