@@ -615,3 +615,32 @@ def test_sharded_d8192_full_vocab_sampled():
     torch.cuda.synchronize()
     np.testing.assert_array_equal(oi.cpu().numpy()[rows], ref["ids"])
     assert np.max(np.abs(op.cpu().numpy()[rows] - ref["probs"])) <= G.PROB_TOL
+
+
+def test_draft_step_two_list_several_second_list_tiles():
+    """The two-list head with 16-row second-list tiles (EVOSPEC_DYN_TILE=16, read once per
+    process: run in a subprocess) -- several second-list tiles per CTA -- against the oracle."""
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np, torch, oracle\n"
+        "from tests import gpu_helpers as G\n"
+        "import paper_2605_27390_b200 as es\n"
+        "P = G.make_problem(77, dtype='bf16', V=60000, d=256, n_static=30000, n_sem=6000, n_dyn=5000, n_h=60, k=10)\n"
+        "ctx = es.Context(V=P['V'], d=P['d'], w_dtype=torch.bfloat16, h_dtype=torch.bfloat16, max_subset=35000,\n"
+        "                 max_rows=60, max_k=10, max_sem=6000)\n"
+        "W = G.to_dev(P['W'], 'cuda:0'); ctx.prepare_weights(W)\n"
+        "kw = dict(E=W, W_local=W, static_ids=G.to_dev(P['static'], 'cuda:0'), csr_row_ptr=G.to_dev(P['row_ptr'], 'cuda:0'),\n"
+        "          csr_col=G.to_dev(P['col'], 'cuda:0'), k=10, n_sem=6000, n_dyn=5000)\n"
+        "out = ctx.draft_step(q=G.to_dev(P['q'], 'cuda:0'), H=G.to_dev(P['H'], 'cuda:0'), seeds=G.to_dev(P['seeds'], 'cuda:0'), **kw)\n"
+        "torch.cuda.synchronize()\n"
+        "ref = G.oracle_step(oracle, P)\n"
+        "assert np.array_equal(out[0].cpu().numpy(), ref['triple']['ids'])\n"
+        "assert np.max(np.abs(out[3].cpu().numpy() - ref['triple']['probs'])) <= G.PROB_TOL\n"
+        "assert ctx.get_flags() == 0\n"
+        "print('ok')\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, EVOSPEC_DYN_TILE="16", EVOSPEC_OVERLAP="1")
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
