@@ -168,6 +168,7 @@ struct TcParams {
     int pf_dist;     // L2 prefetch distance in 1 KB windows (0 = off)
     int last_tile;   // rows of a CTA's short last tile (ranges longer than one tile)
     int dyn_tile;    // two-list mode: rows per second-list tile (EVOSPEC_DYN_TILE)
+    int dyn_stride;  // two-list mode: CTA rank stride of the second-list round robin
     size_t off_b, off_epi, off_bar, off_rows;  // smem carve offsets
 };
 
@@ -268,6 +269,9 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
     // list's stream, and a few full tiles on a few CTAs stream far faster than a
     // sliver of it on every CTA (a short tile still pays all d / 64 stages of H).
     int nt2 = a.list2 ? -1 : 0, n2 = 0;
+    // the CTA's rank in the second-list round robin: blockIdx scattered by a stride coprime
+    // with the grid (EVOSPEC_DYN_STRIDE) so the CTAs holding second-list tiles spread over the chip
+    const int dyn_rank = (int)(((long long)blockIdx.x * tp.dyn_stride) % gridDim.x);
     auto ensure2 = [&]() {
         if (nt2 >= 0) return;
         pdl_wait();
@@ -278,7 +282,7 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
             nt2 = (s1 - s0 + kTileM - 1) / kTileM;
             return;
         }
-        const int first = tp.dyn_tile * (int)blockIdx.x, step = tp.dyn_tile * (int)gridDim.x;
+        const int first = tp.dyn_tile * dyn_rank, step = tp.dyn_tile * (int)gridDim.x;
         nt2 = first < n2 ? (n2 - first + step - 1) / step : 0;
     };
     auto has_tile = [&](int t) -> bool {
@@ -302,7 +306,7 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
                 tn = a.n1 + s0 + (int)((long long)len2 * (u + 1) / nt2) - t0;
                 return;
             }
-            const int r0 = tp.dyn_tile * ((int)blockIdx.x + (int)gridDim.x * (t - n_tiles1));   // whole tiles, round robin
+            const int r0 = tp.dyn_tile * (dyn_rank + (int)gridDim.x * (t - n_tiles1));   // whole tiles, round robin
             t0 = a.n1 + r0;
             tn = min(tp.dyn_tile, n2 - r0);
             return;
@@ -632,6 +636,13 @@ cudaError_t launch_lmh_tc(const LmhArgs& a, cudaStream_t st) {
     if (const char* e = getenv("EVOSPEC_PF")) tp.pf_dist = atoi(e);
     tp.last_tile = kLastTile;
     tp.dyn_tile = kTileM;
+    tp.dyn_stride = 1;
+    if (const char* e = getenv("EVOSPEC_DYN_STRIDE")) tp.dyn_stride = std::max(1, atoi(e));
+    {   // coprime with the grid, so that the ranks are a permutation
+        const int G = lmh_tc_grid(a);
+        auto gcd = [](int x, int y) { while (y) { const int t = x % y; x = y; y = t; } return x; };
+        while (gcd(tp.dyn_stride, G) != 1) ++tp.dyn_stride;
+    }
     if (const char* e = getenv("EVOSPEC_DYN_TILE")) tp.dyn_tile = atoi(e) <= 0 ? 0 : std::max(16, std::min(kTileM, atoi(e)));
     if (const char* e = getenv("EVOSPEC_LAST_TILE")) tp.last_tile = std::max(1, std::min(kTileM, atoi(e)));
     uint32_t cols = 2 * tp.n_pad, c = 32;
