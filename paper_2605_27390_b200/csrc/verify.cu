@@ -53,7 +53,11 @@ struct VerSmem {
     double c_part;   // this CTA's partial, read by the cluster (DSMEM)
     float c_v;
     int c_i;
+    int s_lb[2];     // the subset positions bounding this CTA's id slice
+    int s_xi;        // the proposal's subset position
+    int32_t s_cache[8192];   // the subset entries of this CTA's id slice (when they fit)
 };
+constexpr int kVerSCap = 8192;
 
 ES_DEV double warp_sum_dd(double v) {
 #pragma unroll
@@ -115,14 +119,40 @@ ES_DEV int lower_bound_i32(const int32_t* S, int n, int v) {
     return lo;
 }
 
-// r(v) = max(0, p(v) - q(v)) over [v0, v1), q from qj on S (qj == nullptr: q = 0)
+// first index i of the sorted S with S[i] >= v, by one warp: a 32-ary search
+// (log32 n dependent rounds of 32 parallel probes); every lane returns it
+ES_DEV int warp_lower_bound(const int32_t* S, int n, int v) {
+    const int lane = lane_id();
+    int lo = 0, hi = n;
+    while (hi - lo > 32) {
+        const int step = (hi - lo + 31) / 32;
+        const int p = lo + lane * step;
+        const bool below = p < hi && __ldg(&S[p]) < v;
+        const int k = __popc(__ballot_sync(0xffffffffu, below));   // probes below v (a prefix)
+        if (k == 0) return lo;                                     // S[lo] >= v
+        const int nlo = lo + (k - 1) * step + 1;
+        hi = min(hi, lo + k * step + 1);
+        lo = nlo;
+    }
+    const int p = lo + lane;
+    const bool below = p < hi && __ldg(&S[p]) < v;
+    return lo + __popc(__ballot_sync(0xffffffffu, below));
+}
+
+// r(v) = max(0, p(v) - q(v)) over [v0, v1), q from qj on S (qj == nullptr: q = 0);
+// S entries [c_off, c_off + c_cnt) also in shared memory (cache, may be null)
 struct Resid {
     const float* zj; double it, M, s;
     const int32_t* S; int n_S; const float* qj;
+    const int32_t* cache = nullptr; int c_off = 0, c_cnt = 0;
+    ES_DEV int32_t s_at(int i) const {
+        const int o = i - c_off;
+        return (cache && o >= 0 && o < c_cnt) ? cache[o] : __ldg(&S[i]);
+    }
     ES_DEV double q_at(int v, int& i) const {
         if (!qj) return 0.0;
-        while (i < n_S && __ldg(&S[i]) < v) ++i;
-        return (i < n_S && __ldg(&S[i]) == v) ? (double)__ldg(&qj[i]) : 0.0;
+        while (i < n_S && s_at(i) < v) ++i;
+        return (i < n_S && s_at(i) == v) ? (double)__ldg(&qj[i]) : 0.0;
     }
     ES_DEV double r_at(int v, int& i) const {
         const double p = exp((double)__ldg(&zj[v]) * it - M) / s;
@@ -150,11 +180,37 @@ ES_DEV double cluster_sum_d(double v, VerSmem& sm, cg::cluster_group& cl) {
 // order) holds w * total finds the id by a block scan and one thread's re-walk.
 // Returns -2 on every CTA if the total mass is 0, else the id on the picking
 // CTA's thread 0 (-1 elsewhere).
-ES_DEV int cluster_draw(const Resid& R, int c0, int c1, double w, VerSmem& sm, cg::cluster_group& cl) {
+ES_DEV int cluster_draw(const Resid& R0, int c0, int c1, double w, VerSmem& sm, cg::cluster_group& cl) {
     const int tid = threadIdx.x;
     const int n = c1 - c0;
     const int v0 = c0 + (int)((long long)n * tid / kVerThreads), v1 = c0 + (int)((long long)n * (tid + 1) / kVerThreads);
-    const int i0 = R.qj ? lower_bound_i32(R.S, R.n_S, v0) : 0;
+    Resid R = R0;
+    int i0 = 0;
+    if (R.qj) {
+        // the subset entries of this CTA's id slice [c0, c1): bounds by two warps' 32-ary
+        // searches, the entries staged in shared memory, each thread's start found there
+        if (warp_id() < 2) {
+            const int b = warp_lower_bound(R.S, R.n_S, warp_id() == 0 ? c0 : c1);
+            if (lane_id() == 0) sm.s_lb[warp_id()] = b;
+        }
+        __syncthreads();
+        const int lb0 = sm.s_lb[0], cnt = sm.s_lb[1] - lb0;
+        if (cnt <= kVerSCap) {
+            for (int i = tid; i < cnt; i += kVerThreads) sm.s_cache[i] = __ldg(&R.S[lb0 + i]);
+            R.cache = sm.s_cache; R.c_off = lb0; R.c_cnt = cnt;
+        }
+        __syncthreads();
+        if (R.cache) {
+            int lo = 0, hi = cnt;
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (sm.s_cache[mid] < v0) lo = mid + 1; else hi = mid;
+            }
+            i0 = lb0 + lo;
+        } else {
+            i0 = lower_bound_i32(R.S, R.n_S, v0);
+        }
+    }
     double loc = 0.0;
     int last = -1;
     {
@@ -261,6 +317,12 @@ verify_pos_kernel(const float* __restrict__ z, int V, int g, const int32_t* __re
         }
         return;
     }
+    // the proposal's subset position: warp 0's 32-ary search, overlapping the sum below
+    if (j < g && wid == 0) {
+        const int xj = __ldg(&x[j]);
+        const int i = (xj >= 0 && xj < V) ? warp_lower_bound(S, n_S, xj) : n_S;
+        if (lane == 0) sm.s_xi = i;
+    }
     // 2. s = sum_v exp(z it - M), fp64, cluster-wide
     double loc = 0.0;
     for (int v = v0; v < v1; ++v) loc += exp((double)__ldg(&zj[v]) * it - M);
@@ -270,7 +332,7 @@ verify_pos_kernel(const float* __restrict__ z, int V, int g, const int32_t* __re
     if (j < g) {
         const int xj = __ldg(&x[j]);
         qj = qS + (size_t)j * n_S;
-        const int i = (xj >= 0 && xj < V) ? lower_bound_i32(S, n_S, xj) : n_S;
+        const int i = sm.s_xi;   // (written before the block reductions of the sum: visible)
         const bool in = i < n_S && __ldg(&S[i]) == xj && __ldg(&qj[i]) > 0.0f;
         if (!in) {
             if (me == 0 && tid == 0) { atomicOr(flags, kFlagBadIds); pos_acc[j] = 0; pos_tok[j] = -1; }
