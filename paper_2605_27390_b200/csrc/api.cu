@@ -613,7 +613,15 @@ static evospec_status lmh_impl(evospec_ctx* ctx, const void* W, int64_t n_w_rows
     float gamma = gemv_gamma(c.d);
     {
         StageTimer t(ctx, EVOSPEC_STAGE_LMH, st);
-        if (use_tc(a)) {
+        static const bool hl_env = getenv("EVOSPEC_LMH_HL") ? atoi(getenv("EVOSPEC_LMH_HL")) != 0 : true;
+        if (use_tc(a) && hl_env && lmh_hl_supported(a) && !segs) {
+            // H rows on the TMEM lanes (lmh_hl.cu): per-CTA candidate buffers (<= 64, unsorted)
+            a.LS = 64;
+            CUDA_TRY(launch_lmh_hl(a, st));
+            ctx->launches += 1;
+            n_cta = a.grid > 0 ? a.grid : lmh_tc_grid();
+            gamma = kTcGamma;
+        } else if (use_tc(a)) {
             // finalisation fused into the tensor-core kernel's last CTAs (k + 8 <= 32, no
             // segments, rows <= CTAs): opt-in (EVOSPEC_FUSED_FIN=1) -- measured slower than
             // the separate PDL-chained kernel (416 threads per row instead of 512, and no

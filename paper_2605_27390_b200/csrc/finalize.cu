@@ -313,7 +313,7 @@ lmh_finalize_kernel(LmhArgs a, int n_cta, int k, float gamma, const float* __res
 
 
 
-template <int U, int NT>
+template <int U, int NT, int LSX = kFin32LS>
 __global__ void __launch_bounds__(NT)
 lmh_finalize32_kernel(LmhArgs a, int n_cta_arg, int k, float gamma, const float* __restrict__ wmax_dev,
                       int32_t* __restrict__ topk_ids, float* __restrict__ topk_vals,
@@ -325,14 +325,31 @@ lmh_finalize32_kernel(LmhArgs a, int n_cta_arg, int k, float gamma, const float*
     const bool pre = a.fin_opt & 1;
     const double hacc = pre ? fin32_stage_h<NT>(a, blockIdx.x, sm) : 0.0;
     pdl_wait();
-    fin32_row<U, NT>(a, blockIdx.x, n_cta_arg, k, gamma, wmax_dev, topk_ids, topk_vals, row_max,
-                     row_sumexp, flags, sm, pre, hacc);
+    fin32_row<U, NT, LSX>(a, blockIdx.x, n_cta_arg, k, gamma, wmax_dev, topk_ids, topk_vals, row_max,
+                          row_sumexp, flags, sm, pre, hacc);
 
 }
 
 void launch_lmh_finalize(const LmhArgs& a, int n_cta, int k, const float* wmax_dev, int32_t* topk_ids,
                          float* topk_vals, float* row_max, float* row_sumexp, int* flags, cudaStream_t st,
                          float gamma) {
+    if (a.KP <= 32 && a.LS == 32 && n_cta * 8 <= 10 * kFin32Threads) {
+        // sorted per-CTA top-KP lists of lmh_hl_kernel (stride 32)
+        const int nq = n_cta * 8;
+        auto go = [&](auto kern, bool& attr_set) {
+            const size_t smem = std::max(fin32_smem_bytes(kFin32Threads), (size_t)(a.n_h <= kNumSMs ? 120 * 1024 : 0));
+            if (!attr_set)
+                attr_set = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                (int)std::max(smem, (size_t)120 * 1024)) == cudaSuccess;
+            launch_pdl(kern, dim3(a.n_h), dim3(kFin32Threads), smem, st, a, n_cta, k, gamma, wmax_dev, topk_ids,
+                       topk_vals, row_max, row_sumexp, flags);
+        };
+        static thread_local bool s3 = false, s5 = false, s10 = false;
+        if (nq <= 3 * kFin32Threads) go(lmh_finalize32_kernel<3, kFin32Threads, 32>, s3);
+        else if (nq <= 5 * kFin32Threads) go(lmh_finalize32_kernel<5, kFin32Threads, 32>, s5);
+        else go(lmh_finalize32_kernel<10, kFin32Threads, 32>, s10);
+        return;
+    }
     if (a.KP <= 32 && a.LS == kFin32LS && n_cta * (kFin32LS / 4) <= 10 * kFin32Threads) {
         // one CTA per SM while the rows fit one wave (the dynamic allocation is only
         // a placement hint: two CTAs sharing an SM measured slower); more rows pack.

@@ -139,7 +139,10 @@ ES_DEV double fin32_stage_h(const LmhArgs& a, const int r, const Fin32Smem& sm) 
     return hacc;
 }
 
-template <int U, int NT>
+// LSX: list stride. 64 = the unsorted candidate buffers of lmh_tc_kernel (cnt = 0,
+// xcnt = entries); 32 = the sorted exact per-CTA top-KP lists of lmh_hl_kernel
+// (cnt = entries, xcnt = 1 when the CTA dropped entries beyond its list).
+template <int U, int NT, int LSX = kFin32LS>
 ES_DEV void fin32_row(const LmhArgs& a, const int r, int n_cta_arg, int k, float gamma,
                       const float* __restrict__ wmax_dev, int32_t* __restrict__ topk_ids,
                       float* __restrict__ topk_vals, float* __restrict__ row_max, float* __restrict__ row_sumexp,
@@ -171,7 +174,8 @@ ES_DEV void fin32_row(const LmhArgs& a, const int r, int n_cta_arg, int k, float
         }
     }
     // A. every global load at once
-    const int nq = n_cta * (kFin32LS / 4);
+    constexpr int QL = LSX / 4;   // float4 per list
+    const int nq = n_cta * QL;
     float4 vv[U];
     int4 ii[U];
 #pragma unroll
@@ -179,19 +183,21 @@ ES_DEV void fin32_row(const LmhArgs& a, const int r, int n_cta_arg, int k, float
         const int q = threadIdx.x + u * NT;
         vv[u] = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
         if (q < nq) {
-            const size_t o = ((size_t)(c_base + (q >> 4)) * a.n_h + r) * kFin32LS + (q & 15) * 4;
+            const size_t o = ((size_t)(c_base + q / QL) * a.n_h + r) * LSX + (q % QL) * 4;
             vv[u] = __ldcg((const float4*)&a.part.val[o]);
             ii[u] = __ldcg((const int4*)&a.part.id[o]);
         }
     }
     float cm_ = -INFINITY, cs_ = 0.0f, thl = -INFINITY;
+    int dropped = 0;   // sorted lists: entries a CTA dropped (counted into tot, the uncertified test)
     if ((int)threadIdx.x < n_cta) {
         const size_t o = (size_t)(c_base + threadIdx.x) * a.n_h + r;
         cm_ = __ldcg(&a.part.m[o]);
         cs_ = __ldcg(&a.part.s[o]);
         const int cn = __ldcg(&a.part.cnt[o]);
-        const float vk = __ldcg(&a.part.val[o * kFin32LS + KP - 1]);
+        const float vk = __ldcg(&a.part.val[o * LSX + KP - 1]);
         if (cn >= KP) thl = vk;
+        if (LSX == 32) dropped = __ldcg(&a.part.xcnt[o]);
         // the list maximum: every producer keeps the CTA row's best entry, whose value
         // is the row's running maximum m (sorted lists: also slot 0)
         s_head[threadIdx.x] = cm_;
@@ -260,7 +266,7 @@ ES_DEV void fin32_row(const LmhArgs& a, const int r, int n_cta_arg, int k, float
     }
     {
         auto keep = [&](float x) { return x != -INFINITY && x >= th0; };
-        int nk = 0, tcnt = 0;
+        int nk = 0, tcnt = dropped;
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             nk += keep(vv[u].x) + keep(vv[u].y) + keep(vv[u].z) + keep(vv[u].w);
@@ -322,7 +328,7 @@ ES_DEV void fin32_row(const LmhArgs& a, const int r, int n_cta_arg, int k, float
             } else {
                 const int q = (b >> 2) * 32 + lane, comp = b & 3;
                 if (q < nq) {
-                    const size_t o = ((size_t)(c_base + (q >> 4)) * a.n_h + r) * kFin32LS + (q & 15) * 4 + comp;
+                    const size_t o = ((size_t)(c_base + q / QL) * a.n_h + r) * LSX + (q % QL) * 4 + comp;
                     bv = __ldcg(&a.part.val[o]);
                     bp = __ldcg(&a.part.id[o]);
                 }

@@ -141,6 +141,10 @@ void launch_verify(const float* z, int V, int g, const int32_t* x, const int32_t
 bool lmh_tc_supported(const LmhArgs& a);
 int lmh_tc_grid();
 cudaError_t launch_lmh_tc(const LmhArgs& a, cudaStream_t st);
+// H rows on the TMEM lanes (lmh_hl.cu): n_h <= 64, k + 8 <= 32, bf16; writes sorted
+// per-CTA top-KP lists with stride a.LS = 32 (finalised by the LS = 32 path)
+bool lmh_hl_supported(const LmhArgs& a);
+cudaError_t launch_lmh_hl(const LmhArgs& a, cudaStream_t st);
 
 // ---- finalize / merge / prepare (finalize.cu)
 void launch_lmh_finalize(const LmhArgs& a, int n_cta, int k, const float* wmax_dev,

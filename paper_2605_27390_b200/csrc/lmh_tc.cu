@@ -32,6 +32,7 @@
 
 #include "common.cuh"
 #include "kernels.cuh"
+#include "tc_ptx.cuh"
 #include "lmh_epilogue.cuh"
 #include "finalize32.cuh"
 
@@ -53,109 +54,6 @@ constexpr int kBlockK = 64;        // bf16 columns per stage = one 128-byte swiz
 constexpr int kTileM = 128;
 constexpr int kLastTile = 128;    // rows of a short last tile (128 = no split; see the launch)
 
-// ------------------------------------------------------------------ PTX
-ES_DEV uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
-ES_DEV void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-ES_DEV void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
-}
-ES_DEV void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-ES_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        "@!p bra WAIT_%=;\n"
-        "}\n" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
-
-ES_DEV void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, uint64_t policy) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
-        " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
-        "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "l"(policy)
-        : "memory");
-}
-ES_DEV void cp_async16(uint32_t dst, const void* src, uint64_t policy) {
-    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "l"(policy)
-                 : "memory");
-}
-ES_DEV void cp_async_arrive_noinc(uint64_t* bar) {
-    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-ES_DEV void l2_prefetch(const void* p, uint32_t bytes) {
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
-}
-ES_DEV uint64_t policy_evict_first() {
-    uint64_t p;
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-    return p;
-}
-ES_DEV uint64_t policy_evict_last() {
-    uint64_t p;
-    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-    return p;
-}
-
-ES_DEV void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-ES_DEV void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-
-// K-major, 128B-swizzled UMMA shared-memory descriptor (8-row groups 1024 B apart).
-ES_DEV uint64_t umma_desc_sw128(uint32_t saddr) {
-    uint64_t desc = 0;
-    desc |= (uint64_t)((saddr >> 4) & 0x3FFF);          // start address
-    desc |= (uint64_t)1 << 16;                           // LBO (unused for swizzled K-major)
-    desc |= (uint64_t)(1024 >> 4) << 32;                 // SBO = 1024 B
-    desc |= (uint64_t)1 << 46;                           // descriptor version (sm_100)
-    desc |= (uint64_t)2 << 61;                           // SWIZZLE_128B
-    return desc;
-}
-
-// kind::f16 instruction descriptor: D fp32, A/B bf16, both K-major.
-__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
-    return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
-}
-
-ES_DEV void umma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t accumulate) {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "setp.ne.b32 p, %4, 0;\n"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
-        "}\n" ::"r"(tmem_d),
-        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
-}
-ES_DEV void umma_commit(uint64_t* bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
-                 : "memory");
-}
-
-ES_DEV void tmem_ld16(uint32_t taddr, float (&v)[16]) {
-    uint32_t r[16];
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-        : "r"(taddr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
-}
-
-ES_DEV long long gtime() {
-    long long t;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    return t;
-}
 #define TC_TRACE(slot) do { if (a.trace) a.trace[(size_t)blockIdx.x * 8 + (slot)] = gtime(); } while (0)
 
 
@@ -558,66 +456,6 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
 }
 
 // ------------------------------------------------------------------ host
-static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
-    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-    if (!fn) {
-        cudaDriverEntryPointQueryResult q;
-        void* p = nullptr;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-            q == cudaDriverEntryPointSuccess)
-            fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
-    }
-    return fn;
-}
-
-static bool make_map(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, uint32_t box0, uint32_t box1,
-                     CUtensorMapL2promotion prom) {
-    auto fn = encode_fn();
-    if (!fn) return false;
-    cuuint64_t dims[2] = {inner, outer};
-    cuuint64_t strides[1] = {inner * 2};
-    cuuint32_t box[2] = {box0, box1};
-    cuuint32_t estr[2] = {1, 1};
-    return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
-              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, prom,
-              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-
-// Encoded tensor maps, cached per thread by (pointer, shape, box): encoding costs
-// host time on every call otherwise (the LM head is a per-draft-step launch).
-static bool cached_map(CUtensorMap* out, const void* ptr, uint64_t inner, uint64_t outer, uint32_t box0,
-                       uint32_t box1, CUtensorMapL2promotion prom) {
-    struct Entry { const void* ptr; uint64_t inner, outer; uint32_t b0, b1; int prom; CUtensorMap m; };
-    thread_local Entry cache[8];
-    thread_local int n = 0, next = 0;
-    for (int i = 0; i < n; ++i) {
-        const Entry& c = cache[i];
-        if (c.ptr == ptr && c.inner == inner && c.outer == outer && c.b0 == box0 && c.b1 == box1 && c.prom == (int)prom) {
-            *out = c.m;
-            return true;
-        }
-    }
-    Entry e{ptr, inner, outer, box0, box1, (int)prom, {}};
-    if (!make_map(&e.m, ptr, inner, outer, box0, box1, prom)) return false;
-    cache[next] = e;
-    next = (next + 1) % 8;
-    n = n < 8 ? n + 1 : 8;
-    *out = e.m;
-    return true;
-}
-
-// cudaFuncSetAttribute once per device and size (not on every launch)
-template <typename K>
-static cudaError_t ensure_smem(K kern, size_t smem) {
-    thread_local int done[16] = {0};
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (dev < 16 && done[dev] >= (int)smem) return cudaSuccess;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e == cudaSuccess && dev < 16) done[dev] = (int)smem;
-    return e;
-}
-
 int lmh_tc_grid() { return kNumSMs; }
 static int lmh_tc_grid(const LmhArgs& a) { return a.grid > 0 ? a.grid : kNumSMs; }
 
