@@ -613,7 +613,9 @@ static evospec_status lmh_impl(evospec_ctx* ctx, const void* W, int64_t n_w_rows
     float gamma = gemv_gamma(c.d);
     {
         StageTimer t(ctx, EVOSPEC_STAGE_LMH, st);
-        static const bool hl_env = getenv("EVOSPEC_LMH_HL") ? atoi(getenv("EVOSPEC_LMH_HL")) != 0 : true;
+        // H-on-lanes kernel: opt-in (EVOSPEC_LMH_HL=1); measured slower than lmh_tc at every
+        // subset size: its thread-per-row epilogue is latency-bound
+        static const bool hl_env = getenv("EVOSPEC_LMH_HL") ? atoi(getenv("EVOSPEC_LMH_HL")) != 0 : false;
         if (use_tc(a) && hl_env && lmh_hl_supported(a) && !segs) {
             // H rows on the TMEM lanes (lmh_hl.cu): per-CTA candidate buffers (<= 64, unsorted)
             a.LS = 64;

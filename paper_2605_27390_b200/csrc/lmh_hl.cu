@@ -60,9 +60,11 @@ constexpr int kHlRows = 64;          // H rows (TMEM lanes 0..63)
 constexpr int kHlTile = 256;         // W rows per tile (MMA N <= 256)
 constexpr int kHlCap = 64;           // candidate buffer per row
 constexpr int kHlCapS = kHlCap + 1;  // its row stride (conflict-free column reads)
-constexpr int kHlGS = 68;            // group-maxima row stride (16-byte rows, conflict-free float4)
+constexpr int kHlGS = 65;            // group-maxima row stride (conflict-free scalar access across rows)
 constexpr int kHlHBytes = kHlRows * 128;   // H K-block: 64 rows x 128 B
 constexpr int kHlMaxSlots = 16;
+constexpr int kHlRB = (kHlRows + kHlWarps - 1) / kHlWarps;   // rows per warp in the last-tile phase (5)
+constexpr int kHlZS = 260;           // staged last-tile logits: row stride (16-byte rows, conflict-free float4)
 constexpr int kHlBar = 1;            // named barrier of the 256 epilogue threads
 constexpr float kL2E = 1.4426950408889634f;
 
@@ -72,6 +74,23 @@ ES_DEV float ex2f(float x) {
     return y;
 }
 ES_DEV float key_to_float(uint32_t k) { return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k); }
+// 16 floats sorted descending in registers (bitonic network, branch-free)
+ES_DEV void bitonic_desc16(float (&v)[16]) {
+#pragma unroll
+    for (int k = 2; k <= 16; k <<= 1)
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1)
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                const int l = i ^ j;
+                if (l > i) {
+                    const float a = v[i], b = v[l];
+                    const bool desc = (i & k) == 0;
+                    v[i] = desc ? fmaxf(a, b) : fminf(a, b);
+                    v[l] = desc ? fminf(a, b) : fmaxf(a, b);
+                }
+            }
+}
 // 32 floats sorted descending in registers (bitonic network, branch-free)
 ES_DEV void bitonic_desc32(float (&v)[32]) {
 #pragma unroll
@@ -118,19 +137,65 @@ ES_DEV void tmem_ld64(uint32_t taddr, float (&v)[64]) {
     for (int i = 0; i < 64; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// 16 consecutive accumulator columns of this warp's 32 lanes (load and wait in one
+// asm statement, so no use of the registers precedes the wait)
+ES_DEV void tmem_ld16w(uint32_t taddr, float (&v)[16]) {
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+        "tcgen05.wait::ld.sync.aligned;\n"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr)
+        : "memory");
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// chunks at taddr a and b (16 columns each) into v[0..15], v[16..31], one wait
+ES_DEV void tmem_ld16x2w(uint32_t ta, uint32_t tb, float (&v)[32]) {
+    uint32_t r[32];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%32];\n"
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%33];\n"
+        "tcgen05.wait::ld.sync.aligned;\n"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(ta), "r"(tb)
+        : "memory");
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// Column of element j (0..63) of epilogue thread cq: the thread's 4 chunks of 16
+// interleave with the other threads' (64 c + 16 cq), so every thread holds about
+// tn / 4 valid columns whatever the tile length
+ES_DEV int hl_col(int cq, int j) { return 64 * (j >> 4) + 16 * cq + (j & 15); }
+ES_DEV void hl_load64(uint32_t taddr0, int cq, float (&z)[64]) {
+    float t[16];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        tmem_ld16w(taddr0 + 64 * c + 16 * cq, t);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) z[16 * c + j] = t[j];
+    }
+}
+
 // Overflow of a row's candidate buffer (rare: massive ties): the exact KP-th value
 // T of the candidates (this tile's admitted values + the buffer) by bisection on
 // the monotone float key, then the buffer := the KP best (ties by position: the
 // buffer's entries, then the columns in order). Executed by all 256 epilogue
 // threads (named barriers); rows without overflow (ov false) only take the
 // barriers. The logits are re-read from TMEM (the accumulator is still held).
-__device__ __noinline__ void hl_overflow(uint32_t taddr, bool rv, bool ov, int tn, int c0, float inv_temp, float B,
+__device__ __noinline__ void hl_overflow(uint32_t taddr0, bool rv, bool ov, int tn, float inv_temp, float B,
                                          float Br, int KP, int n_old, int t0, int r, int cq, float* bv, int* bp,
                                          int* t_c, int* t_x, int* st_n, float* b_run) {
     float z[64];
-    tmem_ld64(taddr, z);
+    hl_load64(taddr0, cq, z);
 #pragma unroll
-    for (int j = 0; j < 64; ++j) z[j] = (rv && c0 + j < tn) ? z[j] * inv_temp : -INFINITY;
+    for (int j = 0; j < 64; ++j) z[j] = (rv && hl_col(cq, j) < tn) ? z[j] * inv_temp : -INFINITY;
     uint32_t mlo = 0u, mhi = 0u;
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
@@ -213,7 +278,7 @@ __device__ __noinline__ void hl_overflow(uint32_t taddr, bool rv, bool ov, int t
                 if (k > T || (k == T && take > 0)) {
                     if (k == T) --take;
                     bv[o] = z[j];
-                    bp[o] = t0 + c0 + j;
+                    bp[o] = t0 + hl_col(cq, j);
                     ++o;
                 }
             }
@@ -227,12 +292,82 @@ __device__ __noinline__ void hl_overflow(uint32_t taddr, bool rv, bool ov, int t
 }
 
 // debug output of this thread's 64 logits (re-read from TMEM)
-__device__ __noinline__ void hl_logits_out(uint32_t taddr, int tn, int c0, float inv_temp, float* out) {
+__device__ __noinline__ void hl_logits_out(uint32_t taddr0, int tn, int cq, float inv_temp, float* out) {
     float z[64];
-    tmem_ld64(taddr, z);
+    hl_load64(taddr0, cq, z);
 #pragma unroll
     for (int j = 0; j < 64; ++j)
-        if (c0 + j < tn) out[c0 + j] = z[j] * inv_temp;
+        if (hl_col(cq, j) < tn) out[hl_col(cq, j)] = z[j] * inv_temp;
+}
+
+// Exact warp-level selection of a row's best KP when the candidates overflow its
+// buffer (rare: massive ties). Candidates: the buffer's [0, n_old) (earlier tiles:
+// smaller positions) and this tile's values >= B and > Br (the staged row zrow,
+// column lane + 32 j).
+// T = the KP-th largest key by bisection on the monotone float key (warp sums); the
+// selection: every key > T, then the ties in position order (the buffer's by their
+// positions, then the tile's by column). Writes KP entries to rbv / rbp [0, KP).
+__device__ __noinline__ void hl_warp_select(const float* zrow, float B, float Br, float* rbv, int* rbp, int n_old,
+                                            int t0, int KP, int lane) {
+    float v[8];
+    uint32_t bal[8];
+    for (int j = 0; j < 8; ++j) {
+        v[j] = zrow[lane + 32 * j];
+        bal[j] = __ballot_sync(0xffffffffu, v[j] >= B && v[j] > Br);
+    }
+    const bool hb0 = lane < n_old, hb1 = lane + 32 < n_old;
+    const float bv0 = hb0 ? rbv[lane] : -INFINITY, bv1 = hb1 ? rbv[lane + 32] : -INFINITY;
+    const int bp0 = hb0 ? rbp[lane] : INT_MAX, bp1 = hb1 ? rbp[lane + 32] : INT_MAX;
+    const uint32_t kb0 = float_key(bv0), kb1 = float_key(bv1);
+    uint32_t kt[8];
+    bool ht[8];
+    for (int j = 0; j < 8; ++j) { ht[j] = (bal[j] >> lane) & 1u; kt[j] = float_key(v[j]); }
+    uint32_t lo = 0u, hi = 0xffffffffu;
+    while (lo < hi) {   // (uniform: the counts are warp sums)
+        const uint32_t mid = lo + (uint32_t)(((uint64_t)hi - lo + 1) >> 1);
+        int c = (hb0 && kb0 >= mid) + (hb1 && kb1 >= mid);
+        for (int j = 0; j < 8; ++j) c += ht[j] && kt[j] >= mid;
+        if (warp_sum_i(c) >= KP) lo = mid;
+        else hi = mid - 1;
+    }
+    const uint32_t T = lo;
+    int gt = (hb0 && kb0 > T) + (hb1 && kb1 > T);
+    for (int j = 0; j < 8; ++j) gt += ht[j] && kt[j] > T;
+    const int need = KP - warp_sum_i(gt);
+    // ties of the buffer, ranked by position among themselves
+    const bool tb0 = hb0 && kb0 == T, tb1 = hb1 && kb1 == T;
+    int rb0 = 0, rb1 = 0;
+    for (int w = 0; w < 2; ++w)
+        for (int l = 0; l < 32; ++l) {
+            const bool ts = __shfl_sync(0xffffffffu, w ? tb1 : tb0, l);
+            const int ps = __shfl_sync(0xffffffffu, w ? bp1 : bp0, l);
+            rb0 += ts && ps < bp0;
+            rb1 += ts && ps < bp1;
+        }
+    const int nbt = warp_sum_i(tb0 + tb1);
+    const uint32_t lt = (1u << lane) - 1u;
+    bool sel[10];
+    sel[0] = hb0 && (kb0 > T || (tb0 && rb0 < need));
+    sel[1] = hb1 && (kb1 > T || (tb1 && rb1 < need));
+    int tpre = 0;
+    for (int j = 0; j < 8; ++j) {
+        const uint32_t tt = __ballot_sync(0xffffffffu, ht[j] && kt[j] == T);
+        const bool tie = (tt >> lane) & 1u;
+        sel[2 + j] = ht[j] && (kt[j] > T || (tie && nbt + tpre + __popc(tt & lt) < need));
+        tpre += __popc(tt);
+    }
+    __syncwarp();   // (every lane read its buffer entries above)
+    int pos = 0;
+    for (int q = 0; q < 10; ++q) {
+        const uint32_t sb = __ballot_sync(0xffffffffu, sel[q]);
+        if (sel[q]) {
+            const int sl = pos + __popc(sb & lt);
+            rbv[sl] = q == 0 ? bv0 : q == 1 ? bv1 : v[q - 2];
+            rbp[sl] = q == 0 ? bp0 : q == 1 ? bp1 : t0 + lane + 32 * (q - 2);
+        }
+        pos += __popc(sb);
+    }
+    __syncwarp();
 }
 
 struct HlParams {
@@ -242,6 +377,7 @@ struct HlParams {
     int bh;           // H rows per TMA box (n_h padded to 8)
     int off_epi, off_bar;
     int exp;          // experiment bits (EVOSPEC_HL_EXP): 1 no MMA, 2 no W copies, 4 no H loads
+    int warm;         // dry run of the epilogue before tile 0 (EVOSPEC_HL_WARM, default on)
     int hrep;         // experiment (EVOSPEC_HL_HREP): CTA b reads its own copy of H (rows b * n_h)
 };
 
@@ -250,7 +386,7 @@ __host__ __device__ constexpr int hl_epi_bytes() {
     return 4 * (2 * kHlRows * kHlCapS      // buf_v, buf_p
                 + kHlRows * kHlGS          // gmax
                 + 6 * kHlRows * 4          // t_m, t_s, t_c[2], t_x[2]
-                + 6 * kHlRows + 4);        // st_m, st_s, st_n, b_t, b_run, ovf, flag
+                + 6 * kHlRows + 8);        // st_m, st_s, st_n, ctr, b_run, ovf, flag, last tile
 }
 
 __global__ void __launch_bounds__(kHlThreads, 1)
@@ -273,10 +409,11 @@ lmh_hl_kernel(const __grid_constant__ CUtensorMap tmap_h, LmhArgs a, HlParams hp
     float* st_m = (float*)(t_x + 2 * kHlRows * 4);         // running row maximum
     float* st_s = st_m + kHlRows;                          // running sum of e^(z - st_m)
     int* st_n = (int*)(st_s + kHlRows);                    // buffer fill
-    float* b_t = (float*)(st_n + kHlRows);                 // this tile's bound
-    float* b_run = b_t + kHlRows;                          // running bound (strict)
+    int* ctr = st_n + kHlRows;                             // this tile's append counter
+    float* b_run = (float*)(ctr + kHlRows);                // running bound (strict)
     int* ovf = (int*)(b_run + kHlRows);                    // row overflow
     int* any_ovf = ovf + kHlRows;
+    int* fin_tile = any_ovf + 1;                           // [3] the last tile's t0, tn, positions seen
 
     const int warp = warp_id(), lane = lane_id();
     pdl_trigger();
@@ -451,182 +588,206 @@ lmh_hl_kernel(const __grid_constant__ CUtensorMap tmap_h, LmhArgs a, HlParams hp
         }
         if (lane == 0) HL_TRACE(2);
     } else if ((warp & 3) < 2) {
-        // ===== epilogue: row r = 32 (w % 4) + lane, columns [64 cq, 64 cq + 64) of the tile
+        // ===== epilogue: row r = 32 (w % 4) + lane, columns [64 cq, 64 cq + 64) of the tile.
+        // The code runs once per tile, so it is paid for by its footprint (instruction
+        // fetch), not its issue count: every pass is a rolled loop over 4 chunks of 16
+        // columns re-read from TMEM (tcgen05.ld 32x32b.x16), nothing is unrolled 64-wide.
         const int qd = warp & 3, cq = warp >> 2;
         const int r = 32 * qd + lane;
         const bool rv = r < a.n_h;
         const int KP = a.KP;
-        const int LS = a.LS;
         float* bv = buf_v + r * kHlCapS;
         int* bp = buf_p + r * kHlCapS;
+        float* gr = gmax + r * kHlGS;
         if (cq == 0) {
             st_m[r] = -INFINITY; st_s[r] = 0.0f; st_n[r] = 0; b_run[r] = -INFINITY; ovf[r] = 0;
             if (r == 0) *any_ovf = 0;
         }
         hl_bar();
         int seen = 0;   // subset positions of this CTA so far (entries beyond the list were dropped)
-        int t = 0;
-        for (; has_tile(t); ++t) {
-            int t0, tn;
-            tile_range(t, t0, tn);
-            seen += tn;
-            const int b = t & 1;
-            mbar_wait_sleep(&tfull[b], (uint32_t)(t >> 1) & 1, 200);
-            if (warp == 0 && lane == 0) HL_TRACE(t == 0 ? 3 : 5);
-            HL_CLK(0);
-            tc_fence_after();
-            const uint32_t taddr = tmem_base + ((uint32_t)(32 * qd) << 16) + (uint32_t)(b * kHlTile + 64 * cq);
-            const int c0 = 64 * cq;
-            // this thread's 64 scaled logits (-inf outside the tile / the tree rows)
-            auto load_z = [&](float (&z)[64]) {
-                tmem_ld64(taddr, z);
-#pragma unroll
-                for (int j = 0; j < 64; ++j) z[j] = (rv && c0 + j < tn) ? z[j] * a.inv_temp : -INFINITY;
-            };
-            float z[64];
-            load_z(z);
-            HL_CLK(1);
-            // group maxima (8 columns; 4 on tiles of <= 128 rows, so that a bound exists)
-            const bool g4 = tn <= 128;
-            float tm = -INFINITY;
-            float* gr = gmax + r * kHlGS;
-            if (g4) {
-#pragma unroll
-                for (int g = 0; g < 16; g += 4) {
-                    float4 q;
-                    q.x = fmaxf(fmaxf(z[4 * g + 0], z[4 * g + 1]), fmaxf(z[4 * g + 2], z[4 * g + 3]));
-                    q.y = fmaxf(fmaxf(z[4 * g + 4], z[4 * g + 5]), fmaxf(z[4 * g + 6], z[4 * g + 7]));
-                    q.z = fmaxf(fmaxf(z[4 * g + 8], z[4 * g + 9]), fmaxf(z[4 * g + 10], z[4 * g + 11]));
-                    q.w = fmaxf(fmaxf(z[4 * g + 12], z[4 * g + 13]), fmaxf(z[4 * g + 14], z[4 * g + 15]));
-                    *(float4*)&gr[16 * cq + g] = q;
-                    tm = fmaxf(tm, fmaxf(fmaxf(q.x, q.y), fmaxf(q.z, q.w)));
-                }
-            } else {
-#pragma unroll
-                for (int g = 0; g < 8; g += 4) {
-                    float q4[4];
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        float m8 = z[8 * (g + u)];
-#pragma unroll
-                        for (int e = 1; e < 8; ++e) m8 = fmaxf(m8, z[8 * (g + u) + e]);
-                        q4[u] = m8;
-                    }
-                    *(float4*)&gr[8 * cq + g] = make_float4(q4[0], q4[1], q4[2], q4[3]);
-                    tm = fmaxf(tm, fmaxf(fmaxf(q4[0], q4[1]), fmaxf(q4[2], q4[3])));
-                }
+        int t;
+        // t = -1: a dry run of the whole tile epilogue while tile 0 still streams, on
+        // the idle accumulator buffer 1 with every global / state side effect masked:
+        // the code runs once per tile, so its first execution is instruction-fetch
+        // bound (~500 cycles per KB of code, measured) -- warm it before it counts
+        for (t = hp.warm ? -1 : 0; t < 0 || has_tile(t); ++t) {
+            const bool dry = t < 0;
+            int t0 = 0, tn = kHlTile;
+            if (!dry) {
+                tile_range(t, t0, tn);
+                seen += tn;
             }
+            const int b = dry ? 1 : (t & 1);
+            // (two-list mode: resolving the next tile may wait for the union here)
+            const bool last = !dry && !has_tile(t + 1);
+            if (!dry) {
+                mbar_wait_sleep(&tfull[b], (uint32_t)(t >> 1) & 1, 200);
+                if (warp == 0 && lane == 0) HL_TRACE(t == 0 ? 3 : 5);
+                HL_CLK(0);
+            }
+            tc_fence_after();
+            const uint32_t taddr = tmem_base + ((uint32_t)(32 * qd) << 16) + (uint32_t)(b * kHlTile);
+            const float it = a.inv_temp;
+            if (last) {
+                // the CTA's last tile: its logits go to shared memory (the ring is idle
+                // now) and all 14 warps finish its rows below, one warp per row
+                float z[64];
+                hl_load64(taddr, cq, z);
+                float* zr = (float*)base + r * kHlZS;
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        float4 w;
+                        const int col = 64 * c + 16 * cq + 4 * q;
+                        w.x = (rv && col + 0 < tn) ? z[16 * c + 4 * q + 0] * it : -INFINITY;
+                        w.y = (rv && col + 1 < tn) ? z[16 * c + 4 * q + 1] * it : -INFINITY;
+                        w.z = (rv && col + 2 < tn) ? z[16 * c + 4 * q + 2] * it : -INFINITY;
+                        w.w = (rv && col + 3 < tn) ? z[16 * c + 4 * q + 3] * it : -INFINITY;
+                        *(float4*)&zr[col] = w;
+                    }
+                if (a.logits_out)   // debug output (out of line: re-read from TMEM; the whole warp loads)
+                    hl_logits_out(taddr, rv ? tn : 0, cq, it, a.logits_out + (size_t)(rv ? r : 0) * a.n_subset_max + t0);
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&tempty[b]);
+                if (warp == 0 && lane == 0) { fin_tile[0] = t0; fin_tile[1] = tn; fin_tile[2] = seen; }
+                HL_CLK(1);
+                break;
+            }
+            // ---- pass A: the thread's 64 logits in one TMEM round trip (a load costs ~1000
+            // cycles with 8 warps loading, measured), its maximum, exp sum and 16
+            // four-column group maxima, of which it publishes the 8 largest (sorted)
+            float z[64];
+            hl_load64(taddr, cq, z);
+#pragma unroll
+            for (int j = 0; j < 64; ++j) z[j] = (rv && hl_col(cq, j) < tn) ? z[j] * it : -INFINITY;
+            if (!dry) HL_CLK(10);
+            float g[16];
+#pragma unroll
+            for (int u = 0; u < 16; ++u)
+                g[u] = fmaxf(fmaxf(z[4 * u], z[4 * u + 1]), fmaxf(z[4 * u + 2], z[4 * u + 3]));
+            float tm = g[0];
+#pragma unroll
+            for (int u = 1; u < 16; ++u) tm = fmaxf(tm, g[u]);
+            float ts = 0.0f;
+            if (tm != -INFINITY) {
+                const float mb = tm * kL2E;
+                float e0 = 0.0f, e1 = 0.0f, e2 = 0.0f, e3 = 0.0f;
+#pragma unroll
+                for (int j = 0; j < 64; j += 4) {
+                    e0 += ex2f(fmaf(z[j], kL2E, -mb));
+                    e1 += ex2f(fmaf(z[j + 1], kL2E, -mb));
+                    e2 += ex2f(fmaf(z[j + 2], kL2E, -mb));
+                    e3 += ex2f(fmaf(z[j + 3], kL2E, -mb));
+                }
+                ts = (e0 + e1) + (e2 + e3);
+            }
+            if (!dry) HL_CLK(12);
+            bitonic_desc16(g);
+            if (!dry) HL_CLK(13);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) gr[8 * cq + u] = g[u];
+            if (cq == 0) gr[32] = -INFINITY;   // run-end sentinel of the merge below
             t_m[r * 4 + cq] = tm;
+            t_s[r * 4 + cq] = ts;
+            if (cq == 0) ctr[r] = st_n[r];   // the append counter
+            HL_CLK(1);
             hl_bar();
             HL_CLK(2);
-            // softmax partial against the new row maximum
-            const float m_old = st_m[r];
-            const float4 tmv = *(const float4*)&t_m[r * 4];
-            const float m_new = fmaxf(m_old, fmaxf(fmaxf(tmv.x, tmv.y), fmaxf(tmv.z, tmv.w)));
-            float s = 0.0f;
-            if (m_new != -INFINITY) {
-                const float mb = m_new * kL2E;
-#pragma unroll
-                for (int j = 0; j < 64; ++j) s += ex2f(fmaf(z[j], kL2E, -mb));
-            }
-            t_s[r * 4 + cq] = s;
-            HL_CLK(3);
-            // candidate bound: the KP-th largest of the row's 32 group maxima (every thread
-            // of the row sorts the same 32 in registers: no barrier, no shared result).
-            // (Tiles of <= 128 rows: threads 0 and 1 hold all 32 non-empty 4-column groups.)
             const int n_old = st_n[r];
+            // bound B: the KP-th largest of the 32 published group maxima (distinct groups:
+            // at least KP values are >= B, so nothing below B is in the row's best KP),
+            // by a KP-step merge of the 4 sorted runs (every thread of the row, no barrier)
             float B = -INFINITY;
             if (rv && n_old + tn > kHlCap) {
-                float v[32];
-#pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                    const float4 o = *(const float4*)&gr[4 * q];
-                    v[4 * q] = o.x; v[4 * q + 1] = o.y; v[4 * q + 2] = o.z; v[4 * q + 3] = o.w;
+                // branch-free: the rows of a warp pop different runs; the run ends are
+                // -inf sentinels (gr[32])
+                int i0 = 0, i1 = 8, i2 = 16, i3 = 24;
+                float h0 = gr[0], h1 = gr[8], h2 = gr[16], h3 = gr[24];
+#pragma unroll 1
+                for (int k = 0; k < KP; ++k) {
+                    const float m = fmaxf(fmaxf(h0, h1), fmaxf(h2, h3));
+                    B = m;
+                    const bool s0 = h0 == m, s1 = !s0 && h1 == m, s2 = !s0 && !s1 && h2 == m;
+                    const bool s3 = !s0 && !s1 && !s2;
+                    const int lim = s0 ? 8 : s1 ? 16 : s2 ? 24 : 32;
+                    const int ni = (s0 ? i0 : s1 ? i1 : s2 ? i2 : i3) + 1;
+                    const float nv = gr[ni < lim ? ni : 32];
+                    i0 = s0 ? ni : i0; h0 = s0 ? nv : h0;
+                    i1 = s1 ? ni : i1; h1 = s1 ? nv : h1;
+                    i2 = s2 ? ni : i2; h2 = s2 ? nv : h2;
+                    i3 = s3 ? ni : i3; h3 = s3 ? nv : h3;
                 }
-                bitonic_desc32(v);
-#pragma unroll
-                for (int i = 0; i < 32; ++i) B = (i == KP - 1) ? v[i] : B;
             }
-            HL_CLK(4);
-            // admission: >= this tile's bound and strictly above the running bound
             const float Br = b_run[r];
+            HL_CLK(3);
+            // ---- pass B: admission (>= B, > the running bound); the row's slots reserved
+            // with one shared atomic, values written if they fit (else: overflow)
             uint32_t mlo = 0u, mhi = 0u;
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
                 mlo |= (uint32_t)(z[j] >= B && z[j] > Br) << j;
                 mhi |= (uint32_t)(z[32 + j] >= B && z[32 + j] > Br) << j;
             }
-            t_c[r * 4 + cq] = __popc(mlo) + __popc(mhi);
-            hl_bar();
-            HL_CLK(5);
-            {
-                const int4 cc = *(const int4*)&t_c[r * 4];
-                const int pre = (cq > 0 ? cc.x : 0) + (cq > 1 ? cc.y : 0) + (cq > 2 ? cc.z : 0);
-                const int tot = n_old + cc.x + cc.y + cc.z + cc.w;
-                if (tot <= kHlCap) {
-                    int o = n_old + pre;
+            const int na = __popc(mlo) + __popc(mhi);
+            if (na) {
+                const int ob = atomicAdd(&ctr[r], na);
+                if (ob + na <= kHlCap) {
+                    const int o1 = ob + __popc(mlo);
 #pragma unroll
-                    for (int j = 0; j < 64; ++j) {
-                        if (((j < 32 ? mlo : mhi) >> (j & 31)) & 1u) {
+                    for (int j = 0; j < 32; ++j) {
+                        if ((mlo >> j) & 1u) {
+                            const int o = ob + __popc(mlo & ((1u << j) - 1u));
                             bv[o] = z[j];
-                            bp[o] = t0 + c0 + j;
-                            ++o;
+                            bp[o] = t0 + hl_col(cq, j);
+                        }
+                        if ((mhi >> j) & 1u) {
+                            const int o = o1 + __popc(mhi & ((1u << j) - 1u));
+                            bv[o] = z[32 + j];
+                            bp[o] = t0 + hl_col(cq, 32 + j);
                         }
                     }
-                } else if (cq == 0) {
-                    ovf[r] = 1;
-                    *any_ovf = 1;
                 }
-                if (cq == 0) t_x[r * 4] = tot;   // (read by the state update below)
             }
-            hl_bar();
             HL_CLK(6);
-            if (a.logits_out)   // debug output (out of line: re-read from TMEM; the whole warp loads)
-                hl_logits_out(taddr, rv ? tn : 0, c0, a.inv_temp, a.logits_out + (size_t)(rv ? r : 0) * a.n_subset_max + t0);
+            hl_bar();
+            const int tot = ctr[r];
+            if (!dry && cq == 0 && rv && tot > kHlCap) { ovf[r] = 1; *any_ovf = 1; }
+            hl_bar();
+            if (a.logits_out && !dry)   // debug output (out of line: re-read from TMEM; the whole warp loads)
+                hl_logits_out(taddr, rv ? tn : 0, cq, it, a.logits_out + (size_t)(rv ? r : 0) * a.n_subset_max + t0);
             if (*any_ovf)   // rare (ties): out of line, so the common path keeps its registers
-                hl_overflow(taddr, rv, rv && ovf[r], tn, c0, a.inv_temp, B, Br, KP, n_old, t0, r, cq, bv, bp, t_c, t_x,
+                hl_overflow(taddr, rv, rv && ovf[r], tn, it, B, Br, KP, n_old, t0, r, cq, bv, bp, t_c, t_x,
                             st_n, b_run);
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[b]);   // the MMA may reuse this accumulator
+            if (lane == 0 && !dry) mbar_arrive(&tempty[b]);   // the MMA may reuse this accumulator
             HL_CLK(7);
-            // state update (one thread per row)
+            // state update (one thread per row): merge the 4 threads' (max, sum), then the running pair
             if (cq == 0 && rv) {
+                const float4 mv = *(const float4*)&t_m[r * 4];
                 const float4 sv = *(const float4*)&t_s[r * 4];
-                const float sn = (sv.x + sv.y) + (sv.z + sv.w);
-                st_s[r] = (m_old == -INFINITY ? 0.0f : st_s[r] * ex2f((m_old - m_new) * kL2E)) + sn;
-                st_m[r] = m_new;
-                if (!ovf[r]) st_n[r] = t_x[r * 4];
-                ovf[r] = 0;
+                const float mt = fmaxf(fmaxf(mv.x, mv.y), fmaxf(mv.z, mv.w));
+                auto term = [&](float mm, float ss) { return mm == -INFINITY ? 0.0f : ss * ex2f((mm - mt) * kL2E); };
+                const float stile = (term(mv.x, sv.x) + term(mv.y, sv.y)) + (term(mv.z, sv.z) + term(mv.w, sv.w));
+                const float mo = st_m[r], mn = fmaxf(mo, mt);
+                const float so = mo == -INFINITY ? 0.0f : st_s[r] * ex2f((mo - mn) * kL2E);
+                const float sn = mt == -INFINITY ? 0.0f : stile * ex2f((mt - mn) * kL2E);
+                if (!dry) {
+                    st_s[r] = so + sn;
+                    st_m[r] = mn;
+                    if (!ovf[r]) st_n[r] = tot;
+                    ovf[r] = 0;
+                }
             }
             hl_bar();
             if (warp == 0 && lane == 0 && t == 0) HL_TRACE(4);
             if (cq == 0 && r == 0) *any_ovf = 0;   // (every reader passed the barrier above)
             HL_CLK(8);
-            const bool last = !has_tile(t + 1);    // (two-list mode: may wait for the union here)
             const int n = st_n[r];
-            if (last) {
-                // the buffer (a superset of the CTA row's best KP, unsorted) into the CTA's
-                // list: entries [0, n), -inf pads to LS = 64 (the finalisation's buffered format:
-                // cnt = 0, xcnt = n)
-                if (rv) {
-                    const size_t o = (size_t)bid * a.n_h + r;
-                    for (int i = cq; i < LS; i += 4) {
-                        const bool h = i < n;
-                        a.part.val[o * LS + i] = h ? bv[i] : -INFINITY;
-                        a.part.id[o * LS + i] = h ? bp[i] : -1;
-                    }
-                    if (warp == 0 && lane == 0) HL_TRACE(6);
-                    HL_CLK(9);
-                    if (cq == 0) {
-                        a.part.m[o] = st_m[r];
-                        a.part.s[o] = st_s[r];
-                        a.part.cnt[o] = 0;
-                        a.part.xcnt[o] = n;
-                    }
-                }
-            } else {
-                // cut the buffer to its exact top KP (ranked into the group-maxima rows,
+            if (!dry) {
+                // a middle tile: cut the buffer to its exact top KP (ranked into the group-maxima rows,
                 // then copied back); its KP-th entry bounds later tiles
                 const bool cut = rv && n > KP;
                 float* sv = gr;                   // [KP] values
@@ -650,19 +811,109 @@ lmh_hl_kernel(const __grid_constant__ CUtensorMap tmap_h, LmhArgs a, HlParams hp
                 }
             }
         }
-        if (t == 0 && rv) {   // no tile: an empty list (m = -inf, s = 0)
-            const size_t o = (size_t)bid * a.n_h + r;
-            for (int i = cq; i < LS; i += 4) {
-                a.part.val[o * LS + i] = -INFINITY;
-                a.part.id[o * LS + i] = -1;
+    }
+    // ===== the CTA's last tile, one warp per row (all 14 warps): its logits are staged
+    // in shared memory by the epilogue warps (zs rows of kHlZS floats, -inf outside the
+    // tile / the tree rows). Per row: the row maximum and exp sum (warp shuffles) merged
+    // with the running pair of earlier tiles; the candidate bound B = the KP-th largest
+    // of the 32 lane maxima (warp bitonic sort; >= KP distinct values are >= B); the
+    // values >= B (and > the running bound) appended to the row's buffer by ballot
+    // prefix; a buffer overflow (ties) takes the exact warp-level selection; the buffer
+    // is written out as the CTA's list (unsorted, -inf padded: the finalisation's
+    // buffered format cnt = 0, xcnt = n).
+    __syncwarp();   // (role branches diverge inside a warp: reconverge before the aligned barrier)
+    named_bar_sync(2, kHlThreads);
+    HL_CLK(2);
+    {
+        const int KP = a.KP, LS = a.LS;
+        const bool any = has_tile(0);
+        const int ft0 = any ? fin_tile[0] : 0, ftn = any ? fin_tile[1] : 0, fseen = any ? fin_tile[2] : 0;
+        const float* zs = (const float*)base;
+        const int nrep = (hp.exp & 512) ? 2 : 1;   // experiment: run the phase twice (I-cache)
+        for (int rep = 0; rep < nrep; ++rep) {
+        if (rep == nrep - 1) HL_CLK(3);
+        const bool wr = rep == nrep - 1;
+        for (int rr = warp; rr < a.n_h; rr += kHlWarps) {
+            const size_t o = (size_t)bid * a.n_h + rr;
+            float* rbv = buf_v + rr * kHlCapS;
+            int* rbp = buf_p + rr * kHlCapS;
+            float mfin = -INFINITY, sfin = 0.0f;
+            int n = 0;
+            if (any && !(hp.exp & 256)) {
+                float v[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) v[j] = zs[rr * kHlZS + lane + 32 * j];
+                float lm = v[0];
+#pragma unroll
+                for (int j = 1; j < 8; ++j) lm = fmaxf(lm, v[j]);
+                const float M = warp_max(lm);
+                float sacc = 0.0f;
+                if (M != -INFINITY) {
+                    const float mb = M * kL2E;
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) sacc += ex2f(fmaf(v[j], kL2E, -mb));
+                }
+                sacc = warp_sum(sacc);
+                const float mo = st_m[rr], so = st_s[rr];
+                mfin = fmaxf(mo, M);
+                sfin = (mo == -INFINITY ? 0.0f : so * ex2f((mo - mfin) * kL2E)) +
+                       (M == -INFINITY ? 0.0f : sacc * ex2f((M - mfin) * kL2E));
+                const int n_old = st_n[rr];
+                const float Br = b_run[rr];
+                float B = -INFINITY;
+                if (n_old + ftn > kHlCap) {   // the KP-th largest lane maximum (KP <= 32)
+                    float x = lm;
+#pragma unroll 1
+                    for (int k = 2; k <= 32; k <<= 1)
+#pragma unroll 1
+                        for (int j = k >> 1; j > 0; j >>= 1) {
+                            const float y = __shfl_xor_sync(0xffffffffu, x, j);
+                            x = (((lane & k) == 0) == ((lane & j) == 0)) ? fmaxf(x, y) : fminf(x, y);
+                        }
+                    B = __shfl_sync(0xffffffffu, x, KP - 1);
+                }
+                uint32_t bal[8];
+                int cnt = 0;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    bal[j] = __ballot_sync(0xffffffffu, v[j] >= B && v[j] > Br);
+                    cnt += __popc(bal[j]);
+                }
+                if (n_old + cnt <= kHlCap) {
+                    int pos = n_old;
+                    const uint32_t lt = (1u << lane) - 1u;
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        if (wr && ((bal[j] >> lane) & 1u)) {
+                            const int sl = pos + __popc(bal[j] & lt);
+                            rbv[sl] = v[j];
+                            rbp[sl] = ft0 + lane + 32 * j;
+                        }
+                        pos += __popc(bal[j]);
+                    }
+                    n = n_old + cnt;
+                } else if (wr) {
+                    hl_warp_select(zs + rr * kHlZS, B, Br, rbv, rbp, n_old, ft0, KP, lane);   // (rare: ties)
+                    n = KP;
+                }
+                __syncwarp();
             }
-            if (cq == 0) {
-                a.part.m[o] = -INFINITY;
-                a.part.s[o] = 0.0f;
+            for (int i = lane; i < LS && wr && !(hp.exp & 128); i += 32) {
+                const bool h = i < n;
+                a.part.val[o * LS + i] = h ? rbv[i] : -INFINITY;
+                a.part.id[o * LS + i] = h ? rbp[i] : -1;
+            }
+            if (lane == 0 && wr) {
+                a.part.m[o] = mfin;
+                a.part.s[o] = sfin;
                 a.part.cnt[o] = 0;
-                a.part.xcnt[o] = 0;
+                a.part.xcnt[o] = n;
             }
         }
+        }
+        (void)fseen;
+        if (warp == 0 && lane == 0) HL_TRACE(6);
+        HL_CLK(9);
     }
     tc_fence_before();
     __syncthreads();
@@ -703,7 +954,9 @@ cudaError_t launch_lmh_hl(const LmhArgs& a, cudaStream_t st) {
     const int kps = std::max(1, std::min(hp.nkb, budget / S / unit));
     hp.slot_bytes = kps * unit;
     if (budget / hp.slot_bytes < S) S = budget / hp.slot_bytes;
-    if (S < 2) return cudaErrorInvalidConfiguration;
+    // the ring also holds the last tile's staged logits (64 rows x kHlZS floats)
+    while (S * hp.slot_bytes < kHlRows * kHlZS * 4 && (S + 1) * hp.slot_bytes <= budget && S < kHlMaxSlots) ++S;
+    if (S < 2 || S * hp.slot_bytes < kHlRows * kHlZS * 4) return cudaErrorInvalidConfiguration;
     hp.slots = S;
     hp.off_epi = S * hp.slot_bytes;   // (>= 8 KB after the ring: the M = 128 A operand reads past a slot's H block)
     hp.off_bar = (hp.off_epi + epi + 15) & ~15;
@@ -713,6 +966,8 @@ cudaError_t launch_lmh_hl(const LmhArgs& a, cudaStream_t st) {
     uint64_t hrows = (uint64_t)a.n_h;
     static const int hexp = getenv("EVOSPEC_HL_EXP") ? atoi(getenv("EVOSPEC_HL_EXP")) : 0;
     hp.exp = hexp;
+    static const int warm = getenv("EVOSPEC_HL_WARM") ? atoi(getenv("EVOSPEC_HL_WARM")) : 0;
+    hp.warm = warm;
     static const bool hrep = getenv("EVOSPEC_HL_HREP") != nullptr;
     if (hrep) {   // experiment: one private copy of H per CTA (no shared L2 lines)
         static void* rep = nullptr;

@@ -48,8 +48,6 @@ constexpr int kTcMmaWarp = kProdWarps;
 constexpr int kTcEpiWarp0 = kProdWarps + 1;
 constexpr int kTcEpiWarps = 8;
 constexpr int kTcWarps = kProdWarps + 1 + kTcEpiWarps;
-constexpr int kPfBytes = 1024;     // L2 prefetch window per row (8 stages of 128 B)
-constexpr int kPfDist = 0;         // windows ahead (0 = off: measured slower on B200, profiles/r01_trace_lmh.log)
 constexpr int kBlockK = 64;        // bf16 columns per stage = one 128-byte swizzle atom row
 constexpr int kTileM = 128;
 constexpr int kLastTile = 128;    // rows of a short last tile (128 = no split; see the launch)
@@ -63,7 +61,7 @@ struct TcParams {
     int stages;
     int nkb;         // d / 64
     uint32_t tmem_cols;
-    int pf_dist;     // L2 prefetch distance in 1 KB windows (0 = off)
+    int kps;         // K-blocks per barrier stage (ring buffers = stages * kps)
     int last_tile;   // rows of a CTA's short last tile (ranges longer than one tile)
     int dyn_tile;    // two-list mode: rows per second-list tile (EVOSPEC_DYN_TILE)
     int dyn_stride;  // two-list mode: CTA rank stride of the second-list round robin
@@ -225,46 +223,11 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
         // one warp instruction moves 4 whole 128-byte row segments.
         const uint64_t pol_w = policy_evict_first(), pol_h = policy_evict_last();
         const int chunk = lane & 7;
-        // L2 prefetch: thread p (0..127) owns tile row p and pulls its row into L2
-        // in 1 KB windows (8 stages) kPfDist windows ahead of the cp.async stream,
-        // so DRAM sees 1 KB contiguous reads per row instead of 128 B pieces.
-        const int prow = warp * 32 + lane;
         const size_t row_bytes = (size_t)a.d * 2;
-        const int n_win = (int)((row_bytes + kPfBytes - 1) / kPfBytes);
-        auto row_ptr_of = [&](int t, int row) -> const char* {
-            int t0, tn;
-            tile_range(t, t0, tn);
-            const int pos = t0 + (row < tn ? row : 0);
-            return (const char*)a.W + (size_t)(a.subset[pos] / a.R) * row_bytes;
-        };
-        auto prefetch_win = [&](const char* rp, int w) {
-            if (w < 0 || w >= n_win) return;
-            const size_t off = (size_t)w * kPfBytes;
-            const uint32_t sz = (uint32_t)min((size_t)kPfBytes, row_bytes - off);
-            l2_prefetch(rp + off, sz);
-        };
-        const int pf_dist = tp.pf_dist;
-        const int pf_dist_eff = a.list2 ? 0 : pf_dist;   // (prefetch: one-list mode only)
-        const int n_tiles = n_tiles1;
-        const char* pf_cur = n_tiles > 0 && pf_dist_eff > 0 ? row_ptr_of(0, prow) : nullptr;
-        for (int w = 0; w < pf_dist_eff && pf_cur; ++w) prefetch_win(pf_cur, w);
+        const int KPS = tp.kps;
         int stage = 0;
         uint32_t phase = 0;
-        for (int t = 0;; ++t) {
-            if (t == n_tiles1 && a.pf_ids) {
-                // first list issued: pull this CTA's slice of the candidate rows into L2
-                // (HBM is otherwise idle until the union ends; the second list then streams
-                // from L2). Read without the wait: stale ids only cost wasted prefetches.
-                const int n = min(*(volatile const int*)a.pf_n, a.pf_cap);
-                const int c0 = (int)((long long)n * blockIdx.x / gridDim.x);
-                const int c1 = (int)((long long)n * (blockIdx.x + 1) / gridDim.x);
-                for (int i = c0 + warp * 32 + lane; i < c1; i += kProdWarps * 32) {
-                    const int id = __ldcg(&a.pf_ids[i]);
-                    if (id >= 0 && (int64_t)(id / a.R) < a.n_w_rows)
-                        l2_prefetch((const char*)a.W + (size_t)(id / a.R) * row_bytes, (uint32_t)row_bytes);
-                }
-            }
-            if (!has_tile(t)) break;
+        for (int t = 0; has_tile(t); ++t) {
             int t0, tn;
             tile_range(t, t0, tn);
             const char* src[8];
@@ -276,28 +239,33 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
                 src[i] = (const char*)a.W + (size_t)(lmh_id_at(a, pos) / a.R) * row_bytes + chunk * 16;
                 dsto[i] = (uint32_t)(row * 128 + ((chunk ^ (row & 7)) << 4));
             }
-            const char* pf_next = t + 1 < n_tiles && pf_dist_eff > 0 ? row_ptr_of(t + 1, prow) : nullptr;
-            for (int kb = 0; kb < tp.nkb; ++kb) {
-                // prefetch: window (kb/8 + kPfDist) of this tile; the next tile's first
-                // windows once this tile's remaining windows are all requested
-                if (pf_dist_eff > 0 && (kb & 7) == 0) {
-                    const int w = (kb >> 3) + pf_dist_eff;
-                    if (w < n_win) prefetch_win(pf_cur, w);
-                    else if (pf_next) prefetch_win(pf_next, w - n_win);
-                }
+            // a barrier stage carries KPS K-blocks (ring buffers stage * KPS + j): the
+            // stage handshake (consumer wait, MMA issue, commit) costs ~0.3-0.5 us
+            // whatever its size (measured), so it is paid once per KPS K-blocks
+            for (int kb0 = 0; kb0 < tp.nkb; kb0 += KPS) {
+                const int nk = min(KPS, tp.nkb - kb0);
                 mbar_wait(&empty[stage], phase ^ 1);
                 if (warp == 0 && lane == 0) {
-                    mbar_arrive_expect_tx(&full[stage], (uint32_t)(NP * 128));
-                    tma_load_2d(smB + (size_t)stage * NP * 128, &tmap_h, &full[stage], kb * kBlockK, h_row0, pol_h);
+                    mbar_arrive_expect_tx(&full[stage], (uint32_t)(nk * NP * 128));
+                    for (int j = 0; j < nk; ++j)
+                        tma_load_2d(smB + (size_t)(stage * KPS + j) * NP * 128, &tmap_h, &full[stage],
+                                    (kb0 + j) * kBlockK, h_row0, pol_h);
                 }
-                const uint32_t dA = smem_u32(smA + (size_t)stage * kTileM * 128);
+                for (int j = 0; j < nk; ++j) {
+                    const uint32_t dA = smem_u32(smA + (size_t)(stage * KPS + j) * kTileM * 128);
+                    const int ko = (kb0 + j) * 128;
+                    if (tn == kTileM) {
 #pragma unroll
-                for (int i = 0; i < 8; ++i)   // rows past the tile's end are never read back
-                    if (16 * i + 4 * warp + (lane >> 3) < tn) cp_async16(dA + dsto[i], src[i] + kb * 128, pol_w);
+                        for (int i = 0; i < 8; ++i) cp_async16(dA + dsto[i], src[i] + ko, pol_w);
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < 8; ++i)   // rows past the tile's end are never read back
+                            if (16 * i + 4 * warp + (lane >> 3) < tn) cp_async16(dA + dsto[i], src[i] + ko, pol_w);
+                    }
+                }
                 cp_async_arrive_noinc(&full[stage]);
                 if (++stage == S) { stage = 0; phase ^= 1; }
             }
-            pf_cur = pf_next;
         }
         if (warp == 0 && lane == 0) TC_TRACE(1);
         (void)tmap_w;
@@ -312,18 +280,21 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
             if (t >= 2) mbar_wait(&tempty[b], (use - 1) & 1);
             tc_fence_after();
             const uint32_t tmem_d = tmem_base + (uint32_t)(b * NP);
-            for (int kb = 0; kb < tp.nkb; ++kb) {
+            for (int kb0 = 0; kb0 < tp.nkb; kb0 += tp.kps) {
+                const int nk = min(tp.kps, tp.nkb - kb0);
                 mbar_wait(&full[stage], phase);
                 tc_fence_after();
                 if (lane == 0) {
-                    const uint32_t aaddr = smem_u32(smA + (size_t)stage * kTileM * 128);
-                    const uint32_t baddr = smem_u32(smB + (size_t)stage * NP * 128);
+                    for (int j = 0; j < nk; ++j) {
+                        const uint32_t aaddr = smem_u32(smA + (size_t)(stage * tp.kps + j) * kTileM * 128);
+                        const uint32_t baddr = smem_u32(smB + (size_t)(stage * tp.kps + j) * NP * 128);
 #pragma unroll
-                    for (int k = 0; k < kBlockK / 16; ++k)
-                        umma_bf16(tmem_d, umma_desc_sw128(aaddr + k * 32), umma_desc_sw128(baddr + k * 32), idesc,
-                                  (kb | k) != 0);
+                        for (int k = 0; k < kBlockK / 16; ++k)
+                            umma_bf16(tmem_d, umma_desc_sw128(aaddr + k * 32), umma_desc_sw128(baddr + k * 32), idesc,
+                                      ((kb0 + j) | k) != 0);
+                    }
                     umma_commit(&empty[stage]);
-                    if (kb == tp.nkb - 1) umma_commit(&tfull[b]);
+                    if (kb0 + tp.kps >= tp.nkb) umma_commit(&tfull[b]);
                 }
                 __syncwarp();
                 if (++stage == S) { stage = 0; phase ^= 1; }
@@ -470,8 +441,6 @@ cudaError_t launch_lmh_tc(const LmhArgs& a, cudaStream_t st) {
     const int rows = a.nseg > 0 ? a.seg_rows : a.n_h;
     tp.n_pad = ((rows + 15) / 16) * 16;
     tp.nkb = a.d / kBlockK;
-    tp.pf_dist = kPfDist;
-    if (const char* e = getenv("EVOSPEC_PF")) tp.pf_dist = atoi(e);
     tp.last_tile = kLastTile;
     tp.dyn_tile = kTileM;
     tp.dyn_stride = 1;
@@ -490,13 +459,18 @@ cudaError_t launch_lmh_tc(const LmhArgs& a, cudaStream_t st) {
     const size_t epi = epi_smem_bytes(rows, (a.KP <= 32 && a.LS == kBuf) ? kBuf : a.KP, kTcWarps);
     const size_t fixed = epi + 2 * 128 * 4 + 64 * 8 + 1024 /*align slack*/ + 256;
     const size_t budget = 227 * 1024;
-    int S = (int)((budget - fixed) / (stage_a + stage_b));
-    S = std::min(S, 8);
-    if (const char* e = getenv("EVOSPEC_STAGES")) S = std::max(2, std::min(S, atoi(e)));
+    int SS = (int)((budget - fixed) / (stage_a + stage_b));   // ring buffers (one K-block each)
+    SS = std::min(SS, 8);   // (12 buffers measured slower: 36,864 rows 101 vs 87 us)
+    // K-blocks per barrier stage (EVOSPEC_TC_KPS, default 1): 2 and 3 measured equal
+    // here (the stage handshake is hidden by the 8-buffer ring), unlike in lmh_hl
+    static const int kps_env = getenv("EVOSPEC_TC_KPS") ? atoi(getenv("EVOSPEC_TC_KPS")) : 1;
+    int kps = std::max(1, std::min(kps_env, SS / 2));
+    const int S = SS / kps;
     if (S < 2) return cudaErrorInvalidConfiguration;
     tp.stages = S;
-    tp.off_b = (size_t)S * stage_a;
-    tp.off_epi = tp.off_b + (size_t)S * stage_b;
+    tp.kps = kps;
+    tp.off_b = (size_t)S * kps * stage_a;
+    tp.off_epi = tp.off_b + (size_t)S * kps * stage_b;
     tp.off_bar = (tp.off_epi + epi + 15) & ~(size_t)15;
     tp.off_rows = tp.off_bar + (size_t)(2 * S + 4) * 8 + 16;
     const size_t smem = tp.off_rows + 2 * 128 * 4 + 1024;

@@ -28,7 +28,7 @@ for n_S in [int(x) for x in os.environ.get("TRACE_NS", "8192,36864").split(",")]
     nd = torch.tensor([n_S], dtype=torch.int32, device="cuda")
     evs = []
     for it in range(8):
-        flush.fill_(it)
+        if not os.environ.get("TRACE_NOFLUSH"): flush.fill_(it)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         ctx.subset_logits_topk(Wd, Hd, Sd, nd, n_S, k)
@@ -55,7 +55,7 @@ for n_S in [int(x) for x in os.environ.get("TRACE_NS", "8192,36864").split(",")]
     clk = ctx.read_trace(296 * 8 + 48 + 16)[296 * 8 + 48:].astype(np.int64)
     if clk[0] > 0:
         print("   CTA0 warp0 epilogue clock64 (cycles from tfull): ",
-              {i: int(clk[i] - clk[0]) for i in range(1, 10) if clk[i] > 0})
+              {i: int(clk[i] - clk[0]) for i in range(1, 16) if clk[i] > 0})
     g0 = ctx.read_trace(296 * 8 + 48 + 32)[296 * 8 + 48 + 16:].astype(np.float64)
     if g0[0] > 0:
         print("   CTA0 (us from its start):", {n: round((g0[i] - tr[0, 0]) / 1e3, 2) for i, n in enumerate(
