@@ -31,8 +31,13 @@
  *     EVOSPEC_ENCCL. Device-side conditions (unsorted or out-of-range ids when
  *     debug_checks = 1, a top-k row whose exact order could not be certified,
  *     a selection tie band larger than the workspace) are accumulated in a
- *     device flag word read by evospec_get_flags(). Detail for the last error
- *     on the calling thread: evospec_last_error().
+ *     device flag word read by evospec_get_flags(). With debug_checks = 1 the
+ *     build / LM-head calls synchronize their stream before returning and
+ *     return EVOSPEC_EINVARIANT when an invariant flag (EVOSPEC_FLAG_BAD_IDS,
+ *     EVOSPEC_FLAG_BUDGET) is set -- the SPEC's invariant exit on the
+ *     product path; without debug_checks, evospec_sync_status() gives the same
+ *     verdict at a point the caller chooses. Detail for the last error on the
+ *     calling thread: evospec_last_error().
  */
 #ifndef EVOSPEC_H
 #define EVOSPEC_H
@@ -112,6 +117,11 @@ evospec_status evospec_prepare_weights(evospec_ctx *ctx, const void *W_local_dev
 /* Reads (and with clear=1 resets) the device flag word. Synchronises the
  * stream. flags_out: host int32. */
 evospec_status evospec_get_flags(evospec_ctx *ctx, int32_t *flags_out, int clear, void *stream);
+/* Synchronizes `stream` and returns EVOSPEC_EINVARIANT if an invariant flag
+ * (EVOSPEC_FLAG_BAD_IDS or EVOSPEC_FLAG_BUDGET) is set in the context's flag
+ * word (flags are left as they are; evospec_get_flags clears), else EVOSPEC_OK;
+ * CUDA errors as EVOSPEC_ECUDA. */
+evospec_status evospec_sync_status(evospec_ctx *ctx, void *stream);
 
 /* ---- multi-GPU communicator (vocab sharding) ---------------- */
 
@@ -155,6 +165,28 @@ evospec_status evospec_build_subset(evospec_ctx *ctx,
     int32_t *out_ids, int32_t *out_n,
     int32_t *out_local_ids, int32_t *out_local_n,
     void *stream);
+
+/* The sharded build in two steps, without a communicator (the
+ * NCCL path of evospec_build_subset is step 1, an all-gather, step 2):
+ * 1. evospec_build_local_candidates: this shard's exact semantic top-n_sem
+ *    (a2, P:95-96 over the shard's rows: E_local [n_e_rows = this shard's row
+ *    count, d], global id = local row * R + r) -> out_s [n_sem] fp64 scores,
+ *    out_id [n_sem] int32 global ids (device; ordered by (s desc, id asc);
+ *    padded with id -1 when the shard has fewer rows).
+ * 2. evospec_build_subset_from_candidates: the R shards' candidates stacked in
+ *    rank order (cand_s / cand_id [n_cand = R * n_sem], device) -> the global
+ *    exact top-n_sem and the formation / union of evospec_build_subset (a2-a4):
+ *    every rank gets the same S and its owned slice. The caller moves the
+ *    candidates between GPUs (or stacks them on one GPU, as the parity tests do).
+ * EVOSPEC_EINPUT on null / out-of-range arguments (n_e_rows not this shard's,
+ * n_sem outside [1, max_sem], n_cand outside [1, R * max_sem]). Async. */
+evospec_status evospec_build_local_candidates(evospec_ctx *ctx, const void *E_local, int64_t n_e_rows,
+    const void *q_dev, int32_t n_sem, double *out_s, int32_t *out_id, void *stream);
+evospec_status evospec_build_subset_from_candidates(evospec_ctx *ctx, const double *cand_s, const int32_t *cand_id,
+    int32_t n_cand, const int32_t *static_dev, int32_t n_static, const int32_t *seed_dev, int32_t n_seed,
+    const int32_t *csr_row_ptr_dev, const int32_t *csr_col_dev, const int32_t *ctx_dev, int32_t n_ctx,
+    const evospec_build_params *params, int32_t *out_ids, int32_t *out_n, int32_t *out_local_ids,
+    int32_t *out_local_n, void *stream);
 
 /* Batched serving (config Bt, SURVEY §8(a) a4 "a shared static set + 64 ragged
  * dynamic lists"): one query per sequence, the static set shared. For each
@@ -298,8 +330,8 @@ evospec_status evospec_verify_chain(evospec_ctx *ctx, const float *target_logits
  *   recall[r][t]      = |V_t n top-ks[t](p_r)| / ks[t], the target top-k
  *                       ordered (p desc, id asc)
  * target_logits [n_rows, V] fp32; subset_ids [n_subset] sorted ascending
- * unique (V_t); ks [n_ks] int32 in [1, min(V, 1024)] (device; a larger k
- * yields NaN), n_ks <= 64; outputs covered_mass
+ * unique (V_t); ks [n_ks] int32 in [1, min(V, 1024)] (device; an entry outside
+ * yields NaN for that k and raises EVOSPEC_FLAG_BAD_IDS), n_ks <= 64; outputs covered_mass
  * [n_rows] and recall [n_rows, n_ks] fp64 (device). Async, one launch.
  * EVOSPEC_EINPUT on null / out-of-range host arguments. */
 evospec_status evospec_coverage(evospec_ctx *ctx, const float *target_logits, int32_t n_rows, int32_t V,
@@ -320,9 +352,15 @@ evospec_status evospec_coverage(evospec_ctx *ctx, const float *target_logits, in
  *   grad[b][j][i] = weights[b][j] T_kd (p_til[i] - p_hat[i])  (weights held
  *     fixed: a confidence proxy).
  * target_logits / draft_logits [B, g, K] fp32, verified [B] int32 (support
- * index in [0, K)); outputs loss [B], grad [B, g, K] (may be NULL), weights
- * [B, g] (may be NULL), fp32, device. g <= 32, K <= 1024 (the paper: gamma =
- * 6, T_kd = 1, beta = 0.3). fp32 arithmetic. Async. */
+ * index in [0, K); outside: that trajectory's loss / grad / weights are NaN and
+ * EVOSPEC_FLAG_BAD_IDS is raised); outputs loss [B], grad [B, g, K] (may be
+ * NULL), weights [B, g] (may be NULL), fp32, device. g <= 32, K <= 1024 (the
+ * paper: gamma = 6, T_kd = 1, beta = 0.3). fp32 arithmetic.
+ * Terms with p_hat = 0 (a -inf target logit) contribute 0 to the KL. Async.
+ * Reading K1: L_base is taken on the retained first-step support
+ * (the verified token is the target's top-1, so it is on it); SPEC's program
+ * takes the draft's restricted distribution over the V_t snapshot instead --
+ * callers holding that value can pass those logits as draft_logits[b][0]. */
 evospec_status evospec_kd_loss(evospec_ctx *ctx, int32_t B, int32_t g, int32_t K, const float *target_logits,
     const float *draft_logits, const int32_t *verified, float T_kd, float beta,
     float *loss, float *grad, float *weights, void *stream);
@@ -360,9 +398,13 @@ evospec_status evospec_arc_state(const evospec_arc *arc, int32_t *out, int32_t c
  * rebuild): out = sort((subset \ removed) u added). subset [n] sorted unique;
  * removed [n_removed] sorted, a subset of `subset`; added [n_added] sorted,
  * disjoint from subset \ removed; out [n - n_removed + n_added] and n_out [1]
- * device. One kernel (per-element binary searches). Async on `stream`. */
+ * device. One kernel (per-element binary searches). Async on `stream`.
+ * flags (device int32 [1] or NULL): OR-ed with EVOSPEC_FLAG_BAD_IDS when the
+ * contract is violated (a removed id not in subset, an added id already kept);
+ * writes stay inside out[] whatever the input, but the content is then not the
+ * requested set. (evospec_oov_event computes a conforming delta from ARC.) */
 evospec_status evospec_subset_update(const int32_t *subset, int32_t n, const int32_t *removed, int32_t n_removed,
-    const int32_t *added, int32_t n_added, int32_t *out, int32_t *n_out, void *stream);
+    const int32_t *added, int32_t n_added, int32_t *out, int32_t *n_out, int32_t *flags, void *stream);
 
 /* ---- one draft step through the whole path -------------------------------- */
 

@@ -31,6 +31,8 @@ EXPORTED = [
     "evospec_verify_chain", "evospec_coverage", "evospec_kd_loss",
     "evospec_arc_create", "evospec_arc_destroy", "evospec_arc_touch", "evospec_arc_admit", "evospec_arc_state",
     "evospec_subset_update",
+    "evospec_sync_status",
+    "evospec_build_local_candidates", "evospec_build_subset_from_candidates",
 ]
 
 STAGES = ["scan", "select", "union", "lmh", "finalize", "merge", "copy"]
@@ -97,6 +99,9 @@ def lib() -> C.CDLL:
             "evospec_comm_init": ([vp, vp], i32),
             "evospec_build_subset": ([vp, vp, i64, vp, vp, i32, vp, i32, vp, vp, vp, i32,
                                       C.POINTER(BuildParams), vp, vp, vp, vp, vp], i32),
+            "evospec_build_local_candidates": ([vp, vp, i64, vp, i32, vp, vp, vp], i32),
+            "evospec_build_subset_from_candidates": ([vp, vp, vp, i32, vp, i32, vp, i32, vp, vp, vp, i32,
+                                                      C.POINTER(BuildParams), vp, vp, vp, vp, vp], i32),
             "evospec_last_semantic": ([vp, vp, i32, vp], i32),
             "evospec_subset_logits_topk": ([vp, vp, i64, vp, i32, vp, vp, i32, i32, C.c_float,
                                             vp, vp, vp, vp, vp, vp], i32),
@@ -109,7 +114,8 @@ def lib() -> C.CDLL:
             "evospec_arc_touch": ([vp, i32, i64], i32),
             "evospec_arc_admit": ([vp, vp, i32, i64, vp, vp], i32),
             "evospec_arc_state": ([vp, vp, i32, vp], i32),
-            "evospec_subset_update": ([vp, i32, vp, i32, vp, i32, vp, vp, vp], i32),
+            "evospec_subset_update": ([vp, i32, vp, i32, vp, i32, vp, vp, vp, vp], i32),
+            "evospec_sync_status": ([vp, vp], i32),
             "evospec_draft_step": ([vp, C.POINTER(StepIO), vp], i32),
             "evospec_set_timing": ([vp, C.c_int], i32),
             "evospec_read_stats": ([vp, C.POINTER(Stats)], i32),
@@ -206,9 +212,10 @@ class Arc:
         return sorted(s["T1"] + s["T2"])
 
 
-def subset_update(subset, removed, added, *, out=None, stream=None):
+def subset_update(subset, removed, added, *, out=None, flags=None, stream=None):
     """N1: out = sort((subset minus removed) union added) on the device (evospec_subset_update).
-    All int32 device tensors, removed / added sorted. Returns (out, n_out)."""
+    All int32 device tensors, removed / added sorted. flags: optional int32 [1] device tensor,
+    OR-ed with FLAG_BAD_IDS on a contract violation. Returns (out, n_out)."""
     import torch
     n_new = subset.numel() - removed.numel() + added.numel()
     if out is None:
@@ -216,7 +223,8 @@ def subset_update(subset, removed, added, *, out=None, stream=None):
                torch.empty(1, dtype=torch.int32, device=subset.device))
     o, n = out
     _check(lib().evospec_subset_update(_ptr(subset), int(subset.numel()), _ptr(removed), int(removed.numel()),
-                                       _ptr(added), int(added.numel()), _ptr(o), _ptr(n), _stream(stream)))
+                                       _ptr(added), int(added.numel()), _ptr(o), _ptr(n),
+                                       _ptr(flags) if flags is not None else None, _stream(stream)))
     return o[:n_new], n
 
 
@@ -303,6 +311,11 @@ class Context:
         _check(lib().evospec_read_trace(self._h, out.ctypes.data_as(C.c_void_p), out.size))
         return out
 
+    def sync_status(self, stream=None):
+        """evospec_sync_status: synchronizes the stream; raises EvospecError(EINVARIANT)
+        when an invariant flag (bad ids, budget) is set."""
+        _check(lib().evospec_sync_status(self._h, _stream(stream)))
+
     def get_flags(self, clear: bool = True, stream=None) -> int:
         out = C.c_int32(0)
         _check(lib().evospec_get_flags(self._h, C.byref(out), int(clear), _stream(stream)))
@@ -339,6 +352,43 @@ class Context:
             self._h, _ptr(E), E.shape[0], _ptr(q), _ptr(static_ids), static_ids.numel(),
             _ptr(seed_ids) if seed_ids is not None else None,
             0 if seed_ids is None else seed_ids.numel(),
+            _ptr(csr_row_ptr), _ptr(csr_col), _ptr(ctx_ids), n_ctx, C.byref(p),
+            _ptr(ids), _ptr(n), _ptr(lids), _ptr(ln), _stream(stream)))
+        return ids, n, lids, ln
+
+    def build_local_candidates(self, E_local, q, n_sem: int, out=None, stream=None):
+        """Sharded build, step 1 (evospec_build_local_candidates): this shard's exact
+        semantic top-n_sem over its rows of E. Returns (s fp64 [n_sem], ids int32 [n_sem])."""
+        import torch
+        dev = E_local.device
+        if out is None:
+            out = (torch.empty(n_sem, dtype=torch.float64, device=dev), torch.empty(n_sem, dtype=torch.int32, device=dev))
+        cs, ci = out
+        _check(lib().evospec_build_local_candidates(self._h, _ptr(E_local), E_local.shape[0], _ptr(q), int(n_sem),
+                                                    _ptr(cs), _ptr(ci), _stream(stream)))
+        return cs, ci
+
+    def build_subset_from_candidates(self, cand_s, cand_id, static_ids, seed_ids, csr_row_ptr, csr_col, *,
+                                     n_sem: int, n_dyn: int, n_graph_sem_seeds: int = 10, per_seed: int = 8,
+                                     ctx_ids=None, ctx_min_count: int = 0, n_ctx_max: int = 0, out=None,
+                                     stream=None):
+        """Sharded build, step 2 (evospec_build_subset_from_candidates): the R shards'
+        candidates stacked in rank order -> (ids, n_dev, local_ids, local_n_dev), as
+        build_subset."""
+        import torch
+        dev = cand_s.device
+        cap = static_ids.numel() + n_dyn
+        if out is None:
+            out = (torch.empty(max(cap, 1), dtype=torch.int32, device=dev),
+                   torch.empty(1, dtype=torch.int32, device=dev),
+                   torch.empty(max(cap, 1), dtype=torch.int32, device=dev),
+                   torch.empty(1, dtype=torch.int32, device=dev))
+        ids, n, lids, ln = out
+        p = BuildParams(n_sem, n_graph_sem_seeds, per_seed, ctx_min_count, n_ctx_max, n_dyn)
+        n_ctx = 0 if ctx_ids is None else ctx_ids.numel()
+        _check(lib().evospec_build_subset_from_candidates(
+            self._h, _ptr(cand_s), _ptr(cand_id), cand_s.numel(), _ptr(static_ids), static_ids.numel(),
+            _ptr(seed_ids) if seed_ids is not None else None, 0 if seed_ids is None else seed_ids.numel(),
             _ptr(csr_row_ptr), _ptr(csr_col), _ptr(ctx_ids), n_ctx, C.byref(p),
             _ptr(ids), _ptr(n), _ptr(lids), _ptr(ln), _stream(stream)))
         return ids, n, lids, ln

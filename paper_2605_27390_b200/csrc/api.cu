@@ -103,7 +103,6 @@ struct evospec_ctx {
                                   // clears it after the selection has read it)
     bool hist_dirty = false;      // a build stopped between its scan and its union: clear first
     uint32_t* ubits = nullptr;    // [V/32] union bitmap handed to the emit kernel
-    unsigned long long* fin_ctr = nullptr;   // LM-head fused finalisation arrival counter
     int32_t* zero_i = nullptr;    // a device 0 (dyn-only union output at offset 0)
     int32_t* ver_acc = nullptr;   // [kMaxChain + 1] verification: per-position accept flags
     int32_t* ver_tok = nullptr;   // [kMaxChain + 1] verification: per-position emitted token
@@ -230,7 +229,7 @@ evospec_status evospec_destroy(evospec_ctx* ctx) {
                     ctx->flags, ctx->wmax, ctx->g_ids, ctx->g_vals, ctx->g_m, ctx->g_s, ctx->st_q, ctx->st_H,
                     ctx->st_seeds, ctx->st_ctx, ctx->st_S, ctx->st_nS, ctx->st_local, ctx->st_nlocal,
                     ctx->st_tids, ctx->st_tvals, ctx->st_m, ctx->st_s, ctx->st_oids, ctx->st_ovals,
-                    ctx->st_lse, ctx->st_probs, ctx->ubits, ctx->fin_ctr, ctx->rg_ids, ctx->rg_vals, ctx->rg_m, ctx->rg_s, ctx->rg_seg, ctx->rg_segcta, ctx->ver_acc, ctx->ver_tok, ctx->zero_i};
+                    ctx->st_lse, ctx->st_probs, ctx->ubits, ctx->rg_ids, ctx->rg_vals, ctx->rg_m, ctx->rg_s, ctx->rg_seg, ctx->rg_segcta, ctx->ver_acc, ctx->ver_tok, ctx->zero_i};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (ctx->comm && nccl().loaded) nccl().CommDestroy(ctx->comm);
@@ -281,7 +280,7 @@ evospec_status evospec_create(evospec_ctx** out, const evospec_config* cfg, int 
                     cap_v, c.V);
     }
     const size_t cap = (size_t)x->cand_cap;
-    A(dalloc(&x->s64, V)); A(dalloc(&x->key32, V)); A(dalloc(&x->hist12, kHistBins)); A(dalloc(&x->ubits, (V + 31) / 32)); A(dalloc(&x->fin_ctr, 1)); A(cudaMemset(x->fin_ctr, 0, 8)); A(cudaMemset(x->hist12, 0, kHistBins * sizeof(uint32_t)));
+    A(dalloc(&x->s64, V)); A(dalloc(&x->key32, V)); A(dalloc(&x->hist12, kHistBins)); A(dalloc(&x->ubits, (V + 31) / 32)); A(cudaMemset(x->hist12, 0, kHistBins * sizeof(uint32_t)));
     A(dalloc(&x->hist, 12 * kHistBins));
     A(dalloc(&x->ver_acc, kMaxChain + 1)); A(dalloc(&x->ver_tok, kMaxChain + 1));
     A(dalloc(&x->zero_i, 1)); A(cudaMemset(x->zero_i, 0, sizeof(int32_t)));
@@ -332,6 +331,18 @@ evospec_status evospec_prepare_weights(evospec_ctx* ctx, const void* W, int64_t 
     return EVOSPEC_OK;
 }
 
+evospec_status evospec_sync_status(evospec_ctx* ctx, void* stream) {
+    if (!ctx) return fail(EVOSPEC_EINPUT, "sync_status: null context");
+    int32_t f = 0;
+    cudaStream_t st = (cudaStream_t)stream;
+    CUDA_TRY(cudaMemcpyAsync(&f, ctx->flags, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    if (f & (kFlagBadIds | kFlagBudget))
+        return fail(EVOSPEC_EINVARIANT, "invariant violated on the device (flags 0x%x: %s%s)", f,
+                    (f & kFlagBadIds) ? "unsorted / out-of-range ids " : "", (f & kFlagBudget) ? "budget" : "");
+    return EVOSPEC_OK;
+}
+
 evospec_status evospec_get_flags(evospec_ctx* ctx, int32_t* flags_out, int clear, void* stream) {
     if (!ctx || !flags_out) return fail(EVOSPEC_EINPUT, "get_flags: null argument");
     cudaStream_t st = (cudaStream_t)stream;
@@ -366,13 +377,49 @@ evospec_status evospec_comm_init(evospec_ctx* ctx, const void* uid) {
 
 // dyn_base != null: batched mode -- the sorted dynamic list only, written at
 // out_ids + *dyn_base, with *out_n = *dyn_base + its length
+static evospec_status union_from_candidates(evospec_ctx* ctx, const double* cand_s, const int32_t* cand_id,
+                                            int64_t n_cand, const int32_t* static_ids, int32_t n_static,
+                                            const int32_t* seeds, int32_t n_seed, const int32_t* row_ptr,
+                                            const int32_t* col, const int32_t* ctx_ids, int32_t n_ctx,
+                                            const evospec_build_params* p, int32_t* out_ids, int32_t* out_n,
+                                            int32_t* out_local_ids, int32_t* out_local_n, cudaStream_t st,
+                                            const int32_t* dyn_base, cudaEvent_t wait_before_union);
+
+// a2 on a vocabulary shard: exact fp64 scores of this shard's E rows (global id
+// = row * R + r) and the shard's exact top-N (s desc, id asc), padded with id -1
+// when the shard has fewer rows -- what every rank contributes to the candidate
+// all-gather.
+static evospec_status local_candidates_impl(evospec_ctx* ctx, const void* E, int64_t n_e_rows, const void* q,
+                                            int32_t N, double* out_s, int32_t* out_id, cudaStream_t st) {
+    const evospec_config& c = ctx->cfg;
+    const int R = c.n_shards, r = c.shard_rank;
+    StageTimer t(ctx, EVOSPEC_STAGE_SCAN, st);
+    if (ctx->hist_dirty) CUDA_TRY(cudaMemsetAsync(ctx->hist12, 0, kHistBins * sizeof(uint32_t), st));
+    launch_sem_scan(E, c.w_dtype, n_e_rows, c.d, q, c.h_dtype, ctx->s64, ctx->key32, ctx->hist12, st, ctx->hist,
+                    12 * kHistBins, ctx->loc_count, true);
+    ctx->hist_dirty = true;
+    ctx->launches += 2;
+    LAUNCH_CHECK("sem_scan");
+    t.stop();
+    StageTimer t_sel(ctx, EVOSPEC_STAGE_SELECT, st);
+    CUDA_TRY(cudaMemsetAsync(out_id, 0xFF, (size_t)N * sizeof(int32_t), st));
+    CUDA_TRY(launch_topn_cand(ctx->s64, nullptr, n_e_rows, R, r, N, N, ctx->hist12, ctx->hist, ctx->loc_count, out_s,
+                              out_id, st, true));
+    return EVOSPEC_OK;
+}
+
 static evospec_status build_impl(evospec_ctx* ctx, const void* E, int64_t n_e_rows, const void* q,
                                  const int32_t* static_ids, int32_t n_static, const int32_t* seeds, int32_t n_seed,
                                  const int32_t* row_ptr, const int32_t* col, const int32_t* ctx_ids, int32_t n_ctx,
                                  const evospec_build_params* p, int32_t* out_ids, int32_t* out_n,
                                  int32_t* out_local_ids, int32_t* out_local_n, void* stream,
-                                 const int32_t* dyn_base, cudaEvent_t wait_before_union = nullptr) {
-    if (!ctx || !E || !q || !p || !out_ids || !out_n) return fail(EVOSPEC_EINPUT, "build_subset: null argument");
+                                 const int32_t* dyn_base, cudaEvent_t wait_before_union = nullptr,
+                                 const double* ext_s = nullptr, const int32_t* ext_id = nullptr, int64_t n_ext = 0) {
+    // ext_s / ext_id: the shards' stacked local candidates (evospec_build_subset_from_candidates)
+    const bool ext = ext_s != nullptr;
+    if (!ctx || (!ext && (!E || !q)) || !p || !out_ids || !out_n) return fail(EVOSPEC_EINPUT, "build_subset: null argument");
+    if (ext && (!ext_id || n_ext < 1 || n_ext > (int64_t)ctx->cfg.n_shards * ctx->cfg.max_sem))
+        return fail(EVOSPEC_EINPUT, "build_subset_from_candidates: n_cand=%lld not in [1, R * max_sem]", (long long)n_ext);
     const evospec_config& c = ctx->cfg;
     const int R = c.n_shards, r = c.shard_rank;
     cudaStream_t st = (cudaStream_t)stream;
@@ -390,40 +437,34 @@ static evospec_status build_impl(evospec_ctx* ctx, const void* E, int64_t n_e_ro
     if ((row_ptr == nullptr) != (col == nullptr)) return fail(EVOSPEC_EINPUT, "build_subset: CSR half given");
     if (R > 1 && (!out_local_ids || !out_local_n))
         return fail(EVOSPEC_EINPUT, "build_subset: sharded context needs out_local_ids / out_local_n");
+    const int N = p->n_sem;
+    if (ext)
+        return union_from_candidates(ctx, ext_s, ext_id, n_ext, static_ids, n_static, seeds, n_seed, row_ptr, col,
+                                     ctx_ids, n_ctx, p, out_ids, out_n, out_local_ids, out_local_n, st, dyn_base,
+                                     wait_before_union);
     const bool full_scan = n_e_rows == c.V;
     const int64_t local_rows = shard_rows(c.V, R, r);
     if (!full_scan && !(R > 1 && n_e_rows == local_rows))
         return fail(EVOSPEC_EINPUT, "build_subset: n_e_rows must be V=%d or this shard's %lld rows", c.V,
                     (long long)local_rows);
     if (!full_scan && !ctx->comm)
-        return fail(EVOSPEC_EINPUT, "build_subset: a sharded index needs evospec_comm_init");
+        return fail(EVOSPEC_EINPUT, "build_subset: a sharded index needs evospec_comm_init (or the comm-less "
+                                    "evospec_build_local_candidates + evospec_build_subset_from_candidates)");
 
-    const int N = p->n_sem;
-    const uint32_t* hist_pre = nullptr;
-    // a2: exact fp64 scores (+ fused pass-0 histogram), candidate superset of the top-N
-    {
+    if (full_scan) {
+        // a2: exact fp64 scores (+ fused pass-0 histogram), candidate superset of the top-N
         StageTimer t(ctx, EVOSPEC_STAGE_SCAN, st);
         // the scan zeroes the next selection's histogram scratch and count
         if (ctx->hist_dirty) CUDA_TRY(cudaMemsetAsync(ctx->hist12, 0, kHistBins * sizeof(uint32_t), st));
         launch_sem_scan(E, c.w_dtype, n_e_rows, c.d, q, c.h_dtype, ctx->s64, ctx->key32, ctx->hist12, st, ctx->hist,
-                        12 * kHistBins, full_scan ? ctx->cand_count : ctx->loc_count, true);
-        hist_pre = ctx->hist12;
+                        12 * kHistBins, ctx->cand_count, true);
         ctx->hist_dirty = true;
         ctx->launches += 1;
-    }
-    LAUNCH_CHECK("sem_scan");
-    StageTimer t_sel(ctx, EVOSPEC_STAGE_SELECT, st);
-    if (full_scan) {
-        ctx->launches += 1;
-        CUDA_TRY(launch_topn_cand(ctx->s64, nullptr, n_e_rows, 1, 0, N, ctx->cand_cap, hist_pre, ctx->hist,
-                                  ctx->cand_count, ctx->cand_s, ctx->cand_id, st, true));
     } else {
-        // exact local top-N (ids = row*R + r; padded with id -1), all-gather N (s, id) pairs per rank,
-        // candidate superset of the global top-N over the R*N gathered pairs
-        ctx->launches += 2;
-        CUDA_TRY(cudaMemsetAsync(ctx->loc_id, 0xFF, (size_t)N * sizeof(int32_t), st));
-        CUDA_TRY(launch_topn_cand(ctx->s64, nullptr, n_e_rows, R, r, N, N, hist_pre, ctx->hist, ctx->loc_count,
-                                  ctx->loc_s, ctx->loc_id, st, true));
+        // this shard's exact local top-N, all-gathered (N (s, id) pairs per rank)
+        evospec_status ls = local_candidates_impl(ctx, E, n_e_rows, q, N, ctx->loc_s, ctx->loc_id, st);
+        if (ls != EVOSPEC_OK) return ls;
+        StageTimer t_g(ctx, EVOSPEC_STAGE_MERGE, st);
         NcclApi& n = nccl();
         n.GroupStart();
         ncclResult_t r1 = n.AllGather(ctx->loc_s, ctx->gat_s, (size_t)N, ncclFloat64, ctx->comm, st);
@@ -431,7 +472,36 @@ static evospec_status build_impl(evospec_ctx* ctx, const void* E, int64_t n_e_ro
         ncclResult_t r3 = n.GroupEnd();
         if (r1 != ncclSuccess || r2 != ncclSuccess || r3 != ncclSuccess)
             return fail(EVOSPEC_ENCCL, "build_subset all-gather failed");
-        CUDA_TRY(launch_topn_cand(ctx->gat_s, ctx->gat_id, (int64_t)N * R, 0, 0, N, ctx->cand_cap, nullptr, ctx->hist,
+        t_g.stop();
+    }
+    LAUNCH_CHECK("sem_scan");
+    return union_from_candidates(ctx, full_scan ? nullptr : ctx->gat_s, full_scan ? nullptr : ctx->gat_id,
+                                 (int64_t)N * R, static_ids, n_static, seeds, n_seed, row_ptr, col, ctx_ids, n_ctx, p,
+                                 out_ids, out_n, out_local_ids, out_local_n, st, dyn_base, wait_before_union);
+}
+
+// The global candidate superset of the top-N and the formation / union (a2-a4).
+// cand_s / cand_id null: the single-shard scan's scores in the workspace (full
+// scan, fused pass-0 histogram); else n_cand gathered (s, id) pairs of all shards
+// (each shard's exact local top-N, stacked in rank order).
+static evospec_status union_from_candidates(evospec_ctx* ctx, const double* cand_s, const int32_t* cand_id,
+                                            int64_t n_cand, const int32_t* static_ids, int32_t n_static,
+                                            const int32_t* seeds, int32_t n_seed, const int32_t* row_ptr,
+                                            const int32_t* col, const int32_t* ctx_ids, int32_t n_ctx,
+                                            const evospec_build_params* p, int32_t* out_ids, int32_t* out_n,
+                                            int32_t* out_local_ids, int32_t* out_local_n, cudaStream_t st,
+                                            const int32_t* dyn_base, cudaEvent_t wait_before_union) {
+    const evospec_config& c = ctx->cfg;
+    const int R = c.n_shards, r = c.shard_rank;
+    const int N = p->n_sem;
+    StageTimer t_sel(ctx, EVOSPEC_STAGE_SELECT, st);
+    if (!cand_s) {
+        ctx->launches += 1;
+        CUDA_TRY(launch_topn_cand(ctx->s64, nullptr, c.V, 1, 0, N, ctx->cand_cap, ctx->hist12, ctx->hist,
+                                  ctx->cand_count, ctx->cand_s, ctx->cand_id, st, true));
+    } else {
+        ctx->launches += 1;
+        CUDA_TRY(launch_topn_cand(cand_s, cand_id, n_cand, 0, 0, N, ctx->cand_cap, nullptr, ctx->hist,
                                   ctx->cand_count, ctx->cand_s, ctx->cand_id, st));
     }
     t_sel.stop();
@@ -465,7 +535,31 @@ static evospec_status build_impl(evospec_ctx* ctx, const void* E, int64_t n_e_ro
         ctx->launches += 1;
         LAUNCH_CHECK("union_emit");
     }
+    if (c.debug_checks) return evospec_sync_status(ctx, st);
     return EVOSPEC_OK;
+}
+
+evospec_status evospec_build_local_candidates(evospec_ctx* ctx, const void* E_local, int64_t n_e_rows, const void* q,
+                                             int32_t n_sem, double* out_s, int32_t* out_id, void* stream) {
+    if (!ctx || !E_local || !q || !out_s || !out_id) return fail(EVOSPEC_EINPUT, "build_local_candidates: null argument");
+    const evospec_config& c = ctx->cfg;
+    const int64_t local_rows = shard_rows(c.V, c.n_shards, c.shard_rank);
+    if (n_e_rows != local_rows)
+        return fail(EVOSPEC_EINPUT, "build_local_candidates: n_e_rows=%lld, this shard has %lld rows",
+                    (long long)n_e_rows, (long long)local_rows);
+    if (n_sem < 1 || n_sem > c.max_sem) return fail(EVOSPEC_EINPUT, "build_local_candidates: n_sem not in [1, %d]", c.max_sem);
+    return local_candidates_impl(ctx, E_local, n_e_rows, q, n_sem, out_s, out_id, (cudaStream_t)stream);
+}
+
+evospec_status evospec_build_subset_from_candidates(evospec_ctx* ctx, const double* cand_s, const int32_t* cand_id,
+                                                    int32_t n_cand, const int32_t* static_ids, int32_t n_static,
+                                                    const int32_t* seeds, int32_t n_seed, const int32_t* row_ptr,
+                                                    const int32_t* col, const int32_t* ctx_ids, int32_t n_ctx,
+                                                    const evospec_build_params* p, int32_t* out_ids, int32_t* out_n,
+                                                    int32_t* out_local_ids, int32_t* out_local_n, void* stream) {
+    if (!cand_s) return fail(EVOSPEC_EINPUT, "build_subset_from_candidates: null candidates");
+    return build_impl(ctx, nullptr, 0, nullptr, static_ids, n_static, seeds, n_seed, row_ptr, col, ctx_ids, n_ctx, p,
+                      out_ids, out_n, out_local_ids, out_local_n, stream, nullptr, nullptr, cand_s, cand_id, n_cand);
 }
 
 evospec_status evospec_build_subset(evospec_ctx* ctx, const void* E, int64_t n_e_rows, const void* q,
@@ -624,20 +718,6 @@ static evospec_status lmh_impl(evospec_ctx* ctx, const void* W, int64_t n_w_rows
             n_cta = a.grid > 0 ? a.grid : lmh_tc_grid();
             gamma = kTcGamma;
         } else if (use_tc(a)) {
-            // finalisation fused into the tensor-core kernel's last CTAs (k + 8 <= 32, no
-            // segments, rows <= CTAs): opt-in (EVOSPEC_FUSED_FIN=1) -- measured slower than
-            // the separate PDL-chained kernel (416 threads per row instead of 512, and no
-            // earlier start: the arrival wait costs what the launch gap did)
-            static const bool fused_fin = getenv("EVOSPEC_FUSED_FIN") != nullptr;
-            if (fused_fin && a.KP <= 32 && a.LS == 64 && !segs && n_h <= lmh_tc_grid()) {
-                a.fuse_fin = 1;
-                a.fin_k = k;
-                a.fin_gamma = kTcGamma;
-                a.fin_wmax = ctx->wmax;
-                a.fin_ctr = ctx->fin_ctr;
-                a.fin_ids = topk_ids; a.fin_vals = topk_vals; a.fin_m = row_max; a.fin_s = row_sumexp;
-                a.fin_flags = ctx->flags;
-            }
             CUDA_TRY(launch_lmh_tc(a, st));
             ctx->launches += 1;
             n_cta = segs ? segs->seg_ctas : (a.grid > 0 ? a.grid : lmh_tc_grid());
@@ -652,13 +732,14 @@ static evospec_status lmh_impl(evospec_ctx* ctx, const void* W, int64_t n_w_rows
             }
         }
     }
-    if (!a.fuse_fin) {
+    {
         StageTimer t(ctx, EVOSPEC_STAGE_FINALIZE, st);
         launch_lmh_finalize(a, n_cta, k, ctx->wmax, topk_ids, topk_vals, row_max, row_sumexp, ctx->flags, st,
                             gamma);
         ctx->launches += 1;
     }
     LAUNCH_CHECK("lmh_finalize");
+    if (c.debug_checks) return evospec_sync_status(ctx, stream);   // (header: EINVARIANT on the product path)
     return EVOSPEC_OK;
 }
 
@@ -843,6 +924,7 @@ evospec_status evospec_coverage(evospec_ctx* ctx, const float* target_logits, in
     if (!(inv_temp > 0.0f) || !std::isfinite(inv_temp)) return fail(EVOSPEC_EINPUT, "coverage: inv_temp must be > 0");
     if (n_rows == 0) return EVOSPEC_OK;
     launch_coverage(target_logits, n_rows, V, subset_ids, n_subset, (double)inv_temp, ks, n_ks, covered_mass, recall,
+                    ctx->flags,
                     (cudaStream_t)stream);
     ctx->launches += 1;
     LAUNCH_CHECK("coverage");
@@ -858,7 +940,8 @@ evospec_status evospec_kd_loss(evospec_ctx* ctx, int32_t B, int32_t g, int32_t K
     if (!(T_kd > 0.0f) || !std::isfinite(T_kd) || !(beta >= 0.0f) || !std::isfinite(beta))
         return fail(EVOSPEC_EINPUT, "kd_loss: T_kd must be > 0 and beta >= 0");
     if (B == 0) return EVOSPEC_OK;
-    launch_kd_loss(B, g, K, target_logits, draft_logits, verified, T_kd, beta, loss, grad, weights, (cudaStream_t)stream);
+    launch_kd_loss(B, g, K, target_logits, draft_logits, verified, T_kd, beta, loss, grad, weights, ctx->flags,
+                   (cudaStream_t)stream);
     ctx->launches += 1;
     LAUNCH_CHECK("kd_loss");
     return EVOSPEC_OK;

@@ -26,6 +26,7 @@
 #include "../../include/evospec.h"
 #pragma GCC visibility pop
 #include "common.cuh"
+#include "kernels.cuh"
 
 namespace es {
 
@@ -118,31 +119,49 @@ __device__ __forceinline__ int lb32(const int32_t* a, int n, int32_t v) {
     return lo;
 }
 
+// Contract (header): removed is a subset of S, added is disjoint from S \ removed.
+// A violation cannot corrupt memory: every destination is range-checked, and
+// (flags != null) each removed id missing from S / added id already kept raises
+// kFlagBadIds (the output is then not the set the caller asked for).
 __global__ void subset_update_kernel(const int32_t* __restrict__ S, int n, const int32_t* __restrict__ rem, int nr,
                                      const int32_t* __restrict__ add, int na, int32_t* __restrict__ out,
-                                     int32_t* __restrict__ n_out) {
+                                     int32_t* __restrict__ n_out, int32_t* __restrict__ flags) {
     pdl_trigger();
     pdl_wait();
     const int tid = blockIdx.x * blockDim.x + threadIdx.x, T = gridDim.x * blockDim.x;
+    const int n_new = n - nr + na;
+    bool bad = false;
     for (int i = tid; i < n; i += T) {
         const int32_t v = __ldg(&S[i]);
         const int r = lb32(rem, nr, v);
         if (r < nr && __ldg(&rem[r]) == v) continue;     // evicted
-        out[i - r + lb32(add, na, v)] = v;                // r removed entries precede v
+        const int d = i - r + lb32(add, na, v);           // r removed entries precede v
+        if (d >= 0 && d < n_new) out[d] = v;
+        else bad = true;
+    }
+    for (int j = tid; j < nr; j += T) {   // every removed id must be in S
+        const int32_t v = __ldg(&rem[j]);
+        const int p = lb32(S, n, v);
+        bad |= !(p < n && __ldg(&S[p]) == v);
     }
     for (int j = tid; j < na; j += T) {
         const int32_t v = __ldg(&add[j]);
-        const int below = lb32(S, n, v) - lb32(rem, nr, v);   // kept S entries < v
-        out[below + j] = v;
+        const int p = lb32(S, n, v), rp = lb32(rem, nr, v);
+        const bool kept = p < n && __ldg(&S[p]) == v && !(rp < nr && __ldg(&rem[rp]) == v);
+        const int d = p - rp + j;   // kept S entries < v, then j added ones
+        bad |= kept;
+        if (!kept && d >= 0 && d < n_new) out[d] = v;
+        else bad = true;
     }
-    if (tid == 0) *n_out = n - nr + na;
+    if (bad && flags) atomicOr(flags, kFlagBadIds);
+    if (tid == 0) *n_out = n_new;
 }
 
 void launch_subset_update(const int32_t* S, int n, const int32_t* rem, int nr, const int32_t* add, int na,
-                          int32_t* out, int32_t* n_out, cudaStream_t st) {
+                          int32_t* out, int32_t* n_out, int32_t* flags, cudaStream_t st) {
     const int threads = 256;
     const int blocks = std::max(1, std::min(kNumSMs, (n + na + threads - 1) / threads));
-    launch_pdl(subset_update_kernel, dim3(blocks), dim3(threads), 0, st, S, n, rem, nr, add, na, out, n_out);
+    launch_pdl(subset_update_kernel, dim3(blocks), dim3(threads), 0, st, S, n, rem, nr, add, na, out, n_out, flags);
 }
 
 }  // namespace es
@@ -206,12 +225,12 @@ evospec_status evospec_arc_state(const evospec_arc* arc, int32_t* out,
 evospec_status evospec_subset_update(const int32_t* subset, int32_t n,
     const int32_t* removed, int32_t n_removed,
     const int32_t* added, int32_t n_added,
-    int32_t* out, int32_t* n_out,
+    int32_t* out, int32_t* n_out, int32_t* flags,
     void* stream) {
     if (n < 0 || n_removed < 0 || n_added < 0 || n_removed > n || (n > 0 && !subset) ||
         (n_removed > 0 && !removed) || (n_added > 0 && !added) || !out || !n_out)
         return EVOSPEC_EINPUT;
-    es::launch_subset_update(subset, n, removed, n_removed, added, n_added, out, n_out, (cudaStream_t)stream);
+    es::launch_subset_update(subset, n, removed, n_removed, added, n_added, out, n_out, flags, (cudaStream_t)stream);
     const cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? EVOSPEC_OK : EVOSPEC_ECUDA;
 }

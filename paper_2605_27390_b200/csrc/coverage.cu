@@ -123,7 +123,8 @@ ES_DEV uint32_t cov_select(int V, int K, KeyFn KEY, CovSmem& sm) {
 
 __global__ void __launch_bounds__(kCovThreads)
 coverage_kernel(const float* __restrict__ z, int V, const int32_t* __restrict__ S, int n_S, double it,
-                const int32_t* __restrict__ ks, int n_ks, double* __restrict__ mass, double* __restrict__ recall) {
+                const int32_t* __restrict__ ks, int n_ks, double* __restrict__ mass, double* __restrict__ recall,
+                int* __restrict__ flags) {
     __shared__ CovSmem sm;
     pdl_trigger();
     pdl_wait();
@@ -159,6 +160,7 @@ coverage_kernel(const float* __restrict__ z, int V, const int32_t* __restrict__ 
     for (int t = 0; t < n_ks; ++t) K = max(K, __ldg(&ks[t]));
     if (K < 1 || K > kCovMaxK || K > V) {   // outside the header's range: NaN
         if (tid < n_ks) recall[(size_t)r * n_ks + tid] = __longlong_as_double(0x7ff8000000000000ll);
+        if (tid == 0 && flags) atomicOr(flags, kFlagBadIds);
         return;
     }
     const uint32_t tau = cov_select(V, K, [&](int v, uint32_t& key) { key = float_key(__ldg(&zr[v])); return true; }, sm);
@@ -210,6 +212,11 @@ coverage_kernel(const float* __restrict__ z, int V, const int32_t* __restrict__ 
     if (wid == 0) {   // prefix counts over ranks, one lane per k
         for (int t = lane; t < n_ks; t += 32) {
             const int k = __ldg(&ks[t]);
+            if (k < 1) {   // (k > K cannot happen: K is the maximum)
+                recall[(size_t)r * n_ks + t] = __longlong_as_double(0x7ff8000000000000ll);
+                if (flags) atomicOr(flags, kFlagBadIds);
+                continue;
+            }
             int hit = 0;
             for (int i = 0; i < k; ++i) hit += sm.hit_at[i];
             recall[(size_t)r * n_ks + t] = (double)hit / (double)k;
@@ -218,8 +225,9 @@ coverage_kernel(const float* __restrict__ z, int V, const int32_t* __restrict__ 
 }
 
 void launch_coverage(const float* z, int n_rows, int V, const int32_t* S, int n_S, double it, const int32_t* ks,
-                     int n_ks, double* mass, double* recall, cudaStream_t st) {
-    launch_pdl(coverage_kernel, dim3(n_rows), dim3(kCovThreads), 0, st, z, V, S, n_S, it, ks, n_ks, mass, recall);
+                     int n_ks, double* mass, double* recall, int* flags, cudaStream_t st) {
+    launch_pdl(coverage_kernel, dim3(n_rows), dim3(kCovThreads), 0, st, z, V, S, n_S, it, ks, n_ks, mass, recall,
+               flags);
 }
 
 }  // namespace es

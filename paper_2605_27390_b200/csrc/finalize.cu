@@ -23,7 +23,7 @@
 #include "common.cuh"
 #include "kernels.cuh"
 #include "lmh_epilogue.cuh"   // warp_kth_largest
-#include "finalize32.cuh"   // fin32_row (also fused into the LM-head kernel)
+#include "finalize32.cuh"   // fin32_row
 
 namespace es {
 

@@ -1,6 +1,5 @@
-// finalize32.cuh -- the k + 8 <= 32 LM-head finalisation of one H row, shared
-// by the standalone finalisation kernel (finalize.cu) and the LM-head kernel's
-// last-arriving CTAs (lmh_tc.cu, fused finalisation).
+// finalize32.cuh -- the k + 8 <= 32 LM-head finalisation of one H row (the
+// finalisation kernel, finalize.cu).
 #pragma once
 #include "common.cuh"
 #include "kernels.cuh"
@@ -109,9 +108,8 @@ ES_DEV void sort32_rolled(float& v, int& p) {
     }
 }
 
-// One H row's finalisation by a block of NT threads (NT = NT in the
-// standalone kernel, the LM-head kernel's 416 when fused into its last CTAs);
-// shared memory comes from the caller (fin32_carve).
+// One H row's finalisation by a block of NT threads; shared memory comes from
+// the caller (fin32_carve).
 // H row r into shared memory and this thread's share of ||h||^2. Reads only
 // the LM head's inputs (H), never its outputs, so the standalone kernel runs it
 // before griddepcontrol.wait, overlapping the LM head's tail.

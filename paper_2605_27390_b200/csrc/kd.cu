@@ -31,7 +31,7 @@ ES_DEV float kd_warp_sum(float v) {
 
 __global__ void __launch_bounds__(256) kd_loss_kernel(int g, int K, const float* __restrict__ zp, const float* __restrict__ zq,
                                const int32_t* __restrict__ verified, float T, float beta, float* __restrict__ J,
-                               float* __restrict__ grad, float* __restrict__ w_out) {
+                               float* __restrict__ grad, float* __restrict__ w_out, int* __restrict__ flags) {
     __shared__ float s_Lb, s_part[32];
     pdl_trigger();
     pdl_wait();
@@ -46,7 +46,15 @@ __global__ void __launch_bounds__(256) kd_loss_kernel(int g, int K, const float*
         float s = 0.0f;
         for (int i = lane; i < K; i += 32) s += __expf(__ldg(&q0[i]) - m);
         s = kd_warp_sum(s);
-        if (lane == 0) s_Lb = m + __logf(s) - __ldg(&q0[__ldg(&verified[b])]);
+        if (lane == 0) {
+            const int vb = __ldg(&verified[b]);
+            if (vb >= 0 && vb < K) {
+                s_Lb = m + __logf(s) - __ldg(&q0[vb]);
+            } else {   // not a support index: the trajectory's outputs are NaN
+                s_Lb = __int_as_float(0x7fc00000);
+                if (flags) atomicOr(flags, kFlagBadIds);
+            }
+        }
     }
     __syncthreads();
     for (int j = warp_id(); j < g; j += nw) {
@@ -84,7 +92,7 @@ __global__ void __launch_bounds__(256) kd_loss_kernel(int g, int K, const float*
             const int i = lane + 32 * u;
             if (i < K) {
                 const float ph = __expf(a[u] - la), pt = __expf(c[u] - lc);
-                kl += ph * ((a[u] - la) - (c[u] - lc));
+                if (ph > 0.0f) kl += ph * ((a[u] - la) - (c[u] - lc));   // (0 log 0 = 0: no -inf product)
                 if (grad) grad[o + i] = w * T * (pt - ph);
             }
         }
@@ -103,9 +111,9 @@ __global__ void __launch_bounds__(256) kd_loss_kernel(int g, int K, const float*
 }
 
 void launch_kd_loss(int B, int g, int K, const float* zp, const float* zq, const int32_t* verified, float T,
-                    float beta, float* J, float* grad, float* w_out, cudaStream_t st) {
+                    float beta, float* J, float* grad, float* w_out, int* flags, cudaStream_t st) {
     launch_pdl(kd_loss_kernel, dim3(B), dim3(32 * std::min(std::max(g, 1), 8)), 0, st, g, K, zp, zq, verified, T, beta, J, grad,
-               w_out);
+               w_out, flags);
 }
 
 }  // namespace es

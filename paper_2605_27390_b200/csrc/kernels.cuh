@@ -81,9 +81,6 @@ struct LmhArgs {
     // optional fused single-shard merge outputs (R = 1): ids/vals [n_h][k], lse [n_h], probs [n_h][k]
     int32_t* m_ids; float* m_vals; float* m_lse; float* m_probs;
     LmhPartials part;
-    // fused finalisation (tensor-core path, k + 8 <= 32, no segments): the last n_h
-    // CTAs to finish each finalise one row once every CTA has stored its lists
-    int fuse_fin, fin_k;
     int fin_opt;    // finalisation variants (bits; EVOSPEC_FIN_OPT): 1 H before the PDL wait, 2 W-row L2 prefetch,
                     // 4 multi-warp re-score, 8 parallel head threshold
     int par_fold;   // thread-parallel tile fold (lmh_epilogue.cuh epi_par_*), buffered path
@@ -97,10 +94,6 @@ struct LmhArgs {
     // two-list mode: ids whose W rows are pulled into L2 while the union still runs (the
     // semantic candidate superset, a superset of most of the second list; a hint only)
     const int32_t* pf_ids; const int* pf_n; int pf_cap;
-    float fin_gamma;
-    const float* fin_wmax;
-    unsigned long long* fin_ctr;   // monotone arrival counter (G arrivals per launch)
-    int32_t* fin_ids; float* fin_vals; float* fin_m; float* fin_s; int* fin_flags;
 };
 
 // This CTA's contiguous share [p0, p1) of the subset positions: all of
@@ -132,9 +125,9 @@ int lmh_gemv_group_width(const LmhArgs& a, int n_left);
 constexpr int kTcMaxRows = 128;
 constexpr int kMaxChain = 63;   // verification: longest draft chain (the paper's horizon is 6)
 void launch_kd_loss(int B, int g, int K, const float* zp, const float* zq, const int32_t* verified, float T,
-                    float beta, float* J, float* grad, float* w_out, cudaStream_t st);
+                    float beta, float* J, float* grad, float* w_out, int* flags, cudaStream_t st);
 void launch_coverage(const float* z, int n_rows, int V, const int32_t* S, int n_S, double it, const int32_t* ks,
-                     int n_ks, double* mass, double* recall, cudaStream_t st);
+                     int n_ks, double* mass, double* recall, int* flags, cudaStream_t st);
 void launch_verify(const float* z, int V, int g, const int32_t* x, const int32_t* S, int n_S, const float* qS,
                    double it, int greedy, const double* u, const double* w, int32_t* pos_acc, int32_t* pos_tok,
                    int32_t* tokens, int32_t* n_acc_out, int* flags, cudaStream_t st);

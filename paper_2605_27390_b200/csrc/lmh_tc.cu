@@ -23,7 +23,6 @@
 //           while the producers and MMA already stream the next tile; the
 //           CTA's last tile is folded (and its rows stored) by all 13 warps.
 // Segment mode (ragged head): CTAs serve (row group, position range) segments.
-// Optional: the finalisation fused into the last-arriving CTAs (EVOSPEC_FUSED_FIN).
 #include <algorithm>
 #include <cstdlib>
 
@@ -34,7 +33,6 @@
 #include "kernels.cuh"
 #include "tc_ptx.cuh"
 #include "lmh_epilogue.cuh"
-#include "finalize32.cuh"
 
 namespace es {
 
@@ -106,9 +104,7 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
     // clock64 details of CTA 0's last tile (EVOSPEC_TRACE; profiling aid)
     long long* const DTR = a.trace && blockIdx.x == 0 ? a.trace + 2 * kNumSMs * 8 + 48 : nullptr;
     if (DTR && threadIdx.x == 0) { DTR[48] = 0; DTR[49] = 0; }
-    // with the fused finalisation some CTAs wait for all others: dependents are
-    // triggered only at the end, so they cannot take an SM one of ours still needs
-    if (!a.fuse_fin) pdl_trigger();
+    pdl_trigger();
     // setup that needs nothing from the previous kernel overlaps its tail (PDL)
     if (warp == 0 && lane == 0) {
         asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap_h) : "memory");
@@ -391,39 +387,6 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
     if (threadIdx.x == 0) TC_TRACE(7);
     if (warp == kTcMmaWarp)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(tp.tmem_cols));
-    if (a.fuse_fin) {
-        // fused finalisation: arrival order over a monotone counter (G per launch);
-        // the last n_h arrivals each finalise one row after all G have stored
-        __threadfence();
-        __syncthreads();
-        int* tick = (int*)base;   // the ring is free now
-        if (threadIdx.x == 0) {
-            const unsigned long long t = atomicAdd(a.fin_ctr, 1ull);
-            const unsigned long long G = gridDim.x;
-            const int arrival = (int)(t % G);
-            tick[0] = arrival;
-            if (arrival >= (int)G - n_h) {
-                const unsigned long long target = t - (unsigned long long)arrival + G;
-                unsigned long long cur;
-                for (;;) {
-                    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(cur) : "l"(a.fin_ctr) : "memory");
-                    if (cur >= target) break;
-                    __nanosleep(32);
-                }
-            }
-        }
-        __syncthreads();
-        const int arrival = tick[0];
-        if (arrival >= (int)gridDim.x - n_h) {
-            __threadfence();
-            __syncthreads();
-            const int row = arrival - ((int)gridDim.x - n_h);
-            const Fin32Smem sm = fin32_carve(base + 1024, kTcWarps * 32);
-            fin32_row<6, kTcWarps * 32>(a, row, gridDim.x, a.fin_k, a.fin_gamma, a.fin_wmax, a.fin_ids, a.fin_vals,
-                                        a.fin_m, a.fin_s, a.fin_flags, sm);
-        }
-        pdl_trigger();
-    }
 }
 
 // ------------------------------------------------------------------ host

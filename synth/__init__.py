@@ -178,17 +178,19 @@ CONFIGS = {
 }
 
 
-def verify_problem(seed: int, *, V: int, g: int, n_S: int, inv_temp: float = 1.0) -> dict:
+def verify_problem(seed: int, *, V: int, g: int, n_S: int, inv_temp: float = 1.0, s_range: int = 0) -> dict:
     """Inputs of the N2 verification step, seeded: target logits z
     [g+1, V] fp32 (N(0, 1.28^2): the llama head's logit scale, §8(d)), a sorted
     random subset S of n_S ids, the draft's restricted distribution q on S
     ([g, n_S] fp32; a draft whose logits are the target's on S plus N(0, 0.5^2)
     noise, normalised on S -- an input, not the method's arithmetic), proposals
-    x_j drawn from q_j, uniforms u [g] and w [g+1] (fp64, [0, 1))."""
+    x_j drawn from q_j, uniforms u [g] and w [g+1] (fp64, [0, 1)). s_range > 0: the
+    subset is drawn from ids [0, s_range) only (a subset concentrated in one part of
+    the vocabulary)."""
     rng = np.random.default_rng(seed)
     z = (rng.normal(size=(g + 1, V)) * 1.28).astype(np.float32)
     n_S = min(n_S, V)
-    S = np.sort(rng.choice(V, n_S, replace=False)).astype(np.int32)
+    S = np.sort(rng.choice(s_range if s_range > 0 else V, n_S, replace=False)).astype(np.int32)
     dl = z[:g, S].astype(np.float64) * inv_temp + rng.normal(size=(g, n_S)) * 0.5
     q = np.exp(dl - dl.max(axis=1, keepdims=True))
     q /= q.sum(axis=1, keepdims=True)

@@ -79,3 +79,18 @@ def assert_triple_close(ids, vals, m, s, ref, k: int):
     lse = np.asarray(m, np.float64) + np.log(np.asarray(s, np.float64))
     fin = np.isfinite(ref["lse"])
     assert np.all(np.abs(lse[fin] - ref["lse"][fin]) <= LOGIT_TOL * (1 + np.abs(ref["lse"][fin])))
+
+
+def near_tie_count(scores, n: int, rel: float = 1e-12) -> int:
+    """SURVEY §8(c) C10 near-tie counter: 1 if the oracle's fp64 values ranked n and
+    n + 1 (descending) differ by less than rel (relative) without being equal -- a
+    boundary where a reassociated fp64 sum on the GPU could legitimately order the
+    two the other way. Rows: a 2-D array counts per row."""
+    a = np.atleast_2d(np.asarray(scores, np.float64))
+    if a.shape[1] <= n:
+        return 0
+    part = -np.partition(-a, n, axis=1)[:, : n + 1]
+    srt = -np.sort(-part, axis=1)
+    x, y = srt[:, n - 1], srt[:, n]
+    gap = np.abs(x - y)
+    return int(np.sum((gap > 0) & (gap <= rel * np.maximum(np.abs(x), np.abs(y)))))

@@ -58,3 +58,22 @@ def test_coverage_edges():
     np.testing.assert_allclose(m, mo, rtol=1e-12)
     np.testing.assert_array_equal(r, ro)
     assert r[1, 0] == 0.0 and r[1, 3] == (40 - 3) / 40
+
+
+def test_coverage_bad_k_entries():
+    """Every k outside [1, min(V, 1024)] gives NaN for that k (the others stay exact)
+    and raises FLAG_BAD_IDS -- including a non-positive k next to a valid maximum."""
+    rng = np.random.default_rng(4)
+    V = 5000
+    z = rng.normal(size=(2, V)).astype(np.float32)
+    S = np.sort(rng.choice(V, 900, replace=False)).astype(np.int32)
+    ctx = es.Context(V=V, d=64, w_dtype=torch.bfloat16, h_dtype=torch.bfloat16, max_subset=1, max_rows=1,
+                     max_k=1, max_sem=1)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+    m, r = ctx.coverage(t(z), t(S), t(np.asarray([10, 0, -3, 50], np.int32)))
+    torch.cuda.synchronize()
+    r = r.cpu().numpy()
+    _, ro = oracle.coverage(z, S, [10, 50])
+    assert np.all(np.isnan(r[:, 1:3]))
+    np.testing.assert_array_equal(r[:, [0, 3]], ro)
+    assert ctx.get_flags() & es.FLAG_BAD_IDS

@@ -39,3 +39,33 @@ def test_kd_loss(B, g, K, T, beta):
     assert np.all(np.abs(J - Jo) <= 1e-5 * (1 + np.abs(Jo))), np.abs(J - Jo).max()
     assert np.abs(grad - go).max() <= 1e-5
     np.testing.assert_allclose(w, wo, rtol=1e-5, atol=1e-30)
+
+
+def test_kd_loss_bad_verified_index_and_minus_inf_target():
+    """A verified index outside [0, K) gives that trajectory NaN outputs and raises
+    FLAG_BAD_IDS (the others are unaffected); a -inf target logit (p_hat = 0) adds 0 to
+    the KL instead of 0 * -inf."""
+    rng = np.random.default_rng(77)
+    B, g, K = 4, 3, 50
+    zp = (rng.normal(size=(B, g, K)) * 2.0).astype(np.float32)
+    zq = (zp + rng.normal(size=(B, g, K)) * 0.7).astype(np.float32)
+    zp[2, 1, 5] = -np.inf
+    v = rng.integers(0, K, size=B).astype(np.int32)
+    ctx = es.Context(V=1024, d=64, w_dtype=torch.bfloat16, h_dtype=torch.bfloat16, max_subset=1, max_rows=1,
+                     max_k=1, max_sem=1)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+    J, _, _ = ctx.kd_loss(t(zp), t(zq), t(v), T_kd=1.0, beta=0.3)
+    torch.cuda.synchronize()
+    assert ctx.get_flags() == 0
+    assert np.all(np.isfinite(J.cpu().numpy()))
+    zp2 = zp.copy()
+    zp2[2, 1, 5] = -1e30   # (the oracle's stand-in for the -inf target logit: p_hat underflows to 0)
+    Jo, _, _ = oracle.kd_loss(zp2, zq, v, T=1.0, beta=0.3)
+    assert np.all(np.abs(J.cpu().numpy() - Jo) <= 1e-5 * (1 + np.abs(Jo)))
+    v_bad = v.copy()
+    v_bad[1] = K
+    J, _, _ = ctx.kd_loss(t(zp), t(zq), t(v_bad), T_kd=1.0, beta=0.3)
+    torch.cuda.synchronize()
+    J = J.cpu().numpy()
+    assert np.isnan(J[1]) and np.all(np.isfinite(J[[0, 2, 3]]))
+    assert ctx.get_flags() & es.FLAG_BAD_IDS

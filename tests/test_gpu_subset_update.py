@@ -68,3 +68,28 @@ def test_arc_driven_incremental_updates():
         assert set(rem.tolist()) <= set(ev) and set(ev) - set(rem.tolist()) <= set(toks)
         S, n = gpu_update(S, rem, add)
         np.testing.assert_array_equal(S, np.union1d(static, np.array(sorted(after), np.int32)))
+
+
+def test_contract_violation_is_flagged_not_corrupting():
+    """A removed id that is not in the subset, or an added id that is already kept,
+    violates the header's contract: the kernel raises FLAG_BAD_IDS and never writes
+    outside out[] (a guard buffer past it stays intact)."""
+    rng = np.random.default_rng(11)
+    V = 50000
+    S = np.sort(rng.choice(V, 4000, replace=False)).astype(np.int32)
+    free = np.setdiff1d(np.arange(V), S)
+    for rem, add in ((np.sort(rng.choice(free, 5, replace=False)), free[:0]),          # removed not in S
+                     (S[:0], np.sort(np.concatenate([S[:3], free[:2]])))):            # added already kept
+        n_new = S.size - rem.size + add.size
+        buf = torch.full((n_new + 64,), -7, dtype=torch.int32, device=DEV)
+        n = torch.zeros(1, dtype=torch.int32, device=DEV)
+        flags = torch.zeros(1, dtype=torch.int32, device=DEV)
+        es.subset_update(t(S), t(rem), t(add), out=(buf[:max(1, n_new)], n), flags=flags)
+        torch.cuda.synchronize()
+        assert int(flags.item()) & es.FLAG_BAD_IDS
+        assert np.all(buf[n_new:].cpu().numpy() == -7)
+    # a conforming call leaves the flag clear
+    flags = torch.zeros(1, dtype=torch.int32, device=DEV)
+    es.subset_update(t(S), t(S[:4]), t(free[:4]), flags=flags)
+    torch.cuda.synchronize()
+    assert int(flags.item()) == 0

@@ -24,11 +24,11 @@ import paper_2605_27390_b200 as es  # noqa: E402
 DEV = "cuda:0"
 
 
-def problem(seed, V=128256, g=6, n_S=36864, inv_temp=1.0):
+def problem(seed, V=128256, g=6, n_S=36864, inv_temp=1.0, s_range=0):
     """Seeded verification inputs (synth.verify_problem: target logits, subset, draft
     distribution on it, proposals drawn from the draft, uniforms)."""
     # the ABI's inv_temp is fp32: both sides take that value
-    return synth.verify_problem(seed, V=V, g=g, n_S=n_S, inv_temp=float(np.float32(inv_temp)))
+    return synth.verify_problem(seed, V=V, g=g, n_S=n_S, inv_temp=float(np.float32(inv_temp)), s_range=s_range)
 
 
 def run_gpu(P, greedy, ctx=None):
@@ -88,3 +88,12 @@ def test_verify_proposal_outside_support_flags():
     P["x"][0] = np.setdiff1d(np.arange(P["V"]), P["S"])[0]
     tok, n, flags = run_gpu(P, False)
     assert n == 0 and tok[0] == -1 and flags & 0x1
+
+
+@pytest.mark.parametrize("greedy", [False, True])
+def test_verify_subset_slice_beyond_smem(greedy):
+    """A subset concentrated in the first eighth of the vocabulary: the first CTA of
+    each 8-CTA cluster holds 12,000 > 8,192 subset entries, more than its shared-memory
+    slice (kVerSCap), so the residual walk takes the global binary-search path."""
+    for seed in (40, 41):
+        check(problem(seed, n_S=12000, s_range=128256 // 8), greedy)
