@@ -99,6 +99,7 @@ struct evospec_ctx {
     // semantic scan + selection
     double* s64 = nullptr;
     uint32_t* key32 = nullptr;
+    bool no_graph = false;        // draft_step: graph capture failed once (sharded): direct launches
     uint32_t* hist12 = nullptr;   // scan-fused pass-0 histogram; zero between builds (the union kernel
                                   // clears it after the selection has read it)
     bool hist_dirty = false;      // a build stopped between its scan and its union: clear first
@@ -1058,8 +1059,11 @@ static evospec_status draft_step_impl(evospec_ctx* ctx, const evospec_step_io* i
 evospec_status evospec_draft_step(evospec_ctx* ctx, const evospec_step_io* io, void* stream) {
     if (!ctx || !io) return fail(EVOSPEC_EINPUT, "draft_step: null argument");
     cudaStream_t st = (cudaStream_t)stream;
-    const bool use_graph = ctx->cfg.n_shards == 1 && !ctx->timing && !ctx->cfg.debug_checks &&
-                           !getenv("EVOSPEC_NO_GRAPH") && !getenv("EVOSPEC_TRACE");
+    // sharded steps are captured too (NCCL all-gathers are capturable); if a capture
+    // fails the context falls back to direct launches for good
+    const bool use_graph = !ctx->no_graph && !ctx->timing && !ctx->cfg.debug_checks &&
+                           (ctx->cfg.n_shards == 1 || ctx->comm) && !getenv("EVOSPEC_NO_GRAPH") &&
+                           !getenv("EVOSPEC_TRACE");
     if (!use_graph) return draft_step_impl(ctx, io, st);
     // host staging copies stay ordinary stream copies (measured faster than graph
     // memcpy nodes from pinned memory); the graph holds the compute
@@ -1078,6 +1082,11 @@ evospec_status evospec_draft_step(evospec_ctx* ctx, const evospec_step_io* io, v
     const cudaError_t e = cudaStreamEndCapture(ctx->cap_stream, &g);
     if (s != EVOSPEC_OK || e != cudaSuccess) {
         if (g) cudaGraphDestroy(g);
+        if (ctx->cfg.n_shards > 1) {   // (a communicator that cannot be captured: run direct from now on)
+            cudaGetLastError();
+            ctx->no_graph = true;
+            return draft_step_impl(ctx, io, st);
+        }
         if (s != EVOSPEC_OK) return s;
         return fail(EVOSPEC_ECUDA, "draft_step: graph capture failed: %s", cudaGetErrorString(e));
     }

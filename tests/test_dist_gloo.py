@@ -90,3 +90,68 @@ def test_vocab_shard_merge_gloo(world):
         p.join(timeout=60)
     for rank, msg in res:
         assert msg == "ok", f"rank {rank}: {msg}"
+
+
+def _cand_worker(rank, world, port, q):
+    """The sharded build's candidate exchange (what evospec_build_subset
+    all-gathers over NCCL and evospec_build_subset_from_candidates consumes): each rank's
+    exact local top-N over its owned ids (global id = local row * R + r), N (s, id) pairs
+    per rank stacked in rank order; the global top-N of the R * N gathered pairs equals
+    the unsharded top-N, and every rank resolves the same set."""
+    try:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        import oracle
+        import synth
+        from paper_2605_27390_b200 import dist as esd
+
+        V, d, N = 5003, 48, 257
+        E = synth.matrix(40, V, d, 0.5, "bf16")
+        E[100:140] = E[600:640]           # duplicated rows: exact score ties across shards
+        qv = synth.matrix(41, 1, d, 1.0, "bf16")[0]
+        E_loc = np.ascontiguousarray(esd.shard_rows(E, world, rank))
+        s_loc = oracle.sem_scores(E_loc, qv)
+        top = oracle.topn(s_loc, min(N, s_loc.size))          # local rows, (s desc, row asc)
+        ids = (top * world + rank).astype(np.int32)            # local row -> global id
+        s = s_loc[top]
+        ids = np.concatenate([ids, np.full(N - ids.size, -1, np.int32)])
+        s = np.concatenate([s, np.full(N - s.size, -np.inf)])
+
+        def gather(a):
+            tt = torch.from_numpy(np.ascontiguousarray(a))
+            out = [torch.empty_like(tt) for _ in range(world)]
+            dist.all_gather(out, tt)
+            return np.concatenate([o.numpy() for o in out])
+        gs, gi = gather(s), gather(ids)
+        ok = gi >= 0
+        order = np.lexsort((gi[ok], -gs[ok]))[:N]            # the global selection, (s desc, id asc)
+        got = np.sort(gi[ok][order])
+        ref = np.sort(oracle.topn(oracle.sem_scores(E, qv), N))
+        assert np.array_equal(got, ref), "gathered global top-N differs from the unsharded one"
+        h = torch.tensor(int(got.astype(np.int64).sum()))
+        hs = [torch.zeros_like(h) for _ in range(world)]
+        dist.all_gather(hs, h)
+        assert all(int(x) == int(h) for x in hs)
+        dist.destroy_process_group()
+        q.put((rank, "ok"))
+    except Exception:  # pragma: no cover - reported to the parent
+        import traceback
+        q.put((rank, traceback.format_exc()))
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_candidate_exchange_gloo(world):
+    import oracle
+    oracle.build()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_cand_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=240) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    for rank, msg in res:
+        assert msg == "ok", f"rank {rank}: {msg}"
