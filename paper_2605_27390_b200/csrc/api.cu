@@ -686,9 +686,6 @@ static evospec_status lmh_impl(evospec_ctx* ctx, const void* W, int64_t n_w_rows
     if (list2) {   // two-list mode (draft_step overlap): one SM stays free for the union kernel
         a.list2 = list2; a.n_list2_dev = n_list2_dev; a.n_list2_max = n_list2_max; a.n1 = n_subset_max;
         a.grid = lmh_tc_grid() - 1;
-        // L2 prefetch of the candidate rows before the wait: measured slower (299 vs 297 us), opt-in
-        static const bool dyn_pf = getenv("EVOSPEC_DYN_PF") ? atoi(getenv("EVOSPEC_DYN_PF")) != 0 : false;
-        if (dyn_pf && c.n_shards == 1) { a.pf_ids = ctx->cand_id; a.pf_n = ctx->cand_count; a.pf_cap = ctx->cand_cap; }
         if (!use_tc(a) || a.KP > 32 || segs || seg || logits_out)
             return fail(EVOSPEC_EINPUT, "subset_logits_topk: two-list mode needs the tensor-core path and k + 8 <= 32");
     }

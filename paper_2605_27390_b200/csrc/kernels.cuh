@@ -91,9 +91,6 @@ struct LmhArgs {
     // before griddepcontrol.wait. grid: CTAs of the launch (0 = all SMs)
     const int32_t* list2; const int32_t* n_list2_dev; int n_list2_max; int n1;
     int grid;
-    // two-list mode: ids whose W rows are pulled into L2 while the union still runs (the
-    // semantic candidate superset, a superset of most of the second list; a hint only)
-    const int32_t* pf_ids; const int* pf_n; int pf_cap;
 };
 
 // This CTA's contiguous share [p0, p1) of the subset positions: all of

@@ -13,8 +13,7 @@
 //   warps 0-3  producers: 16-byte cp.async of the gathered W rows into a
 //           128B-swizzled smem stage (swizzle applied in the address), one
 //           cp.async.mbarrier.arrive.noinc per thread (rows past a tile's end
-//           skipped); H by one 2D TMA tile per stage (an optional L2 bulk
-//           prefetch run-ahead, EVOSPEC_PF, measured slower: off).
+//           skipped); H by one 2D TMA tile per stage.
 //   warp 4  TMEM allocator + MMA issuer (one elected thread):
 //           4 x tcgen05.mma.cta_group::1.kind::f16 (K = 16) per stage,
 //           tcgen05.commit frees the stage; double-buffered accumulators.
@@ -59,7 +58,6 @@ struct TcParams {
     int stages;
     int nkb;         // d / 64
     uint32_t tmem_cols;
-    int kps;         // K-blocks per barrier stage (ring buffers = stages * kps)
     int last_tile;   // rows of a CTA's short last tile (ranges longer than one tile)
     int dyn_tile;    // two-list mode: rows per second-list tile (EVOSPEC_DYN_TILE)
     int dyn_stride;  // two-list mode: CTA rank stride of the second-list round robin
@@ -220,10 +218,10 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
         const uint64_t pol_w = policy_evict_first(), pol_h = policy_evict_last();
         const int chunk = lane & 7;
         const size_t row_bytes = (size_t)a.d * 2;
-        const int KPS = tp.kps;
         int stage = 0;
         uint32_t phase = 0;
-        for (int t = 0; has_tile(t); ++t) {
+        for (int t = 0;; ++t) {
+            if (!has_tile(t)) break;
             int t0, tn;
             tile_range(t, t0, tn);
             const char* src[8];
@@ -235,30 +233,16 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
                 src[i] = (const char*)a.W + (size_t)(lmh_id_at(a, pos) / a.R) * row_bytes + chunk * 16;
                 dsto[i] = (uint32_t)(row * 128 + ((chunk ^ (row & 7)) << 4));
             }
-            // a barrier stage carries KPS K-blocks (ring buffers stage * KPS + j): the
-            // stage handshake (consumer wait, MMA issue, commit) costs ~0.3-0.5 us
-            // whatever its size (measured), so it is paid once per KPS K-blocks
-            for (int kb0 = 0; kb0 < tp.nkb; kb0 += KPS) {
-                const int nk = min(KPS, tp.nkb - kb0);
+            for (int kb = 0; kb < tp.nkb; ++kb) {
                 mbar_wait(&empty[stage], phase ^ 1);
                 if (warp == 0 && lane == 0) {
-                    mbar_arrive_expect_tx(&full[stage], (uint32_t)(nk * NP * 128));
-                    for (int j = 0; j < nk; ++j)
-                        tma_load_2d(smB + (size_t)(stage * KPS + j) * NP * 128, &tmap_h, &full[stage],
-                                    (kb0 + j) * kBlockK, h_row0, pol_h);
+                    mbar_arrive_expect_tx(&full[stage], (uint32_t)(NP * 128));
+                    tma_load_2d(smB + (size_t)stage * NP * 128, &tmap_h, &full[stage], kb * kBlockK, h_row0, pol_h);
                 }
-                for (int j = 0; j < nk; ++j) {
-                    const uint32_t dA = smem_u32(smA + (size_t)(stage * KPS + j) * kTileM * 128);
-                    const int ko = (kb0 + j) * 128;
-                    if (tn == kTileM) {
+                const uint32_t dA = smem_u32(smA + (size_t)stage * kTileM * 128);
 #pragma unroll
-                        for (int i = 0; i < 8; ++i) cp_async16(dA + dsto[i], src[i] + ko, pol_w);
-                    } else {
-#pragma unroll
-                        for (int i = 0; i < 8; ++i)   // rows past the tile's end are never read back
-                            if (16 * i + 4 * warp + (lane >> 3) < tn) cp_async16(dA + dsto[i], src[i] + ko, pol_w);
-                    }
-                }
+                for (int i = 0; i < 8; ++i)   // rows past the tile's end are never read back
+                    if (16 * i + 4 * warp + (lane >> 3) < tn) cp_async16(dA + dsto[i], src[i] + kb * 128, pol_w);
                 cp_async_arrive_noinc(&full[stage]);
                 if (++stage == S) { stage = 0; phase ^= 1; }
             }
@@ -276,21 +260,18 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
             if (t >= 2) mbar_wait(&tempty[b], (use - 1) & 1);
             tc_fence_after();
             const uint32_t tmem_d = tmem_base + (uint32_t)(b * NP);
-            for (int kb0 = 0; kb0 < tp.nkb; kb0 += tp.kps) {
-                const int nk = min(tp.kps, tp.nkb - kb0);
+            for (int kb = 0; kb < tp.nkb; ++kb) {
                 mbar_wait(&full[stage], phase);
                 tc_fence_after();
                 if (lane == 0) {
-                    for (int j = 0; j < nk; ++j) {
-                        const uint32_t aaddr = smem_u32(smA + (size_t)(stage * tp.kps + j) * kTileM * 128);
-                        const uint32_t baddr = smem_u32(smB + (size_t)(stage * tp.kps + j) * NP * 128);
+                    const uint32_t aaddr = smem_u32(smA + (size_t)stage * kTileM * 128);
+                    const uint32_t baddr = smem_u32(smB + (size_t)stage * NP * 128);
 #pragma unroll
-                        for (int k = 0; k < kBlockK / 16; ++k)
-                            umma_bf16(tmem_d, umma_desc_sw128(aaddr + k * 32), umma_desc_sw128(baddr + k * 32), idesc,
-                                      ((kb0 + j) | k) != 0);
-                    }
+                    for (int k = 0; k < kBlockK / 16; ++k)
+                        umma_bf16(tmem_d, umma_desc_sw128(aaddr + k * 32), umma_desc_sw128(baddr + k * 32), idesc,
+                                  (kb | k) != 0);
                     umma_commit(&empty[stage]);
-                    if (kb0 + tp.kps >= tp.nkb) umma_commit(&tfull[b]);
+                    if (kb == tp.nkb - 1) umma_commit(&tfull[b]);
                 }
                 __syncwarp();
                 if (++stage == S) { stage = 0; phase ^= 1; }
@@ -422,18 +403,12 @@ cudaError_t launch_lmh_tc(const LmhArgs& a, cudaStream_t st) {
     const size_t epi = epi_smem_bytes(rows, (a.KP <= 32 && a.LS == kBuf) ? kBuf : a.KP, kTcWarps);
     const size_t fixed = epi + 2 * 128 * 4 + 64 * 8 + 1024 /*align slack*/ + 256;
     const size_t budget = 227 * 1024;
-    int SS = (int)((budget - fixed) / (stage_a + stage_b));   // ring buffers (one K-block each)
-    SS = std::min(SS, 8);   // (12 buffers measured slower: 36,864 rows 101 vs 87 us)
-    // K-blocks per barrier stage (EVOSPEC_TC_KPS, default 1): 2 and 3 measured equal
-    // here (the stage handshake is hidden by the 8-buffer ring), unlike in lmh_hl
-    static const int kps_env = getenv("EVOSPEC_TC_KPS") ? atoi(getenv("EVOSPEC_TC_KPS")) : 1;
-    int kps = std::max(1, std::min(kps_env, SS / 2));
-    const int S = SS / kps;
+    int S = (int)((budget - fixed) / (stage_a + stage_b));
+    S = std::min(S, 8);
     if (S < 2) return cudaErrorInvalidConfiguration;
     tp.stages = S;
-    tp.kps = kps;
-    tp.off_b = (size_t)S * kps * stage_a;
-    tp.off_epi = tp.off_b + (size_t)S * kps * stage_b;
+    tp.off_b = (size_t)S * stage_a;
+    tp.off_epi = tp.off_b + (size_t)S * stage_b;
     tp.off_bar = (tp.off_epi + epi + 15) & ~(size_t)15;
     tp.off_rows = tp.off_bar + (size_t)(2 * S + 4) * 8 + 16;
     const size_t smem = tp.off_rows + 2 * 128 * 4 + 1024;
