@@ -345,6 +345,7 @@ def run_ours(args):
         torch.cuda.empty_cache()
         extra = dict(qwen_topic_segment=qwen_segment(dev, args), sharded_d8192_r1=sharded_sweep(dev, args),
                      verify_chain=verify_line(dev, args), coverage=coverage_line(dev, args),
+                     oov_overlap=oov_overlap_line(dev, args),
                      kd_loss=kd_line(dev, args), arc_update=arc_line(dev, args))
     if rank != 0:
         if world > 1:
@@ -648,6 +649,74 @@ def arc_line(dev, args):
                          "scan + select + union + emit, breakdown above)",
                 arc_host_us_per_event=t_host / n_ev * 1e6, update_us=e0.elapsed_time(e1) * 1e3 / reps,
                 n_S=int(S.numel()))
+
+
+def oov_overlap_line(dev, args):
+    """N1: an OOV event's rebuild overlapped with drafting
+    (evospec_oov_event_begin / _end; App. B): the llama head, V_t =
+    static 32,768 + an ARC of 256; 21 LM-head calls (n_H = 60, k = 10) back to back on
+    the current subset, with one event begun after call 0 (the formation -- exact
+    semantic scan, selection, union of <= 32 new ids -- on the side stream) and ended
+    after call 10 (ARC admission + device update), calls 11-20 on the updated subset.
+    Reported: the event's marginal cost on the drafting stream (with - without) and its
+    own latency with nothing else running, against the ~270 us full rebuild."""
+    import torch
+    import paper_2605_27390_b200 as es
+    c = dict(synth.CONFIGS["llama"])
+    V, d, n_h, k = c["V"], c["d"], c["n_h"], c["k"]
+    bf = torch.bfloat16
+    W = torch.from_numpy(synth.matrix(0, V, d, c["w_std"], "bf16").view(np.int16)).view(bf).to(dev)
+    H = torch.from_numpy(synth.matrix(1, n_h, d, c["h_std"], "bf16").view(np.int16)).view(bf).to(dev)
+    static = synth.static_ids(3, V, c["n_static"])
+    rp, col, _ = synth.csr_graph(4, V, c["avg_deg"])
+    st_d, rp_d, col_d = (torch.from_numpy(np.ascontiguousarray(a)).to(dev) for a in (static, rp, col))
+    rng = np.random.default_rng(17)
+    ctx = es.Context(V=V, d=d, w_dtype=bf, h_dtype=bf, max_subset=static.size + 256 + 32, max_rows=n_h, max_k=k,
+                     max_sem=16, max_seeds=64)
+    ctx.prepare_weights(W)
+    arc = es.Arc(256)
+    pool = np.setdiff1d(np.arange(V), static)
+    arc.admit(np.sort(rng.choice(pool, 256, replace=False)).astype(np.int32).tolist(), 0)
+    S0 = torch.from_numpy(np.union1d(static, np.asarray(arc.members(), np.int32)).astype(np.int32)).to(dev)
+    qs = [torch.from_numpy(synth.matrix(700 + i, 1, d, 1.0, "bf16")[0].view(np.int16)).view(bf).to(dev)
+          for i in range(4)]
+    seeds = [torch.from_numpy(np.sort(rng.choice(V, 10, replace=False)).astype(np.int32)).to(dev) for _ in range(4)]
+
+    def run(event, it):
+        S, n = S0, S0.numel()
+        nd = torch.tensor([n], dtype=torch.int32, device=dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for i in range(21):
+            ctx.subset_logits_topk_merged(W, H, S, nd, n, k)
+            if event and i == 0:
+                ctx.oov_event_begin(W, qs[it % 4], st_d, seeds[it % 4], rp_d, col_d, n_sem=10, n_dyn=32)
+            if event and i == 10:
+                S, nd, _, _ = ctx.oov_event_end(arc, 100 + it, S, n)
+                n = S.numel()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) * 1e3
+
+    for it in range(2):
+        run(False, it), run(True, it)
+    base = statistics.median([run(False, it) for it in range(5)])
+    withev = statistics.median([run(True, it) for it in range(5)])
+    lat = []
+    for it in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        ctx.oov_event_begin(W, qs[it % 4], st_d, seeds[it % 4], rp_d, col_d, n_sem=10, n_dyn=32)
+        ctx.oov_event_end(arc, 200 + it, S0, S0.numel())
+        e1.record()
+        torch.cuda.synchronize()
+        lat.append(e0.elapsed_time(e1) * 1e3)
+    arc.close()
+    return dict(workload="llama head, V_t = static 32,768 + ARC 256; 21 LM-head calls (n_H=60, k=10) with one OOV "
+                         "event (semantic top-10, graph top-8 of target top-10 u semantic top-10, <= 32 insertions) "
+                         "begun after call 0 on the side stream, ended after call 10",
+                calls_us_without_event=base, calls_us_with_event=withev,
+                event_marginal_us=withev - base, event_latency_alone_us=statistics.median(lat))
 
 
 def verify_parity_cpu_leg(vl):

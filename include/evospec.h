@@ -393,6 +393,13 @@ int32_t        evospec_arc_touch(evospec_arc *arc, int32_t token, int64_t step);
 evospec_status evospec_arc_admit(evospec_arc *arc, const int32_t *tokens, int32_t n, int64_t step,
     int32_t *evicted, int32_t *n_evicted);
 evospec_status evospec_arc_state(const evospec_arc *arc, int32_t *out, int32_t cap, int32_t *n_out);
+/* evospec_arc_admit as a membership delta: admits tokens[n] (one OOV event) and
+ * returns the NET change of the member set T1 u T2 -- added[] (members now, not
+ * before) and removed[] (members before, not now), each ascending, capacity n
+ * each -- exactly the removed / added arguments evospec_subset_update expects (a
+ * token admitted and evicted within the event appears in neither). */
+evospec_status evospec_arc_admit_delta(evospec_arc *arc, const int32_t *tokens, int32_t n, int64_t step,
+    int32_t *added, int32_t *n_added, int32_t *removed, int32_t *n_removed);
 
 /* Incremental update of the sorted active vocabulary on the device (no full
  * rebuild): out = sort((subset \ removed) u added). subset [n] sorted unique;
@@ -405,6 +412,31 @@ evospec_status evospec_arc_state(const evospec_arc *arc, int32_t *out, int32_t c
  * requested set. (evospec_oov_event computes a conforming delta from ARC.) */
 evospec_status evospec_subset_update(const int32_t *subset, int32_t n, const int32_t *removed, int32_t n_removed,
     const int32_t *added, int32_t n_added, int32_t *out, int32_t *n_out, int32_t *flags, void *stream);
+
+/* N1 OOV event, in two phases so that it overlaps the draft steps (Path A runs
+ * asynchronously; App. B): when the verified token falls
+ * outside V_t, _begin enqueues the event's candidate formation on
+ * the context's side stream -- the exact semantic top-n_sem of the target-side
+ * hidden state q (the HNSW top-10 of P:458, C2), the graph top-per_seed of
+ * seeds u S_sem[:n_graph_sem_seeds] (target top-10 u semantic top-10,
+ * 8 successors each), the first n_dyn (max insertions per event, 32 at P:462)
+ * new non-static ids -- after the work already on `stream` (q, seeds), and
+ * returns at once; the caller keeps running LM-head calls on the current
+ * subset (any stream; no build / draft_step on this context meanwhile).
+ * _end waits for the candidates, admits them into the ARC in ascending id order
+ * (reading A3) as one event at `step` (evospec_arc_admit_delta), and enqueues the
+ * incremental update out = sort((subset \ removed) u added) on `stream`; the
+ * net delta is also returned to the host (added_host / removed_host [n_dyn] or
+ * NULL). subset [n]: the current V_t = static u ARC members (sorted); out
+ * [n + n_dyn] and n_out [1] device. Unsharded contexts; one event in flight.
+ * EVOSPEC_EINPUT on null / out-of-range arguments or a second _begin / an _end
+ * without one. */
+evospec_status evospec_oov_event_begin(evospec_ctx *ctx, const void *E_dev, int64_t n_e_rows, const void *q_dev,
+    const int32_t *static_dev, int32_t n_static, const int32_t *seed_dev, int32_t n_seed,
+    const int32_t *csr_row_ptr_dev, const int32_t *csr_col_dev, const evospec_build_params *params, void *stream);
+evospec_status evospec_oov_event_end(evospec_ctx *ctx, evospec_arc *arc, int64_t step, const int32_t *subset_dev,
+    int32_t n, int32_t *out_dev, int32_t *n_out_dev, int32_t *added_host, int32_t *n_added, int32_t *removed_host,
+    int32_t *n_removed, void *stream);
 
 /* ---- one draft step through the whole path -------------------------------- */
 

@@ -33,6 +33,7 @@ EXPORTED = [
     "evospec_subset_update",
     "evospec_sync_status",
     "evospec_build_local_candidates", "evospec_build_subset_from_candidates",
+    "evospec_arc_admit_delta", "evospec_oov_event_begin", "evospec_oov_event_end",
 ]
 
 STAGES = ["scan", "select", "union", "lmh", "finalize", "merge", "copy"]
@@ -114,6 +115,9 @@ def lib() -> C.CDLL:
             "evospec_arc_touch": ([vp, i32, i64], i32),
             "evospec_arc_admit": ([vp, vp, i32, i64, vp, vp], i32),
             "evospec_arc_state": ([vp, vp, i32, vp], i32),
+            "evospec_arc_admit_delta": ([vp, vp, i32, i64, vp, vp, vp, vp], i32),
+            "evospec_oov_event_begin": ([vp, vp, i64, vp, vp, i32, vp, i32, vp, vp, C.POINTER(BuildParams), vp], i32),
+            "evospec_oov_event_end": ([vp, vp, i64, vp, i32, vp, vp, vp, vp, vp, vp, vp], i32),
             "evospec_subset_update": ([vp, i32, vp, i32, vp, i32, vp, vp, vp, vp], i32),
             "evospec_sync_status": ([vp, vp], i32),
             "evospec_draft_step": ([vp, C.POINTER(StepIO), vp], i32),
@@ -194,6 +198,18 @@ class Arc:
         _check(lib().evospec_arc_admit(self._h, t.ctypes.data_as(C.c_void_p), int(t.size), int(step),
                                        ev.ctypes.data_as(C.c_void_p), C.byref(ne)))
         return ev[:ne.value].tolist()
+
+    def admit_delta(self, tokens, step: int):
+        """One OOV event as the net membership change: (added, removed), ascending."""
+        import numpy as np
+        t = np.ascontiguousarray(np.asarray(tokens, dtype=np.int32).reshape(-1))
+        add = np.zeros(max(1, t.size), np.int32)
+        rem = np.zeros(max(1, t.size), np.int32)
+        na, nr = C.c_int32(0), C.c_int32(0)
+        _check(lib().evospec_arc_admit_delta(self._h, t.ctypes.data_as(C.c_void_p), int(t.size), int(step),
+                                             add.ctypes.data_as(C.c_void_p), C.byref(na),
+                                             rem.ctypes.data_as(C.c_void_p), C.byref(nr)))
+        return add[:na.value].tolist(), rem[:nr.value].tolist()
 
     def state(self) -> dict:
         import numpy as np
@@ -355,6 +371,37 @@ class Context:
             _ptr(csr_row_ptr), _ptr(csr_col), _ptr(ctx_ids), n_ctx, C.byref(p),
             _ptr(ids), _ptr(n), _ptr(lids), _ptr(ln), _stream(stream)))
         return ids, n, lids, ln
+
+    def oov_event_begin(self, E, q, static_ids, seed_ids, csr_row_ptr, csr_col, *, n_sem: int = 10,
+                        n_dyn: int = 32, n_graph_sem_seeds: int = 10, per_seed: int = 8, stream=None):
+        """N1: enqueue an OOV event's candidate formation on the context's side stream
+        (evospec_oov_event_begin) and return at once."""
+        p = BuildParams(n_sem, n_graph_sem_seeds, per_seed, 0, 0, n_dyn)
+        self._oov_cap = n_dyn
+        _check(lib().evospec_oov_event_begin(
+            self._h, _ptr(E), E.shape[0], _ptr(q), _ptr(static_ids), static_ids.numel(),
+            _ptr(seed_ids) if seed_ids is not None else None, 0 if seed_ids is None else seed_ids.numel(),
+            _ptr(csr_row_ptr), _ptr(csr_col), C.byref(p), _stream(stream)))
+
+    def oov_event_end(self, arc, step: int, subset, n: int, *, out=None, stream=None):
+        """N1: admit the event's candidates into `arc` and update the subset on the device
+        (evospec_oov_event_end). subset: the current sorted V_t ([>= n] int32 device).
+        Returns (out [n'] device, n_out device, added list, removed list)."""
+        import numpy as np
+        import torch
+        cap = getattr(self, "_oov_cap", 32)
+        if out is None:
+            out = (torch.empty(n + cap, dtype=torch.int32, device=subset.device),
+                   torch.empty(1, dtype=torch.int32, device=subset.device))
+        o, no = out
+        add = np.zeros(max(1, cap), np.int32)
+        rem = np.zeros(max(1, cap), np.int32)
+        na, nr = C.c_int32(0), C.c_int32(0)
+        _check(lib().evospec_oov_event_end(self._h, arc._h, int(step), _ptr(subset), int(n), _ptr(o), _ptr(no),
+                                           add.ctypes.data_as(C.c_void_p), C.byref(na),
+                                           rem.ctypes.data_as(C.c_void_p), C.byref(nr), _stream(stream)))
+        n_new = n - nr.value + na.value
+        return o[:n_new], no, add[:na.value].tolist(), rem[:nr.value].tolist()
 
     def build_local_candidates(self, E_local, q, n_sem: int, out=None, stream=None):
         """Sharded build, step 1 (evospec_build_local_candidates): this shard's exact

@@ -105,6 +105,15 @@ struct evospec_ctx {
     bool hist_dirty = false;      // a build stopped between its scan and its union: clear first
     uint32_t* ubits = nullptr;    // [V/32] union bitmap handed to the emit kernel
     int32_t* zero_i = nullptr;    // a device 0 (dyn-only union output at offset 0)
+    // N1 OOV event (evospec_oov_event_begin / _end): the event's formation runs on a
+    // side stream while the caller keeps drafting on the current subset
+    cudaStream_t oov_stream = nullptr;
+    cudaEvent_t oov_ready = nullptr, oov_done = nullptr;
+    int32_t* oov_dyn = nullptr;   // [oov_cap + 1] device: count, then the event's sorted new ids
+    int32_t* oov_host = nullptr;  // [oov_cap + 1] pinned
+    int32_t* oov_delta = nullptr; // [2 * oov_cap] device: removed, added
+    int oov_cap = 0;
+    bool oov_pending = false;
     int32_t* ver_acc = nullptr;   // [kMaxChain + 1] verification: per-position accept flags
     int32_t* ver_tok = nullptr;   // [kMaxChain + 1] verification: per-position emitted token
     uint32_t* hist = nullptr;     // [12][4096] further select passes
@@ -241,6 +250,12 @@ evospec_status evospec_destroy(evospec_ctx* ctx) {
     if (ctx->s_h) cudaStreamDestroy(ctx->s_h);
     if (ctx->ev_in) cudaEventDestroy(ctx->ev_in);
     if (ctx->ev_h) cudaEventDestroy(ctx->ev_h);
+    if (ctx->oov_stream) cudaStreamDestroy(ctx->oov_stream);
+    if (ctx->oov_ready) cudaEventDestroy(ctx->oov_ready);
+    if (ctx->oov_done) cudaEventDestroy(ctx->oov_done);
+    if (ctx->oov_dyn) cudaFree(ctx->oov_dyn);
+    if (ctx->oov_delta) cudaFree(ctx->oov_delta);
+    if (ctx->oov_host) cudaFreeHost(ctx->oov_host);
     delete ctx;
     return EVOSPEC_OK;
 }
@@ -537,6 +552,77 @@ static evospec_status union_from_candidates(evospec_ctx* ctx, const double* cand
         LAUNCH_CHECK("union_emit");
     }
     if (c.debug_checks) return evospec_sync_status(ctx, st);
+    return EVOSPEC_OK;
+}
+
+evospec_status evospec_oov_event_begin(evospec_ctx* ctx, const void* E, int64_t n_e_rows, const void* q,
+                                      const int32_t* static_ids, int32_t n_static, const int32_t* seeds,
+                                      int32_t n_seed, const int32_t* row_ptr, const int32_t* col,
+                                      const evospec_build_params* p, void* stream) {
+    if (!ctx || !p) return fail(EVOSPEC_EINPUT, "oov_event_begin: null argument");
+    if (ctx->cfg.n_shards != 1) return fail(EVOSPEC_EINPUT, "oov_event_begin: unsharded contexts only");
+    if (ctx->oov_pending) return fail(EVOSPEC_EINPUT, "oov_event_begin: an event is already in flight (call _end)");
+    if (p->n_dyn < 1 || p->n_dyn > 1024) return fail(EVOSPEC_EINPUT, "oov_event_begin: n_dyn (max insertions) not in [1, 1024]");
+    if (!ctx->oov_stream) {
+        CUDA_TRY(cudaStreamCreateWithFlags(&ctx->oov_stream, cudaStreamNonBlocking));
+        CUDA_TRY(cudaEventCreateWithFlags(&ctx->oov_ready, cudaEventDisableTiming));
+        CUDA_TRY(cudaEventCreateWithFlags(&ctx->oov_done, cudaEventDisableTiming));
+    }
+    if (p->n_dyn > ctx->oov_cap) {
+        if (ctx->oov_dyn) cudaFree(ctx->oov_dyn);
+        if (ctx->oov_delta) cudaFree(ctx->oov_delta);
+        if (ctx->oov_host) cudaFreeHost(ctx->oov_host);
+        ctx->oov_dyn = ctx->oov_delta = ctx->oov_host = nullptr;
+        ctx->oov_cap = 0;
+        const int cap = std::max(64, p->n_dyn);
+        CUDA_TRY(cudaMalloc(&ctx->oov_dyn, (size_t)(cap + 1) * sizeof(int32_t)));
+        CUDA_TRY(cudaMalloc(&ctx->oov_delta, (size_t)2 * cap * sizeof(int32_t)));
+        CUDA_TRY(cudaMallocHost(&ctx->oov_host, (size_t)(cap + 1) * sizeof(int32_t)));
+        ctx->oov_cap = cap;
+    }
+    // the side stream starts after the work already on the caller's stream (q, seeds)
+    CUDA_TRY(cudaEventRecord(ctx->oov_ready, (cudaStream_t)stream));
+    CUDA_TRY(cudaStreamWaitEvent(ctx->oov_stream, ctx->oov_ready, 0));
+    // the event's candidates: formation with the cap n_dyn (max insertions per event,
+    // P:462), static members skipped -- the sorted new ids, as one batched-build sequence
+    evospec_status rc = build_impl(ctx, E, n_e_rows, q, static_ids, n_static, seeds, n_seed, row_ptr, col, nullptr, 0,
+                                   p, ctx->oov_dyn + 1, ctx->oov_dyn, nullptr, nullptr, ctx->oov_stream, ctx->zero_i);
+    if (rc != EVOSPEC_OK) return rc;
+    CUDA_TRY(cudaMemcpyAsync(ctx->oov_host, ctx->oov_dyn, (size_t)(p->n_dyn + 1) * sizeof(int32_t),
+                             cudaMemcpyDeviceToHost, ctx->oov_stream));
+    CUDA_TRY(cudaEventRecord(ctx->oov_done, ctx->oov_stream));
+    ctx->oov_pending = true;
+    return EVOSPEC_OK;
+}
+
+evospec_status evospec_oov_event_end(evospec_ctx* ctx, evospec_arc* arc, int64_t step, const int32_t* subset,
+                                    int32_t n, int32_t* out, int32_t* n_out, int32_t* added_host, int32_t* n_added,
+                                    int32_t* removed_host, int32_t* n_removed, void* stream) {
+    if (!ctx || !arc || !out || !n_out || n < 0 || (n > 0 && !subset))
+        return fail(EVOSPEC_EINPUT, "oov_event_end: null / bad argument");
+    if (!ctx->oov_pending) return fail(EVOSPEC_EINPUT, "oov_event_end: no event in flight");
+    ctx->oov_pending = false;
+    CUDA_TRY(cudaEventSynchronize(ctx->oov_done));
+    const int cnt = ctx->oov_host[0];
+    if (cnt < 0 || cnt > ctx->oov_cap) return fail(EVOSPEC_EINVARIANT, "oov_event_end: candidate count %d", cnt);
+    std::vector<int32_t> add(std::max(cnt, 1)), rem(std::max(cnt, 1));
+    int32_t na = 0, nr = 0;
+    evospec_status rc = evospec_arc_admit_delta(arc, ctx->oov_host + 1, cnt, step, add.data(), &na, rem.data(), &nr);
+    if (rc != EVOSPEC_OK) return fail(rc, "oov_event_end: ARC admission failed");
+    if (nr > n) return fail(EVOSPEC_EINPUT, "oov_event_end: %d removals from a %d-id subset (not the ARC's subset?)", nr, n);
+    cudaStream_t st = (cudaStream_t)stream;
+    // (pageable sources: the copies are staged before cudaMemcpyAsync returns)
+    if (nr) CUDA_TRY(cudaMemcpyAsync(ctx->oov_delta, rem.data(), (size_t)nr * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+    if (na) CUDA_TRY(cudaMemcpyAsync(ctx->oov_delta + ctx->oov_cap, add.data(), (size_t)na * sizeof(int32_t),
+                                     cudaMemcpyHostToDevice, st));
+    launch_subset_update(subset, n, ctx->oov_delta, nr, ctx->oov_delta + ctx->oov_cap, na, out, n_out,
+                         (int32_t*)ctx->flags, st);
+    ctx->launches += 1;
+    LAUNCH_CHECK("subset_update");
+    if (added_host) std::copy(add.begin(), add.begin() + na, added_host);
+    if (removed_host) std::copy(rem.begin(), rem.begin() + nr, removed_host);
+    if (n_added) *n_added = na;
+    if (n_removed) *n_removed = nr;
     return EVOSPEC_OK;
 }
 

@@ -17,6 +17,7 @@
 // >= min_res steps since its admission (A1); else the other list's (A2); else
 // plain LRU of the chosen list. Evicted tokens enter B1 / B2 at the MRU
 // end; ghost lists are trimmed at the LRU end to their capacities.
+#include <algorithm>
 #include <cstdint>
 #include <list>
 #include <unordered_map>
@@ -204,6 +205,34 @@ evospec_status evospec_arc_admit(evospec_arc* arc, const int32_t* tokens,
     int32_t* n_evicted) {
     if (!arc || n < 0 || (n > 0 && !tokens) || !n_evicted) return EVOSPEC_EINPUT;
     *n_evicted = arc->a.admit(tokens, n, step, evicted);
+    return EVOSPEC_OK;
+}
+
+evospec_status evospec_arc_admit_delta(evospec_arc* arc, const int32_t* tokens, int32_t n, int64_t step,
+    int32_t* added, int32_t* n_added, int32_t* removed, int32_t* n_removed) {
+    if (!arc || n < 0 || (n > 0 && !tokens) || !added || !n_added || !removed || !n_removed) return EVOSPEC_EINPUT;
+    es::Arc& a = arc->a;
+    std::vector<int32_t> before;
+    before.reserve(a.L[0].size() + a.L[1].size());
+    for (int l = 0; l < 2; ++l) before.insert(before.end(), a.L[l].begin(), a.L[l].end());
+    std::sort(before.begin(), before.end());
+    std::vector<int32_t> ev(n > 0 ? n : 1);
+    a.admit(tokens, n, step, ev.data());
+    std::vector<int32_t> after;
+    after.reserve(a.L[0].size() + a.L[1].size());
+    for (int l = 0; l < 2; ++l) after.insert(after.end(), a.L[l].begin(), a.L[l].end());
+    std::sort(after.begin(), after.end());
+    // net membership change: a token admitted and evicted in the same event, or
+    // evicted and re-admitted, is in neither list (the update's contract)
+    int na = 0, nr = 0;
+    size_t i = 0, j = 0;
+    while (i < before.size() || j < after.size()) {
+        if (j == after.size() || (i < before.size() && before[i] < after[j])) removed[nr++] = before[i++];
+        else if (i == before.size() || after[j] < before[i]) added[na++] = after[j++];
+        else { ++i; ++j; }
+    }
+    *n_added = na;
+    *n_removed = nr;
     return EVOSPEC_OK;
 }
 

@@ -128,6 +128,8 @@ void launch_coverage(const float* z, int n_rows, int V, const int32_t* S, int n_
 void launch_verify(const float* z, int V, int g, const int32_t* x, const int32_t* S, int n_S, const float* qS,
                    double it, int greedy, const double* u, const double* w, int32_t* pos_acc, int32_t* pos_tok,
                    int32_t* tokens, int32_t* n_acc_out, int* flags, cudaStream_t st);
+void launch_subset_update(const int32_t* S, int n, const int32_t* rem, int nr, const int32_t* add, int na,
+                          int32_t* out, int32_t* n_out, int32_t* flags, cudaStream_t st);
 bool lmh_tc_supported(const LmhArgs& a);
 int lmh_tc_grid();
 cudaError_t launch_lmh_tc(const LmhArgs& a, cudaStream_t st);
