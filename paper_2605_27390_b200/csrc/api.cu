@@ -764,11 +764,9 @@ static evospec_status lmh_impl(evospec_ctx* ctx, const void* W, int64_t n_w_rows
     a.logits_out = logits_out;
     a.part = ctx->part;
     a.m_ids = m_ids; a.m_vals = m_vals; a.m_lse = m_lse; a.m_probs = m_probs;
-    // thread-parallel epilogue fold (default; EVOSPEC_PAR_FOLD=0: the warp-per-row fold)
-    static const int par_fold = getenv("EVOSPEC_PAR_FOLD") ? atoi(getenv("EVOSPEC_PAR_FOLD")) : 1;
-    a.par_fold = par_fold;
-    static const int fin_opt = getenv("EVOSPEC_FIN_OPT") ? atoi(getenv("EVOSPEC_FIN_OPT")) : 15;
-    a.fin_opt = fin_opt;
+    a.par_fold = 1;    // thread-parallel epilogue fold (lmh_epilogue.cuh; the warp fold on single-tile CTAs)
+    a.fin_opt = 15;    // finalisation: H staged before the PDL wait, W-row L2 prefetch, multi-warp re-score,
+                       // parallel head threshold (each measured faster, round 1)
     if (list2) {   // two-list mode (draft_step overlap): one SM stays free for the union kernel
         a.list2 = list2; a.n_list2_dev = n_list2_dev; a.n_list2_max = n_list2_max; a.n1 = n_subset_max;
         a.grid = lmh_tc_grid() - 1;
@@ -887,16 +885,15 @@ evospec_status evospec_subset_logits_topk_ragged(evospec_ctx* ctx, const void* W
     LmhArgs probe{};
     probe.w_dtype = c.w_dtype; probe.h_dtype = c.h_dtype; probe.d = c.d; probe.n_w_rows = n_w_rows;
     probe.KP = k + kTopkPad; probe.n_h = 1;
-    const bool seg_ok = lmh_tc_supported(probe) && probe.KP <= 32 && !getenv("EVOSPEC_RAGGED_LOOP");
+    const bool seg_ok = lmh_tc_supported(probe) && probe.KP <= 32;
     int max_rows_seq = 0;
     for (int b = 0; b < B; ++b) max_rows_seq = std::max(max_rows_seq, h_offsets[b + 1] - h_offsets[b]);
     if (seg_ok) {
         // static block: one launch, row groups of <= 128 as segments over the same
         // static range (their CTAs read the same W rows at about the same time)
         // rows per static segment: smaller segments leave shared memory for more
-        // pipeline stages but stream the static rows more often (EVOSPEC_SEG_ROWS)
-        const int seg_cap = getenv("EVOSPEC_SEG_ROWS") ? std::max(16, std::min(kTcMaxRows, atoi(getenv("EVOSPEC_SEG_ROWS"))))
-                                                       : kRaggedSegRows;
+        // pipeline stages but stream the static rows more often (swept, kRaggedSegRows)
+        const int seg_cap = kRaggedSegRows;
         const int ns = (n_rows + seg_cap - 1) / seg_cap;
         const int per = (n_rows + ns - 1) / ns;
         int sh[kMaxSeg + 1];

@@ -355,7 +355,7 @@ void launch_lmh_finalize(const LmhArgs& a, int n_cta, int k, const float* wmax_d
         // a placement hint: two CTAs sharing an SM measured slower); more rows pack.
         // 512 threads with 5 or 10 list loads each; EVOSPEC_FIN_NT=1024 takes 1024
         // threads with 3 while the lists fit (measured equal in the sweep, slower alone)
-        static const int fin_nt = getenv("EVOSPEC_FIN_NT") ? atoi(getenv("EVOSPEC_FIN_NT")) : 512;
+        const int fin_nt = 512;   // (1024 threads with 3 loads each measured no faster)
         const int nq = n_cta * (kFin32LS / 4);
         auto go = [&](auto kern, int nt, bool& attr_set) {
             const size_t smem = std::max(fin32_smem_bytes(nt), (size_t)(a.n_h <= kNumSMs ? 120 * 1024 : 0));

@@ -376,9 +376,6 @@ struct HlParams {
     int nkb;          // d / 64
     int bh;           // H rows per TMA box (n_h padded to 8)
     int off_epi, off_bar;
-    int exp;          // experiment bits (EVOSPEC_HL_EXP): 1 no MMA, 2 no W copies, 4 no H loads
-    int warm;         // dry run of the epilogue before tile 0 (EVOSPEC_HL_WARM, default on)
-    int hrep;         // experiment (EVOSPEC_HL_HREP): CTA b reads its own copy of H (rows b * n_h)
 };
 
 // epilogue shared memory (floats / ints)
@@ -509,11 +506,10 @@ lmh_hl_kernel(const __grid_constant__ CUtensorMap tmap_h, LmhArgs a, HlParams hp
                 mbar_wait(&empty[stage], phase ^ 1);
                 const uint32_t sb = smem_u32(base + (size_t)stage * hp.slot_bytes) + doff;
                 const int nk = min(kps, hp.nkb - kb0);
-                for (int j = 0; j < nk && !(hp.exp & 64); ++j) {
+                for (int j = 0; j < nk; ++j) {
                     const uint32_t dW = sb + j * unit;
                     const int ko = (kb0 + j) * 128;
-                    if (hp.exp & 2) {
-                    } else if (ng == 16) {   // full 256-row tile: no predicates in the issue stream
+                    if (ng == 16) {   // full 256-row tile: no predicates in the issue stream
 #pragma unroll
                         for (int i = 0; i < 16; ++i) cp_async16(dW + i * 2048, src[i] + ko, pol_w);
                     } else {
@@ -523,8 +519,7 @@ lmh_hl_kernel(const __grid_constant__ CUtensorMap tmap_h, LmhArgs a, HlParams hp
                     }
                 }
                 if (warp == 2 && lane == 0 && t == 0 && (kb0 == 0 || kb0 == 8 || kb0 == 32)) HL_G0(2 + (kb0 == 8) + 2 * (kb0 == 32));
-                if (hp.exp & 8) mbar_arrive(&full[stage]);
-                else cp_async_arrive_noinc(&full[stage]);
+                cp_async_arrive_noinc(&full[stage]);
                 if (++stage == S) { stage = 0; phase ^= 1; }
             }
         }
@@ -542,11 +537,9 @@ lmh_hl_kernel(const __grid_constant__ CUtensorMap tmap_h, LmhArgs a, HlParams hp
                 for (int kb0 = 0; kb0 < hp.nkb; kb0 += kps) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     const int nk = min(kps, hp.nkb - kb0);
-                    if (hp.exp & 4) { mbar_arrive(&full[stage]); if (++stage == S) { stage = 0; phase ^= 1; } continue; }
                     mbar_arrive_expect_tx(&full[stage], (uint32_t)(nk * hp.bh * 128));
                     unsigned char* sb = base + (size_t)stage * hp.slot_bytes;
-                    const int hrow = hp.hrep ? bid * a.n_h : 0;
-                    for (int j = 0; j < nk; ++j) tma_load_2d(sb + j * unit, &tmap_h, &full[stage], (kb0 + j) * 64, hrow, pol_h);
+                    for (int j = 0; j < nk; ++j) tma_load_2d(sb + j * unit, &tmap_h, &full[stage], (kb0 + j) * 64, 0, pol_h);
                     if (++stage == S) { stage = 0; phase ^= 1; }
                 }
             }
@@ -571,15 +564,14 @@ lmh_hl_kernel(const __grid_constant__ CUtensorMap tmap_h, LmhArgs a, HlParams hp
                 if (lane == 0) {
                     const uint32_t sb = smem_u32(base + (size_t)stage * hp.slot_bytes);
                     const int nk = min(kps, hp.nkb - kb0);
-                    for (int j = 0; j < nk && !(hp.exp & 1); ++j) {
+                    for (int j = 0; j < nk; ++j) {
                         const uint32_t aa = sb + j * unit, ba = aa + kHlHBytes;
 #pragma unroll
                         for (int k = 0; k < 4; ++k)
                             umma_bf16(tmem_d, umma_desc_sw128(aa + k * 32), umma_desc_sw128(ba + k * 32), idesc,
                                       (uint32_t)((kb0 + j) | k));
                     }
-                    if (hp.exp & 16) mbar_arrive(&empty[stage]);
-                    else umma_commit(&empty[stage]);
+                    umma_commit(&empty[stage]);
                     if (kb0 + kps >= hp.nkb) umma_commit(&tfull[b]);
                 }
                 __syncwarp();
@@ -606,12 +598,11 @@ lmh_hl_kernel(const __grid_constant__ CUtensorMap tmap_h, LmhArgs a, HlParams hp
         hl_bar();
         int seen = 0;   // subset positions of this CTA so far (entries beyond the list were dropped)
         int t;
-        // t = -1: a dry run of the whole tile epilogue while tile 0 still streams, on
-        // the idle accumulator buffer 1 with every global / state side effect masked:
-        // the code runs once per tile, so its first execution is instruction-fetch
-        // bound (~500 cycles per KB of code, measured) -- warm it before it counts
-        for (t = hp.warm ? -1 : 0; t < 0 || has_tile(t); ++t) {
-            const bool dry = t < 0;
+        // (`dry`: a dry run of the tile epilogue on the idle accumulator before tile 0,
+        // to warm the instruction cache, was measured without gain and removed; the
+        // side-effect masks it needed remain as constants)
+        for (t = 0; has_tile(t); ++t) {
+            constexpr bool dry = false;
             int t0 = 0, tn = kHlTile;
             if (!dry) {
                 tile_range(t, t0, tn);
@@ -829,7 +820,7 @@ lmh_hl_kernel(const __grid_constant__ CUtensorMap tmap_h, LmhArgs a, HlParams hp
         const bool any = has_tile(0);
         const int ft0 = any ? fin_tile[0] : 0, ftn = any ? fin_tile[1] : 0, fseen = any ? fin_tile[2] : 0;
         const float* zs = (const float*)base;
-        const int nrep = (hp.exp & 512) ? 2 : 1;   // experiment: run the phase twice (I-cache)
+        const int nrep = 1;
         for (int rep = 0; rep < nrep; ++rep) {
         if (rep == nrep - 1) HL_CLK(3);
         const bool wr = rep == nrep - 1;
@@ -839,7 +830,7 @@ lmh_hl_kernel(const __grid_constant__ CUtensorMap tmap_h, LmhArgs a, HlParams hp
             int* rbp = buf_p + rr * kHlCapS;
             float mfin = -INFINITY, sfin = 0.0f;
             int n = 0;
-            if (any && !(hp.exp & 256)) {
+            if (any) {
                 float v[8];
 #pragma unroll
                 for (int j = 0; j < 8; ++j) v[j] = zs[rr * kHlZS + lane + 32 * j];
@@ -898,7 +889,7 @@ lmh_hl_kernel(const __grid_constant__ CUtensorMap tmap_h, LmhArgs a, HlParams hp
                 }
                 __syncwarp();
             }
-            for (int i = lane; i < LS && wr && !(hp.exp & 128); i += 32) {
+            for (int i = lane; i < LS && wr; i += 32) {
                 const bool h = i < n;
                 a.part.val[o * LS + i] = h ? rbv[i] : -INFINITY;
                 a.part.id[o * LS + i] = h ? rbp[i] : -1;
@@ -948,8 +939,7 @@ cudaError_t launch_lmh_hl(const LmhArgs& a, cudaStream_t st) {
     // S slots of several K-blocks each: every slot costs a fixed handshake (~0.3-0.5 us
     // measured: the consumer's wait + MMA issue + commit), so a slot carries as many
     // K-blocks as the ring allows with S slots (EVOSPEC_HL_SLOTS, default 2)
-    static const int s_env = getenv("EVOSPEC_HL_SLOTS") ? atoi(getenv("EVOSPEC_HL_SLOTS")) : 2;
-    int S = std::max(2, std::min(kHlMaxSlots, s_env));
+    int S = 2;   // (3, 4 and 8 slots measured slower at 36,864 rows)
     while (S > 2 && budget / S < unit) --S;
     const int kps = std::max(1, std::min(hp.nkb, budget / S / unit));
     hp.slot_bytes = kps * unit;
@@ -962,23 +952,7 @@ cudaError_t launch_lmh_hl(const LmhArgs& a, cudaStream_t st) {
     hp.off_bar = (hp.off_epi + epi + 15) & ~15;
     const size_t smem = (size_t)hp.off_bar + (size_t)(2 * S + 4) * 8 + 16 + 1024;
     CUtensorMap mh;
-    const void* hsrc = a.H;
-    uint64_t hrows = (uint64_t)a.n_h;
-    static const int hexp = getenv("EVOSPEC_HL_EXP") ? atoi(getenv("EVOSPEC_HL_EXP")) : 0;
-    hp.exp = hexp;
-    static const int warm = getenv("EVOSPEC_HL_WARM") ? atoi(getenv("EVOSPEC_HL_WARM")) : 0;
-    hp.warm = warm;
-    static const bool hrep = getenv("EVOSPEC_HL_HREP") != nullptr;
-    if (hrep) {   // experiment: one private copy of H per CTA (no shared L2 lines)
-        static void* rep = nullptr;
-        const size_t hb = (size_t)a.n_h * a.d * 2;
-        if (!rep && cudaMalloc(&rep, hb * G + 65536) != cudaSuccess) return cudaErrorMemoryAllocation;
-        for (int b = 0; b < G; ++b) cudaMemcpyAsync((char*)rep + b * hb, a.H, hb, cudaMemcpyDeviceToDevice, st);
-        hsrc = rep;
-        hrows = (uint64_t)a.n_h * G;
-        hp.hrep = 1;
-    }
-    if (!cached_map(&mh, hsrc, (uint64_t)a.d, hrows, 64, (uint32_t)hp.bh, CU_TENSOR_MAP_L2_PROMOTION_L2_128B))
+    if (!cached_map(&mh, a.H, (uint64_t)a.d, (uint64_t)a.n_h, 64, (uint32_t)hp.bh, CU_TENSOR_MAP_L2_PROMOTION_L2_128B))
         return cudaErrorInvalidValue;
     cudaError_t e = ensure_smem(lmh_hl_kernel, smem);
     if (e != cudaSuccess) return e;

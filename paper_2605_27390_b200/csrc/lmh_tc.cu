@@ -159,8 +159,7 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
     // list's stream, and a few full tiles on a few CTAs stream far faster than a
     // sliver of it on every CTA (a short tile still pays all d / 64 stages of H).
     int nt2 = a.list2 ? -1 : 0, n2 = 0;
-    // the CTA's rank in the second-list round robin: blockIdx scattered by a stride coprime
-    // with the grid (EVOSPEC_DYN_STRIDE) so the CTAs holding second-list tiles spread over the chip
+    // the CTA's rank in the second-list round robin
     const int dyn_rank = (int)(((long long)blockIdx.x * tp.dyn_stride) % gridDim.x);
     auto ensure2 = [&]() {
         if (nt2 >= 0) return;
@@ -387,15 +386,8 @@ cudaError_t launch_lmh_tc(const LmhArgs& a, cudaStream_t st) {
     tp.nkb = a.d / kBlockK;
     tp.last_tile = kLastTile;
     tp.dyn_tile = kTileM;
-    tp.dyn_stride = 1;
-    if (const char* e = getenv("EVOSPEC_DYN_STRIDE")) tp.dyn_stride = std::max(1, atoi(e));
-    {   // coprime with the grid, so that the ranks are a permutation
-        const int G = lmh_tc_grid(a);
-        auto gcd = [](int x, int y) { while (y) { const int t = x % y; x = y; y = t; } return x; };
-        while (gcd(tp.dyn_stride, G) != 1) ++tp.dyn_stride;
-    }
+    tp.dyn_stride = 1;   // (scattering the second-list CTAs over the chip measured equal)
     if (const char* e = getenv("EVOSPEC_DYN_TILE")) tp.dyn_tile = atoi(e) <= 0 ? 0 : std::max(16, std::min(kTileM, atoi(e)));
-    if (const char* e = getenv("EVOSPEC_LAST_TILE")) tp.last_tile = std::max(1, std::min(kTileM, atoi(e)));
     uint32_t cols = 2 * tp.n_pad, c = 32;
     while (c < cols) c <<= 1;
     tp.tmem_cols = c;

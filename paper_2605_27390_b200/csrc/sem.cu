@@ -353,33 +353,21 @@ void launch_sem_scan(const void* E, int e_dtype, int64_t n_rows, int d, const vo
     const int elems = e_dtype == 0 ? 8 : 4;
     const int n_slabs = (d + 32 * elems - 1) / (32 * elems);
     const size_t smem = (size_t)n_slabs * 32 * elems * sizeof(double);
-    // rows per stage RS and CTAs per SM: RS = 8, one CTA (216 KB) or RS = 4, two CTAs
-    const char* rse = getenv("EVOSPEC_SCAN_RS");
-    const int RS = rse ? atoi(rse) : kScanRS;
+    // 8-row stages (64 KB at d = 4096) in a 3-stage ring, one CTA per SM (4- and
+    // 2-row stages measured slower: per-stage overhead)
+    constexpr int RS = kScanRS, NS = 3;
     auto smem_for = [&](int rs, int ns) {
         return (size_t)ns * rs * d * 2 + kHistBins * 4 + (size_t)2 * ns * kScanConsumers * rs * 8 + 4 * ns * 8;
     };
-    const int NS = RS == 4 ? 6 : (RS == 2 ? 12 : 3);   // ~192 KB of ring at d = 4096
-    const char* env = getenv("EVOSPEC_SCAN");
-    if (e_dtype == 0 && d % 256 == 0 && d <= 256 * kScanConsumers && smem_for(RS, NS) <= 227 * 1024 &&
-        !(env && !strcmp(env, "v1"))) {
-        const char* pfe = getenv("EVOSPEC_SCAN_PF");
-        const int pf = pfe ? atoi(pfe) : kScanPf;
-        const int il = getenv("EVOSPEC_SCAN_IL") ? atoi(getenv("EVOSPEC_SCAN_IL")) : 1;
+    if (e_dtype == 0 && d % 256 == 0 && d <= 256 * kScanConsumers && smem_for(RS, NS) <= 227 * 1024) {
         const size_t sm = smem_for(RS, NS);
-        if (RS == 4) {
-            cudaFuncSetAttribute(sem_scan_tma_kernel<4, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            sem_scan_tma_kernel<4, 6><<<kNumSMs, (kScanConsumers + 1) * 32, sm, st>>>(
-                (const uint16_t*)E, n_rows, d, q, q_dtype, hist12, s64, key32, pf, il, zero_w, n_zero_w, zero_c);
-        } else if (RS == 2) {
-            cudaFuncSetAttribute(sem_scan_tma_kernel<2, 12>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            sem_scan_tma_kernel<2, 12><<<kNumSMs, (kScanConsumers + 1) * 32, sm, st>>>(
-                (const uint16_t*)E, n_rows, d, q, q_dtype, hist12, s64, key32, pf, il, zero_w, n_zero_w, zero_c);
-        } else {
-            cudaFuncSetAttribute(sem_scan_tma_kernel<8, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            sem_scan_tma_kernel<8, 3><<<kNumSMs, (kScanConsumers + 1) * 32, sm, st>>>(
-                (const uint16_t*)E, n_rows, d, q, q_dtype, hist12, s64, key32, pf, il, zero_w, n_zero_w, zero_c);
+        static thread_local size_t attr = 0;
+        if (attr < sm) {
+            cudaFuncSetAttribute(sem_scan_tma_kernel<RS, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            attr = sm;
         }
+        sem_scan_tma_kernel<RS, NS><<<kNumSMs, (kScanConsumers + 1) * 32, sm, st>>>(
+            (const uint16_t*)E, n_rows, d, q, q_dtype, hist12, s64, key32, kScanPf, 1, zero_w, n_zero_w, zero_c);
     } else if (e_dtype == 0) {
         cudaFuncSetAttribute(sem_scan_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         sem_scan_kernel<0><<<kNumSMs, kScanWarps * 32, smem, st>>>(E, n_rows, d, q, q_dtype, hist12, s64, key32,

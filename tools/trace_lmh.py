@@ -2,7 +2,7 @@
 
 Runs subset_logits_topk on n_S = 36,864 gathered rows, n_h = 60, with
 EVOSPEC_TRACE=1 and prints per-CTA globaltimer phases (us, relative to the
-earliest CTA start), for each EVOSPEC_PF prefetch distance given on argv.
+earliest CTA start), (one run).
 """
 import os
 import statistics
@@ -30,8 +30,7 @@ ctx = es.Context(V=V, d=d, w_dtype=torch.bfloat16, h_dtype=torch.bfloat16, max_s
 ctx.prepare_weights(Wd)
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 names = ["start", "prod_done", "mma_done", "t0_ready", "t0_fold", "t1_ready", "t1_fold", "end"]
-for pf in (sys.argv[1:] or ["2"]):
-    os.environ["EVOSPEC_PF"] = pf
+for pf in ["default"]:
     evs = []
     for it in range(8):
         flush.fill_(it)
