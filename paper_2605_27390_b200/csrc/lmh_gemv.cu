@@ -59,7 +59,10 @@ template <int DT, int NH>
 __global__ void __launch_bounds__(kGemvWarps * 32, 2)
 lmh_gemv_kernel(LmhArgs a, int h_row0) {
     constexpr int ELEMS = DT == 0 ? 8 : 4;
-    constexpr int T = kGemvRows * NH;
+    // rows per warp batch: 16 for a single tree row (one batch per 128-row tile: no
+    // pipeline drain between batches, twice the loads in flight), else 8
+    constexpr int ROWS = NH == 1 ? 16 : kGemvRows;
+    constexpr int T = ROWS * NH;
     constexpr int NV = T >= 32 ? T / 32 : 1;
     extern __shared__ __align__(16) unsigned char g_sm[];
     const int d = a.d;
@@ -88,13 +91,13 @@ lmh_gemv_kernel(LmhArgs a, int h_row0) {
 
     for (int tb = p0; tb < p1; tb += kTile) {
         const int tn = min(kTile, p1 - tb);
-        // each warp: rows [tb + 16 w, tb + 16 w + 16) in two batches of 8
-        for (int bt = 0; bt < kTile / (kGemvWarps * kGemvRows); ++bt) {
-            const int rbase = warp * (kTile / kGemvWarps) + bt * kGemvRows;   // tile-local
-            const char* rowp[kGemvRows];
-            bool ok[kGemvRows];
+        // each warp: rows [tb + 16 w, tb + 16 w + 16) in batches of ROWS
+        for (int bt = 0; bt < kTile / (kGemvWarps * ROWS); ++bt) {
+            const int rbase = warp * (kTile / kGemvWarps) + bt * ROWS;   // tile-local
+            const char* rowp[ROWS];
+            bool ok[ROWS];
 #pragma unroll
-            for (int i = 0; i < kGemvRows; ++i) {
+            for (int i = 0; i < ROWS; ++i) {
                 const int p = rbase + i;
                 ok[i] = p < tn;
                 const int32_t id = ok[i] ? a.subset[tb + p] : 0;
@@ -107,9 +110,9 @@ lmh_gemv_kernel(LmhArgs a, int h_row0) {
             for (int ch = 0; ch < n_chunks; ++ch) {
                 const int c0 = ch * 32 * ELEMS + lane * ELEMS;
                 const bool cok = c0 < d;
-                uint4 u[kGemvRows];
+                uint4 u[ROWS];
 #pragma unroll
-                for (int i = 0; i < kGemvRows; ++i)
+                for (int i = 0; i < ROWS; ++i)
                     u[i] = (ok[i] && cok) ? ld_stream(rowp[i] + (size_t)c0 * (DT == 0 ? 2 : 4))
                                           : make_uint4(0, 0, 0, 0);
 #pragma unroll
@@ -118,7 +121,7 @@ lmh_gemv_kernel(LmhArgs a, int h_row0) {
 #pragma unroll
                     for (int j = 0; j < ELEMS; ++j) hv[j] = H_sm[((r * n_chunks + ch) * ELEMS + j) * 32 + lane];
 #pragma unroll
-                    for (int i = 0; i < kGemvRows; ++i) {
+                    for (int i = 0; i < ROWS; ++i) {
                         float f[ELEMS];
                         if constexpr (DT == 0) {
                             float g[8];
