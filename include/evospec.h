@@ -211,6 +211,10 @@ evospec_status evospec_build_subset_batched(evospec_ctx *ctx,
     int32_t *out_dyn_ids, int32_t *out_dyn_offsets,
     void *stream);
 
+/* The last full-index scan's fp64 scores s_v = q . E_v (a2), rows [0, n) (n <= V)
+ * into out_dev (device): the scan's own output, for testing its ring (the TMA
+ * pipeline's release / refill ordering) against the oracle and itself. */
+evospec_status evospec_last_scores(evospec_ctx *ctx, double *out_dev, int64_t n, void *stream);
 /* Debug/parity accessor: copies the S_sem SET of the last build on this
  * context (N_sem device ids, in no particular order) into out_dev. Async. */
 evospec_status evospec_last_semantic(evospec_ctx *ctx, int32_t *out_dev, int32_t n, void *stream);

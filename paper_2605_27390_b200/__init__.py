@@ -33,7 +33,7 @@ EXPORTED = [
     "evospec_subset_update",
     "evospec_sync_status",
     "evospec_build_local_candidates", "evospec_build_subset_from_candidates",
-    "evospec_arc_admit_delta", "evospec_oov_event_begin", "evospec_oov_event_end",
+    "evospec_arc_admit_delta", "evospec_oov_event_begin", "evospec_oov_event_end", "evospec_last_scores",
 ]
 
 STAGES = ["scan", "select", "union", "lmh", "finalize", "merge", "copy"]
@@ -116,6 +116,7 @@ def lib() -> C.CDLL:
             "evospec_arc_admit": ([vp, vp, i32, i64, vp, vp], i32),
             "evospec_arc_state": ([vp, vp, i32, vp], i32),
             "evospec_arc_admit_delta": ([vp, vp, i32, i64, vp, vp, vp, vp], i32),
+            "evospec_last_scores": ([vp, vp, i64, vp], i32),
             "evospec_oov_event_begin": ([vp, vp, i64, vp, vp, i32, vp, i32, vp, vp, C.POINTER(BuildParams), vp], i32),
             "evospec_oov_event_end": ([vp, vp, i64, vp, i32, vp, vp, vp, vp, vp, vp, vp], i32),
             "evospec_subset_update": ([vp, i32, vp, i32, vp, i32, vp, vp, vp, vp], i32),
@@ -463,6 +464,13 @@ class Context:
             None if co is None else C.cast(co, C.c_void_p), C.byref(p), _ptr(dyn), _ptr(offs),
             _stream(stream)))
         return dyn, offs
+
+    def last_scores(self, n: int, stream=None):
+        """The last full-index scan's fp64 scores of rows [0, n) (evospec_last_scores)."""
+        import torch
+        out = torch.empty(max(n, 1), dtype=torch.float64, device=f"cuda:{self.device}")
+        _check(lib().evospec_last_scores(self._h, _ptr(out), int(n), _stream(stream)))
+        return out[:n]
 
     def last_semantic(self, n: int, stream=None):
         import torch

@@ -685,6 +685,13 @@ evospec_status evospec_build_subset_batched(evospec_ctx* ctx, const void* E, int
     return EVOSPEC_OK;
 }
 
+evospec_status evospec_last_scores(evospec_ctx* ctx, double* out_dev, int64_t n, void* stream) {
+    if (!ctx || !out_dev || n < 0 || n > ctx->cfg.V) return fail(EVOSPEC_EINPUT, "last_scores: bad argument");
+    CUDA_TRY(cudaMemcpyAsync(out_dev, ctx->s64, (size_t)n * sizeof(double), cudaMemcpyDeviceToDevice,
+                             (cudaStream_t)stream));
+    return EVOSPEC_OK;
+}
+
 evospec_status evospec_last_semantic(evospec_ctx* ctx, int32_t* out_dev, int32_t n, void* stream) {
     if (!ctx || !out_dev || n < 0 || n > ctx->cfg.max_sem) return fail(EVOSPEC_EINPUT, "last_semantic: bad argument");
     CUDA_TRY(cudaMemcpyAsync(out_dev, ctx->sem_ids, (size_t)n * 4, cudaMemcpyDeviceToDevice, (cudaStream_t)stream));

@@ -359,9 +359,23 @@ void launch_sem_scan(const void* E, int e_dtype, int64_t n_rows, int d, const vo
     auto smem_for = [&](int rs, int ns) {
         return (size_t)ns * rs * d * 2 + kHistBins * 4 + (size_t)2 * ns * kScanConsumers * rs * 8 + 4 * ns * 8;
     };
+    // EVOSPEC_SCAN_RING2=1 (test only, tests/test_gpu_scan_ring.py): a 2-stage ring -- every
+    // slot is refilled while the slab warps of the stage before it still compute, the
+    // tightest reuse of the release / refill ordering; the scores must equal the 3-stage
+    // ring's bit for bit (same summation order)
+    static const bool ring2 = getenv("EVOSPEC_SCAN_RING2") != nullptr;
     if (e_dtype == 0 && d % 256 == 0 && d <= 256 * kScanConsumers && smem_for(RS, NS) <= 227 * 1024) {
-        const size_t sm = smem_for(RS, NS);
-        static thread_local size_t attr = 0;
+        const size_t sm = smem_for(RS, ring2 ? 2 : NS);
+        static thread_local size_t attr = 0, attr2 = 0;
+        if (ring2) {
+            if (attr2 < sm) {
+                cudaFuncSetAttribute(sem_scan_tma_kernel<RS, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+                attr2 = sm;
+            }
+            sem_scan_tma_kernel<RS, 2><<<kNumSMs, (kScanConsumers + 1) * 32, sm, st>>>(
+                (const uint16_t*)E, n_rows, d, q, q_dtype, hist12, s64, key32, kScanPf, 1, zero_w, n_zero_w, zero_c);
+            return;
+        }
         if (attr < sm) {
             cudaFuncSetAttribute(sem_scan_tma_kernel<RS, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
             attr = sm;
