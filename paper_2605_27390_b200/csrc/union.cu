@@ -247,9 +247,16 @@ ES_DEV void block_topM(const uint64_t* ck, const int32_t* cid, uint8_t* cf, int 
 
 // K exact top-M selections at once (K <= 3): selection j takes the M[j] best
 // (key desc, id asc) of the candidates whose flag has a bit of A[j] and marks
-// them with S[j]. The radix passes of block_topM run in lockstep: one read of
-// the candidates per pass feeds K histograms, one K-wide block scan finds the K
-// boundary bins -- the passes' barriers are paid once instead of K times.
+// them with S[j]. Key-linear binning: selection j keeps a window of keys
+// [base, base + wspan] that holds its boundary; a pass histograms the active
+// keys of every live window into kSelBins equal-width bins (one read of the
+// candidates feeds the K histograms, one K-wide block scan finds the K
+// boundary bins) and narrows the window to the boundary bin. The keys of
+// fp64 scores spread over their range, so one pass usually leaves a boundary
+// bin of a few dozen candidates: those are ranked exactly by counting under
+// (key desc, id asc) and the first `remaining` taken. A boundary bin of more
+// than kRankCap candidates that is a single key (equal scores) goes to
+// block_topM, whose ~id digits settle it.
 template <int K>
 ES_DEV void block_scan_multi(const int (&v)[K], int* warp_tot /*[K][33]*/, int (&excl)[K]) {
     const int lane = lane_id(), wid = warp_id(), nw = blockDim.x / 32;
@@ -281,10 +288,17 @@ ES_DEV void block_scan_multi(const int (&v)[K], int* warp_tot /*[K][33]*/, int (
     __syncthreads();
 }
 
+constexpr int kRankCap = kSelBins;   // the rank lists reuse the selection's histogram
+enum : int { kWLive = 0, kWWhole = 1, kWRank = 2, kWFallback = 3, kWAll = 4, kWNone = 5 };
+struct WSel {
+    uint64_t kmin, kmax, base, wspan;
+    int shift, bin, above, remaining, mode, gn;
+};
+
 template <int K>
 ES_DEV void block_topM_multi(const uint64_t* ck, const int32_t* cid, uint8_t* cf, int n, const uint8_t (&A)[K],
                              const uint8_t (&S)[K], const int (&M)[K], uint32_t* hist /*[K][kSelBins]*/,
-                             BSel* st /*[K]*/, int* warp_tot /*[K][33]*/, long long* tr = nullptr,
+                             WSel* ws /*[K]*/, BSel* bs /*[K]*/, int* warp_tot /*[K][33]*/, long long* tr = nullptr,
                              const int* pre_c = nullptr, const uint64_t* pre_lo = nullptr,
                              const uint64_t* pre_hi = nullptr) {
     const int tid = threadIdx.x, T = blockDim.x, lane = lane_id();
@@ -309,13 +323,10 @@ ES_DEV void block_topM_multi(const uint64_t* ck, const int32_t* cid, uint8_t* cf
         }
     }
     stamp(10);
-    if (tid < K) { st[tid].kmin = ~0ull; st[tid].kmax = 0ull; }
-    int cnt[K];
+    if (tid < K) { ws[tid].kmin = ~0ull; ws[tid].kmax = 0ull; ws[tid].gn = 0; }
     {
         int ex[K];
-        block_scan_multi<K>(c, warp_tot, ex);   // (syncs: st initialised before the atomics)
-#pragma unroll
-        for (int j = 0; j < K; ++j) cnt[j] = 0;
+        block_scan_multi<K>(c, warp_tot, ex);   // (syncs: ws initialised before the atomics)
         // totals: the last thread's exclusive prefix plus its own count
         if (tid == T - 1)
 #pragma unroll
@@ -326,70 +337,54 @@ ES_DEV void block_topM_multi(const uint64_t* ck, const int32_t* cid, uint8_t* cf
         kmin[j] = warp_min_u64(kmin[j]);
         kmax[j] = warp_max_u64(kmax[j]);
         if (lane == 0 && kmin[j] <= kmax[j]) {
-            atomicMin((unsigned long long*)&st[j].kmin, kmin[j]);
-            atomicMax((unsigned long long*)&st[j].kmax, kmax[j]);
+            atomicMin((unsigned long long*)&ws[j].kmin, kmin[j]);
+            atomicMax((unsigned long long*)&ws[j].kmax, kmax[j]);
         }
     }
     __syncthreads();
-#pragma unroll
-    for (int j = 0; j < K; ++j) cnt[j] = warp_tot[j * 33 + 32];
-    bool all[K];   // select every active candidate (M >= count); M <= 0 selects none
-#pragma unroll
-    for (int j = 0; j < K; ++j) all[j] = M[j] >= cnt[j];
     if (tid < K) {
-        st[tid].kmask = 0; st[tid].kval = 0; st[tid].imask = 0; st[tid].ival = 0;
-        st[tid].remaining = M[tid];
-        st[tid].done = (M[tid] <= 0 || M[tid] >= cnt[tid]) ? 1 : 0;
+        WSel& w = ws[tid];
+        const int cnt = warp_tot[tid * 33 + 32];
+        w.remaining = M[tid];
+        if (M[tid] <= 0) w.mode = kWNone;
+        else if (M[tid] >= cnt) w.mode = kWAll;
+        else {
+            w.mode = kWLive;
+            w.base = w.kmin;
+            w.wspan = w.kmax - w.kmin;
+            const int bl = w.wspan ? 64 - __clzll((long long)w.wspan) : 0;
+            w.shift = bl > 10 ? bl - 10 : 0;    // (wspan >> shift) < kSelBins
+        }
     }
     __syncthreads();
-    int kbit[K], ibit[K];
-#pragma unroll
-    for (int j = 0; j < K; ++j) {
-        const uint64_t diff = st[j].kmin ^ st[j].kmax;
-        kbit[j] = diff ? 63 - __clzll((long long)diff) : -1;
-        ibit[j] = 31;
-    }
     stamp(11);
-    for (int pass = 0; pass < 16; ++pass) {
+    for (int pass = 0; pass < 8; ++pass) {
+        WSel my[K];
         bool live[K];
         bool any = false;
 #pragma unroll
         for (int j = 0; j < K; ++j) {
-            live[j] = !st[j].done && (kbit[j] >= 0 || ibit[j] >= 0);
+            my[j] = ws[j];
+            live[j] = my[j].mode == kWLive;
             any |= live[j];
         }
         if (!any) break;
-        int lo[K], hi_[K];
-        uint32_t dmask[K];
-        bool on_key[K];
-#pragma unroll
-        for (int j = 0; j < K; ++j) {
-            on_key[j] = kbit[j] >= 0;
-            hi_[j] = on_key[j] ? kbit[j] : ibit[j];
-            const int width = hi_[j] + 1 < 10 ? hi_[j] + 1 : 10;
-            lo[j] = hi_[j] - width + 1;
-            dmask[j] = (1u << width) - 1u;
-        }
 #pragma unroll
         for (int j = 0; j < K; ++j)
             if (live[j]) for (int b = tid; b < kSelBins; b += T) hist[j * kSelBins + b] = 0;
         __syncthreads();
-        BSel my[K];
-#pragma unroll
-        for (int j = 0; j < K; ++j) my[j] = st[j];
+        // equal-width bins over the window: ~n / kSelBins per bin, plain smem atomics
         for (int i = tid; i < n; i += T) {
             const uint8_t f = cf[i];
             const uint64_t k = ck[i];
-            const int32_t id = cid[i];
 #pragma unroll
             for (int j = 0; j < K; ++j)
-                if (live[j] && (f & A[j]) && bmatch(k, id, my[j]))
-                    atomicAdd(&hist[j * kSelBins + (on_key[j] ? (uint32_t)(k >> lo[j]) & dmask[j]
-                                                              : ((0xFFFFFFFFu - (uint32_t)id) >> lo[j]) & dmask[j])],
-                              1u);
+                if (live[j] && (f & A[j]) && k - my[j].base <= my[j].wspan)   // (k < base wraps: outside)
+                    atomicAdd(&hist[j * kSelBins + (int)((k - my[j].base) >> my[j].shift)], 1u);
         }
         __syncthreads();
         if (pass == 0) stamp(12);
+        // thread t owns bin (kSelBins-1-t): an exclusive scan over t counts the bins above it
         const int bin = kSelBins - 1 - tid;
         int hb[K], above[K];
 #pragma unroll
@@ -398,36 +393,89 @@ ES_DEV void block_topM_multi(const uint64_t* ck, const int32_t* cid, uint8_t* cf
 #pragma unroll
         for (int j = 0; j < K; ++j)
             if (live[j] && tid < kSelBins && above[j] < my[j].remaining && above[j] + hb[j] >= my[j].remaining) {
-                st[j].found_bin = bin;
-                st[j].found_above = above[j];
+                ws[j].bin = bin;
+                ws[j].above = above[j];
             }
         __syncthreads();
         if (tid < K && live[tid]) {
-            BSel& s2 = st[tid];
-            const int b = s2.found_bin;
-            s2.remaining -= s2.found_above;
-            if (on_key[tid]) { s2.kmask |= (uint64_t)dmask[tid] << lo[tid]; s2.kval |= (uint64_t)b << lo[tid]; }
-            else { s2.imask |= dmask[tid] << lo[tid]; s2.ival |= (uint32_t)b << lo[tid]; }
-            if ((uint32_t)s2.remaining == hist[tid * kSelBins + b]) s2.done = 1;
+            WSel& w = ws[tid];
+            w.remaining -= w.above;
+            const uint32_t h = hist[tid * kSelBins + w.bin];
+            if ((uint32_t)w.remaining == h) w.mode = kWWhole;
+            else if (h <= (uint32_t)kRankCap) w.mode = kWRank;
+            else if (w.shift == 0) w.mode = kWFallback;
+            else {   // narrow to the boundary bin
+                w.base += (uint64_t)w.bin << w.shift;
+                w.wspan = (1ull << w.shift) - 1ull;
+                w.shift = w.shift > 10 ? w.shift - 10 : 0;
+            }
         }
         __syncthreads();
-#pragma unroll
-        for (int j = 0; j < K; ++j)
-            if (live[j]) { if (on_key[j]) kbit[j] = lo[j] - 1; else ibit[j] = lo[j] - 1; }
         stamp(1 + pass);
     }
-    BSel my[K];
+    // marking: everything above the boundary bin (and the bin itself when taken
+    // whole); the boundary bins to be ranked are gathered into the histograms.
+    // Per selection: selected iff key >= hi; ranked iff lo <= key < hi.
+    WSel my[K];
+    uint8_t a_eff[K];
+    uint64_t klo[K], khi[K];
 #pragma unroll
-    for (int j = 0; j < K; ++j) my[j] = st[j];
+    for (int j = 0; j < K; ++j) {
+        my[j] = ws[j];
+        a_eff[j] = (my[j].mode == kWNone || my[j].mode == kWFallback) ? 0 : A[j];
+        if (my[j].mode == kWAll) { klo[j] = 0; khi[j] = 0; }
+        else {
+            klo[j] = my[j].base + ((uint64_t)my[j].bin << my[j].shift);
+            const uint64_t up = (uint64_t)(my[j].bin + 1) << my[j].shift;
+            khi[j] = my[j].base + (up > my[j].wspan ? my[j].wspan + 1 : up);
+            if (my[j].mode == kWWhole) khi[j] = klo[j];
+            if (my[j].mode != kWRank) klo[j] = khi[j];
+        }
+    }
     for (int i = tid; i < n; i += T) {
         const uint8_t f = cf[i];
+        const uint64_t k = ck[i];
         uint8_t add = 0;
 #pragma unroll
-        for (int j = 0; j < K; ++j)
-            if ((f & A[j]) && M[j] > 0 && (all[j] || bselected(ck[i], cid[i], my[j]))) add |= S[j];
+        for (int j = 0; j < K; ++j) {
+            if (!(f & a_eff[j])) continue;
+            if (k >= khi[j]) add |= S[j];
+            else if (k >= klo[j]) hist[j * kSelBins + atomicAdd(&ws[j].gn, 1)] = i;
+        }
         if (add) cf[i] = f | add;
     }
     __syncthreads();
+    stamp(13);
+    // the boundary bins: rank each member among its bin's members by counting
+    int tot = 0;
+#pragma unroll
+    for (int j = 0; j < K; ++j) tot += my[j].mode == kWRank ? ws[j].gn : 0;
+    for (int p = tid; p < tot; p += T) {
+        int j = 0, start = 0, cnt = 0, rem = 0, acc = 0;
+        unsigned int sb = 0;
+#pragma unroll
+        for (int q = 0; q < K; ++q) {   // (statically indexed: no local-memory copies of my[])
+            const int g = my[q].mode == kWRank ? ws[q].gn : 0;
+            if (p >= acc && p < acc + g) { j = q; start = acc; cnt = g; rem = my[q].remaining; sb = S[q]; }
+            acc += g;
+        }
+        const uint32_t* list = hist + j * kSelBins;
+        const int a = (int)list[p - start];
+        const uint64_t ka = ck[a];
+        const int32_t ia = cid[a];
+        int rank = 0;
+        for (int q = 0; q < cnt; ++q) {
+            const int b = (int)list[q];
+            rank += before(ck[b], cid[b], ka, ia) ? 1 : 0;
+        }
+        if (rank < rem)   // cf bytes of other members are written concurrently: word atomics
+            atomicOr((unsigned int*)(cf + (a & ~3)), sb << (8 * (a & 3)));
+    }
+    __syncthreads();
+    stamp(14);
+#pragma unroll
+    for (int j = 0; j < K; ++j)
+        if (my[j].mode == kWFallback) block_topM(ck, cid, cf, n, A[j], S[j], M[j], hist, bs[j], warp_tot);
 }
 enum : uint8_t { kCand = 1, kSem = 2, kGs = 4, kNew = 8, kTake = 16 };
 
@@ -457,6 +505,7 @@ union_kernel(int V, const int32_t* __restrict__ static_ids, int n_static,
     __shared__ int warp_tot[3 * 33];
     __shared__ uint32_t hist[3 * kSelBins];
     __shared__ BSel bsel[3];
+    __shared__ WSel wsel[3];
     __shared__ int nG_s, bad_s, taken_s, ngs_s, sem_n_s;
 
     const int tid = threadIdx.x, lane = lane_id(), T = blockDim.x;
@@ -567,7 +616,7 @@ union_kernel(int V, const int32_t* __restrict__ static_ids, int n_static,
         const int M[3] = {n_sem, budget, ngs};
         const int pc[3] = {st_c[0], st_c[1], st_c[0]};
         const uint64_t plo[3] = {st_lo[0], st_lo[1], st_lo[0]}, phi[3] = {st_hi[0], st_hi[1], st_hi[0]};
-        block_topM_multi<3>(ck, cid, cf, n_cand, A, S, M, hist, bsel, warp_tot, trace ? trace + 7 : nullptr, pc, plo,
+        block_topM_multi<3>(ck, cid, cf, n_cand, A, S, M, hist, wsel, bsel, warp_tot, trace ? trace + 7 : nullptr, pc, plo,
                             phi);
         if (trace && tid == 0) trace[16] = n_cand;
     }
