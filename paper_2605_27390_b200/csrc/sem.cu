@@ -267,18 +267,33 @@ sem_scan_tma_kernel(const uint16_t* __restrict__ E, int64_t n_rows, int d, const
             qv[j] = v * 0x1p896;
         }
     }
+    // this lane's 16 bytes of its slab in row 0 of slot 0, as a shared-window address
+    const uint32_t my_s = s_u32(ring) + (uint32_t)(warp * 512 + lane * 16);
     for (int i = 0; i < n_stage; ++i) {
         const int slot = i % kScanStages;
         s_mbar_wait(&full[slot], (uint32_t)(i / kScanStages) & 1);
         const int64_t row0 = stage_row(i);
         const int nr = (int)min((int64_t)kScanRowsPerStage, r_end - row0);
-        const unsigned char* st = ring + slot * stage_bytes + (size_t)warp * 512 + (size_t)lane * 16;
+        const uint32_t st = my_s + (uint32_t)(slot * stage_bytes);
         // this warp's slab of the stage into registers, then the slot goes back to
         // the producer at once: the ring refills while the warp computes
         uint4 u[kScanRowsPerStage];
+        if (nr == kScanRowsPerStage) {
 #pragma unroll
-        for (int r = 0; r < kScanRowsPerStage; ++r)
-            u[r] = r < nr ? *(const uint4*)(st + (size_t)r * row_bytes) : make_uint4(0, 0, 0, 0);
+            for (int r = 0; r < kScanRowsPerStage; ++r)
+                asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                             : "=r"(u[r].x), "=r"(u[r].y), "=r"(u[r].z), "=r"(u[r].w)
+                             : "r"(st + (uint32_t)(r * row_bytes)) : "memory");
+        } else {
+#pragma unroll
+            for (int r = 0; r < kScanRowsPerStage; ++r) {
+                u[r] = make_uint4(0, 0, 0, 0);
+                if (r < nr)
+                    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                                 : "=r"(u[r].x), "=r"(u[r].y), "=r"(u[r].z), "=r"(u[r].w)
+                                 : "r"(st + (uint32_t)(r * row_bytes)) : "memory");
+            }
+        }
         // every lane orders its generic-proxy reads of the slot before the async-proxy
         // (bulk copy) refill that the release lets the producer issue
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
