@@ -104,6 +104,7 @@ struct evospec_ctx {
                                   // clears it after the selection has read it)
     bool hist_dirty = false;      // a build stopped between its scan and its union: clear first
     uint32_t* ubits = nullptr;    // [V/32] union bitmap handed to the emit kernel
+    uint32_t* sbits = nullptr;    // [V/32] static-core bitmap (static_bits_kernel -> union; zero between builds)
     int32_t* zero_i = nullptr;    // a device 0 (dyn-only union output at offset 0)
     // N1 OOV event (evospec_oov_event_begin / _end): the event's formation runs on a
     // side stream while the caller keeps drafting on the current subset
@@ -183,12 +184,14 @@ struct evospec_ctx {
 
 namespace {
 constexpr int kTimingSlots = 4096;
-constexpr int kTraceLen = 2 * kNumSMs * 8 + 16 + 32 + 64;   // LM-head CTAs, finalize rows, union stamps
+constexpr int kTraceLen = 2 * kNumSMs * 8 + 16 + 32 + 64 + 2 * kNumSMs + 8;   // LM-head CTAs, finalize rows,
+                                                                              // union stamps, scan / candidate stamps
 
 // union stamps live after the LM-head / finalize slots
 long long* union_trace(evospec_ctx* ctx, cudaStream_t st) {
     if (!getenv("EVOSPEC_TRACE")) return nullptr;
     if (!ctx->trace && cudaMalloc(&ctx->trace, kTraceLen * sizeof(long long)) != cudaSuccess) return nullptr;
+    set_step_trace(ctx->trace + 2 * kNumSMs * 8 + 112);
     return ctx->trace + 2 * kNumSMs * 8;
 }
 
@@ -239,7 +242,7 @@ evospec_status evospec_destroy(evospec_ctx* ctx) {
                     ctx->flags, ctx->wmax, ctx->g_ids, ctx->g_vals, ctx->g_m, ctx->g_s, ctx->st_q, ctx->st_H,
                     ctx->st_seeds, ctx->st_ctx, ctx->st_S, ctx->st_nS, ctx->st_local, ctx->st_nlocal,
                     ctx->st_tids, ctx->st_tvals, ctx->st_m, ctx->st_s, ctx->st_oids, ctx->st_ovals,
-                    ctx->st_lse, ctx->st_probs, ctx->ubits, ctx->rg_ids, ctx->rg_vals, ctx->rg_m, ctx->rg_s, ctx->rg_seg, ctx->rg_segcta, ctx->ver_acc, ctx->ver_tok, ctx->zero_i};
+                    ctx->st_lse, ctx->st_probs, ctx->ubits, ctx->sbits, ctx->rg_ids, ctx->rg_vals, ctx->rg_m, ctx->rg_s, ctx->rg_seg, ctx->rg_segcta, ctx->ver_acc, ctx->ver_tok, ctx->zero_i};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (ctx->comm && nccl().loaded) nccl().CommDestroy(ctx->comm);
@@ -289,6 +292,7 @@ evospec_status evospec_create(evospec_ctx** out, const evospec_config* cfg, int 
     cudaError_t e = cudaSuccess;
     auto A = [&](cudaError_t r) { if (e == cudaSuccess) e = r; };
     x->cand_cap = union_cand_cap(c.V, 64);
+    if (getenv("EVOSPEC_TRACE")) union_trace(x, nullptr);   // (stamps set up before any graph capture)
     if (c.max_sem > x->cand_cap) {
         const int cap_v = x->cand_cap;
         delete x;
@@ -297,6 +301,7 @@ evospec_status evospec_create(evospec_ctx** out, const evospec_config* cfg, int 
     }
     const size_t cap = (size_t)x->cand_cap;
     A(dalloc(&x->s64, V)); A(dalloc(&x->key32, V)); A(dalloc(&x->hist12, kHistBins)); A(dalloc(&x->ubits, (V + 31) / 32)); A(cudaMemset(x->hist12, 0, kHistBins * sizeof(uint32_t)));
+    A(dalloc(&x->sbits, (V + 31) / 32 + 4)); A(cudaMemset(x->sbits, 0, ((V + 31) / 32 + 4) * sizeof(uint32_t)));
     A(dalloc(&x->hist, 12 * kHistBins));
     A(dalloc(&x->ver_acc, kMaxChain + 1)); A(dalloc(&x->ver_tok, kMaxChain + 1));
     A(dalloc(&x->zero_i, 1)); A(cudaMemset(x->zero_i, 0, sizeof(int32_t)));
@@ -399,7 +404,8 @@ static evospec_status union_from_candidates(evospec_ctx* ctx, const double* cand
                                             const int32_t* col, const int32_t* ctx_ids, int32_t n_ctx,
                                             const evospec_build_params* p, int32_t* out_ids, int32_t* out_n,
                                             int32_t* out_local_ids, int32_t* out_local_n, cudaStream_t st,
-                                            const int32_t* dyn_base, cudaEvent_t wait_before_union);
+                                            const int32_t* dyn_base, cudaEvent_t wait_before_union,
+                                            bool sbits_ready);
 
 // a2 on a vocabulary shard: exact fp64 scores of this shard's E rows (global id
 // = row * R + r) and the shard's exact top-N (s desc, id asc), padded with id -1
@@ -457,7 +463,7 @@ static evospec_status build_impl(evospec_ctx* ctx, const void* E, int64_t n_e_ro
     if (ext)
         return union_from_candidates(ctx, ext_s, ext_id, n_ext, static_ids, n_static, seeds, n_seed, row_ptr, col,
                                      ctx_ids, n_ctx, p, out_ids, out_n, out_local_ids, out_local_n, st, dyn_base,
-                                     wait_before_union);
+                                     wait_before_union, false);
     const bool full_scan = n_e_rows == c.V;
     const int64_t local_rows = shard_rows(c.V, R, r);
     if (!full_scan && !(R > 1 && n_e_rows == local_rows))
@@ -472,10 +478,12 @@ static evospec_status build_impl(evospec_ctx* ctx, const void* E, int64_t n_e_ro
         StageTimer t(ctx, EVOSPEC_STAGE_SCAN, st);
         // the scan zeroes the next selection's histogram scratch and count
         if (ctx->hist_dirty) CUDA_TRY(cudaMemsetAsync(ctx->hist12, 0, kHistBins * sizeof(uint32_t), st));
+        // a4's static bitmap: an input-only kernel the scan overlaps (PDL)
+        launch_static_bits(static_ids, n_static, c.V, c.debug_checks, ctx->sbits, ctx->flags, st);
         launch_sem_scan(E, c.w_dtype, n_e_rows, c.d, q, c.h_dtype, ctx->s64, ctx->key32, ctx->hist12, st, ctx->hist,
                         12 * kHistBins, ctx->cand_count, true);
         ctx->hist_dirty = true;
-        ctx->launches += 1;
+        ctx->launches += 2;
     } else {
         // this shard's exact local top-N, all-gathered (N (s, id) pairs per rank)
         evospec_status ls = local_candidates_impl(ctx, E, n_e_rows, q, N, ctx->loc_s, ctx->loc_id, st);
@@ -493,7 +501,8 @@ static evospec_status build_impl(evospec_ctx* ctx, const void* E, int64_t n_e_ro
     LAUNCH_CHECK("sem_scan");
     return union_from_candidates(ctx, full_scan ? nullptr : ctx->gat_s, full_scan ? nullptr : ctx->gat_id,
                                  (int64_t)N * R, static_ids, n_static, seeds, n_seed, row_ptr, col, ctx_ids, n_ctx, p,
-                                 out_ids, out_n, out_local_ids, out_local_n, st, dyn_base, wait_before_union);
+                                 out_ids, out_n, out_local_ids, out_local_n, st, dyn_base, wait_before_union,
+                                 full_scan);
 }
 
 // The global candidate superset of the top-N and the formation / union (a2-a4).
@@ -506,10 +515,15 @@ static evospec_status union_from_candidates(evospec_ctx* ctx, const double* cand
                                             const int32_t* col, const int32_t* ctx_ids, int32_t n_ctx,
                                             const evospec_build_params* p, int32_t* out_ids, int32_t* out_n,
                                             int32_t* out_local_ids, int32_t* out_local_n, cudaStream_t st,
-                                            const int32_t* dyn_base, cudaEvent_t wait_before_union) {
+                                            const int32_t* dyn_base, cudaEvent_t wait_before_union,
+                                            bool sbits_ready) {
     const evospec_config& c = ctx->cfg;
     const int R = c.n_shards, r = c.shard_rank;
     const int N = p->n_sem;
+    if (!sbits_ready) {   // (the full-scan build launches it ahead of the scan instead)
+        launch_static_bits(static_ids, n_static, c.V, c.debug_checks, ctx->sbits, ctx->flags, st);
+        ctx->launches += 1;
+    }
     StageTimer t_sel(ctx, EVOSPEC_STAGE_SELECT, st);
     if (!cand_s) {
         ctx->launches += 1;
@@ -542,7 +556,7 @@ static evospec_status union_from_candidates(evospec_ctx* ctx, const double* cand
                  N, row_ptr, col, use_ctx ? ctx->ctx_sel : nullptr, ctx->ctx_n, p->n_graph_sem_seeds, p->per_seed,
                  p->n_dyn, R, r, out_ids, out_n, out_local_ids, out_local_n, ctx->sem_ids, ctx->sem_n,
                  c.debug_checks, ctx->flags, st, union_trace(ctx, st), dyn_base, ctx->hist12,
-                 emit ? ctx->ubits : nullptr);
+                 emit ? ctx->ubits : nullptr, ctx->sbits);
     LAUNCH_CHECK("union");
     ctx->hist_dirty = false;
     if (emit) {   // single shard: the sorted ids from the bitmap by a multi-CTA kernel

@@ -23,6 +23,7 @@ constexpr int kFlagSelectOverflow = 0x4;
 constexpr int kFlagBudget = 0x8;
 
 // ---- semantic (sem.cu)
+void set_step_trace(long long* p);   // EVOSPEC_TRACE stamps of the scan / candidate kernels
 void launch_sem_scan(const void* E, int e_dtype, int64_t n_rows, int d, const void* q, int q_dtype,
                      double* s64, uint32_t* key32, uint32_t* hist12, cudaStream_t st, uint32_t* zero_w = nullptr,
                      int n_zero_w = 0, int* zero_c = nullptr, bool hist_zero = false);
@@ -34,6 +35,8 @@ cudaError_t launch_topn_cand(const double* s64, const int32_t* ids, int64_t n, i
 void launch_ctx_select(const int32_t* ctx, int n_ctx, int V, int min_count, int n_max,
                        int32_t* out, int* out_n, int* flags, cudaStream_t st);
 int union_cand_cap(int V, int per_seed);
+void launch_static_bits(const int32_t* static_ids, int n_static, int V, int debug, uint32_t* sbits, int* flags,
+                        cudaStream_t st);
 void launch_union(int V, const int32_t* static_ids, int n_static, const int32_t* seeds, int n_seed,
                   const double* cand_s, const int32_t* cand_id, const int* n_cand_dev, int cap, int n_sem,
                   const int32_t* row_ptr, const int32_t* col,
@@ -42,7 +45,7 @@ void launch_union(int V, const int32_t* static_ids, int n_static, const int32_t*
                   int32_t* out_ids, int32_t* out_n, int32_t* out_local, int32_t* out_local_n,
                   int32_t* sem_out, int* sem_out_n, int debug, int* flags, cudaStream_t st,
                   long long* trace = nullptr, const int32_t* dyn_base = nullptr,
-                  uint32_t* clear_hist = nullptr, uint32_t* emit_bits = nullptr);
+                  uint32_t* clear_hist = nullptr, uint32_t* emit_bits = nullptr, uint32_t* sbits = nullptr);
 void launch_union_emit(const uint32_t* bits, int V, int32_t* out_ids, int32_t* out_n, int32_t* out_local,
                        int32_t* out_local_n, int budget_max, int* flags, cudaStream_t st);
 

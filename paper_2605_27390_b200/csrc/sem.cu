@@ -144,6 +144,16 @@ sem_scan_kernel(const void* __restrict__ E, int64_t n_rows, int d,
         if (hist_sm[i]) atomicAdd(&hist12[i], hist_sm[i]);
 }
 
+// per-kernel globaltimer stamps of the build (EVOSPEC_TRACE; profiling aid):
+// scan CTA b start / end at [2b], [2b + 1]; the candidate kernel's CTA 0 at [2 * 148], [+1]
+static long long* s_step_trace = nullptr;
+void set_step_trace(long long* p) { s_step_trace = p; }
+ES_DEV long long step_gtime() {
+    long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
 // ---------------------------------------------------------------- scan (TMA ring)
 // bf16 E, d % 256 == 0, d <= 4096: the same exact fp64 scores as above, with E
 // streamed through shared memory by the bulk-copy engine instead of per-lane
@@ -160,7 +170,8 @@ sem_scan_kernel(const void* __restrict__ E, int64_t n_rows, int d,
 //   histogram, then frees the stage (the others free it right after their
 //   partials are written).
 constexpr int kScanConsumers = 16;
-constexpr int kScanRS = 8;          // rows per ring stage (8: one CTA per SM; 4 + two CTAs measured slower)
+constexpr int kScanRS = 8;          // rows per ring stage (8: one CTA per SM; measured r2: 4 rows x 6 stages
+                                    // 240 us, 2 x 12 358 us vs 195 us -- the per-stage work dominates)
 constexpr int kScanPf = 0;          // stages of L2 prefetch ahead of the ring (measured slower: off)
 
 ES_DEV uint32_t s_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -189,7 +200,12 @@ template <int kScanRowsPerStage, int kScanStages>
 __global__ void __launch_bounds__((kScanConsumers + 1) * 32, 1)
 sem_scan_tma_kernel(const uint16_t* __restrict__ E, int64_t n_rows, int d, const void* __restrict__ q, int q_dtype,
                     uint32_t* __restrict__ hist12, double* __restrict__ s64, uint32_t* __restrict__ key32, int pf,
-                    int il, uint32_t* __restrict__ zero_w, int n_zero_w, int* __restrict__ zero_c) {
+                    int il, uint32_t* __restrict__ zero_w, int n_zero_w, int* __restrict__ zero_c,
+                    long long* __restrict__ tr) {
+    if (tr && threadIdx.x == 0) tr[2 * blockIdx.x] = step_gtime();
+    // launched behind static_bits_kernel (PDL): overlaps it, and waits for it before
+    // completing (below), so kernels after the scan see the static bitmap
+    pdl_trigger();
     // zero the candidate selection's scratch for the next kernel (saves two memsets)
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_zero_w; i += gridDim.x * blockDim.x) zero_w[i] = 0;
     if (zero_c && blockIdx.x == 0 && threadIdx.x == 0) *zero_c = 0;
@@ -358,6 +374,8 @@ sem_scan_tma_kernel(const uint16_t* __restrict__ E, int64_t n_rows, int d, const
     asm volatile("bar.sync 1, %0;" ::"r"(n_slab * 32) : "memory");
     for (int i = threadIdx.x; i < kHistBins; i += n_slab * 32)
         if (hist_sm[i]) atomicAdd(&hist12[i], hist_sm[i]);
+    if (tr && threadIdx.x == 0) tr[2 * blockIdx.x + 1] = step_gtime();
+    if (threadIdx.x == 0) pdl_wait();
 }
 
 void launch_sem_scan(const void* E, int e_dtype, int64_t n_rows, int d, const void* q, int q_dtype,
@@ -387,16 +405,18 @@ void launch_sem_scan(const void* E, int e_dtype, int64_t n_rows, int d, const vo
                 cudaFuncSetAttribute(sem_scan_tma_kernel<RS, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
                 attr2 = sm;
             }
-            sem_scan_tma_kernel<RS, 2><<<kNumSMs, (kScanConsumers + 1) * 32, sm, st>>>(
-                (const uint16_t*)E, n_rows, d, q, q_dtype, hist12, s64, key32, kScanPf, 1, zero_w, n_zero_w, zero_c);
+            launch_pdl(sem_scan_tma_kernel<RS, 2>, dim3(kNumSMs), dim3((kScanConsumers + 1) * 32), sm, st,
+                       (const uint16_t*)E, n_rows, d, q, q_dtype, hist12, s64, key32, kScanPf, 1, zero_w, n_zero_w,
+                       zero_c, s_step_trace);
             return;
         }
         if (attr < sm) {
             cudaFuncSetAttribute(sem_scan_tma_kernel<RS, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
             attr = sm;
         }
-        sem_scan_tma_kernel<RS, NS><<<kNumSMs, (kScanConsumers + 1) * 32, sm, st>>>(
-            (const uint16_t*)E, n_rows, d, q, q_dtype, hist12, s64, key32, kScanPf, 1, zero_w, n_zero_w, zero_c);
+        launch_pdl(sem_scan_tma_kernel<RS, NS>, dim3(kNumSMs), dim3((kScanConsumers + 1) * 32), sm, st,
+                   (const uint16_t*)E, n_rows, d, q, q_dtype, hist12, s64, key32, kScanPf, 1, zero_w, n_zero_w, zero_c,
+                   s_step_trace);
     } else if (e_dtype == 0) {
         cudaFuncSetAttribute(sem_scan_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         sem_scan_kernel<0><<<kNumSMs, kScanWarps * 32, smem, st>>>(E, n_rows, d, q, q_dtype, hist12, s64, key32,
@@ -456,9 +476,11 @@ __global__ void __launch_bounds__(kSelThreads, 1)
 topn_cand_kernel(const double* __restrict__ s64, const int32_t* __restrict__ ids, int64_t n,
                  int id_mul, int id_add, int N, int cap, const uint32_t* __restrict__ hist_pre,
                  uint32_t* __restrict__ hist_g, int* __restrict__ out_count, double* __restrict__ out_s,
-                 int32_t* __restrict__ out_id) {
+                 int32_t* __restrict__ out_id, long long* __restrict__ tr) {
     cg::grid_group grid = cg::this_grid();
-    pdl_trigger();   // the union kernel may start its input-only prologue (static bitmap) now
+    pdl_trigger();   // the union kernel may be scheduled now (it waits for this grid before reading)
+    pdl_wait();      // the scores / histogram of the scan (launched behind it with PDL)
+    if (tr && blockIdx.x == 0 && threadIdx.x == 0) tr[2 * kNumSMs] = step_gtime();
     __shared__ uint32_t hist[kHistBins];
     __shared__ uint32_t warp_sum_s[kSelThreads / 32];
     __shared__ SelState st;
@@ -564,6 +586,7 @@ topn_cand_kernel(const double* __restrict__ s64, const int32_t* __restrict__ ids
         const int o = base + __popc(m & ((1u << lane) - 1u));
         if (sel && o < cap) { out_s[o] = s; out_id[o] = id; }
     }
+    if (tr && blockIdx.x == 0 && threadIdx.x == 0) tr[2 * kNumSMs + 1] = step_gtime();
 }
 
 cudaError_t launch_topn_cand(const double* s64, const int32_t* ids, int64_t n, int id_mul, int id_add,
@@ -576,9 +599,10 @@ cudaError_t launch_topn_cand(const double* s64, const int32_t* ids, int64_t n, i
     int grid = kNumSMs;
     if (n < (int64_t)grid * 64) grid = (int)((n + 63) / 64);
     if (grid < 1) grid = 1;
-    void* args[] = {(void*)&s64, (void*)&ids, (void*)&n, (void*)&id_mul, (void*)&id_add, (void*)&N, (void*)&cap,
-                    (void*)&hist_pre, (void*)&hist_g, (void*)&out_count, (void*)&out_s, (void*)&out_id};
-    return cudaLaunchCooperativeKernel((void*)topn_cand_kernel, grid, kSelThreads, args, 0, st);
+    // cooperative (the rare multi-pass path syncs the grid) and programmatic: its launch
+    // overlaps the scan's tail, and the union behind it may be scheduled early
+    return launch_pdl_coop(topn_cand_kernel, dim3(grid), dim3(kSelThreads), 0, st, s64, ids, n, id_mul, id_add, N,
+                           cap, hist_pre, hist_g, out_count, out_s, out_id, s_step_trace);
 }
 
 }  // namespace es

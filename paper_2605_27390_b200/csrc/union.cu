@@ -491,7 +491,7 @@ union_kernel(int V, const int32_t* __restrict__ static_ids, int n_static,
              int32_t* __restrict__ out_local, int32_t* __restrict__ out_local_n,
              int32_t* __restrict__ sem_out, int* __restrict__ sem_out_n, int debug, int* flags,
              long long* __restrict__ trace, const int32_t* __restrict__ dyn_base, uint32_t* __restrict__ clear_hist,
-             uint32_t* __restrict__ emit_bits) {
+             uint32_t* __restrict__ emit_bits, uint32_t* __restrict__ sbits) {
     extern __shared__ __align__(16) unsigned char u_sm[];
     const int nwords = (V + 31) / 32;
     uint64_t* ck = (uint64_t*)u_sm;                          // [cap]
@@ -510,30 +510,8 @@ union_kernel(int V, const int32_t* __restrict__ static_ids, int n_static,
 
     const int tid = threadIdx.x, lane = lane_id(), T = blockDim.x;
     pdl_trigger();
-    // 1. static members -- an input, not the predecessor's output: built before
-    //    griddepcontrol.wait, overlapping the candidate selection (8 loads in flight)
     if (trace) { if (threadIdx.x == 0) { long long t_; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); trace[0] = t_; } }
-    for (int w = tid; w < nwords; w += T) bits[w] = 0;
     if (tid == 0) { bad_s = 0; sem_n_s = 0; }
-    __syncthreads();
-    for (int i0 = 0; i0 < n_static; i0 += 8 * T) {
-        int32_t v[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            const int i = i0 + u * T + tid;
-            v[u] = i < n_static ? __ldg(&static_ids[i]) : -1;
-        }
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            const int i = i0 + u * T + tid;
-            if (i >= n_static) continue;
-            if (v[u] < 0 || v[u] >= V) { bad_s = 1; continue; }
-            if (debug && i > 0 && static_ids[i - 1] >= v[u]) bad_s = 1;
-            atomicOr(&bits[v[u] >> 5], 1u << (v[u] & 31));
-        }
-    }
-    // formation starts with the seeds (C6): they and the static set are
-    // inputs, so warp 0 walks them before the wait too
     const unsigned lt_mask = (1u << lane) - 1u;
     auto walk = [&](const int32_t* src, int len, int taken) -> int {
         for (int base = 0; base < len && taken < n_dyn; base += 32) {
@@ -553,12 +531,22 @@ union_kernel(int V, const int32_t* __restrict__ static_ids, int n_static,
         }
         return taken;
     };
+    pdl_wait();
+    // 1. static members: the bitmap static_bits_kernel built ahead of the scan (an
+    //    earlier kernel on the stream: complete once the predecessor is)
+    {
+        const uint4* s4 = (const uint4*)sbits;
+        uint4* b4 = (uint4*)bits;
+        const int n4 = nwords >> 2;
+        for (int w = tid; w < n4; w += T) b4[w] = __ldcg(&s4[w]);
+        for (int w = (n4 << 2) + tid; w < nwords; w += T) bits[w] = __ldcg(&sbits[w]);
+    }
     __syncthreads();
+    // formation starts with the seeds (C6): warp 0 walks them
     if (warp_id() == 0) {
         const int t = walk(seeds, n_seed, 0);
         if (lane == 0) taken_s = t;
     }
-    pdl_wait();
     // the selection has consumed the scan's histogram: leave it zero for the next build
     if (clear_hist)
         for (int i = tid; i < kHistBins; i += T) clear_hist[i] = 0;
@@ -722,14 +710,13 @@ union_kernel(int V, const int32_t* __restrict__ static_ids, int n_static,
     // (out_n = offsets + b + 1 for sequence b, dyn_base = offsets + b)
     int base_off = 0;
     if (dyn_base) {
-        for (int i = tid; i < n_static; i += T) {
-            const int32_t v = static_ids[i];
-            if (v >= 0 && v < V) atomicAnd(&bits[v >> 5], ~(1u << (v & 31)));
-        }
+        for (int w = tid; w < nwords; w += T) bits[w] &= ~__ldcg(&sbits[w]);
         base_off = *dyn_base;
         out_ids += base_off;
-        __syncthreads();
     }
+    // the static bitmap is consumed: leave it zero for the next build's static_bits_kernel
+    for (int w = tid; w < nwords; w += T) sbits[w] = 0;
+    __syncthreads();
     if (emit_bits) {
         // single shard, full output: the sorted ids are written by the multi-CTA
         // emit kernel from the bitmap (union_emit_kernel)
@@ -865,13 +852,38 @@ void launch_union(int V, const int32_t* static_ids, int n_static, const int32_t*
                   int n_graph_sem_seeds, int per_seed, int n_dyn, int R, int r,
                   int32_t* out_ids, int32_t* out_n, int32_t* out_local, int32_t* out_local_n,
                   int32_t* sem_out, int* sem_out_n, int debug, int* flags, cudaStream_t st, long long* trace,
-                  const int32_t* dyn_base, uint32_t* clear_hist, uint32_t* emit_bits) {
+                  const int32_t* dyn_base, uint32_t* clear_hist, uint32_t* emit_bits, uint32_t* sbits) {
     const size_t smem = (size_t)cap * 13 + union_fixed_bytes(V, per_seed) + 16;
     cudaFuncSetAttribute(union_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     launch_pdl(union_kernel, dim3(1), dim3(kUnionThreads), smem, st, V, static_ids, n_static, seeds, n_seed, cand_s, cand_id, n_cand_dev,
                                                   cap, n_sem, row_ptr, col, ctx_sel, n_ctx_sel_dev, n_graph_sem_seeds,
                                                   per_seed, n_dyn, R, r, out_ids, out_n, out_local, out_local_n,
-                                                  sem_out, sem_out_n, debug, flags, trace, dyn_base, clear_hist, emit_bits);
+                                                  sem_out, sem_out_n, debug, flags, trace, dyn_base, clear_hist, emit_bits,
+                                                  sbits);
+}
+
+// a4 static core -> the V-bit membership bitmap the union starts from (sbits: zero
+// on entry -- the union kernel zeroes it after use). Launched ahead of the scan,
+// which overlaps it (PDL) and waits for it before completing. Range-checked (and,
+// with debug, order-checked) like the union's own inputs.
+__global__ void __launch_bounds__(256)
+static_bits_kernel(const int32_t* __restrict__ static_ids, int n_static, int V, int debug,
+                   uint32_t* __restrict__ sbits, int* __restrict__ flags) {
+    pdl_trigger();
+    bool bad = false;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_static; i += gridDim.x * blockDim.x) {
+        const int32_t v = __ldg(&static_ids[i]);
+        if (v < 0 || v >= V) { bad = true; continue; }
+        if (debug && i > 0 && __ldg(&static_ids[i - 1]) >= v) bad = true;
+        atomicOr(&sbits[v >> 5], 1u << (v & 31));
+    }
+    if (bad && flags) atomicOr(flags, kFlagBadIds);
+}
+
+void launch_static_bits(const int32_t* static_ids, int n_static, int V, int debug, uint32_t* sbits, int* flags,
+                        cudaStream_t st) {
+    const int grid = std::max(1, std::min(32, (n_static + 1023) / 1024));
+    static_bits_kernel<<<grid, 256, 0, st>>>(static_ids, n_static, V, debug, sbits, flags);
 }
 
 }  // namespace es

@@ -1,6 +1,7 @@
-"""Timeline of one draft step (profiling aid): union stamps and LM-head per-CTA stamps
-(globaltimer, us from the union's start) -- shows how much of the LM head overlaps the
-union in the two-list mode (EVOSPEC_OVERLAP=1)."""
+"""Timeline of one llama draft step (profiling aid): globaltimer stamps of the
+scan CTAs, the candidate kernel, the union phases, the LM-head CTAs and the
+finalize rows, on one clock, relative to the first scan CTA's start (us).
+EVOSPEC_TRACE=1 (the stamps' own cost included)."""
 import os
 import sys
 
@@ -9,36 +10,52 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import torch
 
+import bench
 import paper_2605_27390_b200 as es
-import synth
 
-c = synth.CONFIGS["llama"]
-V, d = c["V"], c["d"]
-W = torch.from_numpy(synth.matrix(0, V, d, 0.02, "bf16").view(np.int16)).view(torch.bfloat16).cuda()
-H = torch.from_numpy(synth.matrix(1, 60, d, 1.0, "bf16").view(np.int16)).view(torch.bfloat16).cuda()
-q = torch.from_numpy(synth.matrix(2, 1, d, 1.0, "bf16")[0].view(np.int16)).view(torch.bfloat16).cuda()
-static = torch.from_numpy(synth.static_ids(3, V, c["n_static"])).cuda()
-rp, col, _ = synth.csr_graph(4, V, c["avg_deg"])
-seeds = torch.from_numpy(synth.seed_ids(5, V, 10)).cuda()
-ctx = es.Context(V=V, d=d, w_dtype=torch.bfloat16, h_dtype=torch.bfloat16, max_subset=V, max_rows=60, max_k=10,
-                 max_sem=8192)
-ctx.prepare_weights(W)
-kw = dict(E=W, W_local=W, static_ids=static, csr_row_ptr=torch.from_numpy(rp).cuda(),
-          csr_col=torch.from_numpy(col).cuda(), k=10, n_sem=8192, n_dyn=4096)
-for _ in range(4):
-    ctx.draft_step(q=q, H=H, seeds=seeds, **kw)
+c, W, H, q, static, row_ptr, col, seeds = bench.make_workload()
+bf = torch.bfloat16
+T = lambda a: (torch.from_numpy(a.view(np.int16)).view(bf) if a.dtype == np.uint16 else
+               torch.from_numpy(np.ascontiguousarray(a))).cuda()
+Wd, Hd, qd, sd, rpd, cold, seedd = T(W), T(H), T(q), T(static), T(row_ptr), T(col), T(seeds)
+del W
+n_h, k = c["n_h"], c["k"]
+ctx = es.Context(V=c["V"], d=c["d"], w_dtype=bf, h_dtype=bf, max_subset=c["V"], max_rows=n_h, max_k=k,
+                 max_sem=c["n_sem"], max_seeds=32)
+ctx.prepare_weights(Wd)
+kw = dict(E=Wd, W_local=Wd, static_ids=sd, csr_row_ptr=rpd, csr_col=cold, k=k, n_sem=c["n_sem"], n_dyn=c["n_dyn"],
+          n_graph_sem_seeds=c["n_graph_sem_seeds"], per_seed=c["per_seed"])
+out = (torch.empty((n_h, k), dtype=torch.int32, device="cuda"), torch.empty((n_h, k), device="cuda"),
+       torch.empty(n_h, device="cuda"), torch.empty((n_h, k), device="cuda"))
+for it in range(int(os.environ.get("STEPS", "6"))):
+    ctx.draft_step(q=qd, H=Hd, seeds=seedd, out=out, **kw)
 torch.cuda.synchronize()
-tr = ctx.read_trace(2 * 148 * 8 + 17).astype(np.float64)
-lm = tr[:148 * 8].reshape(148, 8)
-un = tr[2 * 148 * 8:2 * 148 * 8 + 7]
-t0 = un[0]
-rel = lambda x: round((x - t0) / 1e3, 1)
-print("union: start 0, loaded", rel(un[1]), "sel", rel(un[2]), "end", rel(un[6]))
-ok = lm[:, 0] > 0
-for j, n in enumerate(["start", "prod_done", "mma_done", "t0_ready", "t0_fold", "t1_ready", "t1_fold", "end"]):
-    col_ = lm[ok, j]
-    col_ = col_[col_ > 0]
-    if col_.size:
-        print(f"  lmh {n:9s} min {rel(col_.min()):7.1f} med {rel(np.median(col_)):7.1f} max {rel(col_.max()):7.1f}")
-fin = tr[148 * 8:148 * 8 + 60 * 8].reshape(60, 8)
-print("  finalize start", rel(fin[:, 0].min()), "end", rel(fin[:, 6].max()))
+N = 148
+tr = ctx.read_trace(2 * N * 8 + 112 + 2 * N + 2).astype(np.float64)
+lmh = tr[:N * 8].reshape(N, 8)
+fin = tr[N * 8:N * 8 + n_h * 8].reshape(n_h, 8)
+uni = tr[2 * N * 8:2 * N * 8 + 7]
+scan = tr[2 * N * 8 + 112:2 * N * 8 + 112 + 2 * N].reshape(N, 2)
+cand = tr[2 * N * 8 + 112 + 2 * N:2 * N * 8 + 112 + 2 * N + 2]
+t0 = scan[:, 0].min()
+rel = lambda x: (x - t0) / 1e3
+
+
+def dist(name, col):
+    col = col[col > 0]
+    if col.size:
+        r = rel(col)
+        print(f"  {name:22s} min {r.min():7.1f}  med {np.median(r):7.1f}  max {r.max():7.1f}")
+
+
+print("draft step timeline (us from the first scan CTA start)")
+dist("scan start", scan[:, 0])
+dist("scan end", scan[:, 1])
+dist("cand kernel start", cand[:1])
+dist("cand kernel end", cand[1:])
+for i, nm in enumerate(["start", "loaded", "S_sem", "gs", "G/graph", "formation", "end"]):
+    dist("union " + nm, uni[i:i + 1])
+for i, nm in enumerate(["start", "prod_done", "mma_done", "t0_ready", "t0_fold", "t1_ready", "t1_fold", "end"]):
+    dist("lmh " + nm, lmh[:, i])
+for i, nm in enumerate(["start", "hnorm", "B1", "filter", "runs", "rescore", "end"]):
+    dist("fin " + nm, fin[:, i])
