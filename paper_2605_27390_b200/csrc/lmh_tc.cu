@@ -61,8 +61,11 @@ struct TcParams {
     int last_tile;   // rows of a CTA's short last tile (ranges longer than one tile)
     int dyn_tile;    // two-list mode: rows per second-list tile (EVOSPEC_DYN_TILE)
     int dyn_stride;  // two-list mode: CTA rank stride of the second-list round robin
+    int dyn_share;   // two-list mode: first-list share (16ths) of the CTAs expected to take a second-list tile
     size_t off_b, off_epi, off_bar, off_rows;  // smem carve offsets
 };
+
+ES_DEV int dyn_rank_of(int b, int stride, int grid) { return (int)(((long long)b * stride) % grid); }
 
 __global__ void __launch_bounds__(kTcWarps * 32, 1)
 lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ CUtensorMap tmap_h,
@@ -125,8 +128,18 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
     if (!a.list2) pdl_wait();
     int p0, p1;
     if (a.list2) {
-        p0 = (int)((long long)a.n1 * blockIdx.x / gridDim.x);
-        p1 = (int)((long long)a.n1 * (blockIdx.x + 1) / gridDim.x);
+        // the CTAs that will take a second-list tile (ranks < nd, for the list's capacity)
+        // stream a smaller share of the first list: their second-list tile starts when
+        // the union ends and costs a full K loop, so they should reach it earlier
+        const int nd = tp.dyn_tile > 0 ? min((int)gridDim.x, (a.n_list2_max + tp.dyn_tile - 1) / tp.dyn_tile) : 0;
+        const long long wt = (long long)nd * tp.dyn_share + 16LL * ((int)gridDim.x - nd);
+        auto pre = [&](int b) -> long long {
+            return (long long)min(b, nd) * tp.dyn_share + 16LL * max(0, b - nd);
+        };
+        const int rb = dyn_rank_of(blockIdx.x, tp.dyn_stride, gridDim.x);
+        // ranks, not block ids, order the shares (rank r covers [pre(r), pre(r + 1)))
+        p0 = (int)((long long)a.n1 * pre(rb) / wt);
+        p1 = (int)((long long)a.n1 * pre(rb + 1) / wt);
     } else if (seg_b >= 0) {
         // the CTAs of a segment split its positions identically for every segment
         // with the same range, so concurrent row groups share W rows through L2
@@ -160,7 +173,7 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
     // sliver of it on every CTA (a short tile still pays all d / 64 stages of H).
     int nt2 = a.list2 ? -1 : 0, n2 = 0;
     // the CTA's rank in the second-list round robin
-    const int dyn_rank = (int)(((long long)blockIdx.x * tp.dyn_stride) % gridDim.x);
+    const int dyn_rank = dyn_rank_of(blockIdx.x, tp.dyn_stride, gridDim.x);
     auto ensure2 = [&]() {
         if (nt2 >= 0) return;
         pdl_wait();
@@ -387,6 +400,10 @@ cudaError_t launch_lmh_tc(const LmhArgs& a, cudaStream_t st) {
     tp.last_tile = kLastTile;
     tp.dyn_tile = kTileM;
     tp.dyn_stride = 1;   // (scattering the second-list CTAs over the chip measured equal)
+    // half a share (llama draft step: those CTAs stream one first-list tile, the others
+    // two; measured r2 with the step timeline: 16/16 277.5 us, 12 282.0, 8 264.8, 6 286.7,
+    // 4 286.4 -- below 8 the other CTAs' ranges grow a third tile)
+    tp.dyn_share = 8;
     if (const char* e = getenv("EVOSPEC_DYN_TILE")) tp.dyn_tile = atoi(e) <= 0 ? 0 : std::max(16, std::min(kTileM, atoi(e)));
     uint32_t cols = 2 * tp.n_pad, c = 32;
     while (c < cols) c <<= 1;
