@@ -105,6 +105,7 @@ struct evospec_ctx {
     bool hist_dirty = false;      // a build stopped between its scan and its union: clear first
     uint32_t* ubits = nullptr;    // [V/32] union bitmap handed to the emit kernel
     uint32_t* sbits = nullptr;    // [V/32] static-core bitmap (static_bits_kernel -> union; zero between builds)
+    int* scan_sched = nullptr;    // [2] the TMA scan's stage counter and exit count (zero between launches)
     int32_t* zero_i = nullptr;    // a device 0 (dyn-only union output at offset 0)
     // N1 OOV event (evospec_oov_event_begin / _end): the event's formation runs on a
     // side stream while the caller keeps drafting on the current subset
@@ -242,7 +243,7 @@ evospec_status evospec_destroy(evospec_ctx* ctx) {
                     ctx->flags, ctx->wmax, ctx->g_ids, ctx->g_vals, ctx->g_m, ctx->g_s, ctx->st_q, ctx->st_H,
                     ctx->st_seeds, ctx->st_ctx, ctx->st_S, ctx->st_nS, ctx->st_local, ctx->st_nlocal,
                     ctx->st_tids, ctx->st_tvals, ctx->st_m, ctx->st_s, ctx->st_oids, ctx->st_ovals,
-                    ctx->st_lse, ctx->st_probs, ctx->ubits, ctx->sbits, ctx->rg_ids, ctx->rg_vals, ctx->rg_m, ctx->rg_s, ctx->rg_seg, ctx->rg_segcta, ctx->ver_acc, ctx->ver_tok, ctx->zero_i};
+                    ctx->st_lse, ctx->st_probs, ctx->ubits, ctx->sbits, ctx->scan_sched, ctx->rg_ids, ctx->rg_vals, ctx->rg_m, ctx->rg_s, ctx->rg_seg, ctx->rg_segcta, ctx->ver_acc, ctx->ver_tok, ctx->zero_i};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (ctx->comm && nccl().loaded) nccl().CommDestroy(ctx->comm);
@@ -301,6 +302,7 @@ evospec_status evospec_create(evospec_ctx** out, const evospec_config* cfg, int 
     }
     const size_t cap = (size_t)x->cand_cap;
     A(dalloc(&x->s64, V)); A(dalloc(&x->key32, V)); A(dalloc(&x->hist12, kHistBins)); A(dalloc(&x->ubits, (V + 31) / 32)); A(cudaMemset(x->hist12, 0, kHistBins * sizeof(uint32_t)));
+    A(dalloc(&x->scan_sched, 2)); A(cudaMemset(x->scan_sched, 0, 2 * sizeof(int)));
     A(dalloc(&x->sbits, (V + 31) / 32 + 4)); A(cudaMemset(x->sbits, 0, ((V + 31) / 32 + 4) * sizeof(uint32_t)));
     A(dalloc(&x->hist, 12 * kHistBins));
     A(dalloc(&x->ver_acc, kMaxChain + 1)); A(dalloc(&x->ver_tok, kMaxChain + 1));
@@ -418,7 +420,7 @@ static evospec_status local_candidates_impl(evospec_ctx* ctx, const void* E, int
     StageTimer t(ctx, EVOSPEC_STAGE_SCAN, st);
     if (ctx->hist_dirty) CUDA_TRY(cudaMemsetAsync(ctx->hist12, 0, kHistBins * sizeof(uint32_t), st));
     launch_sem_scan(E, c.w_dtype, n_e_rows, c.d, q, c.h_dtype, ctx->s64, ctx->key32, ctx->hist12, st, ctx->hist,
-                    12 * kHistBins, ctx->loc_count, true);
+                    12 * kHistBins, ctx->loc_count, true, ctx->scan_sched);
     ctx->hist_dirty = true;
     ctx->launches += 2;
     LAUNCH_CHECK("sem_scan");
@@ -481,7 +483,7 @@ static evospec_status build_impl(evospec_ctx* ctx, const void* E, int64_t n_e_ro
         // a4's static bitmap: an input-only kernel the scan overlaps (PDL)
         launch_static_bits(static_ids, n_static, c.V, c.debug_checks, ctx->sbits, ctx->flags, st);
         launch_sem_scan(E, c.w_dtype, n_e_rows, c.d, q, c.h_dtype, ctx->s64, ctx->key32, ctx->hist12, st, ctx->hist,
-                        12 * kHistBins, ctx->cand_count, true);
+                        12 * kHistBins, ctx->cand_count, true, ctx->scan_sched);
         ctx->hist_dirty = true;
         ctx->launches += 2;
     } else {

@@ -26,7 +26,8 @@ constexpr int kFlagBudget = 0x8;
 void set_step_trace(long long* p);   // EVOSPEC_TRACE stamps of the scan / candidate kernels
 void launch_sem_scan(const void* E, int e_dtype, int64_t n_rows, int d, const void* q, int q_dtype,
                      double* s64, uint32_t* key32, uint32_t* hist12, cudaStream_t st, uint32_t* zero_w = nullptr,
-                     int n_zero_w = 0, int* zero_c = nullptr, bool hist_zero = false);
+                     int n_zero_w = 0, int* zero_c = nullptr, bool hist_zero = false,
+                     int* sched = nullptr);   // sched: 2 ints, zero (the TMA scan's stage counter)
 cudaError_t launch_topn_cand(const double* s64, const int32_t* ids, int64_t n, int id_mul, int id_add,
                              int N, int cap, const uint32_t* hist_pre, uint32_t* hist_g, int* out_count,
                              double* out_s, int32_t* out_id, cudaStream_t st, bool prezeroed = false);

@@ -172,7 +172,6 @@ ES_DEV long long step_gtime() {
 constexpr int kScanConsumers = 16;
 constexpr int kScanRS = 8;          // rows per ring stage (8: one CTA per SM; measured r2: 4 rows x 6 stages
                                     // 240 us, 2 x 12 358 us vs 195 us -- the per-stage work dominates)
-constexpr int kScanPf = 0;          // stages of L2 prefetch ahead of the ring (measured slower: off)
 
 ES_DEV uint32_t s_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 ES_DEV void s_mbar_init(uint64_t* b, uint32_t n) {
@@ -199,8 +198,8 @@ ES_DEV void s_bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar
 template <int kScanRowsPerStage, int kScanStages>
 __global__ void __launch_bounds__((kScanConsumers + 1) * 32, 1)
 sem_scan_tma_kernel(const uint16_t* __restrict__ E, int64_t n_rows, int d, const void* __restrict__ q, int q_dtype,
-                    uint32_t* __restrict__ hist12, double* __restrict__ s64, uint32_t* __restrict__ key32, int pf,
-                    int il, uint32_t* __restrict__ zero_w, int n_zero_w, int* __restrict__ zero_c,
+                    uint32_t* __restrict__ hist12, double* __restrict__ s64, uint32_t* __restrict__ key32,
+                    int* __restrict__ sched, uint32_t* __restrict__ zero_w, int n_zero_w, int* __restrict__ zero_c,
                     long long* __restrict__ tr) {
     if (tr && threadIdx.x == 0) tr[2 * blockIdx.x] = step_gtime();
     // launched behind static_bits_kernel (PDL): overlaps it, and waits for it before
@@ -218,18 +217,12 @@ sem_scan_tma_kernel(const uint16_t* __restrict__ E, int64_t n_rows, int d, const
     uint64_t* full = (uint64_t*)(red + 2 * kScanStages * kScanConsumers * kScanRowsPerStage);
     uint64_t* empty = full + kScanStages;
     uint64_t* part_bar = empty + kScanStages;                                // [2S]
+    int64_t* srow = (int64_t*)(part_bar + 2 * kScanStages);                  // [S] first row of the slot's stage
     const int warp = warp_id(), lane = lane_id();
     const int n_slab = d / 256;                                              // <= 16
-    // stage i of this CTA: rows [8 g, 8 g + 8) of E with g = i * grid + cta (il = 1:
-    // all SMs sweep adjacent rows together), or a contiguous 1/grid block (il = 0)
-    const int64_t n_groups = (n_rows + kScanRowsPerStage - 1) / kScanRowsPerStage;
-    const int64_t r0 = n_rows * blockIdx.x / gridDim.x, r1 = n_rows * (blockIdx.x + 1) / gridDim.x;
-    const int n_stage = il ? (int)((n_groups - blockIdx.x + gridDim.x - 1) / gridDim.x)
-                           : (int)((r1 - r0 + kScanRowsPerStage - 1) / kScanRowsPerStage);
-    auto stage_row = [&](int i) -> int64_t {
-        return il ? ((int64_t)i * gridDim.x + blockIdx.x) * kScanRowsPerStage : r0 + (int64_t)i * kScanRowsPerStage;
-    };
-    const int64_t r_end = il ? n_rows : r1;
+    // stages are groups of 8 consecutive rows handed out by a global counter (sched[0]):
+    // an SM that streams faster takes more of them, so the CTAs end together
+    const int n_groups = (int)((n_rows + kScanRowsPerStage - 1) / kScanRowsPerStage);
     for (int i = threadIdx.x; i < kHistBins; i += blockDim.x) hist_sm[i] = 0;
     if (threadIdx.x == 0) {
         for (int s = 0; s < kScanStages; ++s) {
@@ -245,28 +238,23 @@ sem_scan_tma_kernel(const uint16_t* __restrict__ E, int64_t n_rows, int d, const
         if (lane == 0) {
             uint64_t pol;
             asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-            // L2 prefetch pf stages ahead of the ring: HBM sees (ring + pf) stages of
-            // requests per SM, more than shared memory can hold
-            for (int i = 0; i < min(pf, n_stage); ++i) {
-                const int64_t row = stage_row(i);
-                const int nr = (int)min((int64_t)kScanRowsPerStage, r_end - row);
-                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"((const unsigned char*)E + row * row_bytes),
-                             "r"((uint32_t)(nr * row_bytes)) : "memory");
-            }
-            for (int i = 0; i < n_stage; ++i) {
+            int g = atomicAdd(&sched[0], 1);
+            for (int i = 0;; ++i) {
                 const int slot = i % kScanStages;
-                if (pf > 0 && i + pf < n_stage) {
-                    const int64_t prow = stage_row(i + pf);
-                    const int pnr = (int)min((int64_t)kScanRowsPerStage, r_end - prow);
-                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;"
-                                 ::"l"((const unsigned char*)E + prow * row_bytes), "r"((uint32_t)(pnr * row_bytes)) : "memory");
-                }
                 if (i >= kScanStages) s_mbar_wait(&empty[slot], (uint32_t)((i / kScanStages) - 1) & 1);
-                const int64_t row = stage_row(i);
-                const int nr = (int)min((int64_t)kScanRowsPerStage, r_end - row);
+                if (g >= n_groups) {   // no stage left: an end marker (a plain arrive completes the phase)
+                    srow[slot] = -1;
+                    s_mbar_arrive(&full[slot]);
+                    break;
+                }
+                const int g_next = atomicAdd(&sched[0], 1);   // the next claim overlaps this copy
+                const int64_t row = (int64_t)g * kScanRowsPerStage;
+                const int nr = (int)min((int64_t)kScanRowsPerStage, n_rows - row);
                 const uint32_t bytes = (uint32_t)(nr * row_bytes);
+                srow[slot] = row;
                 s_mbar_expect(&full[slot], bytes);
                 s_bulk_g2s(ring + slot * stage_bytes, (const unsigned char*)E + row * row_bytes, bytes, &full[slot], pol);
+                g = g_next;
             }
         }
         return;
@@ -285,11 +273,12 @@ sem_scan_tma_kernel(const uint16_t* __restrict__ E, int64_t n_rows, int d, const
     }
     // this lane's 16 bytes of its slab in row 0 of slot 0, as a shared-window address
     const uint32_t my_s = s_u32(ring) + (uint32_t)(warp * 512 + lane * 16);
-    for (int i = 0; i < n_stage; ++i) {
+    for (int i = 0;; ++i) {
         const int slot = i % kScanStages;
         s_mbar_wait(&full[slot], (uint32_t)(i / kScanStages) & 1);
-        const int64_t row0 = stage_row(i);
-        const int nr = (int)min((int64_t)kScanRowsPerStage, r_end - row0);
+        const int64_t row0 = srow[slot];
+        if (row0 < 0) break;
+        const int nr = (int)min((int64_t)kScanRowsPerStage, n_rows - row0);
         const uint32_t st = my_s + (uint32_t)(slot * stage_bytes);
         // this warp's slab of the stage into registers, then the slot goes back to
         // the producer at once: the ring refills while the warp computes
@@ -375,12 +364,22 @@ sem_scan_tma_kernel(const uint16_t* __restrict__ E, int64_t n_rows, int d, const
     for (int i = threadIdx.x; i < kHistBins; i += n_slab * 32)
         if (hist_sm[i]) atomicAdd(&hist12[i], hist_sm[i]);
     if (tr && threadIdx.x == 0) tr[2 * blockIdx.x + 1] = step_gtime();
-    if (threadIdx.x == 0) pdl_wait();
+    if (threadIdx.x == 0) {
+        // the last CTA out resets the stage counter for the next launch (every CTA's
+        // claims precede its arrival here)
+        __threadfence();
+        if (atomicAdd(&sched[1], 1) == (int)gridDim.x - 1) {
+            sched[0] = 0;
+            sched[1] = 0;
+            __threadfence();
+        }
+        pdl_wait();
+    }
 }
 
 void launch_sem_scan(const void* E, int e_dtype, int64_t n_rows, int d, const void* q, int q_dtype,
                      double* s64, uint32_t* key32, uint32_t* hist12, cudaStream_t st, uint32_t* zero_w,
-                     int n_zero_w, int* zero_c, bool hist_zero) {
+                     int n_zero_w, int* zero_c, bool hist_zero, int* sched) {
     // hist_zero: hist12 is already zero (the previous build's union kernel cleared it)
     if (!hist_zero) cudaMemsetAsync(hist12, 0, kHistBins * sizeof(uint32_t), st);
     const int elems = e_dtype == 0 ? 8 : 4;
@@ -390,14 +389,14 @@ void launch_sem_scan(const void* E, int e_dtype, int64_t n_rows, int d, const vo
     // 2-row stages measured slower: per-stage overhead)
     constexpr int RS = kScanRS, NS = 3;
     auto smem_for = [&](int rs, int ns) {
-        return (size_t)ns * rs * d * 2 + kHistBins * 4 + (size_t)2 * ns * kScanConsumers * rs * 8 + 4 * ns * 8;
+        return (size_t)ns * rs * d * 2 + kHistBins * 4 + (size_t)2 * ns * kScanConsumers * rs * 8 + 5 * ns * 8;
     };
     // EVOSPEC_SCAN_RING2=1 (test only, tests/test_gpu_scan_ring.py): a 2-stage ring -- every
     // slot is refilled while the slab warps of the stage before it still compute, the
     // tightest reuse of the release / refill ordering; the scores must equal the 3-stage
     // ring's bit for bit (same summation order)
     static const bool ring2 = getenv("EVOSPEC_SCAN_RING2") != nullptr;
-    if (e_dtype == 0 && d % 256 == 0 && d <= 256 * kScanConsumers && smem_for(RS, NS) <= 227 * 1024) {
+    if (e_dtype == 0 && sched && d % 256 == 0 && d <= 256 * kScanConsumers && smem_for(RS, NS) <= 227 * 1024) {
         const size_t sm = smem_for(RS, ring2 ? 2 : NS);
         static thread_local size_t attr = 0, attr2 = 0;
         if (ring2) {
@@ -406,7 +405,7 @@ void launch_sem_scan(const void* E, int e_dtype, int64_t n_rows, int d, const vo
                 attr2 = sm;
             }
             launch_pdl(sem_scan_tma_kernel<RS, 2>, dim3(kNumSMs), dim3((kScanConsumers + 1) * 32), sm, st,
-                       (const uint16_t*)E, n_rows, d, q, q_dtype, hist12, s64, key32, kScanPf, 1, zero_w, n_zero_w,
+                       (const uint16_t*)E, n_rows, d, q, q_dtype, hist12, s64, key32, sched, zero_w, n_zero_w,
                        zero_c, s_step_trace);
             return;
         }
@@ -415,7 +414,7 @@ void launch_sem_scan(const void* E, int e_dtype, int64_t n_rows, int d, const vo
             attr = sm;
         }
         launch_pdl(sem_scan_tma_kernel<RS, NS>, dim3(kNumSMs), dim3((kScanConsumers + 1) * 32), sm, st,
-                   (const uint16_t*)E, n_rows, d, q, q_dtype, hist12, s64, key32, kScanPf, 1, zero_w, n_zero_w, zero_c,
+                   (const uint16_t*)E, n_rows, d, q, q_dtype, hist12, s64, key32, sched, zero_w, n_zero_w, zero_c,
                    s_step_trace);
     } else if (e_dtype == 0) {
         cudaFuncSetAttribute(sem_scan_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
