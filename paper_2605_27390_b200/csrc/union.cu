@@ -323,7 +323,7 @@ ES_DEV void block_topM_multi(const uint64_t* ck, const int32_t* cid, uint8_t* cf
         }
     }
     stamp(10);
-    if (tid < K) { ws[tid].kmin = ~0ull; ws[tid].kmax = 0ull; ws[tid].gn = 0; }
+    if (tid < K) ws[tid].gn = 0;
     {
         int ex[K];
         block_scan_multi<K>(c, warp_tot, ex);   // (syncs: ws initialised before the atomics)
@@ -332,14 +332,21 @@ ES_DEV void block_topM_multi(const uint64_t* ck, const int32_t* cid, uint8_t* cf
 #pragma unroll
             for (int j = 0; j < K; ++j) warp_tot[j * 33 + 32] = ex[j] + c[j];
     }
+    // key range: warp reductions, then one warp per selection over the warps' results
+    // (64-bit shared atomics are CAS loops: 32 warps on one address serialise)
+    uint64_t* red = (uint64_t*)hist;   // [2][K][32] (the histograms are free until the passes)
+    const int wid = warp_id(), nw = T / 32;
 #pragma unroll
     for (int j = 0; j < K; ++j) {
         kmin[j] = warp_min_u64(kmin[j]);
         kmax[j] = warp_max_u64(kmax[j]);
-        if (lane == 0 && kmin[j] <= kmax[j]) {
-            atomicMin((unsigned long long*)&ws[j].kmin, kmin[j]);
-            atomicMax((unsigned long long*)&ws[j].kmax, kmax[j]);
-        }
+        if (lane == 0) { red[j * 32 + wid] = kmin[j]; red[(K + j) * 32 + wid] = kmax[j]; }
+    }
+    __syncthreads();
+    if (wid < K) {
+        const uint64_t lo = warp_min_u64(lane < nw ? red[wid * 32 + lane] : ~0ull);
+        const uint64_t hi = warp_max_u64(lane < nw ? red[(K + wid) * 32 + lane] : 0ull);
+        if (lane == 0) { ws[wid].kmin = lo; ws[wid].kmax = hi; }
     }
     __syncthreads();
     if (tid < K) {
@@ -503,7 +510,7 @@ union_kernel(int V, const int32_t* __restrict__ static_ids, int n_static,
     int32_t* graph = gs + kMaxG;                             // [kMaxG * per_seed]
     uint8_t* cf = (uint8_t*)(graph + kMaxG * per_seed);      // [cap]
     __shared__ int warp_tot[3 * 33];
-    __shared__ uint32_t hist[3 * kSelBins];
+    __shared__ __align__(16) uint32_t hist[3 * kSelBins];
     __shared__ BSel bsel[3];
     __shared__ WSel wsel[3];
     __shared__ int nG_s, bad_s, taken_s, ngs_s, sem_n_s;
@@ -532,6 +539,7 @@ union_kernel(int V, const int32_t* __restrict__ static_ids, int n_static,
         return taken;
     };
     pdl_wait();
+    if (trace) { if (threadIdx.x == 0) { long long t_; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); trace[40] = t_; } }
     // 1. static members: the bitmap static_bits_kernel built ahead of the scan (an
     //    earlier kernel on the stream: complete once the predecessor is)
     {
@@ -542,6 +550,7 @@ union_kernel(int V, const int32_t* __restrict__ static_ids, int n_static,
         for (int w = (n4 << 2) + tid; w < nwords; w += T) bits[w] = __ldcg(&sbits[w]);
     }
     __syncthreads();
+    if (trace) { if (threadIdx.x == 0) { long long t_; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); trace[41] = t_; } }
     // formation starts with the seeds (C6): warp 0 walks them
     if (warp_id() == 0) {
         const int t = walk(seeds, n_seed, 0);
@@ -604,9 +613,9 @@ union_kernel(int V, const int32_t* __restrict__ static_ids, int n_static,
         const int M[3] = {n_sem, budget, ngs};
         const int pc[3] = {st_c[0], st_c[1], st_c[0]};
         const uint64_t plo[3] = {st_lo[0], st_lo[1], st_lo[0]}, phi[3] = {st_hi[0], st_hi[1], st_hi[0]};
-        block_topM_multi<3>(ck, cid, cf, n_cand, A, S, M, hist, wsel, bsel, warp_tot, trace ? trace + 7 : nullptr, pc, plo,
+        block_topM_multi<3>(ck, cid, cf, n_cand, A, S, M, hist, wsel, bsel, warp_tot, trace ? trace + 24 : nullptr, pc, plo,
                             phi);
-        if (trace && tid == 0) trace[16] = n_cand;
+        if (trace && tid == 0) trace[23] = n_cand;   // (stamps 24..39: the selection's phases)
     }
     if (sem_out) {
         for (int base = 0; base < n_cand; base += T) {      // one smem atomic per warp

@@ -31,10 +31,10 @@ print({k: round(v / max(1, st["calls"][k]) * 1e3, 1) for k, v in st["ms"].items(
 tr = ctx.read_trace()[2 * 148 * 8:2 * 148 * 8 + 7].astype(np.float64)
 names = ["start", "loaded", "S_sem", "gs", "G/graph", "formation", "end"]
 print("union phases (us from start):", {n: round((t - tr[0]) / 1e3, 1) for n, t in zip(names, tr)})
-tr2 = ctx.read_trace(2 * 148 * 8 + 24)[2 * 148 * 8:2 * 148 * 8 + 24].astype(np.float64)
+tr2 = ctx.read_trace(2 * 148 * 8 + 40)[2 * 148 * 8 + 17:2 * 148 * 8 + 40].astype(np.float64)   # [7] = selection start
 print("multi-select: setup", round((tr2[8] - tr2[7]) / 1e3, 2) if tr2[8] > 0 else None,
       "later passes (us):", [round((tr2[8 + i] - tr2[7 + i]) / 1e3, 2) for i in range(1, 8) if tr2[8 + i] > 0 and i < 9],
-      "n_cand", int(tr2[16]))
+      "n_cand", int(tr2[6]))
 print("setup detail (us from start): count loop", round((tr2[17] - tr2[7]) / 1e3, 2), "scan+minmax", round((tr2[18] - tr2[7]) / 1e3, 2),
       "pass0 hist done", round((tr2[19] - tr2[7]) / 1e3, 2), "pass0 end", round((tr2[8] - tr2[7]) / 1e3, 2),
       "marked", round((tr2[20] - tr2[7]) / 1e3, 2), "ranked", round((tr2[21] - tr2[7]) / 1e3, 2))

@@ -55,6 +55,12 @@ dist("cand kernel start", cand[:1])
 dist("cand kernel end", cand[1:])
 for i, nm in enumerate(["start", "loaded", "S_sem", "gs", "G/graph", "formation", "end"]):
     dist("union " + nm, uni[i:i + 1])
+dist("union after wait", tr[2 * N * 8 + 40:2 * N * 8 + 41])
+dist("union sbits copied", tr[2 * N * 8 + 41:2 * N * 8 + 42])
+sel = tr[2 * N * 8 + 24:2 * N * 8 + 40]
+for i, nm in [(0, "start"), (10, "stats"), (11, "setup"), (12, "hist0"), (1, "pass0"), (2, "pass1"), (13, "marked"),
+              (14, "ranked")]:
+    dist("  select " + nm, sel[i:i + 1])
 for i, nm in enumerate(["start", "prod_done", "mma_done", "t0_ready", "t0_fold", "t1_ready", "t1_fold", "end"]):
     dist("lmh " + nm, lmh[:, i])
 for i, nm in enumerate(["start", "hnorm", "B1", "filter", "runs", "rescore", "end"]):
