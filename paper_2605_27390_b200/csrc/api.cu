@@ -788,8 +788,7 @@ static evospec_status lmh_impl(evospec_ctx* ctx, const void* W, int64_t n_w_rows
     a.part = ctx->part;
     a.m_ids = m_ids; a.m_vals = m_vals; a.m_lse = m_lse; a.m_probs = m_probs;
     a.par_fold = 1;    // thread-parallel epilogue fold (lmh_epilogue.cuh; the warp fold on single-tile CTAs)
-    a.fin_opt = 15;    // finalisation: H staged before the PDL wait, W-row L2 prefetch, multi-warp re-score,
-                       // parallel head threshold (each measured faster, round 1)
+    a.fin_opt = 2;     // finalisation: the candidates' W rows prefetched to L2 for the re-score
     if (list2) {   // two-list mode (draft_step overlap): one SM stays free for the union kernel
         a.list2 = list2; a.n_list2_dev = n_list2_dev; a.n_list2_max = n_list2_max; a.n1 = n_subset_max;
         a.grid = lmh_tc_grid() - 1;
@@ -812,17 +811,8 @@ static evospec_status lmh_impl(evospec_ctx* ctx, const void* W, int64_t n_w_rows
     float gamma = gemv_gamma(c.d);
     {
         StageTimer t(ctx, EVOSPEC_STAGE_LMH, st);
-        // H-on-lanes kernel: opt-in (EVOSPEC_LMH_HL=1); measured slower than lmh_tc at every
-        // subset size: its thread-per-row epilogue is latency-bound
-        static const bool hl_env = getenv("EVOSPEC_LMH_HL") ? atoi(getenv("EVOSPEC_LMH_HL")) != 0 : false;
-        if (use_tc(a) && hl_env && lmh_hl_supported(a) && !segs) {
-            // H rows on the TMEM lanes (lmh_hl.cu): per-CTA candidate buffers (<= 64, unsorted)
-            a.LS = 64;
-            CUDA_TRY(launch_lmh_hl(a, st));
-            ctx->launches += 1;
-            n_cta = a.grid > 0 ? a.grid : lmh_tc_grid();
-            gamma = kTcGamma;
-        } else if (use_tc(a)) {
+        if (use_tc(a)) {
+            a.gid_keys = (a.KP <= 32 && a.LS == 64) ? 1 : 0;
             CUDA_TRY(launch_lmh_tc(a, st));
             ctx->launches += 1;
             n_cta = segs ? segs->seg_ctas : (a.grid > 0 ? a.grid : lmh_tc_grid());

@@ -23,18 +23,12 @@
 #include "common.cuh"
 #include "kernels.cuh"
 #include "lmh_epilogue.cuh"   // warp_kth_largest
-#include "finalize32.cuh"   // fin32_row
+#include "fin64.cuh"       // lmh_fin64_kernel (k + 8 <= 32)
 
 namespace es {
 
 constexpr int kFinThreads = 256;
-constexpr int kFinCand = 1024;   // candidate buffer of the threshold filter (finalize32)
 
-ES_DEV long long fin_gtime() {
-    long long t;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    return t;
-}
 // profiling stamps (EVOSPEC_TRACE): slots [148*8 + row*8 + i]
 // fine-grained clock64 stamps of row 0 (thread 0 / warp 0 lane 0), slots [2*148*8 + 16 + i]
 #define FIN_DT(i) do { if (a.trace && blockIdx.x == 0) a.trace[2 * 148 * 8 + 16 + (i)] = clock64(); } while (0)
@@ -313,62 +307,18 @@ lmh_finalize_kernel(LmhArgs a, int n_cta, int k, float gamma, const float* __res
 
 
 
-template <int U, int NT, int LSX = kFin32LS>
-__global__ void __launch_bounds__(NT)
-lmh_finalize32_kernel(LmhArgs a, int n_cta_arg, int k, float gamma, const float* __restrict__ wmax_dev,
-                      int32_t* __restrict__ topk_ids, float* __restrict__ topk_vals,
-                      float* __restrict__ row_max, float* __restrict__ row_sumexp, int* flags) {
-    extern __shared__ __align__(16) unsigned char f32_sm[];
-    pdl_trigger();
-    const Fin32Smem sm = fin32_carve(f32_sm, NT);
-    // H row and ||h||^2 need only the LM head's inputs: before the wait (overlaps its tail)
-    const bool pre = a.fin_opt & 1;
-    const double hacc = pre ? fin32_stage_h<NT>(a, blockIdx.x, sm) : 0.0;
-    pdl_wait();
-    fin32_row<U, NT, LSX>(a, blockIdx.x, n_cta_arg, k, gamma, wmax_dev, topk_ids, topk_vals, row_max,
-                          row_sumexp, flags, sm, pre, hacc);
-
-}
-
 void launch_lmh_finalize(const LmhArgs& a, int n_cta, int k, const float* wmax_dev, int32_t* topk_ids,
                          float* topk_vals, float* row_max, float* row_sumexp, int* flags, cudaStream_t st,
                          float gamma) {
-    if (a.KP <= 32 && a.LS == 32 && n_cta * 8 <= 10 * kFin32Threads) {
-        // sorted per-CTA top-KP lists of lmh_hl_kernel (stride 32)
-        const int nq = n_cta * 8;
-        auto go = [&](auto kern, bool& attr_set) {
-            const size_t smem = std::max(fin32_smem_bytes(kFin32Threads), (size_t)(a.n_h <= kNumSMs ? 120 * 1024 : 0));
-            if (!attr_set)
-                attr_set = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                (int)std::max(smem, (size_t)120 * 1024)) == cudaSuccess;
-            launch_pdl(kern, dim3(a.n_h), dim3(kFin32Threads), smem, st, a, n_cta, k, gamma, wmax_dev, topk_ids,
-                       topk_vals, row_max, row_sumexp, flags);
-        };
-        static thread_local bool s3 = false, s5 = false, s10 = false;
-        if (nq <= 3 * kFin32Threads) go(lmh_finalize32_kernel<3, kFin32Threads, 32>, s3);
-        else if (nq <= 5 * kFin32Threads) go(lmh_finalize32_kernel<5, kFin32Threads, 32>, s5);
-        else go(lmh_finalize32_kernel<10, kFin32Threads, 32>, s10);
-        return;
-    }
-    if (a.KP <= 32 && a.LS == kFin32LS && n_cta * (kFin32LS / 4) <= 10 * kFin32Threads) {
-        // one CTA per SM while the rows fit one wave (the dynamic allocation is only
-        // a placement hint: two CTAs sharing an SM measured slower); more rows pack.
-        // 512 threads with 5 or 10 list loads each; EVOSPEC_FIN_NT=1024 takes 1024
-        // threads with 3 while the lists fit (measured equal in the sweep, slower alone)
-        const int fin_nt = 512;   // (1024 threads with 3 loads each measured no faster)
-        const int nq = n_cta * (kFin32LS / 4);
-        auto go = [&](auto kern, int nt, bool& attr_set) {
-            const size_t smem = std::max(fin32_smem_bytes(nt), (size_t)(a.n_h <= kNumSMs ? 120 * 1024 : 0));
-            if (!attr_set)   // once per thread (the placement-hint size is fixed)
-                attr_set = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                (int)std::max(smem, (size_t)120 * 1024)) == cudaSuccess;
-            launch_pdl(kern, dim3(a.n_h), dim3(nt), smem, st, a, n_cta, k, gamma, wmax_dev, topk_ids, topk_vals,
-                       row_max, row_sumexp, flags);
-        };
-        static thread_local bool set3 = false, set5 = false, set10 = false;
-        if (fin_nt >= 1024 && nq <= 3 * 1024) go(lmh_finalize32_kernel<3, 1024>, 1024, set3);
-        else if (nq <= 5 * kFin32Threads) go(lmh_finalize32_kernel<5, kFin32Threads>, kFin32Threads, set5);
-        else go(lmh_finalize32_kernel<10, kFin32Threads>, kFin32Threads, set10);
+    if (a.KP <= 32 && a.LS == kF64LS && n_cta <= kF64MaxCta) {
+        // one CTA per SM while the rows fit one wave (the dynamic allocation is only a
+        // placement hint: CTAs sharing an SM measured slower in round 1)
+        auto kern = lmh_fin64_kernel<kF64Threads>;
+        static thread_local bool attr_set = false;
+        if (!attr_set)
+            attr_set = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 120 * 1024) == cudaSuccess;
+        launch_pdl(kern, dim3(a.n_h), dim3(kF64Threads), a.n_h <= kNumSMs ? (size_t)120 * 1024 : 0, st, a, n_cta, k,
+                   gamma, wmax_dev, topk_ids, topk_vals, row_max, row_sumexp, flags);
         return;
     }
     size_t smem = (size_t)n_cta * 2 * sizeof(int) + (size_t)n_cta * a.KP * 8;

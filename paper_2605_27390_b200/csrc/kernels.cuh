@@ -85,8 +85,7 @@ struct LmhArgs {
     // optional fused single-shard merge outputs (R = 1): ids/vals [n_h][k], lse [n_h], probs [n_h][k]
     int32_t* m_ids; float* m_vals; float* m_lse; float* m_probs;
     LmhPartials part;
-    int fin_opt;    // finalisation variants (bits; EVOSPEC_FIN_OPT): 1 H before the PDL wait, 2 W-row L2 prefetch,
-                    // 4 multi-warp re-score, 8 parallel head threshold
+    int fin_opt;    // finalisation options (bits): 2 = W rows of the candidates prefetched to L2
     int par_fold;   // thread-parallel tile fold (lmh_epilogue.cuh epi_par_*), buffered path
     // two-list mode (draft_step overlap): `subset` holds n1 ids known at launch (the static
     // core, an input) and `list2` the ids produced by the previous kernel (the dynamic
@@ -95,6 +94,8 @@ struct LmhArgs {
     // before griddepcontrol.wait. grid: CTAs of the launch (0 = all SMs)
     const int32_t* list2; const int32_t* n_list2_dev; int n_list2_max; int n1;
     int grid;
+    int gid_keys;   // partial lists carry vocabulary ids, not subset positions (tensor-core
+                    // kernel, buffered lists; ties then order by id in two-list mode too)
 };
 
 // This CTA's contiguous share [p0, p1) of the subset positions: all of
@@ -137,10 +138,6 @@ void launch_subset_update(const int32_t* S, int n, const int32_t* rem, int nr, c
 bool lmh_tc_supported(const LmhArgs& a);
 int lmh_tc_grid();
 cudaError_t launch_lmh_tc(const LmhArgs& a, cudaStream_t st);
-// H rows on the TMEM lanes (lmh_hl.cu): n_h <= 64, k + 8 <= 32, bf16; writes sorted
-// per-CTA top-KP lists with stride a.LS = 32 (finalised by the LS = 32 path)
-bool lmh_hl_supported(const LmhArgs& a);
-cudaError_t launch_lmh_hl(const LmhArgs& a, cudaStream_t st);
 
 // ---- finalize / merge / prepare (finalize.cu)
 void launch_lmh_finalize(const LmhArgs& a, int n_cta, int k, const float* wmax_dev,

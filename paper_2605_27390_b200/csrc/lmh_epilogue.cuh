@@ -43,14 +43,19 @@ struct EpiSmem {
     float* scr_v;    // [n_warps][32] candidate batch scratch
     int* scr_p;      // [n_warps][32]
     int* st_flag;    // [4] block flags (thread-parallel fold: a row overflowed)
+    int* tile_id;    // [kTile] buffered path: the key of each tile position (its vocabulary
+                     // id), or null: keys are the subset positions themselves
 };
+
+// Key of tile position p (the order of ties: value desc, key asc)
+ES_DEV int tile_key(const EpiSmem& e, int base_pos, int p) { return e.tile_id ? e.tile_id[p] : base_pos + p; }
 
 __host__ __device__ inline size_t epi_smem_bytes(int n_h, int cap, int n_warps) {
     return (size_t)n_h * kTile * 4 + (size_t)n_h * cap * 8 + (size_t)n_h * 20 + (size_t)n_h * 32 * 4 +
-           (size_t)n_warps * 32 * 8 + 16;
+           (size_t)n_warps * 32 * 8 + 16 + kTile * 4;
 }
 
-ES_DEV EpiSmem epi_carve(unsigned char* p, int n_h, int cap, int n_warps) {
+ES_DEV EpiSmem epi_carve(unsigned char* p, int n_h, int cap, int n_warps, bool keys = false) {
     EpiSmem e;
     e.tile = (float*)p;        p += (size_t)n_h * kTile * 4;
     e.st_val = (float*)p;      p += (size_t)n_h * cap * 4;
@@ -63,7 +68,8 @@ ES_DEV EpiSmem epi_carve(unsigned char* p, int n_h, int cap, int n_warps) {
     e.st_xcnt = (int*)p;       p += (size_t)n_h * 4;
     e.scr_v = (float*)p;       p += (size_t)n_warps * 32 * 4;
     e.scr_p = (int*)p;         p += (size_t)n_warps * 32 * 4;
-    e.st_flag = (int*)p;
+    e.st_flag = (int*)p;       p += 16;
+    e.tile_id = keys ? (int*)p : nullptr;
     return e;
 }
 
@@ -504,7 +510,7 @@ ES_DEV void fold_buf(const EpiSmem& e, int r, int KP, int tn, int base_pos, cons
         int c = 0;
 #pragma unroll
         for (int j = 0; j < kTileJ; ++j) {
-            const int pj = base_pos + lane + 32 * j;
+            const int pj = tile_key(e, base_pos, lane + 32 * j);
             cand[j] = v[j] != -INFINITY && before(v[j], pj, thv, thp);
             msk[j] = __ballot_sync(0xffffffffu, cand[j]);
             c += __popc(msk[j]);
@@ -518,7 +524,7 @@ ES_DEV void fold_buf(const EpiSmem& e, int r, int KP, int tn, int base_pos, cons
             c = 0;
 #pragma unroll
             for (int j = 0; j < kTileJ; ++j) {
-                cand[j] = cand[j] && before(v[j], base_pos + lane + 32 * j, thv, thp);
+                cand[j] = cand[j] && before(v[j], tile_key(e, base_pos, lane + 32 * j), thv, thp);
                 msk[j] = __ballot_sync(0xffffffffu, cand[j]);
                 c += __popc(msk[j]);
             }
@@ -530,7 +536,7 @@ ES_DEV void fold_buf(const EpiSmem& e, int r, int KP, int tn, int base_pos, cons
                 if (cand[j]) {
                     const int idx = base + __popc(msk[j] & ((1u << lane) - 1u));
                     bv[idx] = v[j];
-                    bp[idx] = base_pos + lane + 32 * j;
+                    bp[idx] = tile_key(e, base_pos, lane + 32 * j);
                 }
                 base += __popc(msk[j]);
             }
@@ -547,7 +553,7 @@ ES_DEV void fold_buf(const EpiSmem& e, int r, int KP, int tn, int base_pos, cons
 #pragma unroll
                 for (int j = 0; j < kTileJ; ++j) {
                     const int idx = base + __popc(msk[j] & ((1u << lane) - 1u)) - done;
-                    if (cand[j] && idx >= 0 && idx < 32) { scr_v[idx] = v[j]; scr_p[idx] = base_pos + lane + 32 * j; }
+                    if (cand[j] && idx >= 0 && idx < 32) { scr_v[idx] = v[j]; scr_p[idx] = tile_key(e, base_pos, lane + 32 * j); }
                     base += __popc(msk[j]);
                 }
                 __syncwarp();
@@ -776,21 +782,25 @@ ES_DEV void epi_par_phase1(const EpiSmem& e, int n_h, int tn, int base_pos, int 
         // positions drop out) and admission (strictly before the bound)
         const float mb = m_new == -INFINITY ? 0.0f : m_new * 1.4426950408889634f;
         float sum0 = 0.0f, sum1 = 0.0f;
-        unsigned cm = 0u;
+        unsigned cm = 0u, em = 0u;
 #pragma unroll 4
         for (int j = 0; j < 8; ++j) {
             float x4[4];
             ld4(j, x4);
-            const int p0 = base_pos + g * 32 + 4 * ((j + rot) & 7);
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
                 const float ex = ex2_approx(fmaf(x4[c], 1.4426950408889634f, -mb));
                 if (c & 1) sum1 += ex; else sum0 += ex;
-                // (bitwise, not short-circuit: no branch per value)
-                const unsigned adm = (unsigned)(x4[c] > thv) |
-                                     ((unsigned)(x4[c] == thv) & (unsigned)(x4[c] != -INFINITY) & (unsigned)(p0 + c < thp));
-                cm |= adm << (4 * j + c);
+                // (bitwise, not short-circuit: no branch per value); values equal to the
+                // bound are admitted by key below (rare)
+                cm |= (unsigned)(x4[c] > thv) << (4 * j + c);
+                em |= ((unsigned)(x4[c] == thv) & (unsigned)(x4[c] != -INFINITY)) << (4 * j + c);
             }
+        }
+        while (em) {
+            const int i = __ffs(em) - 1;
+            em &= em - 1u;
+            if (tile_key(e, base_pos, g * 32 + 4 * (((i >> 2) + rot) & 7) + (i & 3)) < thp) cm |= 1u << i;
         }
         float sum = sum0 + sum1;
         PTR_(1);
@@ -823,7 +833,7 @@ ES_DEV void epi_par_phase1(const EpiSmem& e, int n_h, int tn, int base_pos, int 
                     cm &= cm - 1u;
                     const int pl = g * 32 + 4 * (((i >> 2) + rot) & 7) + (i & 3);
                     bv[at] = trow[pl - g * 32];
-                    bp[at] = base_pos + pl;
+                    bp[at] = tile_key(e, base_pos, pl);
                     ++at;
                 }
             }

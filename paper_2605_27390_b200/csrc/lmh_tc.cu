@@ -94,7 +94,9 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
     unsigned char* smA = base;                                   // [S][128][128 B]
     unsigned char* smB = base + tp.off_b;                        // [S][NP][128 B]
     const bool buffered = a.KP <= 32 && a.LS == kBuf;   // unsorted candidate buffers (lmh_epilogue.cuh)
-    EpiSmem e = epi_carve(base + tp.off_epi, a.nseg > 0 ? a.seg_rows : n_h, buffered ? kBuf : a.KP, kTcWarps);
+    // buffered lists carry vocabulary ids (keys) instead of subset positions (a.gid_keys)
+    EpiSmem e = epi_carve(base + tp.off_epi, a.nseg > 0 ? a.seg_rows : n_h, buffered ? kBuf : a.KP, kTcWarps,
+                          buffered && a.gid_keys);
     uint64_t* full = (uint64_t*)(base + tp.off_bar);             // [S]
     uint64_t* empty = full + S;                                  // [S]
     uint64_t* tfull = empty + S;                                 // [2]
@@ -302,6 +304,9 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
             int t0, tn;
             tile_range(t, t0, tn);
             const int b = t & 1;
+            // the tile's keys (vocabulary ids), loaded while the accumulator fills
+            int key = 0x7fffffff;
+            if (e.tile_id && half == 0 && row < tn) key = lmh_id_at(a, t0 + row);
             // two-list mode: whether a first-list tile is the CTA's last is known only
             // after the union ends -- those are folded as middle tiles (overlapping the
             // wait); a CTA without second-list tiles stores its rows after the loop
@@ -318,6 +323,7 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
                 for (int j = 0; j < 16; ++j)
                     if (c0 + j < n_h) e.tile[(c0 + j) * kTile + row] = v[j] * a.inv_temp;
             }
+            if (e.tile_id && half == 0) e.tile_id[row] = key;
             tc_fence_before();
             mbar_arrive(&tempty[b]);
             if (DTR && ew == 0 && lane == 0 && last_t) DTR[41] = clock64();

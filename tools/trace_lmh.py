@@ -30,10 +30,18 @@ ctx = es.Context(V=V, d=d, w_dtype=torch.bfloat16, h_dtype=torch.bfloat16, max_s
 ctx.prepare_weights(Wd)
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 names = ["start", "prod_done", "mma_done", "t0_ready", "t0_fold", "t1_ready", "t1_fold", "end"]
-for pf in ["default"]:
+small = torch.from_numpy(S[:256].copy()).cuda()
+nsmall = torch.tensor([256], dtype=torch.int32, device="cuda")
+# modes: flushed (L2 flushed before the call), warmcode (flushed, then a 256-row call of
+# the same kernels so their code is in L2 / the I-caches, then the timed call), steady
+# (calls back to back, no flush)
+for pf in os.environ.get("TRACE_MODES", "flushed,warmcode,steady").split(","):
     evs = []
     for it in range(8):
-        flush.fill_(it)
+        if pf != "steady":
+            flush.fill_(it)
+        if pf == "warmcode":
+            ctx.subset_logits_topk(Wd, Hd, small, nsmall, 256, k)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         ctx.subset_logits_topk(Wd, Hd, Sd, nd, n_S, k)
@@ -74,7 +82,10 @@ for pf in ["default"]:
                 print("     row", it, [int(dd[it * 4 + j] - b) for j in range(4)])
     evs = []
     for it in range(8):
-        flush.fill_(it)
+        if pf != "steady":
+            flush.fill_(it)
+        if pf == "warmcode":
+            ctx.subset_logits_topk(Wd, Hd, small, nsmall, 256, k)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         ctx.subset_logits_topk_merged(Wd, Hd, Sd, nd, n_S, k)
