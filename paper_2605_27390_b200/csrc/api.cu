@@ -185,7 +185,7 @@ struct evospec_ctx {
 
 namespace {
 constexpr int kTimingSlots = 4096;
-constexpr int kTraceLen = 2 * kNumSMs * 8 + 16 + 32 + 64 + 2 * kNumSMs + 8;   // LM-head CTAs, finalize rows,
+constexpr int kTraceLen = kTraceOvf + 2 * kNumSMs;   // LM-head CTAs, finalize rows,
                                                                               // union stamps, scan / candidate stamps
 
 // union stamps live after the LM-head / finalize slots
@@ -312,7 +312,7 @@ evospec_status evospec_create(evospec_ctx** out, const evospec_config* cfg, int 
     A(dalloc(&x->gat_s, sem * R)); A(dalloc(&x->gat_id, sem * R));
     A(dalloc(&x->sem_ids, sem)); A(dalloc(&x->sem_n, 1));
     A(dalloc(&x->ctx_sel, std::max(1, c.max_ctx))); A(dalloc(&x->ctx_n, 1));
-    A(dalloc(&x->part.val, pr * kMaxKP)); A(dalloc(&x->part.id, pr * kMaxKP));
+    A(dalloc(&x->part.val, pr * std::max(kMaxKP, kTcListLS))); A(dalloc(&x->part.id, pr * std::max(kMaxKP, kTcListLS)));
     A(dalloc(&x->part.m, pr)); A(dalloc(&x->part.s, pr)); A(dalloc(&x->part.cnt, pr)); A(dalloc(&x->part.xcnt, pr));
     A(dalloc(&x->flags, 1)); A(dalloc(&x->wmax, 1));
     const size_t trip = (size_t)R * c.max_rows * c.max_k;
@@ -804,7 +804,10 @@ static evospec_status lmh_impl(evospec_ctx* ctx, const void* W, int64_t n_w_rows
     if (getenv("EVOSPEC_TRACE")) {
         if (!ctx->trace) CUDA_TRY(cudaMalloc(&ctx->trace, kTraceLen * sizeof(long long)));
         if (!list2)   // (a memset between the union and a two-list head would break the PDL overlap)
+        {
             CUDA_TRY(cudaMemsetAsync(ctx->trace, 0, 2 * kNumSMs * 8 * sizeof(long long), st));
+            CUDA_TRY(cudaMemsetAsync(ctx->trace + kTraceOvf, 0, 2 * kNumSMs * sizeof(long long), st));
+        }
         a.trace = ctx->trace;
     }
     int n_cta = 0;
@@ -812,7 +815,7 @@ static evospec_status lmh_impl(evospec_ctx* ctx, const void* W, int64_t n_w_rows
     {
         StageTimer t(ctx, EVOSPEC_STAGE_LMH, st);
         if (use_tc(a)) {
-            a.gid_keys = (a.KP <= 32 && a.LS == 64) ? 1 : 0;
+            if (a.KP <= 32) { a.gid_keys = 1; a.LS = kTcListLS; }   // buffered lists: ids, stride 128
             CUDA_TRY(launch_lmh_tc(a, st));
             ctx->launches += 1;
             n_cta = segs ? segs->seg_ctas : (a.grid > 0 ? a.grid : lmh_tc_grid());

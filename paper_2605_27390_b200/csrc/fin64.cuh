@@ -4,8 +4,9 @@
 //
 // Inputs per list c (one per LM-head CTA): (m_c, s_c) of the online softmax,
 // cnt_c sorted entries (the GEMV producer) or xcnt_c unsorted ones (the
-// tensor-core producers), 64 value / key slots with -inf pads (keys: subset
-// positions, or vocabulary ids when a.gid_keys). Every
+// tensor-core producers) in the first cnt_c + xcnt_c of LS value / key slots
+// (LS = 64 GEMV, 128 tensor core; keys: subset positions, or vocabulary ids
+// when a.gid_keys; slots past the entries are stale and never used). Every
 // non-empty list holds its maximum m_c (the CTA's best entry for the row is
 // always admitted), so the lists' heads are distinct elements of the row.
 //
@@ -51,7 +52,6 @@ ES_DEV double fin_load_elem(const void* p, int dtype, size_t i) {
 
 constexpr int kF64MaxCta = 320;   // lists per row
 constexpr int kF64Cand = 1024;    // candidate buffer (entries >= th0)
-constexpr int kF64LS = 64;
 constexpr int kF64Threads = 256;
 
 // Massive ties (more than kF64Cand entries >= th0): one warp merges sorted
@@ -59,17 +59,20 @@ constexpr int kF64Threads = 256;
 // (lane i holds entry i). Out of line: never on the common path.
 struct TieOut { float v; int p, cnt; };
 __device__ __noinline__ TieOut fin64_tie_merge(const float* __restrict__ pval, const int32_t* __restrict__ pid, int n_h,
-                                               int r, int c_base, const int* qidx, int nq, float th0, int KP) {
+                                               int r, int c_base, const int* qidx, const int* l_n, int nq, int LS,
+                                               float th0, int KP) {
     const int lane = lane_id();
     float v = -INFINITY;
     int p = 0x7fffffff, cnt = 0;
     float th = -INFINITY;
     int thp = 0x7fffffff;
+    const int per = LS / 32;   // batches per list
 #pragma unroll 1
-    for (int b = 0; b < nq * 2; ++b) {
-        const size_t o = ((size_t)(c_base + qidx[b >> 1]) * n_h + r) * kF64LS + (b & 1) * 32 + lane;
-        float bv = __ldcg(&pval[o]);
-        int bp = __ldcg(&pid[o]);
+    for (int b = 0; b < nq * per; ++b) {
+        const int c = qidx[b / per], sl = (b % per) * 32 + lane;
+        const size_t o = ((size_t)(c_base + c) * n_h + r) * LS + sl;
+        float bv = sl < l_n[c] ? __ldcg(&pval[o]) : -INFINITY;
+        int bp = sl < l_n[c] ? __ldcg(&pid[o]) : 0x7fffffff;
         if (!(bv != -INFINITY && bv >= th0) || (cnt == KP && !before(bv, bp, th, thp))) { bv = -INFINITY; bp = 0x7fffffff; }
         const unsigned m = __ballot_sync(0xffffffffu, bv != -INFINITY);
         if (!m) continue;
@@ -96,6 +99,7 @@ lmh_fin64_kernel(LmhArgs a, int n_cta_arg, int k, float gamma, const float* __re
                  float* __restrict__ row_sumexp, int* flags) {
     constexpr int NW = NT / 32;
     __shared__ float l_m[kF64MaxCta], l_s[kF64MaxCta];
+    __shared__ int l_n[kF64MaxCta];
     __shared__ int qidx[kF64MaxCta];
     __shared__ float cand_v[kF64Cand];
     __shared__ int cand_p[kF64Cand];
@@ -113,7 +117,7 @@ lmh_fin64_kernel(LmhArgs a, int n_cta_arg, int k, float gamma, const float* __re
     const int r = blockIdx.x;
     if (r >= a.n_h) return;   // (grid padding, EVOSPEC_FIN_PAD)
     const int tid = threadIdx.x, lane = lane_id(), warp = warp_id();
-    const int KP = a.KP;
+    const int KP = a.KP, LS = a.LS;
     // ---- ||h||^2 (an input of the LM head only: before the PDL wait)
     const bool h_fast = a.h_dtype == 0 && a.d % 8 == 0;
     double hacc = 0.0;
@@ -165,7 +169,7 @@ lmh_fin64_kernel(LmhArgs a, int n_cta_arg, int k, float gamma, const float* __re
                 s_[i] = __ldcg(&a.part.s[o]);
                 cn_[i] = __ldcg(&a.part.cnt[o]);
                 xc_[i] = __ldcg(&a.part.xcnt[o]);
-                vk_[i] = __ldcg(&a.part.val[o * kF64LS + KP - 1]);
+                vk_[i] = __ldcg(&a.part.val[o * LS + KP - 1]);
             }
         }
 #pragma unroll
@@ -176,6 +180,7 @@ lmh_fin64_kernel(LmhArgs a, int n_cta_arg, int k, float gamma, const float* __re
                 tot += cn_[i] + xc_[i];
                 l_m[c] = s_[i] > 0.0f ? m_[i] : -INFINITY;   // (an empty list has s = 0)
                 l_s[c] = s_[i];
+                l_n[c] = min(cn_[i] + xc_[i], LS);            // entries; slots past them are stale
             }
         }
     }
@@ -232,7 +237,8 @@ lmh_fin64_kernel(LmhArgs a, int n_cta_arg, int k, float gamma, const float* __re
     const size_t row_bytes = (size_t)a.d * (a.w_dtype == 0 ? 2 : 4);
     const bool pf_rows = a.gid_keys && (a.fin_opt & 2) && row_bytes % 16 == 0 && row_bytes <= (1u << 20);
     {
-        const int units = nq * (kF64LS / 4);
+        const int upl = LS / 4;   // float4 units per list
+        const int units = nq * upl;
 #pragma unroll 1
         for (int u0 = tid; u0 < units; u0 += 4 * NT) {
             float4 vv[4];
@@ -241,10 +247,16 @@ lmh_fin64_kernel(LmhArgs a, int n_cta_arg, int k, float gamma, const float* __re
             for (int x = 0; x < 4; ++x) {
                 const int u = u0 + x * NT;
                 vv[x] = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
-                if (u < units) {
-                    const size_t o = ((size_t)(c_base + qidx[u >> 4]) * a.n_h + r) * kF64LS + (u & 15) * 4;
+                const int c = u < units ? qidx[u / upl] : 0, sl = (u % upl) * 4;
+                if (u < units && sl < l_n[c]) {
+                    const size_t o = ((size_t)(c_base + c) * a.n_h + r) * LS + sl;
                     vv[x] = __ldcg((const float4*)&a.part.val[o]);
                     ii[x] = __ldcg((const int4*)&a.part.id[o]);
+                    // slots past the list's entries (stale data) drop out
+                    const int nv = l_n[c] - sl;
+                    if (nv < 4) vv[x].w = -INFINITY;
+                    if (nv < 3) vv[x].z = -INFINITY;
+                    if (nv < 2) vv[x].y = -INFINITY;
                 }
             }
 #pragma unroll
@@ -256,11 +268,6 @@ lmh_fin64_kernel(LmhArgs a, int n_cta_arg, int k, float gamma, const float* __re
                     if (v4[e] != -INFINITY && v4[e] >= th0) {
                         const int o = atomicAdd(&s_cand_n, 1);
                         if (o < kF64Cand) { cand_v[o] = v4[e]; cand_p[o] = p4[e]; }
-                        // a candidate's W row may be re-scored: towards L2 while it is ranked
-                        if (pf_rows && o < 64)
-                            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;"
-                                         :: "l"((const char*)a.W + (size_t)(p4[e] / a.R) * row_bytes), "r"((uint32_t)row_bytes)
-                                         : "memory");
                     }
             }
         }
@@ -269,6 +276,12 @@ lmh_fin64_kernel(LmhArgs a, int n_cta_arg, int k, float gamma, const float* __re
     if (tid == 0) { FIN_TRACE_R(3); FIN_DT_R(3); }
     // ---- 3. the best KP candidates, sorted, then runs
     const int ncand = s_cand_n;
+    if (pf_rows && warp > 0) {   // while warp 0 ranks: the candidates' W rows towards L2 (re-score)
+        for (int i = tid - 32; i < min(ncand, 64); i += NT - 32)
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;"
+                         :: "l"((const char*)a.W + (size_t)(cand_p[i] / a.R) * row_bytes), "r"((uint32_t)row_bytes)
+                         : "memory");
+    }
     if (ncand > 64 && ncand <= kF64Cand) {   // exact ranks by counting
 #pragma unroll 1
         for (int i = tid; i < ncand; i += NT) {
@@ -308,7 +321,7 @@ lmh_fin64_kernel(LmhArgs a, int n_cta_arg, int k, float gamma, const float* __re
             v = lane < cnt ? c_v[lane] : -INFINITY;
             p = lane < cnt ? c_id[lane] : 0x7fffffff;
         } else {
-            const TieOut t = fin64_tie_merge(a.part.val, a.part.id, a.n_h, r, c_base, qidx, nq, th0, KP);
+            const TieOut t = fin64_tie_merge(a.part.val, a.part.id, a.n_h, r, c_base, qidx, l_n, nq, LS, th0, KP);
             v = t.v; p = t.p; cnt = t.cnt;
         }
         if (lane >= cnt) { v = -INFINITY; p = 0x7fffffff; }

@@ -310,7 +310,7 @@ lmh_finalize_kernel(LmhArgs a, int n_cta, int k, float gamma, const float* __res
 void launch_lmh_finalize(const LmhArgs& a, int n_cta, int k, const float* wmax_dev, int32_t* topk_ids,
                          float* topk_vals, float* row_max, float* row_sumexp, int* flags, cudaStream_t st,
                          float gamma) {
-    if (a.KP <= 32 && a.LS == kF64LS && n_cta <= kF64MaxCta) {
+    if (a.KP <= 32 && (a.LS == 64 || a.LS == kTcListLS) && n_cta <= kF64MaxCta) {
         // one CTA per SM while the rows fit one wave (the dynamic allocation is only a
         // placement hint: CTAs sharing an SM measured slower in round 1)
         auto kern = lmh_fin64_kernel<kF64Threads>;

@@ -14,6 +14,7 @@ constexpr int kUnionThreads = 1024;
 constexpr int kTopkPad = 8;         // extra fp32 candidates kept per row for the exact re-score
 constexpr int kMaxK = 64;
 constexpr int kMaxKP = kMaxK + kTopkPad;
+constexpr int kTcListLS = 128;      // list stride of the tensor-core head's candidate lists (k + 8 <= 32)
 constexpr int kMaxCtx = 8192;
 
 // device flag bits (mirror EVOSPEC_FLAG_* in include/evospec.h)
@@ -55,7 +56,10 @@ void launch_union_emit(const uint32_t* bits, int V, int32_t* out_ids, int32_t* o
 // CTA's best candidates sorted by (z desc, id asc); entries [cnt, cnt + xcnt)
 // are unsorted extras from the CTA's last tile that beat entry KP-1 of the
 // sorted list (the last tile is not folded, its survivors are appended).
-constexpr int kMaxSeg = 128;     // segments of one segment-mode LM-head launch
+constexpr int kMaxSeg = 128;
+// EVOSPEC_TRACE: per-CTA counters of rows whose candidate buffer overflowed in the
+// LM head's last tile / a middle tile (profiling aid), after the timestamp slots
+constexpr int kTraceOvf = 2 * 148 * 8 + 16 + 32 + 64 + 2 * 148 + 8;     // segments of one segment-mode LM-head launch
 
 struct LmhPartials {
     float* val;    // [n_cta][n_h][LS]

@@ -608,34 +608,16 @@ ES_DEV void epi_tile_buf(const EpiSmem& e, int n_h, int KP, int tn, int base_pos
     }
 }
 
-// Buffered path store of one row: the row's list is kBuf slots, all "extras"
-// (cnt = 0), the buffer maximum in slot 0 (the finalisation ranks list heads),
-// -inf pads.
-ES_DEV void store_row_buf(const EpiSmem& e, const LmhPartials& P, int cta, int n_h_total, int h_row0, int r) {
+// Buffered path store of one row: the buffer's entries, all "extras" (cnt = 0,
+// xcnt entries), list stride LS; slots past xcnt are never read (no pads).
+ES_DEV void store_row_buf(const EpiSmem& e, const LmhPartials& P, int cta, int n_h_total, int h_row0, int r, int LS) {
     const int lane = lane_id();
     const int cnt = e.st_cnt[r];
     const size_t o = ((size_t)cta * n_h_total + h_row0 + r);
-    float x0 = lane < cnt ? e.st_val[(size_t)r * kBuf + lane] : -INFINITY;
-    float x1 = lane + 32 < cnt ? e.st_val[(size_t)r * kBuf + lane + 32] : -INFINITY;
-    int p0 = lane < cnt ? e.st_pos[(size_t)r * kBuf + lane] : 0;
-    int p1 = lane + 32 < cnt ? e.st_pos[(size_t)r * kBuf + lane + 32] : 0;
-    // slot of the maximum -> 0
-    float mv = fmaxf(x0, x1);
-    int ms = x0 >= x1 ? lane : lane + 32;
-    warp_argbest(mv, ms);   // (value desc, slot asc)
-    if (cnt > 0 && ms != 0) {
-        const float sv = __shfl_sync(0xffffffffu, x0, 0);
-        const int sp = __shfl_sync(0xffffffffu, p0, 0);
-        const float mxv = __shfl_sync(0xffffffffu, ms < 32 ? x0 : x1, ms & 31);
-        const int mxp = __shfl_sync(0xffffffffu, ms < 32 ? p0 : p1, ms & 31);
-        if (lane == 0) { x0 = mxv; p0 = mxp; }
-        if (ms < 32 && lane == ms) { x0 = sv; p0 = sp; }
-        if (ms >= 32 && lane == ms - 32) { x1 = sv; p1 = sp; }
+    for (int i = lane; i < cnt; i += 32) {
+        P.val[o * LS + i] = e.st_val[(size_t)r * kBuf + i];
+        P.id[o * LS + i] = e.st_pos[(size_t)r * kBuf + i];
     }
-    P.val[o * kBuf + lane] = x0;
-    P.val[o * kBuf + lane + 32] = x1;
-    if (lane < cnt) P.id[o * kBuf + lane] = p0;
-    if (lane + 32 < cnt) P.id[o * kBuf + lane + 32] = p1;
     const float ssum = warp_sum(e.st_ls[r * 32 + lane]);
     if (lane == 0) {
         P.cnt[o] = 0;
@@ -646,14 +628,14 @@ ES_DEV void store_row_buf(const EpiSmem& e, const LmhPartials& P, int cta, int n
 }
 
 ES_DEV void epi_store_buf(const EpiSmem& e, const LmhPartials& P, int cta, int n_h_total, int h_row0, int n_h,
-                          int warp, int n_warps) {
-    for (int r = warp; r < n_h; r += n_warps) store_row_buf(e, P, cta, n_h_total, h_row0, r);
+                          int warp, int n_warps, int LS) {
+    for (int r = warp; r < n_h; r += n_warps) store_row_buf(e, P, cta, n_h_total, h_row0, r, LS);
 }
 
 // The CTA's last tile (all warps): fold, then store each row right away (the
 // warp that folds a row writes its partial list -- no block-wide barrier).
 ES_DEV void epi_tile_buf_last_store(const EpiSmem& e, const LmhPartials& P, int cta, int n_h_total, int h_row0,
-                                    int n_h, int KP, int tn, int base_pos, int warp, int n_warps,
+                                    int n_h, int KP, int LS, int tn, int base_pos, int warp, int n_warps,
                                     long long* dtr = nullptr) {
     const int lane = lane_id();
     int it = 0;
@@ -673,7 +655,7 @@ ES_DEV void epi_tile_buf_last_store(const EpiSmem& e, const LmhPartials& P, int 
             fold_buf(e, r, KP, tn, base_pos, v, lm, false, e.scr_v + warp * 32, e.scr_p + warp * 32);
             if (dtr && lane == 0 && it < 5) dtr[it * 4 + 2] = clock64();
         }
-        store_row_buf(e, P, cta, n_h_total, h_row0, r);
+        store_row_buf(e, P, cta, n_h_total, h_row0, r, LS);
         if (dtr && lane == 0 && it < 5) dtr[it * 4 + 3] = clock64();
     }
 }
@@ -709,7 +691,7 @@ ES_DEV float ex2_approx(float x) {   // 2^x, flush-to-zero (ex2 of -inf is +0)
 // measured ~20k cycles per tile from instruction-cache misses alone)
 template <int J>
 ES_DEV void epi_par_phase1(const EpiSmem& e, int n_h, int tn, int base_pos, int tid, int nthr, bool last,
-                           const LmhPartials& P, int cta, int n_h_total, int h_row0, long long* dtr) {
+                           const LmhPartials& P, int cta, int n_h_total, int h_row0, int LS, long long* dtr) {
 #define PTR_(i) do { if (dtr && lane == 0) dtr[i] = clock64(); } while (0)
     const int lane = lane_id();
     for (int base = tid - lane; base < n_h * kParG; base += nthr) {
@@ -821,65 +803,82 @@ ES_DEV void epi_par_phase1(const EpiSmem& e, int n_h, int tn, int base_pos, int 
             }
         }
         PTR_(2);
-        // pass 3 (candidates only): append at the row's shared-memory atomic offset
-        const int nc = __popc(cm);
-        if (act && nc) {
-            int at = n_old + atomicAdd(&e.st_xcnt[r], nc);
-            if (at + nc <= kBuf) {   // else the row overflows: phase 2 folds it (fold_buf)
-                float* bv = e.st_val + (size_t)r * kBuf;
-                int* bp = e.st_pos + (size_t)r * kBuf;
-                while (cm) {
-                    const int i = __ffs(cm) - 1;
-                    cm &= cm - 1u;
-                    const int pl = g * 32 + 4 * (((i >> 2) + rot) & 7) + (i & 3);
-                    bv[at] = trow[pl - g * 32];
-                    bp[at] = tile_key(e, base_pos, pl);
-                    ++at;
-                }
+        // pass 3 (candidates only): offsets within the row's group of kParG adjacent lanes by
+        // two shuffles (no atomics); on the CTA's last tile the candidates go straight into the
+        // row's global list behind the buffer's n_old entries, which the group copies too, and
+        // the list's count is final here -- no second phase unless a row overflows
+        const int nc = act ? __popc(cm) : 0;
+        int pre = nc;   // inclusive prefix over the group
+        {
+            int t = __shfl_up_sync(0xffffffffu, pre, 1);
+            if (g >= 1) pre += t;
+            t = __shfl_up_sync(0xffffffffu, pre, 2);
+            if (g >= 2) pre += t;
+        }
+        const int gtot = __shfl_sync(0xffffffffu, pre, lane | (kParG - 1));
+        const int cap = last ? LS : kBuf;
+        const bool fits = n_old + gtot <= cap;   // else the row overflows: phase 2 folds it (fold_buf)
+        if (act && g == 0) {
+            e.st_xcnt[r] = gtot;
+            if (!fits) e.st_flag[0] = 1;
+            if (last && fits) {
+                const size_t o = (size_t)cta * n_h_total + h_row0 + r;
+                P.cnt[o] = 0;
+                P.xcnt[o] = n_old + gtot;
             }
+        }
+        if (act && fits) {
+            const size_t go = ((size_t)cta * n_h_total + h_row0 + r) * LS;
+            float* bv = last ? P.val + go : e.st_val + (size_t)r * kBuf;
+            int* bp = last ? P.id + go : e.st_pos + (size_t)r * kBuf;
+            int at = n_old + pre - nc;
+            while (cm) {
+                const int i = __ffs(cm) - 1;
+                cm &= cm - 1u;
+                const int pl = g * 32 + 4 * (((i >> 2) + rot) & 7) + (i & 3);
+                bv[at] = trow[pl - g * 32];
+                bp[at] = tile_key(e, base_pos, pl);
+                ++at;
+            }
+            if (last)   // the buffer's entries into slots [0, n_old)
+                for (int i = g; i < n_old; i += kParG) {
+                    bv[i] = e.st_val[(size_t)r * kBuf + i];
+                    bp[i] = e.st_pos[(size_t)r * kBuf + i];
+                }
         }
     }
 }
 
 ES_DEV void epi_par_phase1_any(const EpiSmem& e, int n_h, int KP, int tn, int base_pos, int tid, int nthr,
-                               bool last, const LmhPartials& P, int cta, int n_h_total, int h_row0,
+                               bool last, const LmhPartials& P, int cta, int n_h_total, int h_row0, int LS,
                                long long* dtr = nullptr) {
     // J = ceil(KP / 4) would be exact; three instantiations keep the code small
     // (a larger J is still a valid bound, only a looser one)
-    if (KP <= 12) epi_par_phase1<3>(e, n_h, tn, base_pos, tid, nthr, last, P, cta, n_h_total, h_row0, dtr);
-    else if (KP <= 20) epi_par_phase1<5>(e, n_h, tn, base_pos, tid, nthr, last, P, cta, n_h_total, h_row0, dtr);
-    else epi_par_phase1<8>(e, n_h, tn, base_pos, tid, nthr, last, P, cta, n_h_total, h_row0, dtr);
+    if (KP <= 12) epi_par_phase1<3>(e, n_h, tn, base_pos, tid, nthr, last, P, cta, n_h_total, h_row0, LS, dtr);
+    else if (KP <= 20) epi_par_phase1<5>(e, n_h, tn, base_pos, tid, nthr, last, P, cta, n_h_total, h_row0, LS, dtr);
+    else epi_par_phase1<8>(e, n_h, tn, base_pos, tid, nthr, last, P, cta, n_h_total, h_row0, LS, dtr);
 }
 
 // Phase 2 (after a barrier over the group of nthr threads, named barrier bar):
-//   2a one thread per row commits the appended count (a row that would overflow
-//      keeps its count and raises a block flag);
-//   2b only if flagged: overflowed rows take the warp fold (fold_buf);
+//   2a only if phase 1 raised the block flag: overflowed rows (their candidates
+//      were not written) take the warp fold (fold_buf) -- on the last tile this
+//      is all phase 2 does (phase 1 wrote the lists);
+//   2b between tiles, one thread per row commits the appended count;
 //   2c between tiles, one warp per row compacts a buffer above KP entries to its
-//      best KP (the bound becomes its KP-th entry) -- hidden behind streaming;
-//      on the last tile every thread stores list slots instead (kBuf slots per
-//      row, -inf pads; the list maximum is the row's m, stored in phase 1).
+//      best KP (the bound becomes its KP-th entry) -- hidden behind streaming.
+// On the last tile the global list is the buffer's entries followed by the
+// tile's candidates (stride LS = 128 > kBuf, so a last tile cannot overflow in
+// practice; no pads: the finalisation reads xcnt entries; its maximum is m).
 ES_DEV void epi_par_phase2(const EpiSmem& e, int n_h, int KP, int tn, int base_pos, int tid, int nthr, int bar,
-                           bool last, const LmhPartials& P, int cta, int n_h_total, int h_row0) {
+                           bool last, const LmhPartials& P, int cta, int n_h_total, int h_row0, int LS,
+                           long long* ovf = nullptr) {
     const int lane = lane_id(), warp = tid >> 5, n_warps = nthr >> 5;
-    for (int r = tid; r < n_h; r += nthr) {
-        const int add = e.st_xcnt[r], cnt = e.st_cnt[r];
-        if (cnt + add > kBuf) {
-            e.st_flag[0] = 1;
-        } else {
-            e.st_cnt[r] = cnt + add;
-            e.st_xcnt[r] = 0;
-            if (last) {
-                const size_t o = (size_t)cta * n_h_total + h_row0 + r;
-                P.cnt[o] = 0;
-                P.xcnt[o] = cnt + add;
-            }
-        }
-    }
-    named_bar_sync(bar, nthr);
-    if (e.st_flag[0]) {   // uniform: read by every thread after the barrier
+    const int cap = last ? LS : kBuf;
+    if (e.st_flag[0]) {   // uniform (set in phase 1, read after the caller's barrier): overflowed rows
         for (int r = warp; r < n_h; r += n_warps) {
-            if (e.st_xcnt[r] == 0) continue;
+            const int add = e.st_xcnt[r];
+            if (add == 0 || e.st_cnt[r] + add <= cap) continue;
+            if (ovf && lane == 0) atomicAdd((unsigned long long*)ovf, 1ull);
             float v[kTileJ];
             float lm = -INFINITY;
 #pragma unroll
@@ -888,38 +887,40 @@ ES_DEV void epi_par_phase2(const EpiSmem& e, int n_h, int KP, int tn, int base_p
                 v[j] = p < tn ? e.tile[r * kTile + p] : -INFINITY;
                 lm = fmaxf(lm, v[j]);
             }
+            // (the buffer still holds only the earlier tiles' entries: fold the tile into it)
             fold_buf(e, r, KP, tn, base_pos, v, lm, !last, e.scr_v + warp * 32, e.scr_p + warp * 32);
-            if (lane == 0) {
-                e.st_xcnt[r] = 0;
-                if (last) {
-                    const size_t o = (size_t)cta * n_h_total + h_row0 + r;
-                    P.cnt[o] = 0;
-                    P.xcnt[o] = e.st_cnt[r];
+            if (last) {   // the list: the buffer's entries
+                const size_t o = (size_t)cta * n_h_total + h_row0 + r;
+                const int cnt = e.st_cnt[r];
+                for (int i = lane; i < cnt; i += 32) {
+                    P.val[o * LS + i] = e.st_val[(size_t)r * kBuf + i];
+                    P.id[o * LS + i] = e.st_pos[(size_t)r * kBuf + i];
                 }
+                if (lane == 0) { P.cnt[o] = 0; P.xcnt[o] = cnt; }
             }
+            __syncwarp();
+            if (lane == 0) e.st_xcnt[r] = 0;
             __syncwarp();
         }
         named_bar_sync(bar, nthr);
         if (tid == 0) e.st_flag[0] = 0;
     }
-    if (!last) {
-        for (int r = warp; r < n_h; r += n_warps) {
-            const int cnt = e.st_cnt[r];
-            if (cnt > KP) {
-                float thv;
-                int thp;
-                buf_compact_sorted(e.st_val + (size_t)r * kBuf, e.st_pos + (size_t)r * kBuf, cnt, KP, thv, thp);
-                if (lane == 0) { e.st_cnt[r] = KP; e.st_thv[r] = thv; e.st_thp[r] = thp; }
-                __syncwarp();
-            }
-        }
-    } else {
-        for (int i = tid; i < n_h * kBuf; i += nthr) {
-            const int r = i / kBuf, sl = i - r * kBuf;
-            const size_t o = (size_t)cta * n_h_total + h_row0 + r;
-            const int cnt = e.st_cnt[r];
-            P.val[o * kBuf + sl] = sl < cnt ? e.st_val[i] : -INFINITY;
-            if (sl < cnt) P.id[o * kBuf + sl] = e.st_pos[i];
+    if (last) return;
+    for (int r = tid; r < n_h; r += nthr) {   // commit the appended counts
+        e.st_cnt[r] += e.st_xcnt[r];
+        e.st_xcnt[r] = 0;
+    }
+    named_bar_sync(bar, nthr);
+    // between tiles (the next tile still streams): compact buffers above KP entries to their
+    // best KP, the bound becomes the KP-th entry
+    for (int r = warp; r < n_h; r += n_warps) {
+        const int cnt = e.st_cnt[r];
+        if (cnt > KP) {
+            float thv;
+            int thp;
+            buf_compact_sorted(e.st_val + (size_t)r * kBuf, e.st_pos + (size_t)r * kBuf, cnt, KP, thv, thp);
+            if (lane == 0) { e.st_cnt[r] = KP; e.st_thv[r] = thv; e.st_thp[r] = thp; }
+            __syncwarp();
         }
     }
 }

@@ -93,7 +93,7 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
     }
     unsigned char* smA = base;                                   // [S][128][128 B]
     unsigned char* smB = base + tp.off_b;                        // [S][NP][128 B]
-    const bool buffered = a.KP <= 32 && a.LS == kBuf;   // unsorted candidate buffers (lmh_epilogue.cuh)
+    const bool buffered = a.KP <= 32 && a.LS >= kBuf;   // unsorted candidate buffers (lmh_epilogue.cuh)
     // buffered lists carry vocabulary ids (keys) instead of subset positions (a.gid_keys)
     EpiSmem e = epi_carve(base + tp.off_epi, a.nseg > 0 ? a.seg_rows : n_h, buffered ? kBuf : a.KP, kTcWarps,
                           buffered && a.gid_keys);
@@ -336,9 +336,11 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
             }
             if (last_t) break;                      // the last tile is folded by all warps below
             if (par) {
-                epi_par_phase1_any(e, n_h, a.KP, tn, t0, ew * 32 + lane, nthr, false, a.part, blockIdx.x, a.n_h, h_row0);
+                epi_par_phase1_any(e, n_h, a.KP, tn, t0, ew * 32 + lane, nthr, false, a.part, blockIdx.x, a.n_h, h_row0,
+                                   a.LS);
                 named_bar_sync(1, nthr);
-                epi_par_phase2(e, n_h, a.KP, tn, t0, ew * 32 + lane, nthr, 1, false, a.part, blockIdx.x, a.n_h, h_row0);
+                epi_par_phase2(e, n_h, a.KP, tn, t0, ew * 32 + lane, nthr, 1, false, a.part, blockIdx.x, a.n_h, h_row0,
+                           a.LS, a.trace ? a.trace + kTraceOvf + kNumSMs + blockIdx.x : nullptr);
             } else if (buffered) {
                 epi_tile_buf(e, n_h, a.KP, tn, t0, ew, kTcEpiWarps, true);
             } else {
@@ -360,14 +362,15 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
         if (DTR && warp == kTcEpiWarp0 && lane == 0) DTR[43] = clock64();
         if (par) {
             epi_par_phase1_any(e, n_h, a.KP, tn, t0, threadIdx.x, kTcWarps * 32, true, a.part, blockIdx.x, a.n_h, h_row0,
-                               DTR && warp == kTcEpiWarp0 ? DTR + 50 : nullptr);
+                               a.LS, DTR && warp == kTcEpiWarp0 ? DTR + 50 : nullptr);
             if (DTR && warp == kTcEpiWarp0 && lane == 0) DTR[44] = clock64();
             named_bar_sync(2, kTcWarps * 32);
             if (DTR && warp == kTcEpiWarp0 && lane == 0) DTR[45] = clock64();
-            epi_par_phase2(e, n_h, a.KP, tn, t0, threadIdx.x, kTcWarps * 32, 2, true, a.part, blockIdx.x, a.n_h, h_row0);
+            epi_par_phase2(e, n_h, a.KP, tn, t0, threadIdx.x, kTcWarps * 32, 2, true, a.part, blockIdx.x, a.n_h, h_row0,
+                           a.LS, a.trace ? a.trace + kTraceOvf + blockIdx.x : nullptr);
             if (DTR && warp == kTcEpiWarp0 && lane == 0) DTR[46] = clock64();
         } else if (buffered) {
-            epi_tile_buf_last_store(e, a.part, blockIdx.x, a.n_h, h_row0, n_h, a.KP, tn, t0, warp, kTcWarps,
+            epi_tile_buf_last_store(e, a.part, blockIdx.x, a.n_h, h_row0, n_h, a.KP, a.LS, tn, t0, warp, kTcWarps,
                                     warp == kTcEpiWarp0 ? DTR : nullptr);
         } else {
             epi_tile_last(e, a.part, blockIdx.x, a.n_h, h_row0, n_h, a.KP, a.LS, tn, t0, warp, kTcWarps);
@@ -378,7 +381,7 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
     __syncthreads();
     tc_fence_after();
     if (buffered) {
-        if (n_tiles == 0 || store_after) epi_store_buf(e, a.part, blockIdx.x, a.n_h, h_row0, n_h, warp, kTcWarps);
+        if (n_tiles == 0 || store_after) epi_store_buf(e, a.part, blockIdx.x, a.n_h, h_row0, n_h, warp, kTcWarps, a.LS);
         // (otherwise the last tile's fold stored every row)
     } else {
         epi_store(e, a.part, blockIdx.x, a.n_h, h_row0, n_h, a.KP, a.LS, warp, kTcWarps);
@@ -415,11 +418,12 @@ cudaError_t launch_lmh_tc(const LmhArgs& a, cudaStream_t st) {
     while (c < cols) c <<= 1;
     tp.tmem_cols = c;
     const size_t stage_a = (size_t)kTileM * 128, stage_b = (size_t)tp.n_pad * 128;
-    const size_t epi = epi_smem_bytes(rows, (a.KP <= 32 && a.LS == kBuf) ? kBuf : a.KP, kTcWarps);
+    const size_t epi = epi_smem_bytes(rows, (a.KP <= 32 && a.LS >= kBuf) ? kBuf : a.KP, kTcWarps);
     const size_t fixed = epi + 2 * 128 * 4 + 64 * 8 + 1024 /*align slack*/ + 256;
     const size_t budget = 227 * 1024;
     int S = (int)((budget - fixed) / (stage_a + stage_b));
     S = std::min(S, 8);
+    if (const char* e = getenv("EVOSPEC_TC_SMAX")) S = std::max(2, std::min(S, atoi(e)));   // (experiment)
     if (S < 2) return cudaErrorInvalidConfiguration;
     tp.stages = S;
     tp.off_b = (size_t)S * stage_a;

@@ -1,5 +1,4 @@
-# experiment runner: build, the scan/union parity subset, Bt breakdown, one bench line
 python -c "import paper_2605_27390_b200._build as b; b.build()" > gpurun_out/build.log 2>&1
-timeout 600 python -m pytest tests/test_gpu_scan_ring.py tests/test_gpu_parity.py -q -x -k "scan_ring or llama_full or union_selection or medium" > gpurun_out/exp_tests.log 2>&1; echo "rc=$?" >> gpurun_out/exp_tests.log
-timeout 300 python tools/trace_bt.py > gpurun_out/trace_bt.log 2>&1
-timeout 300 python bench.py --steps 50 --warmup 5 > gpurun_out/bench_exp.log 2>&1
+for v in "60 8" "60 5" "60 4" "16 8" "16 6" "32 8"; do set -- $v
+  EVOSPEC_TC_SMAX=$2 TRACE_NH=$1 TRACE_MODES=steady TRACE_NS=36864 timeout 300 python tools/trace_lmh.py > gpurun_out/trace_nh$1_s$2.log 2>&1
+done

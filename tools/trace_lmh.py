@@ -16,13 +16,14 @@ import torch
 import paper_2605_27390_b200 as es
 import synth
 
-V, d, n_h, k = 128256, 4096, 60, 10
+V, d, k = 128256, 4096, 10
+n_h = int(os.environ.get("TRACE_NH", "60"))
 n_S = int(os.environ.get("TRACE_NS", "36864"))
 W = synth.matrix(0, V, d, 0.02, "bf16")
 H = synth.matrix(1, n_h, d, 1.0, "bf16")
 Wd = torch.from_numpy(W.view(np.int16)).view(torch.bfloat16).cuda()
 Hd = torch.from_numpy(H.view(np.int16)).view(torch.bfloat16).cuda()
-S = np.sort(np.random.default_rng(11).permutation(V)[:n_S]).astype(np.int32)
+S = np.sort(np.random.default_rng(int(os.environ.get("TRACE_SEED", "11"))).permutation(V)[:n_S]).astype(np.int32)
 Sd = torch.from_numpy(S).cuda()
 nd = torch.tensor([n_S], dtype=torch.int32, device="cuda")
 ctx = es.Context(V=V, d=d, w_dtype=torch.bfloat16, h_dtype=torch.bfloat16, max_subset=V, max_rows=n_h, max_k=k,
@@ -60,6 +61,13 @@ for pf in os.environ.get("TRACE_MODES", "flushed,warmcode,steady").split(","):
         col = col[tr[:, j] > 0]
         if col.size:
             print(f"   {n:10s} min {col.min():7.1f}  med {np.median(col):7.1f}  max {col.max():7.1f}")
+    ovf_base = 2 * 148 * 8 + 16 + 32 + 64 + 2 * 148 + 8
+    ovf = ctx.read_trace(ovf_base + 296)[ovf_base:].astype(np.int64)
+    print("   rows overflowing their candidate buffer: last tile", {int(b): int(ovf[b]) for b in np.nonzero(ovf[:148])[0]},
+          "middle tiles", {int(b): int(ovf[148 + b]) for b in np.nonzero(ovf[148:])[0]})
+    fold = rel[:, 6] - rel[:, 5]
+    slow = np.argsort(-fold)[:6]
+    print("   slowest last folds (block: t1_ready -> t1_fold us):", [(int(b), round(fold[b], 1)) for b in slow])
     late = np.argsort(-rel[:, 7])[:8]
     print("   latest CTAs (block: end / prod_done us):", [(int(b), round(rel[b, 7], 1), round(rel[b, 1], 1)) for b in late])
     frel = (fin[:, :7] - t0) / 1e3
