@@ -61,6 +61,7 @@ struct TcParams {
     int last_tile;   // rows of a CTA's short last tile (ranges longer than one tile)
     int dyn_tile;    // two-list mode: rows per second-list tile (EVOSPEC_DYN_TILE)
     int dyn_stride;  // two-list mode: CTA rank stride of the second-list round robin
+    int compact_at;  // between tiles, buffers above this many entries are compacted to their best KP
     int dyn_share;   // two-list mode: first-list share (16ths) of the CTAs expected to take a second-list tile
     size_t off_b, off_epi, off_bar, off_rows;  // smem carve offsets
 };
@@ -292,25 +293,38 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
             }
         }
         if (lane == 0) TC_TRACE(2);
-    } else {
-        // ===== epilogue warps: TMEM lane quadrant = warp % 4; the two
-        // warps of a quadrant split the accumulator columns (16-column chunks)
-        const int ew = warp - kTcEpiWarp0;          // 0..7
-        const int quad = warp & 3;
-        const int half = ew >> 2;
-        const int row = quad * 32 + lane;           // tile row (TMEM lane)
-        const int nthr = kTcEpiWarps * 32;
-        for (int t = 0; has_tile(t); ++t) {
-            int t0, tn;
-            tile_range(t, t0, tn);
+    }
+    // ===== epilogue: the 8 epilogue warps take every tile's accumulator out of TMEM
+    // (lane quadrant = warp % 4; the two warps of a quadrant split the columns) and fold
+    // the middle tiles; the CTA's last tile -- the exposed tail -- is folded by all 13
+    // warps: the producers and the MMA warp join this loop at that tile, so the middle
+    // and last tiles run ONE copy of the fold code (code run once per launch comes in
+    // cold, ~2.6 cycles per instruction, tools/ubench/icache.cu; this copy is warm from
+    // the middle tiles)
+    const bool epi = warp >= kTcEpiWarp0;
+    const int ew = warp - kTcEpiWarp0;          // 0..7 (epilogue warps)
+    const int quad = warp & 3;
+    const int half = ew >> 2;
+    const int row = quad * 32 + lane;           // tile row (TMEM lane)
+    const int nthr = kTcEpiWarps * 32;
+    int t_first = 0;
+    if (!epi) {
+        if (a.list2) ensure2();
+        const int nt = n_tiles1 + nt2;
+        t_first = (nt > 0 && par && !(a.list2 && nt2 == 0)) ? nt - 1 : 0x7fffffff;
+    }
+    for (int t = t_first; t != 0x7fffffff && has_tile(t); ++t) {
+        int t0, tn;
+        tile_range(t, t0, tn);
+        // two-list mode: whether a first-list tile is the CTA's last is known only
+        // after the union ends -- those are folded as middle tiles (overlapping the
+        // wait); a CTA without second-list tiles stores its rows after the loop
+        const bool last_t = a.list2 ? (t >= n_tiles1 && !has_tile(t + 1)) : !has_tile(t + 1);
+        if (epi) {
             const int b = t & 1;
             // the tile's keys (vocabulary ids), loaded while the accumulator fills
             int key = 0x7fffffff;
             if (e.tile_id && half == 0 && row < tn) key = lmh_id_at(a, t0 + row);
-            // two-list mode: whether a first-list tile is the CTA's last is known only
-            // after the union ends -- those are folded as middle tiles (overlapping the
-            // wait); a CTA without second-list tiles stores its rows after the loop
-            const bool last_t = a.list2 ? (t >= n_tiles1 && !has_tile(t + 1)) : !has_tile(t + 1);
             mbar_wait(&tfull[b], (uint32_t)(t >> 1) & 1);
             if (ew == 0 && lane == 0 && t < 2) TC_TRACE(3 + 2 * t);
             if (DTR && ew == 0 && lane == 0 && last_t) DTR[40] = clock64();
@@ -334,42 +348,44 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
                     for (int p = lane; p < tn; p += 32)
                         a.logits_out[(size_t)r * a.n_subset_max + t0 + p] = e.tile[r * kTile + p];
             }
-            if (last_t) break;                      // the last tile is folded by all warps below
-            if (par) {
-                epi_par_phase1_any(e, n_h, a.KP, tn, t0, ew * 32 + lane, nthr, false, a.part, blockIdx.x, a.n_h, h_row0,
-                                   a.LS);
-                named_bar_sync(1, nthr);
-                epi_par_phase2(e, n_h, a.KP, tn, t0, ew * 32 + lane, nthr, 1, false, a.part, blockIdx.x, a.n_h, h_row0,
-                           a.LS, a.trace ? a.trace + kTraceOvf + kNumSMs + blockIdx.x : nullptr);
-            } else if (buffered) {
-                epi_tile_buf(e, n_h, a.KP, tn, t0, ew, kTcEpiWarps, true);
-            } else {
-                epi_tile(e, n_h, a.KP, tn, t0, ew, kTcEpiWarps);
-            }
-            if (ew == 0 && lane == 0 && t < 2) TC_TRACE(4 + 2 * t);
-            named_bar_sync(1, nthr);
+            if (last_t && !par) break;   // folded by all warps after the loop
         }
+        if (par) {
+            // middle tile: the epilogue warps (barrier 1); last tile: all warps (barrier 2)
+            const int ftid = last_t ? (int)threadIdx.x : ew * 32 + lane;
+            const int fn = last_t ? kTcWarps * 32 : nthr;
+            const int bar = last_t ? 2 : 1;
+            if (last_t) named_bar_sync(2, fn);
+            if (DTR && last_t && warp == kTcEpiWarp0 && lane == 0) DTR[43] = clock64();
+            epi_par_phase1_any(e, n_h, a.KP, tn, t0, ftid, fn, last_t, a.part, blockIdx.x, a.n_h, h_row0, a.LS,
+                               DTR && last_t && warp == kTcEpiWarp0 ? DTR + 50 : nullptr);
+            if (DTR && last_t && warp == kTcEpiWarp0 && lane == 0) DTR[44] = clock64();
+            named_bar_sync(bar, fn);
+            epi_par_phase2(e, n_h, a.KP, tn, t0, ftid, fn, bar, last_t, a.part, blockIdx.x, a.n_h, h_row0, a.LS,
+                           a.trace ? a.trace + kTraceOvf + (last_t ? 0 : kNumSMs) + blockIdx.x : nullptr,
+                           tp.compact_at);
+            if (DTR && last_t && warp == kTcEpiWarp0 && lane == 0) DTR[46] = clock64();
+            if (warp == kTcEpiWarp0 && lane == 0 && t < 2) TC_TRACE(4 + 2 * t);
+            if (last_t) break;
+        } else if (buffered) {
+            epi_tile_buf(e, n_h, a.KP, tn, t0, ew, kTcEpiWarps, true);
+            if (ew == 0 && lane == 0 && t < 2) TC_TRACE(4 + 2 * t);
+        } else {
+            epi_tile(e, n_h, a.KP, tn, t0, ew, kTcEpiWarps);
+            if (ew == 0 && lane == 0 && t < 2) TC_TRACE(4 + 2 * t);
+        }
+        named_bar_sync(1, nthr);
     }
-    // the last tile's fold is the exposed tail: producers and the MMA warp are
-    // idle by now, so all 13 warps split its rows
     if (a.list2) ensure2();
     const int n_tiles = n_tiles1 + nt2;
     const bool store_after = a.list2 && nt2 == 0;   // (two-list mode, no second-list tile)
-    if (n_tiles > 0 && !store_after) {
+    if (n_tiles > 0 && !store_after && !par) {
+        // the last tile without the thread-parallel fold (single-tile CTAs, sorted lists):
+        // all 13 warps split its rows
         int t0, tn;
         tile_range(n_tiles - 1, t0, tn);
         named_bar_sync(2, kTcWarps * 32);
-        if (DTR && warp == kTcEpiWarp0 && lane == 0) DTR[43] = clock64();
-        if (par) {
-            epi_par_phase1_any(e, n_h, a.KP, tn, t0, threadIdx.x, kTcWarps * 32, true, a.part, blockIdx.x, a.n_h, h_row0,
-                               a.LS, DTR && warp == kTcEpiWarp0 ? DTR + 50 : nullptr);
-            if (DTR && warp == kTcEpiWarp0 && lane == 0) DTR[44] = clock64();
-            named_bar_sync(2, kTcWarps * 32);
-            if (DTR && warp == kTcEpiWarp0 && lane == 0) DTR[45] = clock64();
-            epi_par_phase2(e, n_h, a.KP, tn, t0, threadIdx.x, kTcWarps * 32, 2, true, a.part, blockIdx.x, a.n_h, h_row0,
-                           a.LS, a.trace ? a.trace + kTraceOvf + blockIdx.x : nullptr);
-            if (DTR && warp == kTcEpiWarp0 && lane == 0) DTR[46] = clock64();
-        } else if (buffered) {
+        if (buffered) {
             epi_tile_buf_last_store(e, a.part, blockIdx.x, a.n_h, h_row0, n_h, a.KP, a.LS, tn, t0, warp, kTcWarps,
                                     warp == kTcEpiWarp0 ? DTR : nullptr);
         } else {
@@ -413,6 +429,7 @@ cudaError_t launch_lmh_tc(const LmhArgs& a, cudaStream_t st) {
     // two; measured r2 with the step timeline: 16/16 277.5 us, 12 282.0, 8 264.8, 6 286.7,
     // 4 286.4 -- below 8 the other CTAs' ranges grow a third tile)
     tp.dyn_share = 8;
+    tp.compact_at = getenv("EVOSPEC_COMPACT_AT") ? atoi(getenv("EVOSPEC_COMPACT_AT")) : 0;
     if (const char* e = getenv("EVOSPEC_DYN_TILE")) tp.dyn_tile = atoi(e) <= 0 ? 0 : std::max(16, std::min(kTileM, atoi(e)));
     uint32_t cols = 2 * tp.n_pad, c = 32;
     while (c < cols) c <<= 1;
