@@ -105,7 +105,7 @@ lmh_fin64_kernel(LmhArgs a, int n_cta_arg, int k, float gamma, const float* __re
     __shared__ int cand_p[kF64Cand];
     __shared__ float c_v[32];
     __shared__ int c_id[32], c_gid[32], need_list[32];
-    __shared__ double c_e[32], res_d[NW * 4];
+    __shared__ double c_e[32], res_d[NW * 8];
     __shared__ double red_d[NW];
     __shared__ float red_th[NW];
     __shared__ int red_tot[NW];
@@ -137,6 +137,8 @@ lmh_fin64_kernel(LmhArgs a, int n_cta_arg, int k, float gamma, const float* __re
             hacc = fma(h, h, hacc);
         }
     }
+    hacc = warp_sum_d(hacc);
+    if (lane == 0) red_d[warp] = hacc;
     if (tid == 0) s_cand_n = 0;
     pdl_wait();
     if (tid == 0) { FIN_TRACE_R(0); FIN_DT_R(0); }
@@ -186,8 +188,7 @@ lmh_fin64_kernel(LmhArgs a, int n_cta_arg, int k, float gamma, const float* __re
     }
     thl = warp_max(thl);
     tot = warp_sum_i(tot);
-    hacc = warp_sum_d(hacc);
-    if (lane == 0) { red_th[warp] = thl; red_tot[warp] = tot; red_d[warp] = hacc; }
+    if (lane == 0) { red_th[warp] = thl; red_tot[warp] = tot; }
     __syncthreads();
     if (tid == 0) { FIN_TRACE_R(1); FIN_DT_R(1); }
     // ---- 2. (warp 0) th0, M, and the lists that can hold entries >= th0 (head >= th0)
@@ -233,34 +234,36 @@ lmh_fin64_kernel(LmhArgs a, int n_cta_arg, int k, float gamma, const float* __re
         S = warp_sum(S);
         if (lane == 0) red_s[warp] = S;
     }
+    if (tid == 0) FIN_DT_R(8);
     // the qualifying lists' entries >= th0 -> candidate buffer (16 float4 per list)
     const size_t row_bytes = (size_t)a.d * (a.w_dtype == 0 ? 2 : 4);
     const bool pf_rows = a.gid_keys && (a.fin_opt & 2) && row_bytes % 16 == 0 && row_bytes <= (1u << 20);
     {
-        const int upl = LS / 4;   // float4 units per list
-        const int units = nq * upl;
+        const int ush = LS == 128 ? 5 : 4;   // float4 units per list: 1 << ush
+        const int units = nq << ush;
 #pragma unroll 1
         for (int u0 = tid; u0 < units; u0 += 4 * NT) {
             float4 vv[4];
             int4 ii[4];
+            int nv[4];   // valid entries in the unit (slots past a list's entries hold stale data)
 #pragma unroll
-            for (int x = 0; x < 4; ++x) {
+            for (int x = 0; x < 4; ++x) {   // all loads in flight before any use
                 const int u = u0 + x * NT;
-                vv[x] = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
-                const int c = u < units ? qidx[u / upl] : 0, sl = (u % upl) * 4;
-                if (u < units && sl < l_n[c]) {
-                    const size_t o = ((size_t)(c_base + c) * a.n_h + r) * LS + sl;
+                const int c = u < units ? qidx[u >> ush] : 0, sl = (u & ((1 << ush) - 1)) * 4;
+                nv[x] = u < units ? l_n[c] - sl : 0;
+                const size_t o = ((size_t)(c_base + c) * a.n_h + r) * LS + sl;
+                if (nv[x] > 0) {
                     vv[x] = __ldcg((const float4*)&a.part.val[o]);
                     ii[x] = __ldcg((const int4*)&a.part.id[o]);
-                    // slots past the list's entries (stale data) drop out
-                    const int nv = l_n[c] - sl;
-                    if (nv < 4) vv[x].w = -INFINITY;
-                    if (nv < 3) vv[x].z = -INFINITY;
-                    if (nv < 2) vv[x].y = -INFINITY;
                 }
             }
+            if (tid == 0 && u0 == 0) FIN_DT_R(9);
 #pragma unroll
             for (int x = 0; x < 4; ++x) {
+                if (nv[x] <= 0) vv[x] = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+                if (nv[x] < 4) vv[x].w = -INFINITY;
+                if (nv[x] < 3) vv[x].z = -INFINITY;
+                if (nv[x] < 2) vv[x].y = -INFINITY;
                 const float v4[4] = {vv[x].x, vv[x].y, vv[x].z, vv[x].w};
                 const int p4[4] = {ii[x].x, ii[x].y, ii[x].z, ii[x].w};
 #pragma unroll
@@ -272,6 +275,7 @@ lmh_fin64_kernel(LmhArgs a, int n_cta_arg, int k, float gamma, const float* __re
             }
         }
     }
+    if (tid == 0) FIN_DT_R(10);
     __syncthreads();
     if (tid == 0) { FIN_TRACE_R(3); FIN_DT_R(3); }
     // ---- 3. the best KP candidates, sorted, then runs
@@ -370,7 +374,7 @@ lmh_fin64_kernel(LmhArgs a, int n_cta_arg, int k, float gamma, const float* __re
     __syncthreads();
     if (tid == 0) { FIN_TRACE_R(4); FIN_DT_R(4); }
     // ---- 4. exact re-score of the flagged entries: bf16 rows block-wide (every thread a
-    //         slice of the columns of up to 4 entries at once: one round trip of loads),
+    //         slice of the columns of up to 8 entries at once: one round trip of loads),
     //         other dtypes one warp per entry
     const int nn = s_nneed;
     if (nn > 0) {
@@ -378,22 +382,24 @@ lmh_fin64_kernel(LmhArgs a, int n_cta_arg, int k, float gamma, const float* __re
             const int nc = a.d / 8;
             const uint4* hp = (const uint4*)((const uint16_t*)a.H + (size_t)r * a.d);
 #pragma unroll 1
-            for (int q0 = 0; q0 < nn; q0 += 4) {
-                const uint4* wp[4];
+            for (int q0 = 0; q0 < nn; q0 += 8) {
+                const uint4* wp[8];
 #pragma unroll
-                for (int u = 0; u < 4; ++u)
+                for (int u = 0; u < 8; ++u)
                     wp[u] = (const uint4*)((const uint16_t*)a.W +
                                            (size_t)(c_gid[need_list[min(q0 + u, nn - 1)]] / a.R) * a.d);
-                double acc[4] = {0.0, 0.0, 0.0, 0.0};
+                double acc[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) acc[u] = 0.0;
 #pragma unroll 2
                 for (int c = tid; c < nc; c += NT) {
-                    uint4 wv[4];
+                    uint4 wv[8];
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) wv[u] = __ldg(&wp[u][c]);
+                    for (int u = 0; u < 8; ++u) wv[u] = q0 + u < nn ? __ldg(&wp[u][c]) : make_uint4(0, 0, 0, 0);
                     float fh[8];
                     unpack_bf16x8(__ldg(&hp[c]), fh);
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) {
+                    for (int u = 0; u < 8; ++u) {
                         float fw[8];
                         unpack_bf16x8(wv[u], fw);
 #pragma unroll
@@ -401,15 +407,15 @@ lmh_fin64_kernel(LmhArgs a, int n_cta_arg, int k, float gamma, const float* __re
                     }
                 }
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
+                for (int u = 0; u < 8; ++u) {
                     const double t = warp_sum_d(acc[u]);
-                    if (lane == 0) res_d[warp * 4 + u] = t;
+                    if (lane == 0) res_d[warp * 8 + u] = t;
                 }
                 __syncthreads();
-                if (tid < 4 && q0 + tid < nn) {
+                if (tid < 8 && q0 + tid < nn) {
                     double t = 0.0;
 #pragma unroll
-                    for (int w = 0; w < NW; ++w) t += res_d[w * 4 + tid];
+                    for (int w = 0; w < NW; ++w) t += res_d[w * 8 + tid];
                     c_e[need_list[q0 + tid]] = t * (double)a.inv_temp;
                 }
                 __syncthreads();
