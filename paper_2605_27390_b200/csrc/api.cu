@@ -314,6 +314,7 @@ evospec_status evospec_create(evospec_ctx** out, const evospec_config* cfg, int 
     A(dalloc(&x->ctx_sel, std::max(1, c.max_ctx))); A(dalloc(&x->ctx_n, 1));
     A(dalloc(&x->part.val, pr * std::max(kMaxKP, kTcListLS))); A(dalloc(&x->part.id, pr * std::max(kMaxKP, kTcListLS)));
     A(dalloc(&x->part.m, pr)); A(dalloc(&x->part.s, pr)); A(dalloc(&x->part.cnt, pr)); A(dalloc(&x->part.xcnt, pr));
+    x->part.cs = cta_cap;
     A(dalloc(&x->flags, 1)); A(dalloc(&x->wmax, 1));
     const size_t trip = (size_t)R * c.max_rows * c.max_k;
     A(dalloc(&x->g_ids, trip)); A(dalloc(&x->g_vals, trip));

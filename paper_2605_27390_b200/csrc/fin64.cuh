@@ -166,11 +166,11 @@ lmh_fin64_kernel(LmhArgs a, int n_cta_arg, int k, float gamma, const float* __re
         for (int i = 0; i < R1; ++i) {
             const int c = tid + i * NT;
             if (c < n_cta) {
-                const size_t o = (size_t)(c_base + c) * a.n_h + r;
-                m_[i] = __ldcg(&a.part.m[o]);
-                s_[i] = __ldcg(&a.part.s[o]);
-                cn_[i] = __ldcg(&a.part.cnt[o]);
-                xc_[i] = __ldcg(&a.part.xcnt[o]);
+                const size_t o = (size_t)(c_base + c) * a.n_h + r, so = part_st(a.part, c_base + c, r);
+                m_[i] = __ldcg(&a.part.m[so]);
+                s_[i] = __ldcg(&a.part.s[so]);
+                cn_[i] = __ldcg(&a.part.cnt[so]);
+                xc_[i] = __ldcg(&a.part.xcnt[so]);
                 vk_[i] = __ldcg(&a.part.val[o * LS + KP - 1]);
             }
         }

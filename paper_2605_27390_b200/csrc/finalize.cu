@@ -65,7 +65,7 @@ lmh_finalize_kernel(LmhArgs a, int n_cta, int k, float gamma, const float* __res
     // 1. softmax state; ||h_r||^2 (warp 7) for delta
     float M = -INFINITY;
     for (int c = threadIdx.x; c < n_cta; c += blockDim.x) {
-        size_t o = (size_t)c * a.n_h + r;
+        const size_t o = part_st(a.part, c, r);
         if (a.part.s[o] > 0.0f) M = fmaxf(M, a.part.m[o]);
         head[c] = 0;
     }
@@ -102,7 +102,7 @@ lmh_finalize_kernel(LmhArgs a, int n_cta, int k, float gamma, const float* __res
     float S = 0.0f;
     int tot = 0;
     for (int c = threadIdx.x; c < n_cta; c += blockDim.x) {
-        size_t o = (size_t)c * a.n_h + r;
+        const size_t o = part_st(a.part, c, r);
         float sc = a.part.s[o];
         if (sc > 0.0f) S += sc * expf(a.part.m[o] - M);
         tot += a.part.cnt[o];
@@ -112,7 +112,7 @@ lmh_finalize_kernel(LmhArgs a, int n_cta, int k, float gamma, const float* __res
     if (lane == 0) { red_s[warp] = S; red_t[warp] = tot; }
     // stage every CTA's sorted list in shared memory: flat, 4 independent loads
     // in flight per thread (entries past a list's count are -inf / -1)
-    for (int c = threadIdx.x; c < n_cta; c += blockDim.x) l_cnt[c] = a.part.cnt[(size_t)c * a.n_h + r];
+    for (int c = threadIdx.x; c < n_cta; c += blockDim.x) l_cnt[c] = a.part.cnt[part_st(a.part, c, r)];
     for (int f0 = 0; f0 < n_cta * KP; f0 += 4 * blockDim.x) {
         float vv[4];
         int32_t ii[4];

@@ -63,12 +63,15 @@ constexpr int kTraceOvf = 2 * 148 * 8 + 16 + 32 + 64 + 2 * 148 + 8;     // segme
 
 struct LmhPartials {
     float* val;    // [n_cta][n_h][LS]
-    int32_t* id;   // [n_cta][n_h][LS] subset positions (sorted subset: position order = id order)
-    float* m;      // [n_cta][n_h]
-    float* s;      // [n_cta][n_h]
-    int* cnt;      // [n_cta][n_h] sorted entries
-    int* xcnt;     // [n_cta][n_h] unsorted extras
+    int32_t* id;   // [n_cta][n_h][LS] keys: subset positions (sorted subset: position order = id order) or ids
+    float* m;      // [n_h][cs]  (row-major by H row: a row's states are contiguous for the finalisation)
+    float* s;      // [n_h][cs]
+    int* cnt;      // [n_h][cs] sorted entries
+    int* xcnt;     // [n_h][cs] unsorted extras
+    int cs;        // CTA stride of the state arrays (the context's CTA capacity)
 };
+// index of CTA cta's softmax / count state for H row `row`
+__host__ __device__ inline size_t part_st(const LmhPartials& P, int cta, int row) { return (size_t)row * P.cs + cta; }
 struct LmhArgs {
     const void* W; int64_t n_w_rows; int d; int w_dtype;
     const void* H; int n_h; int h_dtype;

@@ -340,10 +340,10 @@ ES_DEV void epi_store(const EpiSmem& e, const LmhPartials& P, int cta, int n_h_t
             for (int i = cnt + e.st_xcnt[r] + lane_id(); i < LS; i += 32) P.val[o * LS + i] = -INFINITY;
         const float ssum = warp_sum(e.st_ls[r * 32 + lane_id()]);
         if (lane_id() == 0) {
-            P.cnt[o] = cnt;
-            P.xcnt[o] = e.st_xcnt[r];
-            P.m[o] = e.st_m[r];
-            P.s[o] = ssum;
+            P.cnt[part_st(P, cta, h_row0 + r)] = cnt;
+            P.xcnt[part_st(P, cta, h_row0 + r)] = e.st_xcnt[r];
+            P.m[part_st(P, cta, h_row0 + r)] = e.st_m[r];
+            P.s[part_st(P, cta, h_row0 + r)] = ssum;
         }
     }
 }
@@ -620,10 +620,10 @@ ES_DEV void store_row_buf(const EpiSmem& e, const LmhPartials& P, int cta, int n
     }
     const float ssum = warp_sum(e.st_ls[r * 32 + lane]);
     if (lane == 0) {
-        P.cnt[o] = 0;
-        P.xcnt[o] = cnt;
-        P.m[o] = e.st_m[r];
-        P.s[o] = ssum;
+        P.cnt[part_st(P, cta, h_row0 + r)] = 0;
+        P.xcnt[part_st(P, cta, h_row0 + r)] = cnt;
+        P.m[part_st(P, cta, h_row0 + r)] = e.st_m[r];
+        P.s[part_st(P, cta, h_row0 + r)] = ssum;
     }
 }
 
@@ -798,8 +798,8 @@ ES_DEV void epi_par_phase1(const EpiSmem& e, int n_h, int tn, int base_pos, int 
             tot += __shfl_xor_sync(0xffffffffu, tot, 2);
             if (act && g == 0) {
                 const size_t o = (size_t)cta * n_h_total + h_row0 + r;
-                P.m[o] = m_new;
-                P.s[o] = tot;
+                P.m[part_st(P, cta, h_row0 + r)] = m_new;
+                P.s[part_st(P, cta, h_row0 + r)] = tot;
             }
         }
         PTR_(2);
@@ -823,8 +823,8 @@ ES_DEV void epi_par_phase1(const EpiSmem& e, int n_h, int tn, int base_pos, int 
             if (!fits) e.st_flag[0] = 1;
             if (last && fits) {
                 const size_t o = (size_t)cta * n_h_total + h_row0 + r;
-                P.cnt[o] = 0;
-                P.xcnt[o] = n_old + gtot;
+                P.cnt[part_st(P, cta, h_row0 + r)] = 0;
+                P.xcnt[part_st(P, cta, h_row0 + r)] = n_old + gtot;
             }
         }
         if (act && fits) {
@@ -896,7 +896,7 @@ ES_DEV void epi_par_phase2(const EpiSmem& e, int n_h, int KP, int tn, int base_p
                     P.val[o * LS + i] = e.st_val[(size_t)r * kBuf + i];
                     P.id[o * LS + i] = e.st_pos[(size_t)r * kBuf + i];
                 }
-                if (lane == 0) { P.cnt[o] = 0; P.xcnt[o] = cnt; }
+                if (lane == 0) { P.cnt[part_st(P, cta, h_row0 + r)] = 0; P.xcnt[part_st(P, cta, h_row0 + r)] = cnt; }
             }
             __syncwarp();
             if (lane == 0) e.st_xcnt[r] = 0;

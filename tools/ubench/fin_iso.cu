@@ -22,7 +22,7 @@ int main(int argc, char** argv) {
     std::vector<int> id((size_t)n_cta * n_h * LS, 0), cnt(n_cta * n_h, 0), xcnt(n_cta * n_h);
     for (int c = 0; c < n_cta; ++c)
         for (int r = 0; r < n_h; ++r) {
-            const size_t o = (size_t)c * n_h + r;
+            const size_t o = (size_t)c * n_h + r, so = (size_t)r * n_cta + c;   // lists [cta][row], state [row][cta]
             // the list: the CTA's 249 values' best ~25 (a gaussian sample, sorted desc)
             std::vector<float> x(249);
             for (auto& v : x) v = nd(rng);
@@ -31,10 +31,10 @@ int main(int argc, char** argv) {
             for (int i = 0; i < nc; ++i) { val[o * LS + i] = x[i]; id[o * LS + i] = (int)(rng() % V); }
             std::swap(val[o * LS], val[o * LS + nc / 2]);   // unsorted buffer, max somewhere
             std::swap(id[o * LS], id[o * LS + nc / 2]);
-            m[o] = x[0];
+            m[so] = x[0];
             double ss = 0; for (float v : x) ss += std::exp(v - x[0]);
-            s[o] = (float)ss;
-            xcnt[o] = nc;
+            s[so] = (float)ss;
+            xcnt[so] = nc;
         }
     LmhArgs a{};
     float *dv, *dm, *ds, *wmax; int *di, *dc, *dx, *flags;
@@ -54,7 +54,7 @@ int main(int argc, char** argv) {
     int32_t* ids; float *vals, *rm, *rs; cudaMalloc(&ids, n_h * k * 4); cudaMalloc(&vals, n_h * k * 4);
     cudaMalloc(&rm, n_h * 4); cudaMalloc(&rs, n_h * 4);
     a.W = W; a.d = d; a.w_dtype = 0; a.H = H; a.n_h = n_h; a.h_dtype = 0; a.R = 1; a.KP = KP; a.LS = LS;
-    a.inv_temp = 1.0f; a.part = LmhPartials{dv, di, dm, ds, dc, dx}; a.fin_opt = 15; a.gid_keys = 1;
+    a.inv_temp = 1.0f; a.part = LmhPartials{dv, di, dm, ds, dc, dx, n_cta}; a.fin_opt = 15; a.gid_keys = 1;
     a.trace = trace;
     // gamma: make runs frequent (~ the LM head's 2^-16 envelope scaled to these values)
     const float gamma = argc > 1 ? atof(argv[1]) : 1.0f / 65536.0f;
