@@ -140,6 +140,7 @@ lmh_fin64_kernel(LmhArgs a, int n_cta_arg, int k, float gamma, const float* __re
     hacc = warp_sum_d(hacc);
     if (lane == 0) red_d[warp] = hacc;
     if (tid == 0) s_cand_n = 0;
+    const float wmax = warp == 0 ? __ldg(wmax_dev) : 0.0f;   // (an input: before the wait; warp 0 uses it)
     pdl_wait();
     if (tid == 0) { FIN_TRACE_R(0); FIN_DT_R(0); }
     // the row's lists: CTAs [c_base, c_base + n_cta) (segment mode: its segment's CTAs)
@@ -280,7 +281,10 @@ lmh_fin64_kernel(LmhArgs a, int n_cta_arg, int k, float gamma, const float* __re
     if (tid == 0) { FIN_TRACE_R(3); FIN_DT_R(3); }
     // ---- 3. the best KP candidates, sorted, then runs
     const int ncand = s_cand_n;
-    if (pf_rows && warp > 0) {   // while warp 0 ranks: the candidates' W rows towards L2 (re-score)
+    // while warp 0 ranks: the candidates' W rows towards L2 for the re-score (measured: the
+    // re-score's loads take 5.0k cycles with this, 5.2k with the kept KP prefetched after
+    // the sort, 6.7k without a prefetch)
+    if (pf_rows && warp > 0) {
         for (int i = tid - 32; i < min(ncand, 64); i += NT - 32)
             asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;"
                          :: "l"((const char*)a.W + (size_t)(cand_p[i] / a.R) * row_bytes), "r"((uint32_t)row_bytes)
@@ -328,9 +332,10 @@ lmh_fin64_kernel(LmhArgs a, int n_cta_arg, int k, float gamma, const float* __re
             const TieOut t = fin64_tie_merge(a.part.val, a.part.id, a.n_h, r, c_base, qidx, l_n, nq, LS, th0, KP);
             v = t.v; p = t.p; cnt = t.cnt;
         }
+        if (lane == 0) FIN_DT_R(11);
         if (lane >= cnt) { v = -INFINITY; p = 0x7fffffff; }
         const int gid = lane < cnt ? (a.gid_keys ? p : lmh_id_at(a, p)) : -1;
-        if ((a.fin_opt & 2) && !a.gid_keys && lane < cnt) {   // the re-score reads a few of these rows: towards L2 now
+        if ((a.fin_opt & 2) && !a.gid_keys && lane < cnt) {   // (position keys) the re-score's rows towards L2 now
             const size_t rb = (size_t)a.d * (a.w_dtype == 0 ? 2 : 4);
             if (rb % 16 == 0 && rb <= (1u << 20)) {
                 const char* wr = (const char*)a.W + (size_t)(gid / a.R) * rb;
@@ -343,7 +348,7 @@ lmh_fin64_kernel(LmhArgs a, int n_cta_arg, int k, float gamma, const float* __re
         double hn = 0.0;
 #pragma unroll
         for (int w = 0; w < NW; ++w) hn += red_d[w];
-        const double delta = (double)gamma * sqrt(hn) * (double)__ldg(wmax_dev) * (double)a.inv_temp;
+        const double delta = (double)gamma * sqrt(hn) * (double)wmax * (double)a.inv_temp;
         const float nv = __shfl_down_sync(0xffffffffu, v, 1);
         const bool close = lane + 1 < cnt && (double)v - (double)nv <= 2.0 * delta + 2.4e-7 * fabs((double)v);
         const unsigned cm = __ballot_sync(0xffffffffu, close);   // bit i: entries i and i+1 in one run
@@ -391,27 +396,41 @@ lmh_fin64_kernel(LmhArgs a, int n_cta_arg, int k, float gamma, const float* __re
                 double acc[8];
 #pragma unroll
                 for (int u = 0; u < 8; ++u) acc[u] = 0.0;
-#pragma unroll 2
-                for (int c = tid; c < nc; c += NT) {
-                    uint4 wv[8];
+#pragma unroll 1
+                for (int c0 = tid; c0 < nc; c0 += 2 * NT) {   // two column chunks, all 18 loads in flight
+                    uint4 wv[2][8], hv2[2];
 #pragma unroll
-                    for (int u = 0; u < 8; ++u) wv[u] = q0 + u < nn ? __ldg(&wp[u][c]) : make_uint4(0, 0, 0, 0);
-                    float fh[8];
-                    unpack_bf16x8(__ldg(&hp[c]), fh);
+                    for (int x = 0; x < 2; ++x) {
+                        const int c = c0 + x * NT;
+                        hv2[x] = c < nc ? __ldg(&hp[c]) : make_uint4(0, 0, 0, 0);
 #pragma unroll
-                    for (int u = 0; u < 8; ++u) {
-                        float fw[8];
-                        unpack_bf16x8(wv[u], fw);
+                        for (int u = 0; u < 8; ++u)
+                            wv[x][u] = (c < nc && q0 + u < nn) ? __ldg(&wp[u][c]) : make_uint4(0, 0, 0, 0);
+                    }
 #pragma unroll
-                        for (int j = 0; j < 8; ++j) acc[u] = fma((double)fw[j], (double)fh[j], acc[u]);
+                    for (int x = 0; x < 2; ++x) {
+                        float fh[8];
+                        unpack_bf16x8(hv2[x], fh);
+                        double dh[8];   // (fp32 -> fp64 conversions: H once per chunk)
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) dh[j] = (double)fh[j];
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) {
+                            float fw[8];
+                            unpack_bf16x8(wv[x][u], fw);
+#pragma unroll
+                            for (int j = 0; j < 8; ++j) acc[u] = fma((double)fw[j], dh[j], acc[u]);
+                        }
                     }
                 }
+                if (tid == 0 && q0 == 0) FIN_DT_R(13);
 #pragma unroll
                 for (int u = 0; u < 8; ++u) {
                     const double t = warp_sum_d(acc[u]);
                     if (lane == 0) res_d[warp * 8 + u] = t;
                 }
                 __syncthreads();
+                if (tid == 0 && q0 == 0) FIN_DT_R(14);
                 if (tid < 8 && q0 + tid < nn) {
                     double t = 0.0;
 #pragma unroll
