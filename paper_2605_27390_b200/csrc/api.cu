@@ -757,7 +757,8 @@ static evospec_status lmh_impl(evospec_ctx* ctx, const void* W, int64_t n_w_rows
                                float* row_sumexp, float* logits_out, void* stream, int32_t* m_ids, float* m_vals,
                                float* m_lse, float* m_probs, const int32_t* seg = nullptr,
                                const LmhSegs* segs = nullptr, const int32_t* list2 = nullptr,
-                               const int32_t* n_list2_dev = nullptr, int32_t n_list2_max = 0) {
+                               const int32_t* n_list2_dev = nullptr, int32_t n_list2_max = 0,
+                               int part_cta0 = 0, bool skip_fin = false, const int* fin_a = nullptr) {
     if (!ctx || !W || !H || !subset || (!n_subset_dev && !seg && !list2) || !topk_ids || !topk_vals || !row_max ||
         !row_sumexp)
         return fail(EVOSPEC_EINPUT, "subset_logits_topk: null argument");
@@ -784,7 +785,9 @@ static evospec_status lmh_impl(evospec_ctx* ctx, const void* W, int64_t n_w_rows
     a.R = c.n_shards; a.KP = k + kTopkPad; a.LS = a.KP <= 32 ? 64 : a.KP; a.inv_temp = inv_temp;
     // a triple that is merged with other parts (vocabulary shards, or the static /
     // dynamic parts of the ragged head) carries exact top-k values
-    a.exact_vals = (c.n_shards > 1 || segs || seg) ? 1 : 0;
+    a.exact_vals = (c.n_shards > 1 || ((segs || seg) && !fin_a)) ? 1 : 0;
+    a.part_cta0 = part_cta0;
+    if (fin_a) { a.fin_a_rows = fin_a[0]; a.fin_a_ctas = fin_a[1]; a.fin_a_cta0 = fin_a[2]; }
     a.logits_out = logits_out;
     a.part = ctx->part;
     a.m_ids = m_ids; a.m_vals = m_vals; a.m_lse = m_lse; a.m_probs = m_probs;
@@ -831,6 +834,7 @@ static evospec_status lmh_impl(evospec_ctx* ctx, const void* W, int64_t n_w_rows
             }
         }
     }
+    if (skip_fin) return EVOSPEC_OK;   // (the ragged head's static block: finalised with its dynamic lists)
     {
         StageTimer t(ctx, EVOSPEC_STAGE_FINALIZE, st);
         launch_lmh_finalize(a, n_cta, k, ctx->wmax, topk_ids, topk_vals, row_max, row_sumexp, ctx->flags, st,
@@ -905,6 +909,11 @@ evospec_status evospec_subset_logits_topk_ragged(evospec_ctx* ctx, const void* W
     const bool seg_ok = lmh_tc_supported(probe) && probe.KP <= 32;
     int max_rows_seq = 0;
     for (int b = 0; b < B; ++b) max_rows_seq = std::max(max_rows_seq, h_offsets[b + 1] - h_offsets[b]);
+    // both blocks in segment mode: one finalisation per row reads the row's static-group
+    // lists and its sequence's dynamic lists together (no exact re-score of every top-k
+    // entry for a merge, no merge launch); the dynamic launch's lists sit behind the static's
+    const bool dyn_seg = seg_ok && B <= std::min(kMaxSeg, lmh_tc_grid()) && max_rows_seq <= kTcMaxRows;
+    int fin_a[3] = {0, 0, 0};
     if (seg_ok) {
         // static block: one launch, row groups of <= 128 as segments over the same
         // static range (their CTAs read the same W rows at about the same time)
@@ -918,8 +927,10 @@ evospec_status evospec_subset_logits_topk_ragged(evospec_ctx* ctx, const void* W
         const LmhSegs ss{ns, lmh_tc_grid() / ns, per, nullptr, sh, nullptr};
         evospec_status rc = lmh_impl(ctx, W, n_w_rows, H, n_rows, static_ids ? static_ids : dyn_ids, ctx->rg_seg + 1,
                                      n_static, k, inv_temp, ctx->rg_ids, ctx->rg_vals, ctx->rg_m, ctx->rg_s, nullptr,
-                                     stream, nullptr, nullptr, nullptr, nullptr, nullptr, &ss);
+                                     stream, nullptr, nullptr, nullptr, nullptr, nullptr, &ss, nullptr, nullptr, 0,
+                                     0, dyn_seg);
         if (rc != EVOSPEC_OK) return rc;
+        fin_a[0] = per; fin_a[1] = ss.seg_ctas; fin_a[2] = 0;
     } else {
         for (int r0 = 0; r0 < n_rows; r0 += kTcMaxRows) {
             const int g = std::min(kTcMaxRows, n_rows - r0);
@@ -931,17 +942,16 @@ evospec_status evospec_subset_logits_topk_ragged(evospec_ctx* ctx, const void* W
             if (rc != EVOSPEC_OK) return rc;
         }
     }
-    if (seg_ok && B <= std::min(kMaxSeg, lmh_tc_grid()) && max_rows_seq <= kTcMaxRows) {
+    if (dyn_seg) {
         // dynamic blocks: one launch, sequence b = segment b (its rows, its dyn_b)
         // CTAs in proportion to each sequence's dyn_b length (device sizes -> device schedule)
         launch_seg_schedule(dyn_offsets, h_offsets, B, lmh_tc_grid(), ctx->rg_segcta, st);
         ctx->launches += 1;
         LAUNCH_CHECK("seg_schedule");
         const LmhSegs ds{B, lmh_tc_grid() / B, std::max(1, max_rows_seq), dyn_offsets, h_offsets, ctx->rg_segcta};
-        evospec_status rc = lmh_impl(ctx, W, n_w_rows, H, n_rows, dyn_ids, nullptr, max_dyn, k, inv_temp, ids1, vals1,
-                                     ctx->rg_m + n_rows, ctx->rg_s + n_rows, nullptr, stream, nullptr, nullptr,
-                                     nullptr, nullptr, ctx->rg_seg, &ds);
-        if (rc != EVOSPEC_OK) return rc;
+        return lmh_impl(ctx, W, n_w_rows, H, n_rows, dyn_ids, nullptr, max_dyn, k, inv_temp, topk_ids, topk_vals,
+                        row_max, row_sumexp, nullptr, stream, nullptr, nullptr, nullptr, nullptr, ctx->rg_seg, &ds,
+                        nullptr, nullptr, 0, lmh_tc_grid(), false, fin_a);
     } else {
         for (int b = 0; b < B; ++b) {
             const int r0 = h_offsets[b], g = h_offsets[b + 1] - r0;

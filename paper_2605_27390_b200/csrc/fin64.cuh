@@ -59,7 +59,7 @@ constexpr int kF64Threads = 256;
 // (lane i holds entry i). Out of line: never on the common path.
 struct TieOut { float v; int p, cnt; };
 __device__ __noinline__ TieOut fin64_tie_merge(const float* __restrict__ pval, const int32_t* __restrict__ pid, int n_h,
-                                               int r, int c_base, const int* qidx, const int* l_n, int nq, int LS,
+                                               int r, int cA0, int nA, int c_base, const int* qidx, const int* l_n, int nq, int LS,
                                                float th0, int KP) {
     const int lane = lane_id();
     float v = -INFINITY;
@@ -70,7 +70,8 @@ __device__ __noinline__ TieOut fin64_tie_merge(const float* __restrict__ pval, c
 #pragma unroll 1
     for (int b = 0; b < nq * per; ++b) {
         const int c = qidx[b / per], sl = (b % per) * 32 + lane;
-        const size_t o = ((size_t)(c_base + c) * n_h + r) * LS + sl;
+        const int cta = c < nA ? cA0 + c : c_base + (c - nA);
+        const size_t o = ((size_t)cta * n_h + r) * LS + sl;
         float bv = sl < l_n[c] ? __ldcg(&pval[o]) : -INFINITY;
         int bp = sl < l_n[c] ? __ldcg(&pid[o]) : 0x7fffffff;
         if (!(bv != -INFINITY && bv >= th0) || (cnt == KP && !before(bv, bp, th, thp))) { bv = -INFINITY; bp = 0x7fffffff; }
@@ -143,19 +144,25 @@ lmh_fin64_kernel(LmhArgs a, int n_cta_arg, int k, float gamma, const float* __re
     const float wmax = warp == 0 ? __ldg(wmax_dev) : 0.0f;   // (an input: before the wait; warp 0 uses it)
     pdl_wait();
     if (tid == 0) { FIN_TRACE_R(0); FIN_DT_R(0); }
-    // the row's lists: CTAs [c_base, c_base + n_cta) (segment mode: its segment's CTAs)
-    int n_cta = n_cta_arg, c_base = 0;
+    // the row's lists: CTAs [c_base, c_base + n_cta) (segment mode: its segment's CTAs,
+    // behind part_cta0), and for the ragged head also its static row group's nA lists
+    int n_cta = n_cta_arg, c_base = a.part_cta0;
     if (a.nseg > 0) {
         int b = 0;
         while (b + 1 < a.nseg && a.seg_h[b + 1] <= r) ++b;
         if (a.seg_cta) {
-            c_base = a.seg_cta[b];
-            n_cta = a.seg_cta[b + 1] - c_base;
+            c_base = a.part_cta0 + a.seg_cta[b];
+            n_cta = a.seg_cta[b + 1] - a.seg_cta[b];
         } else {
-            c_base = b * a.seg_ctas;
+            c_base = a.part_cta0 + b * a.seg_ctas;
             n_cta = a.seg_ctas;
         }
     }
+    const int nA = a.fin_a_rows > 0 ? a.fin_a_ctas : 0;
+    const int cA0 = a.fin_a_rows > 0 ? a.fin_a_cta0 + (r / a.fin_a_rows) * a.fin_a_ctas : 0;
+    n_cta += nA;
+    // list ordinal c -> list index: the static group's lists first, then the launch's own
+    auto cta_of = [&](int c) -> int { return c < nA ? cA0 + c : c_base + (c - nA); };
     // ---- 1. softmax states, counts, sorted lists' entry KP-1 (all loads in flight at once)
     float thl = -INFINITY;
     int tot = 0;
@@ -167,7 +174,7 @@ lmh_fin64_kernel(LmhArgs a, int n_cta_arg, int k, float gamma, const float* __re
         for (int i = 0; i < R1; ++i) {
             const int c = tid + i * NT;
             if (c < n_cta) {
-                const size_t o = (size_t)(c_base + c) * a.n_h + r, so = part_st(a.part, c_base + c, r);
+                const size_t o = (size_t)cta_of(c) * a.n_h + r, so = part_st(a.part, cta_of(c), r);
                 m_[i] = __ldcg(&a.part.m[so]);
                 s_[i] = __ldcg(&a.part.s[so]);
                 cn_[i] = __ldcg(&a.part.cnt[so]);
@@ -252,7 +259,7 @@ lmh_fin64_kernel(LmhArgs a, int n_cta_arg, int k, float gamma, const float* __re
                 const int u = u0 + x * NT;
                 const int c = u < units ? qidx[u >> ush] : 0, sl = (u & ((1 << ush) - 1)) * 4;
                 nv[x] = u < units ? l_n[c] - sl : 0;
-                const size_t o = ((size_t)(c_base + c) * a.n_h + r) * LS + sl;
+                const size_t o = ((size_t)cta_of(c) * a.n_h + r) * LS + sl;
                 if (nv[x] > 0) {
                     vv[x] = __ldcg((const float4*)&a.part.val[o]);
                     ii[x] = __ldcg((const int4*)&a.part.id[o]);
@@ -329,7 +336,7 @@ lmh_fin64_kernel(LmhArgs a, int n_cta_arg, int k, float gamma, const float* __re
             v = lane < cnt ? c_v[lane] : -INFINITY;
             p = lane < cnt ? c_id[lane] : 0x7fffffff;
         } else {
-            const TieOut t = fin64_tie_merge(a.part.val, a.part.id, a.n_h, r, c_base, qidx, l_n, nq, LS, th0, KP);
+            const TieOut t = fin64_tie_merge(a.part.val, a.part.id, a.n_h, r, cA0, nA, c_base, qidx, l_n, nq, LS, th0, KP);
             v = t.v; p = t.p; cnt = t.cnt;
         }
         if (lane == 0) FIN_DT_R(11);

@@ -101,6 +101,11 @@ struct LmhArgs {
     // before griddepcontrol.wait. grid: CTAs of the launch (0 = all SMs)
     const int32_t* list2; const int32_t* n_list2_dev; int n_list2_max; int n1;
     int grid;
+    int part_cta0;   // list / state index of this launch's CTA 0 (a second launch writes behind the first)
+    // the finalisation of the ragged head reads two list ranges per row: its launch's segment
+    // (the dynamic lists) and, when fin_a_rows > 0, static row group r / fin_a_rows, whose
+    // fin_a_ctas lists start at fin_a_cta0 + group * fin_a_ctas
+    int fin_a_rows, fin_a_ctas, fin_a_cta0;
     int gid_keys;   // partial lists carry vocabulary ids, not subset positions (tensor-core
                     // kernel, buffered lists; ties then order by id in two-list mode too)
 };

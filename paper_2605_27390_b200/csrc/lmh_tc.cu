@@ -105,6 +105,7 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
     uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
 
     const int warp = warp_id(), lane = lane_id();
+    const int pcta = a.part_cta0 + (int)blockIdx.x;   // this CTA's partial list / state index
     // clock64 details of CTA 0's last tile (EVOSPEC_TRACE; profiling aid)
     long long* const DTR = a.trace && blockIdx.x == 0 ? a.trace + 2 * kNumSMs * 8 + 48 : nullptr;
     if (DTR && threadIdx.x == 0) { DTR[48] = 0; DTR[49] = 0; }
@@ -357,11 +358,11 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
             const int bar = last_t ? 2 : 1;
             if (last_t) named_bar_sync(2, fn);
             if (DTR && last_t && warp == kTcEpiWarp0 && lane == 0) DTR[43] = clock64();
-            epi_par_phase1_any(e, n_h, a.KP, tn, t0, ftid, fn, last_t, a.part, blockIdx.x, a.n_h, h_row0, a.LS,
+            epi_par_phase1_any(e, n_h, a.KP, tn, t0, ftid, fn, last_t, a.part, pcta, a.n_h, h_row0, a.LS,
                                DTR && last_t && warp == kTcEpiWarp0 ? DTR + 50 : nullptr);
             if (DTR && last_t && warp == kTcEpiWarp0 && lane == 0) DTR[44] = clock64();
             named_bar_sync(bar, fn);
-            epi_par_phase2(e, n_h, a.KP, tn, t0, ftid, fn, bar, last_t, a.part, blockIdx.x, a.n_h, h_row0, a.LS,
+            epi_par_phase2(e, n_h, a.KP, tn, t0, ftid, fn, bar, last_t, a.part, pcta, a.n_h, h_row0, a.LS,
                            a.trace ? a.trace + kTraceOvf + (last_t ? 0 : kNumSMs) + blockIdx.x : nullptr,
                            tp.compact_at);
             if (DTR && last_t && warp == kTcEpiWarp0 && lane == 0) DTR[46] = clock64();
@@ -386,10 +387,10 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
         tile_range(n_tiles - 1, t0, tn);
         named_bar_sync(2, kTcWarps * 32);
         if (buffered) {
-            epi_tile_buf_last_store(e, a.part, blockIdx.x, a.n_h, h_row0, n_h, a.KP, a.LS, tn, t0, warp, kTcWarps,
+            epi_tile_buf_last_store(e, a.part, pcta, a.n_h, h_row0, n_h, a.KP, a.LS, tn, t0, warp, kTcWarps,
                                     warp == kTcEpiWarp0 ? DTR : nullptr);
         } else {
-            epi_tile_last(e, a.part, blockIdx.x, a.n_h, h_row0, n_h, a.KP, a.LS, tn, t0, warp, kTcWarps);
+            epi_tile_last(e, a.part, pcta, a.n_h, h_row0, n_h, a.KP, a.LS, tn, t0, warp, kTcWarps);
         }
         if (warp == kTcEpiWarp0 && lane == 0 && n_tiles - 1 < 2) TC_TRACE(4 + 2 * (n_tiles - 1));
     }
@@ -397,10 +398,10 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
     __syncthreads();
     tc_fence_after();
     if (buffered) {
-        if (n_tiles == 0 || store_after) epi_store_buf(e, a.part, blockIdx.x, a.n_h, h_row0, n_h, warp, kTcWarps, a.LS);
+        if (n_tiles == 0 || store_after) epi_store_buf(e, a.part, pcta, a.n_h, h_row0, n_h, warp, kTcWarps, a.LS);
         // (otherwise the last tile's fold stored every row)
     } else {
-        epi_store(e, a.part, blockIdx.x, a.n_h, h_row0, n_h, a.KP, a.LS, warp, kTcWarps);
+        epi_store(e, a.part, pcta, a.n_h, h_row0, n_h, a.KP, a.LS, warp, kTcWarps);
     }
     if (threadIdx.x == 0) TC_TRACE(7);
     if (warp == kTcMmaWarp)

@@ -1,2 +1,3 @@
 python -c "import paper_2605_27390_b200._build as b; b.build()" > gpurun_out/build.log 2>&1
-for nt in 256 512; do EVOSPEC_FIN_NT=$nt TRACE_MODES=steady TRACE_NS=36864 timeout 300 python tools/trace_lmh.py > gpurun_out/trace_nt$nt.log 2>&1; done
+timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_gpu.log
+timeout 600 python tools/trace_bt.py > gpurun_out/trace_bt.log 2>&1
