@@ -329,32 +329,43 @@ void launch_lmh_finalize(const LmhArgs& a, int n_cta, int k, const float* wmax_d
 }
 
 // ------------------------------------------------------------ segment schedule
-// CTAs per segment for a segment-mode LM-head launch: one for every segment with
-// rows and positions, the rest in proportion to the segment's positions (the
-// work is rows of W streamed). Measured on config Bt (tools/bench_bt.py) faster
-// than the min-max share (sum_b ceil(size_b / T) <= grid) by ~10%.
-//   seg_cta[b] = active(<b) + floor((grid - n_active) * cum_size(<b) / total)
+// CTAs per segment for a segment-mode LM-head launch (the work is rows of W streamed)
 __global__ void seg_schedule_kernel(const int32_t* __restrict__ seg_pos, const SegRows seg_h_p, int nseg, int grid,
                                     int32_t* __restrict__ seg_cta) {
+    // CTAs per segment minimising the largest per-CTA share of rows: the smallest L with
+    // sum_b ceil(size_b / L) <= grid over the active segments (binary search, one warp;
+    // a segment's CTAs split its rows evenly), then an exclusive prefix sum
     const int* seg_h = seg_h_p.h;
     pdl_trigger();
     pdl_wait();
-    if (threadIdx.x != 0) return;
-    long long total = 0;
-    int n_active = 0;
-    for (int b = 0; b < nseg; ++b) {
+    if (threadIdx.x >= 32) return;
+    const int lane = threadIdx.x;
+    auto size_of = [&](int b) -> int {
         const int sz = seg_pos[b + 1] - seg_pos[b];
-        if (sz > 0 && seg_h[b + 1] > seg_h[b]) { total += sz; ++n_active; }
+        return (sz > 0 && seg_h[b + 1] > seg_h[b]) ? sz : 0;
+    };
+    int mx = 0;
+    for (int b = lane; b < nseg; b += 32) mx = max(mx, size_of(b));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    int lo = 1, hi = max(1, mx);   // need(hi) <= number of active segments <= grid
+    while (lo < hi) {
+        const int L = (lo + hi) >> 1;
+        int need = 0;
+        for (int b = lane; b < nseg; b += 32) need += (size_of(b) + L - 1) / L;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) need += __shfl_xor_sync(0xffffffffu, need, o);
+        if (need <= grid) hi = L; else lo = L + 1;
     }
-    const int spare = max(0, grid - n_active);
-    long long cum = 0;
-    int act = 0;
-    for (int b = 0; b < nseg; ++b) {
-        seg_cta[b] = act + (total > 0 ? (int)((long long)spare * cum / total) : 0);
-        const int sz = seg_pos[b + 1] - seg_pos[b];
-        if (sz > 0 && seg_h[b + 1] > seg_h[b]) { cum += sz; ++act; }
+    const int L = lo;
+    if (lane == 0) {
+        int acc = 0;
+        for (int b = 0; b < nseg; ++b) {
+            seg_cta[b] = acc;
+            acc += (size_of(b) + L - 1) / L;
+        }
+        seg_cta[nseg] = min(acc, grid);
     }
-    seg_cta[nseg] = act + (total > 0 ? (int)((long long)spare * cum / total) : 0);
 }
 
 void launch_seg_schedule(const int32_t* seg_pos, const int32_t* seg_h_host, int nseg, int grid, int32_t* seg_cta,
