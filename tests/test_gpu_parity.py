@@ -329,6 +329,27 @@ def test_draft_step_two_list_shapes(n_h, k, n_dyn, dup, n_static):
     assert ctx.get_flags() == 0
 
 
+@pytest.mark.parametrize("seed,n_h,k", [(0, 10, 10), (1, 60, 24), (2, 3, 1)])
+def test_draft_step_two_list_integer_ties(seed, n_h, k):
+    """The two-list LM head on integer data ({-3..3}: every logit an exact integer, massive
+    ties inside and across the static and dynamic lists, whose subset positions do not
+    follow id order): the candidate buffers order ties by vocabulary id (DESIGN §5.3,
+    keys), so the top-k ids equal the oracle's lower-id-first order."""
+    P = G.make_problem(70 + seed, dtype="bf16", integer=True, V=30000, d=128, n_static=20000, n_sem=3000,
+                       n_dyn=2500, n_h=n_h, k=k)
+    ctx = ctx_for(P)
+    W = G.to_dev(P["W"], DEV)
+    ctx.prepare_weights(W)
+    kw = dict(E=W, W_local=W, static_ids=G.to_dev(P["static"], DEV), csr_row_ptr=G.to_dev(P["row_ptr"], DEV),
+              csr_col=G.to_dev(P["col"], DEV), k=P["k"], n_sem=P["n_sem"], n_dyn=P["n_dyn"])
+    out = ctx.draft_step(q=G.to_dev(P["q"], DEV), H=G.to_dev(P["H"], DEV), seeds=G.to_dev(P["seeds"], DEV), **kw)
+    torch.cuda.synchronize()
+    ref = G.oracle_step(oracle, P)
+    np.testing.assert_array_equal(out[0].cpu().numpy(), ref["triple"]["ids"])
+    np.testing.assert_allclose(out[1].cpu().numpy(), ref["triple"]["vals"], rtol=0, atol=1e-6)
+    assert ctx.get_flags() == 0
+
+
 def test_input_errors():
     P = G.make_problem(0, dtype="fp32", **TINY)
     ctx = ctx_for(P)
