@@ -361,6 +361,7 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
             epi_par_phase1_any(e, n_h, a.KP, tn, t0, ftid, fn, last_t, a.part, pcta, a.n_h, h_row0, a.LS,
                                DTR && last_t && warp == kTcEpiWarp0 ? DTR + 50 : nullptr);
             if (DTR && last_t && warp == kTcEpiWarp0 && lane == 0) DTR[44] = clock64();
+            if (DTR && last_t && lane == 0) DTR[20 + warp] = clock64();   // (each warp's phase-1 end)
             named_bar_sync(bar, fn);
             epi_par_phase2(e, n_h, a.KP, tn, t0, ftid, fn, bar, last_t, a.part, pcta, a.n_h, h_row0, a.LS,
                            a.trace ? a.trace + kTraceOvf + (last_t ? 0 : kNumSMs) + blockIdx.x : nullptr,

@@ -85,6 +85,7 @@ for pf in os.environ.get("TRACE_MODES", "flushed,warmcode,steady").split(","):
         print("   CTA0 last tile clock64 (cycles from tfull): tmem->smem", dd[41] - b, "bar1", dd[42] - b, "bar2", dd[43] - b,
               "par1", dd[44] - b, "bar", dd[45] - b, "par2", dd[46] - b, "cands overflow/ok", dd[48], dd[49])
         print("   phase1 detail (rowstate, pass1 done, pass2 done, stores done):", [int(dd[50 + i] - b) for i in (3, 0, 1, 2)])
+        print("   phase1 end per warp (cycles from tfull):", [int(dd[20 + w] - b) for w in range(13)])
         for it in range(5):
             if dd[it * 4] > 0:
                 print("     row", it, [int(dd[it * 4 + j] - b) for j in range(4)])
