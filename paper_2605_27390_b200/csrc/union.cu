@@ -561,6 +561,7 @@ union_kernel(int V, const int32_t* __restrict__ static_ids, int n_static,
         for (int i = tid; i < kHistBins; i += T) clear_hist[i] = 0;
     const int n_cand = min(*n_cand_dev, cap);
     __syncthreads();   // the seeds walk (warp 0) has set its bits: kNew is decided while loading
+    if (trace) { if (threadIdx.x == 0) { long long t_; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); trace[42] = t_; } }
     // per-thread statistics of the three selections below (count, key range), gathered
     // while loading: kCand (selections 0 and 2) and kNew (selection 1)
     int st_c[2] = {0, 0};
@@ -593,6 +594,7 @@ union_kernel(int V, const int32_t* __restrict__ static_ids, int n_static,
             cf[i] = f;
         }
     }
+    if (trace) { if (threadIdx.x == 0) { long long t_; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); trace[43] = t_; } }
     __syncthreads();
     if (trace) { __syncthreads(); if (threadIdx.x == 0) { long long t_; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); trace[1] = t_; } }
     // 2.-3. three exact selections in one set of radix passes (block_topM_multi):

@@ -57,6 +57,9 @@ for i, nm in enumerate(["start", "loaded", "S_sem", "gs", "G/graph", "formation"
     dist("union " + nm, uni[i:i + 1])
 dist("union after wait", tr[2 * N * 8 + 40:2 * N * 8 + 41])
 dist("union sbits copied", tr[2 * N * 8 + 41:2 * N * 8 + 42])
+dist("union seeds walked", tr[2 * N * 8 + 42:2 * N * 8 + 43])
+dist("union cands in (t0)", tr[2 * N * 8 + 43:2 * N * 8 + 44])
+print("  union n_cand", int(tr[2 * N * 8 + 23]))
 sel = tr[2 * N * 8 + 24:2 * N * 8 + 40]
 for i, nm in [(0, "start"), (10, "stats"), (11, "setup"), (12, "hist0"), (1, "pass0"), (2, "pass1"), (13, "marked"),
               (14, "ranked")]:
