@@ -71,16 +71,32 @@ lmh_gemv_kernel(LmhArgs a, int h_row0) {
     EpiSmem e = epi_carve(g_sm + (size_t)NH * n_chunks * ELEMS * 32 * 4, NH, a.KP, kGemvWarps);
     const int lane = lane_id(), warp = warp_id();
 
-    for (int i = threadIdx.x; i < NH * n_chunks * ELEMS * 32; i += blockDim.x) {
-        int r = i / (n_chunks * ELEMS * 32), rem = i % (n_chunks * ELEMS * 32);
-        int ch = rem / (ELEMS * 32), j = (rem / 32) % ELEMS, ln = rem % 32;
-        int c = ch * 32 * ELEMS + ln * ELEMS + j;
-        float v = 0.0f;
-        if (c < d) {
-            size_t o = (size_t)(h_row0 + r) * d + c;
-            v = a.h_dtype == 0 ? bf16_bits_to_f32(((const uint16_t*)a.H)[o]) : ((const float*)a.H)[o];
+    if (a.h_dtype == 0 && d % 8 == 0 && ELEMS == 8) {
+        // bf16 H: one 16-byte load per (row, chunk, lane) -> its 8 elements (every CTA
+        // stages H first, so this is a fixed cost of the launch: vectorised, no divisions)
+        const int per_row = n_chunks * 32;
+        for (int i = threadIdx.x; i < NH * per_row; i += blockDim.x) {
+            const int r = i / per_row, rem = i - r * per_row;   // rem = ch * 32 + ln
+            const int ch = rem >> 5, ln = rem & 31;
+            const int c = ch * 32 * 8 + ln * 8;
+            float f[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            if (c < d) unpack_bf16x8(__ldg((const uint4*)((const uint16_t*)a.H + (size_t)(h_row0 + r) * d + c)), f);
+            float* dst = H_sm + ((size_t)(r * n_chunks + ch) * 8) * 32 + ln;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) dst[j * 32] = f[j];
         }
-        H_sm[i] = v;
+    } else {
+        for (int i = threadIdx.x; i < NH * n_chunks * ELEMS * 32; i += blockDim.x) {
+            int r = i / (n_chunks * ELEMS * 32), rem = i % (n_chunks * ELEMS * 32);
+            int ch = rem / (ELEMS * 32), j = (rem / 32) % ELEMS, ln = rem % 32;
+            int c = ch * 32 * ELEMS + ln * ELEMS + j;
+            float v = 0.0f;
+            if (c < d) {
+                size_t o = (size_t)(h_row0 + r) * d + c;
+                v = a.h_dtype == 0 ? bf16_bits_to_f32(((const uint16_t*)a.H)[o]) : ((const float*)a.H)[o];
+            }
+            H_sm[i] = v;
+        }
     }
     epi_init(e, NH);
     __syncthreads();
