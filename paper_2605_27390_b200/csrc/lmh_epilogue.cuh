@@ -871,7 +871,7 @@ ES_DEV void epi_par_phase1_any(const EpiSmem& e, int n_h, int KP, int tn, int ba
 // practice; no pads: the finalisation reads xcnt entries; its maximum is m).
 ES_DEV void epi_par_phase2(const EpiSmem& e, int n_h, int KP, int tn, int base_pos, int tid, int nthr, int bar,
                            bool last, const LmhPartials& P, int cta, int n_h_total, int h_row0, int LS,
-                           long long* ovf = nullptr, int compact_at = 0) {
+                           long long* ovf = nullptr) {
     const int lane = lane_id(), warp = tid >> 5, n_warps = nthr >> 5;
     const int cap = last ? LS : kBuf;
     if (e.st_flag[0]) {   // uniform (set in phase 1, read after the caller's barrier): overflowed rows
@@ -915,7 +915,7 @@ ES_DEV void epi_par_phase2(const EpiSmem& e, int n_h, int KP, int tn, int base_p
     // best KP, the bound becomes the KP-th entry
     for (int r = warp; r < n_h; r += n_warps) {
         const int cnt = e.st_cnt[r];
-        if (cnt > max(KP, compact_at)) {
+        if (cnt > KP) {
             float thv;
             int thp;
             buf_compact_sorted(e.st_val + (size_t)r * kBuf, e.st_pos + (size_t)r * kBuf, cnt, KP, thv, thp);

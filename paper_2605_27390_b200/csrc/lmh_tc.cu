@@ -61,7 +61,6 @@ struct TcParams {
     int last_tile;   // rows of a CTA's short last tile (ranges longer than one tile)
     int dyn_tile;    // two-list mode: rows per second-list tile (EVOSPEC_DYN_TILE)
     int dyn_stride;  // two-list mode: CTA rank stride of the second-list round robin
-    int compact_at;  // between tiles, buffers above this many entries are compacted to their best KP
     int dyn_share;   // two-list mode: first-list share (16ths) of the CTAs expected to take a second-list tile
     size_t off_b, off_epi, off_bar, off_rows;  // smem carve offsets
 };
@@ -364,8 +363,7 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
             if (DTR && last_t && lane == 0) DTR[20 + warp] = clock64();   // (each warp's phase-1 end)
             named_bar_sync(bar, fn);
             epi_par_phase2(e, n_h, a.KP, tn, t0, ftid, fn, bar, last_t, a.part, pcta, a.n_h, h_row0, a.LS,
-                           a.trace ? a.trace + kTraceOvf + (last_t ? 0 : kNumSMs) + blockIdx.x : nullptr,
-                           tp.compact_at);
+                           a.trace ? a.trace + kTraceOvf + (last_t ? 0 : kNumSMs) + blockIdx.x : nullptr);
             if (DTR && last_t && warp == kTcEpiWarp0 && lane == 0) DTR[46] = clock64();
             if (warp == kTcEpiWarp0 && lane == 0 && t < 2) TC_TRACE(4 + 2 * t);
             if (last_t) break;
@@ -431,7 +429,6 @@ cudaError_t launch_lmh_tc(const LmhArgs& a, cudaStream_t st) {
     // two; measured r2 with the step timeline: 16/16 277.5 us, 12 282.0, 8 264.8, 6 286.7,
     // 4 286.4 -- below 8 the other CTAs' ranges grow a third tile)
     tp.dyn_share = 8;
-    tp.compact_at = getenv("EVOSPEC_COMPACT_AT") ? atoi(getenv("EVOSPEC_COMPACT_AT")) : 0;
     if (const char* e = getenv("EVOSPEC_DYN_TILE")) tp.dyn_tile = atoi(e) <= 0 ? 0 : std::max(16, std::min(kTileM, atoi(e)));
     uint32_t cols = 2 * tp.n_pad, c = 32;
     while (c < cols) c <<= 1;
