@@ -418,15 +418,24 @@ lmh_fin64_kernel(LmhArgs a, int n_cta_arg, int k, float gamma, const float* __re
                     for (int x = 0; x < 2; ++x) {
                         float fh[8];
                         unpack_bf16x8(hv2[x], fh);
-                        double dh[8];   // (fp32 -> fp64 conversions: H once per chunk)
+                        // H in fp64 pre-scaled by 2^896 (exact), W entering the fma as the raw
+                        // double whose fields are the bf16 fields in place (value w * 2^-896,
+                        // exact: two integer ops, no conversion unit -- the fp32 -> fp64
+                        // conversions of W were the re-score's bottleneck); every product
+                        // and hence every fma is bit-identical to the unscaled one
+                        double dh[8];
 #pragma unroll
-                        for (int j = 0; j < 8; ++j) dh[j] = (double)fh[j];
+                        for (int j = 0; j < 8; ++j) dh[j] = (double)fh[j] * 0x1p896;
 #pragma unroll
                         for (int u = 0; u < 8; ++u) {
-                            float fw[8];
-                            unpack_bf16x8(wv[x][u], fw);
+                            const uint32_t w4[4] = {wv[x][u].x, wv[x][u].y, wv[x][u].z, wv[x][u].w};
 #pragma unroll
-                            for (int j = 0; j < 8; ++j) acc[u] = fma((double)fw[j], dh[j], acc[u]);
+                            for (int j = 0; j < 4; ++j) {
+                                const uint32_t lo = (uint32_t)((int32_t)(w4[j] << 16) >> 3) & 0x8FFFE000u;
+                                const uint32_t hi = (uint32_t)((int32_t)w4[j] >> 3) & 0x8FFFE000u;
+                                acc[u] = fma(__hiloint2double((int)lo, 0), dh[2 * j], acc[u]);
+                                acc[u] = fma(__hiloint2double((int)hi, 0), dh[2 * j + 1], acc[u]);
+                            }
                         }
                     }
                 }
