@@ -428,6 +428,7 @@ lmh_fin64_kernel(LmhArgs a, int n_cta_arg, int k, float gamma, const float* __re
                         for (int j = 0; j < 8; ++j) dh[j] = (double)fh[j] * 0x1p896;
 #pragma unroll
                         for (int u = 0; u < 8; ++u) {
+                            if (q0 + u >= nn) break;   // (uniform: the group's last entries)
                             const uint32_t w4[4] = {wv[x][u].x, wv[x][u].y, wv[x][u].z, wv[x][u].w};
 #pragma unroll
                             for (int j = 0; j < 4; ++j) {
@@ -442,6 +443,7 @@ lmh_fin64_kernel(LmhArgs a, int n_cta_arg, int k, float gamma, const float* __re
                 if (tid == 0 && q0 == 0) FIN_DT_R(13);
 #pragma unroll
                 for (int u = 0; u < 8; ++u) {
+                    if (q0 + u >= nn) break;
                     const double t = warp_sum_d(acc[u]);
                     if (lane == 0) res_d[warp * 8 + u] = t;
                 }
