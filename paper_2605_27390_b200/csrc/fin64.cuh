@@ -113,6 +113,7 @@ lmh_fin64_kernel(LmhArgs a, int n_cta_arg, int k, float gamma, const float* __re
     __shared__ float red_s[NW];
     __shared__ int s_cand_n, s_nk, s_nneed, s_nq;
     __shared__ float s_th0, s_M, s_lse;
+    __shared__ double s_delta;
 
     pdl_trigger();
     const int r = blockIdx.x;
@@ -140,8 +141,15 @@ lmh_fin64_kernel(LmhArgs a, int n_cta_arg, int k, float gamma, const float* __re
     }
     hacc = warp_sum_d(hacc);
     if (lane == 0) red_d[warp] = hacc;
+    // delta = gamma ||h|| max_v ||W_v|| inv_temp: inputs only, so before the wait
+    __syncthreads();
+    if (tid == 0) {
+        double hn = 0.0;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) hn += red_d[w];
+        s_delta = (double)gamma * sqrt(hn) * (double)__ldg(wmax_dev) * (double)a.inv_temp;
+    }
     if (tid == 0) s_cand_n = 0;
-    const float wmax = warp == 0 ? __ldg(wmax_dev) : 0.0f;   // (an input: before the wait; warp 0 uses it)
     pdl_wait();
     if (tid == 0) { FIN_TRACE_R(0); FIN_DT_R(0); }
     // the row's lists: CTAs [c_base, c_base + n_cta) (segment mode: its segment's CTAs,
@@ -352,10 +360,7 @@ lmh_fin64_kernel(LmhArgs a, int n_cta_arg, int k, float gamma, const float* __re
         c_v[lane] = v;
         c_id[lane] = p;
         c_gid[lane] = gid;
-        double hn = 0.0;
-#pragma unroll
-        for (int w = 0; w < NW; ++w) hn += red_d[w];
-        const double delta = (double)gamma * sqrt(hn) * (double)wmax * (double)a.inv_temp;
+        const double delta = s_delta;   // (computed before the PDL wait)
         const float nv = __shfl_down_sync(0xffffffffu, v, 1);
         const bool close = lane + 1 < cnt && (double)v - (double)nv <= 2.0 * delta + 2.4e-7 * fabs((double)v);
         const unsigned cm = __ballot_sync(0xffffffffu, close);   // bit i: entries i and i+1 in one run
