@@ -402,9 +402,10 @@ lmh_fin64_kernel(LmhArgs a, int n_cta_arg, int k, float gamma, const float* __re
             for (int q0 = 0; q0 < nn; q0 += 8) {
                 const uint4* wp[8];
 #pragma unroll
-                for (int u = 0; u < 8; ++u)
-                    wp[u] = (const uint4*)((const uint16_t*)a.W +
-                                           (size_t)(c_gid[need_list[min(q0 + u, nn - 1)]] / a.R) * a.d);
+                for (int u = 0; u < 8; ++u) {
+                    const int gidu = c_gid[need_list[min(q0 + u, nn - 1)]];
+                    wp[u] = (const uint4*)((const uint16_t*)a.W + (size_t)(a.R == 1 ? gidu : gidu / a.R) * a.d);
+                }
                 double acc[8];
 #pragma unroll
                 for (int u = 0; u < 8; ++u) acc[u] = 0.0;
@@ -489,7 +490,11 @@ lmh_fin64_kernel(LmhArgs a, int n_cta_arg, int k, float gamma, const float* __re
         double e = lane < cnt ? (flagged ? c_e[lane] : (double)c_v[lane]) : -INFINITY;
         int gid = c_gid[lane];
         int id = lane < cnt ? gid : 0x7fffffff;
-        if (nn > 0) {
+        // (the exact values usually keep the fp32 order: sort only if some pair is out of order)
+        const double ne = __shfl_down_sync(0xffffffffu, e, 1);
+        const int ni = __shfl_down_sync(0xffffffffu, id, 1);
+        const bool in_order = lane + 1 >= cnt || !before(ne, ni, e, id);
+        if (nn > 0 && !__all_sync(0xffffffffu, in_order)) {
 #pragma unroll
             for (int kk = 2; kk <= 32; kk <<= 1) {
 #pragma unroll
