@@ -242,14 +242,6 @@ lmh_fin64_kernel(LmhArgs a, int n_cta_arg, int k, float gamma, const float* __re
     const float th0 = s_th0;
     const int nq = s_nq;
     const float M = s_M;
-    {   // the softmax sum (reduced in step 3)
-        float S = 0.0f;
-#pragma unroll 1
-        for (int c = tid; c < n_cta; c += NT)
-            if (l_m[c] != -INFINITY) S += l_s[c] * __expf(l_m[c] - M);
-        S = warp_sum(S);
-        if (lane == 0) red_s[warp] = S;
-    }
     if (tid == 0) FIN_DT_R(8);
     // the qualifying lists' entries >= th0 -> candidate buffer (16 float4 per list)
     const size_t row_bytes = (size_t)a.d * (a.w_dtype == 0 ? 2 : 4);
@@ -257,14 +249,25 @@ lmh_fin64_kernel(LmhArgs a, int n_cta_arg, int k, float gamma, const float* __re
     {
         const int ush = LS == 128 ? 5 : 4;   // float4 units per list: 1 << ush
         const int units = nq << ush;
+        // the softmax sum (reduced in step 3), by every thread once
+        auto softmax_sum = [&]() {
+            float S = 0.0f;
 #pragma unroll 1
-        for (int u0 = tid; u0 < units; u0 += 4 * NT) {
+            for (int c = tid; c < n_cta; c += NT)
+                if (l_m[c] != -INFINITY) S += l_s[c] * __expf(l_m[c] - M);
+            S = warp_sum(S);
+            if (lane == 0) red_s[warp] = S;
+        };
+        const int wbase = tid - lane;   // (warp-uniform loop: the softmax sum's shuffles)
+        if (wbase >= units) softmax_sum();   // (warps without filter units: right away)
+#pragma unroll 1
+        for (int u0 = wbase; u0 < units; u0 += 4 * NT) {
             float4 vv[4];
             int4 ii[4];
             int nv[4];   // valid entries in the unit (slots past a list's entries hold stale data)
 #pragma unroll
             for (int x = 0; x < 4; ++x) {   // all loads in flight before any use
-                const int u = u0 + x * NT;
+                const int u = u0 + lane + x * NT;
                 const int c = u < units ? qidx[u >> ush] : 0, sl = (u & ((1 << ush) - 1)) * 4;
                 nv[x] = u < units ? l_n[c] - sl : 0;
                 const size_t o = ((size_t)cta_of(c) * a.n_h + r) * LS + sl;
@@ -273,7 +276,8 @@ lmh_fin64_kernel(LmhArgs a, int n_cta_arg, int k, float gamma, const float* __re
                     ii[x] = __ldcg((const int4*)&a.part.id[o]);
                 }
             }
-            if (tid == 0 && u0 == 0) FIN_DT_R(9);
+            if (tid == 0 && u0 == 0) FIN_DT_R(9);   // (u0 = warp base)
+            if (u0 == wbase) softmax_sum();   // (while the first loads fly)
 #pragma unroll
             for (int x = 0; x < 4; ++x) {
                 if (nv[x] <= 0) vv[x] = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
