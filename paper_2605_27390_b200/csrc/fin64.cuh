@@ -526,7 +526,7 @@ lmh_fin64_kernel(LmhArgs a, int n_cta_arg, int k, float gamma, const float* __re
         if (lane == 0) {
             FIN_TRACE_R(6);
             FIN_DT_R(6);
-            if (a.trace && r < 148) a.trace[148 * 8 + (size_t)r * 8 + 7] = ncand;
+            if (a.trace && r < 148) a.trace[148 * 8 + (size_t)r * 8 + 7] = ncand + 10000LL * nn;   // (+ re-scored)
         }
     }
 }

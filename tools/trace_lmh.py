@@ -74,7 +74,11 @@ for pf in os.environ.get("TRACE_MODES", "flushed,warmcode,steady").split(","):
     for j, n in enumerate(["fin_start", "fin_hnorm", "fin_B1", "fin_filter", "fin_runs", "fin_rescore", "fin_end"]):
         col = frel[:, j]
         print(f"   {n:10s} min {col.min():7.1f}  med {np.median(col):7.1f}  max {col.max():7.1f}")
-    print("   ncand per row: mean", fin[:, 7].mean(), "max", fin[:, 7].max())
+    nc, nn = fin[:, 7] % 10000, fin[:, 7] // 10000
+    print("   ncand per row: mean", nc.mean(), "max", nc.max(), "| re-scored per row: mean", nn.mean(), "max", nn.max())
+    dur = (fin[:, 6] - fin[:, 0]) / 1e3
+    slow = np.argsort(-dur)[:6]
+    print("   slowest rows (row: us, ncand, re-scored):", [(int(i), round(dur[i], 1), int(nc[i]), int(nn[i])) for i in slow])
     det = ctx.read_trace(296 * 8 + 16 + 32)[296 * 8 + 16:].astype(np.int64)
     if det[0] > 0:
         print("   finalize row 0 clock64 deltas (cycles from slot 0):",
