@@ -396,6 +396,7 @@ def run_ours(args):
                          d2h_bytes_per_step=d2h),
                 gpu_launches=launches, clocks=clk, breakdown=breakdown, device_flags=flags,
                 lmh_tokens_per_s=n_h / (per["lmh"] + per["finalize"] + per["merge"]) * 1e3 if per["lmh"] else None,
+                north_star_lmh=north_star_lmh(sweep),
                 subset_sweep=sweep, per_depth=per_depth, batched=bt, extra_configs=extra, parity_vs_oracle=parity,
                 paper_reference=PAPER_REFERENCE)
     print(json.dumps(line), flush=True)
@@ -809,6 +810,20 @@ def per_depth_line(ctx, Wd, Hd, k, V, d, dev, args):
         us = statistics.median(times[w])
         out[key] = dict(us=us, GBps=nbytes(w) / us / 1e3, frac_of_copy_peak=nbytes(w) / us / 1e3 / peak)
     return out
+
+
+def north_star_lmh(sweep):
+    """The north star's LM-head target in one place: subset LM head + softmax + top-k at
+    36,864 rows (llama), as a fraction of the measured copy bandwidth, L2 flushed before
+    each call and back to back (steady state of a draft loop); the target is >= 0.70."""
+    if not sweep:
+        return None
+    row = next((r for r in sweep if r["n_S"] == 36864), None)
+    if row is None:
+        return None
+    return dict(n_S=36864, target_frac=0.70, us_flushed=row["us"], frac_flushed=row["frac_of_copy_peak"],
+                us_steady=row.get("us_steady"), frac_steady=row.get("frac_of_copy_peak_steady"),
+                peak_gbs=load_peaks()["hbm_gbs"])
 
 
 def subset_sweep(ctx, Wd, Hd, n_h, k, V, d, dev, args):
