@@ -837,8 +837,9 @@ static evospec_status lmh_impl(evospec_ctx* ctx, const void* W, int64_t n_w_rows
     if (skip_fin) return EVOSPEC_OK;   // (the ragged head's static block: finalised with its dynamic lists)
     {
         StageTimer t(ctx, EVOSPEC_STAGE_FINALIZE, st);
-        launch_lmh_finalize(a, n_cta, k, ctx->wmax, topk_ids, topk_vals, row_max, row_sumexp, ctx->flags, st,
-                            gamma);
+        if (!launch_lmh_finalize(a, n_cta, k, ctx->wmax, topk_ids, topk_vals, row_max, row_sumexp, ctx->flags, st,
+                                 gamma))
+            return fail(EVOSPEC_EINPUT, "subset_logits_topk: %d partial lists exceed the finalisation's capacity", n_cta);
         ctx->launches += 1;
     }
     LAUNCH_CHECK("lmh_finalize");

@@ -307,7 +307,7 @@ lmh_finalize_kernel(LmhArgs a, int n_cta, int k, float gamma, const float* __res
 
 
 
-void launch_lmh_finalize(const LmhArgs& a, int n_cta, int k, const float* wmax_dev, int32_t* topk_ids,
+bool launch_lmh_finalize(const LmhArgs& a, int n_cta, int k, const float* wmax_dev, int32_t* topk_ids,
                          float* topk_vals, float* row_max, float* row_sumexp, int* flags, cudaStream_t st,
                          float gamma) {
     if (a.KP <= 32 && (a.LS == 64 || a.LS == kTcListLS) && n_cta <= kF64MaxCta) {
@@ -320,12 +320,14 @@ void launch_lmh_finalize(const LmhArgs& a, int n_cta, int k, const float* wmax_d
             attr_set = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 120 * 1024) == cudaSuccess;
         launch_pdl(kern, dim3(a.n_h), dim3(kF64Threads), a.n_h <= kNumSMs ? (size_t)120 * 1024 : 0, st, a, n_cta, k,
                    gamma, wmax_dev, topk_ids, topk_vals, row_max, row_sumexp, flags);
-        return;
+        return true;
     }
+    if (a.KP <= 32) return false;   // (lists of a shape only fin64 reads: more lists than kF64MaxCta)
     size_t smem = (size_t)n_cta * 2 * sizeof(int) + (size_t)n_cta * a.KP * 8;
     cudaFuncSetAttribute(lmh_finalize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     lmh_finalize_kernel<<<a.n_h, kFinThreads, smem, st>>>(a, n_cta, k, gamma, wmax_dev, topk_ids, topk_vals,
                                                            row_max, row_sumexp, flags);
+    return true;
 }
 
 // ------------------------------------------------------------ segment schedule

@@ -152,7 +152,7 @@ int lmh_tc_grid();
 cudaError_t launch_lmh_tc(const LmhArgs& a, cudaStream_t st);
 
 // ---- finalize / merge / prepare (finalize.cu)
-void launch_lmh_finalize(const LmhArgs& a, int n_cta, int k, const float* wmax_dev,
+bool launch_lmh_finalize(const LmhArgs& a, int n_cta, int k, const float* wmax_dev,
                          int32_t* topk_ids, float* topk_vals, float* row_max, float* row_sumexp,
                          int* flags, cudaStream_t st, float gamma);
 struct SegRows { int h[kMaxSeg + 1]; };
