@@ -1,3 +1,3 @@
+# ncu of the north-star call (LM head + top-k at 36,864 rows, one-list mode) and its launch list
 python -c "import paper_2605_27390_b200._build as b; b.build()" > gpurun_out/build.log 2>&1
-for v in 0 1; do for ns in 8192 16384; do EVOSPEC_PAR_SINGLE=$v TRACE_MODES=flushed,steady TRACE_NS=$ns timeout 300 python tools/trace_lmh.py > gpurun_out/trace_ps${v}_$ns.log 2>&1; done; done
-EVOSPEC_PAR_SINGLE=1 timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -k "tiny or medium or lmh_paths or integer or ties or odd or empty or duplicate" > gpurun_out/pytest_ps.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_ps.log
+TRACE_MODES=steady TRACE_NS=36864 EVOSPEC_NOTRACE=1 ncu --set full --import-source on --clock-control none -k regex:"lmh_tc|lmh_fin64" -s 6 -c 2 -o gpurun_out/prof_lmh36k -f env NH=60 python tools/gemv_probe.py > gpurun_out/ncu_lmh36k.log 2>&1
