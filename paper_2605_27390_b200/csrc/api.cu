@@ -304,7 +304,7 @@ evospec_status evospec_create(evospec_ctx** out, const evospec_config* cfg, int 
     A(dalloc(&x->s64, V)); A(dalloc(&x->key32, V)); A(dalloc(&x->hist12, kHistBins)); A(dalloc(&x->ubits, (V + 31) / 32)); A(cudaMemset(x->hist12, 0, kHistBins * sizeof(uint32_t)));
     A(dalloc(&x->scan_sched, 2)); A(cudaMemset(x->scan_sched, 0, 2 * sizeof(int)));
     A(dalloc(&x->sbits, (V + 31) / 32 + 4)); A(cudaMemset(x->sbits, 0, ((V + 31) / 32 + 4) * sizeof(uint32_t)));
-    A(dalloc(&x->hist, 12 * kHistBins));
+    A(dalloc(&x->hist, 12 * kHistBins + 32)); A(cudaMemset(x->hist, 0, (12 * kHistBins + 32) * sizeof(uint32_t)));
     A(dalloc(&x->ver_acc, kMaxChain + 1)); A(dalloc(&x->ver_tok, kMaxChain + 1));
     A(dalloc(&x->zero_i, 1)); A(cudaMemset(x->zero_i, 0, sizeof(int32_t)));
     A(dalloc(&x->cand_count, 4)); A(dalloc(&x->cand_s, cap)); A(dalloc(&x->cand_id, cap));

@@ -8,7 +8,7 @@
 namespace es {
 
 constexpr int kScanWarps = 16;      // sem scan: warps per CTA (1 CTA / SM)
-constexpr int kSelThreads = 512;    // topn candidates (cooperative), 4096 bins = 8 / thread
+constexpr int kSelThreads = 512;    // topn candidates (PDL, soft grid barrier), 4096 bins = 8 / thread
 constexpr int kHistBins = 4096;     // top 12 bits of the fp32 score key
 constexpr int kUnionThreads = 1024;
 constexpr int kTopkPad = 8;         // extra fp32 candidates kept per row for the exact re-score

@@ -13,24 +13,22 @@
 //                       fp64 copy in shared memory.
 //                       The scan also histograms the top 12 bits of the
 //                       order-preserving fp32 key of every score.
-//   topn_cand_kernel    cooperative radix select over the composite key
+//   topn_cand_kernel    grid-wide radix select over the composite key
 //                       (float_key(s), double_key(s), ~id). Pass 0 reuses the
 //                       scan's histogram, so in the common case no grid-wide
 //                       sync runs: every CTA finds the boundary bin b and emits
 //                       all scores in bins >= b -- a candidate SUPERSET of the
 //                       top-N of at most `cap` elements, carrying exact keys.
-//                       Further passes (grid.sync) run only if that superset
+//                       Further passes (soft_grid_sync) run only if that superset
 //                       would not fit. The exact top-N, its order where the
 //                       formation needs it, and the cap are resolved in the
 //                       union kernel (union.cu) on those exact keys.
-#include <cooperative_groups.h>
 #include <cstdlib>
 #include <cstring>
 
 #include "common.cuh"
 #include "kernels.cuh"
 
-namespace cg = cooperative_groups;
 
 namespace es {
 
@@ -471,13 +469,35 @@ ES_DEV void pass_digit(int pass, int& word, int& shift, int& nbits) {
     else { shift = part == 0 ? 21 : (part == 1 ? 10 : 0); nbits = part == 2 ? 10 : 11; }
 }
 
+// Grid barrier for topn_cand_kernel's rare multi-pass path, without a cooperative
+// launch (whose start waits for the whole predecessor grid to drain): every CTA runs
+// griddepcontrol.launch_dependents first, so no later kernel of the stream is scheduled
+// before all of this grid's CTAs are resident, and waiting CTAs cannot starve the
+// others. One counter, never reset: CTA 0 adds 2^31 - (G - 1), the others 1, so the
+// top bit flips exactly when the last CTA arrives (the low bits return to 0).
+ES_DEV void soft_grid_sync(unsigned* ctr) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned inc = blockIdx.x == 0 ? 0x80000000u - (gridDim.x - 1) : 1u;
+        __threadfence();
+        const unsigned old = atomicAdd(ctr, inc);
+        unsigned cur;
+        do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(ctr) : "memory");
+            if (((old ^ cur) & 0x80000000u) == 0) __nanosleep(32);
+        } while (((old ^ cur) & 0x80000000u) == 0);
+        __threadfence();
+    }
+    __syncthreads();
+}
+
 __global__ void __launch_bounds__(kSelThreads, 1)
 topn_cand_kernel(const double* __restrict__ s64, const int32_t* __restrict__ ids, int64_t n,
                  int id_mul, int id_add, int N, int cap, const uint32_t* __restrict__ hist_pre,
                  uint32_t* __restrict__ hist_g, int* __restrict__ out_count, double* __restrict__ out_s,
                  int32_t* __restrict__ out_id, long long* __restrict__ tr) {
-    cg::grid_group grid = cg::this_grid();
-    pdl_trigger();   // the union kernel may be scheduled now (it waits for this grid before reading)
+    pdl_trigger();   // the union kernel may be scheduled now (it waits for this grid before reading);
+                     // first, so that every CTA is resident before any later kernel (soft_grid_sync)
     pdl_wait();      // the scores / histogram of the scan (launched behind it with PDL)
     if (tr && blockIdx.x == 0 && threadIdx.x == 0) tr[2 * kNumSMs] = step_gtime();
     __shared__ uint32_t hist[kHistBins];
@@ -521,7 +541,7 @@ topn_cand_kernel(const double* __restrict__ s64, const int32_t* __restrict__ ids
             uint32_t* hw = hist_g + (size_t)pass * kHistBins;
             for (int b = threadIdx.x; b < (1 << nbits); b += blockDim.x)
                 if (hist[b]) atomicAdd(&hw[b], hist[b]);
-            grid.sync();
+            soft_grid_sync(hist_g + 12 * kHistBins);   // (the counter word after the 12 histograms)
             hp = hw;
         }
         // every CTA: the bin (descending) where the running count reaches `remaining`;
@@ -598,9 +618,10 @@ cudaError_t launch_topn_cand(const double* s64, const int32_t* ids, int64_t n, i
     int grid = kNumSMs;
     if (n < (int64_t)grid * 64) grid = (int)((n + 63) / 64);
     if (grid < 1) grid = 1;
-    // cooperative (the rare multi-pass path syncs the grid) and programmatic: its launch
-    // overlaps the scan's tail, and the union behind it may be scheduled early
-    return launch_pdl_coop(topn_cand_kernel, dim3(grid), dim3(kSelThreads), 0, st, s64, ids, n, id_mul, id_add, N,
+    // programmatic: its CTAs take the SMs the scan's CTAs leave and wait there, and the
+    // union behind it may be scheduled early (the rare multi-pass path syncs the grid
+    // with soft_grid_sync: hist_g holds 12 * kHistBins + 1 words)
+    return launch_pdl(topn_cand_kernel, dim3(grid), dim3(kSelThreads), 0, st, s64, ids, n, id_mul, id_add, N,
                            cap, hist_pre, hist_g, out_count, out_s, out_id, s_step_trace);
 }
 

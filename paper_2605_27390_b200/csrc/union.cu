@@ -559,7 +559,8 @@ union_kernel(int V, const int32_t* __restrict__ static_ids, int n_static,
     // the selection has consumed the scan's histogram: leave it zero for the next build
     if (clear_hist)
         for (int i = tid; i < kHistBins; i += T) clear_hist[i] = 0;
-    const int n_cand = min(*n_cand_dev, cap);
+    const int n_cand_raw = *n_cand_dev;
+    const int n_cand = min(n_cand_raw, cap);
     __syncthreads();   // the seeds walk (warp 0) has set its bits: kNew is decided while loading
     if (trace) { if (threadIdx.x == 0) { long long t_; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); trace[42] = t_; } }
     // per-thread statistics of the three selections below (count, key range), gathered
@@ -699,6 +700,16 @@ union_kernel(int V, const int32_t* __restrict__ static_ids, int n_static,
     __syncthreads();
 
     if (trace) { __syncthreads(); if (threadIdx.x == 0) { long long t_; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); trace[4] = t_; } }
+    // dynamic-list mode: this thread's static words of its compaction range (below),
+    // loaded now so their round trip overlaps the formation
+    const int w0 = (int)((long long)nwords * tid / T), w1 = (int)((long long)nwords * (tid + 1) / T);
+    const bool sreg = dyn_base && !emit_bits && nwords <= 8 * T;   // (w1 - w0 <= 8)
+    uint32_t sw[8];
+    const int base_pre = sreg ? *dyn_base : 0;
+    if (sreg) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) sw[j] = w0 + j < w1 ? __ldcg(&sbits[w0 + j]) : 0u;
+    }
     // 5. formation: seeds ++ S_sem ++ S_graph ++ S_ctx, first occurrence, skip
     //    members (static or taken), stop at N_dyn. The seeds were walked before
     //    the wait; the S_sem part is T_b and S_sem (selected above); graph and
@@ -720,14 +731,22 @@ union_kernel(int V, const int32_t* __restrict__ static_ids, int n_static,
     // written at out_ids + *dyn_base, and *out_n = *dyn_base + its length
     // (out_n = offsets + b + 1 for sequence b, dyn_base = offsets + b)
     int base_off = 0;
-    if (dyn_base) {
-        for (int w = tid; w < nwords; w += T) bits[w] &= ~__ldcg(&sbits[w]);
-        base_off = *dyn_base;
+    if (sreg) {   // own words only (the compaction below reads only its own range): no barrier
+        base_off = base_pre;
         out_ids += base_off;
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            if (w0 + j < w1) { bits[w0 + j] &= ~sw[j]; sbits[w0 + j] = 0; }
+    } else {
+        if (dyn_base) {
+            for (int w = tid; w < nwords; w += T) bits[w] &= ~__ldcg(&sbits[w]);
+            base_off = *dyn_base;
+            out_ids += base_off;
+        }
+        // the static bitmap is consumed: leave it zero for the next build's static_bits_kernel
+        for (int w = tid; w < nwords; w += T) sbits[w] = 0;
+        __syncthreads();
     }
-    // the static bitmap is consumed: leave it zero for the next build's static_bits_kernel
-    for (int w = tid; w < nwords; w += T) sbits[w] = 0;
-    __syncthreads();
     if (emit_bits) {
         // single shard, full output: the sorted ids are written by the multi-CTA
         // emit kernel from the bitmap (union_emit_kernel)
@@ -735,7 +754,7 @@ union_kernel(int V, const int32_t* __restrict__ static_ids, int n_static,
         if (tid == 0) {
             if (sem_out_n) *sem_out_n = sem_n_s;
             if (bad_s) atomicOr(flags, kFlagBadIds);
-            if (*n_cand_dev > cap) atomicOr(flags, kFlagSelectOverflow);
+            if (n_cand_raw > cap) atomicOr(flags, kFlagSelectOverflow);
         }
         if (trace) { __syncthreads(); if (threadIdx.x == 0) { long long t_; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); trace[6] = t_; } }
         return;
@@ -746,17 +765,18 @@ union_kernel(int V, const int32_t* __restrict__ static_ids, int n_static,
     //    and copied out coalesced; the shard slice (v mod R == r) is filtered
     //    from the staged copy. Outputs larger than the staging area fall back to
     //    direct per-thread stores.
-    const int w0 = (int)((long long)nwords * tid / T), w1 = (int)((long long)nwords * (tid + 1) / T);
     int cnt = 0;
     for (int w = w0; w < w1; ++w) cnt += __popc(bits[w]);
     int total = 0, total_local = 0;
     int off = block_excl_scan(cnt, warp_tot, total);
     int32_t* stage = (int32_t*)u_sm;                          // aliases ck/cid: 3*cap int32
-    const bool staged = total <= 3 * cap;
+    // (a dynamic list alone -- a few thousand ids -- goes straight out: each thread's ids
+    // are contiguous and follow its left neighbour's, no staging barrier)
+    const bool staged = total <= 3 * cap && !(sreg && !out_local);
     int32_t* dst = staged ? stage : out_ids;
     for (int w = w0; w < w1; ++w)
         for (uint32_t bb = bits[w]; bb; bb &= bb - 1) dst[off++] = w * 32 + __ffs(bb) - 1;
-    __syncthreads();
+    if (staged || out_local) __syncthreads();
     if (staged)
         for (int i = tid; i < total; i += T) out_ids[i] = stage[i];
     if (out_local) {
@@ -782,7 +802,7 @@ union_kernel(int V, const int32_t* __restrict__ static_ids, int n_static,
         if (sem_out_n) *sem_out_n = sem_n_s;
         if (bad_s) atomicOr(flags, kFlagBadIds);
         if (total > (dyn_base ? 0 : n_static) + n_dyn) atomicOr(flags, kFlagBudget);
-        if (*n_cand_dev > cap) atomicOr(flags, kFlagSelectOverflow);
+        if (n_cand_raw > cap) atomicOr(flags, kFlagSelectOverflow);
     }
     if (trace) { __syncthreads(); if (threadIdx.x == 0) { long long t_; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); trace[6] = t_; } }
 }

@@ -109,7 +109,7 @@ def test_duplicate_rows_tie_to_lower_id():
     check(P, got, ref, P["k"])
 
 
-@pytest.mark.parametrize("regime", ["tie_block", "sign_span", "narrow_span"])
+@pytest.mark.parametrize("regime", ["tie_block", "sign_span", "narrow_span", "multipass"])
 def test_union_selection_regimes(regime):
     """The union's three exact selections (S_sem, the budget of new candidates, the
     graph-seed prefix) in the regimes their key-linear binning treats differently:
@@ -118,8 +118,19 @@ def test_union_selection_regimes(regime):
     fallback); sign_span -- N_sem = 70% of V, candidates of both signs, so the key
     range spans the sign flip and the boundary bin is narrowed over several passes;
     narrow_span -- all scores within a few ulps of each other (one row plus ulp-level
-    perturbations), so one bin covers single keys from the first pass."""
-    if regime == "tie_block":
+    perturbations), so one bin covers single keys from the first pass; multipass --
+    20,000 copies of the best row at V = 40,000: the candidate superset of the scan's
+    histogram (>= 20,000 equal keys) exceeds the union's capacity (~16k), so the
+    candidate kernel runs its further passes down to the id digits (grid barriers)."""
+    if regime == "multipass":
+        P = G.make_problem(64, dtype="fp32", V=40000, d=64, n_static=3000, n_sem=2000, n_dyn=1500, n_h=2, k=8,
+                           w_std=1.0)
+        sc = oracle.sem_scores(P["W"], P["q"])
+        top = int(np.argmax(sc))
+        rng = np.random.default_rng(5)
+        dst = rng.choice(P["V"], 20000, replace=False)
+        P["W"][dst] = P["W"][top]
+    elif regime == "tie_block":
         P = G.make_problem(61, dtype="bf16", V=8192, d=256, n_static=1000, n_sem=1500, n_dyn=1200, n_h=2, k=8)
         sc = oracle.sem_scores(P["W"], P["q"])
         top = int(np.argsort(-sc)[20])
