@@ -503,7 +503,7 @@ topn_cand_kernel(const double* __restrict__ s64, const int32_t* __restrict__ ids
     __shared__ uint32_t hist[kHistBins];
     __shared__ uint32_t warp_sum_s[kSelThreads / 32];
     __shared__ SelState st;
-    __shared__ int found_bin, found_above;
+    __shared__ int found_bin, found_above, found_cnt, s_base;
 
     const int64_t lo = n * blockIdx.x / gridDim.x, hi = n * (blockIdx.x + 1) / gridDim.x;
     auto id_of = [&](int64_t i) -> int32_t { return ids ? ids[i] : (int32_t)(i * id_mul + id_add); };
@@ -569,13 +569,13 @@ topn_cand_kernel(const double* __restrict__ s64, const int32_t* __restrict__ ids
         uint32_t run = above_w + inc - tot;   // count in bins above this thread's range
 #pragma unroll
         for (int j = BPT - 1; j >= 0; --j) {
-            if (run < rem && run + c[j] >= rem) { found_bin = BPT * t + j; found_above = (int)run; }
+            if (run < rem && run + c[j] >= rem) { found_bin = BPT * t + j; found_above = (int)run; found_cnt = (int)c[j]; }
             run += c[j];
         }
         __syncthreads();
         if (threadIdx.x == 0) {
             const int b = found_bin;
-            const uint32_t in_bin = __ldcg(&hp[b]);
+            const uint32_t in_bin = (uint32_t)found_cnt;
             const long long superset = (long long)(N - st.remaining) + found_above + in_bin;
             st.remaining -= found_above;
             st.pmask[word] |= dmask << shift;
@@ -585,9 +585,53 @@ topn_cand_kernel(const double* __restrict__ s64, const int32_t* __restrict__ ids
         }
         __syncthreads();
     }
-    // compaction: warp-aggregated appends of (double_key(s), id)
+    // compaction: appends of (s, id), one global atomic per CTA (a few hundred rows per
+    // CTA: every row's load in flight, a block scan orders the CTA's appends); wider
+    // slices take warp-aggregated appends
     SelState my = st;
     const bool take_all = (N >= n);
+    constexpr int kCandIt = 4;
+    if (hi - lo <= (int64_t)kCandIt * blockDim.x) {
+        double sv[kCandIt];
+        int32_t iv[kCandIt];
+        bool sl[kCandIt];
+        int cnt = 0;
+#pragma unroll
+        for (int u = 0; u < kCandIt; ++u) {
+            const int64_t i = lo + (int64_t)u * blockDim.x + threadIdx.x;
+            sv[u] = 0.0;
+            iv[u] = -1;
+            if (i < hi) { sv[u] = s64[i]; iv[u] = id_of(i); }
+        }
+#pragma unroll
+        for (int u = 0; u < kCandIt; ++u) {
+            sl[u] = iv[u] >= 0 && (take_all || (N > 0 && sel_selected(sel_words(sv[u], iv[u]), my)));
+            cnt += sl[u] ? 1 : 0;
+        }
+        int inc = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += v;
+        }
+        if (lane == 31) warp_sum_s[wid] = (uint32_t)inc;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int tot = 0;
+            for (int w = 0; w < (int)(blockDim.x / 32); ++w) { const int x = (int)warp_sum_s[w]; warp_sum_s[w] = tot; tot += x; }
+            s_base = tot ? atomicAdd(out_count, tot) : 0;
+        }
+        __syncthreads();
+        int o = s_base + (int)warp_sum_s[wid] + inc - cnt;
+#pragma unroll
+        for (int u = 0; u < kCandIt; ++u)
+            if (sl[u]) {
+                if (o < cap) { out_s[o] = sv[u]; out_id[o] = iv[u]; }
+                ++o;
+            }
+        if (tr && blockIdx.x == 0 && threadIdx.x == 0) tr[2 * kNumSMs + 1] = step_gtime();
+        return;
+    }
     for (int64_t b0 = lo; b0 < hi; b0 += blockDim.x) {
         const int64_t i = b0 + threadIdx.x;
         bool sel = false;
