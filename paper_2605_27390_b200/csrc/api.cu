@@ -166,6 +166,9 @@ struct evospec_ctx {
     float* rg_s = nullptr;
     int32_t* rg_seg = nullptr;   // device {0, n_static}
     int32_t* rg_segcta = nullptr;   // device [kMaxSeg+1] CTA schedule of the dynamic blocks
+    // two-list draft step: the union's early copy of the dynamic list + its flag (lmh_tc.cu)
+    int32_t* early_ids = nullptr;
+    int* early_flag = nullptr;
     // draft_step as a CUDA graph (see evospec_draft_step)
     cudaGraphExec_t g_exec = nullptr;
     evospec_step_io g_key{};
@@ -249,6 +252,8 @@ evospec_status evospec_destroy(evospec_ctx* ctx) {
     if (ctx->comm && nccl().loaded) nccl().CommDestroy(ctx->comm);
     for (cudaEvent_t e : ctx->ev) cudaEventDestroy(e);
     if (ctx->trace) cudaFree(ctx->trace);
+    if (ctx->early_ids) cudaFree(ctx->early_ids);
+    if (ctx->early_flag) cudaFree(ctx->early_flag);
     if (ctx->g_exec) cudaGraphExecDestroy(ctx->g_exec);
     if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
     if (ctx->s_h) cudaStreamDestroy(ctx->s_h);
@@ -304,6 +309,8 @@ evospec_status evospec_create(evospec_ctx** out, const evospec_config* cfg, int 
     A(dalloc(&x->s64, V)); A(dalloc(&x->key32, V)); A(dalloc(&x->hist12, kHistBins)); A(dalloc(&x->ubits, (V + 31) / 32)); A(cudaMemset(x->hist12, 0, kHistBins * sizeof(uint32_t)));
     A(dalloc(&x->scan_sched, 2)); A(cudaMemset(x->scan_sched, 0, 2 * sizeof(int)));
     A(dalloc(&x->sbits, (V + 31) / 32 + 4)); A(cudaMemset(x->sbits, 0, ((V + 31) / 32 + 4) * sizeof(uint32_t)));
+    A(dalloc(&x->early_ids, (size_t)c.max_subset + 64)); A(dalloc(&x->early_flag, 1));
+    A(cudaMemset(x->early_flag, 0, sizeof(int)));
     A(dalloc(&x->hist, 12 * kHistBins + 32)); A(cudaMemset(x->hist, 0, (12 * kHistBins + 32) * sizeof(uint32_t)));
     A(dalloc(&x->ver_acc, kMaxChain + 1)); A(dalloc(&x->ver_tok, kMaxChain + 1));
     A(dalloc(&x->zero_i, 1)); A(cudaMemset(x->zero_i, 0, sizeof(int32_t)));
@@ -408,7 +415,7 @@ static evospec_status union_from_candidates(evospec_ctx* ctx, const double* cand
                                             const evospec_build_params* p, int32_t* out_ids, int32_t* out_n,
                                             int32_t* out_local_ids, int32_t* out_local_n, cudaStream_t st,
                                             const int32_t* dyn_base, cudaEvent_t wait_before_union,
-                                            bool sbits_ready);
+                                            bool sbits_ready, bool early = false);
 
 // a2 on a vocabulary shard: exact fp64 scores of this shard's E rows (global id
 // = row * R + r) and the shard's exact top-N (s desc, id asc), padded with id -1
@@ -439,7 +446,8 @@ static evospec_status build_impl(evospec_ctx* ctx, const void* E, int64_t n_e_ro
                                  const evospec_build_params* p, int32_t* out_ids, int32_t* out_n,
                                  int32_t* out_local_ids, int32_t* out_local_n, void* stream,
                                  const int32_t* dyn_base, cudaEvent_t wait_before_union = nullptr,
-                                 const double* ext_s = nullptr, const int32_t* ext_id = nullptr, int64_t n_ext = 0) {
+                                 const double* ext_s = nullptr, const int32_t* ext_id = nullptr, int64_t n_ext = 0,
+                                 bool early = false) {
     // ext_s / ext_id: the shards' stacked local candidates (evospec_build_subset_from_candidates)
     const bool ext = ext_s != nullptr;
     if (!ctx || (!ext && (!E || !q)) || !p || !out_ids || !out_n) return fail(EVOSPEC_EINPUT, "build_subset: null argument");
@@ -505,7 +513,7 @@ static evospec_status build_impl(evospec_ctx* ctx, const void* E, int64_t n_e_ro
     return union_from_candidates(ctx, full_scan ? nullptr : ctx->gat_s, full_scan ? nullptr : ctx->gat_id,
                                  (int64_t)N * R, static_ids, n_static, seeds, n_seed, row_ptr, col, ctx_ids, n_ctx, p,
                                  out_ids, out_n, out_local_ids, out_local_n, st, dyn_base, wait_before_union,
-                                 full_scan);
+                                 full_scan, early);
 }
 
 // The global candidate superset of the top-N and the formation / union (a2-a4).
@@ -519,7 +527,7 @@ static evospec_status union_from_candidates(evospec_ctx* ctx, const double* cand
                                             const evospec_build_params* p, int32_t* out_ids, int32_t* out_n,
                                             int32_t* out_local_ids, int32_t* out_local_n, cudaStream_t st,
                                             const int32_t* dyn_base, cudaEvent_t wait_before_union,
-                                            bool sbits_ready) {
+                                            bool sbits_ready, bool early) {
     const evospec_config& c = ctx->cfg;
     const int R = c.n_shards, r = c.shard_rank;
     const int N = p->n_sem;
@@ -559,7 +567,8 @@ static evospec_status union_from_candidates(evospec_ctx* ctx, const double* cand
                  N, row_ptr, col, use_ctx ? ctx->ctx_sel : nullptr, ctx->ctx_n, p->n_graph_sem_seeds, p->per_seed,
                  p->n_dyn, R, r, out_ids, out_n, out_local_ids, out_local_n, ctx->sem_ids, ctx->sem_n,
                  c.debug_checks, ctx->flags, st, union_trace(ctx, st), dyn_base, ctx->hist12,
-                 emit ? ctx->ubits : nullptr, ctx->sbits);
+                 emit ? ctx->ubits : nullptr, ctx->sbits, early ? ctx->early_ids : nullptr,
+                 early ? ctx->early_flag : nullptr);
     LAUNCH_CHECK("union");
     ctx->hist_dirty = false;
     if (emit) {   // single shard: the sorted ids from the bitmap by a multi-CTA kernel
@@ -751,6 +760,13 @@ struct LmhSegs {
 
 // merged outputs (m_*) non-null: the single-shard merge (LSE, probabilities)
 // is fused into the finalisation kernel (used by evospec_draft_step at R = 1)
+// Two-list draft step: the union publishes a complete dynamic list before its end
+// (EVOSPEC_EARLY_LIST=0: the LM head waits for the union's end)
+static bool early_list_enabled() {
+    static const bool v = getenv("EVOSPEC_EARLY_LIST") ? atoi(getenv("EVOSPEC_EARLY_LIST")) != 0 : true;
+    return v;
+}
+
 static evospec_status lmh_impl(evospec_ctx* ctx, const void* W, int64_t n_w_rows, const void* H, int32_t n_h,
                                const int32_t* subset, const int32_t* n_subset_dev, int32_t n_subset_max, int32_t k,
                                float inv_temp, int32_t* topk_ids, float* topk_vals, float* row_max,
@@ -795,6 +811,7 @@ static evospec_status lmh_impl(evospec_ctx* ctx, const void* W, int64_t n_w_rows
     a.fin_opt = 2;     // finalisation: the candidates' W rows prefetched to L2 for the re-score
     if (list2) {   // two-list mode (draft_step overlap): one SM stays free for the union kernel
         a.list2 = list2; a.n_list2_dev = n_list2_dev; a.n_list2_max = n_list2_max; a.n1 = n_subset_max;
+        if (early_list_enabled()) { a.early_ids = ctx->early_ids; a.early_flag = ctx->early_flag; }
         a.grid = lmh_tc_grid() - 1;
         if (!use_tc(a) || a.KP > 32 || segs || seg || logits_out)
             return fail(EVOSPEC_EINPUT, "subset_logits_topk: two-list mode needs the tensor-core path and k + 8 <= 32");
@@ -1107,7 +1124,8 @@ static evospec_status draft_step_impl(evospec_ctx* ctx, const evospec_step_io* i
         // so the union -> LM head PDL edge stays intact
         evospec_status s = build_impl(ctx, io->E, io->n_e_rows, q, io->static_ids, io->n_static, seeds, io->n_seed,
                                       io->csr_row_ptr, io->csr_col, cx, io->n_ctx, &io->build, ctx->st_S, ctx->st_nS,
-                                      nullptr, nullptr, st, ctx->zero_i, io->host_io ? ctx->ev_h : nullptr);
+                                      nullptr, nullptr, st, ctx->zero_i, io->host_io ? ctx->ev_h : nullptr,
+                                      nullptr, nullptr, 0, early_list_enabled());
         if (s != EVOSPEC_OK) return s;
         s = lmh_impl(ctx, io->W_local, io->n_w_rows, H, io->n_h, io->static_ids, nullptr, io->n_static, io->k,
                      io->inv_temp, ctx->st_tids, ctx->st_tvals, ctx->st_m, ctx->st_s, nullptr, st, oi, ov, ol, op,

@@ -121,6 +121,11 @@ inline cudaError_t launch_pdl_coop(void (*kern)(KArgs...), dim3 grid, dim3 block
     return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 ES_DEV int warp_id() { return threadIdx.x >> 5; }
+ES_DEV long long globaltimer_ns() {
+    long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
 ES_DEV void named_bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
 }  // namespace es

@@ -151,6 +151,8 @@ lmh_fin64_kernel(LmhArgs a, int n_cta_arg, int k, float gamma, const float* __re
     }
     if (tid == 0) s_cand_n = 0;
     pdl_wait();
+    // (every LM-head CTA has read the union's early-list flag: reset it for the next step)
+    if (a.early_flag && blockIdx.x == 0 && tid == 0) *(volatile int*)a.early_flag = 0;
     if (tid == 0) { FIN_TRACE_R(0); FIN_DT_R(0); }
     // the row's lists: CTAs [c_base, c_base + n_cta) (segment mode: its segment's CTAs,
     // behind part_cta0), and for the ragged head also its static row group's nA lists

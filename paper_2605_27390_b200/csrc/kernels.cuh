@@ -47,7 +47,8 @@ void launch_union(int V, const int32_t* static_ids, int n_static, const int32_t*
                   int32_t* out_ids, int32_t* out_n, int32_t* out_local, int32_t* out_local_n,
                   int32_t* sem_out, int* sem_out_n, int debug, int* flags, cudaStream_t st,
                   long long* trace = nullptr, const int32_t* dyn_base = nullptr,
-                  uint32_t* clear_hist = nullptr, uint32_t* emit_bits = nullptr, uint32_t* sbits = nullptr);
+                  uint32_t* clear_hist = nullptr, uint32_t* emit_bits = nullptr, uint32_t* sbits = nullptr,
+                  int32_t* early_ids = nullptr, int* early_flag = nullptr);
 void launch_union_emit(const uint32_t* bits, int V, int32_t* out_ids, int32_t* out_n, int32_t* out_local,
                        int32_t* out_local_n, int budget_max, int* flags, cudaStream_t st);
 
@@ -100,6 +101,10 @@ struct LmhArgs {
     // [vp], else list2[vp - n1]); the tensor-core kernel streams its slice of the first list
     // before griddepcontrol.wait. grid: CTAs of the launch (0 = all SMs)
     const int32_t* list2; const int32_t* n_list2_dev; int n_list2_max; int n1;
+    // two-list mode, early second list: the union publishes the complete dynamic list
+    // (unsorted) at early_ids with *early_flag = length + 1 before its end, or -1 (wait
+    // for the end: list2 / n_list2_dev); the finalisation resets the flag to 0
+    const int32_t* early_ids; int* early_flag;
     int grid;
     int part_cta0;   // list / state index of this launch's CTA 0 (a second launch writes behind the first)
     // the finalisation of the ragged head reads two list ranges per row: its launch's segment

@@ -102,6 +102,8 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
     uint64_t* tfull = empty + S;                                 // [2]
     uint64_t* tempty = tfull + 2;                                // [2]
     uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+    // two-list mode, early list: its length (-1: wait for the union's end; -2: not known yet)
+    int& s_n2 = *(int*)(tmem_slot + 1);
 
     const int warp = warp_id(), lane = lane_id();
     const int pcta = a.part_cta0 + (int)blockIdx.x;   // this CTA's partial list / state index
@@ -122,6 +124,7 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     epi_init(e, n_h);
+    if (threadIdx.x == 0) s_n2 = -2;
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -175,12 +178,43 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
     // list's stream, and a few full tiles on a few CTAs stream far faster than a
     // sliver of it on every CTA (a short tile still pays all d / 64 stages of H).
     int nt2 = a.list2 ? -1 : 0, n2 = 0;
+    bool early = false;   // the second list is the union's early copy (a.early_ids)
     // the CTA's rank in the second-list round robin
     const int dyn_rank = dyn_rank_of(blockIdx.x, tp.dyn_stride, gridDim.x);
     auto ensure2 = [&]() {
         if (nt2 >= 0) return;
-        pdl_wait();
-        n2 = max(0, min(*a.n_list2_dev, a.n_list2_max));
+        if (a.early_flag) {
+            // producer warp 0 polls the union's flag (one poller per CTA) and hands the
+            // outcome to the other warps through shared memory
+            int v;
+            if (warp == 0) {
+                int f = 0;
+                if (lane == 0) {
+                    const long long t0 = globaltimer_ns();
+                    for (;;) {
+                        asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(f) : "l"(a.early_flag) : "memory");
+                        if (f != 0) break;
+                        if (globaltimer_ns() - t0 > 200000000LL) __trap();   // (200 ms: the union never published)
+                        __nanosleep(256);
+                    }
+                }
+                f = __shfl_sync(0xffffffffu, f, 0);
+                v = f > 0 ? min(f - 1, a.n_list2_max) : -1;
+                if (lane == 0) asm volatile("st.release.cta.shared.b32 [%0], %1;" ::"r"(smem_u32(&s_n2)), "r"(v) : "memory");
+            } else {
+                for (;;) {
+                    asm volatile("ld.acquire.cta.shared.b32 %0, [%1];" : "=r"(v) : "r"(smem_u32(&s_n2)) : "memory");
+                    if (v != -2) break;
+                    __nanosleep(64);
+                }
+            }
+            early = v >= 0;
+            if (early) n2 = v;
+        }
+        if (!early) {
+            pdl_wait();
+            n2 = max(0, min(*a.n_list2_dev, a.n_list2_max));
+        }
         if (tp.dyn_tile == 0) {   // even split: this CTA's slice, one tile
             const int s0 = (int)((long long)n2 * blockIdx.x / gridDim.x);
             const int s1 = (int)((long long)n2 * (blockIdx.x + 1) / gridDim.x);
@@ -189,6 +223,10 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
         }
         const int first = tp.dyn_tile * dyn_rank, step = tp.dyn_tile * (int)gridDim.x;
         nt2 = first < n2 ? (n2 - first + step - 1) / step : 0;
+    };
+    auto id_at = [&](int vp) -> int32_t {
+        if (early && vp >= a.n1) return __ldcg(&a.early_ids[vp - a.n1]);
+        return lmh_id_at(a, vp);
     };
     auto has_tile = [&](int t) -> bool {
         if (t < n_tiles1) return true;
@@ -245,7 +283,7 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
             for (int i = 0; i < 8; ++i) {
                 const int row = 16 * i + 4 * warp + (lane >> 3);
                 const int pos = t0 + (row < tn ? row : 0);
-                src[i] = (const char*)a.W + (size_t)(lmh_id_at(a, pos) / a.R) * row_bytes + chunk * 16;
+                src[i] = (const char*)a.W + (size_t)(id_at(pos) / a.R) * row_bytes + chunk * 16;
                 dsto[i] = (uint32_t)(row * 128 + ((chunk ^ (row & 7)) << 4));
             }
             for (int kb = 0; kb < tp.nkb; ++kb) {
@@ -311,20 +349,20 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
     if (!epi) {
         if (a.list2) ensure2();
         const int nt = n_tiles1 + nt2;
-        t_first = (nt > 0 && par && !(a.list2 && nt2 == 0)) ? nt - 1 : 0x7fffffff;
+        t_first = (nt > 0 && par) ? nt - 1 : 0x7fffffff;
     }
     for (int t = t_first; t != 0x7fffffff && has_tile(t); ++t) {
         int t0, tn;
         tile_range(t, t0, tn);
-        // two-list mode: whether a first-list tile is the CTA's last is known only
-        // after the union ends -- those are folded as middle tiles (overlapping the
-        // wait); a CTA without second-list tiles stores its rows after the loop
-        const bool last_t = a.list2 ? (t >= n_tiles1 && !has_tile(t + 1)) : !has_tile(t + 1);
+        // two-list mode: whether the last first-list tile is the CTA's last is known once the
+        // union has published the second list (early, or at its end): a CTA without a
+        // second-list tile folds it as its last tile, with all warps
+        const bool last_t = !has_tile(t + 1);
         if (epi) {
             const int b = t & 1;
             // the tile's keys (vocabulary ids), loaded while the accumulator fills
             int key = 0x7fffffff;
-            if (e.tile_id && half == 0 && row < tn) key = lmh_id_at(a, t0 + row);
+            if (e.tile_id && half == 0 && row < tn) key = id_at(t0 + row);
             mbar_wait(&tfull[b], (uint32_t)(t >> 1) & 1);
             if (ew == 0 && lane == 0 && t < 2) TC_TRACE(3 + 2 * t);
             if (DTR && ew == 0 && lane == 0 && last_t) DTR[40] = clock64();
@@ -378,7 +416,7 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
     }
     if (a.list2) ensure2();
     const int n_tiles = n_tiles1 + nt2;
-    const bool store_after = a.list2 && nt2 == 0;   // (two-list mode, no second-list tile)
+    const bool store_after = a.list2 && nt2 == 0 && !par;   // (two-list mode, no second-list tile)
     if (n_tiles > 0 && !store_after && !par) {
         // the last tile without the thread-parallel fold (single-tile CTAs, sorted lists):
         // all 13 warps split its rows

@@ -498,7 +498,8 @@ union_kernel(int V, const int32_t* __restrict__ static_ids, int n_static,
              int32_t* __restrict__ out_local, int32_t* __restrict__ out_local_n,
              int32_t* __restrict__ sem_out, int* __restrict__ sem_out_n, int debug, int* flags,
              long long* __restrict__ trace, const int32_t* __restrict__ dyn_base, uint32_t* __restrict__ clear_hist,
-             uint32_t* __restrict__ emit_bits, uint32_t* __restrict__ sbits) {
+             uint32_t* __restrict__ emit_bits, uint32_t* __restrict__ sbits, int32_t* __restrict__ early_ids,
+             int* __restrict__ early_flag) {
     extern __shared__ __align__(16) unsigned char u_sm[];
     const int nwords = (V + 31) / 32;
     uint64_t* ck = (uint64_t*)u_sm;                          // [cap]
@@ -513,14 +514,18 @@ union_kernel(int V, const int32_t* __restrict__ static_ids, int n_static,
     __shared__ __align__(16) uint32_t hist[3 * kSelBins];
     __shared__ BSel bsel[3];
     __shared__ WSel wsel[3];
-    __shared__ int nG_s, bad_s, taken_s, ngs_s, sem_n_s;
+    __shared__ int nG_s, bad_s, taken_s, ngs_s, sem_n_s, early_n_s;
 
     const int tid = threadIdx.x, lane = lane_id(), T = blockDim.x;
+    // (the finalisation after the LM head resets the early-list flag; cleared here too,
+    // ahead of the trigger, in case a step ended without it)
+    if (early_flag && tid == 0) *(volatile int*)early_flag = 0;
     pdl_trigger();
     if (trace) { if (threadIdx.x == 0) { long long t_; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); trace[0] = t_; } }
     if (tid == 0) { bad_s = 0; sem_n_s = 0; }
     const unsigned lt_mask = (1u << lane) - 1u;
-    auto walk = [&](const int32_t* src, int len, int taken) -> int {
+    // rec: the new members' ids at their formation positions (the seeds, for the early list)
+    auto walk = [&](const int32_t* src, int len, int taken, int32_t* rec) -> int {
         for (int base = 0; base < len && taken < n_dyn; base += 32) {
             const int idx = base + lane;
             int32_t c = idx < len ? src[idx] : -1;
@@ -532,7 +537,10 @@ union_kernel(int V, const int32_t* __restrict__ static_ids, int n_static,
             const bool cand = first && !((bits[c < 0 ? 0 : (c >> 5)] >> (c & 31)) & 1u);
             const unsigned bal = __ballot_sync(0xffffffffu, cand);
             const int bf = __popc(bal & lt_mask);
-            if (cand && taken + bf < n_dyn) atomicOr(&bits[c >> 5], 1u << (c & 31));
+            if (cand && taken + bf < n_dyn) {
+                atomicOr(&bits[c >> 5], 1u << (c & 31));
+                if (rec) rec[taken + bf] = c;
+            }
             taken += min(__popc(bal), n_dyn - taken);
             __syncwarp();
         }
@@ -553,7 +561,7 @@ union_kernel(int V, const int32_t* __restrict__ static_ids, int n_static,
     if (trace) { if (threadIdx.x == 0) { long long t_; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); trace[41] = t_; } }
     // formation starts with the seeds (C6): warp 0 walks them
     if (warp_id() == 0) {
-        const int t = walk(seeds, n_seed, 0);
+        const int t = walk(seeds, n_seed, 0, early_ids);
         if (lane == 0) taken_s = t;
     }
     // the selection has consumed the scan's histogram: leave it zero for the next build
@@ -629,6 +637,39 @@ union_kernel(int V, const int32_t* __restrict__ static_ids, int n_static,
             if (lane == 0 && m) o = atomicAdd(&sem_n_s, __popc(m));
             o = __shfl_sync(0xffffffffu, o, 0) + __popc(m & ((1u << lane) - 1u));
             if (in) sem_out[o] = cid[i];
+        }
+    }
+    // the formation's semantic part (step 5 below): T_b ∩ S_sem, the new members of S_sem
+    // in S_sem order up to the budget
+    int c_take = 0;
+    for (int i = tid; i < n_cand; i += T)
+        if ((cf[i] & kTake) && (cf[i] & kSem)) { atomicOr(&bits[cid[i] >> 5], 1u << (cid[i] & 31)); ++c_take; }
+    const int took = block_count(c_take, warp_tot);
+    if (early_flag) {
+        // two-list LM head (lmh_tc.cu): when the seeds and the semantic part fill the
+        // budget, the graph and context walks add nothing and the dynamic list is
+        // complete now -- published (unsorted: new seeds ++ T_b ∩ S_sem) ahead of the
+        // sorted list, which follows at the kernel's end; otherwise the head is told to
+        // wait for the end (flag -1)
+        const bool complete = taken0 + took >= n_dyn;
+        if (complete) {
+            if (tid == 0) early_n_s = taken0;
+            __syncthreads();
+            for (int base = 0; base < n_cand; base += T) {
+                const int i = base + tid;
+                const bool in = i < n_cand && (cf[i] & kTake) && (cf[i] & kSem);
+                const unsigned m = __ballot_sync(0xffffffffu, in);
+                int o = 0;
+                if (lane == 0 && m) o = atomicAdd(&early_n_s, __popc(m));
+                o = __shfl_sync(0xffffffffu, o, 0) + __popc(m & lt_mask);
+                if (in) early_ids[o] = cid[i];
+            }
+            __threadfence();
+            __syncthreads();
+        }
+        if (tid == 0) {
+            const int f = complete ? early_n_s + 1 : -1;
+            asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(early_flag), "r"(f) : "memory");
         }
     }
     if (trace) { __syncthreads(); if (threadIdx.x == 0) { long long t_; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); trace[2] = t_; } }
@@ -714,15 +755,12 @@ union_kernel(int V, const int32_t* __restrict__ static_ids, int n_static,
     //    members (static or taken), stop at N_dyn. The seeds were walked before
     //    the wait; the S_sem part is T_b and S_sem (selected above); graph and
     //    ctx are walked by warp 0 in 32-wide windows.
-    int c_take = 0;
-    for (int i = tid; i < n_cand; i += T)
-        if ((cf[i] & kTake) && (cf[i] & kSem)) { atomicOr(&bits[cid[i] >> 5], 1u << (cid[i] & 31)); ++c_take; }
-    const int took = block_count(c_take, warp_tot);
+    // (T_b ∩ S_sem was marked above)
     if (warp_id() == 0) {
         const int n_ctx_sel = ctx_sel ? *n_ctx_sel_dev : 0;
         int t = taken0 + took;
-        if (t < n_dyn) t = walk(graph, n_graph, t);
-        if (t < n_dyn) t = walk(ctx_sel, n_ctx_sel, t);
+        if (t < n_dyn) t = walk(graph, n_graph, t, nullptr);
+        if (t < n_dyn) t = walk(ctx_sel, n_ctx_sel, t, nullptr);
     }
     __syncthreads();
 
@@ -883,14 +921,15 @@ void launch_union(int V, const int32_t* static_ids, int n_static, const int32_t*
                   int n_graph_sem_seeds, int per_seed, int n_dyn, int R, int r,
                   int32_t* out_ids, int32_t* out_n, int32_t* out_local, int32_t* out_local_n,
                   int32_t* sem_out, int* sem_out_n, int debug, int* flags, cudaStream_t st, long long* trace,
-                  const int32_t* dyn_base, uint32_t* clear_hist, uint32_t* emit_bits, uint32_t* sbits) {
+                  const int32_t* dyn_base, uint32_t* clear_hist, uint32_t* emit_bits, uint32_t* sbits,
+                  int32_t* early_ids, int* early_flag) {
     const size_t smem = (size_t)cap * 13 + union_fixed_bytes(V, per_seed) + 16;
     cudaFuncSetAttribute(union_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     launch_pdl(union_kernel, dim3(1), dim3(kUnionThreads), smem, st, V, static_ids, n_static, seeds, n_seed, cand_s, cand_id, n_cand_dev,
                                                   cap, n_sem, row_ptr, col, ctx_sel, n_ctx_sel_dev, n_graph_sem_seeds,
                                                   per_seed, n_dyn, R, r, out_ids, out_n, out_local, out_local_n,
                                                   sem_out, sem_out_n, debug, flags, trace, dyn_base, clear_hist, emit_bits,
-                                                  sbits);
+                                                  sbits, early_ids, early_flag);
 }
 
 // a4 static core -> the V-bit membership bitmap the union starts from (sbits: zero

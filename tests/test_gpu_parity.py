@@ -340,14 +340,18 @@ def test_draft_step_two_list_shapes(n_h, k, n_dyn, dup, n_static):
     assert ctx.get_flags() == 0
 
 
-@pytest.mark.parametrize("seed,n_h,k", [(0, 10, 10), (1, 60, 24), (2, 3, 1)])
-def test_draft_step_two_list_integer_ties(seed, n_h, k):
+@pytest.mark.parametrize("seed,n_h,k,n_dyn", [(0, 10, 10, 2500), (1, 60, 24, 2500), (2, 3, 1, 2500),
+                                               (3, 60, 10, 600), (4, 17, 24, 800)])
+def test_draft_step_two_list_integer_ties(seed, n_h, k, n_dyn):
     """The two-list LM head on integer data ({-3..3}: every logit an exact integer, massive
     ties inside and across the static and dynamic lists, whose subset positions do not
     follow id order): the candidate buffers order ties by vocabulary id (DESIGN §5.3,
-    keys), so the top-k ids equal the oracle's lower-id-first order."""
+    keys), so the top-k ids equal the oracle's lower-id-first order. n_dyn = 2500 (~1000
+    new semantic members: the graph walk adds the rest, the head waits for the union's
+    end); n_dyn <= 800: the semantic part fills the budget and the head takes the union's
+    early, unsorted copy of the dynamic list."""
     P = G.make_problem(70 + seed, dtype="bf16", integer=True, V=30000, d=128, n_static=20000, n_sem=3000,
-                       n_dyn=2500, n_h=n_h, k=k)
+                       n_dyn=n_dyn, n_h=n_h, k=k)
     ctx = ctx_for(P)
     W = G.to_dev(P["W"], DEV)
     ctx.prepare_weights(W)
