@@ -67,6 +67,35 @@ struct TcParams {
 
 ES_DEV int dyn_rank_of(int b, int stride, int grid) { return (int)(((long long)b * stride) % grid); }
 
+// Two-list mode, early second list: producer warp 0 polls the union's flag (one
+// poller per CTA) and hands the outcome to the other warps through shared memory.
+// Returns the list's length, or -1 (wait for the union's end).
+__device__ __noinline__ int lmh_list2_resolve(const int* flag, int n_max, int* s_n2, int warp, int lane) {
+    int v;
+    if (warp == 0) {
+        int f = 0;
+        if (lane == 0) {
+            const long long t0 = globaltimer_ns();
+            for (;;) {
+                asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(f) : "l"(flag) : "memory");
+                if (f != 0) break;
+                if (globaltimer_ns() - t0 > 200000000LL) __trap();   // (200 ms: the union never published)
+                __nanosleep(256);
+            }
+        }
+        f = __shfl_sync(0xffffffffu, f, 0);
+        v = f > 0 ? min(f - 1, n_max) : -1;
+        if (lane == 0) asm volatile("st.release.cta.shared.b32 [%0], %1;" ::"r"(smem_u32(s_n2)), "r"(v) : "memory");
+    } else {
+        for (;;) {
+            asm volatile("ld.acquire.cta.shared.b32 %0, [%1];" : "=r"(v) : "r"(smem_u32(s_n2)) : "memory");
+            if (v != -2) break;
+            __nanosleep(64);
+        }
+    }
+    return v;
+}
+
 __global__ void __launch_bounds__(kTcWarps * 32, 1)
 lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ CUtensorMap tmap_h,
               LmhArgs a, TcParams tp) {
@@ -179,37 +208,15 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
     // sliver of it on every CTA (a short tile still pays all d / 64 stages of H).
     int nt2 = a.list2 ? -1 : 0, n2 = 0;
     bool early = false;   // the second list is the union's early copy (a.early_ids)
+    const int32_t* l2p = a.list2;   // the second list's ids (a.list2, or a.early_ids once published)
     // the CTA's rank in the second-list round robin
     const int dyn_rank = dyn_rank_of(blockIdx.x, tp.dyn_stride, gridDim.x);
     auto ensure2 = [&]() {
         if (nt2 >= 0) return;
-        if (a.early_flag) {
-            // producer warp 0 polls the union's flag (one poller per CTA) and hands the
-            // outcome to the other warps through shared memory
-            int v;
-            if (warp == 0) {
-                int f = 0;
-                if (lane == 0) {
-                    const long long t0 = globaltimer_ns();
-                    for (;;) {
-                        asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(f) : "l"(a.early_flag) : "memory");
-                        if (f != 0) break;
-                        if (globaltimer_ns() - t0 > 200000000LL) __trap();   // (200 ms: the union never published)
-                        __nanosleep(256);
-                    }
-                }
-                f = __shfl_sync(0xffffffffu, f, 0);
-                v = f > 0 ? min(f - 1, a.n_list2_max) : -1;
-                if (lane == 0) asm volatile("st.release.cta.shared.b32 [%0], %1;" ::"r"(smem_u32(&s_n2)), "r"(v) : "memory");
-            } else {
-                for (;;) {
-                    asm volatile("ld.acquire.cta.shared.b32 %0, [%1];" : "=r"(v) : "r"(smem_u32(&s_n2)) : "memory");
-                    if (v != -2) break;
-                    __nanosleep(64);
-                }
-            }
+        if (a.early_flag) {   // (out of line: keeps the loops that call has_tile compact)
+            const int v = lmh_list2_resolve(a.early_flag, a.n_list2_max, &s_n2, warp, lane);
             early = v >= 0;
-            if (early) n2 = v;
+            if (early) { n2 = v; l2p = a.early_ids; }
         }
         if (!early) {
             pdl_wait();
@@ -224,9 +231,10 @@ lmh_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant_
         const int first = tp.dyn_tile * dyn_rank, step = tp.dyn_tile * (int)gridDim.x;
         nt2 = first < n2 ? (n2 - first + step - 1) / step : 0;
     };
+    // (the early copy is read only after its flag: the first read of each line in this
+    // kernel, so the read-only path fetches it from L2)
     auto id_at = [&](int vp) -> int32_t {
-        if (early && vp >= a.n1) return __ldcg(&a.early_ids[vp - a.n1]);
-        return lmh_id_at(a, vp);
+        return (a.list2 && vp >= a.n1) ? __ldg(&l2p[vp - a.n1]) : __ldg(&a.subset[vp]);
     };
     auto has_tile = [&](int t) -> bool {
         if (t < n_tiles1) return true;
