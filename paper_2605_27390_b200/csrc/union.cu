@@ -522,7 +522,7 @@ union_kernel(int V, const int32_t* __restrict__ static_ids, int n_static,
     if (early_flag && tid == 0) *(volatile int*)early_flag = 0;
     pdl_trigger();
     if (trace) { if (threadIdx.x == 0) { long long t_; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); trace[0] = t_; } }
-    if (tid == 0) { bad_s = 0; sem_n_s = 0; }
+    if (tid == 0) { bad_s = 0; sem_n_s = 0; early_n_s = 0; }
     const unsigned lt_mask = (1u << lane) - 1u;
     // rec: the new members' ids at their formation positions (the seeds, for the early list)
     auto walk = [&](const int32_t* src, int len, int taken, int32_t* rec) -> int {
@@ -628,6 +628,32 @@ union_kernel(int V, const int32_t* __restrict__ static_ids, int n_static,
                             phi);
         if (trace && tid == 0) trace[23] = n_cand;   // (stamps 24..39: the selection's phases)
     }
+    // the formation's semantic part (step 5 below): T_b ∩ S_sem, the new members of S_sem
+    // in S_sem order up to the budget, marked in the bitmap. Two-list draft step
+    // (early_flag, lmh_tc.cu): also appended after the new seeds to early_ids; when the
+    // seeds and the semantic part fill the budget, the graph and context walks add
+    // nothing and the dynamic list is complete now -- its length is published (release)
+    // ahead of the sorted list that follows at the kernel's end; otherwise the head is
+    // told to wait for the end (flag -1)
+    int c_take = 0;
+    for (int base = 0; base < n_cand; base += T) {
+        const int i = base + tid;
+        const bool in = i < n_cand && (cf[i] & kTake) && (cf[i] & kSem);
+        if (in) { atomicOr(&bits[cid[i] >> 5], 1u << (cid[i] & 31)); ++c_take; }
+        if (early_flag) {
+            const unsigned m = __ballot_sync(0xffffffffu, in);
+            int o = 0;
+            if (lane == 0 && m) o = atomicAdd(&early_n_s, __popc(m));
+            o = __shfl_sync(0xffffffffu, o, 0) + __popc(m & lt_mask);
+            if (in) early_ids[taken0 + o] = cid[i];
+        }
+    }
+    if (early_flag) __threadfence();
+    const int took = block_count(c_take, warp_tot);   // (syncs: every append fenced before the flag)
+    if (early_flag && tid == 0) {
+        const int f = taken0 + took >= n_dyn ? taken0 + took + 1 : -1;
+        asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(early_flag), "r"(f) : "memory");
+    }
     if (sem_out) {
         for (int base = 0; base < n_cand; base += T) {      // one smem atomic per warp
             const int i = base + tid;
@@ -637,39 +663,6 @@ union_kernel(int V, const int32_t* __restrict__ static_ids, int n_static,
             if (lane == 0 && m) o = atomicAdd(&sem_n_s, __popc(m));
             o = __shfl_sync(0xffffffffu, o, 0) + __popc(m & ((1u << lane) - 1u));
             if (in) sem_out[o] = cid[i];
-        }
-    }
-    // the formation's semantic part (step 5 below): T_b ∩ S_sem, the new members of S_sem
-    // in S_sem order up to the budget
-    int c_take = 0;
-    for (int i = tid; i < n_cand; i += T)
-        if ((cf[i] & kTake) && (cf[i] & kSem)) { atomicOr(&bits[cid[i] >> 5], 1u << (cid[i] & 31)); ++c_take; }
-    const int took = block_count(c_take, warp_tot);
-    if (early_flag) {
-        // two-list LM head (lmh_tc.cu): when the seeds and the semantic part fill the
-        // budget, the graph and context walks add nothing and the dynamic list is
-        // complete now -- published (unsorted: new seeds ++ T_b ∩ S_sem) ahead of the
-        // sorted list, which follows at the kernel's end; otherwise the head is told to
-        // wait for the end (flag -1)
-        const bool complete = taken0 + took >= n_dyn;
-        if (complete) {
-            if (tid == 0) early_n_s = taken0;
-            __syncthreads();
-            for (int base = 0; base < n_cand; base += T) {
-                const int i = base + tid;
-                const bool in = i < n_cand && (cf[i] & kTake) && (cf[i] & kSem);
-                const unsigned m = __ballot_sync(0xffffffffu, in);
-                int o = 0;
-                if (lane == 0 && m) o = atomicAdd(&early_n_s, __popc(m));
-                o = __shfl_sync(0xffffffffu, o, 0) + __popc(m & lt_mask);
-                if (in) early_ids[o] = cid[i];
-            }
-            __threadfence();
-            __syncthreads();
-        }
-        if (tid == 0) {
-            const int f = complete ? early_n_s + 1 : -1;
-            asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(early_flag), "r"(f) : "memory");
         }
     }
     if (trace) { __syncthreads(); if (threadIdx.x == 0) { long long t_; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_)); trace[2] = t_; } }
