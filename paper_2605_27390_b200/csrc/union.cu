@@ -18,6 +18,12 @@
 //      are taken -- the same set the sequential walk of the definition takes;
 //   5. block-wide popcount scan of the bitmap writes the sorted ids (and this
 //      shard's slice v mod R == r).
+// Two-list draft step (early_flag != null): right after the selections the
+// new seeds and the semantic part are also written, unsorted, to early_ids; if
+// they fill N_dyn the dynamic list is complete (steps 3-4's graph and context
+// walks add nothing) and its length + 1 is release-stored to *early_flag, else
+// -1 -- the LM head (lmh_tc.cu) starts its dynamic tiles on that, ~11 us
+// before this kernel's end.
 #include "common.cuh"
 #include "kernels.cuh"
 
