@@ -1073,6 +1073,16 @@ evospec_status evospec_kd_loss(evospec_ctx* ctx, int32_t B, int32_t g, int32_t K
     return EVOSPEC_OK;
 }
 
+// The draft step's two-list mode (single shard, tensor-core head): the LM head streams
+// the static rows while the union forms the dynamic list
+static bool step_overlap(const evospec_ctx* ctx, const evospec_step_io* io) {
+    const evospec_config& c = ctx->cfg;
+    static const bool ov_env = getenv("EVOSPEC_OVERLAP") ? atoi(getenv("EVOSPEC_OVERLAP")) != 0 : kOverlapDefault;
+    return ov_env && c.n_shards == 1 && c.w_dtype == EVOSPEC_BF16 && c.h_dtype == EVOSPEC_BF16 && c.d % 64 == 0 &&
+           io->n_h >= kTcMinRows && io->n_h <= kTcMaxRows && io->k + kTopkPad <= 32 && io->n_static > 0 &&
+           !c.debug_checks && !getenv("EVOSPEC_LMH");
+}
+
 // phases: 1 host->device staging, 2 the compute (build + LM head + merge), 4 device->host
 static evospec_status draft_step_impl(evospec_ctx* ctx, const evospec_step_io* io, cudaStream_t st,
                                       int phases = 7) {
@@ -1091,13 +1101,17 @@ static evospec_status draft_step_impl(evospec_ctx* ctx, const evospec_step_io* i
     }
     if (io->host_io && (phases & 1)) {
         StageTimer t(ctx, EVOSPEC_STAGE_COPY, st);
-        CUDA_TRY(cudaMemcpyAsync(ctx->st_q, io->q, (size_t)c.d * hb, cudaMemcpyHostToDevice, st));
-        // H is needed only by the LM head: its copy runs on a side stream under the build
+        // H is needed only by the LM head: its copy runs on a side stream under the build;
+        // in two-list mode the seeds too (only the union reads them, after waiting for it)
+        const bool seeds_side = step_overlap(ctx, io);
         CUDA_TRY(cudaEventRecord(ctx->ev_in, st));
         CUDA_TRY(cudaStreamWaitEvent(ctx->s_h, ctx->ev_in, 0));
+        CUDA_TRY(cudaMemcpyAsync(ctx->st_q, io->q, (size_t)c.d * hb, cudaMemcpyHostToDevice, st));
+        if (io->n_seed > 0 && seeds_side)
+            CUDA_TRY(cudaMemcpyAsync(ctx->st_seeds, io->seeds, (size_t)io->n_seed * 4, cudaMemcpyHostToDevice, ctx->s_h));
         CUDA_TRY(cudaMemcpyAsync(ctx->st_H, io->H, (size_t)io->n_h * c.d * hb, cudaMemcpyHostToDevice, ctx->s_h));
         CUDA_TRY(cudaEventRecord(ctx->ev_h, ctx->s_h));
-        if (io->n_seed > 0)
+        if (io->n_seed > 0 && !seeds_side)
             CUDA_TRY(cudaMemcpyAsync(ctx->st_seeds, io->seeds, (size_t)io->n_seed * 4, cudaMemcpyHostToDevice, st));
         if (io->n_ctx > 0 && io->ctx_ids)
             CUDA_TRY(cudaMemcpyAsync(ctx->st_ctx, io->ctx_ids, (size_t)io->n_ctx * 4, cudaMemcpyHostToDevice, st));
@@ -1115,10 +1129,7 @@ static evospec_status draft_step_impl(evospec_ctx* ctx, const evospec_step_io* i
     // overlap (single shard, tensor-core head): the union writes only the dynamic list and
     // the LM head streams the static rows (an input) while the union still runs, then the
     // dynamic rows (two-list mode, lmh_tc.cu)
-    static const bool ov_env = getenv("EVOSPEC_OVERLAP") ? atoi(getenv("EVOSPEC_OVERLAP")) != 0 : kOverlapDefault;
-    const bool overlap = ov_env && c.n_shards == 1 && c.w_dtype == EVOSPEC_BF16 && c.h_dtype == EVOSPEC_BF16 &&
-                         c.d % 64 == 0 && io->n_h >= kTcMinRows && io->n_h <= kTcMaxRows &&
-                         io->k + kTopkPad <= 32 && io->n_static > 0 && !c.debug_checks && !getenv("EVOSPEC_LMH");
+    const bool overlap = step_overlap(ctx, io);
     if (overlap) {
         // the host-staged H (side stream, under the scan) is waited for before the union,
         // so the union -> LM head PDL edge stays intact
